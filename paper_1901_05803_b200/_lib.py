@@ -1,0 +1,73 @@
+"""ctypes binding of libralpb200.so (the C ABI declared in include/ralpb.h).
+
+The library is the only compute path: if it is missing or fails to load this
+module raises, there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("RALPB_LIB", _PKG / "libralpb200.so"))
+
+_lib = None
+
+c_ll = C.c_longlong
+c_vp = C.c_void_p
+c_i = C.c_int
+c_f = C.c_float
+c_fp = C.c_void_p  # float*
+c_cp = C.c_char_p
+
+# name -> (restype, argtypes); mirrors include/ralpb.h
+SIGNATURES: dict[str, tuple] = {
+    "ralpb_last_error": (c_cp, []),
+    "ralpb_version": (c_i, []),
+    "ralpb_gemm_bf16": (c_i, [c_vp, c_ll, c_ll, c_ll, c_i, c_vp, c_ll, c_ll, c_ll, c_i, c_i, c_i, c_ll,
+                              c_vp, c_i, c_ll, c_ll, c_fp, c_i, c_vp, c_ll, c_i, c_i, c_vp]),
+    "ralpb_conv_fwd": (c_i, [c_vp, c_vp, c_fp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),
+    "ralpb_conv_dgrad": (c_i, [c_vp, c_vp, c_vp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),
+    "ralpb_conv_wgrad": (c_i, [c_vp, c_vp, c_fp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),
+    "ralpb_pack_input": (c_i, [c_fp, c_i, c_i, c_i, c_i, c_vp, c_i, c_i, c_vp]),
+    "ralpb_maxpool_fwd": (c_i, [c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp, c_i, c_vp]),
+    "ralpb_maxpool_bwd": (c_i, [c_vp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp, c_vp]),
+    "ralpb_softmax_xent": (c_i, [c_fp, c_i, c_i, c_ll, c_vp, c_f, c_fp, c_vp, c_ll, c_vp]),
+    "ralpb_sgd_momentum": (c_i, [c_fp, c_fp, c_fp, c_ll, c_f, c_f, c_f, c_vp]),
+    "ralpb_colsum_bf16": (c_i, [c_vp, c_ll, c_i, c_ll, c_fp, c_vp]),
+    "ralpb_conv_weight_prep": (c_i, [c_fp, c_i, c_i, c_i, c_vp, c_vp, c_vp]),
+    "ralpb_cast_bf16": (c_i, [c_fp, c_ll, c_vp, c_vp]),
+}
+
+
+class BackendError(RuntimeError):
+    """A call into libralpb200.so failed."""
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise BackendError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_1901_05803_b200.build` "
+                "(there is no CPU fallback)")
+        handle = C.CDLL(str(LIB_PATH), mode=C.RTLD_GLOBAL)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES)
+
+
+def call(name: str, *args) -> None:
+    fn = getattr(lib(), name)
+    rc = fn(*args)
+    if rc != 0:
+        msg = lib().ralpb_last_error().decode(errors="replace")
+        raise BackendError(f"{name} failed ({rc}): {msg}")

@@ -1,0 +1,37 @@
+// Implicit-GEMM convolution over the padded-flattened NHWC layout.
+//
+// An activation of spatial size HxW with padding p is stored as
+// [N][H+2p][W+2p][C] bf16 with zero borders and viewed as a 2-D matrix of
+// Q = N*(H+2p)*(W+2p) rows.  For a stride-1 "same" convolution (k = 2p+1)
+// output row q (same index space) is
+//     y[q] = sum_t x[q + off(t)] * W[t],   off(r,s) = (r-p)*(W+2p) + (s-p)
+// so every tap is a plain row-shifted 2-D TMA load of the input matrix; rows
+// that fall on padding positions are computed and then zeroed by the epilogue.
+// Backward-data is the same GEMM with the tap order reversed and the filter
+// transposed; backward-filter contracts over q with both operands MN-major.
+// Reference semantics: infer_conv (pkg/src/ralp/layers.py:87-103).
+#pragma once
+#include "gemm_host.cuh"
+
+namespace ralpb {
+
+struct ConvGeom {
+  int n, h, w, cin, cout, k, pad;
+  int hp() const { return h + 2 * pad; }
+  int wp() const { return w + 2 * pad; }
+  long long q() const { return static_cast<long long>(n) * hp() * wp(); }
+  int taps() const { return k * k; }
+};
+
+// y_pad = relu?(conv(x_pad, w) + bias), borders zeroed.  w: [cout][k*k][cin] bf16.
+cudaError_t conv_fwd(const ConvGeom& g, const void* x_pad, const void* w, const float* bias,
+                     void* y_pad, int relu, cudaStream_t s, std::string* why);
+// dx_pad = (conv_transpose(dy_pad, w)) * (mask_pad > 0 if mask_pad), borders zeroed.
+// wd: [cin][k*k][cout] bf16, wd[ci][t][co] = w[co][k*k-1-t][ci].
+cudaError_t conv_dgrad(const ConvGeom& g, const void* dy_pad, const void* wd, const void* mask_pad,
+                       void* dx_pad, cudaStream_t s, std::string* why);
+// dw[co][t][ci] += sum_q dy[q][co] * x[q + off(t)][ci]   (fp32, atomics, split-K).
+cudaError_t conv_wgrad(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw,
+                       cudaStream_t s, std::string* why);
+
+}  // namespace ralpb

@@ -1,0 +1,344 @@
+#include <algorithm>
+#include "elementwise.cuh"
+#include "gemm_host.cuh"
+
+namespace ralpb {
+
+static int grid_for(long long work, int threads) {
+  long long blocks = (work + threads - 1) / threads;
+  long long cap = static_cast<long long>(num_sms()) * 16;
+  return static_cast<int>(std::max<long long>(1, std::min(blocks, cap)));
+}
+
+// ------------------------------------------------------------------ input packing
+__global__ void pack_input_kernel(const float* __restrict__ x, int n, int h, int w, int c,
+                                  __nv_bfloat16* __restrict__ out, int cp, int pad) {
+  const int hp = h + 2 * pad, wp = w + 2 * pad;
+  const long long total = static_cast<long long>(n) * hp * wp;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    long long img = i / (hp * wp);
+    int r = static_cast<int>(i - img * hp * wp);
+    int ph = r / wp, pw = r - (r / wp) * wp;
+    int ih = ph - pad, iw = pw - pad;
+    bool in = ih >= 0 && ih < h && iw >= 0 && iw < w;
+    const float* src = x + ((img * h + ih) * w + iw) * c;
+    __nv_bfloat16* dst = out + i * cp;
+    for (int ch = 0; ch < cp; ch += 2) {
+      float a = (in && ch < c) ? src[ch] : 0.f;
+      float b = (in && ch + 1 < c) ? src[ch + 1] : 0.f;
+      *reinterpret_cast<__nv_bfloat162*>(dst + ch) = __floats2bfloat162_rn(a, b);
+    }
+  }
+}
+
+cudaError_t pack_input(const float* x, int n, int h, int w, int c, __nv_bfloat16* out, int cp,
+                       int pad, cudaStream_t s) {
+  long long total = static_cast<long long>(n) * (h + 2 * pad) * (w + 2 * pad);
+  pack_input_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, n, h, w, c, out, cp, pad);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ max pool
+// One thread = one output position x 8 channels.
+__global__ void maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, int n, int h, int w, int c,
+                                   int pi, int k, int st, __nv_bfloat16* __restrict__ y, int po,
+                                   int oh, int ow) {
+  const int ohp = oh + 2 * po, owp = ow + 2 * po;
+  const int hp = h + 2 * pi, wp = w + 2 * pi;
+  const int cv = c / 8;
+  const long long total = static_cast<long long>(n) * ohp * owp * cv;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    int cg = static_cast<int>(i % cv);
+    long long pos = i / cv;
+    long long img = pos / (ohp * owp);
+    int r = static_cast<int>(pos - img * ohp * owp);
+    int py = r / owp, px = r - (r / owp) * owp;
+    int oy = py - po, ox = px - po;
+    uint4 res = make_uint4(0, 0, 0, 0);
+    if (oy >= 0 && oy < oh && ox >= 0 && ox < ow) {
+      float m[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) m[e] = -INFINITY;
+      for (int ky = 0; ky < k; ++ky) {
+        for (int kx = 0; kx < k; ++kx) {
+          long long src = ((img * hp + oy * st + ky + pi) * wp + ox * st + kx + pi) * c + cg * 8;
+          uint4 u = *reinterpret_cast<const uint4*>(x + src);
+          const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) m[e] = fmaxf(m[e], __bfloat162float(hb[e]));
+        }
+      }
+      __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&res);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ob[e] = __float2bfloat16_rn(m[e]);
+    }
+    *reinterpret_cast<uint4*>(y + pos * c + cg * 8) = res;
+  }
+}
+
+cudaError_t maxpool_fwd(const __nv_bfloat16* x, int n, int h, int w, int c, int pad_in, int k,
+                        int st, __nv_bfloat16* y, int pad_out, cudaStream_t s) {
+  if (c % 8 != 0) return cudaErrorInvalidValue;
+  int oh = (h - k) / st + 1, ow = (w - k) / st + 1;
+  long long total = static_cast<long long>(n) * (oh + 2 * pad_out) * (ow + 2 * pad_out) * (c / 8);
+  maxpool_fwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, n, h, w, c, pad_in, k, st, y, pad_out, oh, ow);
+  return cudaGetLastError();
+}
+
+// One thread = one input position x 8 channels; loops over the windows covering it.
+__global__ void maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                   const __nv_bfloat16* __restrict__ dy, int n, int h, int w, int c,
+                                   int pi, int k, int st, int po, int oh, int ow,
+                                   __nv_bfloat16* __restrict__ dx) {
+  const int hp = h + 2 * pi, wp = w + 2 * pi;
+  const int ohp = oh + 2 * po, owp = ow + 2 * po;
+  const int cv = c / 8;
+  const long long total = static_cast<long long>(n) * hp * wp * cv;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    int cg = static_cast<int>(i % cv);
+    long long pos = i / cv;
+    long long img = pos / (hp * wp);
+    int r = static_cast<int>(pos - img * hp * wp);
+    int py = r / wp, px = r - (r / wp) * wp;
+    int iy = py - pi, ix = px - pi;
+    float g[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) g[e] = 0.f;
+    if (iy >= 0 && iy < h && ix >= 0 && ix < w) {
+      uint4 xs = *reinterpret_cast<const uint4*>(x + pos * c + cg * 8);
+      const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(&xs);
+      // windows oy with oy*st <= iy < oy*st + k
+      const int oy0 = iy - k + 1 > 0 ? (iy - k + st) / st : 0;
+      const int ox0 = ix - k + 1 > 0 ? (ix - k + st) / st : 0;
+      for (int oy = oy0; oy <= iy / st && oy < oh; ++oy) {
+        for (int ox = ox0; ox <= ix / st && ox < ow; ++ox) {
+          // first argmax (row-major) of window (oy, ox), per channel
+          float best[8];
+          int arg[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) { best[e] = -INFINITY; arg[e] = -1; }
+          for (int ky = 0; ky < k; ++ky) {
+            for (int kx = 0; kx < k; ++kx) {
+              long long src = ((img * hp + oy * st + ky + pi) * wp + ox * st + kx + pi) * c + cg * 8;
+              uint4 u = *reinterpret_cast<const uint4*>(x + src);
+              const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                float v = __bfloat162float(hb[e]);
+                if (v > best[e]) { best[e] = v; arg[e] = ky * k + kx; }
+              }
+            }
+          }
+          const int mine = (iy - oy * st) * k + (ix - ox * st);
+          long long dsrc = ((img * ohp + oy + po) * owp + ox + po) * c + cg * 8;
+          uint4 du = *reinterpret_cast<const uint4*>(dy + dsrc);
+          const __nv_bfloat16* db = reinterpret_cast<const __nv_bfloat16*>(&du);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (arg[e] == mine) g[e] += __bfloat162float(db[e]);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (!(__bfloat162float(xb[e]) > 0.f)) g[e] = 0.f;
+    }
+    uint4 res;
+    __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&res);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ob[e] = __float2bfloat16_rn(g[e]);
+    *reinterpret_cast<uint4*>(dx + pos * c + cg * 8) = res;
+  }
+}
+
+cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* dy, int n, int h, int w,
+                        int c, int pad_in, int k, int st, int pad_out, __nv_bfloat16* dx,
+                        cudaStream_t s) {
+  if (c % 8 != 0) return cudaErrorInvalidValue;
+  int oh = (h - k) / st + 1, ow = (w - k) / st + 1;
+  long long total = static_cast<long long>(n) * (h + 2 * pad_in) * (w + 2 * pad_in) * (c / 8);
+  maxpool_bwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, dy, n, h, w, c, pad_in, k, st, pad_out, oh, ow, dx);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ softmax cross-entropy
+__device__ __forceinline__ float block_reduce(float v, float* sh, bool is_max) {
+  for (int o = 16; o > 0; o >>= 1) {
+    float u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, u) : v + u;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  v = lane < nw ? sh[lane] : (is_max ? -INFINITY : 0.f);
+  for (int o = 16; o > 0; o >>= 1) {
+    float u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, u) : v + u;
+  }
+  return v;
+}
+
+__global__ void softmax_xent_kernel(const float* __restrict__ logits, int classes, long long ld,
+                                    const int32_t* __restrict__ labels, float scale,
+                                    float* __restrict__ row_loss, __nv_bfloat16* __restrict__ dl,
+                                    long long ld_d) {
+  __shared__ float sh[32];
+  const int row = blockIdx.x;
+  const float* z = logits + row * ld;
+  float mx = -INFINITY;
+  for (int j = threadIdx.x; j < classes; j += blockDim.x) mx = fmaxf(mx, z[j]);
+  mx = block_reduce(mx, sh, true);
+  float se = 0.f;
+  for (int j = threadIdx.x; j < classes; j += blockDim.x) se += expf(z[j] - mx);
+  se = block_reduce(se, sh, false);
+  const float lse = mx + logf(se);
+  const int lab = labels[row];
+  for (int j = threadIdx.x; j < classes; j += blockDim.x) {
+    float pj = expf(z[j] - lse);
+    float g = (pj - (j == lab ? 1.f : 0.f)) * scale;
+    dl[row * ld_d + j] = __float2bfloat16_rn(g);
+  }
+  if (threadIdx.x == 0) row_loss[row] = lse - z[lab];
+}
+
+cudaError_t softmax_xent(const float* logits, int rows, int classes, long long ld,
+                         const int32_t* labels, float scale, float* row_loss,
+                         __nv_bfloat16* dlogits, long long ld_d, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  softmax_xent_kernel<<<rows, 256, 0, s>>>(logits, classes, ld, labels, scale, row_loss, dlogits, ld_d);
+  return cudaGetLastError();
+}
+
+__global__ void reduce_sum_kernel(const float* __restrict__ x, int n, float scale, float* out) {
+  __shared__ float sh[32];
+  float v = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) v += x[i];
+  v = block_reduce(v, sh, false);
+  if (threadIdx.x == 0) out[0] = v * scale;
+}
+
+cudaError_t reduce_sum(const float* x, int n, float scale, float* out, cudaStream_t s) {
+  reduce_sum_kernel<<<1, 1024, 0, s>>>(x, n, scale, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ SGD momentum
+__global__ void sgd_kernel(float* __restrict__ p, float* __restrict__ v, const float* __restrict__ g,
+                           long long n, float lr, float mu, float gs) {
+  long long n4 = n / 4;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float4 pv = reinterpret_cast<float4*>(p)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    float4 gv = reinterpret_cast<const float4*>(g)[i];
+    vv.x = mu * vv.x + gs * gv.x; pv.x -= lr * vv.x;
+    vv.y = mu * vv.y + gs * gv.y; pv.y -= lr * vv.y;
+    vv.z = mu * vv.z + gs * gv.z; pv.z -= lr * vv.z;
+    vv.w = mu * vv.w + gs * gv.w; pv.w -= lr * vv.w;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    reinterpret_cast<float4*>(p)[i] = pv;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    long long i = n4 * 4 + threadIdx.x;
+    v[i] = mu * v[i] + gs * g[i];
+    p[i] -= lr * v[i];
+  }
+}
+
+cudaError_t sgd_momentum(float* p, float* v, const float* g, long long n, float lr, float mu,
+                         float gscale, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  sgd_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(p, v, g, n, lr, mu, gscale);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ bias gradients
+// Block = 256 threads covering up to 256*8 channels of a row strip; partial sums in
+// registers, one atomic per (block, channel).
+__global__ void colsum_kernel(const __nv_bfloat16* __restrict__ dy, long long rows, int c,
+                              long long ld, float* __restrict__ db, long long rows_per_block) {
+  const int cv = c / 8;
+  const int tx = threadIdx.x % 32;       // channel-group lane
+  const int ty = threadIdx.x / 32;       // row lane (8 rows in flight)
+  long long r0 = blockIdx.x * rows_per_block;
+  long long r1 = min(rows, r0 + rows_per_block);
+  const int cg = blockIdx.y * 32 + tx;
+  const bool valid = cg < cv;
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  if (valid) {
+    for (long long r = r0 + ty; r < r1; r += 8) {
+      uint4 u = *reinterpret_cast<const uint4*>(dy + r * ld + cg * 8);
+      const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += __bfloat162float(hb[e]);
+    }
+  }
+  __shared__ float sh[8][32][9];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) sh[ty][tx][e] = acc[e];
+  __syncthreads();
+  if (ty == 0 && valid) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      float t = 0.f;
+      for (int j = 0; j < 8; ++j) t += sh[j][tx][e];
+      atomicAdd(db + cg * 8 + e, t);
+    }
+  }
+}
+
+cudaError_t colsum_bf16(const __nv_bfloat16* dy, long long rows, int c, long long ld, float* db,
+                        cudaStream_t s) {
+  if (c % 8 != 0) return cudaErrorInvalidValue;
+  int cv = c / 8;
+  int gy = (cv + 31) / 32;
+  long long want_blocks = static_cast<long long>(num_sms()) * 8 / gy + 1;
+  long long rpb = std::max<long long>(64, (rows + want_blocks - 1) / want_blocks);
+  long long gx = (rows + rpb - 1) / rpb;
+  colsum_kernel<<<dim3(static_cast<unsigned>(gx), gy), 256, 0, s>>>(dy, rows, c, ld, db, rpb);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ weight re-layouts
+__global__ void conv_weight_prep_kernel(const float* __restrict__ w, int co, int taps, int ci,
+                                        __nv_bfloat16* __restrict__ wf,
+                                        __nv_bfloat16* __restrict__ wd) {
+  const long long total = static_cast<long long>(co) * taps * ci;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    int c_in = static_cast<int>(i % ci);
+    long long t2 = i / ci;
+    int t = static_cast<int>(t2 % taps);
+    int c_out = static_cast<int>(t2 / taps);
+    __nv_bfloat16 b = __float2bfloat16_rn(w[i]);
+    wf[i] = b;
+    if (wd != nullptr) wd[(static_cast<long long>(c_in) * taps + (taps - 1 - t)) * co + c_out] = b;
+  }
+}
+
+cudaError_t conv_weight_prep(const float* w, int co, int taps, int ci, __nv_bfloat16* wf,
+                             __nv_bfloat16* wd, cudaStream_t s) {
+  long long total = static_cast<long long>(co) * taps * ci;
+  conv_weight_prep_kernel<<<grid_for(total, 256), 256, 0, s>>>(w, co, taps, ci, wf, wd);
+  return cudaGetLastError();
+}
+
+__global__ void cast_kernel(const float* __restrict__ x, long long n, __nv_bfloat16* __restrict__ y) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    y[i] = __float2bfloat16_rn(x[i]);
+}
+
+cudaError_t cast_bf16(const float* x, long long n, __nv_bfloat16* y, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  cast_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, y);
+  return cudaGetLastError();
+}
+
+}  // namespace ralpb

@@ -1,0 +1,50 @@
+// HBM-bound kernels of the step: input packing, max-pool fwd/bwd, softmax
+// cross-entropy, SGD-momentum, bias-gradient column sums, weight re-layouts.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ralpb {
+
+// fp32 NHWC [n][h][w][c] -> bf16 [n][h+2p][w+2p][cp] (zero border, zero channels c..cp).
+cudaError_t pack_input(const float* x, int n, int h, int w, int c, __nv_bfloat16* out, int cp,
+                       int pad, cudaStream_t s);
+
+// Max pool, window k, stride st (no pool padding).  x: [n][h+2pi][w+2pi][c]; y:
+// [n][oh+2po][ow+2po][c] with zero border.  Ties resolve to the first maximum
+// in row-major window order.
+cudaError_t maxpool_fwd(const __nv_bfloat16* x, int n, int h, int w, int c, int pad_in, int k,
+                        int st, __nv_bfloat16* y, int pad_out, cudaStream_t s);
+// dx[i] = sum over windows containing i where i is the (first) argmax: dy[window],
+// then times (x[i] > 0) (the ReLU of the producing conv).  dx has x's padded layout,
+// border written as zero.
+cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* dy, int n, int h, int w,
+                        int c, int pad_in, int k, int st, int pad_out, __nv_bfloat16* dx,
+                        cudaStream_t s);
+
+// Softmax cross-entropy over rows of fp32 logits (row stride ld).  Writes per-row
+// loss (natural log) to row_loss and dlogits = (softmax - onehot) * scale as bf16
+// (row stride ld_d).
+cudaError_t softmax_xent(const float* logits, int rows, int classes, long long ld,
+                         const int32_t* labels, float scale, float* row_loss,
+                         __nv_bfloat16* dlogits, long long ld_d, cudaStream_t s);
+// out[0] = scale * sum(x[0..n)) (single block, deterministic).
+cudaError_t reduce_sum(const float* x, int n, float scale, float* out, cudaStream_t s);
+
+// v = mu*v + gscale*g ; p -= lr*v  (PyTorch SGD-momentum form, no dampening/decay).
+cudaError_t sgd_momentum(float* p, float* v, const float* g, long long n, float lr, float mu,
+                         float gscale, cudaStream_t s);
+
+// db[c] += sum_r dy[r][c]   (bf16 input, fp32 atomics into db).
+cudaError_t colsum_bf16(const __nv_bfloat16* dy, long long rows, int c, long long ld, float* db,
+                        cudaStream_t s);
+
+// Conv weights fp32 [co][t][ci] -> bf16 forward copy [co][t][ci] and bf16
+// backward-data copy [ci][taps-1-t][co].  wd may be null.
+cudaError_t conv_weight_prep(const float* w, int co, int taps, int ci, __nv_bfloat16* wf,
+                             __nv_bfloat16* wd, cudaStream_t s);
+// fp32 -> bf16 cast.
+cudaError_t cast_bf16(const float* x, long long n, __nv_bfloat16* y, cudaStream_t s);
+
+}  // namespace ralpb

@@ -1,0 +1,243 @@
+// Kernel body of the tcgen05 GEMM engine (included by gemm_host.cu only).
+#pragma once
+#include "gemm_types.cuh"
+
+namespace ralpb {
+
+__device__ __forceinline__ bool is_border_row(const GemmParams& p, int m) {
+  int r = m % p.img_rows;
+  int ph = r / p.wp;
+  int pw = r - ph * p.wp;
+  return ph < p.pad || ph >= p.h + p.pad || pw < p.pad || pw >= p.w + p.pad;
+}
+
+// Issue the TMA loads of one operand for one k-block.
+__device__ __forceinline__ void load_operand(const CUtensorMap* tm, int mode, uint8_t* dst,
+                                             uint64_t* bar, int tile0, int rows, int kblk,
+                                             int kb, int swz, const GemmParams& p, bool is_a) {
+  if (mode == LD_K) {
+    tma_load_2d(dst, tm, bar, kblk * kb, tile0);
+  } else if (mode == LD_K_CONV) {
+    int tap = kblk / p.cblks;
+    int cb = kblk - tap * p.cblks;
+    tma_load_2d(dst, tm, bar, cb * kb, tile0 + p.tap_off[tap]);
+  } else {
+    const int atom = swz / 2;              // MN elements per swizzle atom
+    const int natoms = rows / atom;
+    const int atom_bytes = 64 * swz;       // 64 K-rows per block
+    const int k0 = kblk * 64;
+    for (int j = 0; j < natoms; ++j) {
+      int mn = tile0 + j * atom;
+      if (mode == LD_MN) {
+        tma_load_2d(dst + j * atom_bytes, tm, bar, mn, k0);
+      } else {  // LD_MN_CONV
+        int tap = mn / p.a_cin;
+        int ci = mn - tap * p.a_cin;
+        if (tap >= p.taps) { tap = p.taps - 1; }  // rows beyond M: any valid data, never stored
+        tma_load_2d(dst + j * atom_bytes, tm, bar, ci, k0 + p.tap_off[tap]);
+      }
+    }
+  }
+  (void)is_a;
+}
+
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int mode, int swz, int kstep) {
+  if (mode == LD_K || mode == LD_K_CONV) {
+    // K-major: 8-row groups of swz-byte rows; K advances 16 elements = 32 bytes inside the atom.
+    return umma_smem_desc(base + kstep * 32, 16, 8 * swz, swz);
+  }
+  // MN-major: atoms of (swz/2 elements x 64 rows); K advances 16 rows.
+  return umma_smem_desc(base + kstep * 16 * swz, 64 * swz, 8 * swz, swz);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_constant__ GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int stages = p.stages;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + stages * kAStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + stages * p.b_stage_bytes);
+  uint64_t* empty = full + stages;
+  uint64_t* tfull = empty + stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int bn = p.block_n;
+  const uint32_t tmem_cols = bn * 2 <= 32 ? 32 : (bn * 2 <= 64 ? 64 : (bn * 2 <= 128 ? 128 : (bn * 2 <= 256 ? 256 : 512)));
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.tmA);
+    tma_prefetch(&p.tmB);
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int total = p.n_mt * p.n_nt * p.n_ks;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+        int nt = w % p.n_nt;
+        int t = w / p.n_nt;
+        int mt = t % p.n_mt;
+        int ks = t / p.n_mt;
+        int kb0 = ks * p.kblocks_per_split;
+        int kb1 = min(kb0 + p.kblocks_per_split, p.kblocks_total);
+        for (int kk = kb0; kk < kb1; ++kk) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], p.a_bytes + p.b_bytes);
+          load_operand(&p.tmA, p.a_mode, sA + stage * kAStage, &full[stage], mt * kBM, kBM, kk,
+                       p.kb, p.a_swz, p, true);
+          load_operand(&p.tmB, p.b_mode, sB + stage * p.b_stage_bytes, &full[stage], nt * bn, bn,
+                       kk, p.kb, p.b_swz, p, false);
+          if (++stage == stages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      const bool a_k = p.a_mode == LD_K || p.a_mode == LD_K_CONV;
+      const int ksteps = a_k ? p.kb / 16 : 4;
+      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+        int t = w / p.n_nt;
+        int ks = t / p.n_mt;
+        int kb0 = ks * p.kblocks_per_split;
+        int kb1 = min(kb0 + p.kblocks_per_split, p.kblocks_total);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * bn;
+        for (int kk = kb0; kk < kb1; ++kk) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * kAStage);
+          const uint32_t b_base = smem_u32(sB + stage * p.b_stage_bytes);
+          for (int s = 0; s < ksteps; ++s) {
+            uint64_t ad = operand_desc(a_base, p.a_mode, p.a_swz, s);
+            uint64_t bd = operand_desc(b_base, p.b_mode, p.b_swz, s);
+            umma_bf16(d_tmem, ad, bd, p.idesc, (kk > kb0 || s > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == stages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int nt = w % p.n_nt;
+      int t = w / p.n_nt;
+      int mt = t % p.n_mt;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int m = mt * kBM + row;
+      const bool row_ok = m < p.M;
+      const bool zero_row = row_ok && p.border && is_border_row(p, m);
+      const uint32_t t_base = tmem_base + acc * bn + (static_cast<uint32_t>(q * 32) << 16);
+      for (int c = 0; c < bn; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(t_base + c, r);
+        tmem_wait_ld();
+        const int n0 = nt * bn + c;
+        if (!row_ok || n0 >= p.N) continue;
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        const bool full_chunk = n0 + 32 <= p.N;
+        if (p.bias != nullptr) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] += (full_chunk || n0 + j < p.N) ? __ldg(p.bias + n0 + j) : 0.f;
+        }
+        if (p.relu) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+        }
+        if (p.mask != nullptr) {
+          const __nv_bfloat16* mp = p.mask + static_cast<long long>(m) * p.mask_s + n0;
+          if (full_chunk) {
+#pragma unroll
+            for (int j4 = 0; j4 < 4; ++j4) {
+              uint4 u = *reinterpret_cast<const uint4*>(mp + j4 * 8);
+              const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                if (!(__bfloat162float(hb[e]) > 0.f)) v[j4 * 8 + e] = 0.f;
+            }
+          } else {
+            for (int j = 0; j < 32 && n0 + j < p.N; ++j)
+              if (!(__bfloat162float(mp[j]) > 0.f)) v[j] = 0.f;
+          }
+        }
+        if (zero_row) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        }
+        if (p.epi == EPI_BF16) {
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + m * p.s_m + n0 * p.s_n;
+          if (full_chunk && p.s_n == 1) {
+#pragma unroll
+            for (int j4 = 0; j4 < 4; ++j4) {
+              uint4 u;
+              u.x = pack_bf16(v[j4 * 8 + 0], v[j4 * 8 + 1]);
+              u.y = pack_bf16(v[j4 * 8 + 2], v[j4 * 8 + 3]);
+              u.z = pack_bf16(v[j4 * 8 + 4], v[j4 * 8 + 5]);
+              u.w = pack_bf16(v[j4 * 8 + 6], v[j4 * 8 + 7]);
+              *reinterpret_cast<uint4*>(o + j4 * 8) = u;
+            }
+          } else {
+            for (int j = 0; j < 32 && n0 + j < p.N; ++j) o[j * p.s_n] = __float2bfloat16_rn(v[j]);
+          }
+        } else if (p.epi == EPI_F32) {
+          float* o = reinterpret_cast<float*>(p.out) + m * p.s_m + n0 * p.s_n;
+          if (full_chunk && p.s_n == 1) {
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4)
+              *reinterpret_cast<float4*>(o + j4 * 4) =
+                  make_float4(v[j4 * 4], v[j4 * 4 + 1], v[j4 * 4 + 2], v[j4 * 4 + 3]);
+          } else {
+            for (int j = 0; j < 32 && n0 + j < p.N; ++j) o[j * p.s_n] = v[j];
+          }
+        } else {  // EPI_F32_ATOMIC
+          float* o = reinterpret_cast<float*>(p.out) + m * p.s_m + n0 * p.s_n;
+          for (int j = 0; j < 32 && n0 + j < p.N; ++j) red_add_f32(o + j * p.s_n, v[j]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, tmem_cols);
+  }
+}
+
+}  // namespace ralpb

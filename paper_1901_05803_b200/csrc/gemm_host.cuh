@@ -1,0 +1,47 @@
+// Host-side planning for the tcgen05 GEMM engine: tensor-map encoding, tile /
+// split-K choice and the persistent launch.  Internal C++ API (no torch types).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <string>
+#include "gemm_types.cuh"
+
+namespace ralpb {
+
+struct Operand2D {
+  const void* ptr = nullptr;  // bf16, row-major [rows][cols] with leading dimension ld (elements)
+  long long rows = 0, cols = 0, ld = 0;
+};
+
+struct GemmDesc {
+  int M = 0, N = 0;
+  long long K = 0;            // reduction extent: elements (K-major) or rows (MN-major)
+  int a_mode = LD_K, b_mode = LD_K;
+  Operand2D a, b;
+  int kb = 64;                // K elements per k-block for K-major operands (16/32/64)
+  int block_n = 0;            // 0 = choose
+  int k_splits = 1;           // 0 = choose (split-K; only valid with EPI_F32_ATOMIC)
+  // implicit conv
+  int taps = 1;
+  int tap_off[kMaxTaps] = {0};
+  int cblks = 1;
+  int a_cin = 0;
+  // epilogue
+  int epi = EPI_BF16;
+  int relu = 0;
+  void* out = nullptr;
+  long long s_m = 0, s_n = 1;
+  const float* bias = nullptr;
+  const void* mask = nullptr;
+  long long mask_s = 0;
+  int border = 0;
+  int img_rows = 1, wp = 1, pad = 0, h = 0, w = 0;
+};
+
+// Returns cudaSuccess or an error; on a planning error returns cudaErrorInvalidValue and
+// fills *why.
+cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why);
+
+int num_sms();
+
+}  // namespace ralpb

@@ -1,0 +1,65 @@
+// Warp-specialised, persistent tcgen05 GEMM engine used by every dense
+// contraction of the layer-placed step (conv fwd / dgrad / wgrad as implicit
+// GEMMs over the padded-NHWC activation layout, FC fwd / dgrad / wgrad on the
+// PS-owner GPU).
+//
+//   D[m, n] = sum_k A[m, k] * B[n, k]       (bf16 operands, fp32 in TMEM)
+//
+// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer,
+// warp 2 = TMEM allocator, warps 4..7 = epilogue (one TMEM lane = one row each).
+// Accumulators are double-buffered in TMEM so the epilogue of tile i overlaps
+// the main loop of tile i+1.
+//
+// Operand "modes" describe how a K-block of an operand tile is fetched by TMA:
+//   LD_K       K-major 2-D matrix [rows][K]; box {kb, rows}
+//   LD_K_CONV  K-major, rows shifted by a per-tap offset: implicit-GEMM conv
+//              over the padded-flattened NHWC layout (k-block -> (tap, cblk))
+//   LD_MN      MN-major 2-D matrix [K][cols]; box {atom, 64} per MN atom
+//   LD_MN_CONV MN-major, M index = (tap, ci), rows shifted by the tap offset
+//              (the activation operand of conv wgrad)
+#pragma once
+#include "ptx.cuh"
+
+namespace ralpb {
+
+enum LoadMode : int { LD_K = 0, LD_K_CONV = 1, LD_MN = 2, LD_MN_CONV = 3 };
+enum EpiMode : int { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_ATOMIC = 2 };
+
+constexpr int kBM = 128;
+constexpr int kMaxTaps = 32;
+constexpr int kAStage = 128 * 128;  // 16 KB: 128 rows x 128 B (or 2 MN atoms x 64 rows)
+constexpr int kThreads = 256;
+
+struct alignas(64) GemmParams {
+  CUtensorMap tmA;
+  CUtensorMap tmB;
+  int M, N;                 // output extent (rows of A, rows of B)
+  int n_mt, n_nt, n_ks;     // tile grid (m tiles, n tiles, k splits)
+  int kblocks_total;        // k-blocks over the whole K
+  int kblocks_per_split;
+  int block_n;              // BN (32..256)
+  int kb;                   // K elements per k-block (K-major); MN-major blocks are 64 rows
+  int stages;
+  int b_stage_bytes;
+  uint32_t idesc;
+  int a_mode, b_mode;
+  int a_swz, b_swz;         // swizzle row bytes (32/64/128)
+  int a_bytes, b_bytes;     // TMA bytes per stage
+  // implicit-conv geometry
+  int cblks;                // k-blocks per tap (LD_K_CONV)
+  int a_cin;                // channels per tap (LD_MN_CONV)
+  int taps;
+  int tap_off[kMaxTaps];    // row offset per tap in the padded-flattened layout
+  // epilogue
+  int epi;
+  int relu;
+  void* out;
+  long long s_m, s_n;       // element strides of out
+  const float* bias;        // per-n bias (or nullptr)
+  const __nv_bfloat16* mask;  // relu-backward mask source (mask[m*mask_s + n] > 0), or nullptr
+  long long mask_s;
+  int border;               // zero rows that are padding positions of the padded layout
+  int img_rows, wp, pad, h, w;
+};
+
+}  // namespace ralpb

@@ -1,0 +1,161 @@
+"""Per-kernel numerics: each sm_100a kernel against a plain PyTorch fp32
+reference of the same op on the same (bf16-rounded) inputs."""
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_1901_05803_b200 import ops
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _bf(*shape, scale=1.0, gen=None):
+    return (torch.randn(*shape, generator=gen, device=DEV) * scale).to(torch.bfloat16)
+
+
+def _close(got, ref, rtol=2e-2, atol=None):
+    got = got.float()
+    ref = ref.float()
+    if atol is None:
+        atol = 2e-2 * ref.abs().max().item() + 1e-6
+    torch.testing.assert_close(got, ref, rtol=rtol, atol=atol)
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(128, 64, 64, 0), (256, 256, 512, 0), (300, 200, 320, 0),
+                                      (1024, 1000, 4096, 0), (128, 32, 128, 32), (512, 128, 1024, 128)])
+def test_gemm_kk(M, N, K, bn):
+    g = torch.Generator(device=DEV).manual_seed(0)
+    a, b = _bf(M, K, gen=g), _bf(N, K, gen=g)
+    bias = torch.randn(N, device=DEV)
+    out = ops.gemm(a, b, bias=bias, relu=True, block_n=bn)
+    ref = torch.relu(a.float() @ b.float().t() + bias)
+    _close(out, ref)
+    out32 = ops.gemm(a, b, out_kind="f32")
+    _close(out32, a.float() @ b.float().t(), rtol=1e-3, atol=1e-3 * (K ** 0.5))
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 512, 256), (1024, 4096, 1000)])
+def test_gemm_k_mn(M, N, K):
+    # FC dgrad shape: dX[M=rows, N=in] = dY[rows, K=out] @ W[out, in]
+    g = torch.Generator(device=DEV).manual_seed(1)
+    a, w = _bf(M, K, gen=g), _bf(K, N, gen=g)
+    out = ops.gemm(a, w, b_mn=True, out_kind="f32")
+    _close(out, a.float() @ w.float(), rtol=1e-3, atol=1e-3 * (K ** 0.5))
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (256, 512, 1024), (1000, 4096, 512)])
+def test_gemm_mn_mn(M, N, K):
+    # FC wgrad shape: dW[M=out, N=in] = dY[K=rows, out]^T @ X[rows, in]
+    g = torch.Generator(device=DEV).manual_seed(2)
+    dy, x = _bf(K, M, gen=g), _bf(K, N, gen=g)
+    out = ops.gemm(dy, x, a_mn=True, b_mn=True, out_kind="f32")
+    _close(out, dy.float().t() @ x.float(), rtol=1e-3, atol=1e-3 * (K ** 0.5))
+    out2 = ops.gemm(dy, x, a_mn=True, b_mn=True, out_kind="f32_atomic", k_splits=0)
+    _close(out2, dy.float().t() @ x.float(), rtol=1e-3, atol=1e-3 * (K ** 0.5))
+
+
+def _pad(x_nhwc, p):
+    return F.pad(x_nhwc, (0, 0, p, p, p, p))
+
+
+CONV_CASES = [
+    # n, h, w, cin, cout, k, pad
+    (2, 8, 16, 64, 64, 3, 1),
+    (2, 14, 14, 128, 256, 3, 1),
+    (1, 28, 28, 256, 512, 3, 1),
+    (3, 20, 12, 16, 64, 3, 1),
+    (2, 32, 32, 32, 64, 5, 2),
+    (2, 32, 32, 16, 32, 5, 2),
+]
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_fwd(case):
+    n, h, w, cin, cout, k, pad = case
+    g = torch.Generator(device=DEV).manual_seed(3)
+    x = _pad(_bf(n, h, w, cin, gen=g), pad).contiguous()
+    wt = _bf(cout, k * k, cin, scale=(2.0 / (k * k * cin)) ** 0.5, gen=g)
+    bias = torch.randn(cout, device=DEV) * 0.1
+    y = ops.conv_fwd(x, wt, bias, n=n, h=h, w_=w, cin=cin, cout=cout, k=k, pad=pad, relu=True)
+    xr = x[:, pad:pad + h, pad:pad + w, :].permute(0, 3, 1, 2).float()
+    wr = wt.float().view(cout, k, k, cin).permute(0, 3, 1, 2)
+    ref = torch.relu(F.conv2d(xr, wr, bias, padding=pad)).permute(0, 2, 3, 1)
+    _close(y[:, pad:pad + h, pad:pad + w, :], ref)
+    border = y.clone()
+    border[:, pad:pad + h, pad:pad + w, :] = 0
+    assert border.abs().max().item() == 0.0
+
+
+@pytest.mark.parametrize("case", [c for c in CONV_CASES if c[3] >= 32])
+def test_conv_dgrad(case):
+    n, h, w, cin, cout, k, pad = case
+    g = torch.Generator(device=DEV).manual_seed(4)
+    dy = _pad(_bf(n, h, w, cout, gen=g), pad).contiguous()
+    w32 = torch.randn(cout, k * k, cin, generator=g, device=DEV) * (2.0 / (k * k * cin)) ** 0.5
+    wf, wd = ops.conv_weight_prep(w32)
+    mask = _pad(torch.relu(_bf(n, h, w, cin, gen=g).float()).to(torch.bfloat16), pad).contiguous()
+    dx = ops.conv_dgrad(dy, wd, mask, n=n, h=h, w_=w, cin=cin, cout=cout, k=k, pad=pad)
+    dyr = dy[:, pad:pad + h, pad:pad + w, :].permute(0, 3, 1, 2).float()
+    wr = wf.float().view(cout, k, k, cin).permute(0, 3, 1, 2)
+    ref = F.conv_transpose2d(dyr, wr, padding=pad).permute(0, 2, 3, 1)
+    ref = ref * (mask[:, pad:pad + h, pad:pad + w, :].float() > 0)
+    _close(dx[:, pad:pad + h, pad:pad + w, :], ref)
+    border = dx.clone()
+    border[:, pad:pad + h, pad:pad + w, :] = 0
+    assert border.abs().max().item() == 0.0
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_wgrad(case):
+    n, h, w, cin, cout, k, pad = case
+    g = torch.Generator(device=DEV).manual_seed(5)
+    x = _pad(_bf(n, h, w, cin, gen=g), pad).contiguous()
+    dy = _pad(_bf(n, h, w, cout, gen=g), pad).contiguous()
+    dw = ops.conv_wgrad(x, dy, n=n, h=h, w_=w, cin=cin, cout=cout, k=k, pad=pad)
+    xr = x[:, pad:pad + h, pad:pad + w, :].permute(0, 3, 1, 2).float()
+    dyr = dy[:, pad:pad + h, pad:pad + w, :].permute(0, 3, 1, 2).float()
+    ref = torch.nn.grad.conv2d_weight(xr, (cout, cin, k, k), dyr, padding=pad)  # [co, ci, k, k]
+    ref = ref.permute(0, 2, 3, 1).reshape(cout, k * k, cin)
+    _close(dw, ref, rtol=1e-3, atol=1e-3 * ref.abs().max().item())
+
+
+def test_pool_fwd_bwd():
+    n, h, w, c, pad = 2, 8, 12, 64, 1
+    g = torch.Generator(device=DEV).manual_seed(6)
+    x = _pad(torch.relu(_bf(n, h, w, c, gen=g).float()).to(torch.bfloat16), pad).contiguous()
+    y = ops.maxpool_fwd(x, n=n, h=h, w=w, c=c, pad_in=pad, k=2, stride=2, pad_out=1)
+    xr = x[:, pad:pad + h, pad:pad + w, :].permute(0, 3, 1, 2).float().requires_grad_(True)
+    ref = F.max_pool2d(xr, 2)
+    torch.testing.assert_close(y[:, 1:-1, 1:-1, :].float(), ref.permute(0, 2, 3, 1), rtol=0, atol=0)
+    dy = _bf(n, h // 2, w // 2, c, gen=g)
+    dx = ops.maxpool_bwd(x, dy.contiguous(), n=n, h=h, w=w, c=c, pad_in=pad, k=2, stride=2, pad_out=0)
+    ref.backward(dy.permute(0, 3, 1, 2).float())
+    refdx = xr.grad.permute(0, 2, 3, 1) * (xr.detach().permute(0, 2, 3, 1) > 0)
+    torch.testing.assert_close(dx[:, pad:pad + h, pad:pad + w, :].float(), refdx, rtol=0, atol=0)
+
+
+def test_softmax_xent():
+    g = torch.Generator(device=DEV).manual_seed(7)
+    logits = torch.randn(256, 1000, generator=g, device=DEV)
+    labels = torch.randint(0, 1000, (256,), generator=g, device=DEV, dtype=torch.int32)
+    row_loss, dl = ops.softmax_xent(logits, labels, 1.0 / 256)
+    ref = F.cross_entropy(logits, labels.long(), reduction="none")
+    torch.testing.assert_close(row_loss, ref, rtol=1e-5, atol=1e-5)
+    lg = logits.clone().requires_grad_(True)
+    F.cross_entropy(lg, labels.long()).backward()
+    _close(dl, lg.grad, rtol=1e-2, atol=1e-6)
+
+
+def test_sgd_and_colsum():
+    g = torch.Generator(device=DEV).manual_seed(8)
+    p = torch.randn(1001, generator=g, device=DEV)
+    v = torch.randn(1001, generator=g, device=DEV)
+    gr = torch.randn(1001, generator=g, device=DEV)
+    p0, v0 = p.clone(), v.clone()
+    ops.sgd_momentum(p, v, gr, 0.01, 0.9, 0.5)
+    v_ref = 0.9 * v0 + 0.5 * gr
+    torch.testing.assert_close(v, v_ref)
+    torch.testing.assert_close(p, p0 - 0.01 * v_ref)
+    dy = _bf(5000, 192, gen=g)
+    torch.testing.assert_close(ops.colsum(dy), dy.float().sum(0), rtol=1e-4, atol=1e-3)
