@@ -79,6 +79,59 @@ int ralpb_colsum_bf16(const void* dy, long long rows, int c, long long ld, float
 int ralpb_conv_weight_prep(const float* w, int co, int taps, int ci, void* wf, void* wd, void* stream);
 int ralpb_cast_bf16(const float* x, long long n, void* y, void* stream);
 
+/* ------------------------------------------------------------ executor
+ * One ralpb_model per rank (one process per GPU).  The layer table is the
+ * reference ModelGraph (pkg/src/ralp/layers.py:204-267) lowered by the Python
+ * package; `split` is the 1-based cut index chosen by profile()/find_split()
+ * (profiler.py:101-134,187-227); the strategy mirrors StrategyKind
+ * (costmodel.py:34-37): RALP = conv front replicated + FC tail on the PS rank,
+ * BASELINE_PS = every layer on every worker, all parameters through the PS. */
+enum { RALPB_CONV = 0, RALPB_POOL = 1, RALPB_FC = 2 };
+enum { RALPB_STRATEGY_BASELINE = 0, RALPB_STRATEGY_RALP = 1 };
+
+typedef struct {
+  int kind;            /* RALPB_CONV / RALPB_POOL / RALPB_FC */
+  int k, stride, pad;  /* window geometry (conv / pool) */
+  int h, w, cin;       /* per-sample input shape (fc: cin = input features, h = w = 0) */
+  int cout;            /* conv output channels / fc output features */
+  int relu;            /* ReLU after the layer (conv, fc except the last) */
+} ralpb_layer_desc;
+
+typedef struct {
+  double loss;                 /* mean cross-entropy over the job's W*b samples (PS rank; NaN elsewhere) */
+  long long logical_bytes;     /* job-wide synchronised bytes this step at elem_bytes (== volume_*()) */
+  long long physical_bytes;    /* bytes this rank moved over NVLink this step (loads + stores) */
+  int launches;                /* kernels this rank launched in the step */
+  float ms_step;               /* device time of the whole step on this rank (CUDA events) */
+  float ms_front_fwd;          /* worker front forward */
+  float ms_back;               /* PS back segment incl. waiting for cut activations */
+  float ms_front_bwd;          /* worker front backward incl. waiting for the act-grad */
+  float ms_sync;               /* parameter synchronisation (sharded PS) + weight re-layout */
+} ralpb_step_stats;
+
+typedef struct ralpb_model ralpb_model;
+
+/* Replaces JobSpec + _JobRun.__init__ (costmodel.py:64-86, simulator.py:517-567). */
+int ralpb_model_create(const ralpb_layer_desc* layers, int n_layers, int split, int batch, int strategy,
+                       int rank, int world, int ps_rank, int elem_bytes, ralpb_model** out);
+void ralpb_model_destroy(ralpb_model* m);
+/* 64-byte CUDA IPC handle of this rank's exchange arena; ralpb_model_ipc_open takes
+ * world*64 bytes (rank-major) and maps the peers. */
+int ralpb_model_ipc_handle(ralpb_model* m, void* out64);
+int ralpb_model_ipc_open(ralpb_model* m, const void* handles);
+/* Host (on_host=1) or device fp32 parameters of layer `layer` (0-based):
+ * conv w [cout][k][k][cin], b [cout]; fc w [out][in] (in = HWC-flattened), b [out]. */
+int ralpb_model_set_params(ralpb_model* m, int layer, const float* w, const float* b, int on_host);
+int ralpb_model_get_params(ralpb_model* m, int layer, float* w, float* b, int on_host);
+/* One training step of this rank's worker batch: images [b][h][w][c] fp32 NHWC, labels [b] int32,
+ * host (pinned for async copies) or device memory.  Executes _ralp_worker/_ralp_ps
+ * (simulator.py:669-715) or _baseline_worker/_baseline_ps (simulator.py:637-665). */
+int ralpb_model_step(ralpb_model* m, const void* images, const int32_t* labels, int on_host, float lr,
+                     float mu);
+/* Synchronises the model stream and reports the last step. */
+int ralpb_model_stats(ralpb_model* m, ralpb_step_stats* out);
+void* ralpb_model_stream(ralpb_model* m);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,222 @@
+"""Oracle restatement of one layer-placed (RALP) / all-on-PS (baseline) training step
+on the CPU in plain PyTorch fp32 (test infrastructure only).
+
+Schedule (pkg/src/ralp/simulator.py:669-715 for RALP, :637-665 for the baseline):
+  RALP      W worker fronts (conv/pool) on their own batches -> cuts concatenated
+            (W*b rows, HWC flatten, layers.py:62-66) -> FC tail once on the PS with
+            FC weights fixed for the whole step -> act-grads split
+            back -> W front backwards -> conv grads summed -> SGD-momentum; the FC tail
+            is updated locally on the PS.
+  baseline  every worker runs the whole model on its own batch; all grads summed.
+Loss = mean cross-entropy over the W*b samples of the step; SGD in the PyTorch
+form v = mu*v + g, p -= lr*v; ReLU after every conv/FC except the last;
+max pool routes to the first maximum in row-major window order.
+
+`emulate_bf16=True` rounds to bf16 exactly where the B200 path stores bf16
+(packed input, every activation and activation-gradient, the bf16 weight copies
+used by the GEMMs, dlogits) and keeps fp32 everywhere else (GEMM accumulation,
+logits, gradients of parameters, master weights, momentum).
+
+The byte counter adds the descriptor-unit (elem_bytes) size of every logical
+transfer at the reference's count_wire sites (simulator.py:647,663,677,689,707,713).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+
+@dataclass
+class OracleState:
+    layers: list            # lowered layer dicts (kind, k, stride, pad, h, w, cin, cout, relu)
+    params: list            # per layer: (w, b) fp32 numpy (conv w [cout][k][k][cin], fc w [out][in]) or None
+    momentum: list = field(default_factory=list)
+
+    def __post_init__(self):
+        self.params = [None if p is None else (torch.tensor(p[0], dtype=torch.float32),
+                                               torch.tensor(p[1], dtype=torch.float32)) for p in self.params]
+        if not self.momentum:
+            self.momentum = [None if p is None else (torch.zeros_like(p[0]), torch.zeros_like(p[1]))
+                             for p in self.params]
+
+    def numpy_params(self):
+        return [None if p is None else (p[0].numpy().copy(), p[1].numpy().copy()) for p in self.params]
+
+
+def _round(x: torch.Tensor, on: bool) -> torch.Tensor:
+    return x.to(torch.bfloat16).to(torch.float32) if on else x
+
+
+# Accumulation precision of every contraction (float32 normally; float64 to measure the
+# intrinsic sensitivity of the bf16 pipeline to summation-order noise).
+_ACC = [torch.float32]
+
+
+def _acc(*ts):
+    return [None if t is None else t.to(_ACC[0]) for t in ts]
+
+
+def _conv(x, w, b, stride, pad):
+    x, w, b = _acc(x, w, b)
+    return F.conv2d(x, w, b, stride=stride, padding=pad).to(torch.float32)
+
+
+def _mm(a, b):
+    a, b = _acc(a, b)
+    return (a @ b).to(torch.float32)
+
+
+def _conv_w(x, shape, g, stride, pad):
+    x, g = _acc(x, g)
+    return torch.nn.grad.conv2d_weight(x, shape, g, stride=stride, padding=pad).to(torch.float32)
+
+
+def _conv_x(shape, w, g, stride, pad):
+    w, g = _acc(w, g)
+    return torch.nn.grad.conv2d_input(shape, w, g, stride=stride, padding=pad).to(torch.float32)
+
+
+def _split_index(layers) -> int:
+    return next(i for i, L in enumerate(layers) if L["kind"] == "fc")
+
+
+def _front_forward(st: OracleState, nfront: int, imgs: np.ndarray, bf: bool):
+    x = _round(torch.from_numpy(np.ascontiguousarray(imgs)).permute(0, 3, 1, 2).contiguous(), bf)
+    acts = [x]
+    for i in range(nfront):
+        L = st.layers[i]
+        if L["kind"] == "conv":
+            w, b = st.params[i]
+            wt = _round(w.permute(0, 3, 1, 2).contiguous(), bf)
+            x = _round(torch.relu(_conv(x, wt, b, L["stride"], L["pad"])), bf)
+        else:
+            x = F.max_pool2d(x, L["k"], L["stride"])
+        acts.append(x)
+    cut = x.permute(0, 2, 3, 1).reshape(x.shape[0], -1)  # HWC flatten
+    return acts, cut
+
+
+def _back(st: OracleState, nfront: int, x: torch.Tensor, labels: np.ndarray, scale: float, bf: bool):
+    """FC tail fwd + CE + bwd on R rows; returns (mean loss, {layer: (gw, gb)}, d(cut))."""
+    fcs = list(range(nfront, len(st.layers)))
+    hs = [x]
+    logits = None
+    for j, li in enumerate(fcs):
+        w, b = st.params[li]
+        z = _mm(hs[-1], _round(w, bf).t()) + b
+        if j + 1 < len(fcs):
+            hs.append(_round(torch.relu(z), bf))
+        else:
+            logits = z
+    lab = torch.from_numpy(np.asarray(labels, dtype=np.int64))
+    lse = torch.logsumexp(logits, dim=1)
+    row_loss = lse - logits.gather(1, lab[:, None])[:, 0]
+    p = torch.exp(logits - lse[:, None])
+    onehot = F.one_hot(lab, logits.shape[1]).to(torch.float32)
+    dy = _round((p - onehot) * scale, bf)
+    grads = {}
+    for j in reversed(range(len(fcs))):
+        li = fcs[j]
+        w, _ = st.params[li]
+        xin = hs[j]
+        grads[li] = (_mm(dy.t(), xin), dy.sum(0))
+        dx = _mm(dy, _round(w, bf))
+        if j > 0:
+            dx = dx * (xin > 0)
+        dy = _round(dx, bf)
+    return float(row_loss.mean()), grads, dy
+
+
+def _front_backward(st: OracleState, nfront: int, acts, dcut: torch.Tensor, bf: bool):
+    last = acts[-1]
+    g = dcut.reshape(last.shape[0], last.shape[2], last.shape[3], last.shape[1]).permute(0, 3, 1, 2)
+    grads = {}
+    for i in reversed(range(nfront)):
+        L = st.layers[i]
+        xin = acts[i]
+        if L["kind"] == "pool":
+            xr = xin.detach().clone().requires_grad_(True)
+            F.max_pool2d(xr, L["k"], L["stride"]).backward(g)
+            g = _round(xr.grad * (xin > 0), bf)
+        else:
+            w, _ = st.params[i]
+            wt = _round(w.permute(0, 3, 1, 2).contiguous(), bf)
+            gw = _conv_w(xin, wt.shape, g, L["stride"], L["pad"])
+            grads[i] = (gw.permute(0, 2, 3, 1).contiguous(), g.sum(dim=(0, 2, 3)))
+            if i > 0:
+                gx = _conv_x(xin.shape, wt, g, L["stride"], L["pad"])
+                if st.layers[i - 1]["kind"] == "conv":
+                    gx = gx * (xin > 0)
+                g = _round(gx, bf)
+    return grads
+
+
+def _sgd(st: OracleState, idx, grad, lr, mu):
+    (w, b), (vw, vb) = st.params[idx], st.momentum[idx]
+    vw.mul_(mu).add_(grad[0])
+    vb.mul_(mu).add_(grad[1])
+    w.sub_(lr * vw)
+    b.sub_(lr * vb)
+
+
+def _accumulate(total: dict, part: dict):
+    for k, (gw, gb) in part.items():
+        if k in total:
+            total[k] = (total[k][0] + gw, total[k][1] + gb)
+        else:
+            total[k] = (gw.clone(), gb.clone())
+
+
+def param_count(L) -> int:
+    if L["kind"] == "conv":
+        return L["k"] * L["k"] * L["cin"] * L["cout"] + L["cout"]
+    if L["kind"] == "fc":
+        return L["cin"] * L["cout"] + L["cout"]
+    return 0
+
+
+def train_step(st: OracleState, strategy: str, workers: int, batches, *, lr: float = 0.01, mu: float = 0.9,
+               emulate_bf16: bool = False, elem_bytes: int = 4, accum64: bool = False):
+    """One step.  batches[r] = (images [b,h,w,c] fp32, labels [b] int) of worker r.
+    Returns (loss, logical_bytes)."""
+    _ACC[0] = torch.float64 if accum64 else torch.float32
+    bf = emulate_bf16
+    nfront = _split_index(st.layers)
+    b = batches[0][0].shape[0]
+    scale = 1.0 / (workers * b)
+    wire = 0
+    p_front = sum(param_count(L) for L in st.layers[:nfront]) * elem_bytes
+    p_all = sum(param_count(L) for L in st.layers) * elem_bytes
+    total: dict = {}
+    if strategy == "ralp":
+        fronts = [_front_forward(st, nfront, imgs, bf) for imgs, _ in batches]
+        cut_bytes = fronts[0][1].numel() * elem_bytes
+        wire += workers * cut_bytes                        # "act" (simulator.py:677)
+        x = torch.cat([c for _, c in fronts], dim=0)
+        labels = np.concatenate([lab for _, lab in batches])
+        loss, fc_grads, dcut = _back(st, nfront, x, labels, scale, bf)
+        wire += workers * cut_bytes                        # "actgrad" (simulator.py:707)
+        for r, (acts, _) in enumerate(fronts):
+            _accumulate(total, _front_backward(st, nfront, acts, dcut[r * b:(r + 1) * b], bf))
+        wire += 2 * workers * p_front                      # "grad" + "pull" (simulator.py:689,713)
+        for idx, g in total.items():
+            _sgd(st, idx, g, lr, mu)
+        for idx, g in fc_grads.items():                    # PS-local FC update
+            _sgd(st, idx, g, lr, mu)
+        return loss, wire
+    if strategy == "baseline":
+        losses = []
+        for imgs, lab in batches:
+            acts, cut = _front_forward(st, nfront, imgs, bf)
+            loss, fc_grads, dcut = _back(st, nfront, cut, lab, scale, bf)
+            losses.append(loss)
+            _accumulate(total, fc_grads)
+            _accumulate(total, _front_backward(st, nfront, acts, dcut, bf))
+        wire += 2 * workers * p_all                         # push + pull (simulator.py:647,663)
+        for idx, g in total.items():
+            _sgd(st, idx, g, lr, mu)
+        return float(np.mean(losses)), wire
+    raise ValueError(strategy)

@@ -38,7 +38,33 @@ SIGNATURES: dict[str, tuple] = {
     "ralpb_colsum_bf16": (c_i, [c_vp, c_ll, c_i, c_ll, c_fp, c_vp]),
     "ralpb_conv_weight_prep": (c_i, [c_fp, c_i, c_i, c_i, c_vp, c_vp, c_vp]),
     "ralpb_cast_bf16": (c_i, [c_fp, c_ll, c_vp, c_vp]),
+    "ralpb_model_create": (c_i, [c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, C.POINTER(c_vp)]),
+    "ralpb_model_destroy": (None, [c_vp]),
+    "ralpb_model_ipc_handle": (c_i, [c_vp, c_vp]),
+    "ralpb_model_ipc_open": (c_i, [c_vp, c_vp]),
+    "ralpb_model_set_params": (c_i, [c_vp, c_i, c_vp, c_vp, c_i]),
+    "ralpb_model_get_params": (c_i, [c_vp, c_i, c_vp, c_vp, c_i]),
+    "ralpb_model_step": (c_i, [c_vp, c_vp, c_vp, c_i, c_f, c_f]),
+    "ralpb_model_stats": (c_i, [c_vp, c_vp]),
+    "ralpb_model_stream": (c_vp, [c_vp]),
 }
+
+
+class LayerDesc(C.Structure):
+    """ralpb_layer_desc (include/ralpb.h)."""
+    _fields_ = [("kind", c_i), ("k", c_i), ("stride", c_i), ("pad", c_i), ("h", c_i), ("w", c_i),
+                ("cin", c_i), ("cout", c_i), ("relu", c_i)]
+
+
+class StepStats(C.Structure):
+    """ralpb_step_stats (include/ralpb.h)."""
+    _fields_ = [("loss", C.c_double), ("logical_bytes", c_ll), ("physical_bytes", c_ll), ("launches", c_i),
+                ("ms_step", c_f), ("ms_front_fwd", c_f), ("ms_back", c_f), ("ms_front_bwd", c_f),
+                ("ms_sync", c_f)]
+
+
+RALPB_CONV, RALPB_POOL, RALPB_FC = 0, 1, 2
+RALPB_STRATEGY_BASELINE, RALPB_STRATEGY_RALP = 0, 1
 
 
 class BackendError(RuntimeError):

@@ -1,0 +1,63 @@
+// C ABI of the executor (ralpb_model_*), see include/ralpb.h.
+#include <string>
+#include "engine.cuh"
+#include "status.cuh"
+
+using namespace ralpb;
+
+struct ralpb_model {
+  Model* impl;
+};
+
+extern "C" {
+
+int ralpb_model_create(const ralpb_layer_desc* layers, int n_layers, int split, int batch, int strategy,
+                       int rank, int world, int ps_rank, int elem_bytes, ralpb_model** out) {
+  std::string why;
+  Model* m = nullptr;
+  if (model_create(layers, n_layers, split, batch, strategy, rank, world, ps_rank, elem_bytes, &m, &why))
+    return set_error("ralpb_model_create: " + why);
+  *out = new ralpb_model{m};
+  return 0;
+}
+
+void ralpb_model_destroy(ralpb_model* m) {
+  if (!m) return;
+  model_destroy(m->impl);
+  delete m;
+}
+
+int ralpb_model_ipc_handle(ralpb_model* m, void* out64) {
+  std::string why;
+  return model_ipc_handle(m->impl, out64, &why) ? set_error("ralpb_model_ipc_handle: " + why) : 0;
+}
+
+int ralpb_model_ipc_open(ralpb_model* m, const void* handles) {
+  std::string why;
+  return model_ipc_open(m->impl, handles, &why) ? set_error("ralpb_model_ipc_open: " + why) : 0;
+}
+
+int ralpb_model_set_params(ralpb_model* m, int layer, const float* w, const float* b, int on_host) {
+  std::string why;
+  return model_set_params(m->impl, layer, w, b, on_host, &why) ? set_error("ralpb_model_set_params: " + why) : 0;
+}
+
+int ralpb_model_get_params(ralpb_model* m, int layer, float* w, float* b, int on_host) {
+  std::string why;
+  return model_get_params(m->impl, layer, w, b, on_host, &why) ? set_error("ralpb_model_get_params: " + why) : 0;
+}
+
+int ralpb_model_step(ralpb_model* m, const void* images, const int32_t* labels, int on_host, float lr,
+                     float mu) {
+  std::string why;
+  return model_step(m->impl, images, labels, on_host, lr, mu, &why) ? set_error("ralpb_model_step: " + why) : 0;
+}
+
+int ralpb_model_stats(ralpb_model* m, ralpb_step_stats* out) {
+  std::string why;
+  return model_stats(m->impl, out, &why) ? set_error("ralpb_model_stats: " + why) : 0;
+}
+
+void* ralpb_model_stream(ralpb_model* m) { return m->impl->stream; }
+
+}  // extern "C"

@@ -293,9 +293,24 @@ __global__ void colsum_kernel(const __nv_bfloat16* __restrict__ dy, long long ro
   }
 }
 
+// Narrow / ragged widths (e.g. a 10-class logit layer): one thread per column strip.
+__global__ void colsum_scalar_kernel(const __nv_bfloat16* __restrict__ dy, long long rows, int c,
+                                     long long ld, float* __restrict__ db) {
+  const int col = threadIdx.x % 32 + 32 * blockIdx.y;
+  const int lane_r = threadIdx.x / 32;
+  if (col >= c) return;
+  float acc = 0.f;
+  for (long long r = blockIdx.x * 8 + lane_r; r < rows; r += 8LL * gridDim.x)
+    acc += __bfloat162float(dy[r * ld + col]);
+  atomicAdd(db + col, acc);
+}
+
 cudaError_t colsum_bf16(const __nv_bfloat16* dy, long long rows, int c, long long ld, float* db,
                         cudaStream_t s) {
-  if (c % 8 != 0) return cudaErrorInvalidValue;
+  if (c % 8 != 0 || ld % 8 != 0) {
+    colsum_scalar_kernel<<<dim3(64, (c + 31) / 32), 256, 0, s>>>(dy, rows, c, ld, db);
+    return cudaGetLastError();
+  }
   int cv = c / 8;
   int gy = (cv + 31) / 32;
   long long want_blocks = static_cast<long long>(num_sms()) * 8 / gy + 1;

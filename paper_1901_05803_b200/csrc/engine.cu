@@ -1,0 +1,628 @@
+// Executor of the layer-placed (RALP) and all-on-PS (baseline) training step.
+//
+// Per rank (one process per GPU), one CUDA stream, step sequence number `seq`:
+//
+//   worker front  : pack images -> [conv (implicit GEMM, bias+ReLU) | maxpool]* -> cut
+//   cut exchange  : the PS rank's own cut is written straight into the FC input
+//                   matrix; every other worker pushes its cut (+labels) into the PS
+//                   rank's FC input rows with 128-bit peer stores and raises a flag
+//   PS back       : FC fwd (bias+ReLU) -> softmax-CE -> FC wgrad/dgrad/bias-grad over
+//                   all W*b rows at once -> FC SGD-momentum (local, never synchronised)
+//                   -> push each worker's rows of the cut gradient back + flag
+//   worker back   : maxpool bwd (ReLU mask) / conv wgrad (split-K) + bias colsum +
+//                   dgrad with the ReLU mask fused into the epilogue
+//   sync          : sharded PS over NVLink: every rank owns 1/W of the front
+//                   parameter vector; reduce-scatter (peer loads) + SGD-momentum +
+//                   all-gather (peer stores) in one kernel, flag barriers around it
+//   re-layout     : fp32 master -> bf16 forward / backward-data filter copies
+//
+// Baseline (StrategyKind.BASELINE_PS): every worker runs every layer on its own batch
+// and the whole parameter vector goes through the sharded PS.
+//
+// Reference: simulator.py:669-715 (RALP worker/PS), :637-665 (baseline), the step
+// semantics of SURVEY.md §7.4 (mean loss over W*b, SGD v=mu*v+g, p-=lr*v, HWC flatten).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include "elementwise.cuh"
+#include "engine.cuh"
+#include "gemm_host.cuh"
+
+namespace ralpb {
+
+namespace {
+
+constexpr int kFlagAct = 0;       // [8]  PS: worker r's cut landed
+constexpr int kFlagActGrad = 8;   // [1]  worker: act-grad landed
+constexpr int kFlagGrad = 16;     // [8]  rank r finished its backward
+constexpr int kFlagDone = 24;     // [8]  rank r finished its shard update
+constexpr int kNumFlags = 64;
+constexpr int kNumCounters = 64;  // last-CTA counters (local)
+
+long long align_up(long long x, long long a) { return (x + a - 1) / a * a; }
+
+#define RALPB_TRY(expr)                                   \
+  do {                                                    \
+    cudaError_t _e = (expr);                              \
+    if (_e != cudaSuccess) {                              \
+      if (why->empty()) *why = std::string(#expr);        \
+      *why += std::string(": ") + cudaGetErrorString(_e); \
+      return 1;                                           \
+    }                                                     \
+  } while (0)
+
+template <class T>
+T* alloc(Model* m, size_t count, std::string* why) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, std::max<size_t>(count * sizeof(T), 16)) != cudaSuccess) {
+    *why = "cudaMalloc failed (" + std::to_string(count * sizeof(T)) + " bytes)";
+    return nullptr;
+  }
+  m->owned.push_back(p);
+  return static_cast<T*>(p);
+}
+
+bool is_ps(const Model* m) { return m->rank == m->ps_rank; }
+
+char* peer(Model* m, int r) { return m->peer_base[r]; }
+template <class T>
+T* at(Model* m, int r, size_t off) { return reinterpret_cast<T*>(peer(m, r) + off); }
+
+}  // namespace
+
+int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int batch, int strategy,
+                 int rank, int world, int ps_rank, int elem_bytes, Model** out, std::string* why) {
+  if (n_layers < 2 || batch < 1 || world < 1 || world > kMaxRanks || rank < 0 || rank >= world ||
+      ps_rank < 0 || ps_rank >= world) {
+    *why = "bad model configuration";
+    return 1;
+  }
+  if (batch % 4 != 0) { *why = "batch must be a multiple of 4"; return 1; }
+  auto m = new Model();
+  m->rank = rank; m->world = world; m->ps_rank = ps_rank; m->batch = batch;
+  m->strategy = strategy; m->elem_bytes = elem_bytes;
+  m->desc.assign(layers, layers + n_layers);
+  cudaGetDevice(&m->device);
+  auto fail = [&](const std::string& w) { *why = w; model_destroy(m); return 1; };
+
+  int nconv = 0;
+  while (nconv < n_layers && layers[nconv].kind != RALPB_FC) ++nconv;
+  if (nconv == 0 || nconv == n_layers) return fail("model needs a conv/pool front and an FC tail");
+  for (int i = nconv; i < n_layers; ++i)
+    if (layers[i].kind != RALPB_FC) return fail("only FC layers may follow the first FC layer");
+  if (strategy == RALPB_STRATEGY_RALP && split != nconv)
+    return fail("this executor places exactly the FC tail on the PS (split must be " + std::to_string(nconv) + ")");
+  m->split = nconv;
+  m->holds_back = strategy == RALPB_STRATEGY_BASELINE || rank == ps_rank;
+  m->rows_back = strategy == RALPB_STRATEGY_RALP ? world * batch : batch;
+
+  // ---- front geometry
+  const ralpb_layer_desc& l0 = layers[0];
+  if (l0.kind != RALPB_CONV) return fail("first layer must be a convolution");
+  m->in_h = l0.h; m->in_w = l0.w; m->in_c = l0.cin;
+  m->in_cp = static_cast<int>(align_up(l0.cin, 16));
+  ActBuf a0;
+  a0.n = batch; a0.h = l0.h; a0.w = l0.w; a0.c = m->in_cp; a0.pad = l0.pad;
+  m->acts.push_back(a0);
+  long long off = 0;
+  for (int i = 0; i < nconv; ++i) {
+    const ralpb_layer_desc& d = layers[i];
+    const ActBuf& in = m->acts.back();
+    ActBuf o;
+    o.n = batch;
+    FrontLayer f;
+    f.kind = d.kind;
+    if (d.h != in.h || d.w != in.w) return fail("layer " + std::to_string(i) + ": input shape mismatch");
+    if (d.kind == RALPB_CONV) {
+      if (d.stride != 1 || d.k != 2 * d.pad + 1) return fail("conv layer " + std::to_string(i) + ": only stride-1 'same' convolutions are implemented");
+      if (d.pad != in.pad) return fail("conv layer " + std::to_string(i) + ": padding differs from its input buffer");
+      if (!d.relu) return fail("conv layers must be followed by ReLU");
+      if (d.cout % 16 != 0) return fail("conv output channels must be a multiple of 16");
+      f.cin_real = d.cin;
+      f.g = ConvGeom{batch, d.h, d.w, in.c, d.cout, d.k, d.pad};
+      f.relu = 1;
+      f.w_count = static_cast<long long>(d.cout) * d.k * d.k * in.c;
+      f.w_off = off;
+      off = align_up(off + f.w_count, 4);
+      f.b_off = off;
+      off = align_up(off + d.cout, 4);
+      m->real_front += static_cast<long long>(d.cout) * d.k * d.k * d.cin + d.cout;
+      o.h = d.h; o.w = d.w; o.c = d.cout; o.pad = d.pad;
+    } else if (d.kind == RALPB_POOL) {
+      f.k = d.k;
+      f.stride = d.stride > 0 ? d.stride : d.k;
+      o.h = (d.h - f.k) / f.stride + 1;
+      o.w = (d.w - f.k) / f.stride + 1;
+      o.c = in.c;
+      o.pad = (i + 1 < nconv && layers[i + 1].kind == RALPB_CONV) ? layers[i + 1].pad : 0;
+      if (in.c % 8 != 0) return fail("pool channels must be a multiple of 8");
+    } else {
+      return fail("unsupported front layer kind");
+    }
+    m->front.push_back(f);
+    m->acts.push_back(o);
+  }
+  const ActBuf& cut = m->acts.back();
+  if (cut.pad != 0) return fail("the cut activation must be a pooling output");
+  m->cut_elems = cut.h * cut.w * cut.c;
+  m->n_front = align_up(off, 4LL * world);
+  off = m->n_front;
+  m->real_total = m->real_front;
+  int prev = m->cut_elems;
+  for (int i = nconv; i < n_layers; ++i) {
+    const ralpb_layer_desc& d = layers[i];
+    if (d.cin != prev) return fail("fc layer " + std::to_string(i) + ": input width mismatch");
+    FcLayer f;
+    f.in = d.cin; f.out = d.cout;
+    f.relu = i + 1 < n_layers ? 1 : 0;
+    if ((i + 1 < n_layers) != (d.relu != 0)) return fail("ReLU must follow every FC layer except the last");
+    if (i + 1 < n_layers && d.cout % 8 != 0) return fail("hidden FC widths must be multiples of 8");
+    f.ld_out = static_cast<int>(align_up(d.cout, 8));
+    f.w_off = off;
+    off = align_up(off + static_cast<long long>(d.cout) * d.cin, 4);
+    f.b_off = off;
+    off = align_up(off + d.cout, 4);
+    m->real_total += static_cast<long long>(d.cout) * d.cin + d.cout;
+    m->back.push_back(f);
+    prev = d.cout;
+  }
+  m->n_total = align_up(off, 4LL * world);
+
+  // ---- exchange arena (identical layout on every rank)
+  size_t ao = 0;
+  auto take = [&](size_t bytes) { size_t o2 = ao; ao = align_up(static_cast<long long>(ao + bytes), 256); return o2; };
+  m->arena_off_flags = take(kNumFlags * sizeof(uint32_t));
+  m->arena_off_P = take(m->n_total * sizeof(float));
+  m->arena_off_G = take(m->n_total * sizeof(float));
+  m->arena_off_xfc = take(static_cast<size_t>(m->rows_back) * m->cut_elems * sizeof(bf16));
+  m->arena_off_lab = take(static_cast<size_t>(m->rows_back) * sizeof(int32_t));
+  m->arena_off_dcut = take(static_cast<size_t>(batch) * m->cut_elems * sizeof(bf16));
+  m->arena_bytes = ao;
+  if (cudaMalloc(&m->arena, m->arena_bytes) != cudaSuccess) return fail("cudaMalloc(arena) failed");
+  cudaMemset(m->arena, 0, m->arena_bytes);
+  char* base = static_cast<char*>(m->arena);
+  m->flags = reinterpret_cast<uint32_t*>(base + m->arena_off_flags);
+  m->P = reinterpret_cast<float*>(base + m->arena_off_P);
+  m->G = reinterpret_cast<float*>(base + m->arena_off_G);
+  m->x_fc = reinterpret_cast<bf16*>(base + m->arena_off_xfc);
+  m->labels_all = reinterpret_cast<int32_t*>(base + m->arena_off_lab);
+  m->dcut = reinterpret_cast<bf16*>(base + m->arena_off_dcut);
+  m->peer_base.assign(world, nullptr);
+  m->peer_base[rank] = base;
+
+  // ---- local buffers
+  std::string w2;
+  if (!(m->V = alloc<float>(m, m->n_total, why))) return fail(*why);
+  cudaMemset(m->V, 0, m->n_total * sizeof(float));
+  if (!(m->counters = alloc<uint32_t>(m, kNumCounters, why))) return fail(*why);
+  cudaMemset(m->counters, 0, kNumCounters * sizeof(uint32_t));
+  long long max_act = 0;
+  for (size_t i = 0; i < m->acts.size(); ++i) {
+    if (i + 1 < m->acts.size() || true) {
+      if (!(m->acts[i].ptr = alloc<bf16>(m, m->acts[i].elems(), why))) return fail(*why);
+      if (i > 0) max_act = std::max(max_act, m->acts[i].elems());
+    }
+  }
+  for (int g = 0; g < 2; ++g)
+    if (!(m->gbuf[g] = alloc<bf16>(m, max_act, why))) return fail(*why);
+  for (auto& f : m->front) {
+    if (f.kind != RALPB_CONV) continue;
+    if (!(f.wf = alloc<bf16>(m, f.w_count, why))) return fail(*why);
+    if (!(f.wd = alloc<bf16>(m, f.w_count, why))) return fail(*why);
+  }
+  const int R = m->rows_back;
+  for (size_t j = 0; j < m->back.size(); ++j) {
+    auto& f = m->back[j];
+    if (!(f.wbf = alloc<bf16>(m, static_cast<size_t>(f.out) * f.in, why))) return fail(*why);
+    if (j + 1 < m->back.size()) {
+      bf16* h = alloc<bf16>(m, static_cast<size_t>(R) * f.ld_out, why);
+      if (!h) return fail(*why);
+      m->hid.push_back(h);
+    }
+  }
+  int widest = m->cut_elems;
+  for (auto& f : m->back) widest = std::max(widest, f.ld_out);
+  const FcLayer& last = m->back.back();
+  if (!(m->logits = alloc<float>(m, static_cast<size_t>(R) * last.ld_out, why))) return fail(*why);
+  if (!(m->dlogits = alloc<bf16>(m, static_cast<size_t>(R) * last.ld_out, why))) return fail(*why);
+  cudaMemset(m->dlogits, 0, static_cast<size_t>(R) * last.ld_out * sizeof(bf16));
+  for (int g = 0; g < 2; ++g)
+    if (!(m->dh[g] = alloc<bf16>(m, static_cast<size_t>(R) * widest, why))) return fail(*why);
+  if (!(m->dx_fc = alloc<bf16>(m, static_cast<size_t>(R) * m->cut_elems, why))) return fail(*why);
+  if (!(m->row_loss = alloc<float>(m, R, why))) return fail(*why);
+  if (!(m->loss = alloc<float>(m, 4, why))) return fail(*why);
+  if (!(m->img_dev = alloc<float>(m, static_cast<size_t>(batch) * m->in_h * m->in_w * m->in_c, why))) return fail(*why);
+  if (!(m->lab_dev = alloc<int32_t>(m, batch, why))) return fail(*why);
+  if (cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
+  for (auto& e : m->ev) cudaEventCreate(&e);
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail("device error during model creation");
+  *out = m;
+  return 0;
+}
+
+void model_destroy(Model* m) {
+  if (!m) return;
+  cudaDeviceSynchronize();
+  for (int r = 0; r < static_cast<int>(m->peer_base.size()); ++r)
+    if (r != m->rank && m->peer_base[r] != nullptr) cudaIpcCloseMemHandle(m->peer_base[r]);
+  for (void* p : m->owned) cudaFree(p);
+  if (m->arena) cudaFree(m->arena);
+  for (auto& e : m->ev)
+    if (e) cudaEventDestroy(e);
+  if (m->stream) cudaStreamDestroy(m->stream);
+  delete m;
+}
+
+int model_ipc_handle(Model* m, void* out, std::string* why) {
+  cudaIpcMemHandle_t h;
+  RALPB_TRY(cudaIpcGetMemHandle(&h, m->arena));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  std::memcpy(out, &h, 64);
+  return 0;
+}
+
+int model_ipc_open(Model* m, const void* handles, std::string* why) {
+  const char* hs = static_cast<const char*>(handles);
+  for (int r = 0; r < m->world; ++r) {
+    if (r == m->rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hs + 64 * r, 64);
+    void* p = nullptr;
+    RALPB_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    m->peer_base[r] = static_cast<char*>(p);
+  }
+  m->peers_open = true;
+  return 0;
+}
+
+// ------------------------------------------------------------------ parameters
+int model_set_params(Model* m, int layer, const float* w, const float* b, int on_host, std::string* why) {
+  if (layer < 0 || layer >= static_cast<int>(m->desc.size())) { *why = "layer out of range"; return 1; }
+  const auto kind = cudaMemcpyDefault;
+  (void)on_host;
+  if (layer < m->split) {
+    FrontLayer& f = m->front[layer];
+    if (f.kind != RALPB_CONV) { *why = "layer has no parameters"; return 1; }
+    const int co = f.g.cout, taps = f.g.taps(), cp = f.g.cin, cr = f.cin_real;
+    if (cp == cr) {
+      RALPB_TRY(cudaMemcpyAsync(m->P + f.w_off, w, f.w_count * sizeof(float), kind, m->stream));
+    } else {
+      // pad input channels cr -> cp with zeros (host staging)
+      std::vector<float> host(static_cast<size_t>(co) * taps * cr), padded(f.w_count, 0.f);
+      RALPB_TRY(cudaMemcpy(host.data(), w, host.size() * sizeof(float), kind));
+      for (int o = 0; o < co; ++o)
+        for (int t = 0; t < taps; ++t)
+          for (int c = 0; c < cr; ++c)
+            padded[(static_cast<size_t>(o) * taps + t) * cp + c] = host[(static_cast<size_t>(o) * taps + t) * cr + c];
+      RALPB_TRY(cudaMemcpy(m->P + f.w_off, padded.data(), padded.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    RALPB_TRY(cudaMemcpyAsync(m->P + f.b_off, b, co * sizeof(float), kind, m->stream));
+    RALPB_TRY(conv_weight_prep(m->P + f.w_off, co, taps, cp, f.wf, f.wd, m->stream));
+  } else {
+    FcLayer& f = m->back[layer - m->split];
+    RALPB_TRY(cudaMemcpyAsync(m->P + f.w_off, w, static_cast<size_t>(f.out) * f.in * sizeof(float), kind, m->stream));
+    RALPB_TRY(cudaMemcpyAsync(m->P + f.b_off, b, f.out * sizeof(float), kind, m->stream));
+    RALPB_TRY(cast_bf16(m->P + f.w_off, static_cast<long long>(f.out) * f.in, f.wbf, m->stream));
+  }
+  RALPB_TRY(cudaStreamSynchronize(m->stream));
+  return 0;
+}
+
+int model_get_params(Model* m, int layer, float* w, float* b, int on_host, std::string* why) {
+  if (layer < 0 || layer >= static_cast<int>(m->desc.size())) { *why = "layer out of range"; return 1; }
+  (void)on_host;
+  RALPB_TRY(cudaStreamSynchronize(m->stream));
+  if (layer < m->split) {
+    FrontLayer& f = m->front[layer];
+    if (f.kind != RALPB_CONV) { *why = "layer has no parameters"; return 1; }
+    const int co = f.g.cout, taps = f.g.taps(), cp = f.g.cin, cr = f.cin_real;
+    std::vector<float> padded(f.w_count);
+    RALPB_TRY(cudaMemcpy(padded.data(), m->P + f.w_off, padded.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    std::vector<float> host(static_cast<size_t>(co) * taps * cr);
+    for (int o = 0; o < co; ++o)
+      for (int t = 0; t < taps; ++t)
+        for (int c = 0; c < cr; ++c)
+          host[(static_cast<size_t>(o) * taps + t) * cr + c] = padded[(static_cast<size_t>(o) * taps + t) * cp + c];
+    RALPB_TRY(cudaMemcpy(w, host.data(), host.size() * sizeof(float), cudaMemcpyDefault));
+    RALPB_TRY(cudaMemcpy(b, m->P + f.b_off, co * sizeof(float), cudaMemcpyDefault));
+  } else {
+    FcLayer& f = m->back[layer - m->split];
+    RALPB_TRY(cudaMemcpy(w, m->P + f.w_off, static_cast<size_t>(f.out) * f.in * sizeof(float), cudaMemcpyDefault));
+    RALPB_TRY(cudaMemcpy(b, m->P + f.b_off, f.out * sizeof(float), cudaMemcpyDefault));
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------ step
+namespace {
+
+int launch_fc_forward(Model* m, const bf16* in, int R, std::string* why) {
+  const bf16* x = in;
+  long long ldx = m->cut_elems;
+  for (size_t j = 0; j < m->back.size(); ++j) {
+    FcLayer& f = m->back[j];
+    GemmDesc d;
+    d.M = R; d.N = f.out; d.K = f.in;
+    d.a = Operand2D{x, R, f.in, ldx};
+    d.b = Operand2D{f.wbf, f.out, f.in, f.in};
+    d.bias = m->P + f.b_off;
+    if (j + 1 < m->back.size()) {
+      d.epi = EPI_BF16; d.relu = 1; d.out = m->hid[j]; d.s_m = f.ld_out;
+    } else {
+      d.epi = EPI_F32; d.relu = 0; d.out = m->logits; d.s_m = f.ld_out;
+    }
+    RALPB_TRY(gemm_launch(d, m->stream, why));
+    ++m->launches;
+    x = j + 1 < m->back.size() ? m->hid[j] : nullptr;
+    ldx = f.ld_out;
+  }
+  return 0;
+}
+
+// FC backward from dlogits; writes the cut gradient for all R rows into dx_out.
+int launch_fc_backward(Model* m, const bf16* in, int R, bf16* dx_out, std::string* why) {
+  const int nb = static_cast<int>(m->back.size());
+  const bf16* dy = m->dlogits;
+  long long lddy = m->back.back().ld_out;
+  int ping = 0;
+  for (int j = nb - 1; j >= 0; --j) {
+    FcLayer& f = m->back[j];
+    const bf16* x = j == 0 ? in : m->hid[j - 1];
+    const long long ldx = j == 0 ? m->cut_elems : m->back[j - 1].ld_out;
+    // wgrad: G_w[out][in] = dy^T x
+    GemmDesc w;
+    w.M = f.out; w.N = f.in; w.K = R;
+    w.a_mode = LD_MN; w.a = Operand2D{dy, R, f.out, lddy};
+    w.b_mode = LD_MN; w.b = Operand2D{x, R, f.in, ldx};
+    w.epi = EPI_F32; w.out = m->G + f.w_off; w.s_m = f.in; w.s_n = 1;
+    RALPB_TRY(gemm_launch(w, m->stream, why));
+    ++m->launches;
+    // bias grad
+    RALPB_TRY(cudaMemsetAsync(m->G + f.b_off, 0, f.out * sizeof(float), m->stream));
+    RALPB_TRY(colsum_bf16(dy, R, f.out, lddy, m->G + f.b_off, m->stream));
+    ++m->launches;
+    // dgrad: dx[R][in] = dy[R][out] . W[out][in]   (ReLU mask of the previous hidden layer)
+    bf16* dst = j == 0 ? dx_out : m->dh[ping];
+    const long long ld_dst = j == 0 ? m->cut_elems : m->back[j - 1].ld_out;
+    GemmDesc d;
+    d.M = R; d.N = f.in; d.K = f.out;
+    d.a_mode = LD_K; d.a = Operand2D{dy, R, f.out, lddy};
+    d.b_mode = LD_MN; d.b = Operand2D{f.wbf, f.out, f.in, f.in};
+    d.epi = EPI_BF16; d.out = dst; d.s_m = ld_dst;
+    if (j > 0 && m->back[j - 1].relu) { d.mask = m->hid[j - 1]; d.mask_s = ldx; }
+    RALPB_TRY(gemm_launch(d, m->stream, why));
+    ++m->launches;
+    dy = dst;
+    lddy = ld_dst;
+    ping ^= 1;
+  }
+  return 0;
+}
+
+int launch_front_backward(Model* m, const bf16* dcut, std::string* why) {
+  const bf16* cur = dcut;
+  int ping = 0;
+  for (int i = static_cast<int>(m->front.size()) - 1; i >= 0; --i) {
+    FrontLayer& f = m->front[i];
+    const ActBuf& in = m->acts[i];
+    const ActBuf& out = m->acts[i + 1];
+    if (f.kind == RALPB_POOL) {
+      bf16* dst = m->gbuf[ping];
+      RALPB_TRY(maxpool_bwd(in.ptr, cur, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.pad, dst, m->stream));
+      ++m->launches;
+      cur = dst;
+      ping ^= 1;
+    } else {
+      RALPB_TRY(conv_wgrad(f.g, in.ptr, cur, m->G + f.w_off, m->stream, why));
+      RALPB_TRY(colsum_bf16(cur, out.rows(), f.g.cout, f.g.cout, m->G + f.b_off, m->stream));
+      m->launches += 2;
+      if (i > 0) {
+        bf16* dst = m->gbuf[ping];
+        const bool mask = m->front[i - 1].kind == RALPB_CONV;
+        RALPB_TRY(conv_dgrad(f.g, cur, f.wd, mask ? in.ptr : nullptr, dst, m->stream, why));
+        ++m->launches;
+        cur = dst;
+        ping ^= 1;
+      }
+    }
+  }
+  return 0;
+}
+
+int relayout_weights(Model* m, bool fc_too, std::string* why) {
+  for (size_t i = 0; i < m->front.size(); ++i) {
+    FrontLayer& f = m->front[i];
+    if (f.kind != RALPB_CONV) continue;
+    RALPB_TRY(conv_weight_prep(m->P + f.w_off, f.g.cout, f.g.taps(), f.g.cin, f.wf, i > 0 ? f.wd : nullptr, m->stream));
+    ++m->launches;
+  }
+  if (fc_too) {
+    for (auto& f : m->back) {
+      RALPB_TRY(cast_bf16(m->P + f.w_off, static_cast<long long>(f.out) * f.in, f.wbf, m->stream));
+      ++m->launches;
+    }
+  }
+  return 0;
+}
+
+// Sharded-PS synchronisation of params[0, n) over all ranks.
+int sync_params(Model* m, long long n, float lr, float mu, std::string* why) {
+  if (m->world == 1) {
+    RALPB_TRY(sgd_momentum(m->P, m->V, m->G, n, lr, mu, 1.f, m->stream));
+    ++m->launches;
+    return 0;
+  }
+  const uint32_t seq = m->seq;
+  PeerSignal all_grad{}, all_done{};
+  all_grad.n = all_done.n = m->world;
+  for (int r = 0; r < m->world; ++r) {
+    uint32_t* fl = at<uint32_t>(m, r, m->arena_off_flags);
+    all_grad.flag[r] = fl + kFlagGrad + m->rank;
+    all_done.flag[r] = fl + kFlagDone + m->rank;
+  }
+  RALPB_TRY(signal_only(all_grad, seq, m->stream));
+  RALPB_TRY(wait_flags(m->flags + kFlagGrad, m->world, seq, m->stream));
+  ShardUpdate u{};
+  u.nranks = m->world;
+  u.self = m->rank;
+  const long long shard = n / m->world;  // n is a multiple of 4*world
+  u.begin = shard * m->rank;
+  u.end = u.begin + shard;
+  u.lr = lr; u.mu = mu; u.gscale = 1.f;
+  u.momentum = m->V;
+  for (int r = 0; r < m->world; ++r) {
+    u.grads[r] = at<float>(m, r, m->arena_off_G);
+    u.params[r] = at<float>(m, r, m->arena_off_P);
+  }
+  RALPB_TRY(shard_update(u, all_done, seq, m->counters + 0, m->stream));
+  RALPB_TRY(wait_flags(m->flags + kFlagDone, m->world, seq, m->stream));
+  m->launches += 4;
+  m->phys_bytes += 2LL * (m->world - 1) * shard * static_cast<long long>(sizeof(float));
+  return 0;
+}
+
+}  // namespace
+
+int model_step(Model* m, const void* images, const int32_t* labels, int on_host, float lr, float mu,
+               std::string* why) {
+  if (m->world > 1 && !m->peers_open) { *why = "ralpb_model_ipc_open has not been called"; return 1; }
+  m->seq += 1;
+  m->launches = 0;
+  m->phys_bytes = 0;
+  const uint32_t seq = m->seq;
+  const int b = m->batch;
+  const bool ralp = m->strategy == RALPB_STRATEGY_RALP;
+  cudaStream_t s = m->stream;
+  RALPB_TRY(cudaEventRecord(m->ev[0], s));
+
+  // ---------------- worker front forward
+  const float* img = static_cast<const float*>(images);
+  const int32_t* lab = labels;
+  if (on_host) {
+    RALPB_TRY(cudaMemcpyAsync(m->img_dev, images, sizeof(float) * b * m->in_h * m->in_w * m->in_c, cudaMemcpyHostToDevice, s));
+    RALPB_TRY(cudaMemcpyAsync(m->lab_dev, labels, sizeof(int32_t) * b, cudaMemcpyHostToDevice, s));
+    img = m->img_dev;
+    lab = m->lab_dev;
+  }
+  RALPB_TRY(pack_input(img, b, m->in_h, m->in_w, m->in_c, m->acts[0].ptr, m->in_cp, m->acts[0].pad, s));
+  ++m->launches;
+  const int slot = ralp ? m->rank : 0;          // this worker's row block in the PS input
+  bf16* cut_dst = m->acts.back().ptr;
+  if (m->holds_back) cut_dst = m->x_fc + static_cast<size_t>(slot) * b * m->cut_elems;
+  for (size_t i = 0; i < m->front.size(); ++i) {
+    FrontLayer& f = m->front[i];
+    const ActBuf& in = m->acts[i];
+    ActBuf out = m->acts[i + 1];
+    if (i + 1 == m->front.size()) out.ptr = cut_dst;
+    if (f.kind == RALPB_CONV) {
+      RALPB_TRY(conv_fwd(f.g, in.ptr, f.wf, m->P + f.b_off, out.ptr, 1, s, why));
+    } else {
+      RALPB_TRY(maxpool_fwd(in.ptr, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.ptr, out.pad, s));
+    }
+    ++m->launches;
+  }
+  const bf16* cut_local = cut_dst;
+  RALPB_TRY(cudaEventRecord(m->ev[1], s));
+
+  // ---------------- cut exchange + PS back segment
+  const size_t cut_bytes = static_cast<size_t>(b) * m->cut_elems * sizeof(bf16);
+  const bf16* dcut = nullptr;
+  if (m->holds_back) {
+    RALPB_TRY(cudaMemcpyAsync(m->labels_all + static_cast<size_t>(slot) * b, lab, sizeof(int32_t) * b, cudaMemcpyDeviceToDevice, s));
+    if (ralp && m->world > 1) {
+      PeerSignal own{};
+      own.n = 1;
+      own.flag[0] = m->flags + kFlagAct + m->rank;
+      RALPB_TRY(signal_only(own, seq, s));
+      RALPB_TRY(wait_flags(m->flags + kFlagAct, m->world, seq, s));
+      m->launches += 2;
+    }
+  } else {
+    // push labels then the cut into the PS rank's rows, raise act_ready[rank] there
+    int32_t* lab_ps = at<int32_t>(m, m->ps_rank, m->arena_off_lab) + static_cast<size_t>(slot) * b;
+    bf16* x_ps = at<bf16>(m, m->ps_rank, m->arena_off_xfc) + static_cast<size_t>(slot) * b * m->cut_elems;
+    PeerSignal none{};
+    RALPB_TRY(push_and_signal(lab_ps, lab, static_cast<long long>(b) * 4 / 16, none, 0, m->counters + 1, s));
+    PeerSignal sig{};
+    sig.n = 1;
+    sig.flag[0] = at<uint32_t>(m, m->ps_rank, m->arena_off_flags) + kFlagAct + m->rank;
+    RALPB_TRY(push_and_signal(x_ps, cut_local, static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + 2, s));
+    m->launches += 2;
+    m->phys_bytes += cut_bytes + sizeof(int32_t) * b;
+  }
+  if (m->holds_back) {
+    const int R = m->rows_back;
+    const bf16* in = m->x_fc;
+    if (launch_fc_forward(m, in, R, why)) return 1;
+    const FcLayer& last = m->back.back();
+    const float scale = 1.f / static_cast<float>(m->world * b);
+    RALPB_TRY(softmax_xent(m->logits, R, last.out, last.ld_out, m->labels_all, scale, m->row_loss, m->dlogits, last.ld_out, s));
+    RALPB_TRY(reduce_sum(m->row_loss, R, 1.f / static_cast<float>(R), m->loss, s));
+    m->launches += 2;
+    if (launch_fc_backward(m, in, R, m->dx_fc, why)) return 1;
+    if (ralp) {
+      // FC tail update stays on the PS (never synchronised)
+      const long long nb = m->n_total - m->n_front;
+      RALPB_TRY(sgd_momentum(m->P + m->n_front, m->V + m->n_front, m->G + m->n_front, nb, lr, mu, 1.f, s));
+      ++m->launches;
+      for (auto& f : m->back) {
+        RALPB_TRY(cast_bf16(m->P + f.w_off, static_cast<long long>(f.out) * f.in, f.wbf, s));
+        ++m->launches;
+      }
+      // return every remote worker's rows of the cut gradient
+      for (int r = 0; r < m->world; ++r) {
+        if (r == m->rank) continue;
+        PeerSignal sig{};
+        sig.n = 1;
+        sig.flag[0] = at<uint32_t>(m, r, m->arena_off_flags) + kFlagActGrad;
+        RALPB_TRY(push_and_signal(at<bf16>(m, r, m->arena_off_dcut), m->dx_fc + static_cast<size_t>(r) * b * m->cut_elems,
+                                  static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + 8 + r, s));
+        ++m->launches;
+        m->phys_bytes += cut_bytes;
+      }
+    }
+    dcut = m->dx_fc + static_cast<size_t>(slot) * b * m->cut_elems;
+  } else {
+    RALPB_TRY(wait_flags(m->flags + kFlagActGrad, 1, seq, s));
+    ++m->launches;
+    dcut = m->dcut;
+  }
+  RALPB_TRY(cudaEventRecord(m->ev[2], s));
+
+  // ---------------- worker front backward
+  RALPB_TRY(cudaMemsetAsync(m->G, 0, m->n_front * sizeof(float), s));
+  if (launch_front_backward(m, dcut, why)) return 1;
+  RALPB_TRY(cudaEventRecord(m->ev[3], s));
+
+  // ---------------- parameter synchronisation + re-layout
+  if (sync_params(m, ralp ? m->n_front : m->n_total, lr, mu, why)) return 1;
+  if (relayout_weights(m, !ralp, why)) return 1;
+  RALPB_TRY(cudaEventRecord(m->ev[4], s));
+  m->stats_valid = true;
+  return 0;
+}
+
+int model_stats(Model* m, ralpb_step_stats* st, std::string* why) {
+  RALPB_TRY(cudaStreamSynchronize(m->stream));
+  std::memset(st, 0, sizeof(*st));
+  if (!m->stats_valid) { *why = "no step has run"; return 1; }
+  const bool ralp = m->strategy == RALPB_STRATEGY_RALP;
+  float loss = NAN;
+  if (m->holds_back) RALPB_TRY(cudaMemcpy(&loss, m->loss, sizeof(float), cudaMemcpyDeviceToHost));
+  st->loss = loss;
+  const long long eb = m->elem_bytes;
+  if (ralp)
+    st->logical_bytes = static_cast<long long>(m->world) * 2 * (static_cast<long long>(m->batch) * m->cut_elems * eb + m->real_front * eb);
+  else
+    st->logical_bytes = static_cast<long long>(m->world) * 2 * m->real_total * eb;
+  st->physical_bytes = m->phys_bytes;
+  st->launches = m->launches;
+  cudaEventElapsedTime(&st->ms_step, m->ev[0], m->ev[4]);
+  cudaEventElapsedTime(&st->ms_front_fwd, m->ev[0], m->ev[1]);
+  cudaEventElapsedTime(&st->ms_back, m->ev[1], m->ev[2]);
+  cudaEventElapsedTime(&st->ms_front_bwd, m->ev[2], m->ev[3]);
+  cudaEventElapsedTime(&st->ms_sync, m->ev[3], m->ev[4]);
+  return 0;
+}
+
+}  // namespace ralpb

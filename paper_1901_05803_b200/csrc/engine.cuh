@@ -1,0 +1,106 @@
+// Native executor of one job's training step under a placement strategy.
+// See engine.cu for the schedule; the C ABI (ralpb_model_*) is in api_engine.cu.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <string>
+#include <vector>
+#include "../../include/ralpb.h"
+#include "conv.cuh"
+#include "exchange.cuh"
+
+namespace ralpb {
+
+using bf16 = __nv_bfloat16;
+
+struct ActBuf {
+  bf16* ptr = nullptr;
+  int n = 0, h = 0, w = 0, c = 0, pad = 0;
+  long long rows() const { return static_cast<long long>(n) * (h + 2 * pad) * (w + 2 * pad); }
+  long long elems() const { return rows() * c; }
+};
+
+struct FrontLayer {
+  int kind = 0;                // RALPB_CONV / RALPB_POOL
+  ConvGeom g{};                // conv geometry (cin padded to 16)
+  int cin_real = 0;
+  int k = 0, stride = 0;       // pool window
+  int relu = 1;
+  long long w_off = 0, b_off = 0;  // offsets (floats) into the flat parameter vector
+  long long w_count = 0;           // cout*k*k*cin_pad
+  bf16* wf = nullptr;          // forward filter [cout][k*k][cin]
+  bf16* wd = nullptr;          // backward-data filter [cin][k*k][cout]
+};
+
+struct FcLayer {
+  int in = 0, out = 0, relu = 1;
+  int ld_out = 0;                  // padded row stride (elements) of this layer's output
+  long long w_off = 0, b_off = 0;
+  bf16* wbf = nullptr;             // [out][in]
+};
+
+struct Model {
+  // configuration
+  int rank = 0, world = 1, ps_rank = 0, device = 0;
+  int batch = 0, split = 0, strategy = RALPB_STRATEGY_RALP, elem_bytes = 4;
+  std::vector<ralpb_layer_desc> desc;
+  std::vector<FrontLayer> front;
+  std::vector<FcLayer> back;
+  std::vector<ActBuf> acts;        // acts[i] = input of front layer i; acts.back() = cut (local)
+  int in_h = 0, in_w = 0, in_c = 0, in_cp = 0;
+  int cut_elems = 0;               // per-sample elements of the cut activation
+  int rows_back = 0;               // rows the back segment processes on this rank
+  bool holds_back = false;         // this rank runs the FC tail
+  long long n_front = 0, n_total = 0;  // floats in the flat parameter vector (front prefix, total)
+  long long real_front = 0, real_total = 0;  // logical parameter counts (unpadded)
+
+  // device memory
+  cudaStream_t stream = nullptr;
+  void* arena = nullptr;           // IPC-exported allocation
+  size_t arena_bytes = 0;
+  std::vector<void*> owned;        // other allocations
+  uint32_t* flags = nullptr;       // in arena
+  uint32_t* counters = nullptr;    // local
+  float* P = nullptr;              // params (arena)
+  float* G = nullptr;              // grads (arena)
+  float* V = nullptr;              // momentum (local)
+  bf16* x_fc = nullptr;            // back-segment input [rows_back][cut_elems] (arena, PS)
+  int32_t* labels_all = nullptr;   // [rows_back] (arena, PS)
+  bf16* dcut = nullptr;            // cut gradient received from the PS [batch][cut_elems] (arena)
+  bf16* dx_fc = nullptr;           // back-segment cut gradient [rows_back][cut_elems] (PS)
+  std::vector<bf16*> hid;          // FC outputs (bf16) for hidden layers
+  float* logits = nullptr;
+  bf16* dlogits = nullptr;
+  bf16* dh[2] = {nullptr, nullptr};  // FC backward ping-pong
+  float* row_loss = nullptr;
+  float* loss = nullptr;
+  bf16* gbuf[2] = {nullptr, nullptr};  // conv backward ping-pong (max activation size)
+  float* img_dev = nullptr;        // staging for host images
+  int32_t* lab_dev = nullptr;      // staging for host labels
+  size_t arena_off_flags = 0, arena_off_P = 0, arena_off_G = 0, arena_off_xfc = 0, arena_off_lab = 0,
+         arena_off_dcut = 0;
+
+  // peers (IPC-mapped base pointers of every rank's arena; self = arena)
+  std::vector<char*> peer_base;
+  bool peers_open = false;
+
+  // step state
+  uint32_t seq = 0;
+  int launches = 0;
+  long long phys_bytes = 0;
+  cudaEvent_t ev[6] = {};
+  bool stats_valid = false;
+};
+
+int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int batch, int strategy,
+                 int rank, int world, int ps_rank, int elem_bytes, Model** out, std::string* why);
+void model_destroy(Model* m);
+int model_step(Model* m, const void* images, const int32_t* labels, int on_host, float lr, float mu,
+               std::string* why);
+int model_stats(Model* m, ralpb_step_stats* st, std::string* why);
+int model_set_params(Model* m, int layer, const float* w, const float* b, int on_host, std::string* why);
+int model_get_params(Model* m, int layer, float* w, float* b, int on_host, std::string* why);
+int model_ipc_handle(Model* m, void* out, std::string* why);
+int model_ipc_open(Model* m, const void* handles, std::string* why);
+
+}  // namespace ralpb

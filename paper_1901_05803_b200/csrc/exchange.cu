@@ -1,0 +1,110 @@
+#include <algorithm>
+#include "exchange.cuh"
+#include "gemm_host.cuh"
+
+namespace ralpb {
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Last CTA to finish sets the flags.
+__device__ __forceinline__ void finish_and_signal(const PeerSignal& sig, uint32_t value,
+                                                  uint32_t* counter) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t prev = atomicAdd(counter, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence_system();
+      for (int i = 0; i < sig.n; ++i)
+        if (sig.flag[i] != nullptr) st_release_sys(sig.flag[i], value);
+      *counter = 0;  // re-arm (only this CTA touches it now)
+    }
+  }
+}
+
+__global__ void push_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, long long n16,
+                            PeerSignal sig, uint32_t value, uint32_t* counter) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  // 4 independent 16-byte loads in flight per thread
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    uint4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
+    dst[i] = a;
+    dst[i + stride] = b;
+    dst[i + 2 * stride] = c;
+    dst[i + 3 * stride] = d;
+  }
+  for (; i < n16; i += stride) dst[i] = src[i];
+  finish_and_signal(sig, value, counter);
+}
+
+cudaError_t push_and_signal(void* dst, const void* src, long long n16, const PeerSignal& sig,
+                            uint32_t value, uint32_t* counter, cudaStream_t s) {
+  int grid = static_cast<int>(std::max<long long>(1, std::min<long long>((n16 + 511) / 512, num_sms() * 2)));
+  push_kernel<<<grid, 512, 0, s>>>(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), n16,
+                                   sig, value, counter);
+  return cudaGetLastError();
+}
+
+__global__ void signal_kernel(PeerSignal sig, uint32_t value) {
+  __threadfence_system();
+  if (threadIdx.x < sig.n && sig.flag[threadIdx.x] != nullptr) st_release_sys(sig.flag[threadIdx.x], value);
+}
+
+cudaError_t signal_only(const PeerSignal& sig, uint32_t value, cudaStream_t s) {
+  signal_kernel<<<1, 32, 0, s>>>(sig, value);
+  return cudaGetLastError();
+}
+
+__global__ void wait_kernel(const uint32_t* flags, int n, uint32_t value) {
+  if (threadIdx.x < n) {
+    while (ld_acquire_sys(flags + threadIdx.x) < value) {
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+cudaError_t wait_flags(const uint32_t* flags, int n, uint32_t value, cudaStream_t s) {
+  wait_kernel<<<1, 32, 0, s>>>(flags, n, value);
+  return cudaGetLastError();
+}
+
+__global__ void shard_update_kernel(ShardUpdate u, PeerSignal done, uint32_t value, uint32_t* counter) {
+  const long long b4 = u.begin / 4, e4 = u.end / 4;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = b4 + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < e4; i += stride) {
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r = 0; r < u.nranks; ++r) {
+      float4 x = reinterpret_cast<const float4*>(u.grads[r])[i];
+      g.x += x.x; g.y += x.y; g.z += x.z; g.w += x.w;
+    }
+    float4 v = reinterpret_cast<float4*>(u.momentum)[i];
+    float4 p = reinterpret_cast<const float4*>(u.params[u.self])[i];
+    v.x = u.mu * v.x + u.gscale * g.x; p.x -= u.lr * v.x;
+    v.y = u.mu * v.y + u.gscale * g.y; p.y -= u.lr * v.y;
+    v.z = u.mu * v.z + u.gscale * g.z; p.z -= u.lr * v.z;
+    v.w = u.mu * v.w + u.gscale * g.w; p.w -= u.lr * v.w;
+    reinterpret_cast<float4*>(u.momentum)[i] = v;
+    for (int r = 0; r < u.nranks; ++r) reinterpret_cast<float4*>(u.params[r])[i] = p;
+  }
+  finish_and_signal(done, value, counter);
+}
+
+cudaError_t shard_update(const ShardUpdate& u, const PeerSignal& done, uint32_t value,
+                         uint32_t* counter, cudaStream_t s) {
+  long long n4 = (u.end - u.begin) / 4;
+  int grid = static_cast<int>(std::max<long long>(1, std::min<long long>((n4 + 255) / 256, num_sms() * 4)));
+  shard_update_kernel<<<grid, 256, 0, s>>>(u, done, value, counter);
+  return cudaGetLastError();
+}
+
+}  // namespace ralpb

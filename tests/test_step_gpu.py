@@ -1,0 +1,128 @@
+"""Full training-step parity: the B200 executor (through the C ABI) against the CPU
+oracle restatement (oracle/step.py) on identical seeds, synthetic inputs and
+initial parameters.
+
+The split point and the per-step synchronised bytes must match exactly.
+
+Numerics.  Both sides use bf16 operands with fp32 accumulation and the oracle
+rounds to bf16 at exactly the points the GPU stores bf16.  The bf16 pipeline is
+chaotic under summation-order noise (a 1-ulp re-rounding flips a ReLU/max-pool
+decision and re-routes a gradient), so the tolerance is stated against the
+pipeline's own noise floor, measured every time by re-running the oracle with
+float64 accumulation:
+  floor(layer) = ||p_oracle64 - p_oracle32|| / ||p_oracle32 - p_init||
+  dev(layer)   = ||p_gpu      - p_oracle32|| / ||p_oracle32 - p_init||
+  require dev <= 4 * floor + 0.02 for every parameter tensor after N steps,
+  and |loss_gpu - loss_oracle| <= 2e-3 * |loss_oracle| at every step.
+(The B200's tensor-core fp32 accumulation truncates per MMA, so its noise is
+larger than CPU fp32's; the factor 4 covers that, and a real bug shows up as
+dev ~ O(1).)
+"""
+import numpy as np
+import pytest
+
+from oracle import step as ostep
+from paper_1901_05803_b200 import synthetic
+from paper_1901_05803_b200.executor import RankExecutor
+from paper_1901_05803_b200.planner import (JobSpec, Strategy, catalog_lookup, parse_model, profile,
+                                           volume_baseline, volume_ralp)
+
+pytestmark = pytest.mark.gpu
+
+VGG_TINY = """
+model vgg_tiny batch=8 elem_bytes=4 input=32x32x3
+conv1 conv k=3 cout=64 pad=1
+conv2 conv k=3 cout=64 pad=1
+pool1 pool window=2
+conv3 conv k=3 cout=128 pad=1
+conv4 conv k=3 cout=128 pad=1
+pool2 pool window=2
+conv5 conv k=3 cout=256 pad=1
+conv6 conv k=3 cout=256 pad=1
+pool3 pool window=2
+conv7 conv k=3 cout=512 pad=1
+pool4 pool window=2
+fc1 fc out=1024
+fc2 fc out=1024
+fc3 fc out=100
+"""
+
+LOSS_RTOL = 2e-3
+
+
+def _fc_boundary(model):
+    return next(i for i, l in enumerate(model.layers) if l.kind.value == "fc")
+
+
+def _run(model, strategy, steps, seed=0):
+    if strategy == "ralp":
+        split = _fc_boundary(model)  # the FC-tail cut (the partitioner's choice at large batch)
+        job = JobSpec(model, Strategy.ralp(split), 1)
+        expect_bytes = volume_ralp(model, split, 1).total_bytes_per_step
+    else:
+        job = JobSpec(model, Strategy.baseline(), 1)
+        expect_bytes = volume_baseline(model, 1).total_bytes_per_step
+    ex = RankExecutor(job)
+    params = synthetic.init_params(ex.layers, seed)
+    ex.set_params(params)
+    o32 = ostep.OracleState(ex.layers, params)
+    o64 = ostep.OracleState(ex.layers, params)
+    b = model.batch_size
+    losses = []
+    for t in range(steps):
+        imgs, labs = synthetic.batch(seed, t, 0, b, ex.in_shape, ex.classes)
+        ex.step(imgs, labs, lr=0.01, momentum=0.9)
+        st = ex.stats()
+        loss_o, wire = ostep.train_step(o32, strategy, 1, [(imgs, labs)], lr=0.01, mu=0.9, emulate_bf16=True)
+        ostep.train_step(o64, strategy, 1, [(imgs, labs)], lr=0.01, mu=0.9, emulate_bf16=True, accum64=True)
+        assert st.logical_bytes == wire == expect_bytes
+        losses.append((st.loss, loss_o))
+    got = ex.get_params()
+    ex.close()
+    return losses, got, o32.numpy_params(), o64.numpy_params(), params
+
+
+def _check(losses, got, want, want64, init):
+    bad = []
+    for i, (lg, lo) in enumerate(losses):
+        print(f"  step {i}: loss gpu {lg:.6f} oracle {lo:.6f}")
+        if abs(lg - lo) > LOSS_RTOL * abs(lo):
+            bad.append(f"step {i}: loss {lg} vs oracle {lo}")
+    for li, (g, w, w64, p0) in enumerate(zip(got, want, want64, init)):
+        if g is None:
+            continue
+        for nm, a, o, o64, c in zip("wb", g, w, w64, p0):
+            upd = np.linalg.norm(o - c)
+            dev = np.linalg.norm(a - o) / upd
+            floor = np.linalg.norm(o64 - o) / upd
+            print(f"  layer {li}.{nm}: dev {dev:.3e} floor {floor:.3e}")
+            if dev > 4 * floor + 0.02:
+                bad.append(f"layer {li}.{nm}: dev {dev:.3e} > 4 * floor {floor:.3e} + 0.02")
+    assert not bad, "\n".join(bad)
+
+
+@pytest.mark.parametrize("strategy", ["ralp", "baseline"])
+def test_cifar_small_steps(strategy):
+    model = catalog_lookup("cifar_small").with_batch_size(64)
+    assert profile(model).split_index == 4
+    losses, got, want, want64, init = _run(model, strategy, steps=5)
+    print("cifar_small", strategy, losses)
+    _check(losses, got, want, want64, init)
+
+
+def test_vgg_tiny_steps():
+    model = parse_model(VGG_TINY)
+    losses, got, want, want64, init = _run(model, "ralp", steps=3)
+    print("vgg_tiny", losses)
+    _check(losses, got, want, want64, init)
+
+
+def test_vgg16_one_step_b4():
+    # the real VGG-16 geometry (224x224), small batch so the CPU oracle stays fast;
+    # at b=4 the partitioner cuts at pool3 (conv layers in the back segment), so the FC-tail
+    # executor is driven with the baseline plan here and the b=128 pool5 split is covered
+    # by the planner golden tests.
+    model = catalog_lookup("vgg16").with_batch_size(4)
+    losses, got, want, want64, init = _run(model, "baseline", steps=1)
+    print("vgg16 b=4", losses)
+    _check(losses, got, want, want64, init)
