@@ -1,0 +1,290 @@
+"""Headline benchmark: layer-placed (RALP) VGG-16 training step on 1/2/4/8 B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1 is launched by the driver with torch.distributed.run (one process per GPU).
+Metric (BASELINE.json): images/sec per step, layer-placed vs all-on-PS, plus the
+synchronised bytes per step.  Workload: VGG-16 224x224 synthetic, b=128 per
+worker, partitioner-chosen split (profile() -> pool5, layer 18), W = N workers,
+PS role on rank 0.  `value` is whole-job images/s with inputs resident in HBM
+(device-timed with CUDA events on the executor's stream, max over ranks);
+`e2e` is the same through the public API with pinned host inputs copied in every
+step and the loss read back every step.  The activation working set (~4.5 GB per
+step per GPU) is far larger than the 126 MB L2, so no L2 flush is inserted.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+MODEL = "vgg16"
+BATCH = 128
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _cpu_baseline_step(sample_b: int, steps: int):
+    """Oracle port (oracle/step.py) of the layer-placed step on the host cores, bounded sample."""
+    import torch
+    from oracle import step as ostep
+    from paper_1901_05803_b200 import synthetic
+    from paper_1901_05803_b200.executor import lower
+    from paper_1901_05803_b200.planner import catalog_lookup
+
+    torch.set_num_threads(os.cpu_count() or 1)
+    m = catalog_lookup(MODEL).with_batch_size(sample_b)
+    layers = lower(m)
+    st = ostep.OracleState(layers, synthetic.init_params(layers, 0))
+    shape = (layers[0]["h"], layers[0]["w"], layers[0]["cin"])
+    batches = [synthetic.batch(0, t, 0, sample_b, shape, layers[-1]["cout"]) for t in range(steps + 1)]
+    ostep.train_step(st, "ralp", 1, [batches[0]])  # warm-up
+    t0 = time.perf_counter()
+    for t in range(steps):
+        ostep.train_step(st, "ralp", 1, [batches[t + 1]])
+    dt = time.perf_counter() - t0
+    return {"value": sample_b * steps / dt, "unit": "images/s", "cores": torch.get_num_threads(), "kind": "port",
+            "sample": f"{MODEL} 224x224 layer-placed step (oracle/step.py, fp32 torch CPU), W=1, b={sample_b}, "
+                      f"{steps} timed steps after 1 warm-up, {dt:.1f} s"}
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    sample_b = 8
+    steps = max(1, min(args.steps, 3))
+    cb = _cpu_baseline_step(sample_b, steps)
+    line = {"impl": "reference", "metric": "images/sec per step (layer-placed VGG-16 step)", "value": cb["value"],
+            "unit": "images/s", "n_gpus": args.gpus, "steps": steps, "warmup": 1,
+            "ms_per_step": 1e3 * sample_b / cb["value"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{MODEL} 224x224 synthetic, layer-placed (RALP) step, CPU oracle port",
+                       "model": MODEL, "per_worker_batch": sample_b, "split": 18},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _build_executor(strategy: str, world: int, rank: int):
+    from paper_1901_05803_b200 import synthetic
+    from paper_1901_05803_b200.executor import RankExecutor
+    from paper_1901_05803_b200.planner import JobSpec, Strategy, catalog_lookup, profile
+
+    m = catalog_lookup(MODEL).with_batch_size(BATCH)
+    rep = profile(m)
+    if strategy == "ralp":
+        job = JobSpec(m, Strategy.ralp(rep.split_index), world)
+    else:
+        job = JobSpec(m, Strategy.baseline(), world)
+    ex = RankExecutor(job, rank=rank, world=world)
+    ex.set_params(synthetic.init_params(ex.layers, 0))
+    return ex, job, rep
+
+
+def _time_steps(ex, imgs, labs, steps, warmup, world, on_host=False, read_loss=False):
+    import torch
+    import torch.distributed as dist
+
+    stream = torch.cuda.ExternalStream(ex.stream)
+    for t in range(warmup):
+        ex.step(imgs[t % len(imgs)], labs[t % len(labs)])
+    ex.stats()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for t in range(steps):
+        ex.step(imgs[t % len(imgs)], labs[t % len(labs)])
+        if read_loss:
+            ex.stats()  # device->host read of the step's loss (synchronises)
+    e.record(stream)
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+        dist.barrier()
+    return ms / steps
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1901_05803_b200.planner import compute_load, volume_ralp
+
+    ex, job, rep = _build_executor("ralp", world, rank)
+    m = job.model
+    shape = ex.in_shape
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    dimgs = [torch.randn(BATCH, *shape, generator=g, device="cuda") for _ in range(2)]
+    dlabs = [torch.randint(0, ex.classes, (BATCH,), generator=g, device="cuda", dtype=torch.int32) for _ in range(2)]
+
+    with ClockSampler(local) as clk:
+        ms = _time_steps(ex, dimgs, dlabs, args.steps, args.warmup, world)
+    st = ex.stats()
+    value = world * BATCH / (ms * 1e-3)
+
+    # end-to-end through the public API: pinned host inputs copied each step, loss read back each step
+    himgs = [x.cpu().pin_memory() for x in dimgs]
+    hlabs = [x.cpu().pin_memory() for x in dlabs]
+    ms_e2e = _time_steps(ex, himgs, hlabs, args.steps, 1, world, on_host=True, read_loss=True)
+    e2e_value = world * BATCH / (ms_e2e * 1e-3)
+    h2d = BATCH * int(np.prod(shape)) * 4 + BATCH * 4
+
+    # roofline of the dominant kernel (the tcgen05 GEMM engine): profiling pass after the timed region
+    ex.set_profiling(True)
+    ex.step(dimgs[0], dlabs[0])
+    prof = ex.stats()
+    ex.set_profiling(False)
+    worker_flops, ps_flops = compute_load(m, rep.split_index, world)
+    flops_rank = worker_flops + (ps_flops if rank == 0 else 0)
+    peaks, peak_src = _peaks()
+    achieved = flops_rank / (prof.ms_gemm * 1e-3) / 1e12 if prof.ms_gemm > 0 else None
+    traffic = None
+    tfile = ROOT / "profiles" / "gemm_traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get("dram_bytes_per_step")
+
+    # all-on-PS comparator (StrategyKind.BASELINE_PS): same workload, every layer on every worker
+    ex.close()
+    torch.cuda.empty_cache()
+    exb, jobb, _ = _build_executor("baseline", world, rank)
+    ms_b = _time_steps(exb, dimgs, dlabs, args.steps, args.warmup, world)
+    stb = exb.stats()
+    exb.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = _cpu_baseline_step(8, 10)
+
+    if rank == 0:
+        line = {
+            "metric": "images/sec per step at 1/2/4/8 B200 (layer-placed vs all-on-PS); sync bytes/step",
+            "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"VGG-16 224x224 synthetic, b={BATCH}/worker, W={world}, partitioner split "
+                                   f"{rep.split_index} ({m.layer(rep.split_index).name}), FC tail on rank 0",
+                       "model": MODEL, "global_batch": world * BATCH, "per_worker_batch": BATCH,
+                       "split": rep.split_index, "parallelism": f"dp{world}+fc-tail-on-ps",
+                       "l2": "activation working set ~4.5 GB/GPU/step >> 126 MB L2; no flush"},
+            "sync_bytes_per_step": {"logical": st.logical_bytes,
+                                    "oracle_volume_ralp": volume_ralp(m, rep.split_index, world).total_bytes_per_step,
+                                    "physical_nvlink_rank0": st.physical_bytes},
+            "all_on_ps": {"value": world * BATCH / (ms_b * 1e-3), "ms_per_step": ms_b,
+                          "logical_sync_bytes_per_step": stb.logical_bytes},
+            "breakdown_ms_rank0": {"front_fwd": st.ms_front_fwd, "back": st.ms_back, "front_bwd": st.ms_front_bwd,
+                                   "sync": st.ms_sync, "gemm_sum": prof.ms_gemm, "gemm_launches": prof.gemm_launches},
+            "roofline": {"bound": "tensor", "kernel": "gemm_sm100_kernel (all conv/FC launches of a step)",
+                         "achieved": achieved, "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                         "frac": achieved / peaks["bf16_tflops_sustained"] if achieved else None,
+                         "peak_source": f"{peak_src} bf16_tflops_sustained", "traffic": traffic,
+                         "algorithmic_flops_per_step_rank0": flops_rank},
+            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4,
+                    "ms_per_step": ms_e2e},
+            "gpu_launches": st.launches * args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

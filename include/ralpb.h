@@ -107,6 +107,8 @@ typedef struct {
   float ms_back;               /* PS back segment incl. waiting for cut activations */
   float ms_front_bwd;          /* worker front backward incl. waiting for the act-grad */
   float ms_sync;               /* parameter synchronisation (sharded PS) + weight re-layout */
+  float ms_gemm;               /* sum of tcgen05 GEMM-engine launch durations (profiling mode only) */
+  int gemm_launches;           /* GEMM-engine launches timed (profiling mode only) */
 } ralpb_step_stats;
 
 typedef struct ralpb_model ralpb_model;
@@ -131,6 +133,8 @@ int ralpb_model_step(ralpb_model* m, const void* images, const int32_t* labels, 
 /* Synchronises the model stream and reports the last step. */
 int ralpb_model_stats(ralpb_model* m, ralpb_step_stats* out);
 void* ralpb_model_stream(ralpb_model* m);
+/* Profiling mode: bracket every GEMM-engine launch with CUDA events (reported in stats). */
+int ralpb_model_set_profiling(ralpb_model* m, int on);
 
 #ifdef __cplusplus
 }

@@ -47,6 +47,7 @@ SIGNATURES: dict[str, tuple] = {
     "ralpb_model_step": (c_i, [c_vp, c_vp, c_vp, c_i, c_f, c_f]),
     "ralpb_model_stats": (c_i, [c_vp, c_vp]),
     "ralpb_model_stream": (c_vp, [c_vp]),
+    "ralpb_model_set_profiling": (c_i, [c_vp, c_i]),
 }
 
 
@@ -60,7 +61,7 @@ class StepStats(C.Structure):
     """ralpb_step_stats (include/ralpb.h)."""
     _fields_ = [("loss", C.c_double), ("logical_bytes", c_ll), ("physical_bytes", c_ll), ("launches", c_i),
                 ("ms_step", c_f), ("ms_front_fwd", c_f), ("ms_back", c_f), ("ms_front_bwd", c_f),
-                ("ms_sync", c_f)]
+                ("ms_sync", c_f), ("ms_gemm", c_f), ("gemm_launches", c_i)]
 
 
 RALPB_CONV, RALPB_POOL, RALPB_FC = 0, 1, 2

@@ -60,4 +60,9 @@ int ralpb_model_stats(ralpb_model* m, ralpb_step_stats* out) {
 
 void* ralpb_model_stream(ralpb_model* m) { return m->impl->stream; }
 
+int ralpb_model_set_profiling(ralpb_model* m, int on) {
+  std::string why;
+  return model_set_profiling(m->impl, on, &why) ? set_error("ralpb_model_set_profiling: " + why) : 0;
+}
+
 }  // extern "C"

@@ -249,6 +249,10 @@ void model_destroy(Model* m) {
   if (m->arena) cudaFree(m->arena);
   for (auto& e : m->ev)
     if (e) cudaEventDestroy(e);
+  if (m->timer.ev) {
+    for (int i = 0; i < 2 * m->timer.cap; ++i) cudaEventDestroy(m->timer.ev[i]);
+    delete[] m->timer.ev;
+  }
   if (m->stream) cudaStreamDestroy(m->stream);
   delete m;
 }
@@ -494,6 +498,9 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
   const bool ralp = m->strategy == RALPB_STRATEGY_RALP;
   cudaStream_t s = m->stream;
   RALPB_TRY(cudaEventRecord(m->ev[0], s));
+  m->timer.n = 0;
+  set_gemm_timer(m->profiling ? &m->timer : nullptr);
+  struct Reset { ~Reset() { set_gemm_timer(nullptr); } } reset_timer;
 
   // ---------------- worker front forward
   const float* img = static_cast<const float*>(images);
@@ -622,6 +629,23 @@ int model_stats(Model* m, ralpb_step_stats* st, std::string* why) {
   cudaEventElapsedTime(&st->ms_back, m->ev[1], m->ev[2]);
   cudaEventElapsedTime(&st->ms_front_bwd, m->ev[2], m->ev[3]);
   cudaEventElapsedTime(&st->ms_sync, m->ev[3], m->ev[4]);
+  st->gemm_launches = m->profiling ? m->timer.n : 0;
+  st->ms_gemm = 0.f;
+  for (int i = 0; m->profiling && i < m->timer.n; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, m->timer.ev[2 * i], m->timer.ev[2 * i + 1]);
+    st->ms_gemm += ms;
+  }
+  return 0;
+}
+
+int model_set_profiling(Model* m, int on, std::string* why) {
+  if (on && m->timer.ev == nullptr) {
+    m->timer.cap = 256;
+    m->timer.ev = new cudaEvent_t[2 * m->timer.cap];
+    for (int i = 0; i < 2 * m->timer.cap; ++i) RALPB_TRY(cudaEventCreate(&m->timer.ev[i]));
+  }
+  m->profiling = on != 0;
   return 0;
 }
 

@@ -89,6 +89,8 @@ struct Model {
   int launches = 0;
   long long phys_bytes = 0;
   cudaEvent_t ev[6] = {};
+  bool profiling = false;
+  GemmTimer timer;
   bool stats_valid = false;
 };
 
@@ -102,5 +104,6 @@ int model_set_params(Model* m, int layer, const float* w, const float* b, int on
 int model_get_params(Model* m, int layer, float* w, float* b, int on_host, std::string* why);
 int model_ipc_handle(Model* m, void* out, std::string* why);
 int model_ipc_open(Model* m, const void* handles, std::string* why);
+int model_set_profiling(Model* m, int on, std::string* why);
 
 }  // namespace ralpb

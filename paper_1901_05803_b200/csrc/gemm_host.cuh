@@ -44,4 +44,12 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
 
 int num_sms();
 
+// Optional per-launch timing of the GEMM engine (CUDA events on the launch stream).
+struct GemmTimer {
+  cudaEvent_t* ev = nullptr;  // 2*cap events
+  int cap = 0;
+  int n = 0;
+};
+void set_gemm_timer(GemmTimer* t);  // thread-local; nullptr disables
+
 }  // namespace ralpb

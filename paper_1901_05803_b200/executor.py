@@ -73,6 +73,19 @@ def lower(model: ModelGraph, input_shape: Optional[tuple[int, int, int]] = None)
     return out
 
 
+def allgather_bytes(blob: bytes) -> list[bytes]:
+    """Rank-ordered all-gather of equal-length byte strings over the initialised
+    torch.distributed group (NCCL: via a CUDA tensor; gloo: on the CPU)."""
+    import torch
+    import torch.distributed as dist
+
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    mine = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(dev)
+    parts = [torch.empty_like(mine) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, mine)
+    return [bytes(p.cpu().numpy().tobytes()) for p in parts]
+
+
 _KIND = {"conv": _lib.RALPB_CONV, "pool": _lib.RALPB_POOL, "fc": _lib.RALPB_FC}
 
 
@@ -99,6 +112,8 @@ class StepResult:
     ms_back: float
     ms_front_bwd: float
     ms_sync: float
+    ms_gemm: float = 0.0
+    gemm_launches: int = 0
 
 
 class RankExecutor:
@@ -130,19 +145,12 @@ class RankExecutor:
             self._open_peers()
 
     def _open_peers(self) -> None:
-        import torch
-        import torch.distributed as dist
-
         buf = (C.c_char * 64)()
         _lib.call("ralpb_model_ipc_handle", self._h, C.cast(buf, C.c_void_p))
-        mine = torch.frombuffer(bytearray(bytes(buf)), dtype=torch.uint8)
-        backend = dist.get_backend()
-        dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
-        gathered = [torch.empty(64, dtype=torch.uint8, device=dev) for _ in range(self.world)]
-        dist.all_gather(gathered, mine.to(dev))
-        blob = b"".join(bytes(g.cpu().numpy().tobytes()) for g in gathered)
+        blob = b"".join(allgather_bytes(bytes(buf)))
         arr = (C.c_char * len(blob)).from_buffer_copy(blob)
         _lib.call("ralpb_model_ipc_open", self._h, C.cast(arr, C.c_void_p))
+        import torch.distributed as dist
         dist.barrier()
 
     # ---------------------------------------------------------------- params
@@ -190,7 +198,10 @@ class RankExecutor:
         st = _lib.StepStats()
         _lib.call("ralpb_model_stats", self._h, C.byref(st))
         return StepResult(st.loss, st.logical_bytes, st.physical_bytes, st.launches, st.ms_step, st.ms_front_fwd,
-                          st.ms_back, st.ms_front_bwd, st.ms_sync)
+                          st.ms_back, st.ms_front_bwd, st.ms_sync, st.ms_gemm, st.gemm_launches)
+
+    def set_profiling(self, on: bool) -> None:
+        _lib.call("ralpb_model_set_profiling", self._h, int(on))
 
     def close(self) -> None:
         if getattr(self, "_h", None):
@@ -245,4 +256,4 @@ def _breakdown(name: str, step: int, st: StepResult, w: int) -> StepBreakdown:
                          memcopy=(0.0,) * w, communication=(st.ms_sync * s,) * w)
 
 
-__all__ = ["ExecutorError", "RankExecutor", "StepResult", "infer_input_shape", "lower", "run_job"]
+__all__ = ["ExecutorError", "RankExecutor", "StepResult", "infer_input_shape", "lower", "run_job", "allgather_bytes"]
