@@ -1,5 +1,6 @@
 #include <cudaTypedefs.h>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include "gemm_host.cuh"
@@ -115,6 +116,7 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
   const int stage_bytes = kAStage + p.b_stage_bytes;
   const int budget = 227 * 1024 - 1024 - 256;
   p.stages = std::min(8, budget / stage_bytes);
+  if (const char* e = getenv("RALPB_STAGES")) p.stages = std::max(1, std::min(p.stages, atoi(e)));
   const int smem = 1024 + p.stages * stage_bytes + 256;
   p.idesc = umma_idesc_bf16(kBM, bn, !a_k, !b_k);
   p.a_mode = d.a_mode;
