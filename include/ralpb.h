@@ -47,19 +47,25 @@ int ralpb_gemm_bf16(const void* a, long long a_rows, long long a_cols, long long
 
 /* Implicit-GEMM convolution (stride 1, k = 2*pad+1) over the padded NHWC layout
  * [n][h+2pad][w+2pad][c] bf16 with zero borders.  Implements infer_conv
- * (layers.py:87-103) with ReLU fused.
+ * (layers.py:87-103) with ReLU fused.  Outputs are written on interior
+ * pixels only: allocate output buffers with zero borders.
  *   w:  [cout][k*k][cin] bf16      wd: [cin][k*k][cout] bf16 (tap-reversed transpose)
- *   dw: [cout][k*k][cin] fp32, accumulated (caller zeroes). */
+ *   dw: [cout][k*k][cin] fp32 and db: [cout] fp32 (may be NULL), accumulated (caller zeroes). */
 int ralpb_conv_fwd(const void* x_pad, const void* w, const float* bias, void* y_pad, int n, int h,
                    int w_, int cin, int cout, int k, int pad, int relu, void* stream);
 int ralpb_conv_dgrad(const void* dy_pad, const void* wd, const void* mask_pad, void* dx_pad, int n,
                      int h, int w_, int cin, int cout, int k, int pad, void* stream);
-int ralpb_conv_wgrad(const void* x_pad, const void* dy_pad, float* dw, int n, int h, int w_,
+int ralpb_conv_wgrad(const void* x_pad, const void* dy_pad, float* dw, float* db, int n, int h, int w_,
                      int cin, int cout, int k, int pad, void* stream);
 
 /* fp32 NHWC images -> bf16 padded NHWC with cp >= c channels (zero fill). */
 int ralpb_pack_input(const float* x, int n, int h, int w, int c, void* out, int cp, int pad,
                      void* stream);
+/* im2col patch matrix of fp32 NHWC images for a first (RGB) convolution: rows = the conv's
+ * padded output grid [n][ho+2po][wo+2po], columns j = (r*k+s)*c+ch, column k*k*c = 1 (bias),
+ * zero elsewhere and on border rows; kpad >= k*k*c+1, multiple of 8. */
+int ralpb_pack_im2col(const float* x, int n, int h, int w, int c, int k, int stride, int pad, int ho, int wo,
+                      int po, int kpad, void* out, void* stream);
 /* Max pool (infer_pool, layers.py:106-114; stride defaults to window). */
 int ralpb_maxpool_fwd(const void* x, int n, int h, int w, int c, int pad_in, int k, int stride,
                       void* y, int pad_out, void* stream);
@@ -133,6 +139,9 @@ int ralpb_model_step(ralpb_model* m, const void* images, const int32_t* labels, 
 /* Synchronises the model stream and reports the last step. */
 int ralpb_model_stats(ralpb_model* m, ralpb_step_stats* out);
 void* ralpb_model_stream(ralpb_model* m);
+/* Inspection: copies activation (which=0) or activation-gradient (which=1) buffer i (bf16,
+ * padded layout) to host_out (may be NULL to query); returns its element count or -1. */
+long long ralpb_model_debug_buffer(ralpb_model* m, int i, int which, void* host_out);
 /* Profiling mode: bracket every GEMM-engine launch with CUDA events (reported in stats). */
 int ralpb_model_set_profiling(ralpb_model* m, int on);
 

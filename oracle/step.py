@@ -91,7 +91,10 @@ def _front_forward(st: OracleState, nfront: int, imgs: np.ndarray, bf: bool):
         if L["kind"] == "conv":
             w, b = st.params[i]
             wt = _round(w.permute(0, 3, 1, 2).contiguous(), bf)
-            x = _round(torch.relu(_conv(x, wt, b, L["stride"], L["pad"])), bf)
+            # the first (RGB, cin <= 4) conv runs on the B200 as an im2col GEMM whose bias is
+            # a bf16 filter column multiplying a ones column
+            bias = _round(b, bf) if i == 0 and L["cin"] <= 4 else b
+            x = _round(torch.relu(_conv(x, wt, bias, L["stride"], L["pad"])), bf)
         else:
             x = F.max_pool2d(x, L["k"], L["stride"])
         acts.append(x)

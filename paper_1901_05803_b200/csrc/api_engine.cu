@@ -66,3 +66,18 @@ int ralpb_model_set_profiling(ralpb_model* m, int on) {
 }
 
 }  // extern "C"
+
+// Debug/inspection: copy activation buffer acts[i] (bf16, padded layout) or, for which=1,
+// the activation-gradient buffer gacts[i], into host memory; returns the element count.
+extern "C" long long ralpb_model_debug_buffer(ralpb_model* m, int i, int which, void* host_out) {
+  Model* mm = m->impl;
+  if (i < 0 || i >= static_cast<int>(mm->acts.size())) return -1;
+  const long long n = mm->acts[i].elems();
+  const void* src = which == 0 ? static_cast<const void*>(mm->acts[i].ptr) : static_cast<const void*>(mm->gacts[i]);
+  if (src == nullptr) return -1;
+  if (host_out != nullptr) {
+    cudaStreamSynchronize(mm->stream);
+    if (cudaMemcpy(host_out, src, n * sizeof(bf16), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  }
+  return n;
+}

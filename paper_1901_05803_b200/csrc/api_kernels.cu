@@ -25,7 +25,9 @@ int ralpb_gemm_bf16(const void* a, long long a_rows, long long a_cols, long long
   d.b_mode = b_mn ? LD_MN : LD_K;
   d.a = Operand2D{a, a_rows, a_cols, a_ld};
   d.b = Operand2D{b, b_rows, b_cols, b_ld};
-  d.kb = 64;
+  // narrow K-major contractions use a 32/16-wide k-block (64B/32B swizzle) instead of
+  // zero-filling a 64-wide one
+  d.kb = (!a_mn && !b_mn && K <= 16) ? 16 : (!a_mn && !b_mn && K <= 32) ? 32 : 64;
   d.block_n = block_n;
   d.k_splits = k_splits;
   d.epi = out_kind;
@@ -54,11 +56,11 @@ int ralpb_conv_dgrad(const void* dy_pad, const void* wd, const void* mask_pad, v
   return set_status(conv_dgrad(g, dy_pad, wd, mask_pad, dx_pad, static_cast<cudaStream_t>(stream), &why), why);
 }
 
-int ralpb_conv_wgrad(const void* x_pad, const void* dy_pad, float* dw, int n, int h, int w_,
+int ralpb_conv_wgrad(const void* x_pad, const void* dy_pad, float* dw, float* db, int n, int h, int w_,
                      int cin, int cout, int k, int pad, void* stream) {
   std::string why;
   ConvGeom g{n, h, w_, cin, cout, k, pad};
-  return set_status(conv_wgrad(g, x_pad, dy_pad, dw, static_cast<cudaStream_t>(stream), &why), why);
+  return set_status(conv_wgrad(g, x_pad, dy_pad, dw, db, static_cast<cudaStream_t>(stream), &why), why);
 }
 
 }  // extern "C"

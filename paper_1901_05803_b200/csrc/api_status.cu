@@ -57,3 +57,9 @@ int ralpb_cast_bf16(const float* x, long long n, void* y, void* stream) {
 }
 
 }  // extern "C"
+
+extern "C" int ralpb_pack_im2col(const float* x, int n, int h, int w, int c, int k, int stride, int pad, int ho,
+                                 int wo, int po, int kpad, void* out, void* stream) {
+  return set_status(pack_im2col(x, n, h, w, c, k, stride, pad, ho, wo, po, kpad, RALPB_BF(out), RALPB_S(stream)),
+                    "pack_im2col");
+}

@@ -1,5 +1,8 @@
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include "conv.cuh"
+#include "elementwise.cuh"
 
 namespace ralpb {
 
@@ -26,8 +29,8 @@ static void fill_border(const ConvGeom& g, GemmDesc* d) {
   d->w = g.w;
 }
 
-cudaError_t conv_fwd(const ConvGeom& g, const void* x_pad, const void* w, const float* bias,
-                     void* y_pad, int relu, cudaStream_t s, std::string* why) {
+cudaError_t conv_fwd_flat(const ConvGeom& g, const void* x_pad, const void* w, const float* bias,
+                          void* y_pad, int relu, cudaStream_t s, std::string* why) {
   if (!check_geom(g, why)) return cudaErrorInvalidValue;
   GemmDesc d;
   d.M = static_cast<int>(g.q());
@@ -50,8 +53,8 @@ cudaError_t conv_fwd(const ConvGeom& g, const void* x_pad, const void* w, const 
   return gemm_launch(d, s, why);
 }
 
-cudaError_t conv_dgrad(const ConvGeom& g, const void* dy_pad, const void* wd, const void* mask_pad,
-                       void* dx_pad, cudaStream_t s, std::string* why) {
+cudaError_t conv_dgrad_flat(const ConvGeom& g, const void* dy_pad, const void* wd, const void* mask_pad,
+                            void* dx_pad, cudaStream_t s, std::string* why) {
   if (!check_geom(g, why)) return cudaErrorInvalidValue;
   GemmDesc d;
   d.M = static_cast<int>(g.q());
@@ -74,8 +77,8 @@ cudaError_t conv_dgrad(const ConvGeom& g, const void* dy_pad, const void* wd, co
   return gemm_launch(d, s, why);
 }
 
-cudaError_t conv_wgrad(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw,
-                       cudaStream_t s, std::string* why) {
+cudaError_t conv_wgrad_flat(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw,
+                            cudaStream_t s, std::string* why) {
   if (!check_geom(g, why)) return cudaErrorInvalidValue;
   GemmDesc d;
   d.M = g.taps() * g.cin;
@@ -94,6 +97,47 @@ cudaError_t conv_wgrad(const ConvGeom& g, const void* x_pad, const void* dy_pad,
   d.s_m = 1;
   d.s_n = static_cast<long long>(g.taps()) * g.cin;
   return gemm_launch(d, s, why);
+}
+
+// Kernel family per call: RALPB_CONV=slab|flat forces one (A/B comparisons); the default
+// picks by shape from measurements (tools/probe_conv.py): the slab kernels win where the
+// image is large relative to the 16x8 pixel tile.
+enum class Family { kAuto, kSlab, kFlat };
+static Family family() {
+  const char* e = getenv("RALPB_CONV");
+  if (e != nullptr && std::strcmp(e, "flat") == 0) return Family::kFlat;
+  if (e != nullptr && std::strcmp(e, "slab") == 0) return Family::kSlab;
+  return Family::kAuto;
+}
+static bool pick_slab(bool eligible, bool auto_choice) {
+  if (!eligible) return false;
+  switch (family()) {
+    case Family::kFlat: return false;
+    case Family::kSlab: return true;
+    default: return auto_choice;
+  }
+}
+
+cudaError_t conv_fwd(const ConvGeom& g, const void* x_pad, const void* w, const float* bias, void* y_pad,
+                     int relu, cudaStream_t s, std::string* why) {
+  if (pick_slab(slab_fwd_ok(g, g.cin, g.cout), g.h >= 64 || g.cin < 64))
+    return conv_slab_fwd(g, x_pad, w, g.cin, g.cout, bias, relu, nullptr, y_pad, s, why);
+  return conv_fwd_flat(g, x_pad, w, bias, y_pad, relu, s, why);
+}
+
+cudaError_t conv_dgrad(const ConvGeom& g, const void* dy_pad, const void* wd, const void* mask_pad,
+                       void* dx_pad, cudaStream_t s, std::string* why) {
+  if (pick_slab(slab_fwd_ok(g, g.cout, g.cin), g.h >= 64 || g.cout < 64))
+    return conv_slab_fwd(g, dy_pad, wd, g.cout, g.cin, nullptr, 0, mask_pad, dx_pad, s, why);
+  return conv_dgrad_flat(g, dy_pad, wd, mask_pad, dx_pad, s, why);
+}
+
+cudaError_t conv_wgrad(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw, float* db,
+                       cudaStream_t s, std::string* why) {
+  if (pick_slab(slab_wgrad_ok(g), g.h >= 56)) return conv_slab_wgrad(g, x_pad, dy_pad, dw, db, s, why);
+  cudaError_t e = conv_wgrad_flat(g, x_pad, dy_pad, dw, s, why);
+  if (e != cudaSuccess || db == nullptr) return e;
+  return colsum_bf16(static_cast<const __nv_bfloat16*>(dy_pad), g.q(), g.cout, g.cout, db, s);
 }
 
 }  // namespace ralpb

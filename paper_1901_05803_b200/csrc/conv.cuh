@@ -23,15 +23,35 @@ struct ConvGeom {
   int taps() const { return k * k; }
 };
 
-// y_pad = relu?(conv(x_pad, w) + bias), borders zeroed.  w: [cout][k*k][cin] bf16.
+// Every conv entry point takes the padded layout; the slab kernels (the default)
+// write interior pixels only, so output buffers must be allocated with zero borders
+// (the executor zero-initialises every activation/gradient buffer once).
+//
+// y_pad = relu?(conv(x_pad, w) + bias).  w: [cout][k*k][cin] bf16.
 cudaError_t conv_fwd(const ConvGeom& g, const void* x_pad, const void* w, const float* bias,
                      void* y_pad, int relu, cudaStream_t s, std::string* why);
-// dx_pad = (conv_transpose(dy_pad, w)) * (mask_pad > 0 if mask_pad), borders zeroed.
+// dx_pad = conv_transpose(dy_pad, w) * (mask_pad > 0 if mask_pad).
 // wd: [cin][k*k][cout] bf16, wd[ci][t][co] = w[co][k*k-1-t][ci].
 cudaError_t conv_dgrad(const ConvGeom& g, const void* dy_pad, const void* wd, const void* mask_pad,
                        void* dx_pad, cudaStream_t s, std::string* why);
-// dw[co][t][ci] += sum_q dy[q][co] * x[q + off(t)][ci]   (fp32, atomics, split-K).
-cudaError_t conv_wgrad(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw,
+// dw[co][t][ci] += sum_q dy[q][co] * x[q + off(t)][ci];  db[co] += sum_q dy[q][co] if db.
+cudaError_t conv_wgrad(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw, float* db,
                        cudaStream_t s, std::string* why);
+
+// Padded-flattened single-tap-load variants (write the full padded buffer, zero borders).
+cudaError_t conv_fwd_flat(const ConvGeom& g, const void* x_pad, const void* w, const float* bias,
+                          void* y_pad, int relu, cudaStream_t s, std::string* why);
+cudaError_t conv_dgrad_flat(const ConvGeom& g, const void* dy_pad, const void* wd, const void* mask_pad,
+                            void* dx_pad, cudaStream_t s, std::string* why);
+cudaError_t conv_wgrad_flat(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw,
+                            cudaStream_t s, std::string* why);
+
+// Slab-tiled kernels (conv_slab.cu).  `c` = contracted channels, `cout` = produced channels.
+bool slab_fwd_ok(const ConvGeom& g, int c, int cout);
+bool slab_wgrad_ok(const ConvGeom& g);
+cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, int c, int cout, const float* bias,
+                          int relu, const void* mask_pad, void* y_pad, cudaStream_t s, std::string* why);
+cudaError_t conv_slab_wgrad(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw, float* db,
+                            cudaStream_t s, std::string* why);
 
 }  // namespace ralpb

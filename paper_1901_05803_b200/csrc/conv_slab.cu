@@ -1,0 +1,163 @@
+// Host planning / launch of the slab-tiled conv kernels (see conv_slab.cuh).
+#include <cudaTypedefs.h>
+#include <algorithm>
+#include <cstring>
+#include "conv.cuh"
+#include "conv_slab.cuh"
+
+namespace ralpb {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+CUtensorMapSwizzle swz_mode(int bytes) {
+  return bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+}
+
+// Padded activation [n][hp][wp][c] as a 4-D tensor, box {bc, bw, bh, 1}.
+bool encode_act(CUtensorMap* tm, const void* ptr, long long c, long long wp, long long hp, long long n, int bc, int bw,
+                int bh, int swz, std::string* why) {
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(wp), static_cast<cuuint64_t>(hp),
+                        static_cast<cuuint64_t>(n)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * 2, static_cast<cuuint64_t>(wp * c) * 2,
+                           static_cast<cuuint64_t>(hp * wp * c) * 2};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(bc), static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh), 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = encoder()(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz_mode(swz), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { *why = "3-D tensor map encode failed (" + std::to_string(static_cast<int>(r)) + ")"; return false; }
+  return true;
+}
+
+bool encode_mat(CUtensorMap* tm, const void* ptr, long long rows, long long cols, int bc, int br, int swz,
+                std::string* why) {
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(bc), static_cast<cuuint32_t>(br)};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encoder()(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz_mode(swz), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { *why = "2-D tensor map encode failed (" + std::to_string(static_cast<int>(r)) + ")"; return false; }
+  return true;
+}
+
+int align1k(int x) { return (x + 1023) & ~1023; }
+constexpr int kSmemBudget = 227 * 1024 - 1024 - 512;
+
+}  // namespace
+
+bool slab_fwd_ok(const ConvGeom& g, int c, int cout) {
+  return g.k == 2 * g.pad + 1 && g.taps() <= kSlabMaxTaps && (c == 16 || c == 32 || c % 64 == 0) && cout % 16 == 0 &&
+         g.q() < (1LL << 31);
+}
+
+bool slab_wgrad_ok(const ConvGeom& g) {
+  return g.k == 3 && g.pad == 1 && g.cin % 64 == 0 && g.cout % 64 == 0 && g.q() < (1LL << 31);
+}
+
+cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, int c, int cout, const float* bias,
+                          int relu, const void* mask_pad, void* y_pad, cudaStream_t s, std::string* why) {
+  static bool attr[3] = {false, false, false};
+  SlabConvParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.n = g.n; p.h = g.h; p.w = g.w; p.hp = g.hp(); p.wp = g.wp(); p.pad = g.pad; p.k = g.k; p.taps = g.taps();
+  p.c = c; p.cout = cout;
+  p.kb = std::min(64, c);
+  p.row_bytes = p.kb * 2;
+  p.bn = cout >= 256 ? 256 : cout >= 128 ? 128 : cout >= 64 ? 64 : 32;
+  p.macc = p.bn >= 256 ? 1 : p.bn >= 128 ? 2 : 4;
+  p.acc_bufs = p.macc * p.bn <= 256 ? 2 : 1;
+  const int used = p.macc * p.bn * p.acc_bufs;
+  p.tmem_cols = used <= 32 ? 32 : used <= 64 ? 64 : used <= 128 ? 128 : used <= 256 ? 256 : 512;
+  p.sw = 8 + g.k - 1;
+  p.sh = 16 * p.macc + g.k - 1;
+  p.slab_load = p.row_bytes * p.sw * p.sh;
+  p.slab_stage = align1k(p.slab_load);
+  p.b_load = p.bn * p.row_bytes;
+  p.b_stage = align1k(p.b_load);
+  p.na = 2;
+  p.nb = std::min(8, (kSmemBudget - p.na * p.slab_stage) / p.b_stage);
+  if (p.nb < 2) { *why = "slab conv: tile does not fit in shared memory"; return cudaErrorInvalidValue; }
+  p.n_hb = (g.h + 16 * p.macc - 1) / (16 * p.macc);
+  p.n_wb = (g.w + 7) / 8;
+  p.n_nt = (cout + p.bn - 1) / p.bn;
+  p.idesc = umma_idesc_bf16(128, p.bn, false, false);
+  p.out = static_cast<__nv_bfloat16*>(y_pad);
+  p.bias = bias;
+  p.relu = relu;
+  p.mask = static_cast<const __nv_bfloat16*>(mask_pad);
+  if (!encode_act(&p.tmX, x_pad, c, g.wp(), g.hp(), g.n, p.kb, p.sw, p.sh, p.row_bytes, why))
+    return cudaErrorInvalidValue;
+  if (!encode_mat(&p.tmB, w, cout, static_cast<long long>(g.taps()) * c, p.kb, p.bn, p.row_bytes, why))
+    return cudaErrorInvalidValue;
+  const int smem = 1024 + p.na * p.slab_stage + p.nb * p.b_stage + 512;
+  const long long total = static_cast<long long>(g.n) * p.n_hb * p.n_wb * p.n_nt;
+  const int grid = static_cast<int>(std::min<long long>(total, num_sms()));
+  if (p.macc >= 2) {
+    if (!attr[2]) { cudaFuncSetAttribute(conv_slab_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); attr[2] = true; }
+    launch_timed([&] { conv_slab_fwd_kernel<2><<<grid, 384, smem, s>>>(p); }, s);
+  } else {
+    if (!attr[1]) { cudaFuncSetAttribute(conv_slab_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); attr[1] = true; }
+    launch_timed([&] { conv_slab_fwd_kernel<1><<<grid, 256, smem, s>>>(p); }, s);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t conv_slab_wgrad(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw, float* db,
+                            cudaStream_t s, std::string* why) {
+  static bool attr = false;
+  SlabConvParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.n = g.n; p.h = g.h; p.w = g.w; p.hp = g.hp(); p.wp = g.wp(); p.pad = g.pad; p.k = g.k; p.taps = g.taps();
+  p.c = g.cin; p.cout = g.cout;
+  p.kb = 64;
+  p.row_bytes = 128;
+  p.bn = 64;
+  p.sw = 8 + g.k - 1;
+  p.sh = 16 + g.k - 1;
+  p.slab_load = 128 * p.sw * p.sh;
+  p.slab_stage = align1k(p.slab_load);
+  p.b_load = 128 * 8 * 16;
+  p.b_stage = align1k(p.b_load);
+  p.na = std::min(8, (kSmemBudget - 4096) / (p.slab_stage + p.b_stage));
+  const int nacc = (p.taps + 1) / 2;
+  const int used = (nacc + 1) * 64;
+  p.tmem_cols = used <= 256 ? 256 : 512;
+  p.n_hb = (g.h + 15) / 16;
+  p.n_wb = (g.w + 7) / 8;
+  p.n_pix_blocks = g.n * p.n_hb * p.n_wb;
+  p.n_ci_blocks = g.cin / 64;
+  p.n_co_blocks = g.cout / 64;
+  const int sms = num_sms();
+  const int tiles = p.n_ci_blocks * p.n_co_blocks;
+  int splits = std::max(1, (2 * sms + tiles - 1) / tiles);
+  splits = std::min(splits, p.n_pix_blocks);
+  p.blocks_per_split = (p.n_pix_blocks + splits - 1) / splits;
+  p.n_splits = (p.n_pix_blocks + p.blocks_per_split - 1) / p.blocks_per_split;
+  p.idesc = umma_idesc_bf16(128, 64, true, true);
+  p.dw = dw;
+  p.db = db;
+  if (!encode_act(&p.tmX, x_pad, g.cin, g.wp(), g.hp(), g.n, 64, p.sw, p.sh, 128, why))
+    return cudaErrorInvalidValue;
+  if (!encode_act(&p.tmB, dy_pad, g.cout, g.wp(), g.hp(), g.n, 64, 8, 16, 128, why))
+    return cudaErrorInvalidValue;
+  const int smem = 1024 + 4096 + p.na * (p.slab_stage + p.b_stage) + 512;
+  if (!attr) { cudaFuncSetAttribute(conv_slab_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); attr = true; }
+  const long long total = static_cast<long long>(tiles) * p.n_splits;
+  const int grid = static_cast<int>(std::min<long long>(total, sms));
+  launch_timed([&] { conv_slab_wgrad_kernel<<<grid, 256, smem, s>>>(p); }, s);
+  return cudaGetLastError();
+}
+
+}  // namespace ralpb

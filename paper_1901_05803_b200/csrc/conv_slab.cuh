@@ -1,0 +1,394 @@
+// Slab-tiled implicit-GEMM convolution on tcgen05 (stride 1, k = 2p+1, padded NHWC).
+//
+// Output tiles are 2-D pixel blocks: one UMMA M-tile = 16 image rows x 8 columns
+// (8-pixel groups are image-row segments).  For a channel block, ONE 3-D TMA box
+// of (16*macc + k-1) x (8 + k-1) pixels ("halo slab") lands in shared memory with
+// the 128B swizzle, and every tap (r, s) of the filter is the same slab seen
+// through a shifted UMMA descriptor:
+//     start = slab + ((16a + r) * SW + s) * row_bytes,   SBO = SW * row_bytes
+// (SW = 8 + k - 1).  UMMA applies the swizzle from absolute shared-memory
+// address bits, so row-granular starts and SBO = SW*row_bytes are legal
+// (tools/exp_desc.cu).  This cuts operand traffic for the activation by ~k^2
+// versus one TMA load per tap.
+//
+//   conv_slab_fwd_kernel   forward and backward-data (K-major A from the slab,
+//                          K-major B = per-tap filter tiles), fused bias/ReLU or
+//                          ReLU-mask epilogue, writes interior pixels only.
+//   conv_slab_wgrad_kernel backward-filter: M = (tap, ci) pairs of taps read as two
+//                          MN-major atoms of the same slab (LBO = tap distance),
+//                          N = 64 output channels, K = pixels; one extra
+//                          accumulator with an all-ones A yields the bias gradient.
+#pragma once
+#include "ptx.cuh"
+
+namespace ralpb {
+
+// 4-D box load from a padded activation viewed as [n][hp][wp][c]; rows/cols beyond the
+// image (or the tensor) are zero-filled by TMA, so partial pixel tiles contribute nothing.
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+constexpr int kSlabMaxTaps = 25;
+
+struct alignas(64) SlabConvParams {
+  CUtensorMap tmX;      // activation [N][Hp][Wp][C], box {kb, SW, SH, 1}
+  CUtensorMap tmB;      // fwd: filters [Cout][taps*C] box {kb, BN}; wgrad: dY [N][Hp][Wp][Cout] box {64, 8, 16, 1}
+  int n, h, w, hp, wp, pad, k, taps;
+  int c;                // contracted channels (fwd: input channels of the GEMM; wgrad: layer cin)
+  int cout;             // output channels of the GEMM (fwd) / layer cout (wgrad)
+  int kb, row_bytes;    // channels per k-block, bytes per slab row
+  int sw, sh;           // slab width / height in pixels
+  int macc;             // accumulators along M (16-row pixel blocks)
+  int bn;
+  int n_hb, n_wb, n_nt;
+  int slab_stage, b_stage;   // aligned bytes per stage
+  int slab_load, b_load;     // TMA bytes per stage
+  int na, nb;                // ring depths (wgrad uses na only)
+  int acc_bufs;
+  uint32_t tmem_cols;
+  uint32_t idesc;
+  // fwd epilogue
+  __nv_bfloat16* out;
+  const float* bias;
+  int relu;
+  const __nv_bfloat16* mask;
+  // wgrad
+  float* dw;
+  float* db;
+  int n_ci_blocks, n_co_blocks, n_splits, blocks_per_split, n_pix_blocks;
+};
+
+// ------------------------------------------------------------------ forward / backward-data
+template <int EWG>
+__global__ void __launch_bounds__(128 + 128 * EWG, 1) conv_slab_fwd_kernel(const __grid_constant__ SlabConvParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + p.na * p.slab_stage;
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(sB + p.nb * p.b_stage);
+  uint64_t* a_empty = a_full + p.na;
+  uint64_t* b_full = a_empty + p.na;
+  uint64_t* b_empty = b_full + p.nb;
+  uint64_t* tfull = b_empty + p.nb;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.tmX);
+    tma_prefetch(&p.tmB);
+    for (int i = 0; i < p.na; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < p.nb; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128 * EWG); }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total = p.n * p.n_hb * p.n_wb * p.n_nt;
+  const int cblks = p.c / p.kb;
+  const int ksteps = p.kb / 16;
+  const int mrows = 16 * p.macc;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int as = 0, bs = 0;
+      uint32_t aph = 0, bph = 0;
+      for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
+        int t = wi;
+        const int nt = t % p.n_nt; t /= p.n_nt;
+        const int wb = t % p.n_wb; t /= p.n_wb;
+        const int hb = t % p.n_hb;
+        const int img = t / p.n_hb;
+        const int h0 = hb * mrows, w0 = wb * 8;
+        for (int cb = 0; cb < cblks; ++cb) {
+          mbar_wait(&a_empty[as], aph ^ 1);
+          mbar_expect_tx(&a_full[as], p.slab_load);
+          tma_load_4d(sA + as * p.slab_stage, &p.tmX, &a_full[as], cb * p.kb, w0, h0, img);
+          if (++as == p.na) { as = 0; aph ^= 1; }
+          for (int tap = 0; tap < p.taps; ++tap) {
+            mbar_wait(&b_empty[bs], bph ^ 1);
+            mbar_expect_tx(&b_full[bs], p.b_load);
+            tma_load_2d(sB + bs * p.b_stage, &p.tmB, &b_full[bs], tap * p.c + cb * p.kb, nt * p.bn);
+            if (++bs == p.nb) { bs = 0; bph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int as = 0, bs = 0, acc = 0;
+      uint32_t aph = 0, bph = 0, acc_ph = 0;
+      const uint32_t sbo = p.sw * p.row_bytes;
+      for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_ph ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + acc * p.macc * p.bn;
+        for (int cb = 0; cb < cblks; ++cb) {
+          mbar_wait(&a_full[as], aph);
+          tc_fence_after();
+          const uint32_t slab = smem_u32(sA + as * p.slab_stage);
+          for (int tap = 0; tap < p.taps; ++tap) {
+            const int r = tap / p.k, s = tap - (tap / p.k) * p.k;
+            mbar_wait(&b_full[bs], bph);
+            tc_fence_after();
+            const uint32_t bbase = smem_u32(sB + bs * p.b_stage);
+            for (int a = 0; a < p.macc; ++a) {
+              const uint32_t arow = static_cast<uint32_t>((a * 16 + r) * p.sw + s);
+              for (int ks = 0; ks < ksteps; ++ks) {
+                const uint64_t ad = umma_smem_desc(slab + arow * p.row_bytes + ks * 32, 16, sbo, p.row_bytes);
+                const uint64_t bd = umma_smem_desc(bbase + ks * 32, 16, 8 * p.row_bytes, p.row_bytes);
+                umma_bf16(d0 + a * p.bn, ad, bd, p.idesc, (cb > 0 || tap > 0 || ks > 0) ? 1u : 0u);
+              }
+            }
+            umma_commit(&b_empty[bs]);
+            if (++bs == p.nb) { bs = 0; bph ^= 1; }
+          }
+          umma_commit(&a_empty[as]);
+          if (++as == p.na) { as = 0; aph ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == p.acc_bufs) { acc = 0; acc_ph ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int g = (warp - 4) >> 2;   // epilogue warpgroup
+    const int q = warp & 3;          // TMEM lane quarter
+    const int m = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
+      int t = wi;
+      const int nt = t % p.n_nt; t /= p.n_nt;
+      const int wb = t % p.n_wb; t /= p.n_wb;
+      const int hb = t % p.n_hb;
+      const int img = t / p.n_hb;
+      mbar_wait(&tfull[acc], acc_ph);
+      tc_fence_after();
+      for (int a = g; a < p.macc; a += EWG) {
+        const int hh = hb * mrows + a * 16 + (m >> 3);
+        const int ww = wb * 8 + (m & 7);
+        const bool valid = hh < p.h && ww < p.w;
+        const long long orow = (static_cast<long long>(img) * p.hp + hh + p.pad) * p.wp + ww + p.pad;
+        const uint32_t tb = tmem_base + (acc * p.macc + a) * p.bn + (static_cast<uint32_t>(q * 32) << 16);
+        for (int c = 0; c < p.bn; c += 32) {
+          uint32_t rr[32];
+          tmem_ld32(tb + c, rr);
+          tmem_wait_ld();
+          const int n0 = nt * p.bn + c;
+          if (!valid || n0 >= p.cout) continue;
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
+          const bool full = n0 + 32 <= p.cout;
+          if (p.bias != nullptr) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += (full || n0 + j < p.cout) ? __ldg(p.bias + n0 + j) : 0.f;
+          }
+          if (p.relu) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+          }
+          __nv_bfloat16* o = p.out + orow * p.cout + n0;
+          if (p.mask != nullptr) {
+            const __nv_bfloat16* mp = p.mask + orow * p.cout + n0;
+            if (full) {
+#pragma unroll
+              for (int j4 = 0; j4 < 4; ++j4) {
+                uint4 u = *reinterpret_cast<const uint4*>(mp + j4 * 8);
+                const __nv_bfloat16* hb2 = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  if (!(__bfloat162float(hb2[e]) > 0.f)) v[j4 * 8 + e] = 0.f;
+              }
+            } else {
+              for (int j = 0; j < 32 && n0 + j < p.cout; ++j)
+                if (!(__bfloat162float(mp[j]) > 0.f)) v[j] = 0.f;
+            }
+          }
+          if (full) {
+#pragma unroll
+            for (int j4 = 0; j4 < 4; ++j4) {
+              uint4 u;
+              u.x = pack_bf16(v[j4 * 8 + 0], v[j4 * 8 + 1]);
+              u.y = pack_bf16(v[j4 * 8 + 2], v[j4 * 8 + 3]);
+              u.z = pack_bf16(v[j4 * 8 + 4], v[j4 * 8 + 5]);
+              u.w = pack_bf16(v[j4 * 8 + 6], v[j4 * 8 + 7]);
+              *reinterpret_cast<uint4*>(o + j4 * 8) = u;
+            }
+          } else {
+            for (int j = 0; j < 32 && n0 + j < p.cout; ++j) o[j] = __float2bfloat16_rn(v[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == p.acc_bufs) { acc = 0; acc_ph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+}
+
+// ------------------------------------------------------------------ backward-filter
+// Stage = one pixel block (16 x 8 pixels): X halo slab (64 ci) + dY tile (64 co).
+// Accumulator a (0..ceil(taps/2)-1) holds taps (2a, 2a+1) x 64 ci; accumulator
+// `nacc` holds the bias gradient (ones x dY) when this CTA owns ci-block 0.
+__global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_constant__ SlabConvParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sOnes = smem;                           // 4 KB of bf16 ones (MN-major 2 atoms x 16 rows)
+  uint8_t* sStage = smem + 4096;
+  const int stage_bytes = p.slab_stage + p.b_stage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStage + p.na * stage_bytes);
+  uint64_t* empty = full + p.na;
+  uint64_t* tfull = empty + p.na;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 4096 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(sOnes)[i] = 0x3F803F80u;  // bf16 1.0 pairs
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.tmX);
+    tma_prefetch(&p.tmB);
+    for (int i = 0; i < p.na; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tempty[0], 128);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int nacc = (p.taps + 1) / 2;
+  const int total = p.n_ci_blocks * p.n_co_blocks * p.n_splits;
+  const int pb_per_img = p.n_hb * p.n_wb;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
+        const int nb = wi % p.n_co_blocks;
+        const int cb = (wi / p.n_co_blocks) % p.n_ci_blocks;
+        const int sp = wi / (p.n_co_blocks * p.n_ci_blocks);
+        const int pb0 = sp * p.blocks_per_split;
+        const int pb1 = min(pb0 + p.blocks_per_split, p.n_pix_blocks);
+        for (int pb = pb0; pb < pb1; ++pb) {
+          const int img = pb / pb_per_img;
+          const int rem = pb - img * pb_per_img;
+          const int h0 = (rem / p.n_wb) * 16, w0 = (rem % p.n_wb) * 8;
+          mbar_wait(&empty[st], ph ^ 1);
+          mbar_expect_tx(&full[st], p.slab_load + p.b_load);
+          uint8_t* base = sStage + st * stage_bytes;
+          tma_load_4d(base, &p.tmX, &full[st], cb * 64, w0, h0, img);
+          tma_load_4d(base + p.slab_stage, &p.tmB, &full[st], nb * 64, w0 + p.pad, h0 + p.pad, img);
+          if (++st == p.na) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0, acc_ph = 0;
+      const uint32_t ones = smem_u32(sOnes);
+      for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
+        const int cb = (wi / p.n_co_blocks) % p.n_ci_blocks;
+        const int sp = wi / (p.n_co_blocks * p.n_ci_blocks);
+        const int pb0 = sp * p.blocks_per_split;
+        const int pb1 = min(pb0 + p.blocks_per_split, p.n_pix_blocks);
+        const bool with_bias = cb == 0 && p.db != nullptr;
+        mbar_wait(&tempty[0], acc_ph ^ 1);
+        tc_fence_after();
+        for (int pb = pb0; pb < pb1; ++pb) {
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          const uint32_t slab = smem_u32(sStage + st * stage_bytes);
+          const uint32_t dyt = slab + p.slab_stage;
+          for (int a = 0; a < nacc; ++a) {
+            const int t0 = 2 * a;
+            const int t1 = 2 * a + 1 < p.taps ? 2 * a + 1 : t0;
+            const int o0 = (t0 / p.k) * p.sw + t0 % p.k;
+            const int o1 = (t1 / p.k) * p.sw + t1 % p.k;
+            const uint32_t lbo = static_cast<uint32_t>(o1 - o0) * 128u;
+            for (int ks = 0; ks < 8; ++ks) {
+              const uint64_t ad = umma_smem_desc(slab + (o0 + 2 * ks * p.sw) * 128, lbo, p.sw * 128, 128);
+              const uint64_t bd = umma_smem_desc(dyt + ks * 2048, 8192, 1024, 128);
+              umma_bf16(tmem_base + a * 64, ad, bd, p.idesc, (pb > pb0 || ks > 0) ? 1u : 0u);
+            }
+          }
+          if (with_bias) {
+            for (int ks = 0; ks < 8; ++ks) {
+              const uint64_t ad = umma_smem_desc(ones, 2048, 1024, 128);
+              const uint64_t bd = umma_smem_desc(dyt + ks * 2048, 8192, 1024, 128);
+              umma_bf16(tmem_base + nacc * 64, ad, bd, p.idesc, (pb > pb0 || ks > 0) ? 1u : 0u);
+            }
+          }
+          umma_commit(&empty[st]);
+          if (++st == p.na) { st = 0; ph ^= 1; }
+        }
+        umma_commit(&tfull[0]);
+        acc_ph ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int m = q * 32 + lane;
+    uint32_t acc_ph = 0;
+    const long long wstride = static_cast<long long>(p.taps) * p.c;  // dW[co][tap][ci]
+    for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
+      const int nb = wi % p.n_co_blocks;
+      const int cb = (wi / p.n_co_blocks) % p.n_ci_blocks;
+      const bool with_bias = cb == 0 && p.db != nullptr;
+      mbar_wait(&tfull[0], acc_ph);
+      tc_fence_after();
+      for (int a = 0; a <= nacc; ++a) {
+        if (a == nacc && !with_bias) break;
+        const uint32_t tb = tmem_base + a * 64 + (static_cast<uint32_t>(q * 32) << 16);
+        for (int c = 0; c < 64; c += 32) {
+          uint32_t rr[32];
+          tmem_ld32(tb + c, rr);
+          tmem_wait_ld();
+          const int co0 = nb * 64 + c;
+          if (a < nacc) {
+            const int tap = 2 * a + (m >> 6);
+            if (tap < p.taps) {
+              float* dst = p.dw + static_cast<long long>(co0) * wstride + static_cast<long long>(tap) * p.c + cb * 64 + (m & 63);
+#pragma unroll 8
+              for (int j = 0; j < 32; ++j) red_add_f32(dst + j * wstride, __uint_as_float(rr[j]));
+            }
+          } else if (m == 0) {
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j) red_add_f32(p.db + co0 + j, __uint_as_float(rr[j]));
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[0]);
+      acc_ph ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+}
+
+}  // namespace ralpb

@@ -39,6 +39,49 @@ cudaError_t pack_input(const float* x, int n, int h, int w, int c, __nv_bfloat16
   return cudaGetLastError();
 }
 
+// One thread = 8 consecutive columns of one im2col row (a 16-byte store).
+__global__ void pack_im2col_kernel(const float* __restrict__ x, int n, int h, int w, int c, int k, int st, int p,
+                                   int ho, int wo, int po, int kpad, __nv_bfloat16* __restrict__ out) {
+  const int hop = ho + 2 * po, wop = wo + 2 * po;
+  const int groups = kpad / 8;
+  const int kk = k * k * c;
+  const long long total = static_cast<long long>(n) * hop * wop * groups;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i % groups);
+    const long long row = i / groups;
+    const long long img = row / (static_cast<long long>(hop) * wop);
+    const int rem = static_cast<int>(row - img * hop * wop);
+    const int oy = rem / wop - po, ox = rem % wop - po;
+    const bool interior = oy >= 0 && oy < ho && ox >= 0 && ox < wo;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int j = g * 8 + e;
+      float val = 0.f;
+      if (interior) {
+        if (j < kk) {
+          const int ch = j % c, tap = j / c;
+          const int iy = oy * st + tap / k - p, ix = ox * st + tap % k - p;
+          if (iy >= 0 && iy < h && ix >= 0 && ix < w) val = x[((img * h + iy) * w + ix) * c + ch];
+        } else if (j == kk) {
+          val = 1.f;
+        }
+      }
+      v[e] = __float2bfloat16_rn(val);
+    }
+    *reinterpret_cast<uint4*>(out + row * kpad + g * 8) = *reinterpret_cast<const uint4*>(v);
+  }
+}
+
+cudaError_t pack_im2col(const float* x, int n, int h, int w, int c, int k, int st, int p, int ho, int wo,
+                        int po, int kpad, __nv_bfloat16* out, cudaStream_t s) {
+  if (kpad % 8 != 0 || kpad < k * k * c + 1) return cudaErrorInvalidValue;
+  const long long total = static_cast<long long>(n) * (ho + 2 * po) * (wo + 2 * po) * (kpad / 8);
+  pack_im2col_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, n, h, w, c, k, st, p, ho, wo, po, kpad, out);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ max pool
 // One thread = one output position x 8 channels.
 __global__ void maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, int n, int h, int w, int c,

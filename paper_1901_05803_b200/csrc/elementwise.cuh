@@ -11,6 +11,13 @@ namespace ralpb {
 cudaError_t pack_input(const float* x, int n, int h, int w, int c, __nv_bfloat16* out, int cp,
                        int pad, cudaStream_t s);
 
+// im2col of an fp32 NHWC image batch for the first convolution (k x k, stride st, pad p):
+// out[(img, oy+po, ox+po)][j] for the padded output grid [n][ho+2po][wo+2po][kpad], with
+// j = (r*k + s)*c + ch the filter tap, column k*k*c = 1 (bias folded into the GEMM) and zeros
+// elsewhere (incl. every border row).
+cudaError_t pack_im2col(const float* x, int n, int h, int w, int c, int k, int st, int p, int ho, int wo,
+                        int po, int kpad, __nv_bfloat16* out, cudaStream_t s);
+
 // Max pool, window k, stride st (no pool padding).  x: [n][h+2pi][w+2pi][c]; y:
 // [n][oh+2po][ow+2po][c] with zero border.  Ties resolve to the first maximum
 // in row-major window order.

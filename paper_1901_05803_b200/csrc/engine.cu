@@ -101,8 +101,19 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   if (l0.kind != RALPB_CONV) return fail("first layer must be a convolution");
   m->in_h = l0.h; m->in_w = l0.w; m->in_c = l0.cin;
   m->in_cp = static_cast<int>(align_up(l0.cin, 16));
+  // A first convolution over a few input channels (RGB) runs as an im2col GEMM: acts[0] is
+  // then the [rows of the conv's padded output grid][kpad] patch matrix with a ones column
+  // that carries the bias (so bias and its gradient come out of the GEMMs themselves).
+  const bool first_im2col = l0.cin <= 4;
   ActBuf a0;
   a0.n = batch; a0.h = l0.h; a0.w = l0.w; a0.c = m->in_cp; a0.pad = l0.pad;
+  if (first_im2col) {
+    const int kk1 = l0.k * l0.k * l0.cin + 1;
+    a0.h = (l0.h + 2 * l0.pad - l0.k) / l0.stride + 1;
+    a0.w = (l0.w + 2 * l0.pad - l0.k) / l0.stride + 1;
+    a0.c = static_cast<int>(kk1 <= 32 ? 32 : align_up(kk1, 64));
+    a0.pad = (nconv > 1 && layers[1].kind == RALPB_CONV) ? layers[1].pad : 0;
+  }
   m->acts.push_back(a0);
   long long off = 0;
   for (int i = 0; i < nconv; ++i) {
@@ -112,6 +123,24 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     o.n = batch;
     FrontLayer f;
     f.kind = d.kind;
+    if (i == 0 && first_im2col) {
+      if (!d.relu || d.cout % 16 != 0) return fail("first conv: needs ReLU and cout % 16 == 0");
+      f.im2col = true;
+      f.kpad = in.c;
+      f.cin_real = d.cin;
+      f.g = ConvGeom{batch, in.h, in.w, in.c, d.cout, d.k, d.pad};  // h/w = output grid
+      f.k = d.k;
+      f.stride = d.stride;
+      f.w_count = static_cast<long long>(d.cout) * f.kpad;
+      f.w_off = off;
+      f.b_off = -1;  // folded into column k*k*cin of the filter
+      off = align_up(off + f.w_count, 4);
+      m->real_front += static_cast<long long>(d.cout) * d.k * d.k * d.cin + d.cout;
+      o.h = in.h; o.w = in.w; o.c = d.cout; o.pad = in.pad;
+      m->front.push_back(f);
+      m->acts.push_back(o);
+      continue;
+    }
     if (d.h != in.h || d.w != in.w) return fail("layer " + std::to_string(i) + ": input shape mismatch");
     if (d.kind == RALPB_CONV) {
       if (d.stride != 1 || d.k != 2 * d.pad + 1) return fail("conv layer " + std::to_string(i) + ": only stride-1 'same' convolutions are implemented");
@@ -119,6 +148,8 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
       if (!d.relu) return fail("conv layers must be followed by ReLU");
       if (d.cout % 16 != 0) return fail("conv output channels must be a multiple of 16");
       f.cin_real = d.cin;
+      f.k = d.k;
+      f.stride = 1;
       f.g = ConvGeom{batch, d.h, d.w, in.c, d.cout, d.k, d.pad};
       f.relu = 1;
       f.w_count = static_cast<long long>(d.cout) * d.k * d.k * in.c;
@@ -196,19 +227,22 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   cudaMemset(m->V, 0, m->n_total * sizeof(float));
   if (!(m->counters = alloc<uint32_t>(m, kNumCounters, why))) return fail(*why);
   cudaMemset(m->counters, 0, kNumCounters * sizeof(uint32_t));
-  long long max_act = 0;
+  // Every activation and activation-gradient buffer is dedicated and zeroed once: the conv
+  // kernels write interior pixels only, so the padding borders stay zero for the job's life.
+  m->gacts.assign(m->acts.size(), nullptr);
   for (size_t i = 0; i < m->acts.size(); ++i) {
-    if (i + 1 < m->acts.size() || true) {
-      if (!(m->acts[i].ptr = alloc<bf16>(m, m->acts[i].elems(), why))) return fail(*why);
-      if (i > 0) max_act = std::max(max_act, m->acts[i].elems());
+    const size_t bytes = static_cast<size_t>(m->acts[i].elems()) * sizeof(bf16);
+    if (!(m->acts[i].ptr = alloc<bf16>(m, m->acts[i].elems(), why))) return fail(*why);
+    cudaMemset(m->acts[i].ptr, 0, bytes);
+    if (i > 0 && i + 1 < m->acts.size()) {
+      if (!(m->gacts[i] = alloc<bf16>(m, m->acts[i].elems(), why))) return fail(*why);
+      cudaMemset(m->gacts[i], 0, bytes);
     }
   }
-  for (int g = 0; g < 2; ++g)
-    if (!(m->gbuf[g] = alloc<bf16>(m, max_act, why))) return fail(*why);
   for (auto& f : m->front) {
     if (f.kind != RALPB_CONV) continue;
     if (!(f.wf = alloc<bf16>(m, f.w_count, why))) return fail(*why);
-    if (!(f.wd = alloc<bf16>(m, f.w_count, why))) return fail(*why);
+    if (!f.im2col && !(f.wd = alloc<bf16>(m, f.w_count, why))) return fail(*why);
   }
   const int R = m->rows_back;
   for (size_t j = 0; j < m->back.size(); ++j) {
@@ -287,21 +321,29 @@ int model_set_params(Model* m, int layer, const float* w, const float* b, int on
   if (layer < m->split) {
     FrontLayer& f = m->front[layer];
     if (f.kind != RALPB_CONV) { *why = "layer has no parameters"; return 1; }
-    const int co = f.g.cout, taps = f.g.taps(), cp = f.g.cin, cr = f.cin_real;
-    if (cp == cr) {
-      RALPB_TRY(cudaMemcpyAsync(m->P + f.w_off, w, f.w_count * sizeof(float), kind, m->stream));
-    } else {
-      // pad input channels cr -> cp with zeros (host staging)
-      std::vector<float> host(static_cast<size_t>(co) * taps * cr), padded(f.w_count, 0.f);
-      RALPB_TRY(cudaMemcpy(host.data(), w, host.size() * sizeof(float), kind));
+    const int co = f.g.cout, taps = f.k * f.k, cr = f.cin_real;
+    const int kk = taps * cr;
+    std::vector<float> host(static_cast<size_t>(co) * kk), hb(co), packed(f.w_count, 0.f);
+    RALPB_TRY(cudaMemcpy(host.data(), w, host.size() * sizeof(float), kind));
+    RALPB_TRY(cudaMemcpy(hb.data(), b, co * sizeof(float), kind));
+    if (f.im2col) {  // [co][kpad]: taps*cin filter columns, then the bias column
+      for (int o = 0; o < co; ++o) {
+        for (int j = 0; j < kk; ++j) packed[static_cast<size_t>(o) * f.kpad + j] = host[static_cast<size_t>(o) * kk + j];
+        packed[static_cast<size_t>(o) * f.kpad + kk] = hb[o];
+      }
+    } else {  // [co][taps][cin_pad], padded input channels are zero
+      const int cp = f.g.cin;
       for (int o = 0; o < co; ++o)
         for (int t = 0; t < taps; ++t)
           for (int c = 0; c < cr; ++c)
-            padded[(static_cast<size_t>(o) * taps + t) * cp + c] = host[(static_cast<size_t>(o) * taps + t) * cr + c];
-      RALPB_TRY(cudaMemcpy(m->P + f.w_off, padded.data(), padded.size() * sizeof(float), cudaMemcpyHostToDevice));
+            packed[(static_cast<size_t>(o) * taps + t) * cp + c] = host[(static_cast<size_t>(o) * taps + t) * cr + c];
+      RALPB_TRY(cudaMemcpyAsync(m->P + f.b_off, hb.data(), co * sizeof(float), cudaMemcpyHostToDevice, m->stream));
     }
-    RALPB_TRY(cudaMemcpyAsync(m->P + f.b_off, b, co * sizeof(float), kind, m->stream));
-    RALPB_TRY(conv_weight_prep(m->P + f.w_off, co, taps, cp, f.wf, f.wd, m->stream));
+    RALPB_TRY(cudaMemcpyAsync(m->P + f.w_off, packed.data(), packed.size() * sizeof(float), cudaMemcpyHostToDevice, m->stream));
+    if (f.im2col)
+      RALPB_TRY(cast_bf16(m->P + f.w_off, f.w_count, f.wf, m->stream));
+    else
+      RALPB_TRY(conv_weight_prep(m->P + f.w_off, co, taps, f.g.cin, f.wf, f.wd, m->stream));
   } else {
     FcLayer& f = m->back[layer - m->split];
     RALPB_TRY(cudaMemcpyAsync(m->P + f.w_off, w, static_cast<size_t>(f.out) * f.in * sizeof(float), kind, m->stream));
@@ -319,16 +361,25 @@ int model_get_params(Model* m, int layer, float* w, float* b, int on_host, std::
   if (layer < m->split) {
     FrontLayer& f = m->front[layer];
     if (f.kind != RALPB_CONV) { *why = "layer has no parameters"; return 1; }
-    const int co = f.g.cout, taps = f.g.taps(), cp = f.g.cin, cr = f.cin_real;
-    std::vector<float> padded(f.w_count);
-    RALPB_TRY(cudaMemcpy(padded.data(), m->P + f.w_off, padded.size() * sizeof(float), cudaMemcpyDeviceToHost));
-    std::vector<float> host(static_cast<size_t>(co) * taps * cr);
-    for (int o = 0; o < co; ++o)
-      for (int t = 0; t < taps; ++t)
-        for (int c = 0; c < cr; ++c)
-          host[(static_cast<size_t>(o) * taps + t) * cr + c] = padded[(static_cast<size_t>(o) * taps + t) * cp + c];
+    const int co = f.g.cout, taps = f.k * f.k, cr = f.cin_real;
+    const int kk = taps * cr;
+    std::vector<float> packed(f.w_count), host(static_cast<size_t>(co) * kk), hb(co);
+    RALPB_TRY(cudaMemcpy(packed.data(), m->P + f.w_off, packed.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    if (f.im2col) {
+      for (int o = 0; o < co; ++o) {
+        for (int j = 0; j < kk; ++j) host[static_cast<size_t>(o) * kk + j] = packed[static_cast<size_t>(o) * f.kpad + j];
+        hb[o] = packed[static_cast<size_t>(o) * f.kpad + kk];
+      }
+    } else {
+      const int cp = f.g.cin;
+      for (int o = 0; o < co; ++o)
+        for (int t = 0; t < taps; ++t)
+          for (int c = 0; c < cr; ++c)
+            host[(static_cast<size_t>(o) * taps + t) * cr + c] = packed[(static_cast<size_t>(o) * taps + t) * cp + c];
+      RALPB_TRY(cudaMemcpy(hb.data(), m->P + f.b_off, co * sizeof(float), cudaMemcpyDeviceToHost));
+    }
     RALPB_TRY(cudaMemcpy(w, host.data(), host.size() * sizeof(float), cudaMemcpyDefault));
-    RALPB_TRY(cudaMemcpy(b, m->P + f.b_off, co * sizeof(float), cudaMemcpyDefault));
+    RALPB_TRY(cudaMemcpy(b, hb.data(), co * sizeof(float), cudaMemcpyDefault));
   } else {
     FcLayer& f = m->back[layer - m->split];
     RALPB_TRY(cudaMemcpy(w, m->P + f.w_off, static_cast<size_t>(f.out) * f.in * sizeof(float), cudaMemcpyDefault));
@@ -404,29 +455,37 @@ int launch_fc_backward(Model* m, const bf16* in, int R, bf16* dx_out, std::strin
 }
 
 int launch_front_backward(Model* m, const bf16* dcut, std::string* why) {
+  // cur = gradient w.r.t. the output of layer i (for a conv: already ReLU-masked, i.e. the
+  // pre-activation gradient); gacts[i] receives the gradient w.r.t. its input.
   const bf16* cur = dcut;
-  int ping = 0;
   for (int i = static_cast<int>(m->front.size()) - 1; i >= 0; --i) {
     FrontLayer& f = m->front[i];
     const ActBuf& in = m->acts[i];
     const ActBuf& out = m->acts[i + 1];
     if (f.kind == RALPB_POOL) {
-      bf16* dst = m->gbuf[ping];
+      bf16* dst = m->gacts[i];
       RALPB_TRY(maxpool_bwd(in.ptr, cur, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.pad, dst, m->stream));
       ++m->launches;
       cur = dst;
-      ping ^= 1;
+    } else if (f.im2col) {
+      // dW[co][j] += sum_rows dY[row][co] * patches[row][j]  (j = kpad incl. the bias column)
+      GemmDesc d;
+      d.M = f.g.cout; d.N = f.kpad; d.K = in.rows();
+      d.a_mode = LD_MN; d.a = Operand2D{cur, out.rows(), f.g.cout, f.g.cout};
+      d.b_mode = LD_MN; d.b = Operand2D{in.ptr, in.rows(), f.kpad, f.kpad};
+      d.k_splits = 0;
+      d.epi = EPI_F32_ATOMIC; d.out = m->G + f.w_off; d.s_m = f.kpad; d.s_n = 1;
+      RALPB_TRY(gemm_launch(d, m->stream, why));
+      ++m->launches;
     } else {
-      RALPB_TRY(conv_wgrad(f.g, in.ptr, cur, m->G + f.w_off, m->stream, why));
-      RALPB_TRY(colsum_bf16(cur, out.rows(), f.g.cout, f.g.cout, m->G + f.b_off, m->stream));
-      m->launches += 2;
+      RALPB_TRY(conv_wgrad(f.g, in.ptr, cur, m->G + f.w_off, m->G + f.b_off, m->stream, why));
+      ++m->launches;
       if (i > 0) {
-        bf16* dst = m->gbuf[ping];
+        bf16* dst = m->gacts[i];
         const bool mask = m->front[i - 1].kind == RALPB_CONV;
         RALPB_TRY(conv_dgrad(f.g, cur, f.wd, mask ? in.ptr : nullptr, dst, m->stream, why));
         ++m->launches;
         cur = dst;
-        ping ^= 1;
       }
     }
   }
@@ -437,7 +496,10 @@ int relayout_weights(Model* m, bool fc_too, std::string* why) {
   for (size_t i = 0; i < m->front.size(); ++i) {
     FrontLayer& f = m->front[i];
     if (f.kind != RALPB_CONV) continue;
-    RALPB_TRY(conv_weight_prep(m->P + f.w_off, f.g.cout, f.g.taps(), f.g.cin, f.wf, i > 0 ? f.wd : nullptr, m->stream));
+    if (f.im2col)
+      RALPB_TRY(cast_bf16(m->P + f.w_off, f.w_count, f.wf, m->stream));
+    else
+      RALPB_TRY(conv_weight_prep(m->P + f.w_off, f.g.cout, f.g.taps(), f.g.cin, f.wf, i > 0 ? f.wd : nullptr, m->stream));
     ++m->launches;
   }
   if (fc_too) {
@@ -511,7 +573,13 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
     img = m->img_dev;
     lab = m->lab_dev;
   }
-  RALPB_TRY(pack_input(img, b, m->in_h, m->in_w, m->in_c, m->acts[0].ptr, m->in_cp, m->acts[0].pad, s));
+  const FrontLayer& f0 = m->front[0];
+  const ActBuf& a0 = m->acts[0];
+  if (f0.im2col)
+    RALPB_TRY(pack_im2col(img, b, m->in_h, m->in_w, m->in_c, f0.k, f0.stride, m->desc[0].pad, a0.h, a0.w, a0.pad,
+                          f0.kpad, a0.ptr, s));
+  else
+    RALPB_TRY(pack_input(img, b, m->in_h, m->in_w, m->in_c, a0.ptr, m->in_cp, a0.pad, s));
   ++m->launches;
   const int slot = ralp ? m->rank : 0;          // this worker's row block in the PS input
   bf16* cut_dst = m->acts.back().ptr;
@@ -521,7 +589,18 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
     const ActBuf& in = m->acts[i];
     ActBuf out = m->acts[i + 1];
     if (i + 1 == m->front.size()) out.ptr = cut_dst;
-    if (f.kind == RALPB_CONV) {
+    if (f.im2col) {
+      // y = relu(patches . W^T) on the padded output grid (bias rides in the ones column)
+      GemmDesc d;
+      d.M = static_cast<int>(in.rows()); d.N = f.g.cout; d.K = f.kpad;
+      d.kb = std::min(64, f.kpad);
+      d.a = Operand2D{in.ptr, in.rows(), f.kpad, f.kpad};
+      d.b = Operand2D{f.wf, f.g.cout, f.kpad, f.kpad};
+      d.epi = EPI_BF16; d.relu = 1; d.out = out.ptr; d.s_m = f.g.cout;
+      d.border = 1; d.img_rows = (out.h + 2 * out.pad) * (out.w + 2 * out.pad); d.wp = out.w + 2 * out.pad;
+      d.pad = out.pad; d.h = out.h; d.w = out.w;
+      RALPB_TRY(gemm_launch(d, s, why));
+    } else if (f.kind == RALPB_CONV) {
       RALPB_TRY(conv_fwd(f.g, in.ptr, f.wf, m->P + f.b_off, out.ptr, 1, s, why));
     } else {
       RALPB_TRY(maxpool_fwd(in.ptr, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.ptr, out.pad, s));

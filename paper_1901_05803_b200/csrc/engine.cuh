@@ -30,6 +30,8 @@ struct FrontLayer {
   long long w_count = 0;           // cout*k*k*cin_pad
   bf16* wf = nullptr;          // forward filter [cout][k*k][cin]
   bf16* wd = nullptr;          // backward-data filter [cin][k*k][cout]
+  bool im2col = false;         // first conv as a GEMM over the im2col patch matrix acts[0]
+  int kpad = 0;                // im2col row width (k*k*cin + 1 bias column, padded)
 };
 
 struct FcLayer {
@@ -74,7 +76,7 @@ struct Model {
   bf16* dh[2] = {nullptr, nullptr};  // FC backward ping-pong
   float* row_loss = nullptr;
   float* loss = nullptr;
-  bf16* gbuf[2] = {nullptr, nullptr};  // conv backward ping-pong (max activation size)
+  std::vector<bf16*> gacts;        // gacts[i] = gradient w.r.t. acts[i] (dedicated, zero borders)
   float* img_dev = nullptr;        // staging for host images
   int32_t* lab_dev = nullptr;      // staging for host labels
   size_t arena_off_flags = 0, arena_off_P = 0, arena_off_G = 0, arena_off_xfc = 0, arena_off_lab = 0,

@@ -24,6 +24,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 static thread_local GemmTimer* g_timer = nullptr;
 void set_gemm_timer(GemmTimer* t) { g_timer = t; }
+GemmTimer* current_gemm_timer() { return g_timer; }
 
 int num_sms() {
   int dev = 0, n = 148;
@@ -146,11 +147,7 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
   }
   const long long total = static_cast<long long>(p.n_mt) * p.n_nt * p.n_ks;
   const int grid = static_cast<int>(std::min<long long>(total, sms));
-  GemmTimer* tm = g_timer;
-  const bool timed = tm != nullptr && tm->n < tm->cap;
-  if (timed) cudaEventRecord(tm->ev[2 * tm->n], stream);
-  gemm_sm100_kernel<<<grid, kThreads, smem, stream>>>(p);
-  if (timed) cudaEventRecord(tm->ev[2 * tm->n++ + 1], stream);
+  launch_timed([&] { gemm_sm100_kernel<<<grid, kThreads, smem, stream>>>(p); }, stream);
   return cudaGetLastError();
 }
 

@@ -51,5 +51,16 @@ struct GemmTimer {
   int n = 0;
 };
 void set_gemm_timer(GemmTimer* t);  // thread-local; nullptr disables
+GemmTimer* current_gemm_timer();
+
+// Launch `f` (a kernel launch on stream s) bracketed by the timer's events, if armed.
+template <class F>
+void launch_timed(F&& f, cudaStream_t s) {
+  GemmTimer* tm = current_gemm_timer();
+  const bool timed = tm != nullptr && tm->n < tm->cap;
+  if (timed) cudaEventRecord(tm->ev[2 * tm->n], s);
+  f();
+  if (timed) cudaEventRecord(tm->ev[2 * tm->n++ + 1], s);
+}
 
 }  // namespace ralpb

@@ -42,8 +42,8 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, a_mn: bool = False, b_mn: bool = F
 
 
 def conv_fwd(x_pad, w, bias, *, n, h, w_, cin, cout, k, pad, relu=True, out=None):
-    if out is None:
-        out = torch.empty(n, h + 2 * pad, w_ + 2 * pad, cout, dtype=_BF16, device=x_pad.device)
+    if out is None:  # interior-only writes: the padded border must start at zero
+        out = torch.zeros(n, h + 2 * pad, w_ + 2 * pad, cout, dtype=_BF16, device=x_pad.device)
     call("ralpb_conv_fwd", x_pad.data_ptr(), w.data_ptr(), _p(bias), out.data_ptr(), n, h, w_, cin, cout,
          k, pad, int(relu), _stream())
     return out
@@ -51,16 +51,17 @@ def conv_fwd(x_pad, w, bias, *, n, h, w_, cin, cout, k, pad, relu=True, out=None
 
 def conv_dgrad(dy_pad, wd, mask_pad, *, n, h, w_, cin, cout, k, pad, out=None):
     if out is None:
-        out = torch.empty(n, h + 2 * pad, w_ + 2 * pad, cin, dtype=_BF16, device=dy_pad.device)
+        out = torch.zeros(n, h + 2 * pad, w_ + 2 * pad, cin, dtype=_BF16, device=dy_pad.device)
     call("ralpb_conv_dgrad", dy_pad.data_ptr(), wd.data_ptr(), _p(mask_pad), out.data_ptr(), n, h, w_, cin,
          cout, k, pad, _stream())
     return out
 
 
-def conv_wgrad(x_pad, dy_pad, *, n, h, w_, cin, cout, k, pad, out=None):
+def conv_wgrad(x_pad, dy_pad, *, n, h, w_, cin, cout, k, pad, out=None, db=None):
+    """dW[co][t][ci] (+= into `out`) and, when `db` is given, the bias gradient (+= into db)."""
     if out is None:
         out = torch.zeros(cout, k * k, cin, dtype=torch.float32, device=x_pad.device)
-    call("ralpb_conv_wgrad", x_pad.data_ptr(), dy_pad.data_ptr(), out.data_ptr(), n, h, w_, cin, cout, k,
+    call("ralpb_conv_wgrad", x_pad.data_ptr(), dy_pad.data_ptr(), out.data_ptr(), _p(db), n, h, w_, cin, cout, k,
          pad, _stream())
     return out
 
@@ -69,6 +70,14 @@ def pack_input(x, cp, pad):
     n, h, w, c = x.shape
     out = torch.empty(n, h + 2 * pad, w + 2 * pad, cp, dtype=_BF16, device=x.device)
     call("ralpb_pack_input", x.data_ptr(), n, h, w, c, out.data_ptr(), cp, pad, _stream())
+    return out
+
+
+def pack_im2col(x, *, k, stride, pad, po, kpad):
+    n, h, w, c = x.shape
+    ho, wo = (h + 2 * pad - k) // stride + 1, (w + 2 * pad - k) // stride + 1
+    out = torch.empty(n, ho + 2 * po, wo + 2 * po, kpad, dtype=_BF16, device=x.device)
+    call("ralpb_pack_im2col", x.data_ptr(), n, h, w, c, k, stride, pad, ho, wo, po, kpad, out.data_ptr(), _stream())
     return out
 
 

@@ -67,6 +67,9 @@ CONV_CASES = [
     (3, 20, 12, 16, 64, 3, 1),
     (2, 32, 32, 32, 64, 5, 2),
     (2, 32, 32, 16, 32, 5, 2),
+    (2, 56, 56, 128, 256, 3, 1),
+    (3, 30, 17, 64, 128, 3, 1),
+    (1, 112, 112, 64, 64, 3, 1),
 ]
 
 
@@ -112,12 +115,35 @@ def test_conv_wgrad(case):
     g = torch.Generator(device=DEV).manual_seed(5)
     x = _pad(_bf(n, h, w, cin, gen=g), pad).contiguous()
     dy = _pad(_bf(n, h, w, cout, gen=g), pad).contiguous()
-    dw = ops.conv_wgrad(x, dy, n=n, h=h, w_=w, cin=cin, cout=cout, k=k, pad=pad)
+    db = torch.zeros(cout, device=DEV)
+    dw = ops.conv_wgrad(x, dy, n=n, h=h, w_=w, cin=cin, cout=cout, k=k, pad=pad, db=db)
     xr = x[:, pad:pad + h, pad:pad + w, :].permute(0, 3, 1, 2).float()
     dyr = dy[:, pad:pad + h, pad:pad + w, :].permute(0, 3, 1, 2).float()
     ref = torch.nn.grad.conv2d_weight(xr, (cout, cin, k, k), dyr, padding=pad)  # [co, ci, k, k]
     ref = ref.permute(0, 2, 3, 1).reshape(cout, k * k, cin)
     _close(dw, ref, rtol=1e-3, atol=1e-3 * ref.abs().max().item())
+    _close(db, dyr.sum(dim=(0, 2, 3)), rtol=1e-3, atol=1e-3 * dyr.abs().sum(dim=(0, 2, 3)).max().item())
+
+
+@pytest.mark.parametrize("case", [c for c in CONV_CASES if c[3] >= 32])
+def test_slab_matches_flat_path(case, monkeypatch):
+    """The slab-tiled kernels (default) and the single-tap-load kernels agree."""
+    n, h, w, cin, cout, k, pad = case
+    g = torch.Generator(device=DEV).manual_seed(9)
+    x = _pad(torch.relu(_bf(n, h, w, cin, gen=g).float()).to(torch.bfloat16), pad).contiguous()
+    wt = _bf(cout, k * k, cin, scale=(2.0 / (k * k * cin)) ** 0.5, gen=g)
+    wd = _bf(cin, k * k, cout, scale=(2.0 / (k * k * cout)) ** 0.5, gen=g)
+    dy = _pad(_bf(n, h, w, cout, gen=g), pad).contiguous()
+    res = {}
+    for mode in ("slab", "flat"):
+        monkeypatch.setenv("RALPB_CONV", mode)
+        y = ops.conv_fwd(x, wt, None, n=n, h=h, w_=w, cin=cin, cout=cout, k=k, pad=pad, relu=True)
+        dx = ops.conv_dgrad(dy, wd, x, n=n, h=h, w_=w, cin=cin, cout=cout, k=k, pad=pad)
+        dw = ops.conv_wgrad(x, dy, n=n, h=h, w_=w, cin=cin, cout=cout, k=k, pad=pad)
+        torch.cuda.synchronize()
+        res[mode] = (y, dx, dw)
+    for a, b in zip(res["slab"], res["flat"]):
+        _close(a, b, rtol=1e-2)
 
 
 def test_pool_fwd_bwd():
@@ -159,3 +185,32 @@ def test_sgd_and_colsum():
     torch.testing.assert_close(p, p0 - 0.01 * v_ref)
     dy = _bf(5000, 192, gen=g)
     torch.testing.assert_close(ops.colsum(dy), dy.float().sum(0), rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("k,stride,pad,po,kpad,h", [(3, 1, 1, 1, 32, 20), (5, 1, 2, 0, 128, 16), (11, 4, 0, 0, 384, 63)])
+def test_first_conv_im2col(k, stride, pad, po, kpad, h):
+    """First (RGB) conv as pack_im2col + GEMM with the bias folded into a ones column (fwd) and
+    the filter/bias gradient as one MN x MN GEMM."""
+    g = torch.Generator(device=DEV).manual_seed(11)
+    n, c, cout = 2, 3, 64
+    x = torch.randn(n, h, h, c, generator=g, device=DEV)
+    cols = ops.pack_im2col(x, k=k, stride=stride, pad=pad, po=po, kpad=kpad)
+    kk = k * k * c
+    w = torch.randn(cout, k, k, c, generator=g, device=DEV) * (2.0 / kk) ** 0.5
+    b = torch.randn(cout, generator=g, device=DEV) * 0.1
+    wp = torch.zeros(cout, kpad, device=DEV)
+    wp[:, :kk] = w.reshape(cout, kk)
+    wp[:, kk] = b
+    wb = wp.to(torch.bfloat16)
+    rows = cols.shape[0] * cols.shape[1] * cols.shape[2]
+    y = ops.gemm(cols.view(rows, kpad), wb.contiguous(), relu=True).view(*cols.shape[:3], cout)
+    ho = cols.shape[1] - 2 * po
+    xr = x.to(torch.bfloat16).float().permute(0, 3, 1, 2)
+    ref = torch.relu(F.conv2d(xr, wb[:, :kk].float().view(cout, k, k, c).permute(0, 3, 1, 2),
+                              wb[:, kk].float(), stride=stride, padding=pad)).permute(0, 2, 3, 1)
+    _close(y[:, po:po + ho, po:po + ho, :], ref)
+    dy = _bf(*cols.shape[:3], cout, gen=g)
+    dw = ops.gemm(dy.view(rows, cout), cols.view(rows, kpad), a_mn=True, b_mn=True, out_kind="f32_atomic",
+                  k_splits=0)
+    refdw = dy.view(rows, cout).float().t() @ cols.view(rows, kpad).float()
+    _close(dw, refdw, rtol=1e-3, atol=1e-3 * refdw.abs().max().item())
