@@ -1,6 +1,7 @@
 #include <algorithm>
 #include "elementwise.cuh"
 #include "gemm_host.cuh"
+#include "ptx.cuh"
 
 namespace ralpb {
 
@@ -196,11 +197,67 @@ __global__ void maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ x,
   }
 }
 
+// Disjoint windows (stride == window == K): one thread per output window x 8 channels reads
+// the K*K inputs and dy once and writes the K*K input gradients.  Positions no window covers
+// and the padding border are never written (the executor's gradient buffers are zeroed once).
+template <int K>
+__global__ void maxpool_bwd_disjoint_kernel(const __nv_bfloat16* __restrict__ x,
+                                            const __nv_bfloat16* __restrict__ dy, int n, int h, int w, int c,
+                                            int pi, int po, int oh, int ow, __nv_bfloat16* __restrict__ dx) {
+  const int cv = c >> 3;
+  const int total = n * oh * ow * cv;
+  const int hp = h + 2 * pi, wp = w + 2 * pi;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int cg = i % cv;
+    int t = i / cv;
+    const int ox = t % ow;
+    t /= ow;
+    const int oy = t % oh;
+    const int img = t / oh;
+    const long long base = ((static_cast<long long>(img) * hp + oy * K + pi) * wp + ox * K + pi) * c + cg * 8;
+    const long long dyo = ((static_cast<long long>(img) * (oh + 2 * po) + oy + po) * (ow + 2 * po) + ox + po) * c + cg * 8;
+    uint4 xv[K * K];
+#pragma unroll
+    for (int q = 0; q < K * K; ++q)
+      xv[q] = *reinterpret_cast<const uint4*>(x + base + (static_cast<long long>(q / K) * wp + q % K) * c);
+    const uint4 dv = *reinterpret_cast<const uint4*>(dy + dyo);
+    const __nv_bfloat16* db = reinterpret_cast<const __nv_bfloat16*>(&dv);
+    int arg[8];
+    float best[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { best[e] = -INFINITY; arg[e] = -1; }
+#pragma unroll
+    for (int q = 0; q < K * K; ++q) {
+      const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(&xv[q]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float v = __bfloat162float(xb[e]);
+        if (v > best[e]) { best[e] = v; arg[e] = q; }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < K * K; ++q) {
+      const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(&xv[q]);
+      uint4 out;
+      __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&out);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        ob[e] = (arg[e] == q && __bfloat162float(xb[e]) > 0.f) ? db[e] : __float2bfloat16_rn(0.f);
+      *reinterpret_cast<uint4*>(dx + base + (static_cast<long long>(q / K) * wp + q % K) * c) = out;
+    }
+  }
+}
+
 cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* dy, int n, int h, int w,
                         int c, int pad_in, int k, int st, int pad_out, __nv_bfloat16* dx,
                         cudaStream_t s) {
   if (c % 8 != 0) return cudaErrorInvalidValue;
   int oh = (h - k) / st + 1, ow = (w - k) / st + 1;
+  const long long windows = static_cast<long long>(n) * oh * ow * (c / 8);
+  if (k == st && k == 2 && windows < (1LL << 31)) {
+    maxpool_bwd_disjoint_kernel<2><<<grid_for(windows, 256), 256, 0, s>>>(x, dy, n, h, w, c, pad_in, pad_out, oh, ow, dx);
+    return cudaGetLastError();
+  }
   long long total = static_cast<long long>(n) * (h + 2 * pad_in) * (w + 2 * pad_in) * (c / 8);
   maxpool_bwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, dy, n, h, w, c, pad_in, k, st, pad_out, oh, ow, dx);
   return cudaGetLastError();
@@ -270,8 +327,10 @@ cudaError_t reduce_sum(const float* x, int n, float scale, float* out, cudaStrea
 }
 
 // ------------------------------------------------------------------ SGD momentum
+// Optionally also writes the bf16 copy of the updated parameters (the GEMM operand), so the
+// fp32 master is not re-read by a separate cast.
 __global__ void sgd_kernel(float* __restrict__ p, float* __restrict__ v, const float* __restrict__ g,
-                           long long n, float lr, float mu, float gs) {
+                           long long n, float lr, float mu, float gs, __nv_bfloat16* __restrict__ out) {
   long long n4 = n / 4;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -284,18 +343,30 @@ __global__ void sgd_kernel(float* __restrict__ p, float* __restrict__ v, const f
     vv.w = mu * vv.w + gs * gv.w; pv.w -= lr * vv.w;
     reinterpret_cast<float4*>(v)[i] = vv;
     reinterpret_cast<float4*>(p)[i] = pv;
+    if (out != nullptr) {
+      uint2 b;
+      b.x = pack_bf16(pv.x, pv.y);
+      b.y = pack_bf16(pv.z, pv.w);
+      reinterpret_cast<uint2*>(out)[i] = b;
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
     long long i = n4 * 4 + threadIdx.x;
     v[i] = mu * v[i] + gs * g[i];
     p[i] -= lr * v[i];
+    if (out != nullptr) out[i] = __float2bfloat16_rn(p[i]);
   }
 }
 
 cudaError_t sgd_momentum(float* p, float* v, const float* g, long long n, float lr, float mu,
                          float gscale, cudaStream_t s) {
+  return sgd_momentum_bf16(p, v, g, n, lr, mu, gscale, nullptr, s);
+}
+
+cudaError_t sgd_momentum_bf16(float* p, float* v, const float* g, long long n, float lr, float mu,
+                              float gscale, __nv_bfloat16* out, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  sgd_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(p, v, g, n, lr, mu, gscale);
+  sgd_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(p, v, g, n, lr, mu, gscale, out);
   return cudaGetLastError();
 }
 
@@ -315,7 +386,19 @@ __global__ void colsum_kernel(const __nv_bfloat16* __restrict__ dy, long long ro
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.f;
   if (valid) {
-    for (long long r = r0 + ty; r < r1; r += 8) {
+    long long r = r0 + ty;
+    for (; r + 24 < r1; r += 32) {  // four independent 16-byte loads in flight
+      uint4 u[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) u[q] = *reinterpret_cast<const uint4*>(dy + (r + 8 * q) * ld + cg * 8);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&u[q]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += __bfloat162float(hb[e]);
+      }
+    }
+    for (; r < r1; r += 8) {
       uint4 u = *reinterpret_cast<const uint4*>(dy + r * ld + cg * 8);
       const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&u);
 #pragma unroll

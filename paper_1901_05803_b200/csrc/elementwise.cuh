@@ -42,6 +42,9 @@ cudaError_t reduce_sum(const float* x, int n, float scale, float* out, cudaStrea
 // v = mu*v + gscale*g ; p -= lr*v  (PyTorch SGD-momentum form, no dampening/decay).
 cudaError_t sgd_momentum(float* p, float* v, const float* g, long long n, float lr, float mu,
                          float gscale, cudaStream_t s);
+// Same, also writing bf16(p) to `out` (may be null).
+cudaError_t sgd_momentum_bf16(float* p, float* v, const float* g, long long n, float lr, float mu,
+                              float gscale, __nv_bfloat16* out, cudaStream_t s);
 
 // db[c] += sum_r dy[r][c]   (bf16 input, fp32 atomics into db).
 cudaError_t colsum_bf16(const __nv_bfloat16* dy, long long rows, int c, long long ld, float* db,

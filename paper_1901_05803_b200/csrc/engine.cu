@@ -648,12 +648,12 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
     if (launch_fc_backward(m, in, R, m->dx_fc, why)) return 1;
     if (ralp) {
       // FC tail update stays on the PS (never synchronised)
-      const long long nb = m->n_total - m->n_front;
-      RALPB_TRY(sgd_momentum(m->P + m->n_front, m->V + m->n_front, m->G + m->n_front, nb, lr, mu, 1.f, s));
-      ++m->launches;
+      // SGD on each FC layer's weights also refreshes its bf16 GEMM copy (one pass over P)
       for (auto& f : m->back) {
-        RALPB_TRY(cast_bf16(m->P + f.w_off, static_cast<long long>(f.out) * f.in, f.wbf, s));
-        ++m->launches;
+        const long long nw = static_cast<long long>(f.out) * f.in;
+        RALPB_TRY(sgd_momentum_bf16(m->P + f.w_off, m->V + f.w_off, m->G + f.w_off, nw, lr, mu, 1.f, f.wbf, s));
+        RALPB_TRY(sgd_momentum(m->P + f.b_off, m->V + f.b_off, m->G + f.b_off, f.out, lr, mu, 1.f, s));
+        m->launches += 2;
       }
       // return every remote worker's rows of the cut gradient
       for (int r = 0; r < m->world; ++r) {

@@ -89,7 +89,7 @@ def maxpool_fwd(x_pad, *, n, h, w, c, pad_in, k, stride, pad_out):
 
 
 def maxpool_bwd(x_pad, dy, *, n, h, w, c, pad_in, k, stride, pad_out):
-    dx = torch.empty_like(x_pad)
+    dx = torch.zeros_like(x_pad)  # borders / uncovered positions are not written
     call("ralpb_maxpool_bwd", x_pad.data_ptr(), dy.data_ptr(), n, h, w, c, pad_in, k, stride, pad_out,
          dx.data_ptr(), _stream())
     return dx
