@@ -100,8 +100,8 @@ cudaError_t conv_wgrad_flat(const ConvGeom& g, const void* x_pad, const void* dy
 }
 
 // Kernel family per call: RALPB_CONV=slab|flat forces one (A/B comparisons); the default
-// picks by shape from measurements (tools/probe_conv.py): the slab kernels win where the
-// image is large relative to the 16x8 pixel tile.
+// uses the slab kernels wherever they apply (they win at every VGG-16 shape once the MMA
+// issue loop uses compile-time descriptor offsets; tools/probe_conv.py).
 enum class Family { kAuto, kSlab, kFlat };
 static Family family() {
   const char* e = getenv("RALPB_CONV");
@@ -120,21 +120,21 @@ static bool pick_slab(bool eligible, bool auto_choice) {
 
 cudaError_t conv_fwd(const ConvGeom& g, const void* x_pad, const void* w, const float* bias, void* y_pad,
                      int relu, cudaStream_t s, std::string* why) {
-  if (pick_slab(slab_fwd_ok(g, g.cin, g.cout), g.h >= 64 || g.cin < 64))
+  if (pick_slab(slab_fwd_ok(g, g.cin, g.cout), true))
     return conv_slab_fwd(g, x_pad, w, g.cin, g.cout, bias, relu, nullptr, y_pad, s, why);
   return conv_fwd_flat(g, x_pad, w, bias, y_pad, relu, s, why);
 }
 
 cudaError_t conv_dgrad(const ConvGeom& g, const void* dy_pad, const void* wd, const void* mask_pad,
                        void* dx_pad, cudaStream_t s, std::string* why) {
-  if (pick_slab(slab_fwd_ok(g, g.cout, g.cin), g.h >= 64 || g.cout < 64))
+  if (pick_slab(slab_fwd_ok(g, g.cout, g.cin), true))
     return conv_slab_fwd(g, dy_pad, wd, g.cout, g.cin, nullptr, 0, mask_pad, dx_pad, s, why);
   return conv_dgrad_flat(g, dy_pad, wd, mask_pad, dx_pad, s, why);
 }
 
 cudaError_t conv_wgrad(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw, float* db,
                        cudaStream_t s, std::string* why) {
-  if (pick_slab(slab_wgrad_ok(g), g.h >= 56)) return conv_slab_wgrad(g, x_pad, dy_pad, dw, db, s, why);
+  if (pick_slab(slab_wgrad_ok(g), true)) return conv_slab_wgrad(g, x_pad, dy_pad, dw, db, s, why);
   cudaError_t e = conv_wgrad_flat(g, x_pad, dy_pad, dw, s, why);
   if (e != cudaSuccess || db == nullptr) return e;
   return colsum_bf16(static_cast<const __nv_bfloat16*>(dy_pad), g.q(), g.cout, g.cout, db, s);

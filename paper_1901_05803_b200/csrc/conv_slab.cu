@@ -1,6 +1,7 @@
 // Host planning / launch of the slab-tiled conv kernels (see conv_slab.cuh).
 #include <cudaTypedefs.h>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include "conv.cuh"
 #include "conv_slab.cuh"
@@ -58,7 +59,7 @@ constexpr int kSmemBudget = 227 * 1024 - 1024 - 512;
 }  // namespace
 
 bool slab_fwd_ok(const ConvGeom& g, int c, int cout) {
-  return g.k == 2 * g.pad + 1 && g.taps() <= kSlabMaxTaps && (c == 16 || c == 32 || c % 64 == 0) && cout % 16 == 0 &&
+  return g.k == 2 * g.pad + 1 && (g.k == 3 || g.k == 5) && (c == 16 || c == 32 || c % 64 == 0) && cout % 16 == 0 &&
          g.q() < (1LL << 31);
 }
 
@@ -68,7 +69,6 @@ bool slab_wgrad_ok(const ConvGeom& g) {
 
 cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, int c, int cout, const float* bias,
                           int relu, const void* mask_pad, void* y_pad, cudaStream_t s, std::string* why) {
-  static bool attr[3] = {false, false, false};
   SlabConvParams p;
   std::memset(&p, 0, sizeof(p));
   p.n = g.n; p.h = g.h; p.w = g.w; p.hp = g.hp(); p.wp = g.wp(); p.pad = g.pad; p.k = g.k; p.taps = g.taps();
@@ -88,6 +88,24 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
   p.b_stage = align1k(p.b_load);
   p.na = 2;
   p.nb = std::min(8, (kSmemBudget - p.na * p.slab_stage) / p.b_stage);
+  // Filters resident in shared memory when one channel block and one N tile cover the layer
+  // (e.g. 64->64 at 224x224): the per-tile filter reloads disappear.
+  if (c == p.kb && cout <= p.bn && p.macc >= 2) {
+    const int macc2 = 2;
+    const int slab2 = align1k(p.row_bytes * p.sw * (16 * macc2 + g.k - 1));
+    const int na2 = 3;
+    if (g.taps() * p.b_stage + na2 * slab2 <= kSmemBudget && g.taps() <= 16) {
+      p.wres = 1;
+      p.macc = macc2;
+      p.sh = 16 * macc2 + g.k - 1;
+      p.slab_load = p.row_bytes * p.sw * p.sh;
+      p.slab_stage = slab2;
+      p.na = na2;
+      p.nb = g.taps();
+      p.acc_bufs = 2;
+      p.tmem_cols = p.macc * p.bn * 2 <= 256 ? 256 : 512;
+    }
+  }
   if (p.nb < 2) { *why = "slab conv: tile does not fit in shared memory"; return cudaErrorInvalidValue; }
   p.n_hb = (g.h + 16 * p.macc - 1) / (16 * p.macc);
   p.n_wb = (g.w + 7) / 8;
@@ -97,6 +115,7 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
   p.bias = bias;
   p.relu = relu;
   p.mask = static_cast<const __nv_bfloat16*>(mask_pad);
+  if (const char* e = getenv("RALPB_DEBUG")) p.dbg = atoi(e);
   if (!encode_act(&p.tmX, x_pad, c, g.wp(), g.hp(), g.n, p.kb, p.sw, p.sh, p.row_bytes, why))
     return cudaErrorInvalidValue;
   if (!encode_mat(&p.tmB, w, cout, static_cast<long long>(g.taps()) * c, p.kb, p.bn, p.row_bytes, why))
@@ -104,13 +123,23 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
   const int smem = 1024 + p.na * p.slab_stage + p.nb * p.b_stage + 512;
   const long long total = static_cast<long long>(g.n) * p.n_hb * p.n_wb * p.n_nt;
   const int grid = static_cast<int>(std::min<long long>(total, num_sms()));
-  if (p.macc >= 2) {
-    if (!attr[2]) { cudaFuncSetAttribute(conv_slab_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); attr[2] = true; }
-    launch_timed([&] { conv_slab_fwd_kernel<2><<<grid, 384, smem, s>>>(p); }, s);
-  } else {
-    if (!attr[1]) { cudaFuncSetAttribute(conv_slab_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); attr[1] = true; }
-    launch_timed([&] { conv_slab_fwd_kernel<1><<<grid, 256, smem, s>>>(p); }, s);
-  }
+  const int ks = p.kb / 16;
+  bool launched = false;
+  auto go = [&](auto kern, int threads) {
+    static_cast<void>(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    launch_timed([&] { kern<<<grid, threads, smem, s>>>(p); }, s);
+    launched = true;
+  };
+#define RALPB_SLAB_CASE(KK, KS, MA)                                            \
+  if (g.k == KK && ks == KS && p.macc == MA) go(conv_slab_fwd_kernel<KK, KS, MA>, 128 + 128 * (MA >= 2 ? 2 : 1));
+  RALPB_SLAB_CASE(3, 4, 1) RALPB_SLAB_CASE(3, 4, 2) RALPB_SLAB_CASE(3, 4, 4)
+  RALPB_SLAB_CASE(3, 2, 1) RALPB_SLAB_CASE(3, 2, 2) RALPB_SLAB_CASE(3, 2, 4)
+  RALPB_SLAB_CASE(3, 1, 1) RALPB_SLAB_CASE(3, 1, 2) RALPB_SLAB_CASE(3, 1, 4)
+  RALPB_SLAB_CASE(5, 4, 1) RALPB_SLAB_CASE(5, 4, 2) RALPB_SLAB_CASE(5, 4, 4)
+  RALPB_SLAB_CASE(5, 2, 1) RALPB_SLAB_CASE(5, 2, 2) RALPB_SLAB_CASE(5, 2, 4)
+  RALPB_SLAB_CASE(5, 1, 1) RALPB_SLAB_CASE(5, 1, 2) RALPB_SLAB_CASE(5, 1, 4)
+#undef RALPB_SLAB_CASE
+  if (!launched) { *why = "slab conv: no kernel instance for this filter/channel/tile shape"; return cudaErrorInvalidValue; }
   return cudaGetLastError();
 }
 

@@ -62,11 +62,19 @@ struct alignas(64) SlabConvParams {
   float* dw;
   float* db;
   int n_ci_blocks, n_co_blocks, n_splits, blocks_per_split, n_pix_blocks;
+  int dbg;              // experiments: bit0 skip epilogue stores, bit1 skip MMAs
+  int wres;             // filters resident in smem: B stage t holds tap t, loaded once per CTA
 };
 
 // ------------------------------------------------------------------ forward / backward-data
-template <int EWG>
-__global__ void __launch_bounds__(128 + 128 * EWG, 1) conv_slab_fwd_kernel(const __grid_constant__ SlabConvParams p) {
+// Template parameters fix the filter size, the k-steps per channel block and the M
+// accumulators so that every UMMA descriptor in the issue loop is a base plus a
+// compile-time offset (a descriptor computed at run time costs ~100+ cycles of issue
+// latency per MMA; tools/exp_mma.cu).
+template <int K, int KSTEPS, int MACC>
+__global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
+    conv_slab_fwd_kernel(const __grid_constant__ SlabConvParams p) {
+  constexpr int EWG = MACC >= 2 ? 2 : 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -98,10 +106,13 @@ __global__ void __launch_bounds__(128 + 128 * EWG, 1) conv_slab_fwd_kernel(const
   const int ksteps = p.kb / 16;
   const int mrows = 16 * p.macc;
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 2 || warp == 3) {
+    // Producers: warp 0 streams the activation slabs, warps 2 and 3 take alternate filter
+    // tiles (a TMA issue occupies its thread for hundreds of cycles; see tools/exp_tma.cu).
     if (lane == 0) {
       int as = 0, bs = 0;
       uint32_t aph = 0, bph = 0;
+      int bseq = 0;
       for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
         int t = wi;
         const int nt = t % p.n_nt; t /= p.n_nt;
@@ -110,54 +121,76 @@ __global__ void __launch_bounds__(128 + 128 * EWG, 1) conv_slab_fwd_kernel(const
         const int img = t / p.n_hb;
         const int h0 = hb * mrows, w0 = wb * 8;
         for (int cb = 0; cb < cblks; ++cb) {
-          mbar_wait(&a_empty[as], aph ^ 1);
-          mbar_expect_tx(&a_full[as], p.slab_load);
-          tma_load_4d(sA + as * p.slab_stage, &p.tmX, &a_full[as], cb * p.kb, w0, h0, img);
-          if (++as == p.na) { as = 0; aph ^= 1; }
-          for (int tap = 0; tap < p.taps; ++tap) {
-            mbar_wait(&b_empty[bs], bph ^ 1);
-            mbar_expect_tx(&b_full[bs], p.b_load);
-            tma_load_2d(sB + bs * p.b_stage, &p.tmB, &b_full[bs], tap * p.c + cb * p.kb, nt * p.bn);
+          if (warp == 0) {
+            mbar_wait(&a_empty[as], aph ^ 1);
+            mbar_expect_tx(&a_full[as], p.slab_load);
+            tma_load_4d(sA + as * p.slab_stage, &p.tmX, &a_full[as], cb * p.kb, w0, h0, img);
+            if (++as == p.na) { as = 0; aph ^= 1; }
+            continue;
+          }
+          if (p.wres) {  // whole filter bank once per CTA (single channel block, single N tile)
+            if (wi == static_cast<int>(blockIdx.x))
+              for (int tap = warp - 2; tap < p.taps; tap += 2) {
+                mbar_expect_tx(&b_full[tap], p.b_load);
+                tma_load_2d(sB + tap * p.b_stage, &p.tmB, &b_full[tap], tap * p.c, 0);
+              }
+            continue;
+          }
+          for (int tap = 0; tap < p.taps; ++tap, ++bseq) {
+            if ((bseq & 1) == (warp - 2)) {
+              mbar_wait(&b_empty[bs], bph ^ 1);
+              mbar_expect_tx(&b_full[bs], p.b_load);
+              tma_load_2d(sB + bs * p.b_stage, &p.tmB, &b_full[bs], tap * p.c + cb * p.kb, nt * p.bn);
+            }
             if (++bs == p.nb) { bs = 0; bph ^= 1; }
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      int as = 0, bs = 0, acc = 0;
-      uint32_t aph = 0, bph = 0, acc_ph = 0;
-      const uint32_t sbo = p.sw * p.row_bytes;
-      for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
-        mbar_wait(&tempty[acc], acc_ph ^ 1);
+    constexpr int SW = 8 + K - 1;       // slab width (pixels)
+    constexpr int RB = KSTEPS * 32;     // slab row bytes
+    constexpr int TAPS = K * K;
+    int as = 0, bs = 0, acc = 0;
+    uint32_t aph = 0, bph = 0, acc_ph = 0;
+    const uint64_t a0 = umma_smem_desc(smem_u32(sA), 16, SW * RB, RB);
+    const uint64_t b0 = umma_smem_desc(smem_u32(sB), 16, 8 * RB, RB);
+    const bool issue = !(p.dbg & 2);
+    for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_ph ^ 1);
+      tc_fence_after();
+      const uint32_t d0 = tmem_base + acc * MACC * p.bn;
+      for (int cb = 0; cb < cblks; ++cb) {
+        mbar_wait(&a_full[as], aph);
         tc_fence_after();
-        const uint32_t d0 = tmem_base + acc * p.macc * p.bn;
-        for (int cb = 0; cb < cblks; ++cb) {
-          mbar_wait(&a_full[as], aph);
+        const uint64_t ad = desc_add(a0, as * p.slab_stage);
+#pragma unroll
+        for (int tap = 0; tap < TAPS; ++tap) {
+          const int bst = p.wres ? tap : bs;
+          mbar_wait(&b_full[bst], p.wres ? 0u : bph);
           tc_fence_after();
-          const uint32_t slab = smem_u32(sA + as * p.slab_stage);
-          for (int tap = 0; tap < p.taps; ++tap) {
-            const int r = tap / p.k, s = tap - (tap / p.k) * p.k;
-            mbar_wait(&b_full[bs], bph);
-            tc_fence_after();
-            const uint32_t bbase = smem_u32(sB + bs * p.b_stage);
-            for (int a = 0; a < p.macc; ++a) {
-              const uint32_t arow = static_cast<uint32_t>((a * 16 + r) * p.sw + s);
-              for (int ks = 0; ks < ksteps; ++ks) {
-                const uint64_t ad = umma_smem_desc(slab + arow * p.row_bytes + ks * 32, 16, sbo, p.row_bytes);
-                const uint64_t bd = umma_smem_desc(bbase + ks * 32, 16, 8 * p.row_bytes, p.row_bytes);
-                umma_bf16(d0 + a * p.bn, ad, bd, p.idesc, (cb > 0 || tap > 0 || ks > 0) ? 1u : 0u);
-              }
+          const uint64_t bd = desc_add(b0, bst * p.b_stage);
+          if (elect_one()) {
+            if (issue) {
+#pragma unroll
+              for (int a = 0; a < MACC; ++a)
+#pragma unroll
+                for (int ks = 0; ks < KSTEPS; ++ks)
+                  umma_bf16(d0 + a * p.bn, desc_add(ad, ((a * 16 + tap / K) * SW + tap % K) * RB + ks * 32),
+                            desc_add(bd, ks * 32), p.idesc, (cb > 0 || tap > 0 || ks > 0) ? 1u : 0u);
             }
-            umma_commit(&b_empty[bs]);
-            if (++bs == p.nb) { bs = 0; bph ^= 1; }
+            if (!p.wres) umma_commit(&b_empty[bs]);
           }
-          umma_commit(&a_empty[as]);
-          if (++as == p.na) { as = 0; aph ^= 1; }
+          __syncwarp();
+          if (!p.wres && ++bs == p.nb) { bs = 0; bph ^= 1; }
         }
-        umma_commit(&tfull[acc]);
-        if (++acc == p.acc_bufs) { acc = 0; acc_ph ^= 1; }
+        if (elect_one()) umma_commit(&a_empty[as]);
+        __syncwarp();
+        if (++as == p.na) { as = 0; aph ^= 1; }
       }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+      if (++acc == p.acc_bufs) { acc = 0; acc_ph ^= 1; }
     }
   } else if (warp >= 4) {
     const int g = (warp - 4) >> 2;   // epilogue warpgroup
@@ -184,7 +217,7 @@ __global__ void __launch_bounds__(128 + 128 * EWG, 1) conv_slab_fwd_kernel(const
           tmem_ld32(tb + c, rr);
           tmem_wait_ld();
           const int n0 = nt * p.bn + c;
-          if (!valid || n0 >= p.cout) continue;
+          if (!valid || n0 >= p.cout || (p.dbg & 1)) continue;
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
@@ -210,7 +243,7 @@ __global__ void __launch_bounds__(128 + 128 * EWG, 1) conv_slab_fwd_kernel(const
                   if (!(__bfloat162float(hb2[e]) > 0.f)) v[j4 * 8 + e] = 0.f;
               }
             } else {
-              for (int j = 0; j < 32 && n0 + j < p.cout; ++j)
+              _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n0 + j < p.cout)
                 if (!(__bfloat162float(mp[j]) > 0.f)) v[j] = 0.f;
             }
           }
@@ -225,7 +258,7 @@ __global__ void __launch_bounds__(128 + 128 * EWG, 1) conv_slab_fwd_kernel(const
               *reinterpret_cast<uint4*>(o + j4 * 8) = u;
             }
           } else {
-            for (int j = 0; j < 32 && n0 + j < p.cout; ++j) o[j] = __float2bfloat16_rn(v[j]);
+            _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n0 + j < p.cout) o[j] = __float2bfloat16_rn(v[j]);
           }
         }
       }
@@ -303,48 +336,51 @@ __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_co
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      int st = 0;
-      uint32_t ph = 0, acc_ph = 0;
-      const uint32_t ones = smem_u32(sOnes);
-      for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
-        const int cb = (wi / p.n_co_blocks) % p.n_ci_blocks;
-        const int sp = wi / (p.n_co_blocks * p.n_ci_blocks);
-        const int pb0 = sp * p.blocks_per_split;
-        const int pb1 = min(pb0 + p.blocks_per_split, p.n_pix_blocks);
-        const bool with_bias = cb == 0 && p.db != nullptr;
-        mbar_wait(&tempty[0], acc_ph ^ 1);
+    // 3x3 filters only (slab_wgrad_ok): SW = 10, taps 0..8 in pairs, all offsets compile-time.
+    constexpr int SW = 10;
+    int st = 0;
+    uint32_t ph = 0, acc_ph = 0;
+    const uint64_t ones_d = umma_smem_desc(smem_u32(sOnes), 2048, 1024, 128);
+    const uint64_t x0 = umma_smem_desc(smem_u32(sStage), 0, SW * 128, 128);   // LBO set per tap pair
+    const uint64_t y0 = umma_smem_desc(smem_u32(sStage) + p.slab_stage, 8192, 1024, 128);
+    for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
+      const int cb = (wi / p.n_co_blocks) % p.n_ci_blocks;
+      const int sp = wi / (p.n_co_blocks * p.n_ci_blocks);
+      const int pb0 = sp * p.blocks_per_split;
+      const int pb1 = min(pb0 + p.blocks_per_split, p.n_pix_blocks);
+      const bool with_bias = cb == 0 && p.db != nullptr;
+      mbar_wait(&tempty[0], acc_ph ^ 1);
+      tc_fence_after();
+      for (int pb = pb0; pb < pb1; ++pb) {
+        mbar_wait(&full[st], ph);
         tc_fence_after();
-        for (int pb = pb0; pb < pb1; ++pb) {
-          mbar_wait(&full[st], ph);
-          tc_fence_after();
-          const uint32_t slab = smem_u32(sStage + st * stage_bytes);
-          const uint32_t dyt = slab + p.slab_stage;
-          for (int a = 0; a < nacc; ++a) {
-            const int t0 = 2 * a;
-            const int t1 = 2 * a + 1 < p.taps ? 2 * a + 1 : t0;
-            const int o0 = (t0 / p.k) * p.sw + t0 % p.k;
-            const int o1 = (t1 / p.k) * p.sw + t1 % p.k;
-            const uint32_t lbo = static_cast<uint32_t>(o1 - o0) * 128u;
-            for (int ks = 0; ks < 8; ++ks) {
-              const uint64_t ad = umma_smem_desc(slab + (o0 + 2 * ks * p.sw) * 128, lbo, p.sw * 128, 128);
-              const uint64_t bd = umma_smem_desc(dyt + ks * 2048, 8192, 1024, 128);
-              umma_bf16(tmem_base + a * 64, ad, bd, p.idesc, (pb > pb0 || ks > 0) ? 1u : 0u);
-            }
+        const uint32_t soff = st * stage_bytes;
+        if (elect_one()) {
+#pragma unroll
+          for (int a = 0; a < 5; ++a) {
+            const int t0 = 2 * a, t1 = 2 * a + 1 < 9 ? 2 * a + 1 : 2 * a;
+            const int o0 = (t0 / 3) * SW + t0 % 3, o1 = (t1 / 3) * SW + t1 % 3;
+            // LBO (bits 16..29, >>4) = distance between the two taps' atoms inside the slab
+            const uint64_t xa = desc_add(x0, soff + o0 * 128) | (static_cast<uint64_t>(((o1 - o0) * 128) >> 4) << 16);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+              umma_bf16(tmem_base + a * 64, desc_add(xa, 2 * ks * SW * 128), desc_add(y0, soff + ks * 2048), p.idesc,
+                        (pb > pb0 || ks > 0) ? 1u : 0u);
           }
           if (with_bias) {
-            for (int ks = 0; ks < 8; ++ks) {
-              const uint64_t ad = umma_smem_desc(ones, 2048, 1024, 128);
-              const uint64_t bd = umma_smem_desc(dyt + ks * 2048, 8192, 1024, 128);
-              umma_bf16(tmem_base + nacc * 64, ad, bd, p.idesc, (pb > pb0 || ks > 0) ? 1u : 0u);
-            }
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+              umma_bf16(tmem_base + 5 * 64, ones_d, desc_add(y0, soff + ks * 2048), p.idesc,
+                        (pb > pb0 || ks > 0) ? 1u : 0u);
           }
           umma_commit(&empty[st]);
-          if (++st == p.na) { st = 0; ph ^= 1; }
         }
-        umma_commit(&tfull[0]);
-        acc_ph ^= 1;
+        __syncwarp();
+        if (++st == p.na) { st = 0; ph ^= 1; }
       }
+      if (elect_one()) umma_commit(&tfull[0]);
+      __syncwarp();
+      acc_ph ^= 1;
     }
   } else if (warp >= 4) {
     const int q = warp & 3;

@@ -483,3 +483,36 @@ cudaError_t cast_bf16(const float* x, long long n, __nv_bfloat16* y, cudaStream_
 }
 
 }  // namespace ralpb
+
+namespace ralpb {
+
+// out = act(acc + bias) [* (mask > 0)] for split-K GEMM results (fp32 accumulators).
+__global__ void gemm_finalize_kernel(const float* __restrict__ acc, int rows, int cols, long long ld_acc,
+                                     const float* __restrict__ bias, int relu, const __nv_bfloat16* __restrict__ mask,
+                                     long long ld_mask, __nv_bfloat16* __restrict__ out_bf16, float* __restrict__ out_f32,
+                                     long long ld_out) {
+  const long long total = static_cast<long long>(rows) * cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / cols;
+    const int c = static_cast<int>(i - r * cols);
+    float v = acc[r * ld_acc + c];
+    if (bias != nullptr) v += bias[c];
+    if (relu) v = fmaxf(v, 0.f);
+    if (mask != nullptr && !(__bfloat162float(mask[r * ld_mask + c]) > 0.f)) v = 0.f;
+    if (out_bf16 != nullptr) out_bf16[r * ld_out + c] = __float2bfloat16_rn(v);
+    if (out_f32 != nullptr) out_f32[r * ld_out + c] = v;
+  }
+}
+
+cudaError_t gemm_finalize(const float* acc, int rows, int cols, long long ld_acc, const float* bias, int relu,
+                          const __nv_bfloat16* mask, long long ld_mask, __nv_bfloat16* out_bf16, float* out_f32,
+                          long long ld_out, cudaStream_t s) {
+  const long long total = static_cast<long long>(rows) * cols;
+  if (total <= 0) return cudaSuccess;
+  gemm_finalize_kernel<<<grid_for(total, 256), 256, 0, s>>>(acc, rows, cols, ld_acc, bias, relu, mask, ld_mask,
+                                                            out_bf16, out_f32, ld_out);
+  return cudaGetLastError();
+}
+
+}  // namespace ralpb

@@ -54,6 +54,11 @@ cudaError_t colsum_bf16(const __nv_bfloat16* dy, long long rows, int c, long lon
 // backward-data copy [ci][taps-1-t][co].  wd may be null.
 cudaError_t conv_weight_prep(const float* w, int co, int taps, int ci, __nv_bfloat16* wf,
                              __nv_bfloat16* wd, cudaStream_t s);
+// out = act(acc + bias) [* (mask > 0)] -> bf16 (out_bf16) and/or fp32 (out_f32); finishes a
+// split-K GEMM whose fp32 partial sums were accumulated atomically into `acc`.
+cudaError_t gemm_finalize(const float* acc, int rows, int cols, long long ld_acc, const float* bias, int relu,
+                          const __nv_bfloat16* mask, long long ld_mask, __nv_bfloat16* out_bf16, float* out_f32,
+                          long long ld_out, cudaStream_t s);
 // fp32 -> bf16 cast.
 cudaError_t cast_bf16(const float* x, long long n, __nv_bfloat16* y, cudaStream_t s);
 

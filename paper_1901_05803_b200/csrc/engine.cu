@@ -263,6 +263,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   for (int g = 0; g < 2; ++g)
     if (!(m->dh[g] = alloc<bf16>(m, static_cast<size_t>(R) * widest, why))) return fail(*why);
   if (!(m->dx_fc = alloc<bf16>(m, static_cast<size_t>(R) * m->cut_elems, why))) return fail(*why);
+  if (!(m->fc_scratch = alloc<float>(m, static_cast<size_t>(R) * std::max(widest, m->cut_elems), why))) return fail(*why);
   if (!(m->row_loss = alloc<float>(m, R, why))) return fail(*why);
   if (!(m->loss = alloc<float>(m, 4, why))) return fail(*why);
   if (!(m->img_dev = alloc<float>(m, static_cast<size_t>(batch) * m->in_h * m->in_w * m->in_c, why))) return fail(*why);
@@ -391,6 +392,37 @@ int model_get_params(Model* m, int layer, float* w, float* b, int on_host, std::
 // ------------------------------------------------------------------ step
 namespace {
 
+// An FC GEMM with a bias / ReLU / ReLU-mask epilogue.  With few rows (e.g. W = 1, R = b) the
+// output tile grid cannot fill 148 SMs, so K is split across CTAs with fp32 atomics into a
+// scratch buffer and gemm_finalize applies the epilogue.
+int fc_gemm(Model* m, GemmDesc d, long long ld_out, const float* bias, int relu, const bf16* mask,
+            long long ld_mask, bf16* out_bf16, float* out_f32, std::string* why) {
+  const int bn = d.N >= 256 ? 256 : (d.N > 64 ? 128 : (d.N > 32 ? 64 : 32));
+  const long long tiles = static_cast<long long>((d.M + 127) / 128) * ((d.N + bn - 1) / bn);
+  if (tiles * 2 >= num_sms()) {
+    d.epi = out_bf16 != nullptr ? EPI_BF16 : EPI_F32;
+    d.out = out_bf16 != nullptr ? static_cast<void*>(out_bf16) : static_cast<void*>(out_f32);
+    d.s_m = ld_out;
+    d.bias = bias;
+    d.relu = relu;
+    d.mask = mask;
+    d.mask_s = ld_mask;
+    RALPB_TRY(gemm_launch(d, m->stream, why));
+    ++m->launches;
+    return 0;
+  }
+  RALPB_TRY(cudaMemsetAsync(m->fc_scratch, 0, sizeof(float) * d.M * ld_out, m->stream));
+  d.epi = EPI_F32_ATOMIC;
+  d.k_splits = 0;
+  d.out = m->fc_scratch;
+  d.s_m = ld_out;
+  RALPB_TRY(gemm_launch(d, m->stream, why));
+  RALPB_TRY(gemm_finalize(m->fc_scratch, d.M, d.N, ld_out, bias, relu, mask, ld_mask, out_bf16, out_f32, ld_out,
+                          m->stream));
+  m->launches += 2;
+  return 0;
+}
+
 int launch_fc_forward(Model* m, const bf16* in, int R, std::string* why) {
   const bf16* x = in;
   long long ldx = m->cut_elems;
@@ -400,14 +432,10 @@ int launch_fc_forward(Model* m, const bf16* in, int R, std::string* why) {
     d.M = R; d.N = f.out; d.K = f.in;
     d.a = Operand2D{x, R, f.in, ldx};
     d.b = Operand2D{f.wbf, f.out, f.in, f.in};
-    d.bias = m->P + f.b_off;
-    if (j + 1 < m->back.size()) {
-      d.epi = EPI_BF16; d.relu = 1; d.out = m->hid[j]; d.s_m = f.ld_out;
-    } else {
-      d.epi = EPI_F32; d.relu = 0; d.out = m->logits; d.s_m = f.ld_out;
-    }
-    RALPB_TRY(gemm_launch(d, m->stream, why));
-    ++m->launches;
+    const bool hidden = j + 1 < m->back.size();
+    if (fc_gemm(m, d, f.ld_out, m->P + f.b_off, hidden ? 1 : 0, nullptr, 0, hidden ? m->hid[j] : nullptr,
+                hidden ? nullptr : m->logits, why))
+      return 1;
     x = j + 1 < m->back.size() ? m->hid[j] : nullptr;
     ldx = f.ld_out;
   }
@@ -443,10 +471,8 @@ int launch_fc_backward(Model* m, const bf16* in, int R, bf16* dx_out, std::strin
     d.M = R; d.N = f.in; d.K = f.out;
     d.a_mode = LD_K; d.a = Operand2D{dy, R, f.out, lddy};
     d.b_mode = LD_MN; d.b = Operand2D{f.wbf, f.out, f.in, f.in};
-    d.epi = EPI_BF16; d.out = dst; d.s_m = ld_dst;
-    if (j > 0 && m->back[j - 1].relu) { d.mask = m->hid[j - 1]; d.mask_s = ldx; }
-    RALPB_TRY(gemm_launch(d, m->stream, why));
-    ++m->launches;
+    const bool masked = j > 0 && m->back[j - 1].relu;
+    if (fc_gemm(m, d, ld_dst, nullptr, 0, masked ? m->hid[j - 1] : nullptr, ldx, dst, nullptr, why)) return 1;
     dy = dst;
     lddy = ld_dst;
     ping ^= 1;

@@ -72,6 +72,7 @@ struct Model {
   bf16* dx_fc = nullptr;           // back-segment cut gradient [rows_back][cut_elems] (PS)
   std::vector<bf16*> hid;          // FC outputs (bf16) for hidden layers
   float* logits = nullptr;
+  float* fc_scratch = nullptr;     // split-K accumulators for FC GEMMs with few rows
   bf16* dlogits = nullptr;
   bf16* dh[2] = {nullptr, nullptr};  // FC backward ping-pong
   float* row_loss = nullptr;

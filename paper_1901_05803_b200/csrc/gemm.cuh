@@ -88,10 +88,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
 
   const int total = p.n_mt * p.n_nt * p.n_ks;
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 3) {
+    // Two producer warps take alternate k-blocks: a TMA issue keeps its thread busy for
+    // hundreds of cycles (tools/exp_tma.cu), so issuing from two threads doubles the rate.
+    const int pid = warp == 0 ? 0 : 1;
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      int seq = 0;
       for (int w = blockIdx.x; w < total; w += gridDim.x) {
         int nt = w % p.n_nt;
         int t = w / p.n_nt;
@@ -99,7 +103,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
         int ks = t / p.n_mt;
         int kb0 = ks * p.kblocks_per_split;
         int kb1 = min(kb0 + p.kblocks_per_split, p.kblocks_total);
-        for (int kk = kb0; kk < kb1; ++kk) {
+        for (int kk = kb0; kk < kb1; ++kk, ++seq) {
+          if ((seq & 1) != pid) {
+            if (++stage == stages) { stage = 0; phase ^= 1; }
+            continue;
+          }
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], p.a_bytes + p.b_bytes);
           load_operand(&p.tmA, p.a_mode, sA + stage * kAStage, &full[stage], mt * kBM, kBM, kk,
@@ -111,37 +119,44 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      const bool a_k = p.a_mode == LD_K || p.a_mode == LD_K_CONV;
-      const int ksteps = a_k ? p.kb / 16 : 4;
-      for (int w = blockIdx.x; w < total; w += gridDim.x) {
-        int t = w / p.n_nt;
-        int ks = t / p.n_mt;
-        int kb0 = ks * p.kblocks_per_split;
-        int kb1 = min(kb0 + p.kblocks_per_split, p.kblocks_total);
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+    // Whole warp runs the loop (warp-uniform state in uniform registers), one elected lane
+    // issues; descriptors are stage bases plus a per-k-step increment (no per-MMA rebuild).
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const bool a_k = p.a_mode == LD_K || p.a_mode == LD_K_CONV;
+    const bool b_k = p.b_mode == LD_K || p.b_mode == LD_K_CONV;
+    const int ksteps = a_k ? p.kb / 16 : 4;
+    const uint64_t a0 = operand_desc(smem_u32(sA), p.a_mode, p.a_swz, 0);
+    const uint64_t b0 = operand_desc(smem_u32(sB), p.b_mode, p.b_swz, 0);
+    const uint32_t a_step = a_k ? 32u : 16u * p.a_swz;
+    const uint32_t b_step = b_k ? 32u : 16u * p.b_swz;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int t = w / p.n_nt;
+      int ks = t / p.n_mt;
+      int kb0 = ks * p.kblocks_per_split;
+      int kb1 = min(kb0 + p.kblocks_per_split, p.kblocks_total);
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * bn;
+      for (int kk = kb0; kk < kb1; ++kk) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * bn;
-        for (int kk = kb0; kk < kb1; ++kk) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + stage * kAStage);
-          const uint32_t b_base = smem_u32(sB + stage * p.b_stage_bytes);
-          for (int s = 0; s < ksteps; ++s) {
-            uint64_t ad = operand_desc(a_base, p.a_mode, p.a_swz, s);
-            uint64_t bd = operand_desc(b_base, p.b_mode, p.b_swz, s);
-            umma_bf16(d_tmem, ad, bd, p.idesc, (kk > kb0 || s > 0) ? 1u : 0u);
-          }
+        const uint64_t ad = desc_add(a0, stage * kAStage);
+        const uint64_t bd = desc_add(b0, stage * p.b_stage_bytes);
+        if (elect_one()) {
+          for (int s = 0; s < ksteps; ++s)
+            umma_bf16(d_tmem, desc_add(ad, s * a_step), desc_add(bd, s * b_step), p.idesc,
+                      (kk > kb0 || s > 0) ? 1u : 0u);
           umma_commit(&empty[stage]);
-          if (++stage == stages) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        __syncwarp();
+        if (++stage == stages) { stage = 0; phase ^= 1; }
       }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 4) {
     const int q = warp & 3;  // TMEM lane quarter this warp may access
@@ -188,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
                 if (!(__bfloat162float(hb[e]) > 0.f)) v[j4 * 8 + e] = 0.f;
             }
           } else {
-            for (int j = 0; j < 32 && n0 + j < p.N; ++j)
+            _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n0 + j < p.N)
               if (!(__bfloat162float(mp[j]) > 0.f)) v[j] = 0.f;
           }
         }
@@ -209,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
               *reinterpret_cast<uint4*>(o + j4 * 8) = u;
             }
           } else {
-            for (int j = 0; j < 32 && n0 + j < p.N; ++j) o[j * p.s_n] = __float2bfloat16_rn(v[j]);
+            _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n0 + j < p.N) o[j * p.s_n] = __float2bfloat16_rn(v[j]);
           }
         } else if (p.epi == EPI_F32) {
           float* o = reinterpret_cast<float*>(p.out) + m * p.s_m + n0 * p.s_n;
@@ -219,11 +234,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
               *reinterpret_cast<float4*>(o + j4 * 4) =
                   make_float4(v[j4 * 4], v[j4 * 4 + 1], v[j4 * 4 + 2], v[j4 * 4 + 3]);
           } else {
-            for (int j = 0; j < 32 && n0 + j < p.N; ++j) o[j * p.s_n] = v[j];
+            _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n0 + j < p.N) o[j * p.s_n] = v[j];
           }
         } else {  // EPI_F32_ATOMIC
           float* o = reinterpret_cast<float*>(p.out) + m * p.s_m + n0 * p.s_n;
-          for (int j = 0; j < 32 && n0 + j < p.N; ++j) red_add_f32(o + j * p.s_n, v[j]);
+          _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n0 + j < p.N) red_add_f32(o + j * p.s_n, v[j]);
         }
       }
       tc_fence_before();

@@ -133,6 +133,28 @@ __host__ __device__ inline uint32_t umma_idesc_bf16(int M, int N, bool a_mn, boo
   return d;
 }
 
+// One lane of a fully active warp returns true (elect.sync).  MMA-issuing loops run on the
+// whole warp (warp-uniform values live in uniform registers) and elect one lane per issue.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .b32 rx;\n"
+      ".reg .pred px;\n"
+      "elect.sync rx|px, %1;\n"
+      "@px mov.s32 %0, 1;\n"
+      "}\n"
+      : "+r"(pred)
+      : "r"(0xffffffffu));
+  return pred != 0;
+}
+
+// A UMMA descriptor advanced by `bytes` (start-address field is addr >> 4, 14 bits; shared
+// memory offsets stay far below the field's 256 KB range, so the add never carries out).
+__device__ __forceinline__ uint64_t desc_add(uint64_t desc, uint32_t bytes) {
+  return desc + static_cast<uint64_t>(bytes >> 4);
+}
+
 // ---------------------------------------------------------------- misc
 __device__ __forceinline__ void red_add_f32(float* addr, float v) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
