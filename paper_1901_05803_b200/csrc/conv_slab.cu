@@ -145,7 +145,6 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
 
 cudaError_t conv_slab_wgrad(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw, float* db,
                             cudaStream_t s, std::string* why) {
-  static bool attr = false;
   SlabConvParams p;
   std::memset(&p, 0, sizeof(p));
   p.n = g.n; p.h = g.h; p.w = g.w; p.hp = g.hp(); p.wp = g.wp(); p.pad = g.pad; p.k = g.k; p.taps = g.taps();
@@ -153,39 +152,34 @@ cudaError_t conv_slab_wgrad(const ConvGeom& g, const void* x_pad, const void* dy
   p.kb = 64;
   p.row_bytes = 128;
   p.bn = 64;
+  // pixel blocks of bh rows x 8 columns; 14 divides every VGG feature-map height
+  const int bh = g.h % 14 == 0 ? 14 : 16;
   p.sw = 8 + g.k - 1;
-  p.sh = 16 + g.k - 1;
+  p.sh = bh + g.k - 1;
   p.slab_load = 128 * p.sw * p.sh;
   p.slab_stage = align1k(p.slab_load);
-  p.b_load = 128 * 8 * 16;
+  p.b_load = 128 * 8 * bh;
   p.b_stage = align1k(p.b_load);
   p.na = std::min(8, (kSmemBudget - 4096) / (p.slab_stage + p.b_stage));
-  const int nacc = (p.taps + 1) / 2;
-  const int used = (nacc + 1) * 64;
-  p.tmem_cols = used <= 256 ? 256 : 512;
-  p.n_hb = (g.h + 15) / 16;
+  p.tmem_cols = 512;  // 5 tap-pair accumulators + bias = 384 columns
+  p.n_hb = (g.h + bh - 1) / bh;
   p.n_wb = (g.w + 7) / 8;
   p.n_pix_blocks = g.n * p.n_hb * p.n_wb;
   p.n_ci_blocks = g.cin / 64;
   p.n_co_blocks = g.cout / 64;
-  const int sms = num_sms();
-  const int tiles = p.n_ci_blocks * p.n_co_blocks;
-  int splits = std::max(1, (2 * sms + tiles - 1) / tiles);
-  splits = std::min(splits, p.n_pix_blocks);
-  p.blocks_per_split = (p.n_pix_blocks + splits - 1) / splits;
-  p.n_splits = (p.n_pix_blocks + p.blocks_per_split - 1) / p.blocks_per_split;
   p.idesc = umma_idesc_bf16(128, 64, true, true);
   p.dw = dw;
   p.db = db;
-  if (!encode_act(&p.tmX, x_pad, g.cin, g.wp(), g.hp(), g.n, 64, p.sw, p.sh, 128, why))
-    return cudaErrorInvalidValue;
-  if (!encode_act(&p.tmB, dy_pad, g.cout, g.wp(), g.hp(), g.n, 64, 8, 16, 128, why))
-    return cudaErrorInvalidValue;
+  if (!encode_act(&p.tmX, x_pad, g.cin, g.wp(), g.hp(), g.n, 64, p.sw, p.sh, 128, why)) return cudaErrorInvalidValue;
+  if (!encode_act(&p.tmB, dy_pad, g.cout, g.wp(), g.hp(), g.n, 64, 8, bh, 128, why)) return cudaErrorInvalidValue;
   const int smem = 1024 + 4096 + p.na * (p.slab_stage + p.b_stage) + 512;
-  if (!attr) { cudaFuncSetAttribute(conv_slab_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); attr = true; }
-  const long long total = static_cast<long long>(tiles) * p.n_splits;
-  const int grid = static_cast<int>(std::min<long long>(total, sms));
-  launch_timed([&] { conv_slab_wgrad_kernel<<<grid, 256, smem, s>>>(p); }, s);
+  const long long units = static_cast<long long>(p.n_ci_blocks) * p.n_co_blocks * p.n_pix_blocks;
+  const int grid = static_cast<int>(std::min<long long>(units, num_sms()));
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    launch_timed([&] { kern<<<grid, 256, smem, s>>>(p); }, s);
+  };
+  if (bh == 14) go(conv_slab_wgrad_kernel<14>); else go(conv_slab_wgrad_kernel<16>);
   return cudaGetLastError();
 }
 

@@ -276,10 +276,16 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
 }
 
 // ------------------------------------------------------------------ backward-filter
-// Stage = one pixel block (16 x 8 pixels): X halo slab (64 ci) + dY tile (64 co).
-// Accumulator a (0..ceil(taps/2)-1) holds taps (2a, 2a+1) x 64 ci; accumulator
-// `nacc` holds the bias gradient (ones x dY) when this CTA owns ci-block 0.
+// Stage = one pixel block of BH image rows x 8 columns (BH = 14 divides every VGG feature-map
+// height, so blocks never straddle the image edge there): X halo slab (64 ci) + dY tile
+// (64 co).  Accumulator a (0..4) holds taps (2a, 2a+1) x 64 ci; accumulator 5 holds the bias
+// gradient (ones x dY) when this CTA owns ci-block 0.  Work is split stream-K style: the
+// (tile, pixel-block) units are divided evenly over the persistent CTAs, and every
+// contiguous run of one tile is flushed with fp32 reductions.
+template <int BH>
 __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_constant__ SlabConvParams p) {
+  constexpr int SW = 10;            // 3x3 filters only (slab_wgrad_ok)
+  constexpr int KSTEPS = BH / 2;    // 16-pixel K-steps per block (two 8-pixel rows each)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sOnes = smem;                           // 4 KB of bf16 ones (MN-major 2 atoms x 16 rows)
@@ -308,24 +314,25 @@ __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int nacc = (p.taps + 1) / 2;
-  const int total = p.n_ci_blocks * p.n_co_blocks * p.n_splits;
+  const int PB = p.n_pix_blocks;
+  const long long units = static_cast<long long>(p.n_ci_blocks) * p.n_co_blocks * PB;
+  const long long u_begin = units * blockIdx.x / gridDim.x;
+  const long long u_end = units * (blockIdx.x + 1) / gridDim.x;
   const int pb_per_img = p.n_hb * p.n_wb;
 
   if (warp == 0) {
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
-      for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
-        const int nb = wi % p.n_co_blocks;
-        const int cb = (wi / p.n_co_blocks) % p.n_ci_blocks;
-        const int sp = wi / (p.n_co_blocks * p.n_ci_blocks);
-        const int pb0 = sp * p.blocks_per_split;
-        const int pb1 = min(pb0 + p.blocks_per_split, p.n_pix_blocks);
+      for (long long u = u_begin; u < u_end;) {
+        const int tile = static_cast<int>(u / PB);
+        const int pb0 = static_cast<int>(u - static_cast<long long>(tile) * PB);
+        const int pb1 = static_cast<int>(u_end - u < PB - pb0 ? pb0 + (u_end - u) : PB);
+        const int nb = tile % p.n_co_blocks, cb = tile / p.n_co_blocks;
         for (int pb = pb0; pb < pb1; ++pb) {
           const int img = pb / pb_per_img;
           const int rem = pb - img * pb_per_img;
-          const int h0 = (rem / p.n_wb) * 16, w0 = (rem % p.n_wb) * 8;
+          const int h0 = (rem / p.n_wb) * BH, w0 = (rem % p.n_wb) * 8;
           mbar_wait(&empty[st], ph ^ 1);
           mbar_expect_tx(&full[st], p.slab_load + p.b_load);
           uint8_t* base = sStage + st * stage_bytes;
@@ -333,22 +340,20 @@ __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_co
           tma_load_4d(base + p.slab_stage, &p.tmB, &full[st], nb * 64, w0 + p.pad, h0 + p.pad, img);
           if (++st == p.na) { st = 0; ph ^= 1; }
         }
+        u += pb1 - pb0;
       }
     }
   } else if (warp == 1) {
-    // 3x3 filters only (slab_wgrad_ok): SW = 10, taps 0..8 in pairs, all offsets compile-time.
-    constexpr int SW = 10;
     int st = 0;
     uint32_t ph = 0, acc_ph = 0;
     const uint64_t ones_d = umma_smem_desc(smem_u32(sOnes), 2048, 1024, 128);
     const uint64_t x0 = umma_smem_desc(smem_u32(sStage), 0, SW * 128, 128);   // LBO set per tap pair
     const uint64_t y0 = umma_smem_desc(smem_u32(sStage) + p.slab_stage, 8192, 1024, 128);
-    for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
-      const int cb = (wi / p.n_co_blocks) % p.n_ci_blocks;
-      const int sp = wi / (p.n_co_blocks * p.n_ci_blocks);
-      const int pb0 = sp * p.blocks_per_split;
-      const int pb1 = min(pb0 + p.blocks_per_split, p.n_pix_blocks);
-      const bool with_bias = cb == 0 && p.db != nullptr;
+    for (long long u = u_begin; u < u_end;) {
+      const int tile = static_cast<int>(u / PB);
+      const int pb0 = static_cast<int>(u - static_cast<long long>(tile) * PB);
+      const int pb1 = static_cast<int>(u_end - u < PB - pb0 ? pb0 + (u_end - u) : PB);
+      const bool with_bias = tile / p.n_co_blocks == 0 && p.db != nullptr;
       mbar_wait(&tempty[0], acc_ph ^ 1);
       tc_fence_after();
       for (int pb = pb0; pb < pb1; ++pb) {
@@ -363,13 +368,13 @@ __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_co
             // LBO (bits 16..29, >>4) = distance between the two taps' atoms inside the slab
             const uint64_t xa = desc_add(x0, soff + o0 * 128) | (static_cast<uint64_t>(((o1 - o0) * 128) >> 4) << 16);
 #pragma unroll
-            for (int ks = 0; ks < 8; ++ks)
+            for (int ks = 0; ks < KSTEPS; ++ks)
               umma_bf16(tmem_base + a * 64, desc_add(xa, 2 * ks * SW * 128), desc_add(y0, soff + ks * 2048), p.idesc,
                         (pb > pb0 || ks > 0) ? 1u : 0u);
           }
           if (with_bias) {
 #pragma unroll
-            for (int ks = 0; ks < 8; ++ks)
+            for (int ks = 0; ks < KSTEPS; ++ks)
               umma_bf16(tmem_base + 5 * 64, ones_d, desc_add(y0, soff + ks * 2048), p.idesc,
                         (pb > pb0 || ks > 0) ? 1u : 0u);
           }
@@ -381,35 +386,38 @@ __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_co
       if (elect_one()) umma_commit(&tfull[0]);
       __syncwarp();
       acc_ph ^= 1;
+      u += pb1 - pb0;
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
     const int m = q * 32 + lane;
     uint32_t acc_ph = 0;
     const long long wstride = static_cast<long long>(p.taps) * p.c;  // dW[co][tap][ci]
-    for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
-      const int nb = wi % p.n_co_blocks;
-      const int cb = (wi / p.n_co_blocks) % p.n_ci_blocks;
+    for (long long u = u_begin; u < u_end;) {
+      const int tile = static_cast<int>(u / PB);
+      const int pb0 = static_cast<int>(u - static_cast<long long>(tile) * PB);
+      const int pb1 = static_cast<int>(u_end - u < PB - pb0 ? pb0 + (u_end - u) : PB);
+      const int nb = tile % p.n_co_blocks, cb = tile / p.n_co_blocks;
       const bool with_bias = cb == 0 && p.db != nullptr;
       mbar_wait(&tfull[0], acc_ph);
       tc_fence_after();
-      for (int a = 0; a <= nacc; ++a) {
-        if (a == nacc && !with_bias) break;
+      for (int a = 0; a <= 5; ++a) {
+        if (a == 5 && !with_bias) break;
         const uint32_t tb = tmem_base + a * 64 + (static_cast<uint32_t>(q * 32) << 16);
         for (int c = 0; c < 64; c += 32) {
           uint32_t rr[32];
           tmem_ld32(tb + c, rr);
           tmem_wait_ld();
           const int co0 = nb * 64 + c;
-          if (a < nacc) {
+          if (a < 5) {
             const int tap = 2 * a + (m >> 6);
-            if (tap < p.taps) {
+            if (tap < 9) {
               float* dst = p.dw + static_cast<long long>(co0) * wstride + static_cast<long long>(tap) * p.c + cb * 64 + (m & 63);
-#pragma unroll 8
+#pragma unroll
               for (int j = 0; j < 32; ++j) red_add_f32(dst + j * wstride, __uint_as_float(rr[j]));
             }
           } else if (m == 0) {
-#pragma unroll 8
+#pragma unroll
             for (int j = 0; j < 32; ++j) red_add_f32(p.db + co0 + j, __uint_as_float(rr[j]));
           }
         }
@@ -417,6 +425,7 @@ __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_co
       tc_fence_before();
       mbar_arrive(&tempty[0]);
       acc_ph ^= 1;
+      u += pb1 - pb0;
     }
   }
   tc_fence_before();

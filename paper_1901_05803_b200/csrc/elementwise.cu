@@ -75,9 +75,50 @@ __global__ void pack_im2col_kernel(const float* __restrict__ x, int n, int h, in
   }
 }
 
+// Fully unrolled variant (one thread = one patch row, all columns in registers) for the
+// common small first layers, e.g. VGG's 3x3x3 (+bias) -> 32 columns.
+template <int K, int C, int KPAD>
+__global__ void pack_im2col_row_kernel(const float* __restrict__ x, int n, int h, int w, int st, int p, int ho,
+                                       int wo, int po, __nv_bfloat16* __restrict__ out) {
+  const int hop = ho + 2 * po, wop = wo + 2 * po;
+  const int rows = n * hop * wop;
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < rows; row += gridDim.x * blockDim.x) {
+    const int img = row / (hop * wop);
+    const int rem = row - img * hop * wop;
+    const int py = rem / wop;
+    const int oy = py - po, ox = rem - py * wop - po;
+    const bool interior = oy >= 0 && oy < ho && ox >= 0 && ox < wo;
+    const float* base = x + static_cast<long long>(img) * h * w * C;
+    __align__(16) __nv_bfloat16 v[KPAD];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const int iy = oy * st + r - p;
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        const int ix = ox * st + s - p;
+        const bool in = interior && iy >= 0 && iy < h && ix >= 0 && ix < w;
+        const float* src = base + (static_cast<long long>(in ? iy : 0) * w + (in ? ix : 0)) * C;
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) v[(r * K + s) * C + ch] = __float2bfloat16_rn(in ? __ldg(src + ch) : 0.f);
+      }
+    }
+    v[K * K * C] = __float2bfloat16_rn(interior ? 1.f : 0.f);
+#pragma unroll
+    for (int j = K * K * C + 1; j < KPAD; ++j) v[j] = __float2bfloat16_rn(0.f);
+    uint4* o = reinterpret_cast<uint4*>(out + static_cast<long long>(row) * KPAD);
+#pragma unroll
+    for (int q = 0; q < KPAD / 8; ++q) o[q] = reinterpret_cast<const uint4*>(v)[q];
+  }
+}
+
 cudaError_t pack_im2col(const float* x, int n, int h, int w, int c, int k, int st, int p, int ho, int wo,
                         int po, int kpad, __nv_bfloat16* out, cudaStream_t s) {
   if (kpad % 8 != 0 || kpad < k * k * c + 1) return cudaErrorInvalidValue;
+  const long long rows = static_cast<long long>(n) * (ho + 2 * po) * (wo + 2 * po);
+  if (k == 3 && c == 3 && kpad == 32 && rows < (1LL << 31)) {
+    pack_im2col_row_kernel<3, 3, 32><<<grid_for(rows, 256), 256, 0, s>>>(x, n, h, w, st, p, ho, wo, po, out);
+    return cudaGetLastError();
+  }
   const long long total = static_cast<long long>(n) * (ho + 2 * po) * (wo + 2 * po) * (kpad / 8);
   pack_im2col_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, n, h, w, c, k, st, p, ho, wo, po, kpad, out);
   return cudaGetLastError();
