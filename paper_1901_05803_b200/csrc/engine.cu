@@ -23,6 +23,7 @@
 // semantics of SURVEY.md §7.4 (mean loss over W*b, SGD v=mu*v+g, p-=lr*v, HWC flatten).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include "elementwise.cuh"
 #include "engine.cuh"
@@ -443,7 +444,12 @@ int launch_fc_forward(Model* m, const bf16* in, int R, std::string* why) {
 }
 
 // FC backward from dlogits; writes the cut gradient for all R rows into dx_out.
-int launch_fc_backward(Model* m, const bf16* in, int R, bf16* dx_out, std::string* why) {
+// FC backward from dlogits; writes the cut gradient for all R rows into dx_out.  With
+// `update` (the RALP PS: the FC tail is never synchronised) the weight-gradient GEMM applies
+// SGD-momentum in its epilogue (EPI_SGD) -- after the layer's dgrad has consumed the old bf16
+// weights -- so FC gradients never round-trip through HBM.
+int launch_fc_backward(Model* m, const bf16* in, int R, bf16* dx_out, bool update, float lr, float mu,
+                       std::string* why) {
   const int nb = static_cast<int>(m->back.size());
   const bf16* dy = m->dlogits;
   long long lddy = m->back.back().ld_out;
@@ -452,18 +458,6 @@ int launch_fc_backward(Model* m, const bf16* in, int R, bf16* dx_out, std::strin
     FcLayer& f = m->back[j];
     const bf16* x = j == 0 ? in : m->hid[j - 1];
     const long long ldx = j == 0 ? m->cut_elems : m->back[j - 1].ld_out;
-    // wgrad: G_w[out][in] = dy^T x
-    GemmDesc w;
-    w.M = f.out; w.N = f.in; w.K = R;
-    w.a_mode = LD_MN; w.a = Operand2D{dy, R, f.out, lddy};
-    w.b_mode = LD_MN; w.b = Operand2D{x, R, f.in, ldx};
-    w.epi = EPI_F32; w.out = m->G + f.w_off; w.s_m = f.in; w.s_n = 1;
-    RALPB_TRY(gemm_launch(w, m->stream, why));
-    ++m->launches;
-    // bias grad
-    RALPB_TRY(cudaMemsetAsync(m->G + f.b_off, 0, f.out * sizeof(float), m->stream));
-    RALPB_TRY(colsum_bf16(dy, R, f.out, lddy, m->G + f.b_off, m->stream));
-    ++m->launches;
     // dgrad: dx[R][in] = dy[R][out] . W[out][in]   (ReLU mask of the previous hidden layer)
     bf16* dst = j == 0 ? dx_out : m->dh[ping];
     const long long ld_dst = j == 0 ? m->cut_elems : m->back[j - 1].ld_out;
@@ -473,6 +467,28 @@ int launch_fc_backward(Model* m, const bf16* in, int R, bf16* dx_out, std::strin
     d.b_mode = LD_MN; d.b = Operand2D{f.wbf, f.out, f.in, f.in};
     const bool masked = j > 0 && m->back[j - 1].relu;
     if (fc_gemm(m, d, ld_dst, nullptr, 0, masked ? m->hid[j - 1] : nullptr, ldx, dst, nullptr, why)) return 1;
+    // bias grad (+ its SGD step when updating in place)
+    RALPB_TRY(cudaMemsetAsync(m->G + f.b_off, 0, f.out * sizeof(float), m->stream));
+    RALPB_TRY(colsum_bf16(dy, R, f.out, lddy, m->G + f.b_off, m->stream));
+    ++m->launches;
+    // wgrad: G_w[out][in] = dy^T x   (or, with update, v = mu*v + g; p -= lr*v; bf16 copy)
+    GemmDesc w;
+    w.M = f.out; w.N = f.in; w.K = R;
+    w.a_mode = LD_MN; w.a = Operand2D{dy, R, f.out, lddy};
+    w.b_mode = LD_MN; w.b = Operand2D{x, R, f.in, ldx};
+    w.s_m = f.in; w.s_n = 1;
+    if (update) {
+      w.epi = EPI_SGD; w.out = m->P + f.w_off; w.sgd_mom = m->V + f.w_off; w.sgd_bf16 = f.wbf;
+      w.sgd_lr = lr; w.sgd_mu = mu;
+    } else {
+      w.epi = EPI_F32; w.out = m->G + f.w_off;
+    }
+    RALPB_TRY(gemm_launch(w, m->stream, why));
+    ++m->launches;
+    if (update) {
+      RALPB_TRY(sgd_momentum(m->P + f.b_off, m->V + f.b_off, m->G + f.b_off, f.out, lr, mu, 1.f, m->stream));
+      ++m->launches;
+    }
     dy = dst;
     lddy = ld_dst;
     ping ^= 1;
@@ -671,16 +687,21 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
     RALPB_TRY(softmax_xent(m->logits, R, last.out, last.ld_out, m->labels_all, scale, m->row_loss, m->dlogits, last.ld_out, s));
     RALPB_TRY(reduce_sum(m->row_loss, R, 1.f / static_cast<float>(R), m->loss, s));
     m->launches += 2;
-    if (launch_fc_backward(m, in, R, m->dx_fc, why)) return 1;
-    if (ralp) {
-      // FC tail update stays on the PS (never synchronised)
-      // SGD on each FC layer's weights also refreshes its bf16 GEMM copy (one pass over P)
+    // SGD fused into the FC weight-gradient epilogue (RALPB_FC_FUSED_SGD=1) or as a separate
+    // streaming pass (default: the epilogue's per-row access pattern measured slower).
+    const char* fused_env = getenv("RALPB_FC_FUSED_SGD");
+    const bool fused = ralp && fused_env != nullptr && fused_env[0] == '1';
+    if (launch_fc_backward(m, in, R, m->dx_fc, fused, lr, mu, why)) return 1;
+    if (ralp && !fused) {
       for (auto& f : m->back) {
         const long long nw = static_cast<long long>(f.out) * f.in;
         RALPB_TRY(sgd_momentum_bf16(m->P + f.w_off, m->V + f.w_off, m->G + f.w_off, nw, lr, mu, 1.f, f.wbf, s));
         RALPB_TRY(sgd_momentum(m->P + f.b_off, m->V + f.b_off, m->G + f.b_off, f.out, lr, mu, 1.f, s));
         m->launches += 2;
       }
+    }
+    if (ralp) {
+      // FC tail update stays on the PS (never synchronised)
       // return every remote worker's rows of the cut gradient
       for (int r = 0; r < m->world; ++r) {
         if (r == m->rank) continue;

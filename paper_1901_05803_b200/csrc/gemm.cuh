@@ -236,6 +236,36 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
           } else {
             _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n0 + j < p.N) o[j * p.s_n] = v[j];
           }
+        } else if (p.epi == EPI_SGD) {
+          const long long base = m * p.s_m + n0 * p.s_n;
+          float* pp = reinterpret_cast<float*>(p.out) + base;
+          float* vv = p.sgd_mom + base;
+          __nv_bfloat16* bb = p.sgd_bf16 + base;
+          if (full_chunk && p.s_n == 1) {
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4) {
+              float4 pv = *reinterpret_cast<float4*>(pp + j4 * 4);
+              float4 mv = *reinterpret_cast<float4*>(vv + j4 * 4);
+              mv.x = p.sgd_mu * mv.x + v[j4 * 4 + 0]; pv.x -= p.sgd_lr * mv.x;
+              mv.y = p.sgd_mu * mv.y + v[j4 * 4 + 1]; pv.y -= p.sgd_lr * mv.y;
+              mv.z = p.sgd_mu * mv.z + v[j4 * 4 + 2]; pv.z -= p.sgd_lr * mv.z;
+              mv.w = p.sgd_mu * mv.w + v[j4 * 4 + 3]; pv.w -= p.sgd_lr * mv.w;
+              *reinterpret_cast<float4*>(pp + j4 * 4) = pv;
+              *reinterpret_cast<float4*>(vv + j4 * 4) = mv;
+              uint2 b2;
+              b2.x = pack_bf16(pv.x, pv.y);
+              b2.y = pack_bf16(pv.z, pv.w);
+              *reinterpret_cast<uint2*>(bb + j4 * 4) = b2;
+            }
+          } else {
+            _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n0 + j < p.N) {
+              const long long o = j * p.s_n;
+              const float mv = p.sgd_mu * vv[o] + v[j];
+              vv[o] = mv;
+              pp[o] -= p.sgd_lr * mv;
+              bb[o] = __float2bfloat16_rn(pp[o]);
+            }
+          }
         } else {  // EPI_F32_ATOMIC
           float* o = reinterpret_cast<float*>(p.out) + m * p.s_m + n0 * p.s_n;
           _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n0 + j < p.N) red_add_f32(o + j * p.s_n, v[j]);

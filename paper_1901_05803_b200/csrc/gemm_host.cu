@@ -133,6 +133,10 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
   p.s_m = d.s_m;
   p.s_n = d.s_n;
   p.bias = d.bias;
+  p.sgd_mom = d.sgd_mom;
+  p.sgd_bf16 = d.sgd_bf16;
+  p.sgd_lr = d.sgd_lr;
+  p.sgd_mu = d.sgd_mu;
   p.mask = reinterpret_cast<const __nv_bfloat16*>(d.mask);
   p.mask_s = d.mask_s;
   p.border = d.border;

@@ -32,6 +32,9 @@ struct GemmDesc {
   void* out = nullptr;
   long long s_m = 0, s_n = 1;
   const float* bias = nullptr;
+  float* sgd_mom = nullptr;
+  __nv_bfloat16* sgd_bf16 = nullptr;
+  float sgd_lr = 0.f, sgd_mu = 0.f;
   const void* mask = nullptr;
   long long mask_s = 0;
   int border = 0;

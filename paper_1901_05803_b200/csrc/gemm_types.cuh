@@ -23,7 +23,10 @@
 namespace ralpb {
 
 enum LoadMode : int { LD_K = 0, LD_K_CONV = 1, LD_MN = 2, LD_MN_CONV = 3 };
-enum EpiMode : int { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_ATOMIC = 2 };
+// EPI_SGD: the accumulator is a parameter gradient g; the epilogue applies SGD-momentum in
+// place (v = mu*v + g; p -= lr*v on out = p, sgd_mom = v) and refreshes the bf16 copy, so
+// the gradient never round-trips through HBM.
+enum EpiMode : int { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_ATOMIC = 2, EPI_SGD = 3 };
 
 constexpr int kBM = 128;
 constexpr int kMaxTaps = 32;
@@ -56,6 +59,9 @@ struct alignas(64) GemmParams {
   void* out;
   long long s_m, s_n;       // element strides of out
   const float* bias;        // per-n bias (or nullptr)
+  float* sgd_mom;           // EPI_SGD: momentum (same layout as out)
+  __nv_bfloat16* sgd_bf16;  // EPI_SGD: bf16 copy of the updated parameters (same layout)
+  float sgd_lr, sgd_mu;
   const __nv_bfloat16* mask;  // relu-backward mask source (mask[m*mask_s + n] > 0), or nullptr
   long long mask_s;
   int border;               // zero rows that are padding positions of the padded layout
