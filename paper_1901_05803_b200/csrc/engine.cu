@@ -228,6 +228,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   cudaMemset(m->V, 0, m->n_total * sizeof(float));
   if (!(m->counters = alloc<uint32_t>(m, kNumCounters, why))) return fail(*why);
   cudaMemset(m->counters, 0, kNumCounters * sizeof(uint32_t));
+  m->seq_dev = m->counters + kNumCounters - 1;
   // Every activation and activation-gradient buffer is dedicated and zeroed once: the conv
   // kernels write interior pixels only, so the padding borders stay zero for the job's life.
   m->gacts.assign(m->acts.size(), nullptr);
@@ -279,6 +280,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
 void model_destroy(Model* m) {
   if (!m) return;
   cudaDeviceSynchronize();
+  if (m->graph) cudaGraphExecDestroy(m->graph);
   for (int r = 0; r < static_cast<int>(m->peer_base.size()); ++r)
     if (r != m->rank && m->peer_base[r] != nullptr) cudaIpcCloseMemHandle(m->peer_base[r]);
   for (void* p : m->owned) cudaFree(p);
@@ -312,6 +314,7 @@ int model_ipc_open(Model* m, const void* handles, std::string* why) {
     m->peer_base[r] = static_cast<char*>(p);
   }
   m->peers_open = true;
+  if (m->graph) { cudaGraphExecDestroy(m->graph); m->graph = nullptr; }  // peer pointers are baked in
   return 0;
 }
 
@@ -560,7 +563,7 @@ int sync_params(Model* m, long long n, float lr, float mu, std::string* why) {
     ++m->launches;
     return 0;
   }
-  const uint32_t seq = m->seq;
+  const uint32_t* seq = m->seq_dev;
   PeerSignal all_grad{}, all_done{};
   all_grad.n = all_done.n = m->world;
   for (int r = 0; r < m->world; ++r) {
@@ -591,30 +594,26 @@ int sync_params(Model* m, long long n, float lr, float mu, std::string* why) {
 
 }  // namespace
 
-int model_step(Model* m, const void* images, const int32_t* labels, int on_host, float lr, float mu,
-               std::string* why) {
-  if (m->world > 1 && !m->peers_open) { *why = "ralpb_model_ipc_open has not been called"; return 1; }
-  m->seq += 1;
-  m->launches = 0;
-  m->phys_bytes = 0;
-  const uint32_t seq = m->seq;
+namespace {
+
+// Event record that also works as a graph node while the stream is being captured.
+cudaError_t mark(Model* m, int i, bool capturing) {
+  return capturing ? cudaEventRecordWithFlags(m->ev[i], m->stream, cudaEventRecordExternal)
+                   : cudaEventRecord(m->ev[i], m->stream);
+}
+
+// Everything of one step after the inputs are resident in HBM: bump the device step
+// counter, front forward, cut exchange, back segment, front backward, sync, re-layout.
+int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu, bool capturing,
+              std::string* why) {
+  const uint32_t* seq = m->seq_dev;
   const int b = m->batch;
   const bool ralp = m->strategy == RALPB_STRATEGY_RALP;
   cudaStream_t s = m->stream;
-  RALPB_TRY(cudaEventRecord(m->ev[0], s));
-  m->timer.n = 0;
-  set_gemm_timer(m->profiling ? &m->timer : nullptr);
-  struct Reset { ~Reset() { set_gemm_timer(nullptr); } } reset_timer;
+  RALPB_TRY(bump_counter(m->seq_dev, s));
+  ++m->launches;
 
   // ---------------- worker front forward
-  const float* img = static_cast<const float*>(images);
-  const int32_t* lab = labels;
-  if (on_host) {
-    RALPB_TRY(cudaMemcpyAsync(m->img_dev, images, sizeof(float) * b * m->in_h * m->in_w * m->in_c, cudaMemcpyHostToDevice, s));
-    RALPB_TRY(cudaMemcpyAsync(m->lab_dev, labels, sizeof(int32_t) * b, cudaMemcpyHostToDevice, s));
-    img = m->img_dev;
-    lab = m->lab_dev;
-  }
   const FrontLayer& f0 = m->front[0];
   const ActBuf& a0 = m->acts[0];
   if (f0.im2col)
@@ -650,7 +649,7 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
     ++m->launches;
   }
   const bf16* cut_local = cut_dst;
-  RALPB_TRY(cudaEventRecord(m->ev[1], s));
+  RALPB_TRY(mark(m, 1, capturing));
 
   // ---------------- cut exchange + PS back segment
   const size_t cut_bytes = static_cast<size_t>(b) * m->cut_elems * sizeof(bf16);
@@ -670,7 +669,7 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
     int32_t* lab_ps = at<int32_t>(m, m->ps_rank, m->arena_off_lab) + static_cast<size_t>(slot) * b;
     bf16* x_ps = at<bf16>(m, m->ps_rank, m->arena_off_xfc) + static_cast<size_t>(slot) * b * m->cut_elems;
     PeerSignal none{};
-    RALPB_TRY(push_and_signal(lab_ps, lab, static_cast<long long>(b) * 4 / 16, none, 0, m->counters + 1, s));
+    RALPB_TRY(push_and_signal(lab_ps, lab, static_cast<long long>(b) * 4 / 16, none, seq, m->counters + 1, s));
     PeerSignal sig{};
     sig.n = 1;
     sig.flag[0] = at<uint32_t>(m, m->ps_rank, m->arena_off_flags) + kFlagAct + m->rank;
@@ -720,16 +719,79 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
     ++m->launches;
     dcut = m->dcut;
   }
-  RALPB_TRY(cudaEventRecord(m->ev[2], s));
+  RALPB_TRY(mark(m, 2, capturing));
 
   // ---------------- worker front backward
   RALPB_TRY(cudaMemsetAsync(m->G, 0, m->n_front * sizeof(float), s));
   if (launch_front_backward(m, dcut, why)) return 1;
-  RALPB_TRY(cudaEventRecord(m->ev[3], s));
+  RALPB_TRY(mark(m, 3, capturing));
 
   // ---------------- parameter synchronisation + re-layout
   if (sync_params(m, ralp ? m->n_front : m->n_total, lr, mu, why)) return 1;
   if (relayout_weights(m, !ralp, why)) return 1;
+  return 0;
+}
+
+bool graphs_enabled() {
+  const char* e = getenv("RALPB_GRAPH");
+  return e == nullptr || e[0] != '0';
+}
+
+}  // namespace
+
+int model_step(Model* m, const void* images, const int32_t* labels, int on_host, float lr, float mu,
+               std::string* why) {
+  if (m->world > 1 && !m->peers_open) { *why = "ralpb_model_ipc_open has not been called"; return 1; }
+  const int b = m->batch;
+  cudaStream_t s = m->stream;
+  m->seq += 1;
+  RALPB_TRY(cudaEventRecord(m->ev[0], s));
+  const float* img = static_cast<const float*>(images);
+  const int32_t* lab = labels;
+  if (on_host) {
+    RALPB_TRY(cudaMemcpyAsync(m->img_dev, images, sizeof(float) * b * m->in_h * m->in_w * m->in_c, cudaMemcpyHostToDevice, s));
+    RALPB_TRY(cudaMemcpyAsync(m->lab_dev, labels, sizeof(int32_t) * b, cudaMemcpyHostToDevice, s));
+    img = m->img_dev;
+    lab = m->lab_dev;
+  }
+  if (m->profiling || !graphs_enabled()) {
+    m->launches = 0;
+    m->phys_bytes = 0;
+    m->timer.n = 0;
+    set_gemm_timer(m->profiling ? &m->timer : nullptr);
+    struct Reset { ~Reset() { set_gemm_timer(nullptr); } } reset_timer;
+    if (step_body(m, img, lab, lr, mu, false, why)) return 1;
+  } else {
+    if (m->graph == nullptr || m->graph_img != img || m->graph_lab != lab || m->graph_lr != lr || m->graph_mu != mu) {
+      m->launches = 0;
+      m->phys_bytes = 0;
+      RALPB_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      const int rc = step_body(m, img, lab, lr, mu, true, why);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(s, &g);
+      if (rc) { if (g) cudaGraphDestroy(g); return 1; }
+      if (ce != cudaSuccess) { *why = std::string("step capture failed: ") + cudaGetErrorString(ce); return 1; }
+      bool updated = false;
+      if (m->graph != nullptr) {
+        cudaGraphExecUpdateResultInfo info{};
+        updated = cudaGraphExecUpdate(m->graph, g, &info) == cudaSuccess;
+        if (!updated) {
+          cudaGetLastError();
+          cudaGraphExecDestroy(m->graph);
+          m->graph = nullptr;
+        }
+      }
+      cudaError_t ie = updated ? cudaSuccess : cudaGraphInstantiate(&m->graph, g, 0);
+      cudaGraphDestroy(g);
+      if (ie != cudaSuccess) { m->graph = nullptr; *why = std::string("graph instantiate failed: ") + cudaGetErrorString(ie); return 1; }
+      m->graph_img = img; m->graph_lab = lab; m->graph_lr = lr; m->graph_mu = mu;
+      m->graph_launches = m->launches;
+      m->graph_phys = m->phys_bytes;
+    }
+    RALPB_TRY(cudaGraphLaunch(m->graph, s));
+    m->launches = m->graph_launches;
+    m->phys_bytes = m->graph_phys;
+  }
   RALPB_TRY(cudaEventRecord(m->ev[4], s));
   m->stats_valid = true;
   return 0;

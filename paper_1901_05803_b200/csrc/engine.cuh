@@ -88,7 +88,16 @@ struct Model {
   bool peers_open = false;
 
   // step state
-  uint32_t seq = 0;
+  uint32_t seq = 0;                // host mirror of *seq_dev (steps issued)
+  uint32_t* seq_dev = nullptr;     // device step counter: flag value of the exchange kernels
+  // CUDA graph of the step body (everything after the input upload), re-captured when the
+  // input pointers or hyper-parameters change; disabled while profiling or RALPB_GRAPH=0
+  cudaGraphExec_t graph = nullptr;
+  const void* graph_img = nullptr;
+  const void* graph_lab = nullptr;
+  float graph_lr = 0.f, graph_mu = 0.f;
+  int graph_launches = 0;
+  long long graph_phys = 0;
   int launches = 0;
   long long phys_bytes = 0;
   cudaEvent_t ev[6] = {};

@@ -14,7 +14,7 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 }
 
 // Last CTA to finish sets the flags.
-__device__ __forceinline__ void finish_and_signal(const PeerSignal& sig, uint32_t value,
+__device__ __forceinline__ void finish_and_signal(const PeerSignal& sig, const uint32_t* value,
                                                   uint32_t* counter) {
   __threadfence_system();
   __syncthreads();
@@ -23,14 +23,14 @@ __device__ __forceinline__ void finish_and_signal(const PeerSignal& sig, uint32_
     if (prev == gridDim.x - 1) {
       __threadfence_system();
       for (int i = 0; i < sig.n; ++i)
-        if (sig.flag[i] != nullptr) st_release_sys(sig.flag[i], value);
+        if (sig.flag[i] != nullptr) st_release_sys(sig.flag[i], *value);
       *counter = 0;  // re-arm (only this CTA touches it now)
     }
   }
 }
 
 __global__ void push_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, long long n16,
-                            PeerSignal sig, uint32_t value, uint32_t* counter) {
+                            PeerSignal sig, const uint32_t* value, uint32_t* counter) {
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   // 4 independent 16-byte loads in flight per thread
@@ -46,26 +46,34 @@ __global__ void push_kernel(uint4* __restrict__ dst, const uint4* __restrict__ s
 }
 
 cudaError_t push_and_signal(void* dst, const void* src, long long n16, const PeerSignal& sig,
-                            uint32_t value, uint32_t* counter, cudaStream_t s) {
+                            const uint32_t* value, uint32_t* counter, cudaStream_t s) {
   int grid = static_cast<int>(std::max<long long>(1, std::min<long long>((n16 + 511) / 512, num_sms() * 2)));
   push_kernel<<<grid, 512, 0, s>>>(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), n16,
                                    sig, value, counter);
   return cudaGetLastError();
 }
 
-__global__ void signal_kernel(PeerSignal sig, uint32_t value) {
+__global__ void signal_kernel(PeerSignal sig, const uint32_t* value) {
   __threadfence_system();
-  if (threadIdx.x < sig.n && sig.flag[threadIdx.x] != nullptr) st_release_sys(sig.flag[threadIdx.x], value);
+  if (threadIdx.x < sig.n && sig.flag[threadIdx.x] != nullptr) st_release_sys(sig.flag[threadIdx.x], *value);
 }
 
-cudaError_t signal_only(const PeerSignal& sig, uint32_t value, cudaStream_t s) {
+__global__ void bump_kernel(uint32_t* counter) { *counter += 1; }
+
+cudaError_t bump_counter(uint32_t* counter, cudaStream_t s) {
+  bump_kernel<<<1, 1, 0, s>>>(counter);
+  return cudaGetLastError();
+}
+
+cudaError_t signal_only(const PeerSignal& sig, const uint32_t* value, cudaStream_t s) {
   signal_kernel<<<1, 32, 0, s>>>(sig, value);
   return cudaGetLastError();
 }
 
-__global__ void wait_kernel(const uint32_t* flags, int n, uint32_t value) {
+__global__ void wait_kernel(const uint32_t* flags, int n, const uint32_t* value) {
+  const uint32_t target = *value;
   if (threadIdx.x < n) {
-    while (ld_acquire_sys(flags + threadIdx.x) < value) {
+    while (ld_acquire_sys(flags + threadIdx.x) < target) {
       __nanosleep(64);
     }
   }
@@ -73,12 +81,12 @@ __global__ void wait_kernel(const uint32_t* flags, int n, uint32_t value) {
   __threadfence_system();
 }
 
-cudaError_t wait_flags(const uint32_t* flags, int n, uint32_t value, cudaStream_t s) {
+cudaError_t wait_flags(const uint32_t* flags, int n, const uint32_t* value, cudaStream_t s) {
   wait_kernel<<<1, 32, 0, s>>>(flags, n, value);
   return cudaGetLastError();
 }
 
-__global__ void shard_update_kernel(ShardUpdate u, PeerSignal done, uint32_t value, uint32_t* counter) {
+__global__ void shard_update_kernel(ShardUpdate u, PeerSignal done, const uint32_t* value, uint32_t* counter) {
   const long long b4 = u.begin / 4, e4 = u.end / 4;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long i = b4 + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < e4; i += stride) {
@@ -99,7 +107,7 @@ __global__ void shard_update_kernel(ShardUpdate u, PeerSignal done, uint32_t val
   finish_and_signal(done, value, counter);
 }
 
-cudaError_t shard_update(const ShardUpdate& u, const PeerSignal& done, uint32_t value,
+cudaError_t shard_update(const ShardUpdate& u, const PeerSignal& done, const uint32_t* value,
                          uint32_t* counter, cudaStream_t s) {
   long long n4 = (u.end - u.begin) / 4;
   int grid = static_cast<int>(std::max<long long>(1, std::min<long long>((n4 + 255) / 256, num_sms() * 4)));

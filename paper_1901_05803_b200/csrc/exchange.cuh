@@ -29,13 +29,18 @@ struct PeerSignal {
 // once all CTAs' stores are globally visible (system scope).  `counter` is a
 // local zero-initialised word used for last-CTA detection.
 cudaError_t push_and_signal(void* dst, const void* src, long long n16, const PeerSignal& sig,
-                            uint32_t value, uint32_t* counter, cudaStream_t s);
+                            const uint32_t* value, uint32_t* counter, cudaStream_t s);
 
 // Set flags only (after a fence of this kernel's predecessors on the stream).
-cudaError_t signal_only(const PeerSignal& sig, uint32_t value, cudaStream_t s);
+cudaError_t signal_only(const PeerSignal& sig, const uint32_t* value, cudaStream_t s);
 
-// Spin until flags[i] >= value for i in [0, n).
-cudaError_t wait_flags(const uint32_t* flags, int n, uint32_t value, cudaStream_t s);
+// *counter += 1 (the per-step sequence number, first node of the step).
+cudaError_t bump_counter(uint32_t* counter, cudaStream_t s);
+
+// Flag values are read from device memory (`value` points at the rank's step counter) so a
+// captured CUDA graph of the step replays correctly.
+// Spin until flags[i] >= *value for i in [0, n).
+cudaError_t wait_flags(const uint32_t* flags, int n, const uint32_t* value, cudaStream_t s);
 
 // Sharded-PS aggregation over NVLink (reduce-scatter + SGD-momentum + all-gather):
 // for i in this rank's shard [begin, end):
@@ -52,7 +57,7 @@ struct ShardUpdate {
   float lr, mu, gscale;
   float* momentum;       // local, full-size vector (only the shard is touched)
 };
-cudaError_t shard_update(const ShardUpdate& u, const PeerSignal& done, uint32_t value,
+cudaError_t shard_update(const ShardUpdate& u, const PeerSignal& done, const uint32_t* value,
                          uint32_t* counter, cudaStream_t s);
 
 }  // namespace ralpb
