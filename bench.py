@@ -252,7 +252,8 @@ def run_ours(args):
                           "logical_sync_bytes_per_step": stb.logical_bytes},
             "breakdown_ms_rank0": {"front_fwd": st.ms_front_fwd, "back": st.ms_back, "front_bwd": st.ms_front_bwd,
                                    "sync": st.ms_sync, "gemm_sum": prof.ms_gemm, "gemm_launches": prof.gemm_launches},
-            "roofline": {"bound": "tensor", "kernel": "gemm_sm100_kernel (all conv/FC launches of a step)",
+            "roofline": {"bound": "tensor", "kernel": "tcgen05 tensor-core kernels (conv_slab_fwd/conv_slab_wgrad implicit-GEMM convs + gemm_sm100 "
+                                   "FC/im2col GEMMs): algorithmic FLOPs of the step / summed event-timed launch durations",
                          "achieved": achieved, "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
                          "frac": achieved / peaks["bf16_tflops_sustained"] if achieved else None,
                          "peak_source": f"{peak_src} bf16_tflops_sustained", "traffic": traffic,
