@@ -28,6 +28,7 @@ sys.path.insert(0, str(ROOT))
 
 MODEL = "vgg16"
 BATCH = 128
+METRIC = "images/sec per step at 1/2/4/8 B200 (layer-placed vs all-on-PS); sync bytes/step"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -112,8 +113,13 @@ def _cpu_baseline_step(sample_b: int, steps: int):
         ostep.train_step(st, "ralp", 1, [batches[t + 1]])
     dt = time.perf_counter() - t0
     return {"value": sample_b * steps / dt, "unit": "images/s", "cores": torch.get_num_threads(), "kind": "port",
-            "sample": f"{MODEL} 224x224 layer-placed step (oracle/step.py, fp32 torch CPU), W=1, b={sample_b}, "
+            "sample": f"{MODEL} {shape[0]}x{shape[1]} layer-placed step (oracle/step.py, fp32 torch CPU), W=1, b={sample_b}, "
                       f"{steps} timed steps after 1 warm-up, {dt:.1f} s"}
+
+
+def _headline_split():
+    from paper_1901_05803_b200.planner import catalog_lookup, profile
+    return profile(catalog_lookup(MODEL).with_batch_size(BATCH)).split_index
 
 
 def run_reference(args):
@@ -123,12 +129,12 @@ def run_reference(args):
     sample_b = 8
     steps = max(1, min(args.steps, 3))
     cb = _cpu_baseline_step(sample_b, steps)
-    line = {"impl": "reference", "metric": "images/sec per step (layer-placed VGG-16 step)", "value": cb["value"],
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"],
             "unit": "images/s", "n_gpus": args.gpus, "steps": steps, "warmup": 1,
             "ms_per_step": 1e3 * sample_b / cb["value"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{MODEL} 224x224 synthetic, layer-placed (RALP) step, CPU oracle port",
-                       "model": MODEL, "per_worker_batch": sample_b, "split": 18},
+            "config": {"workload": f"{MODEL} synthetic, layer-placed (RALP) step, CPU oracle port",
+                       "model": MODEL, "per_worker_batch": sample_b, "split": _headline_split()},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -236,11 +242,11 @@ def run_ours(args):
 
     if rank == 0:
         line = {
-            "metric": "images/sec per step at 1/2/4/8 B200 (layer-placed vs all-on-PS); sync bytes/step",
+            "metric": METRIC,
             "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"VGG-16 224x224 synthetic, b={BATCH}/worker, W={world}, partitioner split "
+            "config": {"workload": f"{MODEL} {shape[0]}x{shape[1]} synthetic, b={BATCH}/worker, W={world}, partitioner split "
                                    f"{rep.split_index} ({m.layer(rep.split_index).name}), FC tail on rank 0",
                        "model": MODEL, "global_batch": world * BATCH, "per_worker_batch": BATCH,
                        "split": rep.split_index, "parallelism": f"dp{world}+fc-tail-on-ps",
@@ -278,7 +284,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--model", default=MODEL, help="catalog model (BASELINE configs: vgg16 headline, alexnet)")
+    ap.add_argument("--batch", type=int, default=BATCH, help="per-worker batch")
     args = ap.parse_args()
+    globals()["MODEL"] = args.model
+    globals()["BATCH"] = args.batch
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

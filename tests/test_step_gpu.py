@@ -54,7 +54,7 @@ def _fc_boundary(model):
     return next(i for i, l in enumerate(model.layers) if l.kind.value == "fc")
 
 
-def _run(model, strategy, steps, seed=0):
+def _run(model, strategy, steps, seed=0, lr=0.01):
     if strategy == "ralp":
         split = _fc_boundary(model)  # the FC-tail cut (the partitioner's choice at large batch)
         job = JobSpec(model, Strategy.ralp(split), 1)
@@ -71,10 +71,10 @@ def _run(model, strategy, steps, seed=0):
     losses = []
     for t in range(steps):
         imgs, labs = synthetic.batch(seed, t, 0, b, ex.in_shape, ex.classes)
-        ex.step(imgs, labs, lr=0.01, momentum=0.9)
+        ex.step(imgs, labs, lr=lr, momentum=0.9)
         st = ex.stats()
-        loss_o, wire = ostep.train_step(o32, strategy, 1, [(imgs, labs)], lr=0.01, mu=0.9, emulate_bf16=True)
-        ostep.train_step(o64, strategy, 1, [(imgs, labs)], lr=0.01, mu=0.9, emulate_bf16=True, accum64=True)
+        loss_o, wire = ostep.train_step(o32, strategy, 1, [(imgs, labs)], lr=lr, mu=0.9, emulate_bf16=True)
+        ostep.train_step(o64, strategy, 1, [(imgs, labs)], lr=lr, mu=0.9, emulate_bf16=True, accum64=True)
         assert st.logical_bytes == wire == expect_bytes
         losses.append((st.loss, loss_o))
     got = ex.get_params()
@@ -125,4 +125,15 @@ def test_vgg16_one_step_b4():
     model = catalog_lookup("vgg16").with_batch_size(4)
     losses, got, want, want64, init = _run(model, "baseline", steps=1)
     print("vgg16 b=4", losses)
+    _check(losses, got, want, want64, init)
+
+
+def test_alexnet_steps_b4():
+    # AlexNet config of BASELINE.json: 11x11/4 first conv (im2col GEMM), 5x5 conv, overlapping
+    # 3/2 max-pools, FC tail on the PS; small batch so the CPU oracle stays fast.  At lr=0.01
+    # the unnormalised 227x227 input makes step 1 overshoot (loss ~24, a chaotic regime), so
+    # the parity run uses lr=1e-3.
+    model = catalog_lookup("alexnet").with_batch_size(4)
+    losses, got, want, want64, init = _run(model, "ralp", steps=3, lr=1e-3)
+    print("alexnet b=4", losses)
     _check(losses, got, want, want64, init)
