@@ -50,11 +50,13 @@ int ralpb_gemm_bf16(const void* a, long long a_rows, long long a_cols, long long
  * (layers.py:87-103) with ReLU fused.  Outputs are written on interior
  * pixels only: allocate output buffers with zero borders.
  *   w:  [cout][k*k][cin] bf16      wd: [cin][k*k][cout] bf16 (tap-reversed transpose)
- *   dw: [cout][k*k][cin] fp32 and db: [cout] fp32 (may be NULL), accumulated (caller zeroes). */
+ *   dw: [cout][k*k][cin] fp32 and db: [cout] fp32 (may be NULL), accumulated (caller zeroes).
+ *   colsum (dgrad, may be NULL): colsum[ci] += sum over pixels of the stored bf16 dx -- the bias
+ *   gradient of the convolution that produced the masked activation, fused into this producer. */
 int ralpb_conv_fwd(const void* x_pad, const void* w, const float* bias, void* y_pad, int n, int h,
                    int w_, int cin, int cout, int k, int pad, int relu, void* stream);
-int ralpb_conv_dgrad(const void* dy_pad, const void* wd, const void* mask_pad, void* dx_pad, int n,
-                     int h, int w_, int cin, int cout, int k, int pad, void* stream);
+int ralpb_conv_dgrad(const void* dy_pad, const void* wd, const void* mask_pad, void* dx_pad, float* colsum,
+                     int n, int h, int w_, int cin, int cout, int k, int pad, void* stream);
 int ralpb_conv_wgrad(const void* x_pad, const void* dy_pad, float* dw, float* db, int n, int h, int w_,
                      int cin, int cout, int k, int pad, void* stream);
 
@@ -69,8 +71,10 @@ int ralpb_pack_im2col(const float* x, int n, int h, int w, int c, int k, int str
 /* Max pool (infer_pool, layers.py:106-114; stride defaults to window). */
 int ralpb_maxpool_fwd(const void* x, int n, int h, int w, int c, int pad_in, int k, int stride,
                       void* y, int pad_out, void* stream);
+/* colsum (may be NULL, c <= 1024): colsum[ch] += sum of the stored dx (bias gradient of the conv
+ * feeding the pool, fused into the pool backward). */
 int ralpb_maxpool_bwd(const void* x, const void* dy, int n, int h, int w, int c, int pad_in, int k,
-                      int stride, int pad_out, void* dx, void* stream);
+                      int stride, int pad_out, void* dx, float* colsum, void* stream);
 /* Softmax cross-entropy (the LOSS layer, layers.py:161-163): per-row loss and
  * dlogits = (softmax - onehot) * scale (bf16). */
 int ralpb_softmax_xent(const float* logits, int rows, int classes, long long ld,

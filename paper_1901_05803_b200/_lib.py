@@ -28,12 +28,12 @@ SIGNATURES: dict[str, tuple] = {
     "ralpb_gemm_bf16": (c_i, [c_vp, c_ll, c_ll, c_ll, c_i, c_vp, c_ll, c_ll, c_ll, c_i, c_i, c_i, c_ll,
                               c_vp, c_i, c_ll, c_ll, c_fp, c_i, c_vp, c_ll, c_i, c_i, c_vp]),
     "ralpb_conv_fwd": (c_i, [c_vp, c_vp, c_fp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),
-    "ralpb_conv_dgrad": (c_i, [c_vp, c_vp, c_vp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),
+    "ralpb_conv_dgrad": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),
     "ralpb_conv_wgrad": (c_i, [c_vp, c_vp, c_fp, c_fp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),
     "ralpb_pack_input": (c_i, [c_fp, c_i, c_i, c_i, c_i, c_vp, c_i, c_i, c_vp]),
     "ralpb_pack_im2col": (c_i, [c_fp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp, c_vp]),
     "ralpb_maxpool_fwd": (c_i, [c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp, c_i, c_vp]),
-    "ralpb_maxpool_bwd": (c_i, [c_vp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp, c_vp]),
+    "ralpb_maxpool_bwd": (c_i, [c_vp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp, c_vp, c_vp]),
     "ralpb_softmax_xent": (c_i, [c_fp, c_i, c_i, c_ll, c_vp, c_f, c_fp, c_vp, c_ll, c_vp]),
     "ralpb_sgd_momentum": (c_i, [c_fp, c_fp, c_fp, c_ll, c_f, c_f, c_f, c_vp]),
     "ralpb_colsum_bf16": (c_i, [c_vp, c_ll, c_i, c_ll, c_fp, c_vp]),

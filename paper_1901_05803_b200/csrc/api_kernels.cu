@@ -49,11 +49,12 @@ int ralpb_conv_fwd(const void* x_pad, const void* w, const float* bias, void* y_
   return set_status(conv_fwd(g, x_pad, w, bias, y_pad, relu, static_cast<cudaStream_t>(stream), &why), why);
 }
 
-int ralpb_conv_dgrad(const void* dy_pad, const void* wd, const void* mask_pad, void* dx_pad, int n,
-                     int h, int w_, int cin, int cout, int k, int pad, void* stream) {
+int ralpb_conv_dgrad(const void* dy_pad, const void* wd, const void* mask_pad, void* dx_pad, float* colsum,
+                     int n, int h, int w_, int cin, int cout, int k, int pad, void* stream) {
   std::string why;
   ConvGeom g{n, h, w_, cin, cout, k, pad};
-  return set_status(conv_dgrad(g, dy_pad, wd, mask_pad, dx_pad, static_cast<cudaStream_t>(stream), &why), why);
+  return set_status(conv_dgrad(g, dy_pad, wd, mask_pad, dx_pad, colsum, static_cast<cudaStream_t>(stream), &why),
+                    why);
 }
 
 int ralpb_conv_wgrad(const void* x_pad, const void* dy_pad, float* dw, float* db, int n, int h, int w_,

@@ -31,9 +31,9 @@ int ralpb_maxpool_fwd(const void* x, int n, int h, int w, int c, int pad_in, int
                                 RALPB_S(stream)), "maxpool_fwd");
 }
 int ralpb_maxpool_bwd(const void* x, const void* dy, int n, int h, int w, int c, int pad_in, int k,
-                      int stride, int pad_out, void* dx, void* stream) {
+                      int stride, int pad_out, void* dx, float* colsum, void* stream) {
   return set_status(maxpool_bwd(RALPB_CBF(x), RALPB_CBF(dy), n, h, w, c, pad_in, k, stride, pad_out,
-                                RALPB_BF(dx), RALPB_S(stream)), "maxpool_bwd");
+                                RALPB_BF(dx), colsum, RALPB_S(stream)), "maxpool_bwd");
 }
 int ralpb_softmax_xent(const float* logits, int rows, int classes, long long ld,
                        const int32_t* labels, float scale, float* row_loss, void* dlogits,

@@ -121,15 +121,17 @@ static bool pick_slab(bool eligible, bool auto_choice) {
 cudaError_t conv_fwd(const ConvGeom& g, const void* x_pad, const void* w, const float* bias, void* y_pad,
                      int relu, cudaStream_t s, std::string* why) {
   if (pick_slab(slab_fwd_ok(g, g.cin, g.cout), true))
-    return conv_slab_fwd(g, x_pad, w, g.cin, g.cout, bias, relu, nullptr, y_pad, s, why);
+    return conv_slab_fwd(g, x_pad, w, g.cin, g.cout, bias, relu, nullptr, y_pad, nullptr, s, why);
   return conv_fwd_flat(g, x_pad, w, bias, y_pad, relu, s, why);
 }
 
 cudaError_t conv_dgrad(const ConvGeom& g, const void* dy_pad, const void* wd, const void* mask_pad,
-                       void* dx_pad, cudaStream_t s, std::string* why) {
+                       void* dx_pad, float* colsum, cudaStream_t s, std::string* why) {
   if (pick_slab(slab_fwd_ok(g, g.cout, g.cin), true))
-    return conv_slab_fwd(g, dy_pad, wd, g.cout, g.cin, nullptr, 0, mask_pad, dx_pad, s, why);
-  return conv_dgrad_flat(g, dy_pad, wd, mask_pad, dx_pad, s, why);
+    return conv_slab_fwd(g, dy_pad, wd, g.cout, g.cin, nullptr, 0, mask_pad, dx_pad, colsum, s, why);
+  cudaError_t e = conv_dgrad_flat(g, dy_pad, wd, mask_pad, dx_pad, s, why);
+  if (e != cudaSuccess || colsum == nullptr) return e;
+  return colsum_bf16(static_cast<const __nv_bfloat16*>(dx_pad), g.q(), g.cin, g.cin, colsum, s);
 }
 
 cudaError_t conv_wgrad(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw, float* db,

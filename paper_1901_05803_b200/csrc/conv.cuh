@@ -32,8 +32,10 @@ cudaError_t conv_fwd(const ConvGeom& g, const void* x_pad, const void* w, const 
                      void* y_pad, int relu, cudaStream_t s, std::string* why);
 // dx_pad = conv_transpose(dy_pad, w) * (mask_pad > 0 if mask_pad).
 // wd: [cin][k*k][cout] bf16, wd[ci][t][co] = w[co][k*k-1-t][ci].
+// colsum (optional): colsum[ci] += sum over pixels of the stored bf16 dx -- the bias gradient of
+// the previous convolution, fused into this producer so the wgrad kernel needs no bias pass.
 cudaError_t conv_dgrad(const ConvGeom& g, const void* dy_pad, const void* wd, const void* mask_pad,
-                       void* dx_pad, cudaStream_t s, std::string* why);
+                       void* dx_pad, float* colsum, cudaStream_t s, std::string* why);
 // dw[co][t][ci] += sum_q dy[q][co] * x[q + off(t)][ci];  db[co] += sum_q dy[q][co] if db.
 cudaError_t conv_wgrad(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw, float* db,
                        cudaStream_t s, std::string* why);
@@ -50,7 +52,8 @@ cudaError_t conv_wgrad_flat(const ConvGeom& g, const void* x_pad, const void* dy
 bool slab_fwd_ok(const ConvGeom& g, int c, int cout);
 bool slab_wgrad_ok(const ConvGeom& g);
 cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, int c, int cout, const float* bias,
-                          int relu, const void* mask_pad, void* y_pad, cudaStream_t s, std::string* why);
+                          int relu, const void* mask_pad, void* y_pad, float* colsum, cudaStream_t s,
+                          std::string* why);
 cudaError_t conv_slab_wgrad(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw, float* db,
                             cudaStream_t s, std::string* why);
 

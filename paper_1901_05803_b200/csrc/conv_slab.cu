@@ -54,7 +54,7 @@ bool encode_mat(CUtensorMap* tm, const void* ptr, long long rows, long long cols
 }
 
 int align1k(int x) { return (x + 1023) & ~1023; }
-constexpr int kSmemBudget = 227 * 1024 - 1024 - 512;
+constexpr int kSmemBudget = 227 * 1024 - 1024 - 512 - 2048;
 
 }  // namespace
 
@@ -68,7 +68,9 @@ bool slab_wgrad_ok(const ConvGeom& g) {
 }
 
 cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, int c, int cout, const float* bias,
-                          int relu, const void* mask_pad, void* y_pad, cudaStream_t s, std::string* why) {
+                          int relu, const void* mask_pad, void* y_pad, float* colsum, cudaStream_t s,
+                          std::string* why) {
+  if (colsum != nullptr && cout > 512) { *why = "slab conv: fused colsum supports <= 512 channels"; return cudaErrorInvalidValue; }
   SlabConvParams p;
   std::memset(&p, 0, sizeof(p));
   p.n = g.n; p.h = g.h; p.w = g.w; p.hp = g.hp(); p.wp = g.wp(); p.pad = g.pad; p.k = g.k; p.taps = g.taps();
@@ -115,12 +117,13 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
   p.bias = bias;
   p.relu = relu;
   p.mask = static_cast<const __nv_bfloat16*>(mask_pad);
+  p.colsum = colsum;
   if (const char* e = getenv("RALPB_DEBUG")) p.dbg = atoi(e);
   if (!encode_act(&p.tmX, x_pad, c, g.wp(), g.hp(), g.n, p.kb, p.sw, p.sh, p.row_bytes, why))
     return cudaErrorInvalidValue;
   if (!encode_mat(&p.tmB, w, cout, static_cast<long long>(g.taps()) * c, p.kb, p.bn, p.row_bytes, why))
     return cudaErrorInvalidValue;
-  const int smem = 1024 + p.na * p.slab_stage + p.nb * p.b_stage + 512;
+  const int smem = 1024 + p.na * p.slab_stage + p.nb * p.b_stage + 512 + 2048;  // barriers, colsum
   const long long total = static_cast<long long>(g.n) * p.n_hb * p.n_wb * p.n_nt;
   const int grid = static_cast<int>(std::min<long long>(total, num_sms()));
   const int ks = p.kb / 16;

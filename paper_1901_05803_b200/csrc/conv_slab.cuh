@@ -58,6 +58,7 @@ struct alignas(64) SlabConvParams {
   const float* bias;
   int relu;
   const __nv_bfloat16* mask;
+  float* colsum;        // optional: += per-channel sum over pixels of the stored (bf16) output
   // wgrad
   float* dw;
   float* db;
@@ -86,8 +87,11 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
   uint64_t* tfull = b_empty + p.nb;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* s_col = reinterpret_cast<float*>(tmem_slot + 4);  // [cout] when p.colsum
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (p.colsum != nullptr)
+    for (int i = threadIdx.x; i < p.cout; i += blockDim.x) s_col[i] = 0.f;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.tmX);
     tma_prefetch(&p.tmB);
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
           tmem_ld32(tb + c, rr);
           tmem_wait_ld();
           const int n0 = nt * p.bn + c;
-          if (!valid || n0 >= p.cout || (p.dbg & 1)) continue;
+          if (n0 >= p.cout || (p.dbg & 1)) continue;   // warp-uniform
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
@@ -230,9 +234,9 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
           }
-          __nv_bfloat16* o = p.out + orow * p.cout + n0;
-          if (p.mask != nullptr) {
-            const __nv_bfloat16* mp = p.mask + orow * p.cout + n0;
+          const long long oidx = orow * p.cout + n0;
+          if (p.mask != nullptr && valid) {
+            const __nv_bfloat16* mp = p.mask + oidx;
             if (full) {
 #pragma unroll
               for (int j4 = 0; j4 < 4; ++j4) {
@@ -247,18 +251,40 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
                 if (!(__bfloat162float(mp[j]) > 0.f)) v[j] = 0.f;
             }
           }
-          if (full) {
+          uint32_t pk[16];
 #pragma unroll
-            for (int j4 = 0; j4 < 4; ++j4) {
-              uint4 u;
-              u.x = pack_bf16(v[j4 * 8 + 0], v[j4 * 8 + 1]);
-              u.y = pack_bf16(v[j4 * 8 + 2], v[j4 * 8 + 3]);
-              u.z = pack_bf16(v[j4 * 8 + 4], v[j4 * 8 + 5]);
-              u.w = pack_bf16(v[j4 * 8 + 6], v[j4 * 8 + 7]);
-              *reinterpret_cast<uint4*>(o + j4 * 8) = u;
+          for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
+          if (valid) {
+            __nv_bfloat16* o = p.out + oidx;
+            if (full) {
+#pragma unroll
+              for (int j4 = 0; j4 < 4; ++j4)
+                *reinterpret_cast<uint4*>(o + j4 * 8) = make_uint4(pk[4 * j4], pk[4 * j4 + 1], pk[4 * j4 + 2], pk[4 * j4 + 3]);
+            } else {
+              _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n0 + j < p.cout) o[j] = __float2bfloat16_rn(v[j]);
             }
-          } else {
-            _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n0 + j < p.cout) o[j] = __float2bfloat16_rn(v[j]);
+          }
+          if (p.colsum != nullptr) {
+            // sum of the stored bf16 values over this warp's 32 pixels: transpose-reduce so
+            // that lane l ends with channel n0 + l (31 shuffles), then one shared atomic
+            float r[32];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&pk[j]);
+              r[2 * j] = valid ? __low2float(b2) : 0.f;
+              r[2 * j + 1] = valid ? __high2float(b2) : 0.f;
+            }
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+              const bool up = lane & off;
+#pragma unroll
+              for (int j = 0; j < off; ++j) {
+                const float send = up ? r[j] : r[j + off];
+                const float keep = up ? r[j + off] : r[j];
+                r[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+              }
+            }
+            if (n0 + lane < p.cout) atomicAdd(&s_col[n0 + lane], r[0]);
           }
         }
       }
@@ -273,6 +299,8 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, p.tmem_cols);
   }
+  if (p.colsum != nullptr)
+    for (int i = threadIdx.x; i < p.cout; i += blockDim.x) atomicAdd(p.colsum + i, s_col[i]);
 }
 
 // ------------------------------------------------------------------ backward-filter

@@ -172,11 +172,32 @@ cudaError_t maxpool_fwd(const __nv_bfloat16* x, int n, int h, int w, int c, int 
   return cudaGetLastError();
 }
 
+// Bias gradient of the convolution feeding a max-pool, fused into the pool backward: every
+// thread keeps a fixed 8-channel group (the block size and the grid stride are multiples of
+// c/8), sums the bf16 values it stores, and the block folds them through shared memory into
+// one global atomic per channel.
+constexpr int kPoolColsumMax = 1024;
+__device__ __forceinline__ void block_colsum_flush(const float* csum, int cg, int c, float* s_col, float* colsum) {
+  for (int i = threadIdx.x; i < c; i += blockDim.x) s_col[i] = 0.f;
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < 8; ++e) atomicAdd(&s_col[cg * 8 + e], csum[e]);
+  __syncthreads();
+  for (int i = threadIdx.x; i < c; i += blockDim.x) atomicAdd(colsum + i, s_col[i]);
+}
+
+static int pool_threads(int c) {  // a multiple of c/8 (fixed channel group per thread)
+  const int cv = c / 8;
+  return cv <= 256 ? (256 / cv) * cv : 256;
+}
+
 // One thread = one input position x 8 channels; loops over the windows covering it.
 __global__ void maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ x,
                                    const __nv_bfloat16* __restrict__ dy, int n, int h, int w, int c,
                                    int pi, int k, int st, int po, int oh, int ow,
-                                   __nv_bfloat16* __restrict__ dx) {
+                                   __nv_bfloat16* __restrict__ dx, float* __restrict__ colsum) {
+  __shared__ float s_col[kPoolColsumMax];
+  float csum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   const int hp = h + 2 * pi, wp = w + 2 * pi;
   const int ohp = oh + 2 * po, owp = ow + 2 * po;
   const int cv = c / 8;
@@ -233,9 +254,13 @@ __global__ void maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ x,
     uint4 res;
     __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&res);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) ob[e] = __float2bfloat16_rn(g[e]);
+    for (int e = 0; e < 8; ++e) {
+      ob[e] = __float2bfloat16_rn(g[e]);
+      csum[e] += __bfloat162float(ob[e]);
+    }
     *reinterpret_cast<uint4*>(dx + pos * c + cg * 8) = res;
   }
+  if (colsum != nullptr) block_colsum_flush(csum, threadIdx.x % cv, c, s_col, colsum);
 }
 
 // Disjoint windows (stride == window == K): one thread per output window x 8 channels reads
@@ -244,7 +269,10 @@ __global__ void maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ x,
 template <int K>
 __global__ void maxpool_bwd_disjoint_kernel(const __nv_bfloat16* __restrict__ x,
                                             const __nv_bfloat16* __restrict__ dy, int n, int h, int w, int c,
-                                            int pi, int po, int oh, int ow, __nv_bfloat16* __restrict__ dx) {
+                                            int pi, int po, int oh, int ow, __nv_bfloat16* __restrict__ dx,
+                                            float* __restrict__ colsum) {
+  __shared__ float s_col[kPoolColsumMax];
+  float csum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   const int cv = c >> 3;
   const int total = n * oh * ow * cv;
   const int hp = h + 2 * pi, wp = w + 2 * pi;
@@ -282,25 +310,37 @@ __global__ void maxpool_bwd_disjoint_kernel(const __nv_bfloat16* __restrict__ x,
       uint4 out;
       __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&out);
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        ob[e] = (arg[e] == q && __bfloat162float(xb[e]) > 0.f) ? db[e] : __float2bfloat16_rn(0.f);
+      for (int e = 0; e < 8; ++e) {
+        const bool hit = arg[e] == q && __bfloat162float(xb[e]) > 0.f;
+        ob[e] = hit ? db[e] : __float2bfloat16_rn(0.f);
+        if (hit) csum[e] += __bfloat162float(db[e]);
+      }
       *reinterpret_cast<uint4*>(dx + base + (static_cast<long long>(q / K) * wp + q % K) * c) = out;
     }
   }
+  if (colsum != nullptr) block_colsum_flush(csum, threadIdx.x % cv, c, s_col, colsum);
 }
 
 cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* dy, int n, int h, int w,
-                        int c, int pad_in, int k, int st, int pad_out, __nv_bfloat16* dx,
+                        int c, int pad_in, int k, int st, int pad_out, __nv_bfloat16* dx, float* colsum,
                         cudaStream_t s) {
   if (c % 8 != 0) return cudaErrorInvalidValue;
+  if (colsum != nullptr && (c > kPoolColsumMax || c / 8 > 256)) return cudaErrorInvalidValue;
   int oh = (h - k) / st + 1, ow = (w - k) / st + 1;
   const long long windows = static_cast<long long>(n) * oh * ow * (c / 8);
+  const int threads = pool_threads(c);
+  // with a fused column sum the grid stays small (one global atomic per channel per block)
+  auto grid = [&](long long work) {
+    const long long cap = static_cast<long long>(num_sms()) * (colsum != nullptr ? 4 : 16);
+    return static_cast<int>(std::max<long long>(1, std::min((work + threads - 1) / threads, cap)));
+  };
   if (k == st && k == 2 && windows < (1LL << 31)) {
-    maxpool_bwd_disjoint_kernel<2><<<grid_for(windows, 256), 256, 0, s>>>(x, dy, n, h, w, c, pad_in, pad_out, oh, ow, dx);
+    maxpool_bwd_disjoint_kernel<2><<<grid(windows), threads, 0, s>>>(x, dy, n, h, w, c, pad_in, pad_out, oh, ow, dx,
+                                                                     colsum);
     return cudaGetLastError();
   }
   long long total = static_cast<long long>(n) * (h + 2 * pad_in) * (w + 2 * pad_in) * (c / 8);
-  maxpool_bwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, dy, n, h, w, c, pad_in, k, st, pad_out, oh, ow, dx);
+  maxpool_bwd_kernel<<<grid(total), threads, 0, s>>>(x, dy, n, h, w, c, pad_in, k, st, pad_out, oh, ow, dx, colsum);
   return cudaGetLastError();
 }
 

@@ -25,9 +25,10 @@ cudaError_t maxpool_fwd(const __nv_bfloat16* x, int n, int h, int w, int c, int 
                         int st, __nv_bfloat16* y, int pad_out, cudaStream_t s);
 // dx[i] = sum over windows containing i where i is the (first) argmax: dy[window],
 // then times (x[i] > 0) (the ReLU of the producing conv).  dx has x's padded layout,
-// border written as zero.
+// border written as zero.  colsum (optional, c <= 1024): colsum[ch] += sum of the stored dx
+// (the producing conv's bias gradient).
 cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* dy, int n, int h, int w,
-                        int c, int pad_in, int k, int st, int pad_out, __nv_bfloat16* dx,
+                        int c, int pad_in, int k, int st, int pad_out, __nv_bfloat16* dx, float* colsum,
                         cudaStream_t s);
 
 // Softmax cross-entropy over rows of fp32 logits (row stride ld).  Writes per-row

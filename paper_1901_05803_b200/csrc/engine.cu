@@ -503,15 +503,23 @@ int launch_front_backward(Model* m, const bf16* dcut, std::string* why) {
   // cur = gradient w.r.t. the output of layer i (for a conv: already ReLU-masked, i.e. the
   // pre-activation gradient); gacts[i] receives the gradient w.r.t. its input.
   const bf16* cur = dcut;
+  bool db_done = false;  // the bias gradient of the layer `cur` belongs to is already summed
   for (int i = static_cast<int>(m->front.size()) - 1; i >= 0; --i) {
     FrontLayer& f = m->front[i];
     const ActBuf& in = m->acts[i];
     const ActBuf& out = m->acts[i + 1];
+    // bias gradient of a (non-im2col) conv i-1 is summed by the kernel that produces its dY
+    float* prev_db = (i > 0 && m->front[i - 1].kind == RALPB_CONV && !m->front[i - 1].im2col &&
+                      m->front[i - 1].g.cout <= 512)
+                         ? m->G + m->front[i - 1].b_off
+                         : nullptr;
     if (f.kind == RALPB_POOL) {
       bf16* dst = m->gacts[i];
-      RALPB_TRY(maxpool_bwd(in.ptr, cur, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.pad, dst, m->stream));
+      RALPB_TRY(maxpool_bwd(in.ptr, cur, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.pad, dst, prev_db,
+                            m->stream));
       ++m->launches;
       cur = dst;
+      db_done = prev_db != nullptr;
     } else if (f.im2col) {
       // dW[co][j] += sum_rows dY[row][co] * patches[row][j]  (j = kpad incl. the bias column)
       GemmDesc d;
@@ -523,14 +531,16 @@ int launch_front_backward(Model* m, const bf16* dcut, std::string* why) {
       RALPB_TRY(gemm_launch(d, m->stream, why));
       ++m->launches;
     } else {
-      RALPB_TRY(conv_wgrad(f.g, in.ptr, cur, m->G + f.w_off, m->G + f.b_off, m->stream, why));
+      // db of this layer: already summed by the producer of `cur` unless `cur` is the cut gradient
+      RALPB_TRY(conv_wgrad(f.g, in.ptr, cur, m->G + f.w_off, db_done ? nullptr : m->G + f.b_off, m->stream, why));
       ++m->launches;
       if (i > 0) {
         bf16* dst = m->gacts[i];
         const bool mask = m->front[i - 1].kind == RALPB_CONV;
-        RALPB_TRY(conv_dgrad(f.g, cur, f.wd, mask ? in.ptr : nullptr, dst, m->stream, why));
+        RALPB_TRY(conv_dgrad(f.g, cur, f.wd, mask ? in.ptr : nullptr, dst, prev_db, m->stream, why));
         ++m->launches;
         cur = dst;
+        db_done = prev_db != nullptr;
       }
     }
   }

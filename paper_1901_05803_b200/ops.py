@@ -49,11 +49,12 @@ def conv_fwd(x_pad, w, bias, *, n, h, w_, cin, cout, k, pad, relu=True, out=None
     return out
 
 
-def conv_dgrad(dy_pad, wd, mask_pad, *, n, h, w_, cin, cout, k, pad, out=None):
+def conv_dgrad(dy_pad, wd, mask_pad, *, n, h, w_, cin, cout, k, pad, out=None, colsum=None):
+    """dx (and, if `colsum` is given, colsum += per-channel sum of the stored dx)."""
     if out is None:
         out = torch.zeros(n, h + 2 * pad, w_ + 2 * pad, cin, dtype=_BF16, device=dy_pad.device)
-    call("ralpb_conv_dgrad", dy_pad.data_ptr(), wd.data_ptr(), _p(mask_pad), out.data_ptr(), n, h, w_, cin,
-         cout, k, pad, _stream())
+    call("ralpb_conv_dgrad", dy_pad.data_ptr(), wd.data_ptr(), _p(mask_pad), out.data_ptr(), _p(colsum), n, h, w_,
+         cin, cout, k, pad, _stream())
     return out
 
 
@@ -88,10 +89,10 @@ def maxpool_fwd(x_pad, *, n, h, w, c, pad_in, k, stride, pad_out):
     return y
 
 
-def maxpool_bwd(x_pad, dy, *, n, h, w, c, pad_in, k, stride, pad_out):
+def maxpool_bwd(x_pad, dy, *, n, h, w, c, pad_in, k, stride, pad_out, colsum=None):
     dx = torch.zeros_like(x_pad)  # borders / uncovered positions are not written
     call("ralpb_maxpool_bwd", x_pad.data_ptr(), dy.data_ptr(), n, h, w, c, pad_in, k, stride, pad_out,
-         dx.data_ptr(), _stream())
+         dx.data_ptr(), _p(colsum), _stream())
     return dx
 
 

@@ -98,7 +98,8 @@ def test_conv_dgrad(case):
     w32 = torch.randn(cout, k * k, cin, generator=g, device=DEV) * (2.0 / (k * k * cin)) ** 0.5
     wf, wd = ops.conv_weight_prep(w32)
     mask = _pad(torch.relu(_bf(n, h, w, cin, gen=g).float()).to(torch.bfloat16), pad).contiguous()
-    dx = ops.conv_dgrad(dy, wd, mask, n=n, h=h, w_=w, cin=cin, cout=cout, k=k, pad=pad)
+    colsum = torch.zeros(cin, device=DEV)
+    dx = ops.conv_dgrad(dy, wd, mask, n=n, h=h, w_=w, cin=cin, cout=cout, k=k, pad=pad, colsum=colsum)
     dyr = dy[:, pad:pad + h, pad:pad + w, :].permute(0, 3, 1, 2).float()
     wr = wf.float().view(cout, k, k, cin).permute(0, 3, 1, 2)
     ref = F.conv_transpose2d(dyr, wr, padding=pad).permute(0, 2, 3, 1)
@@ -107,6 +108,9 @@ def test_conv_dgrad(case):
     border = dx.clone()
     border[:, pad:pad + h, pad:pad + w, :] = 0
     assert border.abs().max().item() == 0.0
+    # fused bias gradient of the producing conv: the sum of the stored bf16 dx per channel
+    want = dx.float().sum(dim=(0, 1, 2))
+    _close(colsum, want, rtol=1e-4, atol=1e-4 * dx.float().abs().sum(dim=(0, 1, 2)).max().item())
 
 
 @pytest.mark.parametrize("case", CONV_CASES)
@@ -155,10 +159,30 @@ def test_pool_fwd_bwd():
     ref = F.max_pool2d(xr, 2)
     torch.testing.assert_close(y[:, 1:-1, 1:-1, :].float(), ref.permute(0, 2, 3, 1), rtol=0, atol=0)
     dy = _bf(n, h // 2, w // 2, c, gen=g)
-    dx = ops.maxpool_bwd(x, dy.contiguous(), n=n, h=h, w=w, c=c, pad_in=pad, k=2, stride=2, pad_out=0)
+    colsum = torch.zeros(c, device=DEV)
+    dx = ops.maxpool_bwd(x, dy.contiguous(), n=n, h=h, w=w, c=c, pad_in=pad, k=2, stride=2, pad_out=0,
+                         colsum=colsum)
     ref.backward(dy.permute(0, 3, 1, 2).float())
     refdx = xr.grad.permute(0, 2, 3, 1) * (xr.detach().permute(0, 2, 3, 1) > 0)
     torch.testing.assert_close(dx[:, pad:pad + h, pad:pad + w, :].float(), refdx, rtol=0, atol=0)
+    torch.testing.assert_close(colsum, refdx.sum(dim=(0, 1, 2)), rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("c", [64, 192])
+def test_pool_bwd_overlapping_colsum(c):
+    # AlexNet's 3/2 pools (generic kernel); c = 192 -> 24 channel groups (block size 240)
+    n, h, w, pad = 2, 13, 13, 0
+    g = torch.Generator(device=DEV).manual_seed(16)
+    x = torch.relu(_bf(n, h, w, c, gen=g).float()).to(torch.bfloat16).contiguous()
+    oh = (h - 3) // 2 + 1
+    dy = _bf(n, oh, oh, c, gen=g).contiguous()
+    colsum = torch.zeros(c, device=DEV)
+    dx = ops.maxpool_bwd(x, dy, n=n, h=h, w=w, c=c, pad_in=0, k=3, stride=2, pad_out=0, colsum=colsum)
+    xr = x.permute(0, 3, 1, 2).float().requires_grad_(True)
+    F.max_pool2d(xr, 3, 2).backward(dy.permute(0, 3, 1, 2).float())
+    refdx = xr.grad.permute(0, 2, 3, 1) * (x.float() > 0)
+    torch.testing.assert_close(dx.float(), refdx.to(torch.bfloat16).float(), rtol=1e-2, atol=1e-2)
+    torch.testing.assert_close(colsum, dx.float().sum(dim=(0, 1, 2)), rtol=1e-5, atol=1e-5)
 
 
 def test_softmax_xent():
