@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <cstring>
 #include "conv.cuh"
+#include "elementwise.cuh"
 #include "conv_slab.cuh"
 
 namespace ralpb {
@@ -178,6 +179,24 @@ cudaError_t conv_slab_wgrad(const ConvGeom& g, const void* x_pad, const void* dy
   const int smem = 1024 + 4096 + p.na * (p.slab_stage + p.b_stage) + 512;
   const long long units = static_cast<long long>(p.n_ci_blocks) * p.n_co_blocks * p.n_pix_blocks;
   const int grid = static_cast<int>(std::min<long long>(units, num_sms()));
+  // CTA-pair kernel (M=256 x N=128 UMMAs) when the output channels come in 128s
+  const char* wenv = getenv("RALPB_WGRAD");
+  const bool pair = g.cout % 128 == 0 && !(wenv != nullptr && std::strcmp(wenv, "single") == 0);
+  if (pair) {
+    p.n_co_blocks = g.cout / 128;
+    p.idesc = umma_idesc_bf16(256, 128, true, true);
+    const int smem2 = 1024 + p.na * (p.slab_stage + p.b_stage) + 512;
+    const long long units2 = static_cast<long long>(p.n_ci_blocks) * p.n_co_blocks * p.n_pix_blocks;
+    const int clusters = static_cast<int>(std::min<long long>(units2, num_sms() / 2));
+    auto go2 = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      launch_timed([&] { kern<<<2 * clusters, 256, smem2, s>>>(p); }, s);
+    };
+    if (bh == 14) go2(conv_slab_wgrad_pair_kernel<14>); else go2(conv_slab_wgrad_pair_kernel<16>);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || db == nullptr) return e;
+    return colsum_bf16(static_cast<const __nv_bfloat16*>(dy_pad), g.q(), g.cout, g.cout, db, s);
+  }
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     launch_timed([&] { kern<<<grid, 256, smem, s>>>(p); }, s);

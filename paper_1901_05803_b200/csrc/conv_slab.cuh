@@ -464,4 +464,173 @@ __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_co
   }
 }
 
+// ------------------------------------------------------------------ backward-filter, CTA pairs
+// The single-CTA kernel above issues N=64 UMMAs whose A+B shared-memory reads (6 KB per
+// 128x64x16 MMA) exceed the tensor core's math time: it is smem-bound at ~55 cycles/MMA
+// (profiles/r01: the smem->tensor-core pipe at 84-86 %).  Here two CTAs of a cluster issue
+// cta_group::2 UMMAs of M = 256 (2 x (tap pair, 64 ci)) x N = 128 output channels: each SM
+// reads its 4 KB of A plus its 2 KB half of B per MMA (48 cycles) against 64 cycles of math,
+// so the pair is tensor-bound.  TMEM per SM is 128 lanes x N per accumulator, so the 9 taps
+// are covered by three accumulators: CTA 1's slab is CTA 0's shifted down two rows, and
+//   MMA 0: base tap (0,0), atom distance 1 px  -> CTA0 taps (0,0),(0,1)  CTA1 (2,0),(2,1)
+//   MMA 1: base tap (0,2), atom distance 1 row -> CTA0 taps (0,2),(1,2)  CTA1 (2,2), -
+//   MMA 2: base tap (1,0), atom distance 1 px  -> CTA0 taps (1,0),(1,1)  CTA1  -  , -
+// (3 of 12 slots unused: 75 % of the pair's MMA work is useful, vs 4.5/6 x smem-bound for the
+// single-CTA kernel).  The bias gradient is not formed here (the dY producers sum it).
+template <int BH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    conv_slab_wgrad_pair_kernel(const __grid_constant__ SlabConvParams p) {
+  constexpr int SW = 10;
+  constexpr int KSTEPS = BH / 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sStage = smem;
+  const int stage_bytes = p.slab_stage + p.b_stage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStage + p.na * stage_bytes);
+  uint64_t* empty = full + p.na;
+  uint64_t* tfull = empty + p.na;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.tmX);
+    tma_prefetch(&p.tmB);
+    for (int i = 0; i < p.na; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tempty[0], 256);   // both CTAs' epilogue threads release the accumulators
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int PB = p.n_pix_blocks;
+  const long long units = static_cast<long long>(p.n_ci_blocks) * p.n_co_blocks * PB;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const long long u_begin = units * cid / ncl;
+  const long long u_end = units * (cid + 1) / ncl;
+  const int pb_per_img = p.n_hb * p.n_wb;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (long long u = u_begin; u < u_end;) {
+        const int tile = static_cast<int>(u / PB);
+        const int pb0 = static_cast<int>(u - static_cast<long long>(tile) * PB);
+        const int pb1 = static_cast<int>(u_end - u < PB - pb0 ? pb0 + (u_end - u) : PB);
+        const int nb = tile % p.n_co_blocks, cb = tile / p.n_co_blocks;
+        for (int pb = pb0; pb < pb1; ++pb) {
+          const int img = pb / pb_per_img;
+          const int rem = pb - img * pb_per_img;
+          const int h0 = (rem / p.n_wb) * BH, w0 = (rem % p.n_wb) * 8;
+          mbar_wait(&empty[st], ph ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[st], 2 * (p.slab_load + p.b_load));
+          const uint32_t bar0 = mapa_shared(smem_u32(&full[st]), 0);
+          uint8_t* base = sStage + st * stage_bytes;
+          tma_load_4d_pair(base, &p.tmX, bar0, cb * 64, w0, h0 + 2 * static_cast<int>(rank), img);
+          tma_load_4d_pair(base + p.slab_stage, &p.tmB, bar0, nb * 128 + 64 * static_cast<int>(rank), w0 + p.pad,
+                           h0 + p.pad, img);
+          if (++st == p.na) { st = 0; ph ^= 1; }
+        }
+        u += pb1 - pb0;
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      int st = 0;
+      uint32_t ph = 0, acc_ph = 0;
+      const uint64_t x0 = umma_smem_desc(smem_u32(sStage), 0, SW * 128, 128);
+      const uint64_t y0 = umma_smem_desc(smem_u32(sStage) + p.slab_stage, 8192, 1024, 128);
+      for (long long u = u_begin; u < u_end;) {
+        const int tile = static_cast<int>(u / PB);
+        const int pb0 = static_cast<int>(u - static_cast<long long>(tile) * PB);
+        const int pb1 = static_cast<int>(u_end - u < PB - pb0 ? pb0 + (u_end - u) : PB);
+        mbar_wait(&tempty[0], acc_ph ^ 1);
+        tc_fence_after();
+        for (int pb = pb0; pb < pb1; ++pb) {
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          const uint32_t soff = st * stage_bytes;
+          if (elect_one()) {
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              const int o0 = j == 0 ? 0 : j == 1 ? 2 : SW;        // base tap offset (pixels)
+              const int lbo = j == 1 ? SW * 128 : 128;             // second atom's distance
+              const uint64_t xa = desc_add(x0, soff + o0 * 128) | (static_cast<uint64_t>(lbo >> 4) << 16);
+#pragma unroll
+              for (int ks = 0; ks < KSTEPS; ++ks)
+                umma_bf16_pair(tmem_base + j * 128, desc_add(xa, 2 * ks * SW * 128), desc_add(y0, soff + ks * 2048),
+                               p.idesc, (pb > pb0 || ks > 0) ? 1u : 0u);
+            }
+            umma_commit_pair(&empty[st], 0x3);
+          }
+          __syncwarp();
+          if (++st == p.na) { st = 0; ph ^= 1; }
+        }
+        if (elect_one()) umma_commit_pair(&tfull[0], 0x3);
+        __syncwarp();
+        acc_ph ^= 1;
+        u += pb1 - pb0;
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int m = q * 32 + lane;
+    uint32_t acc_ph = 0;
+    const long long wstride = static_cast<long long>(p.taps) * p.c;  // dW[co][tap][ci]
+    const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    // taps held by (accumulator j, row half m>>6) of this CTA; -1 = unused slot
+    const int half = m >> 6;
+    int tap_of[3];
+    if (rank == 0) {
+      tap_of[0] = half ? 1 : 0;
+      tap_of[1] = half ? 5 : 2;
+      tap_of[2] = half ? 4 : 3;
+    } else {
+      tap_of[0] = half ? 7 : 6;
+      tap_of[1] = half ? -1 : 8;
+      tap_of[2] = -1;
+    }
+    for (long long u = u_begin; u < u_end;) {
+      const int tile = static_cast<int>(u / PB);
+      const int pb0 = static_cast<int>(u - static_cast<long long>(tile) * PB);
+      const int pb1 = static_cast<int>(u_end - u < PB - pb0 ? pb0 + (u_end - u) : PB);
+      const int nb = tile % p.n_co_blocks, cb = tile / p.n_co_blocks;
+      mbar_wait(&tfull[0], acc_ph);
+      tc_fence_after();
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        if (rank == 1 && j == 2) break;  // warp-uniform: CTA 1's third accumulator is unused
+        const int tap = tap_of[j];
+        const uint32_t tb = tmem_base + j * 128 + (static_cast<uint32_t>(q * 32) << 16);
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t rr[32];
+          tmem_ld32(tb + c, rr);
+          tmem_wait_ld();
+          if (tap >= 0) {
+            const int co0 = nb * 128 + c;
+            float* dst = p.dw + static_cast<long long>(co0) * wstride + static_cast<long long>(tap) * p.c + cb * 64 + (m & 63);
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) red_add_f32(dst + jj * wstride, __uint_as_float(rr[jj]));
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(tempty0);
+      acc_ph ^= 1;
+      u += pb1 - pb0;
+    }
+  }
+  tc_fence_before();
+  cluster_sync();   // the peer's shared memory / barriers stay alive until the pair is done
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, p.tmem_cols);
+  }
+}
+
 }  // namespace ralpb
