@@ -329,9 +329,9 @@ cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* dy, int n, 
   int oh = (h - k) / st + 1, ow = (w - k) / st + 1;
   const long long windows = static_cast<long long>(n) * oh * ow * (c / 8);
   const int threads = pool_threads(c);
-  // with a fused column sum the grid stays small (one global atomic per channel per block)
+  // (with a fused column sum: one global atomic per channel per block)
   auto grid = [&](long long work) {
-    const long long cap = static_cast<long long>(num_sms()) * (colsum != nullptr ? 4 : 16);
+    const long long cap = static_cast<long long>(num_sms()) * 16;
     return static_cast<int>(std::max<long long>(1, std::min((work + threads - 1) / threads, cap)));
   };
   if (k == st && k == 2 && windows < (1LL << 31)) {
