@@ -60,6 +60,17 @@ int ralpb_conv_dgrad(const void* dy_pad, const void* wd, const void* mask_pad, v
 int ralpb_conv_wgrad(const void* x_pad, const void* dy_pad, float* dw, float* db, int n, int h, int w_,
                      int cin, int cout, int k, int pad, void* stream);
 
+/* First (RGB) convolution fused with its im2col (3x3, stride 1, pad 1, 3 -> 64 channels,
+ * h % 8 == 0, w % 16 == 0): the patch rows are built on chip from the fp32 NHWC image.
+ *   wf: [64][32] bf16, columns (r*3+s)*3+ch, column 27 = bias;  y_pad/dy_pad: [n][h+2p][w+2p][64]
+ *   (y written on interior pixels, ReLU fused);  dw: [64][32] fp32 accumulated (column 27 = db).
+ * Returns an error for other shapes (the im2col GEMM path, ralpb_pack_im2col + ralpb_gemm, covers
+ * them). */
+int ralpb_conv_first_fwd(const float* img, int n, int h, int w, const void* wf, void* y_pad, int pad_out,
+                         void* stream);
+int ralpb_conv_first_wgrad(const float* img, int n, int h, int w, const void* dy_pad, int pad_out, float* dw,
+                           void* stream);
+
 /* fp32 NHWC images -> bf16 padded NHWC with cp >= c channels (zero fill). */
 int ralpb_pack_input(const float* x, int n, int h, int w, int c, void* out, int cp, int pad,
                      void* stream);

@@ -28,6 +28,8 @@ SIGNATURES: dict[str, tuple] = {
     "ralpb_gemm_bf16": (c_i, [c_vp, c_ll, c_ll, c_ll, c_i, c_vp, c_ll, c_ll, c_ll, c_i, c_i, c_i, c_ll,
                               c_vp, c_i, c_ll, c_ll, c_fp, c_i, c_vp, c_ll, c_i, c_i, c_vp]),
     "ralpb_conv_fwd": (c_i, [c_vp, c_vp, c_fp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),
+    "ralpb_conv_first_fwd": (c_i, [c_vp, c_i, c_i, c_i, c_vp, c_vp, c_i, c_vp]),
+    "ralpb_conv_first_wgrad": (c_i, [c_vp, c_i, c_i, c_i, c_vp, c_i, c_vp, c_vp]),
     "ralpb_conv_dgrad": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),
     "ralpb_conv_wgrad": (c_i, [c_vp, c_vp, c_fp, c_fp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),
     "ralpb_pack_input": (c_i, [c_fp, c_i, c_i, c_i, c_i, c_vp, c_i, c_i, c_vp]),

@@ -57,6 +57,21 @@ int ralpb_conv_dgrad(const void* dy_pad, const void* wd, const void* mask_pad, v
                     why);
 }
 
+int ralpb_conv_first_fwd(const float* img, int n, int h, int w, const void* wf, void* y_pad, int pad_out,
+                         void* stream) {
+  std::string why;
+  if (!conv_first_ok(h, w, 3, 64, 3, 1, 1)) return set_status(cudaErrorInvalidValue, "conv_first: unsupported shape");
+  return set_status(conv_first_fwd(img, n, h, w, 3, wf, y_pad, pad_out, static_cast<cudaStream_t>(stream), &why), why);
+}
+
+int ralpb_conv_first_wgrad(const float* img, int n, int h, int w, const void* dy_pad, int pad_out, float* dw,
+                           void* stream) {
+  std::string why;
+  if (!conv_first_ok(h, w, 3, 64, 3, 1, 1)) return set_status(cudaErrorInvalidValue, "conv_first: unsupported shape");
+  return set_status(conv_first_wgrad(img, n, h, w, 3, dy_pad, pad_out, dw, static_cast<cudaStream_t>(stream), &why),
+                    why);
+}
+
 int ralpb_conv_wgrad(const void* x_pad, const void* dy_pad, float* dw, float* db, int n, int h, int w_,
                      int cin, int cout, int k, int pad, void* stream) {
   std::string why;

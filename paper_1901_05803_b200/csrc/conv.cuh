@@ -48,6 +48,22 @@ cudaError_t conv_dgrad_flat(const ConvGeom& g, const void* dy_pad, const void* w
 cudaError_t conv_wgrad_flat(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw,
                             cudaStream_t s, std::string* why);
 
+// Tensor maps (conv_slab.cu): padded activation [n][hp][wp][c] as a 4-D tensor with box
+// {bc, bw, bh, 1}, and a row-major [rows][cols] bf16 matrix with box {bc, br}; swz = 32/64/128.
+bool encode_act(CUtensorMap* tm, const void* ptr, long long c, long long wp, long long hp, long long n, int bc, int bw,
+                int bh, int swz, std::string* why);
+bool encode_mat(CUtensorMap* tm, const void* ptr, long long rows, long long cols, int bc, int br, int swz,
+                std::string* why);
+
+// First (RGB) convolution fused with its im2col (conv_first.cu): 3x3/1/pad 1, cin = 3,
+// 64 output channels, h % 8 == 0, w % 16 == 0.  img: fp32 NHWC; wf: [64][32] bf16 with the bias
+// in column 9*cin; y_pad / dy_pad: [n][h+2p][w+2p][64]; dw: [64][32] fp32 (accumulated).
+bool conv_first_ok(int h, int w, int cin, int cout, int k, int stride, int pad);
+cudaError_t conv_first_fwd(const float* img, int n, int h, int w, int cin, const void* wf, void* y_pad, int pad_out,
+                           cudaStream_t s, std::string* why);
+cudaError_t conv_first_wgrad(const float* img, int n, int h, int w, int cin, const void* dy_pad, int pad_out,
+                             float* dw, cudaStream_t s, std::string* why);
+
 // Slab-tiled kernels (conv_slab.cu).  `c` = contracted channels, `cout` = produced channels.
 bool slab_fwd_ok(const ConvGeom& g, int c, int cout);
 bool slab_wgrad_ok(const ConvGeom& g);

@@ -72,10 +72,18 @@ struct alignas(64) SlabConvParams {
 // accumulators so that every UMMA descriptor in the issue loop is a base plus a
 // compile-time offset (a descriptor computed at run time costs ~100+ cycles of issue
 // latency per MMA; tools/exp_mma.cu).
-template <int K, int KSTEPS, int MACC>
+//
+// PAIR: a cluster of two CTAs issues cta_group::2 UMMAs (M = 2 x 128 pixel rows, N = bn):
+// CTA r owns the pixel rows [h0 + r*16*MACC, +16*MACC) of the work item and HALF of the
+// filter tile (bn/2 rows), so per MMA each SM reads its 4 KB of A and bn/2 x 32 B of B.
+// Used for bn <= 128, where the single-CTA MMA is shared-memory-bound (64-channel filters:
+// 6 KB per 32 cycles of math); every barrier that gates an MMA lives in CTA 0 (the issuer),
+// whose producers expect both CTAs' bytes; MMA completions are multicast to both CTAs.
+template <int K, int KSTEPS, int MACC, bool PAIR>
 __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
     conv_slab_fwd_kernel(const __grid_constant__ SlabConvParams p) {
   constexpr int EWG = MACC >= 2 ? 2 : 1;
+  constexpr int NCTA = PAIR ? 2 : 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -97,18 +105,30 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
     tma_prefetch(&p.tmB);
     for (int i = 0; i < p.na; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
     for (int i = 0; i < p.nb; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128 * EWG); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128 * EWG * NCTA); }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, p.tmem_cols);
-  tc_fence_before();
-  __syncthreads();
+  uint32_t rank = 0;
+  if constexpr (PAIR) {
+    rank = cluster_ctarank();
+    if (warp == 2) tmem_alloc_pair(tmem_slot, p.tmem_cols);
+    tc_fence_before();
+    cluster_sync();
+  } else {
+    if (warp == 2) tmem_alloc(tmem_slot, p.tmem_cols);
+    tc_fence_before();
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total = p.n * p.n_hb * p.n_wb * p.n_nt;
   const int cblks = p.c / p.kb;
   const int ksteps = p.kb / 16;
   const int mrows = 16 * p.macc;
+  const int w_first = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int w_step = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+  // barriers gating the issuer: own (single CTA) or CTA 0's (pair), as shared::cluster addresses
+  auto lead = [&](uint64_t* bar) { return PAIR ? mapa_shared(smem_u32(bar), 0) : smem_u32(bar); };
 
   if (warp == 0 || warp == 2 || warp == 3) {
     // Producers: warp 0 streams the activation slabs, warps 2 and 3 take alternate filter
@@ -117,41 +137,52 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
       int as = 0, bs = 0;
       uint32_t aph = 0, bph = 0;
       int bseq = 0;
-      for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
+      const int bhalf = PAIR ? p.bn / 2 : p.bn;   // filter rows this CTA loads
+      for (int wi = w_first; wi < total; wi += w_step) {
         int t = wi;
         const int nt = t % p.n_nt; t /= p.n_nt;
         const int wb = t % p.n_wb; t /= p.n_wb;
         const int hb = t % p.n_hb;
         const int img = t / p.n_hb;
-        const int h0 = hb * mrows, w0 = wb * 8;
+        const int h0 = (hb * NCTA + static_cast<int>(rank)) * mrows, w0 = wb * 8;
         for (int cb = 0; cb < cblks; ++cb) {
           if (warp == 0) {
             mbar_wait(&a_empty[as], aph ^ 1);
-            mbar_expect_tx(&a_full[as], p.slab_load);
-            tma_load_4d(sA + as * p.slab_stage, &p.tmX, &a_full[as], cb * p.kb, w0, h0, img);
+            if (rank == 0) mbar_expect_tx(&a_full[as], NCTA * p.slab_load);
+            if constexpr (PAIR)
+              tma_load_4d_pair(sA + as * p.slab_stage, &p.tmX, lead(&a_full[as]), cb * p.kb, w0, h0, img);
+            else
+              tma_load_4d(sA + as * p.slab_stage, &p.tmX, &a_full[as], cb * p.kb, w0, h0, img);
             if (++as == p.na) { as = 0; aph ^= 1; }
             continue;
           }
           if (p.wres) {  // whole filter bank once per CTA (single channel block, single N tile)
-            if (wi == static_cast<int>(blockIdx.x))
+            if (wi == w_first)
               for (int tap = warp - 2; tap < p.taps; tap += 2) {
-                mbar_expect_tx(&b_full[tap], p.b_load);
-                tma_load_2d(sB + tap * p.b_stage, &p.tmB, &b_full[tap], tap * p.c, 0);
+                if (rank == 0) mbar_expect_tx(&b_full[tap], NCTA * p.b_load);
+                if constexpr (PAIR)
+                  tma_load_2d_pair(sB + tap * p.b_stage, &p.tmB, lead(&b_full[tap]), tap * p.c, static_cast<int>(rank) * bhalf);
+                else
+                  tma_load_2d(sB + tap * p.b_stage, &p.tmB, &b_full[tap], tap * p.c, 0);
               }
             continue;
           }
           for (int tap = 0; tap < p.taps; ++tap, ++bseq) {
             if ((bseq & 1) == (warp - 2)) {
               mbar_wait(&b_empty[bs], bph ^ 1);
-              mbar_expect_tx(&b_full[bs], p.b_load);
-              tma_load_2d(sB + bs * p.b_stage, &p.tmB, &b_full[bs], tap * p.c + cb * p.kb, nt * p.bn);
+              if (rank == 0) mbar_expect_tx(&b_full[bs], NCTA * p.b_load);
+              if constexpr (PAIR)
+                tma_load_2d_pair(sB + bs * p.b_stage, &p.tmB, lead(&b_full[bs]), tap * p.c + cb * p.kb,
+                                 nt * p.bn + static_cast<int>(rank) * bhalf);
+              else
+                tma_load_2d(sB + bs * p.b_stage, &p.tmB, &b_full[bs], tap * p.c + cb * p.kb, nt * p.bn);
             }
             if (++bs == p.nb) { bs = 0; bph ^= 1; }
           }
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && rank == 0) {
     constexpr int SW = 8 + K - 1;       // slab width (pixels)
     constexpr int RB = KSTEPS * 32;     // slab row bytes
     constexpr int TAPS = K * K;
@@ -160,7 +191,10 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
     const uint64_t a0 = umma_smem_desc(smem_u32(sA), 16, SW * RB, RB);
     const uint64_t b0 = umma_smem_desc(smem_u32(sB), 16, 8 * RB, RB);
     const bool issue = !(p.dbg & 2);
-    for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
+    auto commit = [&](uint64_t* bar) {
+      if constexpr (PAIR) umma_commit_pair(bar, 0x3); else umma_commit(bar);
+    };
+    for (int wi = w_first; wi < total; wi += w_step) {
       mbar_wait(&tempty[acc], acc_ph ^ 1);
       tc_fence_after();
       const uint32_t d0 = tmem_base + acc * MACC * p.bn;
@@ -179,20 +213,25 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
 #pragma unroll
               for (int a = 0; a < MACC; ++a)
 #pragma unroll
-                for (int ks = 0; ks < KSTEPS; ++ks)
-                  umma_bf16(d0 + a * p.bn, desc_add(ad, ((a * 16 + tap / K) * SW + tap % K) * RB + ks * 32),
-                            desc_add(bd, ks * 32), p.idesc, (cb > 0 || tap > 0 || ks > 0) ? 1u : 0u);
+                for (int ks = 0; ks < KSTEPS; ++ks) {
+                  const uint64_t ada = desc_add(ad, ((a * 16 + tap / K) * SW + tap % K) * RB + ks * 32);
+                  const uint32_t accum = (cb > 0 || tap > 0 || ks > 0) ? 1u : 0u;
+                  if constexpr (PAIR)
+                    umma_bf16_pair(d0 + a * p.bn, ada, desc_add(bd, ks * 32), p.idesc, accum);
+                  else
+                    umma_bf16(d0 + a * p.bn, ada, desc_add(bd, ks * 32), p.idesc, accum);
+                }
             }
-            if (!p.wres) umma_commit(&b_empty[bs]);
+            if (!p.wres) commit(&b_empty[bs]);
           }
           __syncwarp();
           if (!p.wres && ++bs == p.nb) { bs = 0; bph ^= 1; }
         }
-        if (elect_one()) umma_commit(&a_empty[as]);
+        if (elect_one()) commit(&a_empty[as]);
         __syncwarp();
         if (++as == p.na) { as = 0; aph ^= 1; }
       }
-      if (elect_one()) umma_commit(&tfull[acc]);
+      if (elect_one()) commit(&tfull[acc]);
       __syncwarp();
       if (++acc == p.acc_bufs) { acc = 0; acc_ph ^= 1; }
     }
@@ -202,7 +241,7 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
     const int m = q * 32 + lane;
     int acc = 0;
     uint32_t acc_ph = 0;
-    for (int wi = blockIdx.x; wi < total; wi += gridDim.x) {
+    for (int wi = w_first; wi < total; wi += w_step) {
       int t = wi;
       const int nt = t % p.n_nt; t /= p.n_nt;
       const int wb = t % p.n_wb; t /= p.n_wb;
@@ -211,7 +250,7 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
       mbar_wait(&tfull[acc], acc_ph);
       tc_fence_after();
       for (int a = g; a < p.macc; a += EWG) {
-        const int hh = hb * mrows + a * 16 + (m >> 3);
+        const int hh = (hb * NCTA + static_cast<int>(rank)) * mrows + a * 16 + (m >> 3);
         const int ww = wb * 8 + (m & 7);
         const bool valid = hh < p.h && ww < p.w;
         const long long orow = (static_cast<long long>(img) * p.hp + hh + p.pad) * p.wp + ww + p.pad;
@@ -289,15 +328,23 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if constexpr (PAIR) mbar_arrive_cluster(lead(&tempty[acc])); else mbar_arrive(&tempty[acc]);
       if (++acc == p.acc_bufs) { acc = 0; acc_ph ^= 1; }
     }
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem_base, p.tmem_cols);
+  if constexpr (PAIR) {
+    cluster_sync();
+    if (warp == 2) {
+      tc_fence_after();
+      tmem_dealloc_pair(tmem_base, p.tmem_cols);
+    }
+  } else {
+    __syncthreads();
+    if (warp == 2) {
+      tc_fence_after();
+      tmem_dealloc(tmem_base, p.tmem_cols);
+    }
   }
   if (p.colsum != nullptr)
     for (int i = threadIdx.x; i < p.cout; i += blockDim.x) atomicAdd(p.colsum + i, s_col[i]);

@@ -127,6 +127,11 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     if (i == 0 && first_im2col) {
       if (!d.relu || d.cout % 16 != 0) return fail("first conv: needs ReLU and cout % 16 == 0");
       f.im2col = true;
+      {
+        const char* fe = getenv("RALPB_FIRST");
+        f.fused = conv_first_ok(d.h, d.w, d.cin, d.cout, d.k, d.stride, d.pad) &&
+                  !(fe != nullptr && std::strcmp(fe, "im2col") == 0);
+      }
       f.kpad = in.c;
       f.cin_real = d.cin;
       f.g = ConvGeom{batch, in.h, in.w, in.c, d.cout, d.k, d.pad};  // h/w = output grid
@@ -520,6 +525,10 @@ int launch_front_backward(Model* m, const bf16* dcut, std::string* why) {
       ++m->launches;
       cur = dst;
       db_done = prev_db != nullptr;
+    } else if (f.fused) {
+      RALPB_TRY(conv_first_wgrad(m->step_img, in.n, m->in_h, m->in_w, m->in_c, cur, out.pad, m->G + f.w_off, m->stream,
+                                 why));
+      ++m->launches;
     } else if (f.im2col) {
       // dW[co][j] += sum_rows dY[row][co] * patches[row][j]  (j = kpad incl. the bias column)
       GemmDesc d;
@@ -626,12 +635,17 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   // ---------------- worker front forward
   const FrontLayer& f0 = m->front[0];
   const ActBuf& a0 = m->acts[0];
-  if (f0.im2col)
+  m->step_img = img;
+  if (f0.fused) {
+    // patches are built on chip by conv_first_fwd / conv_first_wgrad
+  } else if (f0.im2col) {
     RALPB_TRY(pack_im2col(img, b, m->in_h, m->in_w, m->in_c, f0.k, f0.stride, m->desc[0].pad, a0.h, a0.w, a0.pad,
                           f0.kpad, a0.ptr, s));
-  else
+    ++m->launches;
+  } else {
     RALPB_TRY(pack_input(img, b, m->in_h, m->in_w, m->in_c, a0.ptr, m->in_cp, a0.pad, s));
-  ++m->launches;
+    ++m->launches;
+  }
   const int slot = ralp ? m->rank : 0;          // this worker's row block in the PS input
   bf16* cut_dst = m->acts.back().ptr;
   if (m->holds_back) cut_dst = m->x_fc + static_cast<size_t>(slot) * b * m->cut_elems;
@@ -640,7 +654,9 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
     const ActBuf& in = m->acts[i];
     ActBuf out = m->acts[i + 1];
     if (i + 1 == m->front.size()) out.ptr = cut_dst;
-    if (f.im2col) {
+    if (f.fused) {
+      RALPB_TRY(conv_first_fwd(img, b, m->in_h, m->in_w, m->in_c, f.wf, out.ptr, out.pad, s, why));
+    } else if (f.im2col) {
       // y = relu(patches . W^T) on the padded output grid (bias rides in the ones column)
       GemmDesc d;
       d.M = static_cast<int>(in.rows()); d.N = f.g.cout; d.K = f.kpad;

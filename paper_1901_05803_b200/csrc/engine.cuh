@@ -32,6 +32,8 @@ struct FrontLayer {
   bf16* wd = nullptr;          // backward-data filter [cin][k*k][cout]
   bool im2col = false;         // first conv as a GEMM over the im2col patch matrix acts[0]
   int kpad = 0;                // im2col row width (k*k*cin + 1 bias column, padded)
+  bool fused = false;          // im2col layer run by the fused first-conv kernels (conv_first.cu):
+                               // patches built on chip from the fp32 image, acts[0] unused
 };
 
 struct FcLayer {
@@ -79,6 +81,7 @@ struct Model {
   float* loss = nullptr;
   std::vector<bf16*> gacts;        // gacts[i] = gradient w.r.t. acts[i] (dedicated, zero borders)
   float* img_dev = nullptr;        // staging for host images
+  const float* step_img = nullptr; // this step's fp32 image batch (device) -- fused first conv
   int32_t* lab_dev = nullptr;      // staging for host labels
   size_t arena_off_flags = 0, arena_off_P = 0, arena_off_G = 0, arena_off_xfc = 0, arena_off_lab = 0,
          arena_off_dcut = 0;

@@ -49,6 +49,22 @@ def conv_fwd(x_pad, w, bias, *, n, h, w_, cin, cout, k, pad, relu=True, out=None
     return out
 
 
+def conv_first_fwd(img, wf, *, pad_out=1):
+    """Fused im2col + first conv (3x3/1/1, 3 -> 64, ReLU); img fp32 [n,h,w,3], wf bf16 [64,32]."""
+    n, h, w, _ = img.shape
+    y = torch.zeros(n, h + 2 * pad_out, w + 2 * pad_out, 64, dtype=_BF16, device=img.device)
+    call("ralpb_conv_first_fwd", img.data_ptr(), n, h, w, wf.data_ptr(), y.data_ptr(), pad_out, _stream())
+    return y
+
+
+def conv_first_wgrad(img, dy_pad, *, pad_out=1, dw=None):
+    n, h, w, _ = img.shape
+    if dw is None:
+        dw = torch.zeros(64, 32, dtype=torch.float32, device=img.device)
+    call("ralpb_conv_first_wgrad", img.data_ptr(), n, h, w, dy_pad.data_ptr(), pad_out, dw.data_ptr(), _stream())
+    return dw
+
+
 def conv_dgrad(dy_pad, wd, mask_pad, *, n, h, w_, cin, cout, k, pad, out=None, colsum=None):
     """dx (and, if `colsum` is given, colsum += per-channel sum of the stored dx)."""
     if out is None:

@@ -238,3 +238,32 @@ def test_first_conv_im2col(k, stride, pad, po, kpad, h):
                   k_splits=0)
     refdw = dy.view(rows, cout).float().t() @ cols.view(rows, kpad).float()
     _close(dw, refdw, rtol=1e-3, atol=1e-3 * refdw.abs().max().item())
+
+
+@pytest.mark.parametrize("n,h,w", [(2, 32, 32), (3, 16, 48), (1, 224, 224)])
+def test_first_conv_fused(n, h, w):
+    """Fused im2col + first conv (conv_first.cu) against torch on the same bf16-rounded inputs,
+    and its filter/bias gradient against the im2col GEMM formulation."""
+    g = torch.Generator(device=DEV).manual_seed(12)
+    x = torch.randn(n, h, w, 3, generator=g, device=DEV)
+    wp = torch.zeros(64, 32, device=DEV)
+    wp[:, :27] = torch.randn(64, 27, generator=g, device=DEV) * (2.0 / 27) ** 0.5
+    wp[:, 27] = torch.randn(64, generator=g, device=DEV) * 0.1
+    wb = wp.to(torch.bfloat16).contiguous()
+    y = ops.conv_first_fwd(x, wb, pad_out=1)
+    xr = x.to(torch.bfloat16).float().permute(0, 3, 1, 2)
+    wr = wb[:, :27].float().view(64, 3, 3, 3).permute(0, 3, 1, 2)
+    ref = torch.relu(F.conv2d(xr, wr, wb[:, 27].float(), padding=1)).permute(0, 2, 3, 1)
+    _close(y[:, 1:-1, 1:-1, :], ref)
+    border = y.clone()
+    border[:, 1:-1, 1:-1, :] = 0
+    assert border.abs().max().item() == 0.0
+    dy = _pad(_bf(n, h, w, 64, gen=g), 1).contiguous()
+    dw = ops.conv_first_wgrad(x, dy, pad_out=1)
+    dyr = dy[:, 1:-1, 1:-1, :].permute(0, 3, 1, 2).float()
+    refw = torch.nn.grad.conv2d_weight(xr, (64, 3, 3, 3), dyr, padding=1)  # [co, ci, r, s]
+    refw = refw.permute(0, 2, 3, 1).reshape(64, 27)
+    _close(dw[:, :27], refw, rtol=1e-3, atol=1e-3 * refw.abs().max().item())
+    refb = dyr.sum(dim=(0, 2, 3))
+    _close(dw[:, 27], refb, rtol=1e-3, atol=1e-3 * refb.abs().max().item())
+    assert dw[:, 28:].abs().max().item() == 0.0
