@@ -157,6 +157,8 @@ def _build_executor(strategy: str, world: int, rank: int):
 
 
 def _time_steps(ex, imgs, labs, steps, warmup, world, on_host=False, read_loss=False):
+    """read_loss: read every step's loss back to the host (pipelined one step behind: the loss of
+    step t is read after step t+1 has been enqueued, so its host inputs' copy overlaps step t)."""
     import torch
     import torch.distributed as dist
 
@@ -171,8 +173,10 @@ def _time_steps(ex, imgs, labs, steps, warmup, world, on_host=False, read_loss=F
     s.record(stream)
     for t in range(steps):
         ex.step(imgs[t % len(imgs)], labs[t % len(labs)])
-        if read_loss:
-            ex.stats()  # device->host read of the step's loss (synchronises)
+        if read_loss and t > 0:
+            ex.read_loss(1)  # device->host read of step t-1's loss
+    if read_loss:
+        ex.read_loss(0)
     e.record(stream)
     torch.cuda.synchronize()
     ms = s.elapsed_time(e)

@@ -147,12 +147,18 @@ int ralpb_model_ipc_open(ralpb_model* m, const void* handles);
 int ralpb_model_set_params(ralpb_model* m, int layer, const float* w, const float* b, int on_host);
 int ralpb_model_get_params(ralpb_model* m, int layer, float* w, float* b, int on_host);
 /* One training step of this rank's worker batch: images [b][h][w][c] fp32 NHWC, labels [b] int32,
- * host (pinned for async copies) or device memory.  Executes _ralp_worker/_ralp_ps
- * (simulator.py:669-715) or _baseline_worker/_baseline_ps (simulator.py:637-665). */
+ * host or device memory.  Executes _ralp_worker/_ralp_ps (simulator.py:669-715) or
+ * _baseline_worker/_baseline_ps (simulator.py:637-665).  Asynchronous: host inputs are copied on
+ * a copy stream into one of two device staging buffers, so the copy of step t+1 overlaps step t
+ * (pinned host buffers must stay unchanged until that step's loss has been read; pageable ones
+ * are staged before the call returns). */
 int ralpb_model_step(ralpb_model* m, const void* images, const int32_t* labels, int on_host, float lr,
                      float mu);
 /* Synchronises the model stream and reports the last step. */
 int ralpb_model_stats(ralpb_model* m, ralpb_step_stats* out);
+/* Loss of the step issued `lag` steps ago (0 = latest, lag < 4), copied to pinned host memory at
+ * the end of that step; waits for that step only (NaN on ranks without the FC tail). */
+int ralpb_model_read_loss(ralpb_model* m, int lag, float* out);
 void* ralpb_model_stream(ralpb_model* m);
 /* Inspection: copies activation (which=0) or activation-gradient (which=1) buffer i (bf16,
  * padded layout) to host_out (may be NULL to query); returns its element count or -1. */

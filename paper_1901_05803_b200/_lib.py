@@ -49,6 +49,7 @@ SIGNATURES: dict[str, tuple] = {
     "ralpb_model_get_params": (c_i, [c_vp, c_i, c_vp, c_vp, c_i]),
     "ralpb_model_step": (c_i, [c_vp, c_vp, c_vp, c_i, c_f, c_f]),
     "ralpb_model_stats": (c_i, [c_vp, c_vp]),
+    "ralpb_model_read_loss": (c_i, [c_vp, c_i, c_vp]),
     "ralpb_model_stream": (c_vp, [c_vp]),
     "ralpb_model_set_profiling": (c_i, [c_vp, c_i]),
     "ralpb_model_debug_buffer": (c_ll, [c_vp, c_i, c_i, c_vp]),

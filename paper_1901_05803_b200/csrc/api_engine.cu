@@ -58,6 +58,11 @@ int ralpb_model_stats(ralpb_model* m, ralpb_step_stats* out) {
   return model_stats(m->impl, out, &why) ? set_error("ralpb_model_stats: " + why) : 0;
 }
 
+int ralpb_model_read_loss(ralpb_model* m, int lag, float* out) {
+  std::string why;
+  return model_read_loss(m->impl, lag, out, &why) ? set_error("ralpb_model_read_loss: " + why) : 0;
+}
+
 void* ralpb_model_stream(ralpb_model* m) { return m->impl->stream; }
 
 int ralpb_model_set_profiling(ralpb_model* m, int on) {

@@ -273,10 +273,17 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   if (!(m->fc_scratch = alloc<float>(m, static_cast<size_t>(R) * std::max(widest, m->cut_elems), why))) return fail(*why);
   if (!(m->row_loss = alloc<float>(m, R, why))) return fail(*why);
   if (!(m->loss = alloc<float>(m, 4, why))) return fail(*why);
-  if (!(m->img_dev = alloc<float>(m, static_cast<size_t>(batch) * m->in_h * m->in_w * m->in_c, why))) return fail(*why);
-  if (!(m->lab_dev = alloc<int32_t>(m, batch, why))) return fail(*why);
+  for (int i = 0; i < 2; ++i) {
+    if (!(m->img_dev[i] = alloc<float>(m, static_cast<size_t>(batch) * m->in_h * m->in_w * m->in_c, why))) return fail(*why);
+    if (!(m->lab_dev[i] = alloc<int32_t>(m, batch, why))) return fail(*why);
+    cudaEventCreateWithFlags(&m->ev_copied[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&m->ev_consumed[i], cudaEventDisableTiming);
+  }
   if (cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
+  if (cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
   for (auto& e : m->ev) cudaEventCreate(&e);
+  if (cudaMallocHost(&m->loss_host, sizeof(float) * Model::kLossRing) != cudaSuccess) return fail("cudaMallocHost");
+  for (auto& e : m->ev_loss) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail("device error during model creation");
   *out = m;
   return 0;
@@ -285,7 +292,16 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
 void model_destroy(Model* m) {
   if (!m) return;
   cudaDeviceSynchronize();
-  if (m->graph) cudaGraphExecDestroy(m->graph);
+  for (auto& g : m->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (int i = 0; i < 2; ++i) {
+    if (m->ev_copied[i]) cudaEventDestroy(m->ev_copied[i]);
+    if (m->ev_consumed[i]) cudaEventDestroy(m->ev_consumed[i]);
+  }
+  for (auto& e : m->ev_loss)
+    if (e) cudaEventDestroy(e);
+  if (m->loss_host) cudaFreeHost(m->loss_host);
+  if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
   for (int r = 0; r < static_cast<int>(m->peer_base.size()); ++r)
     if (r != m->rank && m->peer_base[r] != nullptr) cudaIpcCloseMemHandle(m->peer_base[r]);
   for (void* p : m->owned) cudaFree(p);
@@ -319,7 +335,8 @@ int model_ipc_open(Model* m, const void* handles, std::string* why) {
     m->peer_base[r] = static_cast<char*>(p);
   }
   m->peers_open = true;
-  if (m->graph) { cudaGraphExecDestroy(m->graph); m->graph = nullptr; }  // peer pointers are baked in
+  for (auto& g : m->graphs)  // peer pointers are baked into captured steps
+    if (g.exec) { cudaGraphExecDestroy(g.exec); g = Model::GraphEntry{}; }
   return 0;
 }
 
@@ -771,15 +788,22 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
   const int b = m->batch;
   cudaStream_t s = m->stream;
   m->seq += 1;
-  RALPB_TRY(cudaEventRecord(m->ev[0], s));
   const float* img = static_cast<const float*>(images);
   const int32_t* lab = labels;
+  const int buf = static_cast<int>(m->seq & 1);
   if (on_host) {
-    RALPB_TRY(cudaMemcpyAsync(m->img_dev, images, sizeof(float) * b * m->in_h * m->in_w * m->in_c, cudaMemcpyHostToDevice, s));
-    RALPB_TRY(cudaMemcpyAsync(m->lab_dev, labels, sizeof(int32_t) * b, cudaMemcpyHostToDevice, s));
-    img = m->img_dev;
-    lab = m->lab_dev;
+    // copy stream: wait until step seq-2 (same staging buffer) consumed it, copy, signal
+    cudaStream_t c = m->copy_stream;
+    RALPB_TRY(cudaStreamWaitEvent(c, m->ev_consumed[buf], 0));
+    RALPB_TRY(cudaMemcpyAsync(m->img_dev[buf], images, sizeof(float) * b * m->in_h * m->in_w * m->in_c,
+                              cudaMemcpyHostToDevice, c));
+    RALPB_TRY(cudaMemcpyAsync(m->lab_dev[buf], labels, sizeof(int32_t) * b, cudaMemcpyHostToDevice, c));
+    RALPB_TRY(cudaEventRecord(m->ev_copied[buf], c));
+    RALPB_TRY(cudaStreamWaitEvent(s, m->ev_copied[buf], 0));
+    img = m->img_dev[buf];
+    lab = m->lab_dev[buf];
   }
+  RALPB_TRY(cudaEventRecord(m->ev[0], s));
   if (m->profiling || !graphs_enabled()) {
     m->launches = 0;
     m->phys_bytes = 0;
@@ -788,7 +812,15 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
     struct Reset { ~Reset() { set_gemm_timer(nullptr); } } reset_timer;
     if (step_body(m, img, lab, lr, mu, false, why)) return 1;
   } else {
-    if (m->graph == nullptr || m->graph_img != img || m->graph_lab != lab || m->graph_lr != lr || m->graph_mu != mu) {
+    // captured step bodies, keyed by (inputs, hyper-parameters); two entries cover the
+    // alternating staging buffers
+    Model::GraphEntry* e = nullptr;
+    for (auto& g : m->graphs)
+      if (g.exec != nullptr && g.img == img && g.lab == lab && g.lr == lr && g.mu == mu) e = &g;
+    if (e == nullptr) {
+      e = &m->graphs[0];
+      for (auto& g : m->graphs)
+        if (g.exec == nullptr || g.used < e->used) e = &g;
       m->launches = 0;
       m->phys_bytes = 0;
       RALPB_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -798,28 +830,45 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
       if (rc) { if (g) cudaGraphDestroy(g); return 1; }
       if (ce != cudaSuccess) { *why = std::string("step capture failed: ") + cudaGetErrorString(ce); return 1; }
       bool updated = false;
-      if (m->graph != nullptr) {
+      if (e->exec != nullptr) {
         cudaGraphExecUpdateResultInfo info{};
-        updated = cudaGraphExecUpdate(m->graph, g, &info) == cudaSuccess;
+        updated = cudaGraphExecUpdate(e->exec, g, &info) == cudaSuccess;
         if (!updated) {
           cudaGetLastError();
-          cudaGraphExecDestroy(m->graph);
-          m->graph = nullptr;
+          cudaGraphExecDestroy(e->exec);
+          e->exec = nullptr;
         }
       }
-      cudaError_t ie = updated ? cudaSuccess : cudaGraphInstantiate(&m->graph, g, 0);
+      cudaError_t ie = updated ? cudaSuccess : cudaGraphInstantiate(&e->exec, g, 0);
       cudaGraphDestroy(g);
-      if (ie != cudaSuccess) { m->graph = nullptr; *why = std::string("graph instantiate failed: ") + cudaGetErrorString(ie); return 1; }
-      m->graph_img = img; m->graph_lab = lab; m->graph_lr = lr; m->graph_mu = mu;
-      m->graph_launches = m->launches;
-      m->graph_phys = m->phys_bytes;
+      if (ie != cudaSuccess) { *e = Model::GraphEntry{}; *why = std::string("graph instantiate failed: ") + cudaGetErrorString(ie); return 1; }
+      e->img = img; e->lab = lab; e->lr = lr; e->mu = mu;
+      e->launches = m->launches;
+      e->phys = m->phys_bytes;
     }
-    RALPB_TRY(cudaGraphLaunch(m->graph, s));
-    m->launches = m->graph_launches;
-    m->phys_bytes = m->graph_phys;
+    e->used = ++m->graph_clock;
+    RALPB_TRY(cudaGraphLaunch(e->exec, s));
+    m->launches = e->launches;
+    m->phys_bytes = e->phys;
   }
+  if (on_host) RALPB_TRY(cudaEventRecord(m->ev_consumed[buf], s));
+  const int slot = static_cast<int>(m->seq % Model::kLossRing);
+  if (m->holds_back) RALPB_TRY(cudaMemcpyAsync(m->loss_host + slot, m->loss, sizeof(float), cudaMemcpyDeviceToHost, s));
+  RALPB_TRY(cudaEventRecord(m->ev_loss[slot], s));
+  m->loss_seq[slot] = m->seq;
   RALPB_TRY(cudaEventRecord(m->ev[4], s));
   m->stats_valid = true;
+  return 0;
+}
+
+// Loss of the step issued `lag` steps ago (0 = the latest), waiting only for that step.
+int model_read_loss(Model* m, int lag, float* out, std::string* why) {
+  if (lag < 0 || lag >= Model::kLossRing || static_cast<uint32_t>(lag) >= m->seq) { *why = "no such step"; return 1; }
+  const uint32_t want = m->seq - static_cast<uint32_t>(lag);
+  const int slot = static_cast<int>(want % Model::kLossRing);
+  if (m->loss_seq[slot] != want) { *why = "step no longer in the loss ring"; return 1; }
+  RALPB_TRY(cudaEventSynchronize(m->ev_loss[slot]));
+  *out = m->holds_back ? m->loss_host[slot] : NAN;
   return 0;
 }
 

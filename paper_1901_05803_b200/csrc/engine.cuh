@@ -80,9 +80,18 @@ struct Model {
   float* row_loss = nullptr;
   float* loss = nullptr;
   std::vector<bf16*> gacts;        // gacts[i] = gradient w.r.t. acts[i] (dedicated, zero borders)
-  float* img_dev = nullptr;        // staging for host images
+  // host inputs: double-buffered device staging filled on a copy stream, so the copy of step
+  // t+1 overlaps the compute of step t (buffer b is reused once step t-1 has consumed it)
+  float* img_dev[2] = {nullptr, nullptr};
+  int32_t* lab_dev[2] = {nullptr, nullptr};
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {}, ev_consumed[2] = {};
   const float* step_img = nullptr; // this step's fp32 image batch (device) -- fused first conv
-  int32_t* lab_dev = nullptr;      // staging for host labels
+  // per-step loss copied to pinned host memory (ring), readable without draining the stream
+  static constexpr int kLossRing = 4;
+  float* loss_host = nullptr;
+  cudaEvent_t ev_loss[kLossRing] = {};
+  uint32_t loss_seq[kLossRing] = {};
   size_t arena_off_flags = 0, arena_off_P = 0, arena_off_G = 0, arena_off_xfc = 0, arena_off_lab = 0,
          arena_off_dcut = 0;
 
@@ -95,12 +104,17 @@ struct Model {
   uint32_t* seq_dev = nullptr;     // device step counter: flag value of the exchange kernels
   // CUDA graph of the step body (everything after the input upload), re-captured when the
   // input pointers or hyper-parameters change; disabled while profiling or RALPB_GRAPH=0
-  cudaGraphExec_t graph = nullptr;
-  const void* graph_img = nullptr;
-  const void* graph_lab = nullptr;
-  float graph_lr = 0.f, graph_mu = 0.f;
-  int graph_launches = 0;
-  long long graph_phys = 0;
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    const void* img = nullptr;
+    const void* lab = nullptr;
+    float lr = 0.f, mu = 0.f;
+    int launches = 0;
+    long long phys = 0;
+    uint64_t used = 0;
+  };
+  GraphEntry graphs[2];            // one per staging buffer (or caller buffers)
+  uint64_t graph_clock = 0;
   int launches = 0;
   long long phys_bytes = 0;
   cudaEvent_t ev[6] = {};
@@ -115,6 +129,7 @@ void model_destroy(Model* m);
 int model_step(Model* m, const void* images, const int32_t* labels, int on_host, float lr, float mu,
                std::string* why);
 int model_stats(Model* m, ralpb_step_stats* st, std::string* why);
+int model_read_loss(Model* m, int lag, float* out, std::string* why);
 int model_set_params(Model* m, int layer, const float* w, const float* b, int on_host, std::string* why);
 int model_get_params(Model* m, int layer, float* w, float* b, int on_host, std::string* why);
 int model_ipc_handle(Model* m, void* out, std::string* why);

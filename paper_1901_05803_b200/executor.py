@@ -200,6 +200,12 @@ class RankExecutor:
         return StepResult(st.loss, st.logical_bytes, st.physical_bytes, st.launches, st.ms_step, st.ms_front_fwd,
                           st.ms_back, st.ms_front_bwd, st.ms_sync, st.ms_gemm, st.gemm_launches)
 
+    def read_loss(self, lag: int = 0) -> float:
+        """Loss of the step issued `lag` steps ago; waits for that step only."""
+        out = C.c_float()
+        _lib.call("ralpb_model_read_loss", self._h, int(lag), C.byref(out))
+        return out.value
+
     def set_profiling(self, on: bool) -> None:
         _lib.call("ralpb_model_set_profiling", self._h, int(on))
 

@@ -137,3 +137,25 @@ def test_alexnet_steps_b4():
     losses, got, want, want64, init = _run(model, "ralp", steps=3, lr=1e-3)
     print("alexnet b=4", losses)
     _check(losses, got, want, want64, init)
+
+
+def test_pipelined_host_inputs_and_async_loss():
+    """Host inputs go through the double-buffered copy stream and the loss ring: enqueueing
+    several steps before reading their losses gives the same losses as stepping synchronously."""
+    model = catalog_lookup("cifar_small").with_batch_size(64)
+    job = JobSpec(model, Strategy.ralp(_fc_boundary(model)), 1)
+    batches = [synthetic.batch(0, t, 0, 64, (32, 32, 3), 10) for t in range(4)]
+    losses = []
+    for pipelined in (False, True):
+        ex = RankExecutor(job)
+        ex.set_params(synthetic.init_params(ex.layers, 0))
+        got = []
+        for imgs, labs in batches:
+            ex.step(imgs, labs)
+            if not pipelined:
+                got.append(ex.stats().loss)
+        if pipelined:
+            got = [ex.read_loss(lag) for lag in (3, 2, 1, 0)]
+        ex.close()
+        losses.append(got)
+    np.testing.assert_allclose(losses[1], losses[0], rtol=1e-3)
