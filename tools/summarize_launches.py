@@ -14,7 +14,7 @@ import json
 import re
 from collections import OrderedDict, defaultdict
 
-TENSOR = re.compile(r"conv_slab_(fwd|wgrad)\w*_kernel|gemm_sm100_kernel")
+TENSOR = re.compile(r"conv_slab_(fwd|wgrad)\w*_kernel|conv_first_\w+_kernel|gemm_sm100_kernel")
 
 
 def family(name: str) -> str:
