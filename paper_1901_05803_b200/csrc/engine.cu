@@ -267,8 +267,11 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   if (!(m->logits = alloc<float>(m, static_cast<size_t>(R) * last.ld_out, why))) return fail(*why);
   if (!(m->dlogits = alloc<bf16>(m, static_cast<size_t>(R) * last.ld_out, why))) return fail(*why);
   cudaMemset(m->dlogits, 0, static_cast<size_t>(R) * last.ld_out * sizeof(bf16));
-  for (int g = 0; g < 2; ++g)
-    if (!(m->dh[g] = alloc<bf16>(m, static_cast<size_t>(R) * widest, why))) return fail(*why);
+  for (size_t j = 0; j + 1 < m->back.size(); ++j) {
+    bf16* d = alloc<bf16>(m, static_cast<size_t>(R) * m->back[j].ld_out, why);
+    if (!d) return fail(*why);
+    m->dyb.push_back(d);
+  }
   if (!(m->dx_fc = alloc<bf16>(m, static_cast<size_t>(R) * m->cut_elems, why))) return fail(*why);
   if (!(m->fc_scratch = alloc<float>(m, static_cast<size_t>(R) * std::max(widest, m->cut_elems), why))) return fail(*why);
   if (!(m->row_loss = alloc<float>(m, R, why))) return fail(*why);
@@ -281,6 +284,9 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   }
   if (cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
   if (cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
+  if (cudaStreamCreateWithFlags(&m->aux_stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
+  cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming);
   for (auto& e : m->ev) cudaEventCreate(&e);
   if (cudaMallocHost(&m->loss_host, sizeof(float) * Model::kLossRing) != cudaSuccess) return fail("cudaMallocHost");
   for (auto& e : m->ev_loss) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -302,6 +308,9 @@ void model_destroy(Model* m) {
     if (e) cudaEventDestroy(e);
   if (m->loss_host) cudaFreeHost(m->loss_host);
   if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
+  if (m->aux_stream) cudaStreamDestroy(m->aux_stream);
+  if (m->ev_fork) cudaEventDestroy(m->ev_fork);
+  if (m->ev_join) cudaEventDestroy(m->ev_join);
   for (int r = 0; r < static_cast<int>(m->peer_base.size()); ++r)
     if (r != m->rank && m->peer_base[r] != nullptr) cudaIpcCloseMemHandle(m->peer_base[r]);
   for (void* p : m->owned) cudaFree(p);
@@ -473,50 +482,60 @@ int launch_fc_forward(Model* m, const bf16* in, int R, std::string* why) {
 // `update` (the RALP PS: the FC tail is never synchronised) the weight-gradient GEMM applies
 // SGD-momentum in its epilogue (EPI_SGD) -- after the layer's dgrad has consumed the old bf16
 // weights -- so FC gradients never round-trip through HBM.
-int launch_fc_backward(Model* m, const bf16* in, int R, bf16* dx_out, bool update, float lr, float mu,
-                       std::string* why) {
+// FC backward-data chain: dyb[j-1] = (dyb[j] . W_j) * relu'(h_{j-1}); the first layer's dx is the
+// cut gradient.  Runs on the main stream (its result is what the workers wait for).
+int launch_fc_backward_data(Model* m, const bf16* in, int R, bf16* dx_out, std::string* why) {
   const int nb = static_cast<int>(m->back.size());
-  const bf16* dy = m->dlogits;
-  long long lddy = m->back.back().ld_out;
-  int ping = 0;
   for (int j = nb - 1; j >= 0; --j) {
     FcLayer& f = m->back[j];
-    const bf16* x = j == 0 ? in : m->hid[j - 1];
+    const bf16* dy = j == nb - 1 ? m->dlogits : m->dyb[j];
+    const long long lddy = f.ld_out;
     const long long ldx = j == 0 ? m->cut_elems : m->back[j - 1].ld_out;
-    // dgrad: dx[R][in] = dy[R][out] . W[out][in]   (ReLU mask of the previous hidden layer)
-    bf16* dst = j == 0 ? dx_out : m->dh[ping];
-    const long long ld_dst = j == 0 ? m->cut_elems : m->back[j - 1].ld_out;
+    bf16* dst = j == 0 ? dx_out : m->dyb[j - 1];
     GemmDesc d;
     d.M = R; d.N = f.in; d.K = f.out;
     d.a_mode = LD_K; d.a = Operand2D{dy, R, f.out, lddy};
     d.b_mode = LD_MN; d.b = Operand2D{f.wbf, f.out, f.in, f.in};
     const bool masked = j > 0 && m->back[j - 1].relu;
-    if (fc_gemm(m, d, ld_dst, nullptr, 0, masked ? m->hid[j - 1] : nullptr, ldx, dst, nullptr, why)) return 1;
-    // bias grad (+ its SGD step when updating in place)
-    RALPB_TRY(cudaMemsetAsync(m->G + f.b_off, 0, f.out * sizeof(float), m->stream));
-    RALPB_TRY(colsum_bf16(dy, R, f.out, lddy, m->G + f.b_off, m->stream));
-    ++m->launches;
-    // wgrad: G_w[out][in] = dy^T x   (or, with update, v = mu*v + g; p -= lr*v; bf16 copy)
+    if (fc_gemm(m, d, ldx, nullptr, 0, masked ? m->hid[j - 1] : nullptr, ldx, dst, nullptr, why)) return 1;
+  }
+  return 0;
+}
+
+// FC weight/bias gradients into G (dW = dy^T x, db = colsum dy) and, when `update`, the PS-local
+// SGD-momentum step with the bf16 weight copy the next forward reads.  Issued on `s`: the aux
+// stream for the layer-placed step (it overlaps the front backward), the main stream otherwise.
+int launch_fc_backward_weights(Model* m, const bf16* in, int R, bool update, float lr, float mu, cudaStream_t s,
+                               cudaStream_t s_update, std::string* why) {
+  const int nb = static_cast<int>(m->back.size());
+  for (int j = nb - 1; j >= 0; --j) {
+    FcLayer& f = m->back[j];
+    const bf16* dy = j == nb - 1 ? m->dlogits : m->dyb[j];
+    const long long lddy = f.ld_out;
+    const bf16* x = j == 0 ? in : m->hid[j - 1];
+    const long long ldx = j == 0 ? m->cut_elems : m->back[j - 1].ld_out;
+    RALPB_TRY(cudaMemsetAsync(m->G + f.b_off, 0, f.out * sizeof(float), s));
+    RALPB_TRY(colsum_bf16(dy, R, f.out, lddy, m->G + f.b_off, s));
     GemmDesc w;
     w.M = f.out; w.N = f.in; w.K = R;
     w.a_mode = LD_MN; w.a = Operand2D{dy, R, f.out, lddy};
     w.b_mode = LD_MN; w.b = Operand2D{x, R, f.in, ldx};
     w.s_m = f.in; w.s_n = 1;
-    if (update) {
-      w.epi = EPI_SGD; w.out = m->P + f.w_off; w.sgd_mom = m->V + f.w_off; w.sgd_bf16 = f.wbf;
-      w.sgd_lr = lr; w.sgd_mu = mu;
-    } else {
-      w.epi = EPI_F32; w.out = m->G + f.w_off;
+    w.epi = EPI_F32; w.out = m->G + f.w_off;
+    RALPB_TRY(gemm_launch(w, s, why));
+    m->launches += 2;
+  }
+  if (update) {
+    if (s_update != s) {
+      RALPB_TRY(cudaEventRecord(m->ev_fork, s));
+      RALPB_TRY(cudaStreamWaitEvent(s_update, m->ev_fork, 0));
     }
-    RALPB_TRY(gemm_launch(w, m->stream, why));
-    ++m->launches;
-    if (update) {
-      RALPB_TRY(sgd_momentum(m->P + f.b_off, m->V + f.b_off, m->G + f.b_off, f.out, lr, mu, 1.f, m->stream));
-      ++m->launches;
+    for (auto& f : m->back) {
+      const long long nw = static_cast<long long>(f.out) * f.in;
+      RALPB_TRY(sgd_momentum_bf16(m->P + f.w_off, m->V + f.w_off, m->G + f.w_off, nw, lr, mu, 1.f, f.wbf, s_update));
+      RALPB_TRY(sgd_momentum(m->P + f.b_off, m->V + f.b_off, m->G + f.b_off, f.out, lr, mu, 1.f, s_update));
+      m->launches += 2;
     }
-    dy = dst;
-    lddy = ld_dst;
-    ping ^= 1;
   }
   return 0;
 }
@@ -646,6 +665,7 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   const int b = m->batch;
   const bool ralp = m->strategy == RALPB_STRATEGY_RALP;
   cudaStream_t s = m->stream;
+  bool fc_forked = false;
   RALPB_TRY(bump_counter(m->seq_dev, s));
   ++m->launches;
 
@@ -729,22 +749,11 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
     RALPB_TRY(softmax_xent(m->logits, R, last.out, last.ld_out, m->labels_all, scale, m->row_loss, m->dlogits, last.ld_out, s));
     RALPB_TRY(reduce_sum(m->row_loss, R, 1.f / static_cast<float>(R), m->loss, s));
     m->launches += 2;
-    // SGD fused into the FC weight-gradient epilogue (RALPB_FC_FUSED_SGD=1) or as a separate
-    // streaming pass (default: the epilogue's per-row access pattern measured slower).
-    const char* fused_env = getenv("RALPB_FC_FUSED_SGD");
-    const bool fused = ralp && fused_env != nullptr && fused_env[0] == '1';
-    if (launch_fc_backward(m, in, R, m->dx_fc, fused, lr, mu, why)) return 1;
-    if (ralp && !fused) {
-      for (auto& f : m->back) {
-        const long long nw = static_cast<long long>(f.out) * f.in;
-        RALPB_TRY(sgd_momentum_bf16(m->P + f.w_off, m->V + f.w_off, m->G + f.w_off, nw, lr, mu, 1.f, f.wbf, s));
-        RALPB_TRY(sgd_momentum(m->P + f.b_off, m->V + f.b_off, m->G + f.b_off, f.out, lr, mu, 1.f, s));
-        m->launches += 2;
-      }
-    }
+    if (launch_fc_backward_data(m, in, R, m->dx_fc, why)) return 1;
     if (ralp) {
-      // FC tail update stays on the PS (never synchronised)
-      // return every remote worker's rows of the cut gradient
+      // return every remote worker's rows of the cut gradient first, then the FC tail's
+      // weight gradients and its (PS-local, never synchronised) update run on the aux
+      // stream, overlapping this rank's front backward
       for (int r = 0; r < m->world; ++r) {
         if (r == m->rank) continue;
         PeerSignal sig{};
@@ -755,6 +764,19 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
         ++m->launches;
         m->phys_bytes += cut_bytes;
       }
+      // weight gradients on this stream (tensor/HBM work that would contend with the persistent
+      // conv kernels), the HBM-bound update on the aux stream, overlapping the front backward
+      // (RALPB_FC_OVERLAP=0: everything in order on one stream)
+      const char* ov = getenv("RALPB_FC_OVERLAP");
+      const bool overlap = !(ov != nullptr && ov[0] == '0');
+      cudaStream_t su = overlap ? m->aux_stream : s;
+      if (launch_fc_backward_weights(m, in, R, true, lr, mu, s, su, why)) return 1;
+      if (overlap) {
+        RALPB_TRY(cudaEventRecord(m->ev_join, m->aux_stream));
+        fc_forked = true;
+      }
+    } else {
+      if (launch_fc_backward_weights(m, in, R, false, lr, mu, s, s, why)) return 1;
     }
     dcut = m->dx_fc + static_cast<size_t>(slot) * b * m->cut_elems;
   } else {
@@ -770,6 +792,9 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   RALPB_TRY(mark(m, 3, capturing));
 
   // ---------------- parameter synchronisation + re-layout
+  // join the FC tail's update before this rank signals the sync: a worker can only start the
+  // next step (and push its cut into x_fc, which the FC wgrads read) after that sync
+  if (fc_forked) RALPB_TRY(cudaStreamWaitEvent(s, m->ev_join, 0));
   if (sync_params(m, ralp ? m->n_front : m->n_total, lr, mu, why)) return 1;
   if (relayout_weights(m, !ralp, why)) return 1;
   return 0;

@@ -76,7 +76,10 @@ struct Model {
   float* logits = nullptr;
   float* fc_scratch = nullptr;     // split-K accumulators for FC GEMMs with few rows
   bf16* dlogits = nullptr;
-  bf16* dh[2] = {nullptr, nullptr};  // FC backward ping-pong
+  std::vector<bf16*> dyb;          // dyb[j] = gradient w.r.t. FC layer j's output (j < last; the
+                                   // last layer's is dlogits), kept for the deferred wgrads
+  cudaStream_t aux_stream = nullptr;   // PS: FC weight gradients + SGD, concurrent with the
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // front backward
   float* row_loss = nullptr;
   float* loss = nullptr;
   std::vector<bf16*> gacts;        // gacts[i] = gradient w.r.t. acts[i] (dedicated, zero borders)
