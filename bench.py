@@ -29,6 +29,12 @@ sys.path.insert(0, str(ROOT))
 MODEL = "vgg16"
 BATCH = 128
 METRIC = "images/sec per step at 1/2/4/8 B200 (layer-placed vs all-on-PS); sync bytes/step"
+KERNEL_NAMES = {"conv_fwd": "conv_slab_fwd_kernel (implicit-GEMM conv forward / backward-data, single CTA)",
+                "conv_fwd_pair": "conv_slab_fwd_kernel (CTA pair)",
+                "conv_wgrad_pair": "conv_slab_wgrad_pair_kernel (backward-filter, CTA pair)",
+                "conv_wgrad": "conv_slab_wgrad_kernel (backward-filter, single CTA)",
+                "first_conv_fwd": "conv_first_fwd_kernel", "first_conv_wgrad": "conv_first_wgrad_kernel",
+                "gemm": "gemm_sm100_kernel (FC)"}
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -218,19 +224,34 @@ def run_ours(args):
     e2e_value = world * BATCH / (ms_e2e * 1e-3)
     h2d = BATCH * int(np.prod(shape)) * 4 + BATCH * 4
 
-    # roofline of the dominant kernel (the tcgen05 GEMM engine): profiling pass after the timed region
+    # roofline: a profiling pass after the timed region brackets every tensor-core launch with
+    # CUDA events on its own stream and records its algorithmic FLOPs (ralpb_model_timed_launches)
     ex.set_profiling(True)
     ex.step(dimgs[0], dlabs[0])
     prof = ex.stats()
+    launches = ex.timed_launches()
     ex.set_profiling(False)
     worker_flops, ps_flops = compute_load(m, rep.split_index, world)
     flops_rank = worker_flops + (ps_flops if rank == 0 else 0)
     peaks, peak_src = _peaks()
-    achieved = flops_rank / (prof.ms_gemm * 1e-3) / 1e12 if prof.ms_gemm > 0 else None
-    traffic = None
+    by_kind = {}
+    for kind, lms, lfl in launches:
+        k = by_kind.setdefault(kind, {"launches": 0, "ms": 0.0, "flops": 0.0})
+        k["launches"] += 1
+        k["ms"] += lms
+        k["flops"] += lfl
+    traffic_doc = {}
     tfile = ROOT / "profiles" / "gemm_traffic.json"
     if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get("dram_bytes_per_step")
+        traffic_doc = json.loads(tfile.read_text())
+    for kind, k in by_kind.items():
+        k["tflops"] = k["flops"] / (k["ms"] * 1e-3) / 1e12 if k["ms"] > 0 else None
+        k["frac"] = k["tflops"] / peaks["bf16_tflops_sustained"] if k["tflops"] else None
+    dominant = max(by_kind, key=lambda kk: by_kind[kk]["ms"]) if by_kind else None
+    dom = by_kind.get(dominant, {})
+    dom_traffic = traffic_doc.get("per_kind", {}).get(dominant, {}).get("dram_bytes_per_launch")
+    step_ms = sum(k["ms"] for k in by_kind.values())
+    step_achieved = flops_rank / (step_ms * 1e-3) / 1e12 if step_ms > 0 else None
 
     # all-on-PS comparator (StrategyKind.BASELINE_PS): same workload, every layer on every worker
     ex.close()
@@ -261,13 +282,26 @@ def run_ours(args):
             "all_on_ps": {"value": world * BATCH / (ms_b * 1e-3), "ms_per_step": ms_b,
                           "logical_sync_bytes_per_step": stb.logical_bytes},
             "breakdown_ms_rank0": {"front_fwd": st.ms_front_fwd, "back": st.ms_back, "front_bwd": st.ms_front_bwd,
-                                   "sync": st.ms_sync, "gemm_sum": prof.ms_gemm, "gemm_launches": prof.gemm_launches},
-            "roofline": {"bound": "tensor", "kernel": "tcgen05 tensor-core kernels (conv_slab_fwd/conv_slab_wgrad implicit-GEMM convs + gemm_sm100 "
-                                   "FC/im2col GEMMs): algorithmic FLOPs of the step / summed event-timed launch durations",
-                         "achieved": achieved, "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
-                         "frac": achieved / peaks["bf16_tflops_sustained"] if achieved else None,
-                         "peak_source": f"{peak_src} bf16_tflops_sustained", "traffic": traffic,
-                         "algorithmic_flops_per_step_rank0": flops_rank},
+                                   "sync": st.ms_sync, "tensor_kernels_sum": prof.ms_gemm,
+                                   "tensor_launches": prof.gemm_launches},
+            "roofline": {"bound": "tensor", "kernel": KERNEL_NAMES.get(dominant, dominant),
+                         "achieved": dom.get("tflops"), "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                         "frac": dom.get("frac"), "peak_source": f"{peak_src} bf16_tflops_sustained",
+                         "traffic": dom_traffic,
+                         "launches_per_step": dom.get("launches"), "ms_per_step": dom.get("ms"),
+                         "flops_per_launch": dom["flops"] / dom["launches"] if dom else None,
+                         "method": "algorithmic FLOPs of each launch (2*pixels*taps*Cin*Cout, 2*M*N*K) / its CUDA-event "
+                                   "duration in a profiling pass on the launching stream; traffic = ncu "
+                                   "dram__bytes_read+write per launch of the same kernel (profiles/gemm_traffic.json)",
+                         "by_kind": {kk: {"launches": v["launches"], "ms": round(v["ms"], 4),
+                                          "tflops": round(v["tflops"], 1) if v["tflops"] else None,
+                                          "frac": round(v["frac"], 3) if v["frac"] else None}
+                                     for kk, v in sorted(by_kind.items(), key=lambda kv: -kv[1]["ms"])},
+                         "step": {"achieved": step_achieved,
+                                  "frac": step_achieved / peaks["bf16_tflops_sustained"] if step_achieved else None,
+                                  "flops": flops_rank, "tensor_ms": step_ms,
+                                  "note": "compute_load() FLOPs of the step (reference 3x-forward convention) / "
+                                          "summed durations of all tensor-core launches"}},
             "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4,
                     "ms_per_step": ms_e2e},
             "gpu_launches": st.launches * args.steps,

@@ -163,8 +163,18 @@ void* ralpb_model_stream(ralpb_model* m);
 /* Inspection: copies activation (which=0) or activation-gradient (which=1) buffer i (bf16,
  * padded layout) to host_out (may be NULL to query); returns its element count or -1. */
 long long ralpb_model_debug_buffer(ralpb_model* m, int i, int which, void* host_out);
-/* Profiling mode: bracket every GEMM-engine launch with CUDA events (reported in stats). */
+/* Profiling mode: bracket every tensor-core launch with CUDA events (reported in stats). */
 int ralpb_model_set_profiling(ralpb_model* m, int on);
+/* Per-launch records of the last profiled step: kind = 0 conv fwd/dgrad (single CTA), 1 conv
+ * fwd/dgrad (CTA pair), 2 conv wgrad (CTA pair), 3 conv wgrad (single CTA), 4 first-conv fwd,
+ * 5 first-conv wgrad, 6 GEMM; ms = CUDA-event duration; flops = algorithmic FLOPs.  Returns the
+ * number of records (writes at most cap) or -1. */
+typedef struct {
+  int kind;
+  float ms;
+  double flops;
+} ralpb_launch_rec;
+int ralpb_model_timed_launches(ralpb_model* m, ralpb_launch_rec* out, int cap);
 
 #ifdef __cplusplus
 }

@@ -50,6 +50,7 @@ SIGNATURES: dict[str, tuple] = {
     "ralpb_model_step": (c_i, [c_vp, c_vp, c_vp, c_i, c_f, c_f]),
     "ralpb_model_stats": (c_i, [c_vp, c_vp]),
     "ralpb_model_read_loss": (c_i, [c_vp, c_i, c_vp]),
+    "ralpb_model_timed_launches": (c_i, [c_vp, c_vp, c_i]),
     "ralpb_model_stream": (c_vp, [c_vp]),
     "ralpb_model_set_profiling": (c_i, [c_vp, c_i]),
     "ralpb_model_debug_buffer": (c_ll, [c_vp, c_i, c_i, c_vp]),
@@ -60,6 +61,15 @@ class LayerDesc(C.Structure):
     """ralpb_layer_desc (include/ralpb.h)."""
     _fields_ = [("kind", c_i), ("k", c_i), ("stride", c_i), ("pad", c_i), ("h", c_i), ("w", c_i),
                 ("cin", c_i), ("cout", c_i), ("relu", c_i)]
+
+
+class LaunchRec(C.Structure):
+    """ralpb_launch_rec (include/ralpb.h)."""
+    _fields_ = [("kind", C.c_int), ("ms", C.c_float), ("flops", C.c_double)]
+
+
+LAUNCH_KINDS = ["conv_fwd", "conv_fwd_pair", "conv_wgrad_pair", "conv_wgrad", "first_conv_fwd", "first_conv_wgrad",
+                "gemm"]
 
 
 class StepStats(C.Structure):
@@ -85,7 +95,11 @@ def lib() -> C.CDLL:
                 f"{LIB_PATH} is missing: build it with `python -m paper_1901_05803_b200.build` "
                 "(there is no CPU fallback)")
         handle = C.CDLL(str(LIB_PATH), mode=C.RTLD_GLOBAL)
+        # RALPB_LIB_LENIENT=1 tolerates entry points an older build lacks (A/B timing of builds)
+        lenient = os.environ.get("RALPB_LIB_LENIENT") == "1"
         for name, (res, args) in SIGNATURES.items():
+            if lenient and not hasattr(handle, name):
+                continue
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
@@ -103,3 +117,13 @@ def call(name: str, *args) -> None:
     if rc != 0:
         msg = lib().ralpb_last_error().decode(errors="replace")
         raise BackendError(f"{name} failed ({rc}): {msg}")
+
+
+def call_count(name: str, *args) -> int:
+    """Entry points that return a count (>= 0) or -1 on error."""
+    fn = getattr(lib(), name)
+    rc = fn(*args)
+    if rc < 0:
+        msg = lib().ralpb_last_error().decode(errors="replace")
+        raise BackendError(f"{name} failed ({rc}): {msg}")
+    return rc

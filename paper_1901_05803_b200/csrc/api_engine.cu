@@ -58,6 +58,13 @@ int ralpb_model_stats(ralpb_model* m, ralpb_step_stats* out) {
   return model_stats(m->impl, out, &why) ? set_error("ralpb_model_stats: " + why) : 0;
 }
 
+int ralpb_model_timed_launches(ralpb_model* m, ralpb_launch_rec* out, int cap) {
+  std::string why;
+  int n = 0;
+  if (model_timed_launches(m->impl, out, cap, &n, &why)) return set_error("ralpb_model_timed_launches: " + why);
+  return n;
+}
+
 int ralpb_model_read_loss(ralpb_model* m, int lag, float* out) {
   std::string why;
   return model_read_loss(m->impl, lag, out, &why) ? set_error("ralpb_model_read_loss: " + why) : 0;

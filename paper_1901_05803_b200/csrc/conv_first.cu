@@ -352,7 +352,8 @@ cudaError_t conv_first_fwd(const float* img, int n, int h, int w, int cin, const
   const int smem = 1024 + 4096 + kStages * 8192 + 2 * 16384 + 256;
   const int grid = std::min(p.total, num_sms());
   cudaFuncSetAttribute(conv_first_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  launch_timed([&] { conv_first_fwd_kernel<<<grid, 288, smem, s>>>(p); }, s);
+  launch_timed([&] { conv_first_fwd_kernel<<<grid, 288, smem, s>>>(p); }, s, KIND_FIRST_FWD,
+               2.0 * n * h * w * 27.0 * 64.0);
   return cudaGetLastError();
 }
 
@@ -364,7 +365,8 @@ cudaError_t conv_first_wgrad(const float* img, int n, int h, int w, int cin, con
   const int smem = 1024 + kStages * (16384 + 8192) + 256;
   const int grid = std::min(p.total, num_sms());
   cudaFuncSetAttribute(conv_first_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  launch_timed([&] { conv_first_wgrad_kernel<<<grid, 192, smem, s>>>(p); }, s);
+  launch_timed([&] { conv_first_wgrad_kernel<<<grid, 192, smem, s>>>(p); }, s, KIND_FIRST_WGRAD,
+               2.0 * n * h * w * 27.0 * 64.0);
   return cudaGetLastError();
 }
 

@@ -80,10 +80,15 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
   p.row_bytes = p.kb * 2;
   p.bn = cout >= 256 ? 256 : cout >= 128 ? 128 : cout >= 64 ? 64 : 32;
   p.macc = p.bn >= 256 ? 1 : p.bn >= 128 ? 2 : 4;
-  // CTA pairs for 64/128-wide filter tiles (RALPB_FWD_PAIR=0 disables)
+  // CTA pairs for 128/256-wide filter tiles: each SM loads half of every filter tile (the
+  // 256-wide tiles' filter stream is ~60 B/cycle/SM from L2 on a single CTA).  Measured +5-8 %
+  // (tools/probe_conv.py); not for 64-wide tiles (-20 % on the filter-resident conv1_2 shape)
+  // nor where stacking two row blocks pads the image further (14x14: -35 %).
+  // RALPB_FWD_PAIR=0 disables.
   const char* penv = getenv("RALPB_FWD_PAIR");
-  // (measured: +5-7 % on 128-wide tiles, -20 % on the 64-wide filter-resident conv1_2 shape)
-  const bool pair = p.bn == 128 && !(penv != nullptr && penv[0] == '0');
+  const int rows1 = (g.h + 16 * p.macc - 1) / (16 * p.macc) * 16 * p.macc;
+  const int rows2 = (g.h + 32 * p.macc - 1) / (32 * p.macc) * 32 * p.macc;
+  const bool pair = (p.bn == 128 || p.bn == 256) && rows2 == rows1 && !(penv != nullptr && penv[0] == '0');
   const int ncta = pair ? 2 : 1;
   const int brows = p.bn / ncta;   // filter rows per CTA
   p.acc_bufs = p.macc * p.bn <= 256 ? 2 : 1;
@@ -152,13 +157,13 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       static_cast<void>(cudaLaunchKernelEx(&cfg, kern, p));
-    }, s);
+    }, s, cluster ? KIND_CONV_FWD_PAIR : KIND_CONV_FWD, 2.0 * g.n * g.h * g.w * static_cast<double>(g.taps()) * c * cout);
     launched = true;
   };
 #define RALPB_SLAB_CASE(KK, KS, MA)                                                                   \
   if (g.k == KK && ks == KS && p.macc == MA) {                                                        \
     if (pair) {                                                                                       \
-      if constexpr (MA >= 2) go(conv_slab_fwd_kernel<KK, KS, MA, true>, 128 + 128 * (MA >= 2 ? 2 : 1), true); \
+      go(conv_slab_fwd_kernel<KK, KS, MA, true>, 128 + 128 * (MA >= 2 ? 2 : 1), true);                \
     } else {                                                                                          \
       go(conv_slab_fwd_kernel<KK, KS, MA, false>, 128 + 128 * (MA >= 2 ? 2 : 1), false);              \
     }                                                                                                 \
@@ -217,7 +222,8 @@ cudaError_t conv_slab_wgrad(const ConvGeom& g, const void* x_pad, const void* dy
     const int clusters = static_cast<int>(std::min<long long>(units2, num_sms() / 2));
     auto go2 = [&](auto kern) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      launch_timed([&] { kern<<<2 * clusters, 256, smem2, s>>>(p); }, s);
+      launch_timed([&] { kern<<<2 * clusters, 256, smem2, s>>>(p); }, s, KIND_WGRAD_PAIR,
+                   2.0 * g.n * g.h * g.w * static_cast<double>(g.taps()) * g.cin * g.cout);
     };
     if (bh == 14) go2(conv_slab_wgrad_pair_kernel<14>); else go2(conv_slab_wgrad_pair_kernel<16>);
     cudaError_t e = cudaGetLastError();
@@ -226,7 +232,8 @@ cudaError_t conv_slab_wgrad(const ConvGeom& g, const void* x_pad, const void* dy
   }
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    launch_timed([&] { kern<<<grid, 256, smem, s>>>(p); }, s);
+    launch_timed([&] { kern<<<grid, 256, smem, s>>>(p); }, s, KIND_WGRAD,
+                 2.0 * g.n * g.h * g.w * static_cast<double>(g.taps()) * g.cin * g.cout);
   };
   if (bh == 14) go(conv_slab_wgrad_kernel<14>); else go(conv_slab_wgrad_kernel<16>);
   return cudaGetLastError();

@@ -319,6 +319,8 @@ void model_destroy(Model* m) {
     if (e) cudaEventDestroy(e);
   if (m->timer.ev) {
     for (int i = 0; i < 2 * m->timer.cap; ++i) cudaEventDestroy(m->timer.ev[i]);
+    delete[] m->timer.kind;
+    delete[] m->timer.flops;
     delete[] m->timer.ev;
   }
   if (m->stream) cudaStreamDestroy(m->stream);
@@ -927,10 +929,26 @@ int model_stats(Model* m, ralpb_step_stats* st, std::string* why) {
   return 0;
 }
 
+// Per-launch records of the last profiled step (kind, CUDA-event time, algorithmic FLOPs).
+int model_timed_launches(Model* m, ralpb_launch_rec* out, int cap, int* n, std::string* why) {
+  RALPB_TRY(cudaStreamSynchronize(m->stream));
+  *n = m->profiling ? m->timer.n : 0;
+  for (int i = 0; i < *n && i < cap; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, m->timer.ev[2 * i], m->timer.ev[2 * i + 1]);
+    out[i].kind = m->timer.kind[i];
+    out[i].ms = ms;
+    out[i].flops = m->timer.flops[i];
+  }
+  return 0;
+}
+
 int model_set_profiling(Model* m, int on, std::string* why) {
   if (on && m->timer.ev == nullptr) {
     m->timer.cap = 256;
     m->timer.ev = new cudaEvent_t[2 * m->timer.cap];
+    m->timer.kind = new int[m->timer.cap];
+    m->timer.flops = new double[m->timer.cap];
     for (int i = 0; i < 2 * m->timer.cap; ++i) RALPB_TRY(cudaEventCreate(&m->timer.ev[i]));
   }
   m->profiling = on != 0;

@@ -138,5 +138,6 @@ int model_get_params(Model* m, int layer, float* w, float* b, int on_host, std::
 int model_ipc_handle(Model* m, void* out, std::string* why);
 int model_ipc_open(Model* m, const void* handles, std::string* why);
 int model_set_profiling(Model* m, int on, std::string* why);
+int model_timed_launches(Model* m, ralpb_launch_rec* out, int cap, int* n, std::string* why);
 
 }  // namespace ralpb

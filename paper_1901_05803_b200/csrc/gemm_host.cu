@@ -151,7 +151,8 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
   }
   const long long total = static_cast<long long>(p.n_mt) * p.n_nt * p.n_ks;
   const int grid = static_cast<int>(std::min<long long>(total, sms));
-  launch_timed([&] { gemm_sm100_kernel<<<grid, kThreads, smem, stream>>>(p); }, stream);
+  launch_timed([&] { gemm_sm100_kernel<<<grid, kThreads, smem, stream>>>(p); }, stream, KIND_GEMM,
+               2.0 * d.M * d.N * static_cast<double>(d.K));
   return cudaGetLastError();
 }
 

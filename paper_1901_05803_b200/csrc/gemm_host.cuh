@@ -48,20 +48,37 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
 int num_sms();
 
 // Optional per-launch timing of the GEMM engine (CUDA events on the launch stream).
+// Tensor-core kernel families, as reported per timed launch (ralpb_launch_rec.kind).
+enum LaunchKind {
+  KIND_CONV_FWD = 0,      // conv_slab_fwd_kernel, single CTA (forward and backward-data)
+  KIND_CONV_FWD_PAIR = 1, // conv_slab_fwd_kernel, CTA pairs
+  KIND_WGRAD_PAIR = 2,    // conv_slab_wgrad_pair_kernel
+  KIND_WGRAD = 3,         // conv_slab_wgrad_kernel
+  KIND_FIRST_FWD = 4,     // conv_first_fwd_kernel
+  KIND_FIRST_WGRAD = 5,   // conv_first_wgrad_kernel
+  KIND_GEMM = 6,          // gemm_sm100_kernel
+};
+
 struct GemmTimer {
   cudaEvent_t* ev = nullptr;  // 2*cap events
   int cap = 0;
   int n = 0;
+  int* kind = nullptr;        // [cap]
+  double* flops = nullptr;    // [cap] algorithmic FLOPs of the launch
 };
 void set_gemm_timer(GemmTimer* t);  // thread-local; nullptr disables
 GemmTimer* current_gemm_timer();
 
 // Launch `f` (a kernel launch on stream s) bracketed by the timer's events, if armed.
 template <class F>
-void launch_timed(F&& f, cudaStream_t s) {
+void launch_timed(F&& f, cudaStream_t s, int kind = KIND_GEMM, double flops = 0.0) {
   GemmTimer* tm = current_gemm_timer();
   const bool timed = tm != nullptr && tm->n < tm->cap;
-  if (timed) cudaEventRecord(tm->ev[2 * tm->n], s);
+  if (timed) {
+    cudaEventRecord(tm->ev[2 * tm->n], s);
+    tm->kind[tm->n] = kind;
+    tm->flops[tm->n] = flops;
+  }
   f();
   if (timed) cudaEventRecord(tm->ev[2 * tm->n++ + 1], s);
 }

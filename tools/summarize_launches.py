@@ -17,6 +17,21 @@ from collections import OrderedDict, defaultdict
 TENSOR = re.compile(r"conv_slab_(fwd|wgrad)\w*_kernel|conv_first_\w+_kernel|gemm_sm100_kernel")
 
 
+def kind_of(name: str) -> str:
+    """Map a kernel name to the engine's launch kind (ralpb_launch_rec.kind names)."""
+    if "conv_slab_wgrad_pair" in name:
+        return "conv_wgrad_pair"
+    if "conv_slab_wgrad" in name:
+        return "conv_wgrad"
+    if "conv_slab_fwd" in name:
+        return "conv_fwd_pair" if re.search(r"\(bool\)1|, 1>|,\s*true>", name) else "conv_fwd"
+    if "conv_first_fwd" in name:
+        return "first_conv_fwd"
+    if "conv_first_wgrad" in name:
+        return "first_conv_wgrad"
+    return "gemm"
+
+
 def family(name: str) -> str:
     n = re.sub(r"\(.*", "", name)
     n = re.sub(r"^void ", "", n)
@@ -76,9 +91,18 @@ def main():
         print(f"  {family(r['name'])[:70]:70s} grid {r['grid']:>14s} {r.get('ns', 0) / 1e3:9.1f} us {by / 1e6:9.1f} MB")
     if a.traffic_json:
         t = [r for r in step if TENSOR.search(r["name"])]
+        per_kind = defaultdict(lambda: {"launches": 0, "dram_bytes": 0.0, "ms": 0.0})
+        for r in t:
+            k = per_kind[kind_of(r["name"])]
+            k["launches"] += 1
+            k["dram_bytes"] += r.get("dram__bytes_read.sum", 0) + r.get("dram__bytes_write.sum", 0)
+            k["ms"] += r.get("ns", 0) / 1e6
+        for k in per_kind.values():
+            k["dram_bytes_per_launch"] = k["dram_bytes"] / k["launches"]
         out = {"source": a.csv, "step": a.step, "tensor_launches": len(t),
                "dram_bytes_per_step": sum(r.get("dram__bytes_read.sum", 0) + r.get("dram__bytes_write.sum", 0) for r in t),
                "serialized_ms": sum(r.get("ns", 0) for r in t) / 1e6,
+               "per_kind": per_kind,
                "note": "ncu launch list, cold-cache serialized launches; bytes summed over the step's tcgen05 kernels"}
         with open(a.traffic_json, "w") as f:
             json.dump(out, f, indent=1)
