@@ -80,18 +80,6 @@ __device__ __forceinline__ void load_filters(const FirstConvParams& p, uint8_t* 
   }
 }
 
-__device__ __forceinline__ void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void named_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void tma_store_4d(const CUtensorMap* tm, const void* src, int c0, int c1, int c2, int c3) {
-  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-                   reinterpret_cast<uint64_t>(tm)),
-               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-               : "memory");
-}
 __device__ __forceinline__ void tma_load_4d_cta(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1,
                                                 int c2, int c3) {
   asm volatile(
@@ -99,15 +87,6 @@ __device__ __forceinline__ void tma_load_4d_cta(void* dst, const CUtensorMap* tm
       " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait() {
-  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ void tile_coords(const FirstConvParams& p, int t, int& img, int& y0, int& x0) {
@@ -135,7 +114,7 @@ __global__ void __launch_bounds__(288, 1) conv_first_fwd_kernel(const __grid_con
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   load_filters(p, sB);
-  fence_async_smem();
+  fence_proxy_async_smem();
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) { mbar_init(&a_full[i], 128); mbar_init(&a_empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128); }
@@ -156,7 +135,7 @@ __global__ void __launch_bounds__(288, 1) conv_first_fwd_kernel(const __grid_con
       tile_coords(p, t, img, y0, x0);
       mbar_wait(&a_empty[st], ph ^ 1);
       build_patch_row(p, img, y0 + m / kTW, x0 + m % kTW, sA + st * 8192, m);
-      fence_async_smem();
+      fence_proxy_async_smem();
       mbar_arrive(&a_full[st]);
       if (++st == kStages) { st = 0; ph ^= 1; }
     }
@@ -200,7 +179,7 @@ __global__ void __launch_bounds__(288, 1) conv_first_fwd_kernel(const __grid_con
       mbar_arrive(&tempty[acc]);
       // the staging buffer written two tiles ago must have been read by its TMA store
       if (m == 0) bulk_wait_read<1>();
-      named_sync(1, 128);
+      named_bar_sync(1, 128);
       uint8_t* row = sOut + ob * 16384 + m * 128;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -211,8 +190,8 @@ __global__ void __launch_bounds__(288, 1) conv_first_fwd_kernel(const __grid_con
         u.w = pack_bf16(fmaxf(__uint_as_float(rr[8 * c + 6]), 0.f), fmaxf(__uint_as_float(rr[8 * c + 7]), 0.f));
         *reinterpret_cast<uint4*>(row + ((c ^ (m & 7)) << 4)) = u;
       }
-      fence_async_smem();
-      named_sync(1, 128);
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
       if (m == 0) {
         tma_store_4d(&p.tmY, sOut + ob * 16384, 0, x0 + p.pad_out, y0 + p.pad_out, img);
         bulk_commit();
@@ -220,7 +199,7 @@ __global__ void __launch_bounds__(288, 1) conv_first_fwd_kernel(const __grid_con
       ob ^= 1;
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
     }
-    if (m == 0) bulk_wait<0>();
+    if (m == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -263,7 +242,7 @@ __global__ void __launch_bounds__(192, 1) conv_first_wgrad_kernel(const __grid_c
       tile_coords(p, t, img, y0, x0);
       mbar_wait(&empty[st], ph ^ 1);
       build_patch_row(p, img, y0 + m / kTW, x0 + m % kTW, sP + st * 8192, m);
-      fence_async_smem();
+      fence_proxy_async_smem();
       mbar_arrive(&full[st]);
       if (++st == kStages) { st = 0; ph ^= 1; }
     }

@@ -52,6 +52,25 @@ bool encode_mat(CUtensorMap* tm, const void* ptr, long long rows, long long cols
   return true;
 }
 
+// Interior view of a padded activation [n][hp][wp][c]: dims {c, w, h, n} starting at pixel
+// (pad, pad) with the padded strides, box {32, 8, 16, 1}, 64B swizzle -- TMA stores through it
+// clip at the image edge, so the zero borders are never written.
+bool encode_interior(CUtensorMap* tm, void* ptr, long long c, long long w, long long h, long long wp, long long hp,
+                     long long n, int pad, std::string* why) {
+  char* base = static_cast<char*>(ptr) + (static_cast<long long>(pad) * wp + pad) * c * 2;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w), static_cast<cuuint64_t>(h),
+                        static_cast<cuuint64_t>(n)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * 2, static_cast<cuuint64_t>(wp * c) * 2,
+                           static_cast<cuuint64_t>(hp * wp * c) * 2};
+  cuuint32_t box[4] = {32, 8, 16, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = encoder()(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { *why = "interior tensor map encode failed (" + std::to_string(static_cast<int>(r)) + ")"; return false; }
+  return true;
+}
+
 namespace {
 
 int align1k(int x) { return (x + 1023) & ~1023; }
@@ -60,7 +79,8 @@ constexpr int kSmemBudget = 227 * 1024 - 1024 - 512 - 2048;
 }  // namespace
 
 bool slab_fwd_ok(const ConvGeom& g, int c, int cout) {
-  return g.k == 2 * g.pad + 1 && (g.k == 3 || g.k == 5) && (c == 16 || c == 32 || c % 64 == 0) && cout % 16 == 0 &&
+  // cout % 32: the TMA-store epilogue writes 32-channel boxes
+  return g.k == 2 * g.pad + 1 && (g.k == 3 || g.k == 5) && (c == 16 || c == 32 || c % 64 == 0) && cout % 32 == 0 &&
          g.q() < (1LL << 31);
 }
 
@@ -91,24 +111,33 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
   const bool pair = (p.bn == 128 || p.bn == 256) && rows2 == rows1 && !(penv != nullptr && penv[0] == '0');
   const int ncta = pair ? 2 : 1;
   const int brows = p.bn / ncta;   // filter rows per CTA
-  p.acc_bufs = p.macc * p.bn <= 256 ? 2 : 1;
-  const int used = p.macc * p.bn * p.acc_bufs;
-  p.tmem_cols = used <= 32 ? 32 : used <= 64 ? 64 : used <= 128 ? 128 : used <= 256 ? 256 : 512;
   p.sw = 8 + g.k - 1;
-  p.sh = 16 * p.macc + g.k - 1;
-  p.slab_load = p.row_bytes * p.sw * p.sh;
-  p.slab_stage = align1k(p.slab_load);
   p.b_load = brows * p.row_bytes;
   p.b_stage = align1k(p.b_load);
   p.na = 2;
-  p.nb = std::min(8, (kSmemBudget - p.na * p.slab_stage) / p.b_stage);
+  int staging = 0, budget = 0;
+  // M accumulators per tile: shrink until two slab stages, two filter stages and the output
+  // staging (2 x 8 KB per epilogue warpgroup, TMA-store epilogue) fit in shared memory
+  for (;;) {
+    p.sh = 16 * p.macc + g.k - 1;
+    p.slab_load = p.row_bytes * p.sw * p.sh;
+    p.slab_stage = align1k(p.slab_load);
+    staging = (p.macc >= 2 ? 2 : 1) * 2 * 8192;
+    budget = kSmemBudget - staging;
+    p.nb = std::min(8, (budget - p.na * p.slab_stage) / p.b_stage);
+    if (p.nb >= 2 || p.macc == 1) break;
+    p.macc /= 2;
+  }
+  p.acc_bufs = p.macc * p.bn <= 256 ? 2 : 1;
+  const int used = p.macc * p.bn * p.acc_bufs;
+  p.tmem_cols = used <= 32 ? 32 : used <= 64 ? 64 : used <= 128 ? 128 : used <= 256 ? 256 : 512;
   // Filters resident in shared memory when one channel block and one N tile cover the layer
   // (e.g. 64->64 at 224x224): the per-tile filter reloads disappear.
   if (c == p.kb && cout <= p.bn && p.macc >= 2) {
     const int macc2 = 2;
     const int slab2 = align1k(p.row_bytes * p.sw * (16 * macc2 + g.k - 1));
-    const int na2 = 3;
-    if (g.taps() * p.b_stage + na2 * slab2 <= kSmemBudget && g.taps() <= 16) {
+    const int na2 = g.taps() * p.b_stage + 3 * slab2 <= budget ? 3 : 2;
+    if (g.taps() * p.b_stage + na2 * slab2 <= budget && g.taps() <= 16) {
       p.wres = 1;
       p.macc = macc2;
       p.sh = 16 * macc2 + g.k - 1;
@@ -135,7 +164,8 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
     return cudaErrorInvalidValue;
   if (!encode_mat(&p.tmB, w, cout, static_cast<long long>(g.taps()) * c, p.kb, brows, p.row_bytes, why))
     return cudaErrorInvalidValue;
-  const int smem = 1024 + p.na * p.slab_stage + p.nb * p.b_stage + 512 + 2048;  // barriers, colsum
+  if (!encode_interior(&p.tmY, y_pad, cout, g.w, g.h, g.wp(), g.hp(), g.n, g.pad, why)) return cudaErrorInvalidValue;
+  const int smem = 1024 + p.na * p.slab_stage + p.nb * p.b_stage + staging + 512 + 2048;  // barriers, colsum
   const long long total = static_cast<long long>(g.n) * p.n_hb * p.n_wb * p.n_nt;
   const int grid = pair ? 2 * static_cast<int>(std::min<long long>(total, num_sms() / 2))
                         : static_cast<int>(std::min<long long>(total, num_sms()));

@@ -39,6 +39,7 @@ constexpr int kSlabMaxTaps = 25;
 struct alignas(64) SlabConvParams {
   CUtensorMap tmX;      // activation [N][Hp][Wp][C], box {kb, SW, SH, 1}
   CUtensorMap tmB;      // fwd: filters [Cout][taps*C] box {kb, BN}; wgrad: dY [N][Hp][Wp][Cout] box {64, 8, 16, 1}
+  CUtensorMap tmY;      // fwd: output INTERIOR view {Cout, W, H, N} (padded strides), box {32, 8, 16, 1}, SW64
   int n, h, w, hp, wp, pad, k, taps;
   int c;                // contracted channels (fwd: input channels of the GEMM; wgrad: layer cin)
   int cout;             // output channels of the GEMM (fwd) / layer cout (wgrad)
@@ -88,7 +89,8 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = sA + p.na * p.slab_stage;
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(sB + p.nb * p.b_stage);
+  uint8_t* sOut = sB + p.nb * p.b_stage;         // EWG x 2 x 8 KB output staging (TMA store)
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(sOut + EWG * 2 * 8192);
   uint64_t* a_empty = a_full + p.na;
   uint64_t* b_full = a_empty + p.na;
   uint64_t* b_empty = b_full + p.nb;
@@ -239,8 +241,9 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
     const int g = (warp - 4) >> 2;   // epilogue warpgroup
     const int q = warp & 3;          // TMEM lane quarter
     const int m = q * 32 + lane;
-    int acc = 0;
+    int acc = 0, ob = 0;
     uint32_t acc_ph = 0;
+    uint8_t* stage = sOut + g * 2 * 8192;
     for (int wi = w_first; wi < total; wi += w_step) {
       int t = wi;
       const int nt = t % p.n_nt; t /= p.n_nt;
@@ -250,7 +253,8 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
       mbar_wait(&tfull[acc], acc_ph);
       tc_fence_after();
       for (int a = g; a < p.macc; a += EWG) {
-        const int hh = (hb * NCTA + static_cast<int>(rank)) * mrows + a * 16 + (m >> 3);
+        const int h0 = (hb * NCTA + static_cast<int>(rank)) * mrows + a * 16;
+        const int hh = h0 + (m >> 3);
         const int ww = wb * 8 + (m & 7);
         const bool valid = hh < p.h && ww < p.w;
         const long long orow = (static_cast<long long>(img) * p.hp + hh + p.pad) * p.wp + ww + p.pad;
@@ -266,16 +270,23 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
           const bool full = n0 + 32 <= p.cout;
           if (p.bias != nullptr) {
+            if (full) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += (full || n0 + j < p.cout) ? __ldg(p.bias + n0 + j) : 0.f;
+              for (int j4 = 0; j4 < 8; ++j4) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + n0) + j4);
+                v[4 * j4] += b4.x; v[4 * j4 + 1] += b4.y; v[4 * j4 + 2] += b4.z; v[4 * j4 + 3] += b4.w;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += n0 + j < p.cout ? __ldg(p.bias + n0 + j) : 0.f;
+            }
           }
           if (p.relu) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
           }
-          const long long oidx = orow * p.cout + n0;
           if (p.mask != nullptr && valid) {
-            const __nv_bfloat16* mp = p.mask + oidx;
+            const __nv_bfloat16* mp = p.mask + orow * p.cout + n0;
             if (full) {
 #pragma unroll
               for (int j4 = 0; j4 < 4; ++j4) {
@@ -293,16 +304,23 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
           uint32_t pk[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
-          if (valid) {
-            __nv_bfloat16* o = p.out + oidx;
-            if (full) {
+          // stage this pixel's 32 channels (one 64-byte SW64 row: chunk j at j ^ ((m >> 1) & 3))
+          // and write the 16x8-pixel x 32-channel block with one TMA store; the interior-view
+          // tensor map clips rows/columns outside the image, so borders are never written
+          uint8_t* buf = stage + ob * 8192;
+          if (m == 0) bulk_wait_read<1>();
+          named_bar_sync(1 + g, 128);
 #pragma unroll
-              for (int j4 = 0; j4 < 4; ++j4)
-                *reinterpret_cast<uint4*>(o + j4 * 8) = make_uint4(pk[4 * j4], pk[4 * j4 + 1], pk[4 * j4 + 2], pk[4 * j4 + 3]);
-            } else {
-              _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n0 + j < p.cout) o[j] = __float2bfloat16_rn(v[j]);
-            }
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<uint4*>(buf + m * 64 + ((j ^ ((m >> 1) & 3)) << 4)) =
+                make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          fence_proxy_async_smem();
+          named_bar_sync(1 + g, 128);
+          if (m == 0) {
+            tma_store_4d(&p.tmY, buf, n0, wb * 8, h0, img);
+            bulk_commit();
           }
+          ob ^= 1;
           if (p.colsum != nullptr) {
             // sum of the stored bf16 values over this warp's 32 pixels: transpose-reduce so
             // that lane l ends with channel n0 + l (31 shuffles), then one shared atomic
@@ -331,6 +349,7 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
       if constexpr (PAIR) mbar_arrive_cluster(lead(&tempty[acc])); else mbar_arrive(&tempty[acc]);
       if (++acc == p.acc_bufs) { acc = 0; acc_ph ^= 1; }
     }
+    if (m == 0) bulk_wait_all();
   }
   tc_fence_before();
   if constexpr (PAIR) {
