@@ -102,13 +102,16 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
   p.macc = p.bn >= 256 ? 1 : p.bn >= 128 ? 2 : 4;
   // CTA pairs for 128/256-wide filter tiles: each SM loads half of every filter tile (the
   // 256-wide tiles' filter stream is ~60 B/cycle/SM from L2 on a single CTA).  Measured +5-8 %
-  // (tools/probe_conv.py); not for 64-wide tiles (-20 % on the filter-resident conv1_2 shape)
-  // nor where stacking two row blocks pads the image further (14x14: -35 %).
+  // (tools/probe_conv.py); not for the 64-wide filter-resident conv1_2 shape (-20 %) nor where
+  // stacking two row blocks pads the image further (14x14: -35 %).
   // RALPB_FWD_PAIR=0 disables.
   const char* penv = getenv("RALPB_FWD_PAIR");
   const int rows1 = (g.h + 16 * p.macc - 1) / (16 * p.macc) * 16 * p.macc;
   const int rows2 = (g.h + 32 * p.macc - 1) / (32 * p.macc) * 32 * p.macc;
-  const bool pair = (p.bn == 128 || p.bn == 256) && rows2 == rows1 && !(penv != nullptr && penv[0] == '0');
+  // 64-wide tiles pair up only outside the filter-resident mode (conv2_1 dgrad: +10 %)
+  const bool wres_shape = c == p.kb && cout <= p.bn;
+  const bool pair = (p.bn == 128 || p.bn == 256 || (p.bn == 64 && !wres_shape)) && rows2 == rows1 &&
+                    !(penv != nullptr && penv[0] == '0');
   const int ncta = pair ? 2 : 1;
   const int brows = p.bn / ncta;   // filter rows per CTA
   p.sw = 8 + g.k - 1;
