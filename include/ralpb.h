@@ -55,6 +55,12 @@ int ralpb_gemm_bf16(const void* a, long long a_rows, long long a_cols, long long
  *   gradient of the convolution that produced the masked activation, fused into this producer. */
 int ralpb_conv_fwd(const void* x_pad, const void* w, const float* bias, void* y_pad, int n, int h,
                    int w_, int cin, int cout, int k, int pad, int relu, void* stream);
+/* conv_fwd plus the 2x2/2 max pool of its output (max_pool2d, layers.py:106-114) written to
+ * pool_out [n][h/2+2pp][w/2+2pp][cout] (interior), fused into the epilogue: the pool reads no
+ * activation back from HBM.  h, w even; errors where the slab kernels do not apply. */
+int ralpb_conv_fwd_pool(const void* x_pad, const void* w, const float* bias, void* y_pad, void* pool_out,
+                        int pool_pad, int n, int h, int w_, int cin, int cout, int k, int pad, int relu,
+                        void* stream);
 int ralpb_conv_dgrad(const void* dy_pad, const void* wd, const void* mask_pad, void* dx_pad, float* colsum,
                      int n, int h, int w_, int cin, int cout, int k, int pad, void* stream);
 int ralpb_conv_wgrad(const void* x_pad, const void* dy_pad, float* dw, float* db, int n, int h, int w_,

@@ -49,6 +49,15 @@ int ralpb_conv_fwd(const void* x_pad, const void* w, const float* bias, void* y_
   return set_status(conv_fwd(g, x_pad, w, bias, y_pad, relu, static_cast<cudaStream_t>(stream), &why), why);
 }
 
+int ralpb_conv_fwd_pool(const void* x_pad, const void* w, const float* bias, void* y_pad, void* pool_out,
+                        int pool_pad, int n, int h, int w_, int cin, int cout, int k, int pad, int relu,
+                        void* stream) {
+  std::string why;
+  ConvGeom g{n, h, w_, cin, cout, k, pad};
+  return set_status(conv_fwd_pool(g, x_pad, w, bias, y_pad, relu, pool_out, pool_pad,
+                                  static_cast<cudaStream_t>(stream), &why), why);
+}
+
 int ralpb_conv_dgrad(const void* dy_pad, const void* wd, const void* mask_pad, void* dx_pad, float* colsum,
                      int n, int h, int w_, int cin, int cout, int k, int pad, void* stream) {
   std::string why;

@@ -125,6 +125,16 @@ cudaError_t conv_fwd(const ConvGeom& g, const void* x_pad, const void* w, const 
   return conv_fwd_flat(g, x_pad, w, bias, y_pad, relu, s, why);
 }
 
+bool conv_fwd_pool_ok(const ConvGeom& g) {
+  return pick_slab(slab_fwd_ok(g, g.cin, g.cout), true) && g.h % 2 == 0 && g.w % 2 == 0;
+}
+
+cudaError_t conv_fwd_pool(const ConvGeom& g, const void* x_pad, const void* w, const float* bias, void* y_pad,
+                          int relu, void* pool_out, int pool_pad, cudaStream_t s, std::string* why) {
+  if (!conv_fwd_pool_ok(g)) { *why = "conv_fwd_pool: shape not supported by the slab kernels"; return cudaErrorInvalidValue; }
+  return conv_slab_fwd(g, x_pad, w, g.cin, g.cout, bias, relu, nullptr, y_pad, nullptr, s, why, pool_out, pool_pad);
+}
+
 cudaError_t conv_dgrad(const ConvGeom& g, const void* dy_pad, const void* wd, const void* mask_pad,
                        void* dx_pad, float* colsum, cudaStream_t s, std::string* why) {
   if (pick_slab(slab_fwd_ok(g, g.cout, g.cin), true))

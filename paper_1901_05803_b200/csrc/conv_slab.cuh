@@ -60,6 +60,8 @@ struct alignas(64) SlabConvParams {
   int relu;
   const __nv_bfloat16* mask;
   float* colsum;        // optional: += per-channel sum over pixels of the stored (bf16) output
+  __nv_bfloat16* pool_out;  // optional fused 2x2/2 max pool of the stored output: [n][h/2+2pp][w/2+2pp][cout]
+  int pool_pad;
   // wgrad
   float* dw;
   float* db;
@@ -321,6 +323,30 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
             bulk_commit();
           }
           ob ^= 1;
+          if (p.pool_out != nullptr) {
+            // fused 2x2/2 max pool: a warp holds 4 image rows x 8 columns, so the window of an
+            // (even row, even column) pixel is lanes {l, l^1, l^8, l^9}
+            uint32_t mx[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(&pk[j]);
+              uint32_t o = __shfl_xor_sync(0xffffffffu, pk[j], 1);
+              a2 = __hmax2(a2, *reinterpret_cast<const __nv_bfloat162*>(&o));
+              uint32_t t2 = *reinterpret_cast<uint32_t*>(&a2);
+              o = __shfl_xor_sync(0xffffffffu, t2, 8);
+              a2 = __hmax2(a2, *reinterpret_cast<const __nv_bfloat162*>(&o));
+              mx[j] = *reinterpret_cast<uint32_t*>(&a2);
+            }
+            if ((m & 9) == 0 && valid) {
+              const int ph = hh >> 1, pw = ww >> 1;
+              const long long prow = (static_cast<long long>(img) * ((p.h >> 1) + 2 * p.pool_pad) + ph + p.pool_pad) *
+                                         ((p.w >> 1) + 2 * p.pool_pad) + pw + p.pool_pad;
+              __nv_bfloat16* po = p.pool_out + prow * p.cout + n0;
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                *reinterpret_cast<uint4*>(po + 8 * j) = make_uint4(mx[4 * j], mx[4 * j + 1], mx[4 * j + 2], mx[4 * j + 3]);
+            }
+          }
           if (p.colsum != nullptr) {
             // sum of the stored bf16 values over this warp's 32 pixels: transpose-reduce so
             // that lane l ends with channel n0 + l (31 shuffles), then one shared atomic

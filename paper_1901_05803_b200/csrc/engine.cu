@@ -661,6 +661,11 @@ cudaError_t mark(Model* m, int i, bool capturing) {
 
 // Everything of one step after the inputs are resident in HBM: bump the device step
 // counter, front forward, cut exchange, back segment, front backward, sync, re-layout.
+bool fuse_pool_enabled() {
+  const char* e = getenv("RALPB_FUSE_POOL");
+  return e == nullptr || e[0] != '0';
+}
+
 int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu, bool capturing,
               std::string* why) {
   const uint32_t* seq = m->seq_dev;
@@ -707,6 +712,18 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
       d.pad = out.pad; d.h = out.h; d.w = out.w;
       RALPB_TRY(gemm_launch(d, s, why));
     } else if (f.kind == RALPB_CONV) {
+      // a following 2x2/2 max pool is fused into the conv epilogue (RALPB_FUSE_POOL=0: separate)
+      const bool pool_next = i + 1 < m->front.size() && m->front[i + 1].kind == RALPB_POOL &&
+                             m->front[i + 1].k == 2 && m->front[i + 1].stride == 2 && conv_fwd_pool_ok(f.g) &&
+                             fuse_pool_enabled();
+      if (pool_next) {
+        const ActBuf& pooled = m->acts[i + 2];
+        bf16* pdst = i + 2 == m->front.size() ? cut_dst : pooled.ptr;
+        RALPB_TRY(conv_fwd_pool(f.g, in.ptr, f.wf, m->P + f.b_off, out.ptr, 1, pdst, pooled.pad, s, why));
+        ++m->launches;
+        ++i;  // the pool layer is done
+        continue;
+      }
       RALPB_TRY(conv_fwd(f.g, in.ptr, f.wf, m->P + f.b_off, out.ptr, 1, s, why));
     } else {
       RALPB_TRY(maxpool_fwd(in.ptr, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.ptr, out.pad, s));

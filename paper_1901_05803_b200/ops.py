@@ -49,6 +49,15 @@ def conv_fwd(x_pad, w, bias, *, n, h, w_, cin, cout, k, pad, relu=True, out=None
     return out
 
 
+def conv_fwd_pool(x_pad, w, bias, *, n, h, w_, cin, cout, k, pad, relu=True, pool_pad=1):
+    """(y, pooled): conv fwd and its 2x2/2 max pool from one kernel."""
+    y = torch.zeros(n, h + 2 * pad, w_ + 2 * pad, cout, dtype=_BF16, device=x_pad.device)
+    pooled = torch.zeros(n, h // 2 + 2 * pool_pad, w_ // 2 + 2 * pool_pad, cout, dtype=_BF16, device=x_pad.device)
+    call("ralpb_conv_fwd_pool", x_pad.data_ptr(), w.data_ptr(), _p(bias), y.data_ptr(), pooled.data_ptr(), pool_pad,
+         n, h, w_, cin, cout, k, pad, int(relu), _stream())
+    return y, pooled
+
+
 def conv_first_fwd(img, wf, *, pad_out=1):
     """Fused im2col + first conv (3x3/1/1, 3 -> 64, ReLU); img fp32 [n,h,w,3], wf bf16 [64,32]."""
     n, h, w, _ = img.shape

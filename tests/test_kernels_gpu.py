@@ -267,3 +267,23 @@ def test_first_conv_fused(n, h, w):
     refb = dyr.sum(dim=(0, 2, 3))
     _close(dw[:, 27], refb, rtol=1e-3, atol=1e-3 * refb.abs().max().item())
     assert dw[:, 28:].abs().max().item() == 0.0
+
+
+@pytest.mark.parametrize("case", [(2, 8, 16, 64, 64, 3, 1), (2, 28, 28, 256, 512, 3, 1), (1, 56, 56, 128, 256, 3, 1),
+                                  (2, 14, 14, 512, 512, 3, 1), (2, 32, 32, 32, 64, 5, 2)])
+def test_conv_fwd_fused_pool(case):
+    """conv fwd with the 2x2/2 max pool fused into its epilogue == max_pool2d of its own output."""
+    n, h, w, cin, cout, k, pad = case
+    g = torch.Generator(device=DEV).manual_seed(14)
+    x = _pad(_bf(n, h, w, cin, gen=g), pad).contiguous()
+    wt = _bf(cout, k * k, cin, scale=(2.0 / (k * k * cin)) ** 0.5, gen=g)
+    bias = torch.randn(cout, device=DEV) * 0.1
+    y, pooled = ops.conv_fwd_pool(x, wt, bias, n=n, h=h, w_=w, cin=cin, cout=cout, k=k, pad=pad, pool_pad=1)
+    y_ref = ops.conv_fwd(x, wt, bias, n=n, h=h, w_=w, cin=cin, cout=cout, k=k, pad=pad, relu=True)
+    torch.testing.assert_close(y.float(), y_ref.float(), rtol=0, atol=0)
+    yi = y[:, pad:pad + h, pad:pad + w, :].permute(0, 3, 1, 2).float()
+    ref = F.max_pool2d(yi, 2).permute(0, 2, 3, 1)
+    torch.testing.assert_close(pooled[:, 1:-1, 1:-1, :].float(), ref, rtol=0, atol=0)
+    border = pooled.clone()
+    border[:, 1:-1, 1:-1, :] = 0
+    assert border.abs().max().item() == 0.0
