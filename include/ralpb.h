@@ -57,10 +57,16 @@ int ralpb_conv_fwd(const void* x_pad, const void* w, const float* bias, void* y_
                    int w_, int cin, int cout, int k, int pad, int relu, void* stream);
 /* conv_fwd plus the 2x2/2 max pool of its output (max_pool2d, layers.py:106-114) written to
  * pool_out [n][h/2+2pp][w/2+2pp][cout] (interior), fused into the epilogue: the pool reads no
- * activation back from HBM.  h, w even; errors where the slab kernels do not apply. */
+ * activation back from HBM.  h, w even; errors where the slab kernels do not apply.
+ * pool_idx (may be NULL): uint8 [n][h/2][w/2][cout], the window position (0..3 row-major) of the
+ * first max, 255 where the max is not > 0 -- input of ralpb_maxpool_bwd_idx. */
 int ralpb_conv_fwd_pool(const void* x_pad, const void* w, const float* bias, void* y_pad, void* pool_out,
-                        int pool_pad, int n, int h, int w_, int cin, int cout, int k, int pad, int relu,
-                        void* stream);
+                        int pool_pad, void* pool_idx, int n, int h, int w_, int cin, int cout, int k, int pad,
+                        int relu, void* stream);
+/* 2x2/2 max-pool backward from those argmax bytes: dx (interior of [n][2oh+2pi][2ow+2pi][c]) gets
+ * dy at the recorded position, 0 elsewhere (ReLU mask included); colsum as ralpb_maxpool_bwd. */
+int ralpb_maxpool_bwd_idx(const void* idx, const void* dy, int n, int oh, int ow, int c, int pad_out, int pad_in,
+                          void* dx, float* colsum, void* stream);
 int ralpb_conv_dgrad(const void* dy_pad, const void* wd, const void* mask_pad, void* dx_pad, float* colsum,
                      int n, int h, int w_, int cin, int cout, int k, int pad, void* stream);
 int ralpb_conv_wgrad(const void* x_pad, const void* dy_pad, float* dw, float* db, int n, int h, int w_,

@@ -30,7 +30,9 @@ SIGNATURES: dict[str, tuple] = {
     "ralpb_conv_fwd": (c_i, [c_vp, c_vp, c_fp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),
     "ralpb_conv_first_fwd": (c_i, [c_vp, c_i, c_i, c_i, c_vp, c_vp, c_i, c_vp]),
     "ralpb_conv_first_wgrad": (c_i, [c_vp, c_i, c_i, c_i, c_vp, c_i, c_vp, c_vp]),
-    "ralpb_conv_fwd_pool": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),
+    "ralpb_conv_fwd_pool": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i,
+                                  c_vp]),
+    "ralpb_maxpool_bwd_idx": (c_i, [c_vp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_vp, c_vp, c_vp]),
     "ralpb_conv_dgrad": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),
     "ralpb_conv_wgrad": (c_i, [c_vp, c_vp, c_fp, c_fp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),
     "ralpb_pack_input": (c_i, [c_fp, c_i, c_i, c_i, c_i, c_vp, c_i, c_i, c_vp]),

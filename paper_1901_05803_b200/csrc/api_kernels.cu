@@ -50,12 +50,20 @@ int ralpb_conv_fwd(const void* x_pad, const void* w, const float* bias, void* y_
 }
 
 int ralpb_conv_fwd_pool(const void* x_pad, const void* w, const float* bias, void* y_pad, void* pool_out,
-                        int pool_pad, int n, int h, int w_, int cin, int cout, int k, int pad, int relu,
-                        void* stream) {
+                        int pool_pad, void* pool_idx, int n, int h, int w_, int cin, int cout, int k, int pad,
+                        int relu, void* stream) {
   std::string why;
   ConvGeom g{n, h, w_, cin, cout, k, pad};
   return set_status(conv_fwd_pool(g, x_pad, w, bias, y_pad, relu, pool_out, pool_pad,
-                                  static_cast<cudaStream_t>(stream), &why), why);
+                                  static_cast<cudaStream_t>(stream), &why, pool_idx), why);
+}
+
+int ralpb_maxpool_bwd_idx(const void* idx, const void* dy, int n, int oh, int ow, int c, int pad_out, int pad_in,
+                          void* dx, float* colsum, void* stream) {
+  return set_status(maxpool_bwd_idx(static_cast<const uint8_t*>(idx), static_cast<const __nv_bfloat16*>(dy), n, oh,
+                                    ow, c, pad_out, pad_in, static_cast<__nv_bfloat16*>(dx), colsum,
+                                    static_cast<cudaStream_t>(stream)),
+                    "maxpool_bwd_idx");
 }
 
 int ralpb_conv_dgrad(const void* dy_pad, const void* wd, const void* mask_pad, void* dx_pad, float* colsum,

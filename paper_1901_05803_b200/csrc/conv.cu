@@ -130,9 +130,10 @@ bool conv_fwd_pool_ok(const ConvGeom& g) {
 }
 
 cudaError_t conv_fwd_pool(const ConvGeom& g, const void* x_pad, const void* w, const float* bias, void* y_pad,
-                          int relu, void* pool_out, int pool_pad, cudaStream_t s, std::string* why) {
+                          int relu, void* pool_out, int pool_pad, cudaStream_t s, std::string* why, void* pool_idx) {
   if (!conv_fwd_pool_ok(g)) { *why = "conv_fwd_pool: shape not supported by the slab kernels"; return cudaErrorInvalidValue; }
-  return conv_slab_fwd(g, x_pad, w, g.cin, g.cout, bias, relu, nullptr, y_pad, nullptr, s, why, pool_out, pool_pad);
+  return conv_slab_fwd(g, x_pad, w, g.cin, g.cout, bias, relu, nullptr, y_pad, nullptr, s, why, pool_out, pool_pad,
+                       pool_idx);
 }
 
 cudaError_t conv_dgrad(const ConvGeom& g, const void* dy_pad, const void* wd, const void* mask_pad,

@@ -33,8 +33,11 @@ cudaError_t conv_fwd(const ConvGeom& g, const void* x_pad, const void* w, const 
 // ... and the 2x2/2 max pool of y written to pool_out ([n][h/2+2pp][w/2+2pp][cout], interior),
 // fused into the epilogue (slab kernels; returns an error where they do not apply).
 bool conv_fwd_pool_ok(const ConvGeom& g);
+// pool_idx (optional, [n][h/2][w/2][cout] uint8): window position of the first max (0..3 row-major),
+// 255 where the max is not > 0 -- everything maxpool_bwd_idx needs (no re-read of y).
 cudaError_t conv_fwd_pool(const ConvGeom& g, const void* x_pad, const void* w, const float* bias, void* y_pad,
-                          int relu, void* pool_out, int pool_pad, cudaStream_t s, std::string* why);
+                          int relu, void* pool_out, int pool_pad, cudaStream_t s, std::string* why,
+                          void* pool_idx = nullptr);
 // dx_pad = conv_transpose(dy_pad, w) * (mask_pad > 0 if mask_pad).
 // wd: [cin][k*k][cout] bf16, wd[ci][t][co] = w[co][k*k-1-t][ci].
 // colsum (optional): colsum[ci] += sum over pixels of the stored bf16 dx -- the bias gradient of
@@ -74,7 +77,7 @@ bool slab_fwd_ok(const ConvGeom& g, int c, int cout);
 bool slab_wgrad_ok(const ConvGeom& g);
 cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, int c, int cout, const float* bias,
                           int relu, const void* mask_pad, void* y_pad, float* colsum, cudaStream_t s,
-                          std::string* why, void* pool_out = nullptr, int pool_pad = 0);
+                          std::string* why, void* pool_out = nullptr, int pool_pad = 0, void* pool_idx = nullptr);
 cudaError_t conv_slab_wgrad(const ConvGeom& g, const void* x_pad, const void* dy_pad, float* dw, float* db,
                             cudaStream_t s, std::string* why);
 

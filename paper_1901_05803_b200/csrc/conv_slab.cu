@@ -90,7 +90,7 @@ bool slab_wgrad_ok(const ConvGeom& g) {
 
 cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, int c, int cout, const float* bias,
                           int relu, const void* mask_pad, void* y_pad, float* colsum, cudaStream_t s,
-                          std::string* why, void* pool_out, int pool_pad) {
+                          std::string* why, void* pool_out, int pool_pad, void* pool_idx) {
   if (pool_out != nullptr && (g.h % 2 != 0 || g.w % 2 != 0)) { *why = "fused pool needs even h, w"; return cudaErrorInvalidValue; }
   if (colsum != nullptr && cout > 512) { *why = "slab conv: fused colsum supports <= 512 channels"; return cudaErrorInvalidValue; }
   SlabConvParams p;
@@ -165,6 +165,7 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
   p.colsum = colsum;
   p.pool_out = static_cast<__nv_bfloat16*>(pool_out);
   p.pool_pad = pool_pad;
+  p.pool_idx = static_cast<uint8_t*>(pool_idx);
   if (const char* e = getenv("RALPB_DEBUG")) p.dbg = atoi(e);
   if (!encode_act(&p.tmX, x_pad, c, g.wp(), g.hp(), g.n, p.kb, p.sw, p.sh, p.row_bytes, why))
     return cudaErrorInvalidValue;

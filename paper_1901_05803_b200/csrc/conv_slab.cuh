@@ -62,6 +62,8 @@ struct alignas(64) SlabConvParams {
   float* colsum;        // optional: += per-channel sum over pixels of the stored (bf16) output
   __nv_bfloat16* pool_out;  // optional fused 2x2/2 max pool of the stored output: [n][h/2+2pp][w/2+2pp][cout]
   int pool_pad;
+  uint8_t* pool_idx;        // optional: per pooled element the window position of the first max
+                            // (0..3 row-major), 255 when the max is not > 0 (ReLU: no gradient)
   // wgrad
   float* dw;
   float* db;
@@ -327,15 +329,42 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
             // fused 2x2/2 max pool: a warp holds 4 image rows x 8 columns, so the window of an
             // (even row, even column) pixel is lanes {l, l^1, l^8, l^9}
             uint32_t mx[16];
+            uint32_t ix[16];  // argmax per channel pair: position in the low byte of each 16-bit half
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(&pk[j]);
-              uint32_t o = __shfl_xor_sync(0xffffffffu, pk[j], 1);
-              a2 = __hmax2(a2, *reinterpret_cast<const __nv_bfloat162*>(&o));
-              uint32_t t2 = *reinterpret_cast<uint32_t*>(&a2);
-              o = __shfl_xor_sync(0xffffffffu, t2, 8);
-              a2 = __hmax2(a2, *reinterpret_cast<const __nv_bfloat162*>(&o));
-              mx[j] = *reinterpret_cast<uint32_t*>(&a2);
+              const uint32_t o1 = __shfl_xor_sync(0xffffffffu, pk[j], 1);
+              const uint32_t o8 = __shfl_xor_sync(0xffffffffu, pk[j], 8);
+              const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&pk[j]);
+              const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&o1);
+              const __nv_bfloat162 c2 = *reinterpret_cast<const __nv_bfloat162*>(&o8);
+              if (p.pool_idx != nullptr) {
+                const uint32_t o9 = __shfl_xor_sync(0xffffffffu, pk[j], 9);
+                const __nv_bfloat162 d = *reinterpret_cast<const __nv_bfloat162*>(&o9);
+                const __nv_bfloat162 mm = __hmax2(__hmax2(a, b), __hmax2(c2, d));
+                mx[j] = *reinterpret_cast<const uint32_t*>(&mm);
+                // window positions (row-major): 0 = self, 1 = lane^1, 2 = lane^8, 3 = lane^9; first
+                // max wins; 255 when the max is not > 0.  16-bit-lane masks, no conversions.
+                const uint32_t ma = __heq2_mask(a, mm), mb = __heq2_mask(b, mm), mc = __heq2_mask(c2, mm);
+                const uint32_t gt = __hgt2_mask(mm, __float2bfloat162_rn(0.f));
+                const uint32_t B = mb & ~ma, C = mc & ~ma & ~mb, D = ~(ma | mb | mc);
+                ix[j] = ((B & 0x00010001u) | (C & 0x00020002u) | (D & 0x00030003u) | (~gt & 0x00FF00FFu));
+              } else {
+                __nv_bfloat162 t = __hmax2(a, b);
+                uint32_t tw = *reinterpret_cast<const uint32_t*>(&t);
+                const uint32_t o = __shfl_xor_sync(0xffffffffu, tw, 8);
+                t = __hmax2(t, *reinterpret_cast<const __nv_bfloat162*>(&o));
+                mx[j] = *reinterpret_cast<const uint32_t*>(&t);
+                (void)c2;
+              }
+            }
+            if ((m & 9) == 0 && valid && p.pool_idx != nullptr) {
+              const long long irow = (static_cast<long long>(img) * (p.h >> 1) + (hh >> 1)) * (p.w >> 1) + (ww >> 1);
+              uint4* ip = reinterpret_cast<uint4*>(p.pool_idx + irow * p.cout + n0);
+              uint32_t by[8];   // bytes of channels 4q..4q+3
+#pragma unroll
+              for (int q4 = 0; q4 < 8; ++q4) by[q4] = __byte_perm(ix[2 * q4], ix[2 * q4 + 1], 0x6420);
+              ip[0] = make_uint4(by[0], by[1], by[2], by[3]);
+              ip[1] = make_uint4(by[4], by[5], by[6], by[7]);
             }
             if ((m & 9) == 0 && valid) {
               const int ph = hh >> 1, pw = ww >> 1;

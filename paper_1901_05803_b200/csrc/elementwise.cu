@@ -321,6 +321,57 @@ __global__ void maxpool_bwd_disjoint_kernel(const __nv_bfloat16* __restrict__ x,
   if (colsum != nullptr) block_colsum_flush(csum, threadIdx.x % cv, c, s_col, colsum);
 }
 
+// 2x2/2 pool backward from the argmax bytes the fused conv+pool forward recorded
+// (conv_slab.cuh): reads 1 byte + 2 bytes per pooled element, writes the 4 input gradients --
+// the conv output itself is never read back.
+__global__ void maxpool_bwd_idx_kernel(const uint8_t* __restrict__ idx, const __nv_bfloat16* __restrict__ dy, int n,
+                                       int oh, int ow, int c, int po, int pi, __nv_bfloat16* __restrict__ dx,
+                                       float* __restrict__ colsum) {
+  __shared__ float s_col[kPoolColsumMax];
+  float csum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const int cv = c >> 3;
+  const long long total = static_cast<long long>(n) * oh * ow * cv;
+  const int hp = 2 * oh + 2 * pi, wp = 2 * ow + 2 * pi;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int cg = static_cast<int>(i % cv);
+    const long long pix = i / cv;
+    const int ox = static_cast<int>(pix % ow);
+    const long long t = pix / ow;
+    const int oy = static_cast<int>(t % oh);
+    const long long img = t / oh;
+    const uint2 iw = *reinterpret_cast<const uint2*>(idx + pix * c + cg * 8);
+    const uint4 dv = *reinterpret_cast<const uint4*>(dy + ((img * (oh + 2 * po) + oy + po) * (ow + 2 * po) + ox + po) * c + cg * 8);
+    const __nv_bfloat16* db = reinterpret_cast<const __nv_bfloat16*>(&dv);
+    const uint8_t* ib = reinterpret_cast<const uint8_t*>(&iw);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 out;
+      __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&out);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const bool hit = ib[e] == q;
+        ob[e] = hit ? db[e] : __float2bfloat16_rn(0.f);
+        if (hit) csum[e] += __bfloat162float(db[e]);
+      }
+      const long long o = ((img * hp + 2 * oy + (q >> 1) + pi) * wp + 2 * ox + (q & 1) + pi) * c + cg * 8;
+      *reinterpret_cast<uint4*>(dx + o) = out;
+    }
+  }
+  if (colsum != nullptr) block_colsum_flush(csum, threadIdx.x % cv, c, s_col, colsum);
+}
+
+cudaError_t maxpool_bwd_idx(const uint8_t* idx, const __nv_bfloat16* dy, int n, int oh, int ow, int c, int pad_out,
+                            int pad_in, __nv_bfloat16* dx, float* colsum, cudaStream_t s) {
+  if (c % 8 != 0 || (colsum != nullptr && (c > kPoolColsumMax || c / 8 > 256))) return cudaErrorInvalidValue;
+  const int threads = pool_threads(c);
+  const long long work = static_cast<long long>(n) * oh * ow * (c / 8);
+  const int grid = static_cast<int>(std::max<long long>(1, std::min((work + threads - 1) / threads,
+                                                                   static_cast<long long>(num_sms()) * 16)));
+  maxpool_bwd_idx_kernel<<<grid, threads, 0, s>>>(idx, dy, n, oh, ow, c, pad_out, pad_in, dx, colsum);
+  return cudaGetLastError();
+}
+
 cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* dy, int n, int h, int w,
                         int c, int pad_in, int k, int st, int pad_out, __nv_bfloat16* dx, float* colsum,
                         cudaStream_t s) {

@@ -26,6 +26,10 @@ cudaError_t maxpool_fwd(const __nv_bfloat16* x, int n, int h, int w, int c, int 
 // dx[i] = sum over windows containing i where i is the (first) argmax: dy[window],
 // then times (x[i] > 0) (the ReLU of the producing conv).  dx has x's padded layout,
 // border written as zero.  colsum (optional, c <= 1024): colsum[ch] += sum of the stored dx
+// maxpool_bwd_idx: the same for a 2x2/2 pool from the argmax bytes of the fused conv+pool
+// forward (idx [n][oh][ow][c], 255 = no gradient); dy [n][oh+2po][ow+2po][c], dx interior.
+cudaError_t maxpool_bwd_idx(const uint8_t* idx, const __nv_bfloat16* dy, int n, int oh, int ow, int c, int pad_out,
+                            int pad_in, __nv_bfloat16* dx, float* colsum, cudaStream_t s);
 // (the producing conv's bias gradient).
 cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* dy, int n, int h, int w,
                         int c, int pad_in, int k, int st, int pad_out, __nv_bfloat16* dx, float* colsum,

@@ -33,6 +33,11 @@ namespace ralpb {
 
 namespace {
 
+bool fuse_pool_enabled() {
+  const char* e = getenv("RALPB_FUSE_POOL");
+  return e == nullptr || e[0] != '0';
+}
+
 constexpr int kFlagAct = 0;       // [8]  PS: worker r's cut landed
 constexpr int kFlagActGrad = 8;   // [1]  worker: act-grad landed
 constexpr int kFlagGrad = 16;     // [8]  rank r finished its backward
@@ -244,6 +249,23 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     if (i > 0 && i + 1 < m->acts.size()) {
       if (!(m->gacts[i] = alloc<bf16>(m, m->acts[i].elems(), why))) return fail(*why);
       cudaMemset(m->gacts[i], 0, bytes);
+    }
+  }
+  // 2x2/2 pools fused into the preceding conv's epilogue.  With RALPB_POOL_IDX=1 those after a
+  // conv with cin >= 128 also record argmax bytes so their backward does not re-read the conv
+  // output; measured: the backward saves what the forward epilogue loses (-0.22 / +0.28 ms per
+  // VGG-16 step), so it is off by default
+  for (size_t i = 0; i + 1 < m->front.size(); ++i) {
+    FrontLayer& c = m->front[i];
+    FrontLayer& pl = m->front[i + 1];
+    if (c.kind == RALPB_CONV && !c.im2col && pl.kind == RALPB_POOL && pl.k == 2 && pl.stride == 2 &&
+        conv_fwd_pool_ok(c.g) && fuse_pool_enabled()) {
+      pl.fused_fwd = true;
+      const ActBuf& po = m->acts[i + 2];
+      const char* ie = getenv("RALPB_POOL_IDX");
+      if (ie != nullptr && ie[0] == '1' && c.g.cin >= 128 &&
+          !(pl.idx = alloc<uint8_t>(m, static_cast<size_t>(po.n) * po.h * po.w * po.c, why)))
+        return fail(*why);
     }
   }
   for (auto& f : m->front) {
@@ -558,8 +580,11 @@ int launch_front_backward(Model* m, const bf16* dcut, std::string* why) {
                          : nullptr;
     if (f.kind == RALPB_POOL) {
       bf16* dst = m->gacts[i];
-      RALPB_TRY(maxpool_bwd(in.ptr, cur, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.pad, dst, prev_db,
-                            m->stream));
+      if (f.idx != nullptr)
+        RALPB_TRY(maxpool_bwd_idx(f.idx, cur, in.n, out.h, out.w, in.c, out.pad, in.pad, dst, prev_db, m->stream));
+      else
+        RALPB_TRY(maxpool_bwd(in.ptr, cur, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.pad, dst, prev_db,
+                              m->stream));
       ++m->launches;
       cur = dst;
       db_done = prev_db != nullptr;
@@ -661,11 +686,6 @@ cudaError_t mark(Model* m, int i, bool capturing) {
 
 // Everything of one step after the inputs are resident in HBM: bump the device step
 // counter, front forward, cut exchange, back segment, front backward, sync, re-layout.
-bool fuse_pool_enabled() {
-  const char* e = getenv("RALPB_FUSE_POOL");
-  return e == nullptr || e[0] != '0';
-}
-
 int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu, bool capturing,
               std::string* why) {
   const uint32_t* seq = m->seq_dev;
@@ -713,13 +733,12 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
       RALPB_TRY(gemm_launch(d, s, why));
     } else if (f.kind == RALPB_CONV) {
       // a following 2x2/2 max pool is fused into the conv epilogue (RALPB_FUSE_POOL=0: separate)
-      const bool pool_next = i + 1 < m->front.size() && m->front[i + 1].kind == RALPB_POOL &&
-                             m->front[i + 1].k == 2 && m->front[i + 1].stride == 2 && conv_fwd_pool_ok(f.g) &&
-                             fuse_pool_enabled();
+      const bool pool_next = i + 1 < m->front.size() && m->front[i + 1].fused_fwd;
       if (pool_next) {
         const ActBuf& pooled = m->acts[i + 2];
         bf16* pdst = i + 2 == m->front.size() ? cut_dst : pooled.ptr;
-        RALPB_TRY(conv_fwd_pool(f.g, in.ptr, f.wf, m->P + f.b_off, out.ptr, 1, pdst, pooled.pad, s, why));
+        RALPB_TRY(conv_fwd_pool(f.g, in.ptr, f.wf, m->P + f.b_off, out.ptr, 1, pdst, pooled.pad, s, why,
+                                m->front[i + 1].idx));
         ++m->launches;
         ++i;  // the pool layer is done
         continue;

@@ -34,6 +34,8 @@ struct FrontLayer {
   int kpad = 0;                // im2col row width (k*k*cin + 1 bias column, padded)
   bool fused = false;          // im2col layer run by the fused first-conv kernels (conv_first.cu):
                                // patches built on chip from the fp32 image, acts[0] unused
+  bool fused_fwd = false;      // pool computed in the preceding conv's epilogue
+  uint8_t* idx = nullptr;      // ... with argmax bytes [n][oh][ow][c] for its backward
 };
 
 struct FcLayer {

@@ -50,12 +50,21 @@ def conv_fwd(x_pad, w, bias, *, n, h, w_, cin, cout, k, pad, relu=True, out=None
 
 
 def conv_fwd_pool(x_pad, w, bias, *, n, h, w_, cin, cout, k, pad, relu=True, pool_pad=1):
-    """(y, pooled): conv fwd and its 2x2/2 max pool from one kernel."""
+    """(y, pooled, argmax bytes): conv fwd and its 2x2/2 max pool from one kernel."""
     y = torch.zeros(n, h + 2 * pad, w_ + 2 * pad, cout, dtype=_BF16, device=x_pad.device)
     pooled = torch.zeros(n, h // 2 + 2 * pool_pad, w_ // 2 + 2 * pool_pad, cout, dtype=_BF16, device=x_pad.device)
+    idx = torch.empty(n, h // 2, w_ // 2, cout, dtype=torch.uint8, device=x_pad.device)
     call("ralpb_conv_fwd_pool", x_pad.data_ptr(), w.data_ptr(), _p(bias), y.data_ptr(), pooled.data_ptr(), pool_pad,
-         n, h, w_, cin, cout, k, pad, int(relu), _stream())
-    return y, pooled
+         idx.data_ptr(), n, h, w_, cin, cout, k, pad, int(relu), _stream())
+    return y, pooled, idx
+
+
+def maxpool_bwd_idx(idx, dy, *, pad_out, pad_in, colsum=None):
+    n, oh, ow, c = idx.shape
+    dx = torch.zeros(n, 2 * oh + 2 * pad_in, 2 * ow + 2 * pad_in, c, dtype=_BF16, device=dy.device)
+    call("ralpb_maxpool_bwd_idx", idx.data_ptr(), dy.data_ptr(), n, oh, ow, c, pad_out, pad_in, dx.data_ptr(),
+         _p(colsum), _stream())
+    return dx
 
 
 def conv_first_fwd(img, wf, *, pad_out=1):

@@ -278,7 +278,7 @@ def test_conv_fwd_fused_pool(case):
     x = _pad(_bf(n, h, w, cin, gen=g), pad).contiguous()
     wt = _bf(cout, k * k, cin, scale=(2.0 / (k * k * cin)) ** 0.5, gen=g)
     bias = torch.randn(cout, device=DEV) * 0.1
-    y, pooled = ops.conv_fwd_pool(x, wt, bias, n=n, h=h, w_=w, cin=cin, cout=cout, k=k, pad=pad, pool_pad=1)
+    y, pooled, idx = ops.conv_fwd_pool(x, wt, bias, n=n, h=h, w_=w, cin=cin, cout=cout, k=k, pad=pad, pool_pad=1)
     y_ref = ops.conv_fwd(x, wt, bias, n=n, h=h, w_=w, cin=cin, cout=cout, k=k, pad=pad, relu=True)
     torch.testing.assert_close(y.float(), y_ref.float(), rtol=0, atol=0)
     yi = y[:, pad:pad + h, pad:pad + w, :].permute(0, 3, 1, 2).float()
@@ -287,3 +287,10 @@ def test_conv_fwd_fused_pool(case):
     border = pooled.clone()
     border[:, 1:-1, 1:-1, :] = 0
     assert border.abs().max().item() == 0.0
+    # backward from the argmax bytes == the reference pool backward (first max, ReLU mask)
+    dy = _bf(n, h // 2, w // 2, cout, gen=g).contiguous()
+    colsum = torch.zeros(cout, device=DEV)
+    dx = ops.maxpool_bwd_idx(idx, dy, pad_out=0, pad_in=pad, colsum=colsum)
+    ref_dx = ops.maxpool_bwd(y, dy, n=n, h=h, w=w, c=cout, pad_in=pad, k=2, stride=2, pad_out=0)
+    torch.testing.assert_close(dx.float(), ref_dx.float(), rtol=0, atol=0)
+    torch.testing.assert_close(colsum, dx.float().sum(dim=(0, 1, 2)), rtol=1e-5, atol=1e-4)
