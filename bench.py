@@ -65,20 +65,43 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        import threading
+        self.lines, self._all, self._t0 = [], [], None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except FileNotFoundError:
             self.proc = None
+            return self
+        first = threading.Event()
+
+        def reader():
+            for line in self.proc.stdout:
+                if line.strip():
+                    self._all.append((time.perf_counter(), line))
+                    first.set()
+        self._thread = threading.Thread(target=reader, daemon=True)
+        self._thread.start()
+        first.wait(timeout=10.0)  # sampling is live before the timed region starts
+        self._t0 = time.perf_counter()
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
         if self.proc is not None:
+            t1 = time.perf_counter()
+            # at least one sample after the region (nvidia-smi samples every 100 ms)
+            deadline = t1 + 1.0
+            while time.perf_counter() < deadline and not any(t >= t1 for t, _ in self._all):
+                time.sleep(0.02)
             self.proc.terminate()
-            out, _ = self.proc.communicate(timeout=10)
-            self.lines = [l for l in out.splitlines() if l.strip()]
+            try:
+                self.proc.wait(timeout=10)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            # samples from just before the region to just after it
+            lo = max((t for t, _ in self._all if t <= self._t0), default=self._t0)
+            self.lines = [l for t, l in self._all if lo <= t <= deadline]
 
     def summary(self):
         sm, smax, reasons = [], None, set()

@@ -579,27 +579,67 @@ cudaError_t colsum_bf16(const __nv_bfloat16* dy, long long rows, int c, long lon
 }
 
 // ------------------------------------------------------------------ weight re-layouts
-__global__ void conv_weight_prep_kernel(const float* __restrict__ w, int co, int taps, int ci,
-                                        __nv_bfloat16* __restrict__ wf,
-                                        __nv_bfloat16* __restrict__ wd) {
-  const long long total = static_cast<long long>(co) * taps * ci;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    int c_in = static_cast<int>(i % ci);
-    long long t2 = i / ci;
-    int t = static_cast<int>(t2 % taps);
-    int c_out = static_cast<int>(t2 / taps);
-    __nv_bfloat16 b = __float2bfloat16_rn(w[i]);
-    wf[i] = b;
-    if (wd != nullptr) wd[(static_cast<long long>(c_in) * taps + (taps - 1 - t)) * co + c_out] = b;
+// All conv layers' filter copies in one launch: every block transposes 32 (co) x 32 (ci) of one tap
+// through shared memory, so both the forward copy wf [co][t][ci] and the tap-reversed transpose
+// wd [ci][taps-1-t][co] are written with coalesced rows.
+__global__ void __launch_bounds__(256) conv_weight_prep_kernel(const __grid_constant__ WeightPrepBatch b) {
+  __shared__ float tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (long long blk = blockIdx.x; blk < b.total_blocks; blk += gridDim.x) {
+    int k = 0;
+    while (k + 1 < b.n && blk >= b.job[k + 1].block0) ++k;
+    const WeightPrepJob& J = b.job[k];
+    long long r = blk - J.block0;
+    const int tci = static_cast<int>(r % J.tiles_ci);
+    r /= J.tiles_ci;
+    const int tco = static_cast<int>(r % J.tiles_co);
+    const int t = static_cast<int>(r / J.tiles_co);
+    const int co0 = tco * 32, ci0 = tci * 32;
+    for (int yy = ty; yy < 32; yy += 8) {
+      const int co = co0 + yy, ci = ci0 + tx;
+      if (co < J.co && ci < J.ci) {
+        const long long i = (static_cast<long long>(co) * J.taps + t) * J.ci + ci;
+        const float v = J.w[i];
+        J.wf[i] = __float2bfloat16_rn(v);
+        tile[yy][tx] = v;
+      }
+    }
+    __syncthreads();
+    if (J.wd != nullptr) {
+      for (int yy = ty; yy < 32; yy += 8) {
+        const int ci = ci0 + yy, co = co0 + tx;
+        if (co < J.co && ci < J.ci)
+          J.wd[(static_cast<long long>(ci) * J.taps + (J.taps - 1 - t)) * J.co + co] = __float2bfloat16_rn(tile[tx][yy]);
+      }
+    }
+    __syncthreads();
   }
+}
+
+cudaError_t conv_weight_prep_batch(const WeightPrepJob* jobs, int n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (n > kMaxPrepJobs) return cudaErrorInvalidValue;
+  WeightPrepBatch b;
+  b.n = n;
+  long long blocks = 0;
+  for (int i = 0; i < n; ++i) {
+    b.job[i] = jobs[i];
+    b.job[i].tiles_co = (jobs[i].co + 31) / 32;
+    b.job[i].tiles_ci = (jobs[i].ci + 31) / 32;
+    b.job[i].block0 = blocks;
+    blocks += static_cast<long long>(b.job[i].tiles_co) * b.job[i].tiles_ci * jobs[i].taps;
+  }
+  b.total_blocks = blocks;
+  const int grid = static_cast<int>(std::min<long long>(blocks, static_cast<long long>(num_sms()) * 8));
+  conv_weight_prep_kernel<<<grid, 256, 0, s>>>(b);
+  return cudaGetLastError();
 }
 
 cudaError_t conv_weight_prep(const float* w, int co, int taps, int ci, __nv_bfloat16* wf,
                              __nv_bfloat16* wd, cudaStream_t s) {
-  long long total = static_cast<long long>(co) * taps * ci;
-  conv_weight_prep_kernel<<<grid_for(total, 256), 256, 0, s>>>(w, co, taps, ci, wf, wd);
-  return cudaGetLastError();
+  WeightPrepJob j{};
+  j.w = w; j.wf = wf; j.wd = wd; j.co = co; j.taps = taps; j.ci = ci;
+  return conv_weight_prep_batch(&j, 1, s);
 }
 
 __global__ void cast_kernel(const float* __restrict__ x, long long n, __nv_bfloat16* __restrict__ y) {

@@ -57,6 +57,22 @@ cudaError_t colsum_bf16(const __nv_bfloat16* dy, long long rows, int c, long lon
 
 // Conv weights fp32 [co][t][ci] -> bf16 forward copy [co][t][ci] and bf16
 // backward-data copy [ci][taps-1-t][co].  wd may be null.
+struct WeightPrepJob {
+  const float* w;
+  __nv_bfloat16* wf;
+  __nv_bfloat16* wd;     // may be null
+  int co, taps, ci;
+  int tiles_co, tiles_ci;   // filled by conv_weight_prep_batch
+  long long block0;
+};
+constexpr int kMaxPrepJobs = 24;
+struct WeightPrepBatch {
+  WeightPrepJob job[kMaxPrepJobs];
+  int n;
+  long long total_blocks;
+};
+// conv_weight_prep for several layers in one launch.
+cudaError_t conv_weight_prep_batch(const WeightPrepJob* jobs, int n, cudaStream_t s);
 cudaError_t conv_weight_prep(const float* w, int co, int taps, int ci, __nv_bfloat16* wf,
                              __nv_bfloat16* wd, cudaStream_t s);
 // out = act(acc + bias) [* (mask > 0)] -> bf16 (out_bf16) and/or fp32 (out_f32); finishes a

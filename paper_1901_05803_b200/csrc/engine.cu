@@ -620,13 +620,28 @@ int launch_front_backward(Model* m, const bf16* dcut, std::string* why) {
 }
 
 int relayout_weights(Model* m, bool fc_too, std::string* why) {
+  WeightPrepJob jobs[kMaxPrepJobs];
+  int nj = 0;
   for (size_t i = 0; i < m->front.size(); ++i) {
     FrontLayer& f = m->front[i];
     if (f.kind != RALPB_CONV) continue;
-    if (f.im2col)
+    if (f.im2col) {
       RALPB_TRY(cast_bf16(m->P + f.w_off, f.w_count, f.wf, m->stream));
-    else
-      RALPB_TRY(conv_weight_prep(m->P + f.w_off, f.g.cout, f.g.taps(), f.g.cin, f.wf, i > 0 ? f.wd : nullptr, m->stream));
+      ++m->launches;
+      continue;
+    }
+    if (nj == kMaxPrepJobs) {
+      RALPB_TRY(conv_weight_prep_batch(jobs, nj, m->stream));
+      ++m->launches;
+      nj = 0;
+    }
+    WeightPrepJob& j = jobs[nj++];
+    j = WeightPrepJob{};
+    j.w = m->P + f.w_off; j.wf = f.wf; j.wd = i > 0 ? f.wd : nullptr;
+    j.co = f.g.cout; j.taps = f.g.taps(); j.ci = f.g.cin;
+  }
+  if (nj > 0) {
+    RALPB_TRY(conv_weight_prep_batch(jobs, nj, m->stream));
     ++m->launches;
   }
   if (fc_too) {
