@@ -132,7 +132,9 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
     if (p.nb >= 2 || p.macc == 1) break;
     p.macc /= 2;
   }
-  p.acc_bufs = p.macc * p.bn <= 256 ? 2 : 1;
+  // as many TMEM accumulator buffers (<= 4) as fit: the MMA runs ahead of the epilogue
+  p.acc_bufs = std::max(1, std::min(4, 512 / (p.macc * p.bn)));
+  if (const char* ae = getenv("RALPB_ACC_BUFS")) p.acc_bufs = std::max(1, std::min(p.acc_bufs, atoi(ae)));
   const int used = p.macc * p.bn * p.acc_bufs;
   p.tmem_cols = used <= 32 ? 32 : used <= 64 ? 64 : used <= 128 ? 128 : used <= 256 ? 256 : 512;
   // Filters resident in shared memory when one channel block and one N tile cover the layer
@@ -149,8 +151,10 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
       p.slab_stage = slab2;
       p.na = na2;
       p.nb = g.taps();
-      p.acc_bufs = 2;
-      p.tmem_cols = p.macc * p.bn * 2 <= 256 ? 256 : 512;
+      p.acc_bufs = std::max(1, std::min(4, 512 / (p.macc * p.bn)));
+      if (const char* ae = getenv("RALPB_ACC_BUFS")) p.acc_bufs = std::max(1, std::min(p.acc_bufs, atoi(ae)));
+      const int used2 = p.macc * p.bn * p.acc_bufs;
+      p.tmem_cols = used2 <= 256 ? 256 : 512;
     }
   }
   if (p.nb < 2) { *why = "slab conv: tile does not fit in shared memory"; return cudaErrorInvalidValue; }

@@ -99,8 +99,8 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
   uint64_t* b_full = a_empty + p.na;
   uint64_t* b_empty = b_full + p.nb;
   uint64_t* tfull = b_empty + p.nb;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + 4;   // up to 4 TMEM accumulator buffers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
   float* s_col = reinterpret_cast<float*>(tmem_slot + 4);  // [cout] when p.colsum
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
     tma_prefetch(&p.tmB);
     for (int i = 0; i < p.na; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
     for (int i = 0; i < p.nb; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128 * EWG * NCTA); }
+    for (int i = 0; i < 4; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128 * EWG * NCTA); }
     fence_barrier_init();
   }
   uint32_t rank = 0;
