@@ -226,6 +226,7 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1901_05803_b200._lib import TENSOR_KINDS
     from paper_1901_05803_b200.planner import compute_load, volume_ralp
 
     ex, job, rep = _build_executor("ralp", world, rank)
@@ -257,16 +258,46 @@ def run_ours(args):
     worker_flops, ps_flops = compute_load(m, rep.split_index, world)
     flops_rank = worker_flops + (ps_flops if rank == 0 else 0)
     peaks, peak_src = _peaks()
-    by_kind = {}
+    by_kind, xchg = {}, {}
     for kind, lms, lfl in launches:
-        k = by_kind.setdefault(kind, {"launches": 0, "ms": 0.0, "flops": 0.0})
+        dst = by_kind if kind in TENSOR_KINDS else xchg
+        k = dst.setdefault(kind, {"launches": 0, "ms": 0.0, "flops": 0.0})
         k["launches"] += 1
         k["ms"] += lms
         k["flops"] += lfl
     traffic_doc = {}
-    tfile = ROOT / "profiles" / "gemm_traffic.json"
+    tfile = ROOT / "profiles" / f"traffic_{MODEL}.json"
     if tfile.exists():
         traffic_doc = json.loads(tfile.read_text())
+    # NVLink: the hand-written exchange kernels' bytes / time, and NCCL all-reduce of the same
+    # front-parameter vector as the comparison baseline (north star)
+    nvlink = None
+    if world > 1:
+        import torch.distributed as dist
+        link = peaks.get("nvlink_gbs_per_direction", 770.0)
+        nvlink = {"peak_gbs": link, "peak_source": "B200_PROFILING.md measured peer copy per direction"}
+        for kind, k in xchg.items():
+            gbs = k["flops"] / (k["ms"] * 1e-3) / 1e9 if k["ms"] > 0 else None
+            nvlink[kind] = {"launches": k["launches"], "ms": k["ms"], "bytes": k["flops"], "gbs": gbs,
+                            "frac": gbs / link if gbs else None}
+        p_front = m.cumulative_param_bytes(rep.split_index) // m.bytes_per_element
+        buf = torch.zeros(p_front, dtype=torch.float32, device="cuda")
+        for _ in range(3):
+            dist.all_reduce(buf)
+        torch.cuda.synchronize()
+        dist.barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(10):
+            dist.all_reduce(buf)
+        s1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([s0.elapsed_time(s1) / 10], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        nvlink["nccl_allreduce_front_params"] = {"ms": t.item(), "floats": p_front,
+                                                 "note": "torch.distributed NCCL all_reduce of the front parameter "
+                                                         "vector (what the sharded-PS RS+SGD+AG kernel replaces)"}
+        del buf
     for kind, k in by_kind.items():
         k["tflops"] = k["flops"] / (k["ms"] * 1e-3) / 1e12 if k["ms"] > 0 else None
         k["frac"] = k["tflops"] / peaks["bf16_tflops_sustained"] if k["tflops"] else None
@@ -315,11 +346,12 @@ def run_ours(args):
                          "flops_per_launch": dom["flops"] / dom["launches"] if dom else None,
                          "method": "algorithmic FLOPs of each launch (2*pixels*taps*Cin*Cout, 2*M*N*K) / its CUDA-event "
                                    "duration in a profiling pass on the launching stream; traffic = ncu "
-                                   "dram__bytes_read+write per launch of the same kernel (profiles/gemm_traffic.json)",
+                                   "dram__bytes_read+write per launch of the same kernel (profiles/traffic_vgg16.json)",
                          "by_kind": {kk: {"launches": v["launches"], "ms": round(v["ms"], 4),
                                           "tflops": round(v["tflops"], 1) if v["tflops"] else None,
                                           "frac": round(v["frac"], 3) if v["frac"] else None}
                                      for kk, v in sorted(by_kind.items(), key=lambda kv: -kv[1]["ms"])},
+                         "nvlink": nvlink,
                          "step": {"achieved": step_achieved,
                                   "frac": step_achieved / peaks["bf16_tflops_sustained"] if step_achieved else None,
                                   "flops": flops_rank, "tensor_ms": step_ms,

@@ -179,7 +179,8 @@ long long ralpb_model_debug_buffer(ralpb_model* m, int i, int which, void* host_
 int ralpb_model_set_profiling(ralpb_model* m, int on);
 /* Per-launch records of the last profiled step: kind = 0 conv fwd/dgrad (single CTA), 1 conv
  * fwd/dgrad (CTA pair), 2 conv wgrad (CTA pair), 3 conv wgrad (single CTA), 4 first-conv fwd,
- * 5 first-conv wgrad, 6 GEMM; ms = CUDA-event duration; flops = algorithmic FLOPs.  Returns the
+ * 5 first-conv wgrad, 6 GEMM, 7 peer push (cut gather / act-grad scatter), 8 sharded-PS update;
+ * ms = CUDA-event duration; flops = algorithmic FLOPs (7, 8: bytes moved over NVLink).  Returns the
  * number of records (writes at most cap) or -1. */
 typedef struct {
   int kind;

@@ -72,7 +72,8 @@ class LaunchRec(C.Structure):
 
 
 LAUNCH_KINDS = ["conv_fwd", "conv_fwd_pair", "conv_wgrad_pair", "conv_wgrad", "first_conv_fwd", "first_conv_wgrad",
-                "gemm"]
+                "gemm", "push", "shard_update"]
+TENSOR_KINDS = LAUNCH_KINDS[:7]
 
 
 class StepStats(C.Structure):

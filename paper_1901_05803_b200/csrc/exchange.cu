@@ -48,8 +48,10 @@ __global__ void push_kernel(uint4* __restrict__ dst, const uint4* __restrict__ s
 cudaError_t push_and_signal(void* dst, const void* src, long long n16, const PeerSignal& sig,
                             const uint32_t* value, uint32_t* counter, cudaStream_t s) {
   int grid = static_cast<int>(std::max<long long>(1, std::min<long long>((n16 + 511) / 512, num_sms() * 2)));
-  push_kernel<<<grid, 512, 0, s>>>(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), n16,
-                                   sig, value, counter);
+  launch_timed([&] {
+    push_kernel<<<grid, 512, 0, s>>>(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), n16, sig,
+                                     value, counter);
+  }, s, KIND_PUSH, 16.0 * n16);
   return cudaGetLastError();
 }
 
@@ -111,7 +113,10 @@ cudaError_t shard_update(const ShardUpdate& u, const PeerSignal& done, const uin
                          uint32_t* counter, cudaStream_t s) {
   long long n4 = (u.end - u.begin) / 4;
   int grid = static_cast<int>(std::max<long long>(1, std::min<long long>((n4 + 255) / 256, num_sms() * 4)));
-  shard_update_kernel<<<grid, 256, 0, s>>>(u, done, value, counter);
+  // NVLink bytes of this rank: peer shard reads of the gradient + peer parameter writes
+  const double peer_bytes = 2.0 * (u.nranks - 1) * static_cast<double>(u.end - u.begin) * sizeof(float);
+  launch_timed([&] { shard_update_kernel<<<grid, 256, 0, s>>>(u, done, value, counter); }, s, KIND_SHARD_UPDATE,
+               peer_bytes);
   return cudaGetLastError();
 }
 

@@ -57,6 +57,8 @@ enum LaunchKind {
   KIND_FIRST_FWD = 4,     // conv_first_fwd_kernel
   KIND_FIRST_WGRAD = 5,   // conv_first_wgrad_kernel
   KIND_GEMM = 6,          // gemm_sm100_kernel
+  KIND_PUSH = 7,          // push_kernel (cut gather / act-grad scatter); "flops" = bytes moved
+  KIND_SHARD_UPDATE = 8,  // shard_update_kernel (sharded-PS RS + SGD + AG); "flops" = NVLink bytes
 };
 
 struct GemmTimer {
