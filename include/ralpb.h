@@ -94,6 +94,13 @@ int ralpb_pack_im2col(const float* x, int n, int h, int w, int c, int k, int str
 /* Max pool (infer_pool, layers.py:106-114; stride defaults to window). */
 int ralpb_maxpool_fwd(const void* x, int n, int h, int w, int c, int pad_in, int k, int stride,
                       void* y, int pad_out, void* stream);
+/* Pool forward that also records, per output element, the window position (ky*k+kx) of the first
+ * max (255 where it is not > 0), and the backward that gathers from those bytes -- any window and
+ * stride, e.g. AlexNet's overlapping 3/2 pools (the input is not re-read). */
+int ralpb_maxpool_fwd_idx(const void* x, int n, int h, int w, int c, int pad_in, int k, int stride, void* y,
+                          int pad_out, void* idx, void* stream);
+int ralpb_maxpool_bwd_gather(const void* idx, const void* dy, int n, int h, int w, int c, int pad_in, int k,
+                             int stride, int pad_out, void* dx, float* colsum, void* stream);
 /* colsum (may be NULL, c <= 1024): colsum[ch] += sum of the stored dx (bias gradient of the conv
  * feeding the pool, fused into the pool backward). */
 int ralpb_maxpool_bwd(const void* x, const void* dy, int n, int h, int w, int c, int pad_in, int k,

@@ -32,6 +32,8 @@ SIGNATURES: dict[str, tuple] = {
     "ralpb_conv_first_wgrad": (c_i, [c_vp, c_i, c_i, c_i, c_vp, c_i, c_vp, c_vp]),
     "ralpb_conv_fwd_pool": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i,
                                   c_vp]),
+    "ralpb_maxpool_fwd_idx": (c_i, [c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp, c_i, c_vp, c_vp]),
+    "ralpb_maxpool_bwd_gather": (c_i, [c_vp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp, c_vp, c_vp]),
     "ralpb_maxpool_bwd_idx": (c_i, [c_vp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_vp, c_vp, c_vp]),
     "ralpb_conv_dgrad": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),
     "ralpb_conv_wgrad": (c_i, [c_vp, c_vp, c_fp, c_fp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_vp]),

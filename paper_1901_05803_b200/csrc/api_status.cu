@@ -30,6 +30,18 @@ int ralpb_maxpool_fwd(const void* x, int n, int h, int w, int c, int pad_in, int
   return set_status(maxpool_fwd(RALPB_CBF(x), n, h, w, c, pad_in, k, stride, RALPB_BF(y), pad_out,
                                 RALPB_S(stream)), "maxpool_fwd");
 }
+int ralpb_maxpool_fwd_idx(const void* x, int n, int h, int w, int c, int pad_in, int k, int stride, void* y,
+                          int pad_out, void* idx, void* stream) {
+  return set_status(maxpool_fwd(RALPB_CBF(x), n, h, w, c, pad_in, k, stride, RALPB_BF(y), pad_out, RALPB_S(stream),
+                                static_cast<uint8_t*>(idx)),
+                    "maxpool_fwd_idx");
+}
+int ralpb_maxpool_bwd_gather(const void* idx, const void* dy, int n, int h, int w, int c, int pad_in, int k,
+                             int stride, int pad_out, void* dx, float* colsum, void* stream) {
+  return set_status(maxpool_bwd_gather(static_cast<const uint8_t*>(idx), RALPB_CBF(dy), n, h, w, c, pad_in, k, stride,
+                                       pad_out, RALPB_BF(dx), colsum, RALPB_S(stream)),
+                    "maxpool_bwd_gather");
+}
 int ralpb_maxpool_bwd(const void* x, const void* dy, int n, int h, int w, int c, int pad_in, int k,
                       int stride, int pad_out, void* dx, float* colsum, void* stream) {
   return set_status(maxpool_bwd(RALPB_CBF(x), RALPB_CBF(dy), n, h, w, c, pad_in, k, stride, pad_out,

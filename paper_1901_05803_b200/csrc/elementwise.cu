@@ -111,8 +111,61 @@ __global__ void pack_im2col_row_kernel(const float* __restrict__ x, int n, int h
   }
 }
 
+// Large first-layer filters (AlexNet's 11x11x3 -> 363 (+bias) columns, kpad 384): one warp per
+// patch row, lane l owns columns [l*KPAD/32, (l+1)*KPAD/32) -- all index arithmetic is by
+// compile-time constants and each lane writes KPAD/32 contiguous bf16 (8-byte stores).
+template <int K, int C, int KPAD>
+__global__ void __launch_bounds__(256) pack_im2col_warp_kernel(const float* __restrict__ x, int n, int h, int w, int st,
+                                                               int p, int ho, int wo, int po,
+                                                               __nv_bfloat16* __restrict__ out) {
+  constexpr int PER = KPAD / 32, KK = K * K * C;
+  static_assert(PER % 4 == 0, "lane span must be a multiple of 4 columns");
+  const int hop = ho + 2 * po, wop = wo + 2 * po;
+  const long long rows = static_cast<long long>(n) * hop * wop;
+  const int lane = threadIdx.x & 31;
+  const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  for (long long row = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += warps) {
+    const long long img = row / (static_cast<long long>(hop) * wop);
+    const int rem = static_cast<int>(row - img * hop * wop);
+    const int oy = rem / wop - po, ox = rem % wop - po;
+    const bool interior = oy >= 0 && oy < ho && ox >= 0 && ox < wo;
+    const float* base = x + img * h * w * C;
+    uint32_t pk[PER / 2];
+#pragma unroll
+    for (int e2 = 0; e2 < PER / 2; ++e2) {
+      float v[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int j = lane * PER + 2 * e2 + q;
+        float val = 0.f;
+        if (interior) {
+          if (j < KK) {
+            const int ch = j % C, tap = j / C;
+            const int iy = oy * st + tap / K - p, ix = ox * st + tap % K - p;
+            if (iy >= 0 && iy < h && ix >= 0 && ix < w) val = __ldg(base + (static_cast<long long>(iy) * w + ix) * C + ch);
+          } else if (j == KK) {
+            val = 1.f;
+          }
+        }
+        v[q] = val;
+      }
+      pk[e2] = pack_bf16(v[0], v[1]);
+    }
+    uint2* dst = reinterpret_cast<uint2*>(out + row * KPAD + lane * PER);
+#pragma unroll
+    for (int e4 = 0; e4 < PER / 4; ++e4) dst[e4] = make_uint2(pk[2 * e4], pk[2 * e4 + 1]);
+  }
+}
+
 cudaError_t pack_im2col(const float* x, int n, int h, int w, int c, int k, int st, int p, int ho, int wo,
                         int po, int kpad, __nv_bfloat16* out, cudaStream_t s) {
+  if (k == 11 && c == 3 && kpad == 384) {
+    const long long rows = static_cast<long long>(n) * (ho + 2 * po) * (wo + 2 * po);
+    const int grid = static_cast<int>(std::min<long long>((rows + 7) / 8, static_cast<long long>(num_sms()) * 32));
+    pack_im2col_warp_kernel<11, 3, 384><<<grid, 256, 0, s>>>(x, n, h, w, st, p, ho, wo, po, out);
+    return cudaGetLastError();
+  }
   if (kpad % 8 != 0 || kpad < k * k * c + 1) return cudaErrorInvalidValue;
   const long long rows = static_cast<long long>(n) * (ho + 2 * po) * (wo + 2 * po);
   if (k == 3 && c == 3 && kpad == 32 && rows < (1LL << 31)) {
@@ -128,7 +181,7 @@ cudaError_t pack_im2col(const float* x, int n, int h, int w, int c, int k, int s
 // One thread = one output position x 8 channels.
 __global__ void maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, int n, int h, int w, int c,
                                    int pi, int k, int st, __nv_bfloat16* __restrict__ y, int po,
-                                   int oh, int ow) {
+                                   int oh, int ow, uint8_t* __restrict__ idx) {
   const int ohp = oh + 2 * po, owp = ow + 2 * po;
   const int hp = h + 2 * pi, wp = w + 2 * pi;
   const int cv = c / 8;
@@ -144,31 +197,43 @@ __global__ void maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, int n, i
     uint4 res = make_uint4(0, 0, 0, 0);
     if (oy >= 0 && oy < oh && ox >= 0 && ox < ow) {
       float m[8];
+      int a[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) m[e] = -INFINITY;
+      for (int e = 0; e < 8; ++e) { m[e] = -INFINITY; a[e] = 0; }
       for (int ky = 0; ky < k; ++ky) {
         for (int kx = 0; kx < k; ++kx) {
           long long src = ((img * hp + oy * st + ky + pi) * wp + ox * st + kx + pi) * c + cg * 8;
           uint4 u = *reinterpret_cast<const uint4*>(x + src);
           const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&u);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) m[e] = fmaxf(m[e], __bfloat162float(hb[e]));
+          for (int e = 0; e < 8; ++e) {
+            const float v = __bfloat162float(hb[e]);
+            if (v > m[e]) { m[e] = v; a[e] = ky * k + kx; }   // first max, row-major
+          }
         }
       }
       __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&res);
 #pragma unroll
       for (int e = 0; e < 8; ++e) ob[e] = __float2bfloat16_rn(m[e]);
+      if (idx != nullptr) {
+        uint2 iw;
+        uint8_t* ib = reinterpret_cast<uint8_t*>(&iw);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ib[e] = m[e] > 0.f ? static_cast<uint8_t>(a[e]) : uint8_t(255);
+        *reinterpret_cast<uint2*>(idx + ((img * oh + oy) * ow + ox) * c + cg * 8) = iw;
+      }
     }
     *reinterpret_cast<uint4*>(y + pos * c + cg * 8) = res;
   }
 }
 
 cudaError_t maxpool_fwd(const __nv_bfloat16* x, int n, int h, int w, int c, int pad_in, int k,
-                        int st, __nv_bfloat16* y, int pad_out, cudaStream_t s) {
+                        int st, __nv_bfloat16* y, int pad_out, cudaStream_t s, uint8_t* idx) {
+  if (idx != nullptr && k * k > 255) return cudaErrorInvalidValue;
   if (c % 8 != 0) return cudaErrorInvalidValue;
   int oh = (h - k) / st + 1, ow = (w - k) / st + 1;
   long long total = static_cast<long long>(n) * (oh + 2 * pad_out) * (ow + 2 * pad_out) * (c / 8);
-  maxpool_fwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, n, h, w, c, pad_in, k, st, y, pad_out, oh, ow);
+  maxpool_fwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, n, h, w, c, pad_in, k, st, y, pad_out, oh, ow, idx);
   return cudaGetLastError();
 }
 
@@ -359,6 +424,70 @@ __global__ void maxpool_bwd_idx_kernel(const uint8_t* __restrict__ idx, const __
     }
   }
   if (colsum != nullptr) block_colsum_flush(csum, threadIdx.x % cv, c, s_col, colsum);
+}
+
+// General k/stride pool backward from argmax bytes (maxpool_fwd with idx): one thread per input
+// position x 8 channels gathers dy from the (at most ceil(k/st)^2) windows whose recorded
+// argmax is this position -- 8 + 16 bytes per covering window instead of re-reading the
+// k*k inputs of every window.
+__global__ void maxpool_bwd_gather_kernel(const uint8_t* __restrict__ idx, const __nv_bfloat16* __restrict__ dy,
+                                          int n, int h, int w, int c, int pi, int k, int st, int po, int oh, int ow,
+                                          __nv_bfloat16* __restrict__ dx, float* __restrict__ colsum) {
+  __shared__ float s_col[kPoolColsumMax];
+  float csum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const int cv = c >> 3;
+  const long long total = static_cast<long long>(n) * h * w * cv;
+  const int hp = h + 2 * pi, wp = w + 2 * pi;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int cg = static_cast<int>(i % cv);
+    const long long pix = i / cv;
+    const int ix = static_cast<int>(pix % w);
+    const long long t = pix / w;
+    const int iy = static_cast<int>(t % h);
+    const long long img = t / h;
+    float g[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const int oy0 = iy - k + 1 > 0 ? (iy - k + st) / st : 0;
+    const int ox0 = ix - k + 1 > 0 ? (ix - k + st) / st : 0;
+    for (int oy = oy0; oy <= iy / st && oy < oh; ++oy) {
+      for (int ox = ox0; ox <= ix / st && ox < ow; ++ox) {
+        const int mine = (iy - oy * st) * k + (ix - ox * st);
+        const long long o = (img * oh + oy) * ow + ox;
+        const uint2 iw = *reinterpret_cast<const uint2*>(idx + o * c + cg * 8);
+        const uint8_t* ib = reinterpret_cast<const uint8_t*>(&iw);
+        bool any = false;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) any |= ib[e] == mine;
+        if (!any) continue;
+        const uint4 dv = *reinterpret_cast<const uint4*>(dy + ((img * (oh + 2 * po) + oy + po) * (ow + 2 * po) + ox + po) * c + cg * 8);
+        const __nv_bfloat16* db = reinterpret_cast<const __nv_bfloat16*>(&dv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (ib[e] == mine) g[e] += __bfloat162float(db[e]);
+      }
+    }
+    uint4 res;
+    __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&res);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      ob[e] = __float2bfloat16_rn(g[e]);
+      csum[e] += __bfloat162float(ob[e]);
+    }
+    *reinterpret_cast<uint4*>(dx + ((img * hp + iy + pi) * wp + ix + pi) * c + cg * 8) = res;
+  }
+  if (colsum != nullptr) block_colsum_flush(csum, threadIdx.x % cv, c, s_col, colsum);
+}
+
+cudaError_t maxpool_bwd_gather(const uint8_t* idx, const __nv_bfloat16* dy, int n, int h, int w, int c, int pad_in,
+                               int k, int st, int pad_out, __nv_bfloat16* dx, float* colsum, cudaStream_t s) {
+  if (c % 8 != 0 || (colsum != nullptr && (c > kPoolColsumMax || c / 8 > 256))) return cudaErrorInvalidValue;
+  const int oh = (h - k) / st + 1, ow = (w - k) / st + 1;
+  const int threads = pool_threads(c);
+  const long long work = static_cast<long long>(n) * h * w * (c / 8);
+  const int grid = static_cast<int>(std::max<long long>(1, std::min((work + threads - 1) / threads,
+                                                                   static_cast<long long>(num_sms()) * 16)));
+  maxpool_bwd_gather_kernel<<<grid, threads, 0, s>>>(idx, dy, n, h, w, c, pad_in, k, st, pad_out, oh, ow, dx, colsum);
+  return cudaGetLastError();
 }
 
 cudaError_t maxpool_bwd_idx(const uint8_t* idx, const __nv_bfloat16* dy, int n, int oh, int ow, int c, int pad_out,

@@ -20,9 +20,10 @@ cudaError_t pack_im2col(const float* x, int n, int h, int w, int c, int k, int s
 
 // Max pool, window k, stride st (no pool padding).  x: [n][h+2pi][w+2pi][c]; y:
 // [n][oh+2po][ow+2po][c] with zero border.  Ties resolve to the first maximum
-// in row-major window order.
+// in row-major window order.  idx (optional, [n][oh][ow][c] uint8): window position of the
+// first max, 255 where it is not > 0 (input of maxpool_bwd_gather).
 cudaError_t maxpool_fwd(const __nv_bfloat16* x, int n, int h, int w, int c, int pad_in, int k,
-                        int st, __nv_bfloat16* y, int pad_out, cudaStream_t s);
+                        int st, __nv_bfloat16* y, int pad_out, cudaStream_t s, uint8_t* idx = nullptr);
 // dx[i] = sum over windows containing i where i is the (first) argmax: dy[window],
 // then times (x[i] > 0) (the ReLU of the producing conv).  dx has x's padded layout,
 // border written as zero.  colsum (optional, c <= 1024): colsum[ch] += sum of the stored dx
@@ -30,6 +31,10 @@ cudaError_t maxpool_fwd(const __nv_bfloat16* x, int n, int h, int w, int c, int 
 // forward (idx [n][oh][ow][c], 255 = no gradient); dy [n][oh+2po][ow+2po][c], dx interior.
 cudaError_t maxpool_bwd_idx(const uint8_t* idx, const __nv_bfloat16* dy, int n, int oh, int ow, int c, int pad_out,
                             int pad_in, __nv_bfloat16* dx, float* colsum, cudaStream_t s);
+// Any k/stride (overlapping windows): gather from the argmax bytes of maxpool_fwd(..., idx)
+// (idx [n][oh][ow][c]: window position ky*k+kx of the first max, 255 = max not > 0).
+cudaError_t maxpool_bwd_gather(const uint8_t* idx, const __nv_bfloat16* dy, int n, int h, int w, int c, int pad_in,
+                               int k, int st, int pad_out, __nv_bfloat16* dx, float* colsum, cudaStream_t s);
 // (the producing conv's bias gradient).
 cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* dy, int n, int h, int w,
                         int c, int pad_in, int k, int st, int pad_out, __nv_bfloat16* dx, float* colsum,

@@ -268,6 +268,14 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
         return fail(*why);
     }
   }
+  // stand-alone pools (overlapping windows, or after a non-slab conv) record argmax bytes in their
+  // forward and gather the backward from them (maxpool_bwd_gather)
+  for (size_t i = 0; i < m->front.size(); ++i) {
+    FrontLayer& pl = m->front[i];
+    if (pl.kind != RALPB_POOL || pl.fused_fwd || pl.k * pl.k > 255) continue;
+    const ActBuf& po = m->acts[i + 1];
+    if (!(pl.idx = alloc<uint8_t>(m, static_cast<size_t>(po.n) * po.h * po.w * po.c, why))) return fail(*why);
+  }
   for (auto& f : m->front) {
     if (f.kind != RALPB_CONV) continue;
     if (!(f.wf = alloc<bf16>(m, f.w_count, why))) return fail(*why);
@@ -580,8 +588,11 @@ int launch_front_backward(Model* m, const bf16* dcut, std::string* why) {
                          : nullptr;
     if (f.kind == RALPB_POOL) {
       bf16* dst = m->gacts[i];
-      if (f.idx != nullptr)
+      if (f.idx != nullptr && f.fused_fwd)
         RALPB_TRY(maxpool_bwd_idx(f.idx, cur, in.n, out.h, out.w, in.c, out.pad, in.pad, dst, prev_db, m->stream));
+      else if (f.idx != nullptr)
+        RALPB_TRY(maxpool_bwd_gather(f.idx, cur, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.pad, dst, prev_db,
+                                     m->stream));
       else
         RALPB_TRY(maxpool_bwd(in.ptr, cur, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.pad, dst, prev_db,
                               m->stream));
@@ -760,7 +771,7 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
       }
       RALPB_TRY(conv_fwd(f.g, in.ptr, f.wf, m->P + f.b_off, out.ptr, 1, s, why));
     } else {
-      RALPB_TRY(maxpool_fwd(in.ptr, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.ptr, out.pad, s));
+      RALPB_TRY(maxpool_fwd(in.ptr, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.ptr, out.pad, s, f.idx));
     }
     ++m->launches;
   }

@@ -59,6 +59,23 @@ def conv_fwd_pool(x_pad, w, bias, *, n, h, w_, cin, cout, k, pad, relu=True, poo
     return y, pooled, idx
 
 
+def maxpool_fwd_idx(x_pad, *, n, h, w, c, pad_in, k, stride, pad_out):
+    oh, ow = (h - k) // stride + 1, (w - k) // stride + 1
+    y = torch.empty(n, oh + 2 * pad_out, ow + 2 * pad_out, c, dtype=_BF16, device=x_pad.device)
+    idx = torch.empty(n, oh, ow, c, dtype=torch.uint8, device=x_pad.device)
+    call("ralpb_maxpool_fwd_idx", x_pad.data_ptr(), n, h, w, c, pad_in, k, stride, y.data_ptr(), pad_out,
+         idx.data_ptr(), _stream())
+    return y, idx
+
+
+def maxpool_bwd_gather(idx, dy, *, h, w, pad_in, k, stride, pad_out, colsum=None):
+    n, _, _, c = idx.shape
+    dx = torch.zeros(n, h + 2 * pad_in, w + 2 * pad_in, c, dtype=_BF16, device=dy.device)
+    call("ralpb_maxpool_bwd_gather", idx.data_ptr(), dy.data_ptr(), n, h, w, c, pad_in, k, stride, pad_out,
+         dx.data_ptr(), _p(colsum), _stream())
+    return dx
+
+
 def maxpool_bwd_idx(idx, dy, *, pad_out, pad_in, colsum=None):
     n, oh, ow, c = idx.shape
     dx = torch.zeros(n, 2 * oh + 2 * pad_in, 2 * ow + 2 * pad_in, c, dtype=_BF16, device=dy.device)

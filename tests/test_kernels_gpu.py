@@ -183,6 +183,13 @@ def test_pool_bwd_overlapping_colsum(c):
     refdx = xr.grad.permute(0, 2, 3, 1) * (x.float() > 0)
     torch.testing.assert_close(dx.float(), refdx.to(torch.bfloat16).float(), rtol=1e-2, atol=1e-2)
     torch.testing.assert_close(colsum, dx.float().sum(dim=(0, 1, 2)), rtol=1e-5, atol=1e-5)
+    # the argmax-byte path (forward records, backward gathers) gives the same forward and backward
+    y_i, idx = ops.maxpool_fwd_idx(x, n=n, h=h, w=w, c=c, pad_in=0, k=3, stride=2, pad_out=0)
+    torch.testing.assert_close(y_i.float(), F.max_pool2d(xr.detach(), 3, 2).permute(0, 2, 3, 1), rtol=0, atol=0)
+    cs2 = torch.zeros(c, device=DEV)
+    dx2 = ops.maxpool_bwd_gather(idx, dy, h=h, w=w, pad_in=0, k=3, stride=2, pad_out=0, colsum=cs2)
+    torch.testing.assert_close(dx2.float(), dx.float(), rtol=0, atol=0)
+    torch.testing.assert_close(cs2, colsum, rtol=1e-5, atol=1e-5)
 
 
 def test_softmax_xent():
@@ -211,7 +218,8 @@ def test_sgd_and_colsum():
     torch.testing.assert_close(ops.colsum(dy), dy.float().sum(0), rtol=1e-4, atol=1e-3)
 
 
-@pytest.mark.parametrize("k,stride,pad,po,kpad,h", [(3, 1, 1, 1, 32, 20), (5, 1, 2, 0, 128, 16), (11, 4, 0, 0, 384, 63)])
+@pytest.mark.parametrize("k,stride,pad,po,kpad,h", [(3, 1, 1, 1, 32, 20), (5, 1, 2, 0, 128, 16), (11, 4, 0, 0, 384, 63),
+                                                  (11, 4, 0, 1, 384, 35)])
 def test_first_conv_im2col(k, stride, pad, po, kpad, h):
     """First (RGB) conv as pack_im2col + GEMM with the bias folded into a ones column (fwd) and
     the filter/bias gradient as one MN x MN GEMM."""
