@@ -56,7 +56,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
   const int stages = p.stages;
   uint8_t* sA = smem;
   uint8_t* sB = smem + stages * kAStage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + stages * p.b_stage_bytes);
+  uint8_t* sC = sB + stages * p.b_stage_bytes;   // tma_epi: 2 x 16 KB output staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(sC + (p.tma_epi ? 2 * 16384 : 0));
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + 2;
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
   } else if (warp >= 4) {
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
-    int acc = 0;
+    int acc = 0, ks_out = 0;
     uint32_t acc_phase = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int nt = w % p.n_nt;
@@ -178,7 +179,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
         tmem_ld32(t_base + c, r);
         tmem_wait_ld();
         const int n0 = nt * bn + c;
-        if (!row_ok || n0 >= p.N) continue;
+        if (n0 >= p.N) continue;           // warp-uniform
+        if (!row_ok && !p.tma_epi) continue;
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
@@ -210,6 +212,37 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
         if (zero_row) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        }
+        if (p.tma_epi) {
+          // stage this row's 32 values (fp32: 128-byte SW128 row; bf16: 64-byte SW64 row) and
+          // write the 128 x 32 block with one TMA store / reduce-add (rows >= M and columns >= N
+          // are clipped by the tensor map)
+          uint8_t* buf = sC + ((ks_out & 1) << 14);
+          if (threadIdx.x == 128) bulk_wait_read<1>();
+          named_bar_sync(1, 128);
+          if (p.epi == EPI_BF16) {
+            uint8_t* rp = buf + row * 64;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint4*>(rp + ((j ^ ((row >> 1) & 3)) << 4)) =
+                  make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                             pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+          } else {
+            uint8_t* rp = buf + row * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(rp + ((j ^ (row & 7)) << 4)) =
+                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (threadIdx.x == 128) {
+            if (p.tma_epi == 2) tma_reduce_add_2d(&p.tmC, buf, n0, mt * kBM);
+            else tma_store_2d(&p.tmC, buf, n0, mt * kBM);
+            bulk_commit();
+          }
+          ++ks_out;
+          continue;
         }
         if (p.epi == EPI_BF16) {
           __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + m * p.s_m + n0 * p.s_n;
@@ -275,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
       mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (p.tma_epi && threadIdx.x == 128) bulk_wait_all();
   }
 
   tc_fence_before();

@@ -113,12 +113,34 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
   if (splits > 1 && d.epi != EPI_F32_ATOMIC) { *why = "split-K needs the atomic epilogue"; return cudaErrorInvalidValue; }
   p.kblocks_per_split = static_cast<int>((kblocks + splits - 1) / splits);
   p.n_ks = static_cast<int>((kblocks + p.kblocks_per_split - 1) / p.kblocks_per_split);
+  // ---- TMA epilogue: coalesced 128x32 boxes (store, or reduce-add for split-K) instead of
+  // per-thread row stores (RALPB_GEMM_TMA_EPI=0 disables)
+  {
+    const char* te = getenv("RALPB_GEMM_TMA_EPI");
+    const bool allowed = !(te != nullptr && te[0] == '0');
+    const int esz = d.epi == EPI_BF16 ? 2 : 4;
+    const bool shape_ok = d.s_n == 1 && !d.border && d.N >= 32 &&
+                          (reinterpret_cast<uintptr_t>(d.out) & 15) == 0 && (d.s_m * esz) % 16 == 0;
+    if (allowed && shape_ok && (d.epi == EPI_F32 || d.epi == EPI_BF16 || d.epi == EPI_F32_ATOMIC)) {
+      auto fn = encode_fn();
+      cuuint64_t dims[2] = {static_cast<cuuint64_t>(d.N), static_cast<cuuint64_t>(d.M)};
+      cuuint64_t strides[1] = {static_cast<cuuint64_t>(d.s_m) * esz};
+      cuuint32_t box[2] = {32, 128};
+      cuuint32_t estr[2] = {1, 1};
+      CUresult r = fn(&p.tmC, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                      d.out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      esz == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r == CUDA_SUCCESS) p.tma_epi = d.epi == EPI_F32_ATOMIC ? 2 : 1;
+    }
+  }
   // ---- stages
   const int stage_bytes = kAStage + p.b_stage_bytes;
-  const int budget = 227 * 1024 - 1024 - 256;
+  const int staging = p.tma_epi ? 2 * 16384 : 0;
+  const int budget = 227 * 1024 - 1024 - 256 - staging;
   p.stages = std::min(8, budget / stage_bytes);
   if (const char* e = getenv("RALPB_STAGES")) p.stages = std::max(1, std::min(p.stages, atoi(e)));
-  const int smem = 1024 + p.stages * stage_bytes + 256;
+  const int smem = 1024 + p.stages * stage_bytes + staging + 256;
   p.idesc = umma_idesc_bf16(kBM, bn, !a_k, !b_k);
   p.a_mode = d.a_mode;
   p.b_mode = d.b_mode;

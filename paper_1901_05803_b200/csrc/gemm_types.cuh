@@ -36,6 +36,8 @@ constexpr int kThreads = 256;
 struct alignas(64) GemmParams {
   CUtensorMap tmA;
   CUtensorMap tmB;
+  CUtensorMap tmC;          // tma_epi: output [M][N] (row stride s_m), box {32, 128}
+  int tma_epi;              // 0: per-thread stores; 1: TMA store (EPI_F32 / EPI_BF16); 2: TMA reduce-add (EPI_F32_ATOMIC)
   int M, N;                 // output extent (rows of A, rows of B)
   int n_mt, n_nt, n_ks;     // tile grid (m tiles, n tiles, k splits)
   int kblocks_total;        // k-blocks over the whole K
