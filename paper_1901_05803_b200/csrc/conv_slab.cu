@@ -110,7 +110,9 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
   const int rows1 = (g.h + 16 * p.macc - 1) / (16 * p.macc) * 16 * p.macc;
   const int rows2 = (g.h + 32 * p.macc - 1) / (32 * p.macc) * 32 * p.macc;
   // 64-wide tiles pair up only outside the filter-resident mode (conv2_1 dgrad: +10 %)
-  const bool wres_shape = c == p.kb && cout <= p.bn;
+  const char* nwe = getenv("RALPB_NO_WRES");
+  const bool no_wres = nwe != nullptr && nwe[0] == '1';
+  const bool wres_shape = c == p.kb && cout <= p.bn && !no_wres;
   const bool pair = (p.bn == 128 || p.bn == 256 || (p.bn == 64 && !wres_shape)) && rows2 == rows1 &&
                     !(penv != nullptr && penv[0] == '0');
   const int ncta = pair ? 2 : 1;
@@ -139,7 +141,7 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
   p.tmem_cols = used <= 32 ? 32 : used <= 64 ? 64 : used <= 128 ? 128 : used <= 256 ? 256 : 512;
   // Filters resident in shared memory when one channel block and one N tile cover the layer
   // (e.g. 64->64 at 224x224): the per-tile filter reloads disappear.
-  if (c == p.kb && cout <= p.bn && p.macc >= 2) {
+  if (wres_shape && p.macc >= 2) {
     const int macc2 = 2;
     const int slab2 = align1k(p.row_bytes * p.sw * (16 * macc2 + g.k - 1));
     const int na2 = g.taps() * p.b_stage + 3 * slab2 <= budget ? 3 : 2;
