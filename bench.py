@@ -169,7 +169,7 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def _build_executor(strategy: str, world: int, rank: int):
+def _build_executor(strategy: str, world: int, rank: int, ring_backend: str = "native"):
     from paper_1901_05803_b200 import synthetic
     from paper_1901_05803_b200.executor import RankExecutor
     from paper_1901_05803_b200.planner import JobSpec, Strategy, catalog_lookup, profile
@@ -178,9 +178,11 @@ def _build_executor(strategy: str, world: int, rank: int):
     rep = profile(m)
     if strategy == "ralp":
         job = JobSpec(m, Strategy.ralp(rep.split_index), world)
+    elif strategy == "ring":
+        job = JobSpec(m, Strategy.ring(), world, ps_count=0)
     else:
         job = JobSpec(m, Strategy.baseline(), world)
-    ex = RankExecutor(job, rank=rank, world=world)
+    ex = RankExecutor(job, rank=rank, world=world, ring_backend=ring_backend)
     ex.set_params(synthetic.init_params(ex.layers, 0))
     return ex, job, rep
 
@@ -314,6 +316,19 @@ def run_ours(args):
     ms_b = _time_steps(exb, dimgs, dlabs, args.steps, args.warmup, world)
     stb = exb.stats()
     exb.close()
+    # ring all-reduce comparators (StrategyKind.RING_ALLREDUCE, the Horovod baseline of the paper):
+    # the hand-written NVLink RS+SGD+AG vs NCCL all_reduce of the gradient vector (N > 1)
+    ring = None
+    if world > 1:
+        ring = {}
+        for backend in ("native", "nccl"):
+            torch.cuda.empty_cache()
+            exr, _, _ = _build_executor("ring", world, rank, backend)
+            ms_r = _time_steps(exr, dimgs, dlabs, args.steps, args.warmup, world)
+            str_ = exr.stats()
+            exr.close()
+            ring[backend] = {"value": world * BATCH / (ms_r * 1e-3), "ms_per_step": ms_r,
+                             "logical_sync_bytes_per_step": str_.logical_bytes}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -335,6 +350,7 @@ def run_ours(args):
                                     "physical_nvlink_rank0": st.physical_bytes},
             "all_on_ps": {"value": world * BATCH / (ms_b * 1e-3), "ms_per_step": ms_b,
                           "logical_sync_bytes_per_step": stb.logical_bytes},
+            "ring_allreduce": ring,
             "breakdown_ms_rank0": {"front_fwd": st.ms_front_fwd, "back": st.ms_back, "front_bwd": st.ms_front_bwd,
                                    "sync": st.ms_sync, "tensor_kernels_sum": prof.ms_gemm,
                                    "tensor_launches": prof.gemm_launches},

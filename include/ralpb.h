@@ -127,7 +127,12 @@ int ralpb_cast_bf16(const float* x, long long n, void* y, void* stream);
  * (costmodel.py:34-37): RALP = conv front replicated + FC tail on the PS rank,
  * BASELINE_PS = every layer on every worker, all parameters through the PS. */
 enum { RALPB_CONV = 0, RALPB_POOL = 1, RALPB_FC = 2 };
-enum { RALPB_STRATEGY_BASELINE = 0, RALPB_STRATEGY_RALP = 1 };
+/* BASELINE: StrategyKind.BASELINE_PS (every layer on every worker, all parameters through the
+ * sharded PS).  RALP: StrategyKind.RALP.  RING: StrategyKind.RING_ALLREDUCE (simulator.py:719-737)
+ * with the hand-written reduce-scatter + SGD + all-gather over NVLink; RING_EXTERNAL: the same
+ * but the step stops after the backward so the caller all-reduces the gradient buffer (e.g. with
+ * NCCL, the comparison baseline) and then calls ralpb_model_apply. */
+enum { RALPB_STRATEGY_BASELINE = 0, RALPB_STRATEGY_RALP = 1, RALPB_STRATEGY_RING = 2, RALPB_STRATEGY_RING_EXTERNAL = 3 };
 
 typedef struct {
   int kind;            /* RALPB_CONV / RALPB_POOL / RALPB_FC */
@@ -182,6 +187,11 @@ void* ralpb_model_stream(ralpb_model* m);
 /* Inspection: copies activation (which=0) or activation-gradient (which=1) buffer i (bf16,
  * padded layout) to host_out (may be NULL to query); returns its element count or -1. */
 long long ralpb_model_debug_buffer(ralpb_model* m, int i, int which, void* host_out);
+/* RING_EXTERNAL: the fp32 gradient vector (all parameters, device memory, `*n` floats) the caller
+ * all-reduces (sum over ranks) after ralpb_model_step, and the update that follows
+ * (SGD-momentum + bf16 re-layout) on the model stream. */
+int ralpb_model_grad_buffer(ralpb_model* m, float** ptr, long long* n);
+int ralpb_model_apply(ralpb_model* m, float lr, float mu);
 /* Profiling mode: bracket every tensor-core launch with CUDA events (reported in stats). */
 int ralpb_model_set_profiling(ralpb_model* m, int on);
 /* Per-launch records of the last profiled step: kind = 0 conv fwd/dgrad (single CTA), 1 conv

@@ -56,6 +56,8 @@ SIGNATURES: dict[str, tuple] = {
     "ralpb_model_stats": (c_i, [c_vp, c_vp]),
     "ralpb_model_read_loss": (c_i, [c_vp, c_i, c_vp]),
     "ralpb_model_timed_launches": (c_i, [c_vp, c_vp, c_i]),
+    "ralpb_model_grad_buffer": (c_i, [c_vp, c_vp, c_vp]),
+    "ralpb_model_apply": (c_i, [c_vp, c_f, c_f]),
     "ralpb_model_stream": (c_vp, [c_vp]),
     "ralpb_model_set_profiling": (c_i, [c_vp, c_i]),
     "ralpb_model_debug_buffer": (c_ll, [c_vp, c_i, c_i, c_vp]),
@@ -86,7 +88,7 @@ class StepStats(C.Structure):
 
 
 RALPB_CONV, RALPB_POOL, RALPB_FC = 0, 1, 2
-RALPB_STRATEGY_BASELINE, RALPB_STRATEGY_RALP = 0, 1
+RALPB_STRATEGY_BASELINE, RALPB_STRATEGY_RALP, RALPB_STRATEGY_RING, RALPB_STRATEGY_RING_EXTERNAL = 0, 1, 2, 3
 
 
 class BackendError(RuntimeError):

@@ -65,6 +65,16 @@ int ralpb_model_timed_launches(ralpb_model* m, ralpb_launch_rec* out, int cap) {
   return n;
 }
 
+int ralpb_model_grad_buffer(ralpb_model* m, float** ptr, long long* n) {
+  std::string why;
+  return model_grad_buffer(m->impl, ptr, n, &why) ? set_error("ralpb_model_grad_buffer: " + why) : 0;
+}
+
+int ralpb_model_apply(ralpb_model* m, float lr, float mu) {
+  std::string why;
+  return model_apply(m->impl, lr, mu, &why) ? set_error("ralpb_model_apply: " + why) : 0;
+}
+
 int ralpb_model_read_loss(ralpb_model* m, int lag, float* out) {
   std::string why;
   return model_read_loss(m->impl, lag, out, &why) ? set_error("ralpb_model_read_loss: " + why) : 0;

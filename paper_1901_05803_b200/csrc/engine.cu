@@ -84,6 +84,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     return 1;
   }
   if (batch % 4 != 0) { *why = "batch must be a multiple of 4"; return 1; }
+  if (strategy < RALPB_STRATEGY_BASELINE || strategy > RALPB_STRATEGY_RING_EXTERNAL) { *why = "unknown strategy"; return 1; }
   auto m = new Model();
   m->rank = rank; m->world = world; m->ps_rank = ps_rank; m->batch = batch;
   m->strategy = strategy; m->elem_bytes = elem_bytes;
@@ -99,7 +100,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   if (strategy == RALPB_STRATEGY_RALP && split != nconv)
     return fail("this executor places exactly the FC tail on the PS (split must be " + std::to_string(nconv) + ")");
   m->split = nconv;
-  m->holds_back = strategy == RALPB_STRATEGY_BASELINE || rank == ps_rank;
+  m->holds_back = strategy != RALPB_STRATEGY_RALP || rank == ps_rank;
   m->rows_back = strategy == RALPB_STRATEGY_RALP ? world * batch : batch;
 
   // ---- front geometry
@@ -859,6 +860,7 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   // join the FC tail's update before this rank signals the sync: a worker can only start the
   // next step (and push its cut into x_fc, which the FC wgrads read) after that sync
   if (fc_forked) RALPB_TRY(cudaStreamWaitEvent(s, m->ev_join, 0));
+  if (m->strategy == RALPB_STRATEGY_RING_EXTERNAL) return 0;  // the caller all-reduces G, then apply
   if (sync_params(m, ralp ? m->n_front : m->n_total, lr, mu, why)) return 1;
   if (relayout_weights(m, !ralp, why)) return 1;
   return 0;
@@ -970,8 +972,11 @@ int model_stats(Model* m, ralpb_step_stats* st, std::string* why) {
   if (m->holds_back) RALPB_TRY(cudaMemcpy(&loss, m->loss, sizeof(float), cudaMemcpyDeviceToHost));
   st->loss = loss;
   const long long eb = m->elem_bytes;
+  const bool ring = m->strategy == RALPB_STRATEGY_RING || m->strategy == RALPB_STRATEGY_RING_EXTERNAL;
   if (ralp)
     st->logical_bytes = static_cast<long long>(m->world) * 2 * (static_cast<long long>(m->batch) * m->cut_elems * eb + m->real_front * eb);
+  else if (ring)  // volume_ring: 2 * S * (W - 1) (costmodel.py:118-121)
+    st->logical_bytes = 2LL * (m->world - 1) * m->real_total * eb;
   else
     st->logical_bytes = static_cast<long long>(m->world) * 2 * m->real_total * eb;
   st->physical_bytes = m->phys_bytes;
@@ -988,6 +993,22 @@ int model_stats(Model* m, ralpb_step_stats* st, std::string* why) {
     cudaEventElapsedTime(&ms, m->timer.ev[2 * i], m->timer.ev[2 * i + 1]);
     st->ms_gemm += ms;
   }
+  return 0;
+}
+
+int model_grad_buffer(Model* m, float** ptr, long long* n, std::string* why) {
+  if (m->strategy != RALPB_STRATEGY_RING_EXTERNAL) { *why = "only for RALPB_STRATEGY_RING_EXTERNAL"; return 1; }
+  *ptr = m->G;
+  *n = m->n_total;
+  return 0;
+}
+
+// Update after the caller's gradient all-reduce (RING_EXTERNAL): SGD-momentum over every
+// parameter, then the bf16 re-layouts the next step reads.
+int model_apply(Model* m, float lr, float mu, std::string* why) {
+  if (m->strategy != RALPB_STRATEGY_RING_EXTERNAL) { *why = "only for RALPB_STRATEGY_RING_EXTERNAL"; return 1; }
+  RALPB_TRY(sgd_momentum(m->P, m->V, m->G, m->n_total, lr, mu, 1.f, m->stream));
+  if (relayout_weights(m, true, why)) return 1;
   return 0;
 }
 

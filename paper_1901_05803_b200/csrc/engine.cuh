@@ -141,5 +141,7 @@ int model_ipc_handle(Model* m, void* out, std::string* why);
 int model_ipc_open(Model* m, const void* handles, std::string* why);
 int model_set_profiling(Model* m, int on, std::string* why);
 int model_timed_launches(Model* m, ralpb_launch_rec* out, int cap, int* n, std::string* why);
+int model_grad_buffer(Model* m, float** ptr, long long* n, std::string* why);
+int model_apply(Model* m, float lr, float mu, std::string* why);
 
 }  // namespace ralpb

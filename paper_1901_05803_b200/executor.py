@@ -121,13 +121,18 @@ class RankExecutor:
     (any backend) so the IPC handles can be exchanged."""
 
     def __init__(self, job: JobSpec, *, rank: int = 0, world: Optional[int] = None, ps_rank: int = 0,
-                 input_shape: Optional[tuple[int, int, int]] = None):
+                 input_shape: Optional[tuple[int, int, int]] = None, ring_backend: str = "native"):
+        """ring_backend (StrategyKind.RING_ALLREDUCE only): "native" = the hand-written
+        reduce-scatter + SGD + all-gather over NVLink peer memory inside the step; "nccl" = the
+        step stops after the backward, torch.distributed (NCCL) all-reduces the gradient vector
+        on the model stream, then the update runs (the comparison baseline)."""
         world = job.worker_count if world is None else world
         if world != job.worker_count:
             raise ExecutorError("one rank per worker: world size must equal worker_count")
         kind = job.strategy.kind
-        if kind is StrategyKind.RING_ALLREDUCE:
-            raise ExecutorError("ring all-reduce execution is not implemented (SURVEY.md §8f.4)")
+        if ring_backend not in ("native", "nccl"):
+            raise ExecutorError(f"unknown ring backend {ring_backend!r}")
+        self.ring_backend = ring_backend if kind is StrategyKind.RING_ALLREDUCE else None
         self.job = job
         self.model = job.model
         self.rank, self.world, self.ps_rank = rank, world, ps_rank
@@ -135,7 +140,12 @@ class RankExecutor:
         self.in_shape = (self.layers[0]["h"], self.layers[0]["w"], self.layers[0]["cin"])
         self.classes = self.layers[-1]["cout"]
         split = job.strategy.split_index if kind is StrategyKind.RALP else 0
-        strategy = _lib.RALPB_STRATEGY_RALP if kind is StrategyKind.RALP else _lib.RALPB_STRATEGY_BASELINE
+        if kind is StrategyKind.RALP:
+            strategy = _lib.RALPB_STRATEGY_RALP
+        elif kind is StrategyKind.RING_ALLREDUCE:
+            strategy = _lib.RALPB_STRATEGY_RING if ring_backend == "native" else _lib.RALPB_STRATEGY_RING_EXTERNAL
+        else:
+            strategy = _lib.RALPB_STRATEGY_BASELINE
         self._descs = _desc_array(self.layers)
         h = C.c_void_p()
         _lib.call("ralpb_model_create", C.cast(self._descs, C.c_void_p), len(self.layers), split,
@@ -193,6 +203,30 @@ class RankExecutor:
             labels = np.ascontiguousarray(labels, dtype=np.int32)
             ip, lp = _ptr(images), _ptr(labels)
         _lib.call("ralpb_model_step", self._h, ip, lp, on_host, float(lr), float(momentum))
+        if self.ring_backend == "nccl":
+            self._nccl_allreduce_and_apply(float(lr), float(momentum))
+
+    def _grad_tensor(self):
+        """The engine's fp32 gradient vector as a zero-copy torch tensor (CUDA array interface)."""
+        if getattr(self, "_gtensor", None) is None:
+            import torch
+            ptr, n = C.c_void_p(), C.c_longlong()
+            _lib.call("ralpb_model_grad_buffer", self._h, C.byref(ptr), C.byref(n))
+
+            class _View:
+                __cuda_array_interface__ = {"shape": (n.value,), "typestr": "<f4", "data": (ptr.value, False),
+                                            "version": 3, "strides": None}
+            self._gtensor = torch.as_tensor(_View(), device="cuda")
+        return self._gtensor
+
+    def _nccl_allreduce_and_apply(self, lr: float, mu: float) -> None:
+        import torch
+        import torch.distributed as dist
+        g = self._grad_tensor()
+        if self.world > 1:
+            with torch.cuda.stream(torch.cuda.ExternalStream(self.stream)):
+                dist.all_reduce(g)
+        _lib.call("ralpb_model_apply", self._h, lr, mu)
 
     def stats(self) -> StepResult:
         st = _lib.StepStats()
@@ -228,14 +262,15 @@ class RankExecutor:
 
 
 def run_job(job: JobSpec, steps: int = 10, *, warmup: int = 0, seed: int = 0, lr: float = 0.01,
-            momentum: float = 0.9, params=None, input_shape=None, name: Optional[str] = None) -> JobReport:
+            momentum: float = 0.9, params=None, input_shape=None, name: Optional[str] = None,
+            ring_backend: str = "native") -> JobReport:
     """Execute `job` for `steps` measured steps on this process's rank (RANK/WORLD_SIZE from the
     environment, torch.distributed already initialised when W > 1).  Returns the job report on
     every rank (rank 0's carries the loss)."""
     from . import synthetic
 
     rank = int(os.environ.get("RANK", "0"))
-    ex = RankExecutor(job, rank=rank, input_shape=input_shape)
+    ex = RankExecutor(job, rank=rank, input_shape=input_shape, ring_backend=ring_backend)
     try:
         if params is None:
             params = synthetic.init_params(ex.layers, seed)
