@@ -35,6 +35,11 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, ui
 }
 
 constexpr int kSlabMaxTaps = 25;
+#ifndef RALPB_B_PRODUCERS
+#define RALPB_B_PRODUCERS 2
+#endif
+constexpr int kBProducers = RALPB_B_PRODUCERS;   // warps issuing filter-tile TMA loads (3: warp 0 joins;
+                                                  // measured +10 % on conv3_1 alone, -1 % per step)
 
 struct alignas(64) SlabConvParams {
   CUtensorMap tmX;      // activation [N][Hp][Wp][C], box {kb, SW, SH, 1}
@@ -160,7 +165,7 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
             else
               tma_load_4d(sA + as * p.slab_stage, &p.tmX, &a_full[as], cb * p.kb, w0, h0, img);
             if (++as == p.na) { as = 0; aph ^= 1; }
-            continue;
+            if (p.wres || kBProducers == 2) continue;   // warp 0 only streams slabs
           }
           if (p.wres) {  // whole filter bank once per CTA (single channel block, single N tile)
             if (wi == w_first)
@@ -173,8 +178,11 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
               }
             continue;
           }
+          // filter tiles rotate over the producer warps (2, 3[, 0]): a TMA issue occupies its
+          // thread for hundreds of cycles (tools/exp_tma.cu)
+          const int pidx = warp == 0 ? 2 : warp - 2;
           for (int tap = 0; tap < p.taps; ++tap, ++bseq) {
-            if ((bseq & 1) == (warp - 2)) {
+            if (bseq % kBProducers == pidx) {
               mbar_wait(&b_empty[bs], bph ^ 1);
               if (rank == 0) mbar_expect_tx(&b_full[bs], NCTA * p.b_load);
               if constexpr (PAIR)
