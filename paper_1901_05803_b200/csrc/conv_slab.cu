@@ -122,6 +122,8 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
   p.b_stage = align1k(p.b_load);
   p.na = 2;
   int staging = 0, budget = 0;
+  int nb_cap = 8;
+  if (const char* e = getenv("RALPB_NB")) nb_cap = std::max(2, std::min(16, atoi(e)));
   // M accumulators per tile: shrink until two slab stages, two filter stages and the output
   // staging (2 x 8 KB per epilogue warpgroup, TMA-store epilogue) fit in shared memory
   for (;;) {
@@ -130,7 +132,7 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
     p.slab_stage = align1k(p.slab_load);
     staging = (p.macc >= 2 ? 2 : 1) * 2 * 8192;
     budget = kSmemBudget - staging;
-    p.nb = std::min(8, (budget - p.na * p.slab_stage) / p.b_stage);
+    p.nb = std::min(nb_cap, (budget - p.na * p.slab_stage) / p.b_stage);
     if (p.nb >= 2 || p.macc == 1) break;
     p.macc /= 2;
   }
