@@ -30,6 +30,11 @@ namespace {
 
 constexpr int kTH = 8, kTW = 16;         // output tile (rows x cols) = 128 pixels
 constexpr int kStages = 4;
+#ifndef RALPB_FIRST_GROUPS
+#define RALPB_FIRST_GROUPS 3
+#endif
+constexpr int kGroups = RALPB_FIRST_GROUPS;   // producer warpgroups (tiles alternate between them)
+constexpr int kProd = 4 * kGroups;            // producer warps
 
 struct FirstConvParams {
   CUtensorMap tmY;        // fwd: output (store); wgrad: dY (load); [n][hp][wp][64] box {64,16,8,1}
@@ -72,6 +77,22 @@ __device__ __forceinline__ void build_patch_row(const FirstConvParams& p, int im
     *reinterpret_cast<uint4*>(dst + ((c ^ sw) << 4)) = make_uint4(w32[4 * c], w32[4 * c + 1], w32[4 * c + 2], w32[4 * c + 3]);
 }
 
+// Producer warpgroup g builds the patch tiles of local tiles j = g, g + kGroups, ... (thread =
+// pixel, 27 gathers each); several groups keep more image loads in flight.
+__device__ __forceinline__ void produce_tiles(const FirstConvParams& p, uint8_t* sP, uint64_t* full, uint64_t* empty) {
+  const int g = threadIdx.x >> 7, m = threadIdx.x & 127;
+  for (int j = g;; j += kGroups) {
+    const int t = static_cast<int>(blockIdx.x) + j * static_cast<int>(gridDim.x);
+    if (t >= p.total) break;
+    const int tw = t % p.tiles_w, th = (t / p.tiles_w) % p.tiles_h, img = t / (p.tiles_w * p.tiles_h);
+    const int st = j % kStages;
+    mbar_wait(&empty[st], ((j / kStages) & 1) ^ 1);
+    build_patch_row(p, img, th * kTH + m / kTW, tw * kTW + m % kTW, sP + st * 8192, m);
+    fence_proxy_async_smem();
+    mbar_arrive(&full[st]);
+  }
+}
+
 __device__ __forceinline__ void load_filters(const FirstConvParams& p, uint8_t* sB) {
   for (int t = threadIdx.x; t < 64 * 4; t += blockDim.x) {
     const int r = t >> 2, c = t & 3;
@@ -98,9 +119,9 @@ __device__ __forceinline__ void tile_coords(const FirstConvParams& p, int t, int
   x0 = tw * kTW;
 }
 
-// warps 0-3: patch producers (thread = pixel); warps 4-7: epilogue (thread = pixel = TMEM lane);
-// warp 8: TMEM allocation + MMA issue.
-__global__ void __launch_bounds__(288, 1) conv_first_fwd_kernel(const __grid_constant__ FirstConvParams p) {
+// warps 0..kProd-1: patch producers (thread = pixel); the next 4: epilogue (thread = pixel = TMEM
+// lane); the last: TMEM allocation + MMA issue.
+__global__ void __launch_bounds__(32 * (kProd + 5), 1) conv_first_fwd_kernel(const __grid_constant__ FirstConvParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = smem;                           // 4 KB filters
@@ -120,26 +141,15 @@ __global__ void __launch_bounds__(288, 1) conv_first_fwd_kernel(const __grid_con
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128); }
     fence_barrier_init();
   }
-  if (warp == 8) tmem_alloc(tmem_slot, 128);
+  if (warp == kProd + 4) tmem_alloc(tmem_slot, 128);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp < 4) {
-    const int m = threadIdx.x;
-    int st = 0;
-    uint32_t ph = 0;
-    for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
-      int img, y0, x0;
-      tile_coords(p, t, img, y0, x0);
-      mbar_wait(&a_empty[st], ph ^ 1);
-      build_patch_row(p, img, y0 + m / kTW, x0 + m % kTW, sA + st * 8192, m);
-      fence_proxy_async_smem();
-      mbar_arrive(&a_full[st]);
-      if (++st == kStages) { st = 0; ph ^= 1; }
-    }
-  } else if (warp == 8) {
+  if (warp < kProd) {
+    produce_tiles(p, sA, a_full, a_empty);
+  } else if (warp == kProd + 4) {
     const uint32_t idesc = umma_idesc_bf16(128, 64, false, false);
     const uint64_t b0 = umma_smem_desc(smem_u32(sB), 16, 512, 64);
     const uint64_t a0 = umma_smem_desc(smem_u32(sA), 16, 512, 64);
@@ -203,7 +213,7 @@ __global__ void __launch_bounds__(288, 1) conv_first_fwd_kernel(const __grid_con
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == kProd + 4) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 128);
   }
@@ -211,7 +221,7 @@ __global__ void __launch_bounds__(288, 1) conv_first_fwd_kernel(const __grid_con
 
 // warps 0-3: patch producers; warp 4: dY TMA; warp 5: TMEM + MMA.  Warp 0 reduces the
 // accumulator into dW at the end (TMEM lanes 0-31 = patch columns).
-__global__ void __launch_bounds__(192, 1) conv_first_wgrad_kernel(const __grid_constant__ FirstConvParams p) {
+__global__ void __launch_bounds__(32 * (kProd + 2), 1) conv_first_wgrad_kernel(const __grid_constant__ FirstConvParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sY = smem;                           // kStages x 16 KB dY tiles
@@ -223,30 +233,19 @@ __global__ void __launch_bounds__(192, 1) conv_first_wgrad_kernel(const __grid_c
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     tma_prefetch(&p.tmY);
-    for (int i = 0; i < kStages; ++i) { mbar_init(&full[i], 129); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < kStages; ++i) { mbar_init(&full[i], 129); mbar_init(&empty[i], 1); }  // 128 producers + TMA
     mbar_init(done, 1);
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, 64);
+  if (warp == kProd + 1) tmem_alloc(tmem_slot, 64);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp < 4) {
-    const int m = threadIdx.x;
-    int st = 0;
-    uint32_t ph = 0;
-    for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
-      int img, y0, x0;
-      tile_coords(p, t, img, y0, x0);
-      mbar_wait(&empty[st], ph ^ 1);
-      build_patch_row(p, img, y0 + m / kTW, x0 + m % kTW, sP + st * 8192, m);
-      fence_proxy_async_smem();
-      mbar_arrive(&full[st]);
-      if (++st == kStages) { st = 0; ph ^= 1; }
-    }
-  } else if (warp == 4) {
+  if (warp < kProd) {
+    produce_tiles(p, sP, full, empty);
+  } else if (warp == kProd) {
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
@@ -259,7 +258,7 @@ __global__ void __launch_bounds__(192, 1) conv_first_wgrad_kernel(const __grid_c
         if (++st == kStages) { st = 0; ph ^= 1; }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kProd + 1) {
     // A = patch^T: MN-major SW64 (M atoms of 32 columns; only atom 0 is real -- LBO = 0 makes
     // the other three alias it, their rows of D are ignored), K = pixels (8-row groups 512 B).
     const uint32_t idesc = umma_idesc_bf16(128, 64, true, true);
@@ -300,7 +299,7 @@ __global__ void __launch_bounds__(192, 1) conv_first_wgrad_kernel(const __grid_c
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == kProd + 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 64);
   }
@@ -331,7 +330,7 @@ cudaError_t conv_first_fwd(const float* img, int n, int h, int w, int cin, const
   const int smem = 1024 + 4096 + kStages * 8192 + 2 * 16384 + 256;
   const int grid = std::min(p.total, num_sms());
   cudaFuncSetAttribute(conv_first_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  launch_timed([&] { conv_first_fwd_kernel<<<grid, 288, smem, s>>>(p); }, s, KIND_FIRST_FWD,
+  launch_timed([&] { conv_first_fwd_kernel<<<grid, 32 * (kProd + 5), smem, s>>>(p); }, s, KIND_FIRST_FWD,
                2.0 * n * h * w * 27.0 * 64.0);
   return cudaGetLastError();
 }
@@ -344,7 +343,7 @@ cudaError_t conv_first_wgrad(const float* img, int n, int h, int w, int cin, con
   const int smem = 1024 + kStages * (16384 + 8192) + 256;
   const int grid = std::min(p.total, num_sms());
   cudaFuncSetAttribute(conv_first_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  launch_timed([&] { conv_first_wgrad_kernel<<<grid, 192, smem, s>>>(p); }, s, KIND_FIRST_WGRAD,
+  launch_timed([&] { conv_first_wgrad_kernel<<<grid, 32 * (kProd + 2), smem, s>>>(p); }, s, KIND_FIRST_WGRAD,
                2.0 * n * h * w * 27.0 * 64.0);
   return cudaGetLastError();
 }
