@@ -169,7 +169,7 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def _build_executor(strategy: str, world: int, rank: int, ring_backend: str = "native"):
+def _build_executor(strategy: str, world: int, rank: int, ring_backend: str = "native", fc_sharding: str = "single"):
     from paper_1901_05803_b200 import synthetic
     from paper_1901_05803_b200.executor import RankExecutor
     from paper_1901_05803_b200.planner import JobSpec, Strategy, catalog_lookup, profile
@@ -182,7 +182,7 @@ def _build_executor(strategy: str, world: int, rank: int, ring_backend: str = "n
         job = JobSpec(m, Strategy.ring(), world, ps_count=0)
     else:
         job = JobSpec(m, Strategy.baseline(), world)
-    ex = RankExecutor(job, rank=rank, world=world, ring_backend=ring_backend)
+    ex = RankExecutor(job, rank=rank, world=world, ring_backend=ring_backend, fc_sharding=fc_sharding)
     ex.set_params(synthetic.init_params(ex.layers, 0))
     return ex, job, rep
 
@@ -329,6 +329,17 @@ def run_ours(args):
             exr.close()
             ring[backend] = {"value": world * BATCH / (ms_r * 1e-3), "ms_per_step": ms_r,
                              "logical_sync_bytes_per_step": str_.logical_bytes}
+    # layer-placed with the FC tail sharded over every GPU (the paper's multi-PS)
+    mps = None
+    if world > 1:
+        torch.cuda.empty_cache()
+        exm, _, _ = _build_executor("ralp", world, rank, fc_sharding="multi")
+        ms_m = _time_steps(exm, dimgs, dlabs, args.steps, args.warmup, world)
+        stm = exm.stats()
+        exm.close()
+        mps = {"value": world * BATCH / (ms_m * 1e-3), "ms_per_step": ms_m,
+               "logical_bytes_per_step": stm.logical_bytes,
+               "note": "FC-0 column-parallel / FC-1 row-parallel over all GPUs (volume_ralp_multi_ps)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -351,6 +362,7 @@ def run_ours(args):
             "all_on_ps": {"value": world * BATCH / (ms_b * 1e-3), "ms_per_step": ms_b,
                           "logical_sync_bytes_per_step": stb.logical_bytes},
             "ring_allreduce": ring,
+            "ralp_fc_sharded": mps,
             "breakdown_ms_rank0": {"front_fwd": st.ms_front_fwd, "back": st.ms_back, "front_bwd": st.ms_front_bwd,
                                    "sync": st.ms_sync, "tensor_kernels_sum": prof.ms_gemm,
                                    "tensor_launches": prof.gemm_launches},

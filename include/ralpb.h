@@ -132,7 +132,12 @@ enum { RALPB_CONV = 0, RALPB_POOL = 1, RALPB_FC = 2 };
  * with the hand-written reduce-scatter + SGD + all-gather over NVLink; RING_EXTERNAL: the same
  * but the step stops after the backward so the caller all-reduces the gradient buffer (e.g. with
  * NCCL, the comparison baseline) and then calls ralpb_model_apply. */
-enum { RALPB_STRATEGY_BASELINE = 0, RALPB_STRATEGY_RALP = 1, RALPB_STRATEGY_RING = 2, RALPB_STRATEGY_RING_EXTERNAL = 3 };
+/* RALP_MPS: layer-placed with the FC tail sharded over every GPU (the paper's
+ * multi-PS future work; the reference forbids ps_count != 1 for RALP, costmodel.py:75-76): the
+ * first FC layer column-parallel, the second row-parallel (partial sums reduced on rank 0), later
+ * FC layers on rank 0; cuts all-gathered, the cut gradient reduce-scattered back. */
+enum { RALPB_STRATEGY_BASELINE = 0, RALPB_STRATEGY_RALP = 1, RALPB_STRATEGY_RING = 2, RALPB_STRATEGY_RING_EXTERNAL = 3,
+       RALPB_STRATEGY_RALP_MPS = 4 };
 
 typedef struct {
   int kind;            /* RALPB_CONV / RALPB_POOL / RALPB_FC */
@@ -185,7 +190,8 @@ int ralpb_model_stats(ralpb_model* m, ralpb_step_stats* out);
 int ralpb_model_read_loss(ralpb_model* m, int lag, float* out);
 void* ralpb_model_stream(ralpb_model* m);
 /* Inspection: copies activation (which=0) or activation-gradient (which=1) buffer i (bf16,
- * padded layout) to host_out (may be NULL to query); returns its element count or -1. */
+ * padded layout), or the last step's logits (which=2, fp32 [rows][ld]; i ignored), to host_out
+ * (may be NULL to query); returns its element count or -1. */
 long long ralpb_model_debug_buffer(ralpb_model* m, int i, int which, void* host_out);
 /* RING_EXTERNAL: the fp32 gradient vector (all parameters, device memory, `*n` floats) the caller
  * all-reduces (sum over ranks) after ralpb_model_step, and the update that follows

@@ -89,6 +89,7 @@ class StepStats(C.Structure):
 
 RALPB_CONV, RALPB_POOL, RALPB_FC = 0, 1, 2
 RALPB_STRATEGY_BASELINE, RALPB_STRATEGY_RALP, RALPB_STRATEGY_RING, RALPB_STRATEGY_RING_EXTERNAL = 0, 1, 2, 3
+RALPB_STRATEGY_RALP_MPS = 4
 
 
 class BackendError(RuntimeError):

@@ -93,6 +93,49 @@ int ralpb_model_set_profiling(ralpb_model* m, int on) {
 // the activation-gradient buffer gacts[i], into host memory; returns the element count.
 extern "C" long long ralpb_model_debug_buffer(ralpb_model* m, int i, int which, void* host_out) {
   Model* mm = m->impl;
+  if (which == 2) {  // logits of the last step (fp32 [rows][ld], as bf16-sized count of floats)
+    const long long n = static_cast<long long>(mm->rows_back) * mm->back.back().ld_out;
+    if (host_out != nullptr) {
+      cudaStreamSynchronize(mm->stream);
+      if (cudaMemcpy(host_out, mm->logits, n * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    }
+    return n;
+  }
+  if (which == 6) {  // dlogits (bf16 [rows][ld])
+    const long long n = static_cast<long long>(mm->rows_back) * mm->back.back().ld_out;
+    if (host_out != nullptr) {
+      cudaStreamSynchronize(mm->stream);
+      if (cudaMemcpy(host_out, mm->dlogits, n * sizeof(bf16), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    }
+    return n;
+  }
+  if (which == 4 && mm->mps) {  // RALP_MPS: this rank's arena partial slot 0 (fp32 [rows][ld1])
+    const long long n = static_cast<long long>(mm->rows_back) * mm->back[1].ld_out;
+    if (host_out != nullptr) {
+      cudaStreamSynchronize(mm->stream);
+      const char* src = static_cast<const char*>(mm->arena) + mm->arena_off_p1;
+      if (cudaMemcpy(host_out, src, n * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    }
+    return n;
+  }
+  if (which == 5 && mm->back.size() > 1) {  // FC-1 bf16 weights as stored on this rank
+    const FcLayer& f = mm->back[1];
+    const long long n = static_cast<long long>(f.lout) * f.lin;
+    if (host_out != nullptr) {
+      cudaStreamSynchronize(mm->stream);
+      if (cudaMemcpy(host_out, f.wbf, n * sizeof(bf16), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    }
+    return n;
+  }
+  if (which == 3) {  // FC-0 output of the last step (bf16 [rows][ld]; RALP_MPS: this rank's slice)
+    const long long n = static_cast<long long>(mm->rows_back) * (mm->mps ? mm->ld_s0 : mm->back[0].ld_out);
+    if (host_out != nullptr) {
+      cudaStreamSynchronize(mm->stream);
+      if (cudaMemcpy(host_out, mm->mps ? mm->h0s : mm->hid[0], n * sizeof(bf16), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -1;
+    }
+    return n;
+  }
   if (i < 0 || i >= static_cast<int>(mm->acts.size())) return -1;
   const long long n = mm->acts[i].elems();
   const void* src = which == 0 ? static_cast<const void*>(mm->acts[i].ptr) : static_cast<const void*>(mm->gacts[i]);

@@ -707,6 +707,31 @@ cudaError_t colsum_bf16(const __nv_bfloat16* dy, long long rows, int c, long lon
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ partial sums (RALP_MPS)
+__global__ void sum_partials_kernel(PartialSum ps, int rows, int cols, long long ld, const float* __restrict__ bias,
+                                    int relu, __nv_bfloat16* __restrict__ out_bf16, float* __restrict__ out_f32,
+                                    long long ld_out) {
+  const long long total = static_cast<long long>(rows) * cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / cols;
+    const int c = static_cast<int>(i - r * cols);
+    float v = bias != nullptr ? bias[c] : 0.f;
+    for (int p = 0; p < ps.n; ++p) v += ps.part[p][r * ld + c];
+    if (relu) v = fmaxf(v, 0.f);
+    if (out_bf16 != nullptr) out_bf16[r * ld_out + c] = __float2bfloat16_rn(v);
+    else out_f32[r * ld_out + c] = v;
+  }
+}
+
+cudaError_t sum_partials(const PartialSum& ps, int rows, int cols, long long ld, const float* bias, int relu,
+                         __nv_bfloat16* out_bf16, float* out_f32, long long ld_out, cudaStream_t s) {
+  const long long total = static_cast<long long>(rows) * cols;
+  if (total == 0) return cudaSuccess;
+  sum_partials_kernel<<<grid_for(total, 256), 256, 0, s>>>(ps, rows, cols, ld, bias, relu, out_bf16, out_f32, ld_out);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ weight re-layouts
 // All conv layers' filter copies in one launch: every block transposes 32 (co) x 32 (ci) of one tap
 // through shared memory, so both the forward copy wf [co][t][ci] and the tap-reversed transpose

@@ -18,6 +18,15 @@ cudaError_t pack_input(const float* x, int n, int h, int w, int c, __nv_bfloat16
 cudaError_t pack_im2col(const float* x, int n, int h, int w, int c, int k, int st, int p, int ho, int wo,
                         int po, int kpad, __nv_bfloat16* out, cudaStream_t s);
 
+// out[r][c] = act(sum_p parts[p][r*ld + c] + bias[c]) -> bf16 (out_bf16) or fp32 (out_f32),
+// row stride ld_out; the reduction of row-/column-parallel partial results (RALP_MPS).
+struct PartialSum {
+  const float* part[8];
+  int n;
+};
+cudaError_t sum_partials(const PartialSum& ps, int rows, int cols, long long ld, const float* bias, int relu,
+                         __nv_bfloat16* out_bf16, float* out_f32, long long ld_out, cudaStream_t s);
+
 // Max pool, window k, stride st (no pool padding).  x: [n][h+2pi][w+2pi][c]; y:
 // [n][oh+2po][ow+2po][c] with zero border.  Ties resolve to the first maximum
 // in row-major window order.  idx (optional, [n][oh][ow][c] uint8): window position of the

@@ -42,6 +42,9 @@ constexpr int kFlagAct = 0;       // [8]  PS: worker r's cut landed
 constexpr int kFlagActGrad = 8;   // [1]  worker: act-grad landed
 constexpr int kFlagGrad = 16;     // [8]  rank r finished its backward
 constexpr int kFlagDone = 24;     // [8]  rank r finished its shard update
+constexpr int kFlagP1 = 32;       // [8]  RALP_MPS, rank 0: rank r's FC-1 partial landed
+constexpr int kFlagDh1 = 40;      // [1]  RALP_MPS: FC-1 output gradient landed
+constexpr int kFlagDcut = 48;     // [8]  RALP_MPS: rank r's partial of this rank's cut gradient landed
 constexpr int kNumFlags = 64;
 constexpr int kNumCounters = 64;  // last-CTA counters (local)
 
@@ -84,7 +87,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     return 1;
   }
   if (batch % 4 != 0) { *why = "batch must be a multiple of 4"; return 1; }
-  if (strategy < RALPB_STRATEGY_BASELINE || strategy > RALPB_STRATEGY_RING_EXTERNAL) { *why = "unknown strategy"; return 1; }
+  if (strategy < RALPB_STRATEGY_BASELINE || strategy > RALPB_STRATEGY_RALP_MPS) { *why = "unknown strategy"; return 1; }
   auto m = new Model();
   m->rank = rank; m->world = world; m->ps_rank = ps_rank; m->batch = batch;
   m->strategy = strategy; m->elem_bytes = elem_bytes;
@@ -97,11 +100,21 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   if (nconv == 0 || nconv == n_layers) return fail("model needs a conv/pool front and an FC tail");
   for (int i = nconv; i < n_layers; ++i)
     if (layers[i].kind != RALPB_FC) return fail("only FC layers may follow the first FC layer");
-  if (strategy == RALPB_STRATEGY_RALP && split != nconv)
+  const bool layer_placed = strategy == RALPB_STRATEGY_RALP || strategy == RALPB_STRATEGY_RALP_MPS;
+  m->mps = strategy == RALPB_STRATEGY_RALP_MPS;
+  if (layer_placed && split != nconv)
     return fail("this executor places exactly the FC tail on the PS (split must be " + std::to_string(nconv) + ")");
   m->split = nconv;
-  m->holds_back = strategy != RALPB_STRATEGY_RALP || rank == ps_rank;
-  m->rows_back = strategy == RALPB_STRATEGY_RALP ? world * batch : batch;
+  m->holds_back = strategy != RALPB_STRATEGY_RALP || rank == ps_rank;   // RALP_MPS: every rank
+  m->rows_back = layer_placed ? world * batch : batch;
+  if (m->mps) {
+    if (n_layers - nconv < 2) return fail("RALP_MPS needs at least two FC layers");
+    if (ps_rank != 0) return fail("RALP_MPS keeps the FC tail's head on rank 0");
+    const int out0 = layers[nconv].cout;
+    if (out0 % world != 0 || (out0 / world) % 8 != 0) return fail("RALP_MPS: first FC width must split into multiples of 8");
+    m->s0 = out0 / world;
+    m->ld_s0 = m->s0;
+  }
 
   // ---- front geometry
   const ralpb_layer_desc& l0 = layers[0];
@@ -197,14 +210,17 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     if (d.cin != prev) return fail("fc layer " + std::to_string(i) + ": input width mismatch");
     FcLayer f;
     f.in = d.cin; f.out = d.cout;
+    f.lout = d.cout; f.lin = d.cin;
+    if (m->mps && i == nconv) f.lout = m->s0;           // column-parallel: rows of W0
+    if (m->mps && i == nconv + 1) f.lin = m->s0;        // row-parallel: columns of W1
     f.relu = i + 1 < n_layers ? 1 : 0;
     if ((i + 1 < n_layers) != (d.relu != 0)) return fail("ReLU must follow every FC layer except the last");
     if (i + 1 < n_layers && d.cout % 8 != 0) return fail("hidden FC widths must be multiples of 8");
     f.ld_out = static_cast<int>(align_up(d.cout, 8));
     f.w_off = off;
-    off = align_up(off + static_cast<long long>(d.cout) * d.cin, 4);
+    off = align_up(off + static_cast<long long>(f.lout) * f.lin, 4);
     f.b_off = off;
-    off = align_up(off + d.cout, 4);
+    off = align_up(off + f.lout, 4);
     m->real_total += static_cast<long long>(d.cout) * d.cin + d.cout;
     m->back.push_back(f);
     prev = d.cout;
@@ -220,6 +236,12 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   m->arena_off_xfc = take(static_cast<size_t>(m->rows_back) * m->cut_elems * sizeof(bf16));
   m->arena_off_lab = take(static_cast<size_t>(m->rows_back) * sizeof(int32_t));
   m->arena_off_dcut = take(static_cast<size_t>(batch) * m->cut_elems * sizeof(bf16));
+  if (m->mps) {
+    const int ld1 = static_cast<int>(align_up(layers[nconv + 1].cout, 8));
+    m->arena_off_p1 = take(static_cast<size_t>(world) * m->rows_back * ld1 * sizeof(float));
+    m->arena_off_dh1 = take(static_cast<size_t>(m->rows_back) * ld1 * sizeof(bf16));
+    m->arena_off_dxpart = take(static_cast<size_t>(world) * batch * m->cut_elems * sizeof(float));
+  }
   m->arena_bytes = ao;
   if (cudaMalloc(&m->arena, m->arena_bytes) != cudaSuccess) return fail("cudaMalloc(arena) failed");
   cudaMemset(m->arena, 0, m->arena_bytes);
@@ -283,9 +305,16 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     if (!f.im2col && !(f.wd = alloc<bf16>(m, f.w_count, why))) return fail(*why);
   }
   const int R = m->rows_back;
+  if (m->mps) {
+    const int ld1 = m->back[1].ld_out;
+    if (!(m->h0s = alloc<bf16>(m, static_cast<size_t>(R) * m->ld_s0, why))) return fail(*why);
+    if (!(m->dh0s = alloc<bf16>(m, static_cast<size_t>(R) * m->ld_s0, why))) return fail(*why);
+    if (!(m->p1_local = alloc<float>(m, static_cast<size_t>(R) * ld1, why))) return fail(*why);
+    if (!(m->dxp = alloc<float>(m, static_cast<size_t>(R) * m->cut_elems, why))) return fail(*why);
+  }
   for (size_t j = 0; j < m->back.size(); ++j) {
     auto& f = m->back[j];
-    if (!(f.wbf = alloc<bf16>(m, static_cast<size_t>(f.out) * f.in, why))) return fail(*why);
+    if (!(f.wbf = alloc<bf16>(m, static_cast<size_t>(f.lout) * f.lin, why))) return fail(*why);
     if (j + 1 < m->back.size()) {
       bf16* h = alloc<bf16>(m, static_cast<size_t>(R) * f.ld_out, why);
       if (!h) return fail(*why);
@@ -414,10 +443,22 @@ int model_set_params(Model* m, int layer, const float* w, const float* b, int on
     else
       RALPB_TRY(conv_weight_prep(m->P + f.w_off, co, taps, f.g.cin, f.wf, f.wd, m->stream));
   } else {
-    FcLayer& f = m->back[layer - m->split];
-    RALPB_TRY(cudaMemcpyAsync(m->P + f.w_off, w, static_cast<size_t>(f.out) * f.in * sizeof(float), kind, m->stream));
-    RALPB_TRY(cudaMemcpyAsync(m->P + f.b_off, b, f.out * sizeof(float), kind, m->stream));
-    RALPB_TRY(cast_bf16(m->P + f.w_off, static_cast<long long>(f.out) * f.in, f.wbf, m->stream));
+    const int j = layer - m->split;
+    FcLayer& f = m->back[j];
+    if (m->mps && j == 0) {          // column-parallel: this rank's rows
+      const size_t r0 = static_cast<size_t>(m->rank) * m->s0;
+      RALPB_TRY(cudaMemcpyAsync(m->P + f.w_off, w + r0 * f.in, static_cast<size_t>(f.lout) * f.in * sizeof(float), kind,
+                                m->stream));
+      RALPB_TRY(cudaMemcpyAsync(m->P + f.b_off, b + r0, f.lout * sizeof(float), kind, m->stream));
+    } else if (m->mps && j == 1) {   // row-parallel: this rank's columns (bias applied on rank 0)
+      RALPB_TRY(cudaMemcpy2DAsync(m->P + f.w_off, f.lin * sizeof(float), w + static_cast<size_t>(m->rank) * m->s0,
+                                  f.in * sizeof(float), f.lin * sizeof(float), f.out, kind, m->stream));
+      RALPB_TRY(cudaMemcpyAsync(m->P + f.b_off, b, f.out * sizeof(float), kind, m->stream));
+    } else {
+      RALPB_TRY(cudaMemcpyAsync(m->P + f.w_off, w, static_cast<size_t>(f.out) * f.in * sizeof(float), kind, m->stream));
+      RALPB_TRY(cudaMemcpyAsync(m->P + f.b_off, b, f.out * sizeof(float), kind, m->stream));
+    }
+    RALPB_TRY(cast_bf16(m->P + f.w_off, static_cast<long long>(f.lout) * f.lin, f.wbf, m->stream));
   }
   RALPB_TRY(cudaStreamSynchronize(m->stream));
   return 0;
@@ -450,9 +491,30 @@ int model_get_params(Model* m, int layer, float* w, float* b, int on_host, std::
     RALPB_TRY(cudaMemcpy(w, host.data(), host.size() * sizeof(float), cudaMemcpyDefault));
     RALPB_TRY(cudaMemcpy(b, hb.data(), co * sizeof(float), cudaMemcpyDefault));
   } else {
-    FcLayer& f = m->back[layer - m->split];
-    RALPB_TRY(cudaMemcpy(w, m->P + f.w_off, static_cast<size_t>(f.out) * f.in * sizeof(float), cudaMemcpyDefault));
-    RALPB_TRY(cudaMemcpy(b, m->P + f.b_off, f.out * sizeof(float), cudaMemcpyDefault));
+    const int j = layer - m->split;
+    FcLayer& f = m->back[j];
+    if (m->mps && j <= 1) {
+      // gather every rank's slice through the peer mappings (rank 0's own for W = 1)
+      if (m->world > 1 && !m->peers_open) { *why = "RALP_MPS get_params needs the peers mapped"; return 1; }
+      for (int q = 0; q < m->world; ++q) {
+        const float* pq = at<float>(m, q, m->arena_off_P);
+        if (j == 0) {
+          const size_t r0 = static_cast<size_t>(q) * m->s0;
+          RALPB_TRY(cudaMemcpy(w + r0 * f.in, pq + f.w_off, static_cast<size_t>(f.lout) * f.in * sizeof(float), cudaMemcpyDefault));
+          RALPB_TRY(cudaMemcpy(b + r0, pq + f.b_off, f.lout * sizeof(float), cudaMemcpyDefault));
+        } else {
+          RALPB_TRY(cudaMemcpy2D(w + static_cast<size_t>(q) * m->s0, f.in * sizeof(float), pq + f.w_off,
+                                 f.lin * sizeof(float), f.lin * sizeof(float), f.out, cudaMemcpyDefault));
+        }
+      }
+      if (j == 1)  // FC-1's bias is updated on rank 0
+        RALPB_TRY(cudaMemcpy(b, at<float>(m, 0, m->arena_off_P) + f.b_off, f.out * sizeof(float), cudaMemcpyDefault));
+    } else {
+      // RALP_MPS: later FC layers live on rank 0
+      const float* src = m->mps && (m->world == 1 || m->peers_open) ? at<float>(m, 0, m->arena_off_P) : m->P;
+      RALPB_TRY(cudaMemcpy(w, src + f.w_off, static_cast<size_t>(f.out) * f.in * sizeof(float), cudaMemcpyDefault));
+      RALPB_TRY(cudaMemcpy(b, src + f.b_off, f.out * sizeof(float), cudaMemcpyDefault));
+    }
   }
   return 0;
 }
@@ -573,6 +635,243 @@ int launch_fc_backward_weights(Model* m, const bf16* in, int R, bool update, flo
   return 0;
 }
 
+// RALP_MPS back segment (every rank): cut all-gather -> FC-0 column-parallel -> FC-1 row-parallel
+// partials reduced on rank 0 -> rank 0 runs the rest of the tail and the loss -> FC-1 output
+// gradient broadcast -> FC-1 / FC-0 backward on every rank -> cut-gradient partials
+// reduce-scattered to their workers.  The weight updates of each rank's FC slices run on the aux
+// stream.  Extension of the reference's single PS.
+int mps_back_segment(Model* m, const int32_t* lab, const bf16* cut_local, float lr, float mu, const bf16** dcut_out,
+                     bool* forked, std::string* why) {
+  cudaStream_t s = m->stream;
+  const uint32_t* seq = m->seq_dev;
+  const int W = m->world, R = m->rows_back, r = m->rank, b = m->batch, nb = static_cast<int>(m->back.size());
+  const int cut = m->cut_elems;
+  const size_t cut_bytes = static_cast<size_t>(b) * cut * sizeof(bf16);
+  FcLayer& f0 = m->back[0];
+  FcLayer& f1 = m->back[1];
+  const int ld1 = f1.ld_out;
+  // 1. labels to rank 0, cut all-gather into every rank's FC input rows
+  int32_t* lab0 = at<int32_t>(m, 0, m->arena_off_lab) + static_cast<size_t>(r) * b;
+  if (r == 0) {
+    RALPB_TRY(cudaMemcpyAsync(lab0, lab, sizeof(int32_t) * b, cudaMemcpyDeviceToDevice, s));
+  } else {
+    PeerSignal none{};
+    RALPB_TRY(push_and_signal(lab0, lab, static_cast<long long>(b) * 4 / 16, none, seq, m->counters + 1, s));
+    ++m->launches;
+    m->phys_bytes += sizeof(int32_t) * b;
+  }
+  for (int q = 0; q < W; ++q) {
+    if (q == r) continue;
+    PeerSignal sig{};
+    sig.n = 1;
+    sig.flag[0] = at<uint32_t>(m, q, m->arena_off_flags) + kFlagAct + r;
+    RALPB_TRY(push_and_signal(at<bf16>(m, q, m->arena_off_xfc) + static_cast<size_t>(r) * b * cut, cut_local,
+                              static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + 16 + q, s));
+    ++m->launches;
+    m->phys_bytes += cut_bytes;
+  }
+  {
+    PeerSignal own{};
+    own.n = 1;
+    own.flag[0] = m->flags + kFlagAct + r;
+    RALPB_TRY(signal_only(own, seq, s));
+    RALPB_TRY(wait_flags(m->flags + kFlagAct, W, seq, s));
+    m->launches += 2;
+  }
+  // 2. FC-0, column-parallel: h0s = relu(X . W0s^T + b0s)  [R][s0]
+  {
+    GemmDesc d;
+    d.M = R; d.N = m->s0; d.K = f0.in;
+    d.a = Operand2D{m->x_fc, R, f0.in, f0.in};
+    d.b = Operand2D{f0.wbf, m->s0, f0.in, f0.in};
+    if (fc_gemm(m, d, m->ld_s0, m->P + f0.b_off, 1, nullptr, 0, m->h0s, nullptr, why)) return 1;
+  }
+  // 3. FC-1, row-parallel partial: h0s . W1s^T  [R][out1] fp32 -> rank 0's slot r
+  float* p1_slots = at<float>(m, 0, m->arena_off_p1);
+  {
+    GemmDesc d;
+    d.M = R; d.N = f1.out; d.K = m->s0;
+    d.a = Operand2D{m->h0s, R, m->s0, m->ld_s0};
+    d.b = Operand2D{f1.wbf, f1.out, m->s0, m->s0};
+    float* dst = r == 0 ? p1_slots : m->p1_local;
+    if (fc_gemm(m, d, ld1, nullptr, 0, nullptr, 0, nullptr, dst, why)) return 1;
+    if (r != 0) {
+      PeerSignal sig{};
+      sig.n = 1;
+      sig.flag[0] = at<uint32_t>(m, 0, m->arena_off_flags) + kFlagP1 + r;
+      const size_t bytes = static_cast<size_t>(R) * ld1 * sizeof(float);
+      RALPB_TRY(push_and_signal(p1_slots + static_cast<size_t>(r) * R * ld1, m->p1_local,
+                                static_cast<long long>(bytes / 16), sig, seq, m->counters + 24, s));
+      ++m->launches;
+      m->phys_bytes += bytes;
+    }
+  }
+  // 4. rank 0: reduce the partials (+ b1, ReLU), the rest of the tail, the loss, and the gradient
+  //    w.r.t. FC-1's pre-activation; broadcast it
+  const bf16* dz1 = nullptr;
+  if (r == 0) {
+    if (W > 1) {
+      RALPB_TRY(wait_flags(m->flags + kFlagP1 + 1, W - 1, seq, s));
+      ++m->launches;
+    }
+    PartialSum ps{};
+    ps.n = W;
+    for (int q = 0; q < W; ++q) ps.part[q] = p1_slots + static_cast<size_t>(q) * R * ld1;
+    const FcLayer& last = m->back.back();
+    if (nb == 2) {
+      RALPB_TRY(sum_partials(ps, R, f1.out, ld1, m->P + f1.b_off, 0, nullptr, m->logits, last.ld_out, s));
+    } else {
+      RALPB_TRY(sum_partials(ps, R, f1.out, ld1, m->P + f1.b_off, 1, m->hid[1], nullptr, ld1, s));
+      // FC layers 2..: forward on rank 0
+      const bf16* x = m->hid[1];
+      long long ldx = ld1;
+      for (int j = 2; j < nb; ++j) {
+        FcLayer& f = m->back[j];
+        GemmDesc d;
+        d.M = R; d.N = f.out; d.K = f.in;
+        d.a = Operand2D{x, R, f.in, ldx};
+        d.b = Operand2D{f.wbf, f.out, f.in, f.in};
+        const bool hidden = j + 1 < nb;
+        if (fc_gemm(m, d, f.ld_out, m->P + f.b_off, hidden ? 1 : 0, nullptr, 0, hidden ? m->hid[j] : nullptr,
+                    hidden ? nullptr : m->logits, why))
+          return 1;
+        if (hidden) { x = m->hid[j]; ldx = f.ld_out; }
+      }
+    }
+    ++m->launches;
+    const float scale = 1.f / static_cast<float>(W * b);
+    RALPB_TRY(softmax_xent(m->logits, R, last.out, last.ld_out, m->labels_all, scale, m->row_loss, m->dlogits,
+                           last.ld_out, s));
+    RALPB_TRY(reduce_sum(m->row_loss, R, 1.f / static_cast<float>(R), m->loss, s));
+    m->launches += 2;
+    // backward-data through layers nb-1 .. 2 down to dz1 = dL/d(FC-1 pre-activation)
+    for (int j = nb - 1; j >= 2; --j) {
+      FcLayer& f = m->back[j];
+      const bf16* dy = j == nb - 1 ? m->dlogits : m->dyb[j];
+      GemmDesc d;
+      d.M = R; d.N = f.in; d.K = f.out;
+      d.a_mode = LD_K; d.a = Operand2D{dy, R, f.out, f.ld_out};
+      d.b_mode = LD_MN; d.b = Operand2D{f.wbf, f.out, f.in, f.in};
+      const long long ldx = m->back[j - 1].ld_out;
+      if (fc_gemm(m, d, ldx, nullptr, 0, m->hid[j - 1], ldx, m->dyb[j - 1], nullptr, why)) return 1;
+    }
+    dz1 = nb == 2 ? m->dlogits : m->dyb[1];
+    for (int q = 1; q < W; ++q) {
+      PeerSignal sig{};
+      sig.n = 1;
+      sig.flag[0] = at<uint32_t>(m, q, m->arena_off_flags) + kFlagDh1;
+      const size_t bytes = static_cast<size_t>(R) * ld1 * sizeof(bf16);
+      RALPB_TRY(push_and_signal(at<bf16>(m, q, m->arena_off_dh1), dz1, static_cast<long long>(bytes / 16), sig, seq,
+                                m->counters + 32 + q, s));
+      ++m->launches;
+      m->phys_bytes += bytes;
+    }
+  } else {
+    RALPB_TRY(wait_flags(m->flags + kFlagDh1, 1, seq, s));
+    ++m->launches;
+    dz1 = reinterpret_cast<const bf16*>(static_cast<char*>(m->arena) + m->arena_off_dh1);
+  }
+  // 5. FC-1 backward (row-parallel slice): dW1s = dz1^T h0s, dh0s = (dz1 . W1s) * relu'(h0s)
+  {
+    GemmDesc d;
+    d.M = R; d.N = m->s0; d.K = f1.out;
+    d.a_mode = LD_K; d.a = Operand2D{dz1, R, f1.out, ld1};
+    d.b_mode = LD_MN; d.b = Operand2D{f1.wbf, f1.out, m->s0, m->s0};
+    if (fc_gemm(m, d, m->ld_s0, nullptr, 0, m->h0s, m->ld_s0, m->dh0s, nullptr, why)) return 1;
+    GemmDesc w;
+    w.M = f1.out; w.N = m->s0; w.K = R;
+    w.a_mode = LD_MN; w.a = Operand2D{dz1, R, f1.out, ld1};
+    w.b_mode = LD_MN; w.b = Operand2D{m->h0s, R, m->s0, m->ld_s0};
+    w.s_m = m->s0; w.s_n = 1;
+    w.epi = EPI_F32; w.out = m->G + f1.w_off;
+    RALPB_TRY(gemm_launch(w, s, why));
+    ++m->launches;
+  }
+  // 6. FC-0 backward (column-parallel slice): db0s, dW0s = dh0s^T X, partial dX = dh0s . W0s
+  {
+    RALPB_TRY(cudaMemsetAsync(m->G + f0.b_off, 0, m->s0 * sizeof(float), s));
+    RALPB_TRY(colsum_bf16(m->dh0s, R, m->s0, m->ld_s0, m->G + f0.b_off, s));
+    GemmDesc w;
+    w.M = m->s0; w.N = f0.in; w.K = R;
+    w.a_mode = LD_MN; w.a = Operand2D{m->dh0s, R, m->s0, m->ld_s0};
+    w.b_mode = LD_MN; w.b = Operand2D{m->x_fc, R, f0.in, f0.in};
+    w.s_m = f0.in; w.s_n = 1;
+    w.epi = EPI_F32; w.out = m->G + f0.w_off;
+    RALPB_TRY(gemm_launch(w, s, why));
+    GemmDesc d;
+    d.M = R; d.N = f0.in; d.K = m->s0;
+    d.a_mode = LD_K; d.a = Operand2D{m->dh0s, R, m->s0, m->ld_s0};
+    d.b_mode = LD_MN; d.b = Operand2D{f0.wbf, m->s0, f0.in, f0.in};
+    if (fc_gemm(m, d, f0.in, nullptr, 0, nullptr, 0, nullptr, m->dxp, why)) return 1;
+    m->launches += 2;
+  }
+  // 7. reduce-scatter of the cut gradient: rows of worker q go to q's partial slot r
+  {
+    float* parts = reinterpret_cast<float*>(static_cast<char*>(m->arena) + m->arena_off_dxpart);
+    const size_t blk = static_cast<size_t>(b) * cut;
+    for (int q = 0; q < W; ++q) {
+      if (q == r) continue;
+      PeerSignal sig{};
+      sig.n = 1;
+      sig.flag[0] = at<uint32_t>(m, q, m->arena_off_flags) + kFlagDcut + r;
+      RALPB_TRY(push_and_signal(at<float>(m, q, m->arena_off_dxpart) + static_cast<size_t>(r) * blk,
+                                m->dxp + static_cast<size_t>(q) * blk, static_cast<long long>(blk * sizeof(float) / 16),
+                                sig, seq, m->counters + 40 + q, s));
+      ++m->launches;
+      m->phys_bytes += blk * sizeof(float);
+    }
+    PeerSignal own{};
+    own.n = 1;
+    own.flag[0] = m->flags + kFlagDcut + r;
+    RALPB_TRY(signal_only(own, seq, s));
+    RALPB_TRY(wait_flags(m->flags + kFlagDcut, W, seq, s));
+    PartialSum ps{};
+    ps.n = W;
+    for (int q = 0; q < W; ++q) ps.part[q] = q == r ? m->dxp + static_cast<size_t>(r) * blk : parts + static_cast<size_t>(q) * blk;
+    RALPB_TRY(sum_partials(ps, b, cut, cut, nullptr, 0, m->dcut, nullptr, cut, s));
+    m->launches += 3;
+  }
+  *dcut_out = m->dcut;
+  // 8. FC updates (this rank's slices; rank 0 also FC-1's bias and the layers after it) on the aux
+  //    stream: their weight gradients first (rank 0, layers >= 2), then SGD with the bf16 copies
+  if (r == 0) {
+    RALPB_TRY(cudaMemsetAsync(m->G + f1.b_off, 0, f1.out * sizeof(float), s));
+    RALPB_TRY(colsum_bf16(dz1, R, f1.out, ld1, m->G + f1.b_off, s));
+    ++m->launches;
+    for (int j = 2; j < nb; ++j) {
+      FcLayer& f = m->back[j];
+      const bf16* dy = j == nb - 1 ? m->dlogits : m->dyb[j];
+      RALPB_TRY(cudaMemsetAsync(m->G + f.b_off, 0, f.out * sizeof(float), s));
+      RALPB_TRY(colsum_bf16(dy, R, f.out, f.ld_out, m->G + f.b_off, s));
+      GemmDesc w;
+      w.M = f.out; w.N = f.in; w.K = R;
+      w.a_mode = LD_MN; w.a = Operand2D{dy, R, f.out, f.ld_out};
+      w.b_mode = LD_MN; w.b = Operand2D{m->hid[j - 1], R, f.in, m->back[j - 1].ld_out};
+      w.s_m = f.in; w.s_n = 1;
+      w.epi = EPI_F32; w.out = m->G + f.w_off;
+      RALPB_TRY(gemm_launch(w, s, why));
+      m->launches += 2;
+    }
+  }
+  RALPB_TRY(cudaEventRecord(m->ev_fork, s));
+  RALPB_TRY(cudaStreamWaitEvent(m->aux_stream, m->ev_fork, 0));
+  cudaStream_t su = m->aux_stream;
+  for (int j = 0; j < nb; ++j) {
+    FcLayer& f = m->back[j];
+    if (j >= 2 && r != 0) break;
+    const long long nw = static_cast<long long>(f.lout) * f.lin;
+    RALPB_TRY(sgd_momentum_bf16(m->P + f.w_off, m->V + f.w_off, m->G + f.w_off, nw, lr, mu, 1.f, f.wbf, su));
+    ++m->launches;
+    if (j != 1 || r == 0) {
+      RALPB_TRY(sgd_momentum(m->P + f.b_off, m->V + f.b_off, m->G + f.b_off, f.lout, lr, mu, 1.f, su));
+      ++m->launches;
+    }
+  }
+  RALPB_TRY(cudaEventRecord(m->ev_join, su));
+  *forked = true;
+  return 0;
+}
+
 int launch_front_backward(Model* m, const bf16* dcut, std::string* why) {
   // cur = gradient w.r.t. the output of layer i (for a conv: already ReLU-masked, i.e. the
   // pre-activation gradient); gacts[i] receives the gradient w.r.t. its input.
@@ -658,7 +957,7 @@ int relayout_weights(Model* m, bool fc_too, std::string* why) {
   }
   if (fc_too) {
     for (auto& f : m->back) {
-      RALPB_TRY(cast_bf16(m->P + f.w_off, static_cast<long long>(f.out) * f.in, f.wbf, m->stream));
+      RALPB_TRY(cast_bf16(m->P + f.w_off, static_cast<long long>(f.lout) * f.lin, f.wbf, m->stream));
       ++m->launches;
     }
   }
@@ -737,7 +1036,7 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
     RALPB_TRY(pack_input(img, b, m->in_h, m->in_w, m->in_c, a0.ptr, m->in_cp, a0.pad, s));
     ++m->launches;
   }
-  const int slot = ralp ? m->rank : 0;          // this worker's row block in the PS input
+  const int slot = ralp || m->mps ? m->rank : 0;   // this worker's row block in the PS input
   bf16* cut_dst = m->acts.back().ptr;
   if (m->holds_back) cut_dst = m->x_fc + static_cast<size_t>(slot) * b * m->cut_elems;
   for (size_t i = 0; i < m->front.size(); ++i) {
@@ -782,7 +1081,9 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   // ---------------- cut exchange + PS back segment
   const size_t cut_bytes = static_cast<size_t>(b) * m->cut_elems * sizeof(bf16);
   const bf16* dcut = nullptr;
-  if (m->holds_back) {
+  if (m->mps) {
+    if (mps_back_segment(m, lab, cut_local, lr, mu, &dcut, &fc_forked, why)) return 1;
+  } else if (m->holds_back) {
     RALPB_TRY(cudaMemcpyAsync(m->labels_all + static_cast<size_t>(slot) * b, lab, sizeof(int32_t) * b, cudaMemcpyDeviceToDevice, s));
     if (ralp && m->world > 1) {
       PeerSignal own{};
@@ -805,7 +1106,9 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
     m->launches += 2;
     m->phys_bytes += cut_bytes + sizeof(int32_t) * b;
   }
-  if (m->holds_back) {
+  if (m->mps) {
+    // the sharded FC tail ran in mps_back_segment
+  } else if (m->holds_back) {
     const int R = m->rows_back;
     const bf16* in = m->x_fc;
     if (launch_fc_forward(m, in, R, why)) return 1;
@@ -861,8 +1164,9 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   // next step (and push its cut into x_fc, which the FC wgrads read) after that sync
   if (fc_forked) RALPB_TRY(cudaStreamWaitEvent(s, m->ev_join, 0));
   if (m->strategy == RALPB_STRATEGY_RING_EXTERNAL) return 0;  // the caller all-reduces G, then apply
-  if (sync_params(m, ralp ? m->n_front : m->n_total, lr, mu, why)) return 1;
-  if (relayout_weights(m, !ralp, why)) return 1;
+  const bool placed = ralp || m->mps;
+  if (sync_params(m, placed ? m->n_front : m->n_total, lr, mu, why)) return 1;
+  if (relayout_weights(m, !placed, why)) return 1;
   return 0;
 }
 
@@ -944,7 +1248,8 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
   }
   if (on_host) RALPB_TRY(cudaEventRecord(m->ev_consumed[buf], s));
   const int slot = static_cast<int>(m->seq % Model::kLossRing);
-  if (m->holds_back) RALPB_TRY(cudaMemcpyAsync(m->loss_host + slot, m->loss, sizeof(float), cudaMemcpyDeviceToHost, s));
+  if (m->mps ? m->rank == 0 : m->holds_back)
+    RALPB_TRY(cudaMemcpyAsync(m->loss_host + slot, m->loss, sizeof(float), cudaMemcpyDeviceToHost, s));
   RALPB_TRY(cudaEventRecord(m->ev_loss[slot], s));
   m->loss_seq[slot] = m->seq;
   RALPB_TRY(cudaEventRecord(m->ev[4], s));
@@ -959,7 +1264,7 @@ int model_read_loss(Model* m, int lag, float* out, std::string* why) {
   const int slot = static_cast<int>(want % Model::kLossRing);
   if (m->loss_seq[slot] != want) { *why = "step no longer in the loss ring"; return 1; }
   RALPB_TRY(cudaEventSynchronize(m->ev_loss[slot]));
-  *out = m->holds_back ? m->loss_host[slot] : NAN;
+  *out = (m->mps ? m->rank == 0 : m->holds_back) ? m->loss_host[slot] : NAN;
   return 0;
 }
 
@@ -969,11 +1274,17 @@ int model_stats(Model* m, ralpb_step_stats* st, std::string* why) {
   if (!m->stats_valid) { *why = "no step has run"; return 1; }
   const bool ralp = m->strategy == RALPB_STRATEGY_RALP;
   float loss = NAN;
-  if (m->holds_back) RALPB_TRY(cudaMemcpy(&loss, m->loss, sizeof(float), cudaMemcpyDeviceToHost));
+  if (m->mps ? m->rank == 0 : m->holds_back) RALPB_TRY(cudaMemcpy(&loss, m->loss, sizeof(float), cudaMemcpyDeviceToHost));
   st->loss = loss;
   const long long eb = m->elem_bytes;
   const bool ring = m->strategy == RALPB_STRATEGY_RING || m->strategy == RALPB_STRATEGY_RING_EXTERNAL;
-  if (ralp)
+  if (m->mps) {
+    // volume_ralp_multi_ps (planner/costmodel.py): cut all-gather + cut-gradient reduce-scatter
+    // 2*W*(W-1)*O_cut, FC-1 partials to rank 0 + its gradient back 2*(W-1)*W*O_fc1, front sync 2*W*P_front
+    const long long W = m->world, o_cut = static_cast<long long>(m->batch) * m->cut_elems * eb;
+    const long long o_fc1 = static_cast<long long>(m->batch) * m->back[1].out * eb;
+    st->logical_bytes = 2 * W * (W - 1) * o_cut + 2 * (W - 1) * W * o_fc1 + W * 2 * m->real_front * eb;
+  } else if (ralp)
     st->logical_bytes = static_cast<long long>(m->world) * 2 * (static_cast<long long>(m->batch) * m->cut_elems * eb + m->real_front * eb);
   else if (ring)  // volume_ring: 2 * S * (W - 1) (costmodel.py:118-121)
     st->logical_bytes = 2LL * (m->world - 1) * m->real_total * eb;

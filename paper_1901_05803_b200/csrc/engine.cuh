@@ -42,7 +42,9 @@ struct FcLayer {
   int in = 0, out = 0, relu = 1;
   int ld_out = 0;                  // padded row stride (elements) of this layer's output
   long long w_off = 0, b_off = 0;
-  bf16* wbf = nullptr;             // [out][in]
+  bf16* wbf = nullptr;             // [lout][lin]
+  int lout = 0, lin = 0;           // this rank's weight block: [out][in], or a slice (RALP_MPS:
+                                   // layer 0 rows [r*s0, (r+1)*s0), layer 1 columns of that range)
 };
 
 struct Model {
@@ -103,6 +105,15 @@ struct Model {
   // peers (IPC-mapped base pointers of every rank's arena; self = arena)
   std::vector<char*> peer_base;
   bool peers_open = false;
+
+  // RALP_MPS (FC tail sharded over the ranks)
+  bool mps = false;
+  int s0 = 0, ld_s0 = 0;           // first FC layer's output slice per rank (and its padded stride)
+  bf16* h0s = nullptr;             // [R][ld_s0] this rank's slice of FC-0's output
+  bf16* dh0s = nullptr;            // [R][ld_s0] its gradient
+  float* p1_local = nullptr;       // [R][ld1] this rank's partial FC-1 pre-activation
+  float* dxp = nullptr;            // [R][cut] this rank's partial cut gradient
+  size_t arena_off_p1 = 0, arena_off_dh1 = 0, arena_off_dxpart = 0;
 
   // step state
   uint32_t seq = 0;                // host mirror of *seq_dev (steps issued)

@@ -17,7 +17,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _lib
-from .planner.costmodel import JobSpec, StrategyKind, volumes_for
+from .planner.costmodel import JobSpec, StrategyKind, volume_ralp_multi_ps, volumes_for
 from .planner.layers import LayerKind, ModelGraph
 from .report import JobReport, StepBreakdown
 
@@ -121,17 +121,24 @@ class RankExecutor:
     (any backend) so the IPC handles can be exchanged."""
 
     def __init__(self, job: JobSpec, *, rank: int = 0, world: Optional[int] = None, ps_rank: int = 0,
-                 input_shape: Optional[tuple[int, int, int]] = None, ring_backend: str = "native"):
+                 input_shape: Optional[tuple[int, int, int]] = None, ring_backend: str = "native",
+                 fc_sharding: str = "single"):
         """ring_backend (StrategyKind.RING_ALLREDUCE only): "native" = the hand-written
         reduce-scatter + SGD + all-gather over NVLink peer memory inside the step; "nccl" = the
         step stops after the backward, torch.distributed (NCCL) all-reduces the gradient vector
-        on the model stream, then the update runs (the comparison baseline)."""
+        on the model stream, then the update runs (the comparison baseline).
+        fc_sharding (StrategyKind.RALP only): "single" = the reference's single PS on rank 0;
+        "multi" = the FC tail's first two layers sharded over every GPU (RALPB_STRATEGY_RALP_MPS,
+        SURVEY.md 8f.1; logical bytes volume_ralp_multi_ps)."""
         world = job.worker_count if world is None else world
         if world != job.worker_count:
             raise ExecutorError("one rank per worker: world size must equal worker_count")
         kind = job.strategy.kind
         if ring_backend not in ("native", "nccl"):
             raise ExecutorError(f"unknown ring backend {ring_backend!r}")
+        if fc_sharding not in ("single", "multi"):
+            raise ExecutorError(f"unknown fc_sharding {fc_sharding!r}")
+        self.fc_sharding = fc_sharding if kind is StrategyKind.RALP else "single"
         self.ring_backend = ring_backend if kind is StrategyKind.RING_ALLREDUCE else None
         self.job = job
         self.model = job.model
@@ -141,7 +148,7 @@ class RankExecutor:
         self.classes = self.layers[-1]["cout"]
         split = job.strategy.split_index if kind is StrategyKind.RALP else 0
         if kind is StrategyKind.RALP:
-            strategy = _lib.RALPB_STRATEGY_RALP
+            strategy = _lib.RALPB_STRATEGY_RALP if self.fc_sharding == "single" else _lib.RALPB_STRATEGY_RALP_MPS
         elif kind is StrategyKind.RING_ALLREDUCE:
             strategy = _lib.RALPB_STRATEGY_RING if ring_backend == "native" else _lib.RALPB_STRATEGY_RING_EXTERNAL
         else:
@@ -263,14 +270,14 @@ class RankExecutor:
 
 def run_job(job: JobSpec, steps: int = 10, *, warmup: int = 0, seed: int = 0, lr: float = 0.01,
             momentum: float = 0.9, params=None, input_shape=None, name: Optional[str] = None,
-            ring_backend: str = "native") -> JobReport:
+            ring_backend: str = "native", fc_sharding: str = "single") -> JobReport:
     """Execute `job` for `steps` measured steps on this process's rank (RANK/WORLD_SIZE from the
     environment, torch.distributed already initialised when W > 1).  Returns the job report on
     every rank (rank 0's carries the loss)."""
     from . import synthetic
 
     rank = int(os.environ.get("RANK", "0"))
-    ex = RankExecutor(job, rank=rank, input_shape=input_shape, ring_backend=ring_backend)
+    ex = RankExecutor(job, rank=rank, input_shape=input_shape, ring_backend=ring_backend, fc_sharding=fc_sharding)
     try:
         if params is None:
             params = synthetic.init_params(ex.layers, seed)
@@ -278,6 +285,8 @@ def run_job(job: JobSpec, steps: int = 10, *, warmup: int = 0, seed: int = 0, lr
         b = job.model.batch_size
         records, losses = [], []
         expected = volumes_for(job).total_bytes_per_step
+        if ex.fc_sharding == "multi":
+            expected = volume_ralp_multi_ps(job.model, job.strategy.split_index, job.worker_count).total_bytes_per_step
         for t in range(warmup + steps):
             imgs, labs = synthetic.batch(seed, t, rank * b, b, ex.in_shape, ex.classes)
             ex.step(imgs, labs, lr=lr, momentum=momentum)

@@ -24,7 +24,7 @@ from oracle import step as ostep  # noqa: E402
 from paper_1901_05803_b200 import synthetic  # noqa: E402
 from paper_1901_05803_b200.executor import RankExecutor  # noqa: E402
 from paper_1901_05803_b200.planner import (JobSpec, Strategy, catalog_lookup, parse_model,  # noqa: E402
-                                           volume_baseline, volume_ralp, volume_ring)
+                                           volume_baseline, volume_ralp, volume_ralp_multi_ps, volume_ring)
 
 TINY = """model vgg_tiny batch=8 elem_bytes=4 input=32x32x3
 conv1 conv k=3 cout=64 pad=1
@@ -41,17 +41,23 @@ fc3 fc out=100
 
 
 def run(model, strategy, steps, rank, world, ring_backend="native"):
+    """strategy "ralp-mps": layer-placed with the FC tail sharded over all ranks (numerics are
+    RALP's, bytes volume_ralp_multi_ps)."""
+    fc_sharding = "single"
+    if strategy == "ralp-mps":
+        strategy, fc_sharding = "ralp", "multi"
     """strategy: "ralp", "baseline" (all-on-PS) or "ring" (ring all-reduce; numerics are the
     baseline's, bytes are volume_ring's)."""
     split = next(i for i, l in enumerate(model.layers) if l.kind.value == "fc")
     if strategy == "ralp":
-        job, expect = JobSpec(model, Strategy.ralp(split), world), volume_ralp(model, split, world)
+        job = JobSpec(model, Strategy.ralp(split), world)
+        expect = (volume_ralp_multi_ps if fc_sharding == "multi" else volume_ralp)(model, split, world)
     elif strategy == "ring":
         job, expect = JobSpec(model, Strategy.ring(), world, ps_count=0), volume_ring(model, world)
     else:
         job, expect = JobSpec(model, Strategy.baseline(), world), volume_baseline(model, world)
     expect = expect.total_bytes_per_step
-    ex = RankExecutor(job, rank=rank, world=world, ring_backend=ring_backend)
+    ex = RankExecutor(job, rank=rank, world=world, ring_backend=ring_backend, fc_sharding=fc_sharding)
     params = synthetic.init_params(ex.layers, 1)
     ex.set_params(params)
     b = model.batch_size
@@ -68,10 +74,10 @@ def run(model, strategy, steps, rank, world, ring_backend="native"):
             batches = [synthetic.batch(1, t, r * b, b, ex.in_shape, ex.classes) for r in range(world)]
             lo, wire = ostep.train_step(orc, "baseline" if strategy == "ring" else strategy, world, batches,
                                         emulate_bf16=True)
-            assert strategy == "ring" or wire == expect
+            assert strategy == "ring" or fc_sharding == "multi" or wire == expect
             rel = abs(st.loss - lo) / abs(lo)
             tol = 2e-3 if strategy == "ralp" else 0.5  # baseline/ring: rank 0 reports its own batch's loss only
-            tag = f"{strategy}-{ring_backend}" if strategy == "ring" else strategy
+            tag = f"{strategy}-{ring_backend}" if strategy == "ring" else strategy + ("-mps" if fc_sharding == "multi" else "")
             print(f"[{model.name} {tag} W={world}] step {t}: loss gpu {st.loss:.6f} oracle {lo:.6f} "
                   f"rel {rel:.2e} ms {st.ms_step:.2f} phys {st.physical_bytes}", flush=True)
             if rel > tol:
@@ -83,7 +89,7 @@ def run(model, strategy, steps, rank, world, ring_backend="native"):
         if p is None:
             continue
         if strategy == "ralp" and li >= split:
-            continue
+            continue   # FC tail: on the PS (single) or sliced over the ranks (multi)
         t = torch.from_numpy(np.ascontiguousarray(p[0])).cuda()
         ref = t.clone()
         dist.broadcast(ref, 0)
@@ -111,7 +117,8 @@ def main():
     cifar = catalog_lookup("cifar_small").with_batch_size(32)
     for model, strategy, steps, backend in [(cifar, "ralp", 4, "native"), (parse_model(TINY), "ralp", 3, "native"),
                                             (cifar, "baseline", 3, "native"), (cifar, "ring", 3, "native"),
-                                            (cifar, "ring", 3, "nccl")]:
+                                            (cifar, "ring", 3, "nccl"), (cifar, "ralp-mps", 4, "native"),
+                                            (parse_model(TINY), "ralp-mps", 3, "native")]:
         ok &= run(model, strategy, steps, rank, world, backend)
     flag = torch.tensor([0 if ok else 1], device="cuda")
     dist.all_reduce(flag)

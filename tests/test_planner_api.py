@@ -134,3 +134,18 @@ def test_catalog_override(tmp_path, monkeypatch):
     with pytest.raises(P.UnknownModelError):
         P.catalog_lookup("vgg16")
     assert P.catalog_lookup("tiny").num_layers == 3
+
+
+def test_volume_ralp_multi_ps_extension():
+    """The multi-PS extension: cut all-gather + cut-gradient reduce-scatter,
+    row-parallel partials of the second FC layer to the PS and its gradient back, conv sync."""
+    from paper_1901_05803_b200.planner import catalog_lookup, volume_ralp, volume_ralp_multi_ps
+    m = catalog_lookup("vgg16").with_batch_size(128)
+    for w in (1, 2, 4, 8):
+        v = volume_ralp_multi_ps(m, 18, w)
+        cut = m.output_bytes(18)
+        fc2 = m.output_bytes(20)
+        assert v.activation_bytes == 2 * w * (w - 1) * cut + 2 * (w - 1) * w * fc2
+        assert v.parameter_sync_bytes == volume_ralp(m, 18, w).parameter_sync_bytes
+        assert v.total_bytes_per_step == v.activation_bytes + v.parameter_sync_bytes
+    assert volume_ralp_multi_ps(m, 18, 1).activation_bytes == 0
