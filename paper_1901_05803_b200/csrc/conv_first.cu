@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(32 * (kProd + 5), 1) conv_first_fwd_kernel(con
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait_and_release();
 
   if (warp < kProd) {
     produce_tiles(p, sA, a_full, a_empty);
@@ -242,6 +243,7 @@ __global__ void __launch_bounds__(32 * (kProd + 2), 1) conv_first_wgrad_kernel(c
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait_and_release();
 
   if (warp < kProd) {
     produce_tiles(p, sP, full, empty);
@@ -330,7 +332,7 @@ cudaError_t conv_first_fwd(const float* img, int n, int h, int w, int cin, const
   const int smem = 1024 + 4096 + kStages * 8192 + 2 * 16384 + 256;
   const int grid = std::min(p.total, num_sms());
   cudaFuncSetAttribute(conv_first_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  launch_timed([&] { conv_first_fwd_kernel<<<grid, 32 * (kProd + 5), smem, s>>>(p); }, s, KIND_FIRST_FWD,
+  launch_timed([&] { static_cast<void>(launch_pdl(conv_first_fwd_kernel, dim3(grid), dim3(32 * (kProd + 5)), smem, s, 1, p)); }, s, KIND_FIRST_FWD,
                2.0 * n * h * w * 27.0 * 64.0);
   return cudaGetLastError();
 }
@@ -343,7 +345,7 @@ cudaError_t conv_first_wgrad(const float* img, int n, int h, int w, int cin, con
   const int smem = 1024 + kStages * (16384 + 8192) + 256;
   const int grid = std::min(p.total, num_sms());
   cudaFuncSetAttribute(conv_first_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  launch_timed([&] { conv_first_wgrad_kernel<<<grid, 32 * (kProd + 2), smem, s>>>(p); }, s, KIND_FIRST_WGRAD,
+  launch_timed([&] { static_cast<void>(launch_pdl(conv_first_wgrad_kernel, dim3(grid), dim3(32 * (kProd + 2)), smem, s, 1, p)); }, s, KIND_FIRST_WGRAD,
                2.0 * n * h * w * 27.0 * 64.0);
   return cudaGetLastError();
 }

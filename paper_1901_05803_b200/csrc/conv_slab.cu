@@ -189,19 +189,7 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
   auto go = [&](auto kern, int threads, bool cluster) {
     static_cast<void>(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     launch_timed([&] {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(grid);
-      cfg.blockDim = dim3(threads);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = s;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = cluster ? 2 : 1;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      static_cast<void>(cudaLaunchKernelEx(&cfg, kern, p));
+      static_cast<void>(launch_pdl(kern, dim3(grid), dim3(threads), smem, s, cluster ? 2 : 1, p));
     }, s, cluster ? KIND_CONV_FWD_PAIR : KIND_CONV_FWD, 2.0 * g.n * g.h * g.w * static_cast<double>(g.taps()) * c * cout);
     launched = true;
   };
@@ -267,7 +255,7 @@ cudaError_t conv_slab_wgrad(const ConvGeom& g, const void* x_pad, const void* dy
     const int clusters = static_cast<int>(std::min<long long>(units2, num_sms() / 2));
     auto go2 = [&](auto kern) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      launch_timed([&] { kern<<<2 * clusters, 256, smem2, s>>>(p); }, s, KIND_WGRAD_PAIR,
+      launch_timed([&] { static_cast<void>(launch_pdl(kern, dim3(2 * clusters), dim3(256), smem2, s, 1, p)); }, s, KIND_WGRAD_PAIR,
                    2.0 * g.n * g.h * g.w * static_cast<double>(g.taps()) * g.cin * g.cout);
     };
     if (bh == 14) go2(conv_slab_wgrad_pair_kernel<14>); else go2(conv_slab_wgrad_pair_kernel<16>);
@@ -277,7 +265,7 @@ cudaError_t conv_slab_wgrad(const ConvGeom& g, const void* x_pad, const void* dy
   }
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    launch_timed([&] { kern<<<grid, 256, smem, s>>>(p); }, s, KIND_WGRAD,
+    launch_timed([&] { static_cast<void>(launch_pdl(kern, dim3(grid), dim3(256), smem, s, 1, p)); }, s, KIND_WGRAD,
                  2.0 * g.n * g.h * g.w * static_cast<double>(g.taps()) * g.cin * g.cout);
   };
   if (bh == 14) go(conv_slab_wgrad_kernel<14>); else go(conv_slab_wgrad_kernel<16>);

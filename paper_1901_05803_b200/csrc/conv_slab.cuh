@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
   }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait_and_release();
   const int total = p.n * p.n_hb * p.n_wb * p.n_nt;
   const int cblks = p.c / p.kb;
   const int ksteps = p.kb / 16;
@@ -471,6 +472,7 @@ __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait_and_release();
   const int PB = p.n_pix_blocks;
   const long long units = static_cast<long long>(p.n_ci_blocks) * p.n_co_blocks * PB;
   const long long u_begin = units * blockIdx.x / gridDim.x;
@@ -636,6 +638,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait_and_release();
   const int PB = p.n_pix_blocks;
   const long long units = static_cast<long long>(p.n_ci_blocks) * p.n_co_blocks * PB;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;

@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, tmem_cols);
+  pdl_wait_and_release();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();

@@ -58,6 +58,14 @@ static bool encode_2d(CUtensorMap* tm, const Operand2D& op, int box_cols, int bo
 
 static bool is_k(int mode) { return mode == LD_K || mode == LD_K_CONV; }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("RALPB_PDL");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on;
+}
+
 cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why) {
   static bool attr_set = false;
   if (d.M <= 0 || d.N <= 0 || d.K <= 0) return cudaSuccess;
@@ -173,7 +181,8 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
   }
   const long long total = static_cast<long long>(p.n_mt) * p.n_nt * p.n_ks;
   const int grid = static_cast<int>(std::min<long long>(total, sms));
-  launch_timed([&] { gemm_sm100_kernel<<<grid, kThreads, smem, stream>>>(p); }, stream, KIND_GEMM,
+  launch_timed([&] { static_cast<void>(launch_pdl(gemm_sm100_kernel, dim3(grid), dim3(kThreads), smem, stream, 1, p)); },
+               stream, KIND_GEMM,
                2.0 * d.M * d.N * static_cast<double>(d.K));
   return cudaGetLastError();
 }

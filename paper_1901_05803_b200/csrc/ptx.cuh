@@ -164,6 +164,15 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Kernels launched with the programmatic-stream-serialization attribute (launch_pdl) may start
+// while their predecessor drains: they set up shared memory / barriers / TMEM, then wait here
+// before touching global memory, and immediately let their own successor start its setup.
+__device__ __forceinline__ void pdl_wait_and_release() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- TMA store / proxy fences
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
