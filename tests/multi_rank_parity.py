@@ -41,13 +41,12 @@ fc3 fc out=100
 
 
 def run(model, strategy, steps, rank, world, ring_backend="native"):
-    """strategy "ralp-mps": layer-placed with the FC tail sharded over all ranks (numerics are
-    RALP's, bytes volume_ralp_multi_ps)."""
+    """strategy: "ralp", "baseline" (all-on-PS), "ring" (ring all-reduce; numerics are the
+    baseline's, bytes are volume_ring's) or "ralp-mps" (layer-placed with the FC tail sharded
+    over all ranks; numerics are RALP's, bytes volume_ralp_multi_ps)."""
     fc_sharding = "single"
     if strategy == "ralp-mps":
         strategy, fc_sharding = "ralp", "multi"
-    """strategy: "ralp", "baseline" (all-on-PS) or "ring" (ring all-reduce; numerics are the
-    baseline's, bytes are volume_ring's)."""
     split = next(i for i, l in enumerate(model.layers) if l.kind.value == "fc")
     if strategy == "ralp":
         job = JobSpec(model, Strategy.ralp(split), world)
