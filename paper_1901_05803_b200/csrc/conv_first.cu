@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(32 * (kProd + 5), 1) conv_first_fwd_kernel(con
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  pdl_wait_and_release();   // the filters are written by the previous step's update
   load_filters(p, sB);
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
@@ -146,7 +147,6 @@ __global__ void __launch_bounds__(32 * (kProd + 5), 1) conv_first_fwd_kernel(con
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait_and_release();
 
   if (warp < kProd) {
     produce_tiles(p, sA, a_full, a_empty);
