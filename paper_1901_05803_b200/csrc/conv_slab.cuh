@@ -257,12 +257,32 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
     int acc = 0, ob = 0;
     uint32_t acc_ph = 0;
     uint8_t* stage = sOut + g * 2 * 8192;
+    // ReLU-mask rows (backward-data) are fetched one 32-channel chunk ahead -- the first chunk
+    // of a work item before its accumulator is waited on -- so the global-load latency hides
+    // behind the MMAs / the previous chunk instead of stalling every chunk of the epilogue.
+    const bool use_mask = p.mask != nullptr;
+    uint4 mk[4];
+    auto mask_fetch = [&](int img_, int hb_, int wb_, int nt_, int a_, int c_) {
+      const int hh_ = (hb_ * NCTA + static_cast<int>(rank)) * mrows + a_ * 16 + (m >> 3);
+      const int ww_ = wb_ * 8 + (m & 7);
+      const int n0_ = nt_ * p.bn + c_;
+      if (hh_ < p.h && ww_ < p.w && n0_ + 32 <= p.cout) {
+        const uint4* mp = reinterpret_cast<const uint4*>(
+            p.mask + ((static_cast<long long>(img_) * p.hp + hh_ + p.pad) * p.wp + ww_ + p.pad) * p.cout + n0_);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mk[j] = __ldg(mp + j);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mk[j] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    };
     for (int wi = w_first; wi < total; wi += w_step) {
       int t = wi;
       const int nt = t % p.n_nt; t /= p.n_nt;
       const int wb = t % p.n_wb; t /= p.n_wb;
       const int hb = t % p.n_hb;
       const int img = t / p.n_hb;
+      if (use_mask) mask_fetch(img, hb, wb, nt, g, 0);
       mbar_wait(&tfull[acc], acc_ph);
       tc_fence_after();
       for (int a = g; a < p.macc; a += EWG) {
@@ -273,6 +293,14 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
         const long long orow = (static_cast<long long>(img) * p.hp + hh + p.pad) * p.wp + ww + p.pad;
         const uint32_t tb = tmem_base + (acc * p.macc + a) * p.bn + (static_cast<uint32_t>(q * 32) << 16);
         for (int c = 0; c < p.bn; c += 32) {
+          uint4 cur[4];
+          if (use_mask) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) cur[j] = mk[j];
+            const int c2 = c + 32 < p.bn ? c + 32 : 0;
+            const int a2 = c + 32 < p.bn ? a : a + EWG;
+            if (a2 < p.macc) mask_fetch(img, hb, wb, nt, a2, c2);
+          }
           uint32_t rr[32];
           tmem_ld32(tb + c, rr);
           tmem_wait_ld();
@@ -303,7 +331,7 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
             if (full) {
 #pragma unroll
               for (int j4 = 0; j4 < 4; ++j4) {
-                uint4 u = *reinterpret_cast<const uint4*>(mp + j4 * 8);
+                const uint4 u = cur[j4];
                 const __nv_bfloat16* hb2 = reinterpret_cast<const __nv_bfloat16*>(&u);
 #pragma unroll
                 for (int e = 0; e < 8; ++e)
