@@ -62,6 +62,12 @@ bool encode_act(CUtensorMap* tm, const void* ptr, long long c, long long wp, lon
                 int bh, int swz, std::string* why);
 bool encode_mat(CUtensorMap* tm, const void* ptr, long long rows, long long cols, int bc, int br, int swz,
                 std::string* why);
+// Interior view of a padded activation (pixel (pad, pad) onward, clipped at the image edge),
+// box {32, bw, bh, 1}, 64-byte swizzle: TMA stores through it never touch the zero borders.
+bool encode_interior(CUtensorMap* tm, void* ptr, long long c, long long w, long long h, long long wp, long long hp,
+                     long long n, int pad, std::string* why);
+bool encode_interior_box(CUtensorMap* tm, void* ptr, long long c, long long w, long long h, long long wp, long long hp,
+                         long long n, int pad, int bw, int bh, std::string* why);
 
 // First (RGB) convolution fused with its im2col (conv_first.cu): 3x3/1/pad 1, cin = 3,
 // 64 output channels, h % 8 == 0, w % 16 == 0.  img: fp32 NHWC; wf: [64][32] bf16 with the bias
@@ -75,6 +81,12 @@ cudaError_t conv_first_wgrad(const float* img, int n, int h, int w, int cin, con
 // Slab-tiled kernels (conv_slab.cu).  `c` = contracted channels, `cout` = produced channels.
 bool slab_fwd_ok(const ConvGeom& g, int c, int cout);
 bool slab_wgrad_ok(const ConvGeom& g);
+// Row-streamed 64 -> 64 channel 3x3 kernel (conv_row.cu), used by conv_slab_fwd when it applies
+// (RALPB_ROW64=0 disables).
+bool row64_ok(const ConvGeom& g, int c, int cout, const void* pool_idx);
+cudaError_t conv_row64_fwd(const ConvGeom& g, const void* x_pad, const void* w, const float* bias, int relu,
+                           const void* mask_pad, void* y_pad, float* colsum, void* pool_out, int pool_pad,
+                           cudaStream_t s, std::string* why);
 cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, int c, int cout, const float* bias,
                           int relu, const void* mask_pad, void* y_pad, float* colsum, cudaStream_t s,
                           std::string* why, void* pool_out = nullptr, int pool_pad = 0, void* pool_idx = nullptr);

@@ -57,12 +57,17 @@ bool encode_mat(CUtensorMap* tm, const void* ptr, long long rows, long long cols
 // clip at the image edge, so the zero borders are never written.
 bool encode_interior(CUtensorMap* tm, void* ptr, long long c, long long w, long long h, long long wp, long long hp,
                      long long n, int pad, std::string* why) {
+  return encode_interior_box(tm, ptr, c, w, h, wp, hp, n, pad, 8, 16, why);
+}
+
+bool encode_interior_box(CUtensorMap* tm, void* ptr, long long c, long long w, long long h, long long wp, long long hp,
+                         long long n, int pad, int bw, int bh, std::string* why) {
   char* base = static_cast<char*>(ptr) + (static_cast<long long>(pad) * wp + pad) * c * 2;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w), static_cast<cuuint64_t>(h),
                         static_cast<cuuint64_t>(n)};
   cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * 2, static_cast<cuuint64_t>(wp * c) * 2,
                            static_cast<cuuint64_t>(hp * wp * c) * 2};
-  cuuint32_t box[4] = {32, 8, 16, 1};
+  cuuint32_t box[4] = {32, static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh), 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = encoder()(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -92,6 +97,8 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
                           int relu, const void* mask_pad, void* y_pad, float* colsum, cudaStream_t s,
                           std::string* why, void* pool_out, int pool_pad, void* pool_idx) {
   if (pool_out != nullptr && (g.h % 2 != 0 || g.w % 2 != 0)) { *why = "fused pool needs even h, w"; return cudaErrorInvalidValue; }
+  if (row64_ok(g, c, cout, pool_idx))   // 64 -> 64 channels: row-streamed kernel (conv_row.cu)
+    return conv_row64_fwd(g, x_pad, w, bias, relu, mask_pad, y_pad, colsum, pool_out, pool_pad, s, why);
   if (colsum != nullptr && cout > 512) { *why = "slab conv: fused colsum supports <= 512 channels"; return cudaErrorInvalidValue; }
   SlabConvParams p;
   std::memset(&p, 0, sizeof(p));

@@ -23,17 +23,6 @@
 
 namespace ralpb {
 
-// 4-D box load from a padded activation viewed as [n][hp][wp][c]; rows/cols beyond the
-// image (or the tensor) are zero-filled by TMA, so partial pixel tiles contribute nothing.
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1,
-                                            int c2, int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
-}
-
 constexpr int kSlabMaxTaps = 25;
 #ifndef RALPB_B_PRODUCERS
 #define RALPB_B_PRODUCERS 2

@@ -49,13 +49,13 @@ def conv_fwd(x_pad, w, bias, *, n, h, w_, cin, cout, k, pad, relu=True, out=None
     return out
 
 
-def conv_fwd_pool(x_pad, w, bias, *, n, h, w_, cin, cout, k, pad, relu=True, pool_pad=1):
-    """(y, pooled, argmax bytes): conv fwd and its 2x2/2 max pool from one kernel."""
+def conv_fwd_pool(x_pad, w, bias, *, n, h, w_, cin, cout, k, pad, relu=True, pool_pad=1, with_idx=True):
+    """(y, pooled, argmax bytes or None): conv fwd and its 2x2/2 max pool from one kernel."""
     y = torch.zeros(n, h + 2 * pad, w_ + 2 * pad, cout, dtype=_BF16, device=x_pad.device)
     pooled = torch.zeros(n, h // 2 + 2 * pool_pad, w_ // 2 + 2 * pool_pad, cout, dtype=_BF16, device=x_pad.device)
-    idx = torch.empty(n, h // 2, w_ // 2, cout, dtype=torch.uint8, device=x_pad.device)
+    idx = torch.empty(n, h // 2, w_ // 2, cout, dtype=torch.uint8, device=x_pad.device) if with_idx else None
     call("ralpb_conv_fwd_pool", x_pad.data_ptr(), w.data_ptr(), _p(bias), y.data_ptr(), pooled.data_ptr(), pool_pad,
-         idx.data_ptr(), n, h, w_, cin, cout, k, pad, int(relu), _stream())
+         _p(idx), n, h, w_, cin, cout, k, pad, int(relu), _stream())
     return y, pooled, idx
 
 

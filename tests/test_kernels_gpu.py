@@ -70,6 +70,10 @@ CONV_CASES = [
     (2, 56, 56, 128, 256, 3, 1),
     (3, 30, 17, 64, 128, 3, 1),
     (1, 112, 112, 64, 64, 3, 1),
+    # 64 -> 64 at w >= 128: the row-streamed kernel (conv_row.cu); 160 = 128 + a shifted block
+    (2, 224, 224, 64, 64, 3, 1),
+    (1, 130, 160, 64, 64, 3, 1),
+    (3, 36, 128, 64, 64, 3, 1),
 ]
 
 
@@ -302,3 +306,25 @@ def test_conv_fwd_fused_pool(case):
     ref_dx = ops.maxpool_bwd(y, dy, n=n, h=h, w=w, c=cout, pad_in=pad, k=2, stride=2, pad_out=0)
     torch.testing.assert_close(dx.float(), ref_dx.float(), rtol=0, atol=0)
     torch.testing.assert_close(colsum, dx.float().sum(dim=(0, 1, 2)), rtol=1e-5, atol=1e-4)
+
+
+@pytest.mark.parametrize("case", [(2, 224, 224), (1, 130, 160), (3, 36, 128)])
+def test_row64_fused_pool(case):
+    """The row-streamed 64->64 kernel with the fused 2x2/2 pool (no argmax bytes), against torch."""
+    n, h, w = case
+    g = torch.Generator(device=DEV).manual_seed(21)
+    x = _pad(_bf(n, h, w, 64, gen=g), 1).contiguous()
+    wt = _bf(64, 9, 64, scale=(2.0 / 576) ** 0.5, gen=g)
+    bias = torch.randn(64, device=DEV) * 0.1
+    y, pooled, idx = ops.conv_fwd_pool(x, wt, bias, n=n, h=h, w_=w, cin=64, cout=64, k=3, pad=1, pool_pad=1,
+                                       with_idx=False)
+    assert idx is None
+    xr = x[:, 1:1 + h, 1:1 + w, :].permute(0, 3, 1, 2).float()
+    ref = torch.relu(F.conv2d(xr, wt.float().view(64, 3, 3, 64).permute(0, 3, 1, 2), bias, padding=1))
+    _close(y[:, 1:1 + h, 1:1 + w, :], ref.permute(0, 2, 3, 1))
+    yi = y[:, 1:1 + h, 1:1 + w, :].permute(0, 3, 1, 2).float()
+    torch.testing.assert_close(pooled[:, 1:-1, 1:-1, :].float(), F.max_pool2d(yi, 2).permute(0, 2, 3, 1), rtol=0, atol=0)
+    for t, inner in ((y, (1, 1 + h, 1, 1 + w)), (pooled, (1, 1 + h // 2, 1, 1 + w // 2))):
+        b = t.clone()
+        b[:, inner[0]:inner[1], inner[2]:inner[3], :] = 0
+        assert b.abs().max().item() == 0.0
