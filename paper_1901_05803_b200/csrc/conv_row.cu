@@ -163,18 +163,24 @@ __global__ void __launch_bounds__(kRowThreads, 1) conv_row64_kernel(const __grid
         mbar_wait(&a_full[as], aph);
         tc_fence_after();
         const uint64_t ad = desc_add(a0, as * kRowStage);
+        // at most two UMMAs per (kc, k-step): taps lo .. lo+c1-1 into slots s1.., the rest
+        // (c2, after the window wraps) from slot 0; everything below is per input row, so the
+        // 12 x (1|2) issues use compile-time descriptor offsets only (a descriptor computed per
+        // MMA costs ~100 issue cycles; tools/exp_mma.cu)
+        const int s1 = row_slot(G + j - lo);
+        const int c1 = min(hi - lo + 1, 8 - s1), c2 = hi - lo + 1 - c1;
+        const uint32_t d1 = tmem_base + s1 * 64, d2 = tmem_base;
+        const uint32_t id1 = idesc0 | (static_cast<uint32_t>(8 * c1) << 17);
+        const uint32_t id2 = idesc0 | (static_cast<uint32_t>(8 * (c2 > 0 ? c2 : 1)) << 17);
+        const uint64_t bd1 = desc_add(b0, lo * kTapBytes), bd2 = desc_add(b0, (lo + c1) * kTapBytes);
         if (elect_one()) {
 #pragma unroll
           for (int kc = 0; kc < 3; ++kc)
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {
               const uint64_t ada = desc_add(ad, kc * 128 + ks * 32);
-              for (int k = lo; k <= hi;) {
-                const int s = row_slot(G + j - k);
-                const int cnt = min(hi - k + 1, 8 - s);
-                umma_bf16(tmem_base + s * 64, ada, desc_add(b0, (kc * 3 + k) * kTapBytes + ks * 32), idesc0 | (static_cast<uint32_t>(8 * cnt) << 17), 1u);
-                k += cnt;
-              }
+              umma_bf16(d1, ada, desc_add(bd1, kc * 3 * kTapBytes + ks * 32), id1, 1u);
+              if (c2 > 0) umma_bf16(d2, ada, desc_add(bd2, kc * 3 * kTapBytes + ks * 32), id2, 1u);
             }
           umma_commit(&a_empty[as]);
           if (j >= 2) umma_commit(&tfull[row_slot(G + j - 2)]);
