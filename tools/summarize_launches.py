@@ -14,7 +14,7 @@ import json
 import re
 from collections import OrderedDict, defaultdict
 
-TENSOR = re.compile(r"conv_slab_(fwd|wgrad)\w*_kernel|conv_first_\w+_kernel|gemm_sm100_kernel")
+TENSOR = re.compile(r"conv_slab_(fwd|wgrad)\w*_kernel|conv_row64_kernel|conv_first_\w+_kernel|gemm_sm100_kernel")
 
 
 def kind_of(name: str) -> str:
@@ -23,6 +23,8 @@ def kind_of(name: str) -> str:
         return "conv_wgrad_pair"
     if "conv_slab_wgrad" in name:
         return "conv_wgrad"
+    if "conv_row64" in name:
+        return "conv_fwd"
     if "conv_slab_fwd" in name:
         return "conv_fwd_pair" if re.search(r"\(bool\)1|, 1>|,\s*true>", name) else "conv_fwd"
     if "conv_first_fwd" in name:
