@@ -40,9 +40,15 @@ namespace {
 constexpr int kRowPx = 128;                 // pixels per M tile (one row segment)
 constexpr int kRowIn = kRowPx + 2;          // input pixels per row stage (3 horizontal taps)
 constexpr int kRowStage = 17408;            // 130 x 128 B, 1 KB aligned
-constexpr int kRowStages = 5;
 constexpr int kTapBytes = 64 * 128;         // one filter tap: 64 out x 64 in bf16
 constexpr int kRowThreads = 384;
+// CTA-pair filter layout (per horizontal tap kc, 40 KB): every UMMA shape the issue loop
+// uses -- N = 192 (kr 0-2), 128 (kr 0-1 or 1-2), 64 (one kr) -- has its own region at the
+// same offset in both CTAs, holding the half of its N filter rows that CTA supplies.
+constexpr int kPairKcBytes = 40960;
+__host__ __device__ constexpr int pair_region(int lo, int cnt) {
+  return cnt == 3 ? 0 : cnt == 2 ? (lo == 0 ? 12288 : 20480) : 28672 + lo * 4096;
+}
 
 struct alignas(64) RowConvParams {
   CUtensorMap tmX;    // padded input [n][hp][wp][64], box {64, 130, 1, 1}, SW128
@@ -74,10 +80,13 @@ struct RowUnit {
   int img, r0, rows, x0, cb;
 };
 
-__device__ __forceinline__ RowUnit row_unit(const RowConvParams& p, int u) {
+// single CTA: unit = (image, strip, column block); CTA pair: unit = (image, strip) and CTA r
+// takes column block r (n_cb == 2)
+template <bool PAIR>
+__device__ __forceinline__ RowUnit row_unit(const RowConvParams& p, int u, uint32_t rank) {
   RowUnit r;
-  r.cb = u % p.n_cb;
-  const int t = u / p.n_cb;
+  r.cb = PAIR ? static_cast<int>(rank) : u % p.n_cb;
+  const int t = PAIR ? u : u / p.n_cb;
   const int strip = t % p.n_strips;
   r.img = t / p.n_strips;
   r.r0 = strip * p.rows;
@@ -86,11 +95,14 @@ __device__ __forceinline__ RowUnit row_unit(const RowConvParams& p, int u) {
   return r;
 }
 
+template <bool PAIR>
 __global__ void __launch_bounds__(kRowThreads, 1) conv_row64_kernel(const __grid_constant__ RowConvParams p) {
+  constexpr int kRowStages = PAIR ? 4 : 5;
+  constexpr int NCTA = PAIR ? 2 : 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sB = smem;                              // 9 taps, ordered (kc, kr)
-  uint8_t* sA = sB + 9 * kTapBytes;                // kRowStages input rows
+  uint8_t* sB = smem;                              // single: 9 taps ordered (kc, kr); pair: 3 x 40 KB
+  uint8_t* sA = sB + (PAIR ? 3 * kPairKcBytes : 9 * kTapBytes);   // kRowStages input rows
   uint8_t* sOut = sA + kRowStages * kRowStage;     // 2 warpgroups x 2 x 8 KB staging
   uint64_t* a_full = reinterpret_cast<uint64_t*>(sOut + 2 * 2 * 8192);
   uint64_t* a_empty = a_full + kRowStages;
@@ -101,19 +113,30 @@ __global__ void __launch_bounds__(kRowThreads, 1) conv_row64_kernel(const __grid
   float* s_col = reinterpret_cast<float*>(tmem_slot + 4);   // [64]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const int u_first = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int u_step = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+  // barriers gating the issuer: own (single CTA) or CTA 0's (pair), as shared::cluster addresses
+  auto lead = [&](uint64_t* bar) { return PAIR ? mapa_shared(smem_u32(bar), 0) : smem_u32(bar); };
   if (threadIdx.x < 64) s_col[threadIdx.x] = 0.f;
   if (threadIdx.x == 0) {
     tma_prefetch(&p.tmX);
     tma_prefetch(&p.tmW);
     tma_prefetch(&p.tmY);
     for (int i = 0; i < kRowStages; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
-    for (int i = 0; i < 8; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128); }
+    for (int i = 0; i < 8; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128 * NCTA); }
     mbar_init(bfull, 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) {
+    if (warp == 2) tmem_alloc_pair(tmem_slot, 512);
+    tc_fence_before();
+    cluster_sync();
+  } else {
+    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (warp >= 4) {   // every slot starts at zero (UMMAs always accumulate)
@@ -122,38 +145,65 @@ __global__ void __launch_bounds__(kRowThreads, 1) conv_row64_kernel(const __grid
     for (int c = wg * 256; c < wg * 256 + 256; c += 32) tmem_st32_zero(tmem_base + lanes + c);
     tmem_wait_st();
   }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
   pdl_wait_and_release();
+  // resident filters (each CTA its own copy / half), then one barrier over the CTA (pair:
+  // the cluster -- CTA 0's UMMAs read CTA 1's filters and write CTA 1's zeroed TMEM)
+  if (threadIdx.x == 0) {
+    if constexpr (PAIR) {
+      mbar_expect_tx(bfull, 3 * kPairKcBytes);
+      auto chunk = [&](int kc, int off, int kr, int half) {
+        tma_load_2d(sB + kc * kPairKcBytes + off, &p.tmW, bfull, (kr * 3 + kc) * 64, half * 32);
+      };
+      const int r = static_cast<int>(rank);
+      for (int kc = 0; kc < 3; ++kc) {
+        // N=192: rows [W0; W1lo] | [W1hi; W2]
+        if (r == 0) { chunk(kc, 0, 0, 0); chunk(kc, 4096, 0, 1); chunk(kc, 8192, 1, 0); }
+        else        { chunk(kc, 0, 1, 1); chunk(kc, 4096, 2, 0); chunk(kc, 8192, 2, 1); }
+        // N=128 kr 0-1: W0 | W1; kr 1-2: W1 | W2
+        chunk(kc, pair_region(0, 2), r, 0); chunk(kc, pair_region(0, 2) + 4096, r, 1);
+        chunk(kc, pair_region(1, 2), 1 + r, 0); chunk(kc, pair_region(1, 2) + 4096, 1 + r, 1);
+        // N=64: Wkr rows [32r, 32r + 32)
+        for (int kr = 0; kr < 3; ++kr) chunk(kc, pair_region(kr, 1), kr, r);
+      }
+    } else {
+      mbar_expect_tx(bfull, 9 * kTapBytes);
+      for (int kc = 0; kc < 3; ++kc)
+        for (int kr = 0; kr < 3; ++kr) {
+          tma_load_2d(sB + (kc * 3 + kr) * kTapBytes, &p.tmW, bfull, (kr * 3 + kc) * 64, 0);
+          tma_load_2d(sB + (kc * 3 + kr) * kTapBytes + 4096, &p.tmW, bfull, (kr * 3 + kc) * 64, 32);
+        }
+    }
+  }
+  mbar_wait(bfull, 0);
+  tc_fence_before();
+  if constexpr (PAIR) cluster_sync(); else __syncthreads();
+  tc_fence_after();
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(bfull, 9 * kTapBytes);
-      for (int kc = 0; kc < 3; ++kc)
-        for (int kr = 0; kr < 3; ++kr) tma_load_2d(sB + (kc * 3 + kr) * kTapBytes, &p.tmW, bfull, (kr * 3 + kc) * 64, 0);
       int as = 0;
       uint32_t aph = 0;
-      for (int u = blockIdx.x; u < p.total; u += gridDim.x) {
-        const RowUnit ru = row_unit(p, u);
+      for (int u = u_first; u < p.total; u += u_step) {
+        const RowUnit ru = row_unit<PAIR>(p, u, rank);
         for (int j = 0; j < ru.rows + 2; ++j) {   // padded input rows r0 .. r0 + rows + 1
           mbar_wait(&a_empty[as], aph ^ 1);
-          mbar_expect_tx(&a_full[as], kRowIn * 128);
-          tma_load_4d(sA + as * kRowStage, &p.tmX, &a_full[as], 0, ru.x0, ru.r0 + j, ru.img);
+          if (rank == 0) mbar_expect_tx(&a_full[as], NCTA * kRowIn * 128);
+          if constexpr (PAIR)
+            tma_load_4d_pair(sA + as * kRowStage, &p.tmX, lead(&a_full[as]), 0, ru.x0, ru.r0 + j, ru.img);
+          else
+            tma_load_4d(sA + as * kRowStage, &p.tmX, &a_full[as], 0, ru.x0, ru.r0 + j, ru.img);
           if (++as == kRowStages) { as = 0; aph ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
-    mbar_wait(bfull, 0);
-    tc_fence_after();
+  } else if (warp == 1 && rank == 0) {
     const uint64_t a0 = umma_smem_desc(smem_u32(sA), 16, 1024, 128);
     const uint64_t b0 = umma_smem_desc(smem_u32(sB), 16, 1024, 128);
-    const uint32_t idesc0 = umma_idesc_bf16(128, 0, false, false);   // | (N >> 3) << 17 below
+    const uint32_t idesc0 = umma_idesc_bf16(128 * NCTA, 0, false, false);   // | (N >> 3) << 17 below
     int as = 0, G = 0;
     uint32_t aph = 0;
-    for (int u = blockIdx.x; u < p.total; u += gridDim.x) {
-      const int R = row_unit(p, u).rows;
+    for (int u = u_first; u < p.total; u += u_step) {
+      const int R = row_unit<PAIR>(p, u, rank).rows;
       for (int j = 0; j < R + 2; ++j) {
         const int lo = max(0, j - R + 1), hi = min(2, j);
         if (j < R && G + j >= 8) {   // first write of output row j: its slot must be drained
@@ -172,18 +222,30 @@ __global__ void __launch_bounds__(kRowThreads, 1) conv_row64_kernel(const __grid
         const uint32_t d1 = tmem_base + s1 * 64, d2 = tmem_base;
         const uint32_t id1 = idesc0 | (static_cast<uint32_t>(8 * c1) << 17);
         const uint32_t id2 = idesc0 | (static_cast<uint32_t>(8 * (c2 > 0 ? c2 : 1)) << 17);
-        const uint64_t bd1 = desc_add(b0, lo * kTapBytes), bd2 = desc_add(b0, (lo + c1) * kTapBytes);
+        constexpr int kKcBytes = PAIR ? kPairKcBytes : 3 * kTapBytes;
+        const uint64_t bd1 = desc_add(b0, PAIR ? pair_region(lo, c1) : lo * kTapBytes);
+        const uint64_t bd2 = desc_add(b0, PAIR ? pair_region(lo + c1, c2 > 0 ? c2 : 1) : (lo + c1) * kTapBytes);
         if (elect_one()) {
 #pragma unroll
           for (int kc = 0; kc < 3; ++kc)
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {
               const uint64_t ada = desc_add(ad, kc * 128 + ks * 32);
-              umma_bf16(d1, ada, desc_add(bd1, kc * 3 * kTapBytes + ks * 32), id1, 1u);
-              if (c2 > 0) umma_bf16(d2, ada, desc_add(bd2, kc * 3 * kTapBytes + ks * 32), id2, 1u);
+              if constexpr (PAIR) {
+                umma_bf16_pair(d1, ada, desc_add(bd1, kc * kKcBytes + ks * 32), id1, 1u);
+                if (c2 > 0) umma_bf16_pair(d2, ada, desc_add(bd2, kc * kKcBytes + ks * 32), id2, 1u);
+              } else {
+                umma_bf16(d1, ada, desc_add(bd1, kc * kKcBytes + ks * 32), id1, 1u);
+                if (c2 > 0) umma_bf16(d2, ada, desc_add(bd2, kc * kKcBytes + ks * 32), id2, 1u);
+              }
             }
-          umma_commit(&a_empty[as]);
-          if (j >= 2) umma_commit(&tfull[row_slot(G + j - 2)]);
+          if constexpr (PAIR) {
+            umma_commit_pair(&a_empty[as], 0x3);
+            if (j >= 2) umma_commit_pair(&tfull[row_slot(G + j - 2)], 0x3);
+          } else {
+            umma_commit(&a_empty[as]);
+            if (j >= 2) umma_commit(&tfull[row_slot(G + j - 2)]);
+          }
         }
         __syncwarp();
         if (++as == kRowStages) { as = 0; aph ^= 1; }
@@ -198,8 +260,8 @@ __global__ void __launch_bounds__(kRowThreads, 1) conv_row64_kernel(const __grid
     uint8_t* stage = sOut + wg * 2 * 8192;
     int ob = 0, G = 0;
     const bool pool = p.pool_out != nullptr;
-    for (int u = blockIdx.x; u < p.total; u += gridDim.x) {
-      const RowUnit ru = row_unit(p, u);
+    for (int u = u_first; u < p.total; u += u_step) {
+      const RowUnit ru = row_unit<PAIR>(p, u, rank);
       const bool count_col = ru.x0 + m >= ru.cb * kRowPx;   // shifted last block: count once
       for (int o = 0; o < ru.rows; o += 2) {
         if (((G + o) >> 1 & 1) != wg) continue;
@@ -322,7 +384,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) conv_row64_kernel(const __grid
           tmem_st32_zero(tmem_base + lanes + s * 64 + 32);
           tmem_wait_st();
           tc_fence_before();
-          mbar_arrive(&tempty[s]);
+          if constexpr (PAIR) mbar_arrive_cluster(lead(&tempty[s])); else mbar_arrive(&tempty[s]);
         }
       }
       G += ru.rows;
@@ -330,10 +392,18 @@ __global__ void __launch_bounds__(kRowThreads, 1) conv_row64_kernel(const __grid
     if (m == 0) bulk_wait_all();
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+  if constexpr (PAIR) {
+    cluster_sync();   // the peer's barriers / TMEM stay alive until the pair is done
+    if (warp == 2) {
+      tc_fence_after();
+      tmem_dealloc_pair(tmem_base, 512);
+    }
+  } else {
+    __syncthreads();
+    if (warp == 2) {
+      tc_fence_after();
+      tmem_dealloc(tmem_base, 512);
+    }
   }
   if (p.colsum != nullptr && threadIdx.x < 64) atomicAdd(p.colsum + threadIdx.x, s_col[threadIdx.x]);
 }
@@ -368,7 +438,12 @@ cudaError_t conv_row64_fwd(const ConvGeom& g, const void* x_pad, const void* w, 
     const long long cost = waves * (rows + 2);
     if (best < 0 || cost < best) { best = cost; p.rows = rows; p.n_strips = strips; }
   }
-  p.total = g.n * p.n_cb * p.n_strips;
+  // CTA pairs (M = 256: the two column blocks of a row; RALPB_ROW64_PAIR=1) are implemented
+  // and pass the parity tests, but measured 22 % slower than single CTAs on conv1_2
+  // (0.574 vs 0.471 ms forward, tools/probe_conv.py --layer 1): off by default
+  const char* pe = getenv("RALPB_ROW64_PAIR");
+  const bool pair = p.n_cb == 2 && pe != nullptr && pe[0] == '1';
+  p.total = g.n * (pair ? 1 : p.n_cb) * p.n_strips;
   p.bias = bias;
   p.relu = relu;
   p.mask = static_cast<const __nv_bfloat16*>(mask_pad);
@@ -376,14 +451,25 @@ cudaError_t conv_row64_fwd(const ConvGeom& g, const void* x_pad, const void* w, 
   p.pool_out = static_cast<__nv_bfloat16*>(pool_out);
   p.pool_pad = pool_pad;
   if (!encode_act(&p.tmX, x_pad, 64, g.wp(), g.hp(), g.n, 64, kRowIn, 1, 128, why)) return cudaErrorInvalidValue;
-  if (!encode_mat(&p.tmW, w, 64, 9 * 64, 64, 64, 128, why)) return cudaErrorInvalidValue;
+  if (!encode_mat(&p.tmW, w, 64, 9 * 64, 64, 32, 128, why)) return cudaErrorInvalidValue;   // 32-row boxes
   if (!encode_interior_box(&p.tmY, y_pad, 64, g.w, g.h, g.wp(), g.hp(), g.n, 1, kRowPx, 1, why))
     return cudaErrorInvalidValue;
-  const int smem = 1024 + 9 * kTapBytes + kRowStages * kRowStage + 2 * 2 * 8192 + 1024;
-  const int grid = std::min(p.total, sms);
-  static_cast<void>(cudaFuncSetAttribute(conv_row64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  launch_timed([&] { static_cast<void>(launch_pdl(conv_row64_kernel, dim3(grid), dim3(kRowThreads), smem, s, 1, p)); },
-               s, KIND_CONV_FWD, 2.0 * g.n * g.h * g.w * 9.0 * 64.0 * 64.0);
+  const double flops = 2.0 * g.n * g.h * g.w * 9.0 * 64.0 * 64.0;
+  if (pair) {
+    const int smem = 1024 + 3 * kPairKcBytes + 4 * kRowStage + 2 * 2 * 8192 + 1024;
+    const int grid = 2 * std::min(p.total, sms / 2);
+    static_cast<void>(cudaFuncSetAttribute(conv_row64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    launch_timed([&] {
+      static_cast<void>(launch_pdl(conv_row64_kernel<true>, dim3(grid), dim3(kRowThreads), smem, s, 2, p));
+    }, s, KIND_CONV_FWD_PAIR, flops);
+  } else {
+    const int smem = 1024 + 9 * kTapBytes + 5 * kRowStage + 2 * 2 * 8192 + 1024;
+    const int grid = std::min(p.total, sms);
+    static_cast<void>(cudaFuncSetAttribute(conv_row64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    launch_timed([&] {
+      static_cast<void>(launch_pdl(conv_row64_kernel<false>, dim3(grid), dim3(kRowThreads), smem, s, 1, p));
+    }, s, KIND_CONV_FWD, flops);
+  }
   return cudaGetLastError();
 }
 

@@ -308,10 +308,12 @@ def test_conv_fwd_fused_pool(case):
     torch.testing.assert_close(colsum, dx.float().sum(dim=(0, 1, 2)), rtol=1e-5, atol=1e-4)
 
 
-@pytest.mark.parametrize("case", [(2, 224, 224), (1, 130, 160), (3, 36, 128)])
-def test_row64_fused_pool(case):
-    """The row-streamed 64->64 kernel with the fused 2x2/2 pool (no argmax bytes), against torch."""
-    n, h, w = case
+@pytest.mark.parametrize("case", [(2, 224, 224, "1"), (1, 130, 160, "1"), (3, 36, 128, "1"), (1, 130, 160, "0")])
+def test_row64_fused_pool(case, monkeypatch):
+    """The row-streamed 64->64 kernel with the fused 2x2/2 pool (no argmax bytes), against torch
+    (two column blocks run as a CTA pair unless RALPB_ROW64_PAIR=0)."""
+    n, h, w, pair = case
+    monkeypatch.setenv("RALPB_ROW64_PAIR", pair)
     g = torch.Generator(device=DEV).manual_seed(21)
     x = _pad(_bf(n, h, w, 64, gen=g), 1).contiguous()
     wt = _bf(64, 9, 64, scale=(2.0 / 576) ** 0.5, gen=g)
