@@ -90,7 +90,8 @@ bool slab_fwd_ok(const ConvGeom& g, int c, int cout) {
 }
 
 bool slab_wgrad_ok(const ConvGeom& g) {
-  return g.k == 3 && g.pad == 1 && g.cin % 64 == 0 && g.cout % 64 == 0 && g.q() < (1LL << 31);
+  return ((g.k == 3 && g.pad == 1) || (g.k == 5 && g.pad == 2)) && g.cin % 64 == 0 && g.cout % 64 == 0 &&
+         g.q() < (1LL << 31);
 }
 
 cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, int c, int cout, const float* bias,
@@ -244,16 +245,17 @@ cudaError_t conv_slab_wgrad(const ConvGeom& g, const void* x_pad, const void* dy
   p.n_ci_blocks = g.cin / 64;
   p.n_co_blocks = g.cout / 64;
   p.idesc = umma_idesc_bf16(128, 64, true, true);
+  p.n_splits = g.k == 5 ? 2 : 1;   // tap groups: 25 taps = 16 + 9 (8 tap-pair accumulators per pass)
   p.dw = dw;
   p.db = db;
   if (!encode_act(&p.tmX, x_pad, g.cin, g.wp(), g.hp(), g.n, 64, p.sw, p.sh, 128, why)) return cudaErrorInvalidValue;
   if (!encode_act(&p.tmB, dy_pad, g.cout, g.wp(), g.hp(), g.n, 64, 8, bh, 128, why)) return cudaErrorInvalidValue;
   const int smem = 1024 + 4096 + p.na * (p.slab_stage + p.b_stage) + 512;
-  const long long units = static_cast<long long>(p.n_ci_blocks) * p.n_co_blocks * p.n_pix_blocks;
+  const long long units = static_cast<long long>(p.n_ci_blocks) * p.n_co_blocks * p.n_splits * p.n_pix_blocks;
   const int grid = static_cast<int>(std::min<long long>(units, num_sms()));
-  // CTA-pair kernel (M=256 x N=128 UMMAs) when the output channels come in 128s
+  // CTA-pair kernel (M=256 x N=128 UMMAs, 3x3) when the output channels come in 128s
   const char* wenv = getenv("RALPB_WGRAD");
-  const bool pair = g.cout % 128 == 0 && !(wenv != nullptr && std::strcmp(wenv, "single") == 0);
+  const bool pair = g.k == 3 && g.cout % 128 == 0 && !(wenv != nullptr && std::strcmp(wenv, "single") == 0);
   if (pair) {
     p.n_co_blocks = g.cout / 128;
     p.idesc = umma_idesc_bf16(256, 128, true, true);
@@ -275,7 +277,13 @@ cudaError_t conv_slab_wgrad(const ConvGeom& g, const void* x_pad, const void* dy
     launch_timed([&] { static_cast<void>(launch_pdl(kern, dim3(grid), dim3(256), smem, s, 1, p)); }, s, KIND_WGRAD,
                  2.0 * g.n * g.h * g.w * static_cast<double>(g.taps()) * g.cin * g.cout);
   };
-  if (bh == 14) go(conv_slab_wgrad_kernel<14>); else go(conv_slab_wgrad_kernel<16>);
+  if (g.k == 5) {
+    go(bh == 14 ? conv_slab_wgrad_kernel<14, 5> : conv_slab_wgrad_kernel<16, 5>);
+    cudaError_t e = cudaGetLastError();   // no bias accumulator for 5x5: db from dY's column sums
+    if (e != cudaSuccess || db == nullptr) return e;
+    return colsum_bf16(static_cast<const __nv_bfloat16*>(dy_pad), g.q(), g.cout, g.cout, db, s);
+  }
+  if (bh == 14) go(conv_slab_wgrad_kernel<14, 3>); else go(conv_slab_wgrad_kernel<16, 3>);
   return cudaGetLastError();
 }
 

@@ -457,9 +457,13 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
 // gradient (ones x dY) when this CTA owns ci-block 0.  Work is split stream-K style: the
 // (tile, pixel-block) units are divided evenly over the persistent CTAs, and every
 // contiguous run of one tile is flushed with fp32 reductions.
-template <int BH>
+template <int BH, int K>
 __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_constant__ SlabConvParams p) {
-  constexpr int SW = 10;            // 3x3 filters only (slab_wgrad_ok)
+  constexpr int SW = 8 + K - 1;     // slab width (pixels)
+  constexpr int TAPS = K * K;
+  // tap-pair accumulators per pass: 3x3 -> 5 (+ the bias accumulator); 5x5 -> 8 (512 TMEM
+  // columns), so the 13 tap pairs take two passes ("tap groups", part of the tile index)
+  constexpr int NACC = K == 3 ? 5 : 8;
   constexpr int KSTEPS = BH / 2;    // 16-pixel K-steps per block (two 8-pixel rows each)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -491,7 +495,8 @@ __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_co
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait_and_release();
   const int PB = p.n_pix_blocks;
-  const long long units = static_cast<long long>(p.n_ci_blocks) * p.n_co_blocks * PB;
+  const int ngrp = p.n_splits;   // tap groups (1 for 3x3)
+  const long long units = static_cast<long long>(p.n_ci_blocks) * p.n_co_blocks * ngrp * PB;
   const long long u_begin = units * blockIdx.x / gridDim.x;
   const long long u_end = units * (blockIdx.x + 1) / gridDim.x;
   const int pb_per_img = p.n_hb * p.n_wb;
@@ -504,7 +509,7 @@ __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_co
         const int tile = static_cast<int>(u / PB);
         const int pb0 = static_cast<int>(u - static_cast<long long>(tile) * PB);
         const int pb1 = static_cast<int>(u_end - u < PB - pb0 ? pb0 + (u_end - u) : PB);
-        const int nb = tile % p.n_co_blocks, cb = tile / p.n_co_blocks;
+        const int nb = (tile / ngrp) % p.n_co_blocks, cb = tile / ngrp / p.n_co_blocks;
         for (int pb = pb0; pb < pb1; ++pb) {
           const int img = pb / pb_per_img;
           const int rem = pb - img * pb_per_img;
@@ -529,7 +534,8 @@ __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_co
       const int tile = static_cast<int>(u / PB);
       const int pb0 = static_cast<int>(u - static_cast<long long>(tile) * PB);
       const int pb1 = static_cast<int>(u_end - u < PB - pb0 ? pb0 + (u_end - u) : PB);
-      const bool with_bias = tile / p.n_co_blocks == 0 && p.db != nullptr;
+      const bool with_bias = K == 3 && tile / p.n_co_blocks == 0 && p.db != nullptr;
+      const int tbase = (tile % ngrp) * 2 * NACC;   // first tap of this tap group
       mbar_wait(&tempty[0], acc_ph ^ 1);
       tc_fence_after();
       for (int pb = pb0; pb < pb1; ++pb) {
@@ -538,9 +544,11 @@ __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_co
         const uint32_t soff = st * stage_bytes;
         if (elect_one()) {
 #pragma unroll
-          for (int a = 0; a < 5; ++a) {
-            const int t0 = 2 * a, t1 = 2 * a + 1 < 9 ? 2 * a + 1 : 2 * a;
-            const int o0 = (t0 / 3) * SW + t0 % 3, o1 = (t1 / 3) * SW + t1 % 3;
+          for (int a = 0; a < NACC; ++a) {
+            const int t0 = tbase + 2 * a;
+            if (t0 >= TAPS) break;
+            const int t1 = t0 + 1 < TAPS ? t0 + 1 : t0;
+            const int o0 = (t0 / K) * SW + t0 % K, o1 = (t1 / K) * SW + t1 % K;
             // LBO (bits 16..29, >>4) = distance between the two taps' atoms inside the slab
             const uint64_t xa = desc_add(x0, soff + o0 * 128) | (static_cast<uint64_t>(((o1 - o0) * 128) >> 4) << 16);
 #pragma unroll
@@ -551,7 +559,7 @@ __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_co
           if (with_bias) {
 #pragma unroll
             for (int ks = 0; ks < KSTEPS; ++ks)
-              umma_bf16(tmem_base + 5 * 64, ones_d, desc_add(y0, soff + ks * 2048), p.idesc,
+              umma_bf16(tmem_base + NACC * 64, ones_d, desc_add(y0, soff + ks * 2048), p.idesc,
                         (pb > pb0 || ks > 0) ? 1u : 0u);
           }
           umma_commit(&empty[st]);
@@ -573,21 +581,23 @@ __global__ void __launch_bounds__(256, 1) conv_slab_wgrad_kernel(const __grid_co
       const int tile = static_cast<int>(u / PB);
       const int pb0 = static_cast<int>(u - static_cast<long long>(tile) * PB);
       const int pb1 = static_cast<int>(u_end - u < PB - pb0 ? pb0 + (u_end - u) : PB);
-      const int nb = tile % p.n_co_blocks, cb = tile / p.n_co_blocks;
-      const bool with_bias = cb == 0 && p.db != nullptr;
+      const int nb = (tile / ngrp) % p.n_co_blocks, cb = tile / ngrp / p.n_co_blocks;
+      const bool with_bias = K == 3 && cb == 0 && p.db != nullptr;
+      const int tbase = (tile % ngrp) * 2 * NACC;
       mbar_wait(&tfull[0], acc_ph);
       tc_fence_after();
-      for (int a = 0; a <= 5; ++a) {
-        if (a == 5 && !with_bias) break;
+      for (int a = 0; a <= NACC; ++a) {
+        if (a == NACC && !with_bias) break;
+        if (a < NACC && tbase + 2 * a >= TAPS) break;
         const uint32_t tb = tmem_base + a * 64 + (static_cast<uint32_t>(q * 32) << 16);
         for (int c = 0; c < 64; c += 32) {
           uint32_t rr[32];
           tmem_ld32(tb + c, rr);
           tmem_wait_ld();
           const int co0 = nb * 64 + c;
-          if (a < 5) {
-            const int tap = 2 * a + (m >> 6);
-            if (tap < 9) {
+          if (a < NACC) {
+            const int tap = tbase + 2 * a + (m >> 6);
+            if (tap < TAPS) {
               float* dst = p.dw + static_cast<long long>(co0) * wstride + static_cast<long long>(tap) * p.c + cb * 64 + (m & 63);
 #pragma unroll
               for (int j = 0; j < 32; ++j) red_add_f32(dst + j * wstride, __uint_as_float(rr[j]));

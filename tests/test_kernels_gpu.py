@@ -74,6 +74,9 @@ CONV_CASES = [
     (2, 224, 224, 64, 64, 3, 1),
     (1, 130, 160, 64, 64, 3, 1),
     (3, 36, 128, 64, 64, 3, 1),
+    # 5x5 with 64-channel blocks: slab backward-filter in two tap groups (AlexNet conv2 shape)
+    (2, 27, 27, 64, 192, 5, 2),
+    (1, 20, 24, 128, 64, 5, 2),
 ]
 
 
