@@ -17,7 +17,11 @@
 //   conv_slab_wgrad_kernel backward-filter: M = (tap, ci) pairs of taps read as two
 //                          MN-major atoms of the same slab (LBO = tap distance),
 //                          N = 64 output channels, K = pixels; one extra
-//                          accumulator with an all-ones A yields the bias gradient.
+//                          accumulator with an all-ones A yields the bias gradient
+//                          (3x3).  5x5 filters: 13 tap pairs > 8 TMEM accumulators,
+//                          so the taps split into two groups (part of the tile index;
+//                          each group re-reads its pixel blocks) and db comes from dY's
+//                          column sums.
 #pragma once
 #include "ptx.cuh"
 
