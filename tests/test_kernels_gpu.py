@@ -226,7 +226,7 @@ def test_sgd_and_colsum():
 
 
 @pytest.mark.parametrize("k,stride,pad,po,kpad,h", [(3, 1, 1, 1, 32, 20), (5, 1, 2, 0, 128, 16), (11, 4, 0, 0, 384, 63),
-                                                  (11, 4, 0, 1, 384, 35)])
+                                                  (11, 4, 0, 1, 384, 35), (11, 4, 0, 0, 384, 227), (11, 4, 2, 1, 384, 224)])
 def test_first_conv_im2col(k, stride, pad, po, kpad, h):
     """First (RGB) conv as pack_im2col + GEMM with the bias folded into a ones column (fwd) and
     the filter/bias gradient as one MN x MN GEMM."""
