@@ -35,6 +35,10 @@ constexpr int kStages = 4;
 #endif
 constexpr int kGroups = RALPB_FIRST_GROUPS;   // producer warpgroups (tiles alternate between them)
 constexpr int kProd = 4 * kGroups;            // producer warps
+#ifndef RALPB_FIRST_OUTBUFS
+#define RALPB_FIRST_OUTBUFS 4
+#endif
+constexpr int kOutBufs = RALPB_FIRST_OUTBUFS;   // forward output staging buffers (16 KB each)
 
 struct FirstConvParams {
   CUtensorMap tmY;        // fwd: output (store); wgrad: dY (load); [n][hp][wp][64] box {64,16,8,1}
@@ -126,8 +130,8 @@ __global__ void __launch_bounds__(32 * (kProd + 5), 1) conv_first_fwd_kernel(con
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = smem;                           // 4 KB filters
   uint8_t* sA = smem + 4096;                    // kStages x 8 KB patches
-  uint8_t* sOut = sA + kStages * 8192;          // 2 x 16 KB output staging
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(sOut + 2 * 16384);
+  uint8_t* sOut = sA + kStages * 8192;          // kOutBufs x 16 KB output staging
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(sOut + kOutBufs * 16384);
   uint64_t* a_empty = a_full + kStages;
   uint64_t* tfull = a_empty + kStages;
   uint64_t* tempty = tfull + 2;
@@ -188,8 +192,9 @@ __global__ void __launch_bounds__(32 * (kProd + 5), 1) conv_first_fwd_kernel(con
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      // the staging buffer written two tiles ago must have been read by its TMA store
-      if (m == 0) bulk_wait_read<1>();
+      // the staging buffer written kOutBufs tiles ago must have been read by its TMA store
+      // (kOutBufs - 1 stores in flight; 4 buffers measured 3 % faster than 2)
+      if (m == 0) bulk_wait_read<kOutBufs - 1>();
       named_bar_sync(1, 128);
       uint8_t* row = sOut + ob * 16384 + m * 128;
 #pragma unroll
@@ -207,7 +212,7 @@ __global__ void __launch_bounds__(32 * (kProd + 5), 1) conv_first_fwd_kernel(con
         tma_store_4d(&p.tmY, sOut + ob * 16384, 0, x0 + p.pad_out, y0 + p.pad_out, img);
         bulk_commit();
       }
-      ob ^= 1;
+      if (++ob == kOutBufs) ob = 0;
       if (++acc == 2) { acc = 0; acc_ph ^= 1; }
     }
     if (m == 0) bulk_wait_all();
@@ -329,7 +334,7 @@ cudaError_t conv_first_fwd(const float* img, int n, int h, int w, int cin, const
   FirstConvParams p;
   if (!first_params(&p, img, n, h, w, cin, y_pad, pad_out, why)) return cudaErrorInvalidValue;
   p.wf = static_cast<const __nv_bfloat16*>(wf);
-  const int smem = 1024 + 4096 + kStages * 8192 + 2 * 16384 + 256;
+  const int smem = 1024 + 4096 + kStages * 8192 + kOutBufs * 16384 + 256;
   const int grid = std::min(p.total, num_sms());
   cudaFuncSetAttribute(conv_first_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   launch_timed([&] { static_cast<void>(launch_pdl(conv_first_fwd_kernel, dim3(grid), dim3(32 * (kProd + 5)), smem, s, 1, p)); }, s, KIND_FIRST_FWD,
