@@ -754,7 +754,7 @@ __global__ void __launch_bounds__(256) conv_weight_prep_kernel(const __grid_cons
       if (co < J.co && ci < J.ci) {
         const long long i = (static_cast<long long>(co) * J.taps + t) * J.ci + ci;
         const float v = J.w[i];
-        J.wf[i] = __float2bfloat16_rn(v);
+        if (J.wf != nullptr) J.wf[i] = __float2bfloat16_rn(v);
         tile[yy][tx] = v;
       }
     }

@@ -347,6 +347,8 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   if (cudaStreamCreateWithFlags(&m->aux_stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
   cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&m->ev_wd_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&m->ev_wd_join, cudaEventDisableTiming);
   for (auto& e : m->ev) cudaEventCreate(&e);
   if (cudaMallocHost(&m->loss_host, sizeof(float) * Model::kLossRing) != cudaSuccess) return fail("cudaMallocHost");
   for (auto& e : m->ev_loss) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -371,6 +373,8 @@ void model_destroy(Model* m) {
   if (m->aux_stream) cudaStreamDestroy(m->aux_stream);
   if (m->ev_fork) cudaEventDestroy(m->ev_fork);
   if (m->ev_join) cudaEventDestroy(m->ev_join);
+  if (m->ev_wd_fork) cudaEventDestroy(m->ev_wd_fork);
+  if (m->ev_wd_join) cudaEventDestroy(m->ev_wd_join);
   for (int r = 0; r < static_cast<int>(m->peer_base.size()); ++r)
     if (r != m->rank && m->peer_base[r] != nullptr) cudaIpcCloseMemHandle(m->peer_base[r]);
   for (void* p : m->owned) cudaFree(p);
@@ -930,31 +934,45 @@ int launch_front_backward(Model* m, const bf16* dcut, std::string* why) {
   return 0;
 }
 
-int relayout_weights(Model* m, bool fc_too, std::string* why) {
+// bf16 filter copies from the fp32 masters, batched into one launch per kMaxPrepJobs layers:
+// forward copies (wf, needed by the next step's first kernel) and/or the tap-reversed
+// transposes the backward-data kernels read (wd).
+int prep_filters(Model* m, bool forward, bool dgrad, cudaStream_t s, std::string* why) {
   WeightPrepJob jobs[kMaxPrepJobs];
   int nj = 0;
   for (size_t i = 0; i < m->front.size(); ++i) {
     FrontLayer& f = m->front[i];
     if (f.kind != RALPB_CONV) continue;
     if (f.im2col) {
-      RALPB_TRY(cast_bf16(m->P + f.w_off, f.w_count, f.wf, m->stream));
-      ++m->launches;
+      if (forward) {
+        RALPB_TRY(cast_bf16(m->P + f.w_off, f.w_count, f.wf, s));
+        ++m->launches;
+      }
       continue;
     }
+    if (!forward && i == 0) continue;   // no backward-data for the first layer
     if (nj == kMaxPrepJobs) {
-      RALPB_TRY(conv_weight_prep_batch(jobs, nj, m->stream));
+      RALPB_TRY(conv_weight_prep_batch(jobs, nj, s));
       ++m->launches;
       nj = 0;
     }
     WeightPrepJob& j = jobs[nj++];
     j = WeightPrepJob{};
-    j.w = m->P + f.w_off; j.wf = f.wf; j.wd = i > 0 ? f.wd : nullptr;
+    j.w = m->P + f.w_off; j.wf = forward ? f.wf : nullptr; j.wd = dgrad && i > 0 ? f.wd : nullptr;
     j.co = f.g.cout; j.taps = f.g.taps(); j.ci = f.g.cin;
   }
   if (nj > 0) {
-    RALPB_TRY(conv_weight_prep_batch(jobs, nj, m->stream));
+    RALPB_TRY(conv_weight_prep_batch(jobs, nj, s));
     ++m->launches;
   }
+  return 0;
+}
+
+// After a parameter update: the forward copies on the model stream; the backward-data
+// transposes are rebuilt at the start of the next step on the aux stream, overlapping the
+// forward pass (step_body), so only `dgrad_now` callers need them here.
+int relayout_weights(Model* m, bool fc_too, std::string* why, bool dgrad_now = false) {
+  if (prep_filters(m, true, dgrad_now, m->stream, why)) return 1;
   if (fc_too) {
     for (auto& f : m->back) {
       RALPB_TRY(cast_bf16(m->P + f.w_off, static_cast<long long>(f.lout) * f.lin, f.wbf, m->stream));
@@ -1021,6 +1039,12 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   bool fc_forked = false;
   RALPB_TRY(bump_counter(m->seq_dev, s));
   ++m->launches;
+
+  // backward-data filter copies from this step's masters, on the aux stream under the forward
+  RALPB_TRY(cudaEventRecord(m->ev_wd_fork, s));
+  RALPB_TRY(cudaStreamWaitEvent(m->aux_stream, m->ev_wd_fork, 0));
+  if (prep_filters(m, false, true, m->aux_stream, why)) return 1;
+  RALPB_TRY(cudaEventRecord(m->ev_wd_join, m->aux_stream));
 
   // ---------------- worker front forward
   const FrontLayer& f0 = m->front[0];
@@ -1155,6 +1179,7 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   RALPB_TRY(mark(m, 2, capturing));
 
   // ---------------- worker front backward
+  RALPB_TRY(cudaStreamWaitEvent(s, m->ev_wd_join, 0));
   RALPB_TRY(cudaMemsetAsync(m->G, 0, m->n_front * sizeof(float), s));
   if (launch_front_backward(m, dcut, why)) return 1;
   RALPB_TRY(mark(m, 3, capturing));

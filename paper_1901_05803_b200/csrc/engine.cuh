@@ -84,6 +84,7 @@ struct Model {
                                    // last layer's is dlogits), kept for the deferred wgrads
   cudaStream_t aux_stream = nullptr;   // PS: FC weight gradients + SGD, concurrent with the
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // front backward
+  cudaEvent_t ev_wd_fork = nullptr, ev_wd_join = nullptr;  // backward-data filter copies (aux stream)
   float* row_loss = nullptr;
   float* loss = nullptr;
   std::vector<bf16*> gacts;        // gacts[i] = gradient w.r.t. acts[i] (dedicated, zero borders)
