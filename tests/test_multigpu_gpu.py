@@ -18,3 +18,27 @@ def test_two_rank_parity():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0 and "MULTI-RANK PARITY PASS" in r.stdout
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_cli_run_scenario_two_gpus(tmp_path):
+    """`run` on a bundled two-worker scenario: layer-placed, all-on-PS and ring jobs executed on
+    two B200s, each reporting the oracle's logical bytes."""
+    from paper_1901_05803_b200.planner import JobSpec, Strategy, catalog_lookup, volumes_for
+
+    out = tmp_path / "r.json"
+    cmd = [sys.executable, "-m", "paper_1901_05803_b200", "run", "vgg16_b200_compare.scn", "--steps", "2",
+           "--warmup", "1", "--out", str(out)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=str(ROOT))
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
+    import json
+    jobs = {j["job"]: j for j in json.loads(out.read_text())["jobs"]}
+    m = catalog_lookup("vgg16").with_batch_size(128)
+    want = {"ralp": volumes_for(JobSpec(m, Strategy.ralp(18), 2)).total_bytes_per_step,
+            "allps": volumes_for(JobSpec(m, Strategy.baseline(), 2)).total_bytes_per_step,
+            "ring": volumes_for(JobSpec(m, Strategy.ring(), 2, ps_count=0)).total_bytes_per_step}
+    for name, b in want.items():
+        assert jobs[name]["bytes_on_wire_per_step"] == b
+        assert jobs[name]["worker_count"] == 2 and len(jobs[name]["losses"]) == 2
+        assert jobs[name]["images_per_sec"] > 1000
