@@ -112,11 +112,19 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
   const int sms = num_sms();
   int splits = d.k_splits;
   if (splits == 0) {
-    // split-K so that the tile grid covers ~2 waves, keeping >= 4 k-blocks per split
-    long long tiles = static_cast<long long>(p.n_mt) * p.n_nt;
-    long long want = (2LL * sms + tiles - 1) / tiles;
-    long long maxs = std::max<long long>(1, kblocks / 4);
-    splits = static_cast<int>(std::max<long long>(1, std::min(want, maxs)));
+    // split-K minimising (waves of the persistent grid) x (k-blocks per unit + a per-unit
+    // epilogue/setup cost of ~8 k-blocks), >= 4 k-blocks per split.  Wave quantisation is what
+    // matters at the FC shapes: M=512 x N=4096 (64 tiles) runs best at 2 splits, M=1024 (128
+    // tiles) unsplit (tools/probe_fc_gemm.py); the old "~2 waves" rule picked 5 and 3.
+    const long long tiles = static_cast<long long>(p.n_mt) * p.n_nt;
+    const long long maxs = std::max<long long>(1, std::min<long long>(kblocks / 4, 4LL * sms));
+    long long best = -1;
+    splits = 1;
+    for (long long sp = 1; sp <= maxs; ++sp) {
+      const long long waves = (tiles * sp + sms - 1) / sms;
+      const long long cost = waves * ((kblocks + sp - 1) / sp + 8);
+      if (best < 0 || cost < best) { best = cost; splits = static_cast<int>(sp); }
+    }
   }
   if (splits > 1 && d.epi != EPI_F32_ATOMIC) { *why = "split-K needs the atomic epilogue"; return cudaErrorInvalidValue; }
   p.kblocks_per_split = static_cast<int>((kblocks + splits - 1) / splits);
