@@ -66,7 +66,7 @@ struct alignas(64) SlabConvParams {
   float* dw;
   float* db;
   int n_ci_blocks, n_co_blocks, n_splits, blocks_per_split, n_pix_blocks;
-  int dbg;              // experiments: bit0 skip epilogue stores, bit1 skip MMAs
+  int dbg;              // experiments: bit0 skip the epilogue, bit1 skip MMAs, bit2 skip pooled stores
   int wres;             // filters resident in smem: B stage t holds tap t, loaded once per CTA
 };
 
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
               ip[0] = make_uint4(by[0], by[1], by[2], by[3]);
               ip[1] = make_uint4(by[4], by[5], by[6], by[7]);
             }
-            if ((m & 9) == 0 && valid) {
+            if ((m & 9) == 0 && valid && !(p.dbg & 4)) {
               const int ph = hh >> 1, pw = ww >> 1;
               const long long prow = (static_cast<long long>(img) * ((p.h >> 1) + 2 * p.pool_pad) + ph + p.pool_pad) *
                                          ((p.w >> 1) + 2 * p.pool_pad) + pw + p.pool_pad;
