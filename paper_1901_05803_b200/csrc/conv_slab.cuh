@@ -341,14 +341,15 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
           // stage this pixel's 32 channels (one 64-byte SW64 row: chunk j at j ^ ((m >> 1) & 3))
           // and write the 16x8-pixel x 32-channel block with one TMA store; the interior-view
           // tensor map clips rows/columns outside the image, so borders are never written
+          // one barrier per box: before it, thread 0 also waits until every earlier store has
+          // read its staging buffer, so the other buffer is free for the next box
           uint8_t* buf = stage + ob * 8192;
-          if (m == 0) bulk_wait_read<1>();
-          named_bar_sync(1 + g, 128);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             *reinterpret_cast<uint4*>(buf + m * 64 + ((j ^ ((m >> 1) & 3)) << 4)) =
                 make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
           fence_proxy_async_smem();
+          if (m == 0) bulk_wait_read<0>();
           named_bar_sync(1 + g, 128);
           if (m == 0) {
             tma_store_4d(&p.tmY, buf, n0, wb * 8, h0, img);
