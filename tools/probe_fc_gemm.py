@@ -1,3 +1,5 @@
+"""The PS's FC-tail GEMM shapes at W*b = 512 / 1024 rows (fc1 forward, K-major x K-major, and
+backward-data, MN-major filters) under several split-K settings; split 0 = the engine's choice."""
 import sys
 sys.path.insert(0, "tools")
 from probe_gemm import run
