@@ -138,7 +138,7 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
     p.sh = 16 * p.macc + g.k - 1;
     p.slab_load = p.row_bytes * p.sw * p.sh;
     p.slab_stage = align1k(p.slab_load);
-    staging = (p.macc >= 2 ? 2 : 1) * 2 * 8192;
+    staging = (p.macc >= 2 ? 2 : 1) * kOutBufs * 8192;
     budget = kSmemBudget - staging;
     p.nb = std::min(nb_cap, (budget - p.na * p.slab_stage) / p.b_stage);
     if (p.nb >= 2 || p.macc == 1) break;

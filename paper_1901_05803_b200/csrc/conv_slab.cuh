@@ -28,6 +28,10 @@
 namespace ralpb {
 
 constexpr int kSlabMaxTaps = 25;
+#ifndef RALPB_OUT_BUFS
+#define RALPB_OUT_BUFS 2
+#endif
+constexpr int kOutBufs = RALPB_OUT_BUFS;   // 8 KB output staging boxes per epilogue warpgroup (3: -1 %, smem)
 #ifndef RALPB_B_PRODUCERS
 #define RALPB_B_PRODUCERS 2
 #endif
@@ -92,7 +96,7 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
   uint8_t* sA = smem;
   uint8_t* sB = sA + p.na * p.slab_stage;
   uint8_t* sOut = sB + p.nb * p.b_stage;         // EWG x 2 x 8 KB output staging (TMA store)
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(sOut + EWG * 2 * 8192);
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(sOut + EWG * kOutBufs * 8192);
   uint64_t* a_empty = a_full + p.na;
   uint64_t* b_full = a_empty + p.na;
   uint64_t* b_empty = b_full + p.nb;
@@ -128,7 +132,6 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
   pdl_wait_and_release();
   const int total = p.n * p.n_hb * p.n_wb * p.n_nt;
   const int cblks = p.c / p.kb;
-  const int ksteps = p.kb / 16;
   const int mrows = 16 * p.macc;
   const int w_first = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
   const int w_step = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
     const int m = q * 32 + lane;
     int acc = 0, ob = 0;
     uint32_t acc_ph = 0;
-    uint8_t* stage = sOut + g * 2 * 8192;
+    uint8_t* stage = sOut + g * kOutBufs * 8192;
     // ReLU-mask rows (backward-data) are fetched one 32-channel chunk ahead -- the first chunk
     // of a work item before its accumulator is waited on -- so the global-load latency hides
     // behind the MMAs / the previous chunk instead of stalling every chunk of the epilogue.
@@ -349,13 +352,13 @@ __global__ void __launch_bounds__(128 + 128 * (MACC >= 2 ? 2 : 1), 1)
             *reinterpret_cast<uint4*>(buf + m * 64 + ((j ^ ((m >> 1) & 3)) << 4)) =
                 make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
           fence_proxy_async_smem();
-          if (m == 0) bulk_wait_read<0>();
+          if (m == 0) bulk_wait_read<kOutBufs - 2>();
           named_bar_sync(1 + g, 128);
           if (m == 0) {
             tma_store_4d(&p.tmY, buf, n0, wb * 8, h0, img);
             bulk_commit();
           }
-          ob ^= 1;
+          if (++ob == kOutBufs) ob = 0;
           if (p.pool_out != nullptr) {
             // fused 2x2/2 max pool: a warp holds 4 image rows x 8 columns, so the window of an
             // (even row, even column) pixel is lanes {l, l^1, l^8, l^9}
