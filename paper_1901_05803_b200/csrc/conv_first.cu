@@ -39,6 +39,16 @@ constexpr int kProd = 4 * kGroups;            // producer warps
 #define RALPB_FIRST_OUTBUFS 4
 #endif
 constexpr int kOutBufs = RALPB_FIRST_OUTBUFS;   // forward output staging buffers (16 KB each)
+#ifndef RALPB_FIRST_EPI
+#define RALPB_FIRST_EPI 2
+#endif
+constexpr int kEpi = RALPB_FIRST_EPI;            // forward epilogue warpgroups (tiles alternate)
+constexpr int kFwdWarps = kProd + 4 * kEpi + 1;  // producers, epilogue warpgroups, MMA warp
+constexpr int kMmaWarp = kProd + 4 * kEpi;
+constexpr int kAccs = 2 * kEpi;                  // 64-column TMEM accumulators
+constexpr int kTmemCols = kAccs * 64 <= 128 ? 128 : kAccs * 64 <= 256 ? 256 : 512;
+static_assert(kAccs * 64 <= 512, "TMEM holds 512 columns");
+static_assert(kOutBufs % kEpi == 0, "staging buffers split evenly over the epilogue warpgroups");
 
 struct FirstConvParams {
   CUtensorMap tmY;        // fwd: output (store); wgrad: dY (load); [n][hp][wp][64] box {64,16,8,1}
@@ -123,9 +133,11 @@ __device__ __forceinline__ void tile_coords(const FirstConvParams& p, int t, int
   x0 = tw * kTW;
 }
 
-// warps 0..kProd-1: patch producers (thread = pixel); the next 4: epilogue (thread = pixel = TMEM
-// lane); the last: TMEM allocation + MMA issue.
-__global__ void __launch_bounds__(32 * (kProd + 5), 1) conv_first_fwd_kernel(const __grid_constant__ FirstConvParams p) {
+// warps 0..kProd-1: patch producers (thread = pixel); then kEpi epilogue warpgroups (thread =
+// pixel = TMEM lane; local tile j goes to warpgroup j % kEpi, accumulator j % kAccs); the last:
+// TMEM allocation + MMA issue.  One epilogue warpgroup capped the kernel at ~1150 cycles per
+// 16 KB tile (TMEM load -> bf16 -> staging -> TMA store latency chain).
+__global__ void __launch_bounds__(32 * kFwdWarps, 1) conv_first_fwd_kernel(const __grid_constant__ FirstConvParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = smem;                           // 4 KB filters
@@ -134,8 +146,8 @@ __global__ void __launch_bounds__(32 * (kProd + 5), 1) conv_first_fwd_kernel(con
   uint64_t* a_full = reinterpret_cast<uint64_t*>(sOut + kOutBufs * 16384);
   uint64_t* a_empty = a_full + kStages;
   uint64_t* tfull = a_empty + kStages;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + kAccs;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccs);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   pdl_wait_and_release();   // the filters are written by the previous step's update
@@ -143,10 +155,10 @@ __global__ void __launch_bounds__(32 * (kProd + 5), 1) conv_first_fwd_kernel(con
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) { mbar_init(&a_full[i], 128); mbar_init(&a_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128); }
+    for (int i = 0; i < kAccs; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128); }
     fence_barrier_init();
   }
-  if (warp == kProd + 4) tmem_alloc(tmem_slot, 128);
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -154,7 +166,7 @@ __global__ void __launch_bounds__(32 * (kProd + 5), 1) conv_first_fwd_kernel(con
 
   if (warp < kProd) {
     produce_tiles(p, sA, a_full, a_empty);
-  } else if (warp == kProd + 4) {
+  } else if (warp == kMmaWarp) {
     const uint32_t idesc = umma_idesc_bf16(128, 64, false, false);
     const uint64_t b0 = umma_smem_desc(smem_u32(sB), 16, 512, 64);
     const uint64_t a0 = umma_smem_desc(smem_u32(sA), 16, 512, 64);
@@ -173,14 +185,16 @@ __global__ void __launch_bounds__(32 * (kProd + 5), 1) conv_first_fwd_kernel(con
       }
       __syncwarp();
       if (++st == kStages) { st = 0; ph ^= 1; }
-      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+      if (++acc == kAccs) { acc = 0; acc_ph ^= 1; }
     }
   } else {
+    const int ewg = (warp - kProd) >> 2;
     const int q = warp & 3;
     const int m = q * 32 + lane;
-    int acc = 0, ob = 0;
+    int acc = ewg, ob = 0;
     uint32_t acc_ph = 0;
-    for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
+    uint8_t* sOutW = sOut + ewg * (kOutBufs / kEpi) * 16384;   // this warpgroup's staging buffers
+    for (int t = blockIdx.x + ewg * static_cast<int>(gridDim.x); t < p.total; t += kEpi * gridDim.x) {
       int img, y0, x0;
       tile_coords(p, t, img, y0, x0);
       mbar_wait(&tfull[acc], acc_ph);
@@ -192,11 +206,10 @@ __global__ void __launch_bounds__(32 * (kProd + 5), 1) conv_first_fwd_kernel(con
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      // the staging buffer written kOutBufs tiles ago must have been read by its TMA store
-      // (kOutBufs - 1 stores in flight; 4 buffers measured 3 % faster than 2)
-      if (m == 0) bulk_wait_read<kOutBufs - 1>();
-      named_bar_sync(1, 128);
-      uint8_t* row = sOut + ob * 16384 + m * 128;
+      // the staging buffer written kOutBufs/kEpi tiles ago must have been read by its TMA store
+      if (m == 0) bulk_wait_read<kOutBufs / kEpi - 1>();
+      named_bar_sync(1 + ewg, 128);
+      uint8_t* row = sOutW + ob * 16384 + m * 128;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         uint4 u;
@@ -207,21 +220,22 @@ __global__ void __launch_bounds__(32 * (kProd + 5), 1) conv_first_fwd_kernel(con
         *reinterpret_cast<uint4*>(row + ((c ^ (m & 7)) << 4)) = u;
       }
       fence_proxy_async_smem();
-      named_bar_sync(1, 128);
+      named_bar_sync(1 + ewg, 128);
       if (m == 0) {
-        tma_store_4d(&p.tmY, sOut + ob * 16384, 0, x0 + p.pad_out, y0 + p.pad_out, img);
+        tma_store_4d(&p.tmY, sOutW + ob * 16384, 0, x0 + p.pad_out, y0 + p.pad_out, img);
         bulk_commit();
       }
-      if (++ob == kOutBufs) ob = 0;
-      if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+      if (++ob == kOutBufs / kEpi) ob = 0;
+      acc += kEpi;
+      if (acc >= kAccs) { acc -= kAccs; acc_ph ^= 1; }
     }
     if (m == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == kProd + 4) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 128);
+    tmem_dealloc(tmem_base, kTmemCols);
   }
 }
 
@@ -337,7 +351,7 @@ cudaError_t conv_first_fwd(const float* img, int n, int h, int w, int cin, const
   const int smem = 1024 + 4096 + kStages * 8192 + kOutBufs * 16384 + 256;
   const int grid = std::min(p.total, num_sms());
   cudaFuncSetAttribute(conv_first_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  launch_timed([&] { static_cast<void>(launch_pdl(conv_first_fwd_kernel, dim3(grid), dim3(32 * (kProd + 5)), smem, s, 1, p)); }, s, KIND_FIRST_FWD,
+  launch_timed([&] { static_cast<void>(launch_pdl(conv_first_fwd_kernel, dim3(grid), dim3(32 * kFwdWarps), smem, s, 1, p)); }, s, KIND_FIRST_FWD,
                2.0 * n * h * w * 27.0 * 64.0);
   return cudaGetLastError();
 }
