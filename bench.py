@@ -122,7 +122,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def _cpu_baseline_step(sample_b: int, steps: int):
+def _cpu_baseline_step(sample_b: int, steps: int, warmup: int = 1):
     """Oracle port (oracle/step.py) of the layer-placed step on the host cores, bounded sample."""
     import torch
     from oracle import step as ostep
@@ -135,15 +135,16 @@ def _cpu_baseline_step(sample_b: int, steps: int):
     layers = lower(m)
     st = ostep.OracleState(layers, synthetic.init_params(layers, 0))
     shape = (layers[0]["h"], layers[0]["w"], layers[0]["cin"])
-    batches = [synthetic.batch(0, t, 0, sample_b, shape, layers[-1]["cout"]) for t in range(steps + 1)]
-    ostep.train_step(st, "ralp", 1, [batches[0]])  # warm-up
+    batches = [synthetic.batch(0, t, 0, sample_b, shape, layers[-1]["cout"]) for t in range(warmup + steps)]
+    for t in range(warmup):
+        ostep.train_step(st, "ralp", 1, [batches[t]])
     t0 = time.perf_counter()
     for t in range(steps):
-        ostep.train_step(st, "ralp", 1, [batches[t + 1]])
+        ostep.train_step(st, "ralp", 1, [batches[warmup + t]])
     dt = time.perf_counter() - t0
     return {"value": sample_b * steps / dt, "unit": "images/s", "cores": torch.get_num_threads(), "kind": "port",
             "sample": f"{MODEL} {shape[0]}x{shape[1]} layer-placed step (oracle/step.py, fp32 torch CPU), W=1, b={sample_b}, "
-                      f"{steps} timed steps after 1 warm-up, {dt:.1f} s"}
+                      f"{steps} timed steps after {warmup} warm-up, {dt:.1f} s"}
 
 
 def _headline_split():
@@ -156,10 +157,10 @@ def run_reference(args):
     if rank != 0:
         return
     sample_b = 8
-    steps = max(1, min(args.steps, 3))
-    cb = _cpu_baseline_step(sample_b, steps)
+    steps = args.steps  # each step is a b=8 sample of the workload (~0.6 s on 16 host cores)
+    cb = _cpu_baseline_step(sample_b, steps, args.warmup)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"],
-            "unit": "images/s", "n_gpus": args.gpus, "steps": steps, "warmup": 1,
+            "unit": "images/s", "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * sample_b / cb["value"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{MODEL} synthetic, layer-placed (RALP) step, CPU oracle port",
