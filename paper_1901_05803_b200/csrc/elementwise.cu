@@ -331,6 +331,9 @@ __global__ void maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ x,
 // Disjoint windows (stride == window == K): one thread per output window x 8 channels reads
 // the K*K inputs and dy once and writes the K*K input gradients.  Positions no window covers
 // and the padding border are never written (the executor's gradient buffers are zeroed once).
+#ifndef RALPB_POOL_ILP
+#define RALPB_POOL_ILP 1  // 2 and 4 measured slower (tools/probe_pool.py: 610 vs 705 vs 978 us)
+#endif
 template <int K>
 __global__ void maxpool_bwd_disjoint_kernel(const __nv_bfloat16* __restrict__ x,
                                             const __nv_bfloat16* __restrict__ dy, int n, int h, int w, int c,
@@ -341,21 +344,37 @@ __global__ void maxpool_bwd_disjoint_kernel(const __nv_bfloat16* __restrict__ x,
   const int cv = c >> 3;
   const int total = n * oh * ow * cv;
   const int hp = h + 2 * pi, wp = w + 2 * pi;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int cg = i % cv;
-    int t = i / cv;
-    const int ox = t % ow;
-    t /= ow;
-    const int oy = t % oh;
-    const int img = t / oh;
-    const long long base = ((static_cast<long long>(img) * hp + oy * K + pi) * wp + ox * K + pi) * c + cg * 8;
-    const long long dyo = ((static_cast<long long>(img) * (oh + 2 * po) + oy + po) * (ow + 2 * po) + ox + po) * c + cg * 8;
-    uint4 xv[K * K];
+  // RALPB_POOL_ILP windows per thread per iteration: all their loads are issued before any
+  // compare, so each thread keeps ILP * (K*K + 1) 16-byte loads in flight.
+  const int stride = gridDim.x * blockDim.x;
+  for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += RALPB_POOL_ILP * stride) {
+    long long base_u[RALPB_POOL_ILP];
+    uint4 xv_u[RALPB_POOL_ILP][K * K];
+    uint4 dv_u[RALPB_POOL_ILP];
 #pragma unroll
-    for (int q = 0; q < K * K; ++q)
-      xv[q] = *reinterpret_cast<const uint4*>(x + base + (static_cast<long long>(q / K) * wp + q % K) * c);
-    const uint4 dv = *reinterpret_cast<const uint4*>(dy + dyo);
-    const __nv_bfloat16* db = reinterpret_cast<const __nv_bfloat16*>(&dv);
+    for (int u = 0; u < RALPB_POOL_ILP; ++u) {
+      const int i = i0 + u * stride;
+      if (i >= total) break;
+      const int cg = i % cv;
+      int t = i / cv;
+      const int ox = t % ow;
+      t /= ow;
+      const int oy = t % oh;
+      const int img = t / oh;
+      base_u[u] = ((static_cast<long long>(img) * hp + oy * K + pi) * wp + ox * K + pi) * c + cg * 8;
+      const long long dyo =
+          ((static_cast<long long>(img) * (oh + 2 * po) + oy + po) * (ow + 2 * po) + ox + po) * c + cg * 8;
+#pragma unroll
+      for (int q = 0; q < K * K; ++q)
+        xv_u[u][q] = *reinterpret_cast<const uint4*>(x + base_u[u] + (static_cast<long long>(q / K) * wp + q % K) * c);
+      dv_u[u] = *reinterpret_cast<const uint4*>(dy + dyo);
+    }
+#pragma unroll
+    for (int u = 0; u < RALPB_POOL_ILP; ++u) {
+    if (i0 + u * stride >= total) break;
+    const long long base = base_u[u];
+    const uint4* xv = xv_u[u];
+    const __nv_bfloat16* db = reinterpret_cast<const __nv_bfloat16*>(&dv_u[u]);
     int arg[8];
     float best[8];
 #pragma unroll
@@ -381,6 +400,7 @@ __global__ void maxpool_bwd_disjoint_kernel(const __nv_bfloat16* __restrict__ x,
         if (hit) csum[e] += __bfloat162float(db[e]);
       }
       *reinterpret_cast<uint4*>(dx + base + (static_cast<long long>(q / K) * wp + q % K) * c) = out;
+    }
     }
   }
   if (colsum != nullptr) block_colsum_flush(csum, threadIdx.x % cv, c, s_col, colsum);
