@@ -1146,15 +1146,32 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
       // return every remote worker's rows of the cut gradient first, then the FC tail's
       // weight gradients and its (PS-local, never synchronised) update run on the aux
       // stream, overlapping this rank's front backward
-      for (int r = 0; r < m->world; ++r) {
-        if (r == m->rank) continue;
+      // (one launch for all peers; RALPB_SCATTER_FUSED=0: one push launch per peer)
+      const char* sf = getenv("RALPB_SCATTER_FUSED");
+      if (sf != nullptr && sf[0] == '0') {
+        for (int r = 0; r < m->world; ++r) {
+          if (r == m->rank) continue;
+          PeerSignal sig{};
+          sig.n = 1;
+          sig.flag[0] = at<uint32_t>(m, r, m->arena_off_flags) + kFlagActGrad;
+          RALPB_TRY(push_and_signal(at<bf16>(m, r, m->arena_off_dcut), m->dx_fc + static_cast<size_t>(r) * b * m->cut_elems,
+                                    static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + 8 + r, s));
+          ++m->launches;
+          m->phys_bytes += cut_bytes;
+        }
+      } else if (m->world > 1) {
+        PeerScatter sc{};
         PeerSignal sig{};
-        sig.n = 1;
-        sig.flag[0] = at<uint32_t>(m, r, m->arena_off_flags) + kFlagActGrad;
-        RALPB_TRY(push_and_signal(at<bf16>(m, r, m->arena_off_dcut), m->dx_fc + static_cast<size_t>(r) * b * m->cut_elems,
-                                  static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + 8 + r, s));
+        for (int r = 0; r < m->world; ++r) {
+          if (r == m->rank) continue;
+          sc.dst[sc.n] = at<bf16>(m, r, m->arena_off_dcut);
+          sc.src[sc.n] = m->dx_fc + static_cast<size_t>(r) * b * m->cut_elems;
+          ++sc.n;
+          sig.flag[sig.n++] = at<uint32_t>(m, r, m->arena_off_flags) + kFlagActGrad;
+          m->phys_bytes += cut_bytes;
+        }
+        RALPB_TRY(scatter_and_signal(sc, static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + 8 + m->rank, s));
         ++m->launches;
-        m->phys_bytes += cut_bytes;
       }
       // weight gradients on this stream (tensor/HBM work that would contend with the persistent
       // conv kernels), the HBM-bound update on the aux stream, overlapping the front backward

@@ -20,7 +20,7 @@ __device__ __forceinline__ void finish_and_signal(const PeerSignal& sig, const u
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t prev = atomicAdd(counter, 1u);
-    if (prev == gridDim.x - 1) {
+    if (prev == gridDim.x * gridDim.y - 1) {
       __threadfence_system();
       for (int i = 0; i < sig.n; ++i)
         if (sig.flag[i] != nullptr) st_release_sys(sig.flag[i], *value);
@@ -52,6 +52,42 @@ cudaError_t push_and_signal(void* dst, const void* src, long long n16, const Pee
     push_kernel<<<grid, 512, 0, s>>>(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), n16, sig,
                                      value, counter);
   }, s, KIND_PUSH, 16.0 * n16);
+  return cudaGetLastError();
+}
+
+// One launch for several destinations: blockIdx.y picks the (dst, src) pair, so the copies to
+// all peers are in flight together instead of one launch (and one drain) per peer.
+__global__ void scatter_kernel(PeerScatter sc, long long n16, PeerSignal sig, const uint32_t* value,
+                               uint32_t* counter) {
+  uint4* __restrict__ dst = reinterpret_cast<uint4*>(sc.dst[blockIdx.y]);
+  const uint4* __restrict__ src = reinterpret_cast<const uint4*>(sc.src[blockIdx.y]);
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    uint4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
+    dst[i] = a;
+    dst[i + stride] = b;
+    dst[i + 2 * stride] = c;
+    dst[i + 3 * stride] = d;
+  }
+  uint4 t[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    if (i + k * stride < n16) t[k] = src[i + k * stride];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    if (i + k * stride < n16) dst[i + k * stride] = t[k];
+  finish_and_signal(sig, value, counter);
+}
+
+cudaError_t scatter_and_signal(const PeerScatter& sc, long long n16, const PeerSignal& sig, const uint32_t* value,
+                               uint32_t* counter, cudaStream_t s) {
+  if (sc.n < 1 || sc.n > kMaxRanks) return cudaErrorInvalidValue;
+  const long long want = std::max<long long>(1, (2LL * num_sms() + sc.n - 1) / sc.n);
+  const int gx = static_cast<int>(std::max<long long>(1, std::min<long long>((n16 + 511) / 512, want)));
+  launch_timed([&] {
+    scatter_kernel<<<dim3(gx, sc.n), 512, 0, s>>>(sc, n16, sig, value, counter);
+  }, s, KIND_PUSH, 16.0 * n16 * sc.n);
   return cudaGetLastError();
 }
 

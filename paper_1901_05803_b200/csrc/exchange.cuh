@@ -25,6 +25,17 @@ struct PeerSignal {
   int n;
 };
 
+struct PeerScatter {
+  void* dst[kMaxRanks];
+  const void* src[kMaxRanks];
+  int n;
+};
+
+// dst[j] = src[j] (n16 chunks of 16 bytes each, j < sc.n) in one launch, then set every flag in
+// `sig` to `value` once all CTAs' stores are globally visible.
+cudaError_t scatter_and_signal(const PeerScatter& sc, long long n16, const PeerSignal& sig, const uint32_t* value,
+                               uint32_t* counter, cudaStream_t s);
+
 // dst = src (n16 chunks of 16 bytes), then set every flag in `sig` to `value`
 // once all CTAs' stores are globally visible (system scope).  `counter` is a
 // local zero-initialised word used for last-CTA detection.
