@@ -1,4 +1,5 @@
 #include <algorithm>
+#include <cstdlib>
 #include "exchange.cuh"
 #include "gemm_host.cuh"
 
@@ -45,8 +46,22 @@ __global__ void push_kernel(uint4* __restrict__ dst, const uint4* __restrict__ s
   finish_and_signal(sig, value, counter);
 }
 
+static int push_ctas_per_sm() {  // RALPB_PUSH_CTAS_PER_SM (A/B knob; default 2)
+  const char* e = getenv("RALPB_PUSH_CTAS_PER_SM");
+  const int v = e != nullptr ? atoi(e) : 2;
+  return v >= 1 && v <= 16 ? v : 2;
+}
+
 cudaError_t push_and_signal(void* dst, const void* src, long long n16, const PeerSignal& sig,
                             const uint32_t* value, uint32_t* counter, cudaStream_t s) {
+  const char* legacy = getenv("RALPB_PUSH_LEGACY");
+  if (legacy == nullptr || legacy[0] != '1') {
+    PeerScatter sc{};
+    sc.dst[0] = dst;
+    sc.src[0] = src;
+    sc.n = 1;
+    return scatter_and_signal(sc, n16, sig, value, counter, s);
+  }
   int grid = static_cast<int>(std::max<long long>(1, std::min<long long>((n16 + 511) / 512, num_sms() * 2)));
   launch_timed([&] {
     push_kernel<<<grid, 512, 0, s>>>(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), n16, sig,
@@ -83,7 +98,7 @@ __global__ void scatter_kernel(PeerScatter sc, long long n16, PeerSignal sig, co
 cudaError_t scatter_and_signal(const PeerScatter& sc, long long n16, const PeerSignal& sig, const uint32_t* value,
                                uint32_t* counter, cudaStream_t s) {
   if (sc.n < 1 || sc.n > kMaxRanks) return cudaErrorInvalidValue;
-  const long long want = std::max<long long>(1, (2LL * num_sms() + sc.n - 1) / sc.n);
+  const long long want = std::max<long long>(1, (static_cast<long long>(push_ctas_per_sm()) * num_sms() + sc.n - 1) / sc.n);
   const int gx = static_cast<int>(std::max<long long>(1, std::min<long long>((n16 + 511) / 512, want)));
   launch_timed([&] {
     scatter_kernel<<<dim3(gx, sc.n), 512, 0, s>>>(sc, n16, sig, value, counter);
