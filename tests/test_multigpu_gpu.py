@@ -20,6 +20,27 @@ def test_two_rank_parity():
     assert r.returncode == 0 and "MULTI-RANK PARITY PASS" in r.stdout
 
 
+def _parity(n: int, port: int, env_extra: dict) -> None:
+    import os
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "tests" / "multi_rank_parity.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env={**os.environ, **env_extra})
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0 and "MULTI-RANK PARITY PASS" in r.stdout
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_two_rank_parity_per_peer_pushes():
+    """The per-peer push kernels (RALPB_SCATTER_FUSED=0, RALPB_PUSH_LEGACY=1) give the same result."""
+    _parity(2, 29612, {"RALPB_SCATTER_FUSED": "0", "RALPB_PUSH_LEGACY": "1"})
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4, reason="needs >= 4 GPUs")
+def test_four_rank_parity_fused_scatter():
+    """W=4: the act-grad return to three workers in one scatter launch (exchange.cu scatter_kernel)."""
+    _parity(4, 29613, {})
+
+
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
 def test_cli_run_scenario_two_gpus(tmp_path):
     """`run` on a bundled two-worker scenario: layer-placed, all-on-PS and ring jobs executed on
