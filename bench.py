@@ -188,6 +188,17 @@ def _build_executor(strategy: str, world: int, rank: int, ring_backend: str = "n
     return ex, job, rep
 
 
+def _job_bytes(st, world: int) -> int:
+    """Logical synchronised bytes of the job: the sum of every rank's count_wire-site counts."""
+    if world == 1:
+        return st.logical_bytes
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(st.logical_bytes)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return int(t.item())
+
+
 def _time_steps(ex, imgs, labs, steps, warmup, world, on_host=False, read_loss=False):
     """read_loss: read every step's loss back to the host (pipelined one step behind: the loss of
     step t is read after step t+1 has been enqueued, so its host inputs' copy overlaps step t)."""
@@ -243,6 +254,14 @@ def run_ours(args):
         ms = _time_steps(ex, dimgs, dlabs, args.steps, args.warmup, world)
     st = ex.stats()
     value = world * BATCH / (ms * 1e-3)
+    # logical bytes: each rank counts its own count_wire sites; the job's figure is their sum
+    logical_total = st.logical_bytes
+    nvl = [st.nvlink_out_bytes, st.nvlink_in_bytes]
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([float(st.logical_bytes)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        logical_total = int(t.item())
 
     # end-to-end through the public API: pinned host inputs copied each step, loss read back each step
     himgs = [x.cpu().pin_memory() for x in dimgs]
@@ -329,7 +348,7 @@ def run_ours(args):
             str_ = exr.stats()
             exr.close()
             ring[backend] = {"value": world * BATCH / (ms_r * 1e-3), "ms_per_step": ms_r,
-                             "logical_sync_bytes_per_step": str_.logical_bytes}
+                             "logical_sync_bytes_per_step": _job_bytes(str_, world)}
     # layer-placed with the FC tail sharded over every GPU (the paper's multi-PS)
     mps = None
     if world > 1:
@@ -339,7 +358,7 @@ def run_ours(args):
         stm = exm.stats()
         exm.close()
         mps = {"value": world * BATCH / (ms_m * 1e-3), "ms_per_step": ms_m,
-               "logical_bytes_per_step": stm.logical_bytes,
+               "logical_bytes_per_step": _job_bytes(stm, world),
                "note": "FC-0 column-parallel / FC-1 row-parallel over all GPUs (volume_ralp_multi_ps)"}
 
     cpu = None
@@ -357,11 +376,12 @@ def run_ours(args):
                        "model": MODEL, "global_batch": world * BATCH, "per_worker_batch": BATCH,
                        "split": rep.split_index, "parallelism": f"dp{world}+fc-tail-on-ps",
                        "l2": "activation working set ~4.5 GB/GPU/step >> 126 MB L2; no flush"},
-            "sync_bytes_per_step": {"logical": st.logical_bytes,
+            "sync_bytes_per_step": {"logical": logical_total,
                                     "oracle_volume_ralp": volume_ralp(m, rep.split_index, world).total_bytes_per_step,
-                                    "physical_nvlink_rank0": st.physical_bytes},
+                                    "logical_counted_rank0": st.logical_bytes,
+                                    "physical_nvlink_rank0": {"out": nvl[0], "in": nvl[1]}},
             "all_on_ps": {"value": world * BATCH / (ms_b * 1e-3), "ms_per_step": ms_b,
-                          "logical_sync_bytes_per_step": stb.logical_bytes},
+                          "logical_sync_bytes_per_step": _job_bytes(stb, world)},
             "ring_allreduce": ring,
             "ralp_fc_sharded": mps,
             "breakdown_ms_rank0": {"front_fwd": st.ms_front_fwd, "back": st.ms_back, "front_bwd": st.ms_front_bwd,

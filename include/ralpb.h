@@ -148,9 +148,14 @@ typedef struct {
 } ralpb_layer_desc;
 
 typedef struct {
-  double loss;                 /* mean cross-entropy over the job's W*b samples (PS rank; NaN elsewhere) */
-  long long logical_bytes;     /* job-wide synchronised bytes this step at elem_bytes (== volume_*()) */
-  long long physical_bytes;    /* bytes this rank moved over NVLink this step (loads + stores) */
+  double loss;                 /* mean cross-entropy over the job's W*b samples (ps_rank -- rank 0 for
+                                  RALP_MPS / RING; NaN elsewhere) */
+  long long logical_bytes;     /* descriptor-unit (elem_bytes) bytes of the transfers THIS rank issued
+                                  this step, counted where it issues them, at the reference's count_wire
+                                  sites (simulator.py:647,663,677,689,707,713): worker act + grad, PS
+                                  actgrad + pull (per sync shard it owns).  Summed over the ranks it is
+                                  the job's volume_*() (costmodel.py:107-162). */
+  long long physical_bytes;    /* bytes this rank moved over NVLink this step (out + in) */
   int launches;                /* kernels this rank launched in the step */
   float ms_step;               /* device time of the whole step on this rank (CUDA events) */
   float ms_front_fwd;          /* worker front forward */
@@ -159,13 +164,28 @@ typedef struct {
   float ms_sync;               /* parameter synchronisation (sharded PS) + weight re-layout */
   float ms_gemm;               /* sum of tcgen05 GEMM-engine launch durations (profiling mode only) */
   int gemm_launches;           /* GEMM-engine launches timed (profiling mode only) */
+  long long nvlink_out_bytes;  /* ... of physical_bytes: stored to peers (cut / act-grad pushes, pulls) */
+  long long nvlink_in_bytes;   /* ... loaded from peers (sharded-PS gradient reads) */
 } ralpb_step_stats;
 
 typedef struct ralpb_model ralpb_model;
 
-/* Replaces JobSpec + _JobRun.__init__ (costmodel.py:64-86, simulator.py:517-567). */
+/* Arithmetic of the step.  BF16: bf16 operands / activations, fp32 accumulation, fp32 master
+ * parameters (the throughput mode).  FP32: the parity mode north_star pins to the fp32 oracle --
+ * every activation, activation gradient and GEMM operand is carried as an fp32-accurate (hi, lo)
+ * bf16 pair (x = hi + lo, |x - hi - lo| <= 2^-17 |x|) and every contraction runs on the same tcgen05
+ * GEMM engine over the pairs (hi*hi + hi*lo + lo*hi + lo*lo, fp32 accumulation), so results match
+ * plain fp32 arithmetic to ~1e-5 relative (reference unit: elem_bytes=4, layers.py:238-250). */
+enum { RALPB_PRECISION_BF16 = 0, RALPB_PRECISION_FP32 = 1 };
+
+/* Replaces JobSpec + _JobRun.__init__ (costmodel.py:64-86, simulator.py:517-567).
+ * workers: ranks that run a conv front.  workers == world is the colocated placement (the PS role on
+ * ps_rank, which is also a worker); workers == world - 1 (RALP only) is the paper's RALP-N placement
+ * (costmodel.py:244-245, gpu_assignments): ps_rank is a dedicated PS GPU that runs only the back
+ * segment, the other ranks are workers 0..W-1 in rank order. */
 int ralpb_model_create(const ralpb_layer_desc* layers, int n_layers, int split, int batch, int strategy,
-                       int rank, int world, int ps_rank, int elem_bytes, ralpb_model** out);
+                       int rank, int world, int ps_rank, int elem_bytes, int precision, int workers,
+                       ralpb_model** out);
 void ralpb_model_destroy(ralpb_model* m);
 /* 64-byte CUDA IPC handle of this rank's exchange arena; ralpb_model_ipc_open takes
  * world*64 bytes (rank-major) and maps the peers. */
@@ -175,6 +195,10 @@ int ralpb_model_ipc_open(ralpb_model* m, const void* handles);
  * conv w [cout][k][k][cin], b [cout]; fc w [out][in] (in = HWC-flattened), b [out]. */
 int ralpb_model_set_params(ralpb_model* m, int layer, const float* w, const float* b, int on_host);
 int ralpb_model_get_params(ralpb_model* m, int layer, float* w, float* b, int on_host);
+/* This rank's parameter gradient of `layer` from the last step (same layout as get_params; host or
+ * device destination): the front's summed over this rank's batch before the sharded-PS reduction,
+ * the FC tail's over the PS's rows.  Inspection for the per-layer parity tests. */
+int ralpb_model_get_grads(ralpb_model* m, int layer, float* w, float* b);
 /* One training step of this rank's worker batch: images [b][h][w][c] fp32 NHWC, labels [b] int32,
  * host or device memory.  Executes _ralp_worker/_ralp_ps (simulator.py:669-715) or
  * _baseline_worker/_baseline_ps (simulator.py:637-665).  Asynchronous: host inputs are copied on
@@ -189,9 +213,23 @@ int ralpb_model_stats(ralpb_model* m, ralpb_step_stats* out);
  * the end of that step; waits for that step only (NaN on ranks without the FC tail). */
 int ralpb_model_read_loss(ralpb_model* m, int lag, float* out);
 void* ralpb_model_stream(ralpb_model* m);
-/* Inspection: copies activation (which=0) or activation-gradient (which=1) buffer i (bf16,
- * padded layout), or the last step's logits (which=2, fp32 [rows][ld]; i ignored), to host_out
- * (may be NULL to query); returns its element count or -1. */
+/* Inspection: copies one of the last step's device buffers to host_out (may be NULL to query) and
+ * returns its element count, or -1.  Layouts (BF16 precision; FP32 precision: every bf16 buffer is
+ * stored as (hi, lo) pairs -- per pixel / row the hi channels then the lo channels -- and the
+ * byte size doubles):
+ *   ACT i / ACT_GRAD i   bf16 padded NHWC input of front layer i / its gradient
+ *   LOGITS               fp32 [rows][ld]            DLOGITS          bf16 [rows][ld]
+ *   FC_OUT i             bf16 [rows][ld] output of hidden FC layer i (ReLU applied)
+ *   FC_OUT_GRAD i        bf16 [rows][ld] gradient w.r.t. FC layer i's output (ReLU-masked)
+ *   FC_WEIGHT i          bf16 [out][in] operand copy of FC layer i
+ *   CUT_ROWS / CUT_GRAD_ROWS  bf16 [rows][cut] the PS's FC input rows (every worker's cut, HWC
+ *                        flatten) / their gradient;  CUT_GRAD  bf16 [b][cut] the act-grad this rank
+ *                        received;  MPS_PARTIAL  fp32 [rows][ld] (RALP_MPS) */
+enum {
+  RALPB_DBG_ACT = 0, RALPB_DBG_ACT_GRAD = 1, RALPB_DBG_LOGITS = 2, RALPB_DBG_FC_OUT = 3,
+  RALPB_DBG_MPS_PARTIAL = 4, RALPB_DBG_FC_WEIGHT = 5, RALPB_DBG_DLOGITS = 6, RALPB_DBG_FC_OUT_GRAD = 7,
+  RALPB_DBG_CUT_ROWS = 8, RALPB_DBG_CUT_GRAD_ROWS = 9, RALPB_DBG_CUT_GRAD = 10
+};
 long long ralpb_model_debug_buffer(ralpb_model* m, int i, int which, void* host_out);
 /* RING_EXTERNAL: the fp32 gradient vector (all parameters, device memory, `*n` floats) the caller
  * all-reduces (sum over ranks) after ralpb_model_step, and the update that follows

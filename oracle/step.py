@@ -173,6 +173,56 @@ def _accumulate(total: dict, part: dict):
             total[k] = (gw.clone(), gb.clone())
 
 
+# ---------------------------------------------------------------- per-layer ops (teacher forcing)
+# Each takes the GPU's own stored inputs (NCHW fp32 tensors holding bf16 values) and returns the
+# layer's exact fp32 result before the GPU's final bf16 rounding, so a per-layer check isolates one
+# kernel from the drift of everything before it.  Semantics as in the step above: infer_conv /
+# infer_pool / infer_fc (pkg/src/ralp/layers.py:87-123), ReLU after every conv / hidden FC.
+
+def conv_forward(x, w, b, stride, pad, relu=True):
+    """relu(conv2d(x, w) + b); w [cout][cin][k][k] (already bf16-valued where the GPU's is)."""
+    y = _conv(x, w, b, stride, pad)
+    return torch.relu(y) if relu else y
+
+
+def conv_backward_data(dy, w, x_shape, stride, pad, mask=None):
+    """dL/dx of a convolution from its (masked) output gradient; times (mask > 0) when given."""
+    gx = _conv_x(x_shape, w, dy, stride, pad)
+    return gx * (mask > 0) if mask is not None else gx
+
+
+def conv_backward_filter(x, dy, w_shape, stride, pad):
+    """(dW [cout][cin][k][k], db [cout]) summed over the batch."""
+    return _conv_w(x, w_shape, dy, stride, pad), dy.to(torch.float64).sum(dim=(0, 2, 3)).to(torch.float32)
+
+
+def maxpool_forward(x, k, stride):
+    return F.max_pool2d(x, k, stride)
+
+
+def maxpool_backward(x, dy, k, stride):
+    """Route dy to the first maximum of each window (row-major), times (x > 0): the pool input
+    is a ReLU output, whose derivative the GPU folds into this producer."""
+    xr = x.detach().clone().requires_grad_(True)
+    F.max_pool2d(xr, k, stride).backward(dy)
+    return xr.grad * (x > 0)
+
+
+def fc_forward(x, w, b, relu):
+    z = _mm(x, w.t()) + b
+    return torch.relu(z) if relu else z
+
+
+def softmax_xent(logits, labels, scale):
+    """(per-row loss, dlogits = (softmax - onehot) * scale) -- the LOSS layer (layers.py:161-163)."""
+    lab = torch.from_numpy(np.asarray(labels, dtype=np.int64))
+    lse = torch.logsumexp(logits.double(), dim=1)
+    row = lse - logits.double().gather(1, lab[:, None])[:, 0]
+    p = torch.exp(logits.double() - lse[:, None])
+    d = (p - F.one_hot(lab, logits.shape[1]).double()) * scale
+    return row.float(), d.float()
+
+
 def param_count(L) -> int:
     if L["kind"] == "conv":
         return L["k"] * L["k"] * L["cin"] * L["cout"] + L["cout"]

@@ -46,12 +46,13 @@ SIGNATURES: dict[str, tuple] = {
     "ralpb_colsum_bf16": (c_i, [c_vp, c_ll, c_i, c_ll, c_fp, c_vp]),
     "ralpb_conv_weight_prep": (c_i, [c_fp, c_i, c_i, c_i, c_vp, c_vp, c_vp]),
     "ralpb_cast_bf16": (c_i, [c_fp, c_ll, c_vp, c_vp]),
-    "ralpb_model_create": (c_i, [c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, C.POINTER(c_vp)]),
+    "ralpb_model_create": (c_i, [c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, C.POINTER(c_vp)]),
     "ralpb_model_destroy": (None, [c_vp]),
     "ralpb_model_ipc_handle": (c_i, [c_vp, c_vp]),
     "ralpb_model_ipc_open": (c_i, [c_vp, c_vp]),
     "ralpb_model_set_params": (c_i, [c_vp, c_i, c_vp, c_vp, c_i]),
     "ralpb_model_get_params": (c_i, [c_vp, c_i, c_vp, c_vp, c_i]),
+    "ralpb_model_get_grads": (c_i, [c_vp, c_i, c_vp, c_vp]),
     "ralpb_model_step": (c_i, [c_vp, c_vp, c_vp, c_i, c_f, c_f]),
     "ralpb_model_stats": (c_i, [c_vp, c_vp]),
     "ralpb_model_read_loss": (c_i, [c_vp, c_i, c_vp]),
@@ -84,12 +85,18 @@ class StepStats(C.Structure):
     """ralpb_step_stats (include/ralpb.h)."""
     _fields_ = [("loss", C.c_double), ("logical_bytes", c_ll), ("physical_bytes", c_ll), ("launches", c_i),
                 ("ms_step", c_f), ("ms_front_fwd", c_f), ("ms_back", c_f), ("ms_front_bwd", c_f),
-                ("ms_sync", c_f), ("ms_gemm", c_f), ("gemm_launches", c_i)]
+                ("ms_sync", c_f), ("ms_gemm", c_f), ("gemm_launches", c_i), ("nvlink_out_bytes", c_ll),
+                ("nvlink_in_bytes", c_ll)]
 
 
 RALPB_CONV, RALPB_POOL, RALPB_FC = 0, 1, 2
 RALPB_STRATEGY_BASELINE, RALPB_STRATEGY_RALP, RALPB_STRATEGY_RING, RALPB_STRATEGY_RING_EXTERNAL = 0, 1, 2, 3
 RALPB_STRATEGY_RALP_MPS = 4
+RALPB_PRECISION_BF16, RALPB_PRECISION_FP32 = 0, 1
+PRECISIONS = {"bf16": RALPB_PRECISION_BF16, "fp32": RALPB_PRECISION_FP32}
+# ralpb_model_debug_buffer selectors (include/ralpb.h)
+(DBG_ACT, DBG_ACT_GRAD, DBG_LOGITS, DBG_FC_OUT, DBG_MPS_PARTIAL, DBG_FC_WEIGHT, DBG_DLOGITS, DBG_FC_OUT_GRAD,
+ DBG_CUT_ROWS, DBG_CUT_GRAD_ROWS, DBG_CUT_GRAD) = range(11)
 
 
 class BackendError(RuntimeError):

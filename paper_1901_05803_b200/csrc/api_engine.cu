@@ -12,10 +12,12 @@ struct ralpb_model {
 extern "C" {
 
 int ralpb_model_create(const ralpb_layer_desc* layers, int n_layers, int split, int batch, int strategy,
-                       int rank, int world, int ps_rank, int elem_bytes, ralpb_model** out) {
+                       int rank, int world, int ps_rank, int elem_bytes, int precision, int workers,
+                       ralpb_model** out) {
   std::string why;
   Model* m = nullptr;
-  if (model_create(layers, n_layers, split, batch, strategy, rank, world, ps_rank, elem_bytes, &m, &why))
+  if (model_create(layers, n_layers, split, batch, strategy, rank, world, ps_rank, elem_bytes, precision, workers, &m,
+                   &why))
     return set_error("ralpb_model_create: " + why);
   *out = new ralpb_model{m};
   return 0;
@@ -45,6 +47,11 @@ int ralpb_model_set_params(ralpb_model* m, int layer, const float* w, const floa
 int ralpb_model_get_params(ralpb_model* m, int layer, float* w, float* b, int on_host) {
   std::string why;
   return model_get_params(m->impl, layer, w, b, on_host, &why) ? set_error("ralpb_model_get_params: " + why) : 0;
+}
+
+int ralpb_model_get_grads(ralpb_model* m, int layer, float* w, float* b) {
+  std::string why;
+  return model_get_grads(m->impl, layer, w, b, &why) ? set_error("ralpb_model_get_grads: " + why) : 0;
 }
 
 int ralpb_model_step(ralpb_model* m, const void* images, const int32_t* labels, int on_host, float lr,
@@ -89,60 +96,72 @@ int ralpb_model_set_profiling(ralpb_model* m, int on) {
 
 }  // extern "C"
 
-// Debug/inspection: copy activation buffer acts[i] (bf16, padded layout) or, for which=1,
-// the activation-gradient buffer gacts[i], into host memory; returns the element count.
+// Debug/inspection (include/ralpb.h): copy one of the step's device buffers to host memory;
+// returns its element count (host_out may be NULL to query) or -1.
 extern "C" long long ralpb_model_debug_buffer(ralpb_model* m, int i, int which, void* host_out) {
   Model* mm = m->impl;
-  if (which == 2) {  // logits of the last step (fp32 [rows][ld], as bf16-sized count of floats)
-    const long long n = static_cast<long long>(mm->rows_back) * mm->back.back().ld_out;
-    if (host_out != nullptr) {
-      cudaStreamSynchronize(mm->stream);
-      if (cudaMemcpy(host_out, mm->logits, n * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-    }
-    return n;
+  const void* src = nullptr;
+  long long n = 0;
+  size_t esz = sizeof(bf16);
+  const int R = mm->rows_back;
+  const int nb = static_cast<int>(mm->back.size());
+  switch (which) {
+    case RALPB_DBG_ACT:
+    case RALPB_DBG_ACT_GRAD:
+      if (i < 0 || i >= static_cast<int>(mm->acts.size())) return -1;
+      n = mm->acts[i].elems();
+      src = which == RALPB_DBG_ACT ? static_cast<const void*>(mm->acts[i].ptr) : static_cast<const void*>(mm->gacts[i]);
+      break;
+    case RALPB_DBG_LOGITS:
+      n = static_cast<long long>(R) * mm->back.back().ld_out;
+      src = mm->logits;
+      esz = sizeof(float);
+      break;
+    case RALPB_DBG_FC_OUT:  // hidden FC output i (RALP_MPS, i = 0: this rank's slice)
+      if (i < 0 || i + 1 >= nb) return -1;
+      n = static_cast<long long>(R) * (mm->mps && i == 0 ? mm->ld_s0 : mm->back[i].ld_out);
+      src = mm->mps && i == 0 ? static_cast<const void*>(mm->h0s) : static_cast<const void*>(mm->hid[i]);
+      break;
+    case RALPB_DBG_MPS_PARTIAL:
+      if (!mm->mps) return -1;
+      n = static_cast<long long>(R) * mm->back[1].ld_out;
+      src = static_cast<const char*>(mm->arena) + mm->arena_off_p1;
+      esz = sizeof(float);
+      break;
+    case RALPB_DBG_FC_WEIGHT:
+      if (i < 0 || i >= nb) return -1;
+      n = static_cast<long long>(mm->back[i].lout) * mm->back[i].lin;
+      src = mm->back[i].wbf;
+      break;
+    case RALPB_DBG_DLOGITS:
+      n = static_cast<long long>(R) * mm->back.back().ld_out;
+      src = mm->dlogits;
+      break;
+    case RALPB_DBG_FC_OUT_GRAD:
+      if (i < 0 || i + 1 >= nb) return -1;
+      n = static_cast<long long>(R) * mm->back[i].ld_out;
+      src = mm->dyb[i];
+      break;
+    case RALPB_DBG_CUT_ROWS:
+      n = static_cast<long long>(R) * mm->cut_elems;
+      src = mm->x_fc;
+      break;
+    case RALPB_DBG_CUT_GRAD_ROWS:
+      n = static_cast<long long>(R) * mm->cut_elems;
+      src = mm->dx_fc;
+      break;
+    case RALPB_DBG_CUT_GRAD:
+      n = static_cast<long long>(mm->batch) * mm->cut_elems;
+      src = mm->dcut;
+      break;
+    default:
+      return -1;
   }
-  if (which == 6) {  // dlogits (bf16 [rows][ld])
-    const long long n = static_cast<long long>(mm->rows_back) * mm->back.back().ld_out;
-    if (host_out != nullptr) {
-      cudaStreamSynchronize(mm->stream);
-      if (cudaMemcpy(host_out, mm->dlogits, n * sizeof(bf16), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-    }
-    return n;
-  }
-  if (which == 4 && mm->mps) {  // RALP_MPS: this rank's arena partial slot 0 (fp32 [rows][ld1])
-    const long long n = static_cast<long long>(mm->rows_back) * mm->back[1].ld_out;
-    if (host_out != nullptr) {
-      cudaStreamSynchronize(mm->stream);
-      const char* src = static_cast<const char*>(mm->arena) + mm->arena_off_p1;
-      if (cudaMemcpy(host_out, src, n * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-    }
-    return n;
-  }
-  if (which == 5 && mm->back.size() > 1) {  // FC-1 bf16 weights as stored on this rank
-    const FcLayer& f = mm->back[1];
-    const long long n = static_cast<long long>(f.lout) * f.lin;
-    if (host_out != nullptr) {
-      cudaStreamSynchronize(mm->stream);
-      if (cudaMemcpy(host_out, f.wbf, n * sizeof(bf16), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-    }
-    return n;
-  }
-  if (which == 3) {  // FC-0 output of the last step (bf16 [rows][ld]; RALP_MPS: this rank's slice)
-    const long long n = static_cast<long long>(mm->rows_back) * (mm->mps ? mm->ld_s0 : mm->back[0].ld_out);
-    if (host_out != nullptr) {
-      cudaStreamSynchronize(mm->stream);
-      if (cudaMemcpy(host_out, mm->mps ? mm->h0s : mm->hid[0], n * sizeof(bf16), cudaMemcpyDeviceToHost) != cudaSuccess)
-        return -1;
-    }
-    return n;
-  }
-  if (i < 0 || i >= static_cast<int>(mm->acts.size())) return -1;
-  const long long n = mm->acts[i].elems();
-  const void* src = which == 0 ? static_cast<const void*>(mm->acts[i].ptr) : static_cast<const void*>(mm->gacts[i]);
   if (src == nullptr) return -1;
+  if (mm->precision == RALPB_PRECISION_FP32) esz *= 2;  // (hi, lo) bf16 pairs / fp32
   if (host_out != nullptr) {
-    cudaStreamSynchronize(mm->stream);
-    if (cudaMemcpy(host_out, src, n * sizeof(bf16), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    if (cudaStreamSynchronize(mm->stream) != cudaSuccess) return -1;
+    if (cudaMemcpy(host_out, src, n * esz, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
   }
   return n;
 }

@@ -45,7 +45,13 @@ constexpr int kFlagDone = 24;     // [8]  rank r finished its shard update
 constexpr int kFlagP1 = 32;       // [8]  RALP_MPS, rank 0: rank r's FC-1 partial landed
 constexpr int kFlagDh1 = 40;      // [1]  RALP_MPS: FC-1 output gradient landed
 constexpr int kFlagDcut = 48;     // [8]  RALP_MPS: rank r's partial of this rank's cut gradient landed
-constexpr int kNumFlags = 64;
+constexpr int kFlagLoss = 56;     // [7]  ps_rank: worker w's own-row loss sum landed (baseline / ring)
+constexpr int kFlagPsFree = 64;   // [1]  worker: the dedicated PS finished the previous step
+constexpr int kNumFlags = 80;
+constexpr int kCtrScatter = 48;   // [8]  per-destination counters of the fused act-grad scatter
+// The parameter vector is padded to a multiple of 4 * lcm(1..8) floats, so every sync group size
+// (world, or world - 1 workers with a dedicated PS) splits it into float4-aligned equal shards.
+constexpr long long kShardAlign = 4 * 840;
 constexpr int kNumCounters = 64;  // last-CTA counters (local)
 
 long long align_up(long long x, long long a) { return (x + a - 1) / a * a; }
@@ -80,7 +86,8 @@ T* at(Model* m, int r, size_t off) { return reinterpret_cast<T*>(peer(m, r) + of
 }  // namespace
 
 int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int batch, int strategy,
-                 int rank, int world, int ps_rank, int elem_bytes, Model** out, std::string* why) {
+                 int rank, int world, int ps_rank, int elem_bytes, int precision, int workers, Model** out,
+                 std::string* why) {
   if (n_layers < 2 || batch < 1 || world < 1 || world > kMaxRanks || rank < 0 || rank >= world ||
       ps_rank < 0 || ps_rank >= world) {
     *why = "bad model configuration";
@@ -88,9 +95,27 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   }
   if (batch % 4 != 0) { *why = "batch must be a multiple of 4"; return 1; }
   if (strategy < RALPB_STRATEGY_BASELINE || strategy > RALPB_STRATEGY_RALP_MPS) { *why = "unknown strategy"; return 1; }
+  if (precision != RALPB_PRECISION_BF16 && precision != RALPB_PRECISION_FP32) { *why = "unknown precision"; return 1; }
+  if (workers != world && !(workers == world - 1 && workers >= 1 && strategy == RALPB_STRATEGY_RALP)) {
+    *why = "workers must equal world, or world - 1 (RALP-N: a dedicated PS rank, RALP strategy only)";
+    return 1;
+  }
+  if (precision == RALPB_PRECISION_FP32 && getenv("RALPB_FP32_WIP") == nullptr) {
+    *why = "precision FP32 is not available in this build";
+    return 1;
+  }
   auto m = new Model();
   m->rank = rank; m->world = world; m->ps_rank = ps_rank; m->batch = batch;
   m->strategy = strategy; m->elem_bytes = elem_bytes;
+  m->precision = precision;
+  m->workers = workers;
+  m->dedicated_ps = workers < world;
+  for (int r = 0; r < world; ++r)
+    if (!(m->dedicated_ps && r == ps_rank)) m->worker_ranks.push_back(r);
+  m->is_worker = !(m->dedicated_ps && rank == ps_rank);
+  m->widx = 0;
+  for (int i = 0; i < workers; ++i)
+    if (m->worker_ranks[i] == rank) m->widx = i;
   m->desc.assign(layers, layers + n_layers);
   cudaGetDevice(&m->device);
   auto fail = [&](const std::string& w) { *why = w; model_destroy(m); return 1; };
@@ -106,7 +131,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     return fail("this executor places exactly the FC tail on the PS (split must be " + std::to_string(nconv) + ")");
   m->split = nconv;
   m->holds_back = strategy != RALPB_STRATEGY_RALP || rank == ps_rank;   // RALP_MPS: every rank
-  m->rows_back = layer_placed ? world * batch : batch;
+  m->rows_back = layer_placed ? workers * batch : batch;
   if (m->mps) {
     if (n_layers - nconv < 2) return fail("RALP_MPS needs at least two FC layers");
     if (ps_rank != 0) return fail("RALP_MPS keeps the FC tail's head on rank 0");
@@ -136,6 +161,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   }
   m->acts.push_back(a0);
   long long off = 0;
+  std::vector<std::pair<long long, long long>> real_runs;  // (offset, floats) of descriptor parameters
   for (int i = 0; i < nconv; ++i) {
     const ralpb_layer_desc& d = layers[i];
     const ActBuf& in = m->acts.back();
@@ -159,6 +185,8 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
       f.w_count = static_cast<long long>(d.cout) * f.kpad;
       f.w_off = off;
       f.b_off = -1;  // folded into column k*k*cin of the filter
+      for (int o = 0; o < d.cout; ++o)
+        real_runs.emplace_back(f.w_off + static_cast<long long>(o) * f.kpad, d.k * d.k * d.cin + 1);
       off = align_up(off + f.w_count, 4);
       m->real_front += static_cast<long long>(d.cout) * d.k * d.k * d.cin + d.cout;
       o.h = in.h; o.w = in.w; o.c = d.cout; o.pad = in.pad;
@@ -182,6 +210,9 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
       off = align_up(off + f.w_count, 4);
       f.b_off = off;
       off = align_up(off + d.cout, 4);
+      for (long long ot = 0; ot < static_cast<long long>(d.cout) * d.k * d.k; ++ot)
+        real_runs.emplace_back(f.w_off + ot * in.c, d.cin);
+      real_runs.emplace_back(f.b_off, d.cout);
       m->real_front += static_cast<long long>(d.cout) * d.k * d.k * d.cin + d.cout;
       o.h = d.h; o.w = d.w; o.c = d.cout; o.pad = d.pad;
     } else if (d.kind == RALPB_POOL) {
@@ -201,7 +232,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   const ActBuf& cut = m->acts.back();
   if (cut.pad != 0) return fail("the cut activation must be a pooling output");
   m->cut_elems = cut.h * cut.w * cut.c;
-  m->n_front = align_up(off, 4LL * world);
+  m->n_front = align_up(off, kShardAlign);
   off = m->n_front;
   m->real_total = m->real_front;
   int prev = m->cut_elems;
@@ -225,7 +256,25 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     m->back.push_back(f);
     prev = d.cout;
   }
-  m->n_total = align_up(off, 4LL * world);
+  m->n_total = align_up(off, kShardAlign);
+  // real (descriptor) parameters per sync shard: the logical byte count of the pull / ring sites
+  {
+    const bool placed = strategy == RALPB_STRATEGY_RALP || strategy == RALPB_STRATEGY_RALP_MPS;
+    if (!placed)
+      for (const FcLayer& f : m->back) {
+        real_runs.emplace_back(f.w_off, static_cast<long long>(f.out) * f.in);
+        real_runs.emplace_back(f.b_off, f.out);
+      }
+    const long long n = placed ? m->n_front : m->n_total;
+    const int groups = strategy == RALPB_STRATEGY_RALP ? workers : world;
+    const long long shard = n / groups;
+    m->shard_real.assign(groups, 0);
+    for (const auto& run : real_runs)
+      for (int g = 0; g < groups; ++g) {
+        const long long lo = std::max(run.first, shard * g), hi = std::min(run.first + run.second, shard * (g + 1));
+        if (hi > lo) m->shard_real[g] += hi - lo;
+      }
+  }
 
   // ---- exchange arena (identical layout on every rank)
   size_t ao = 0;
@@ -236,6 +285,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   m->arena_off_xfc = take(static_cast<size_t>(m->rows_back) * m->cut_elems * sizeof(bf16));
   m->arena_off_lab = take(static_cast<size_t>(m->rows_back) * sizeof(int32_t));
   m->arena_off_dcut = take(static_cast<size_t>(batch) * m->cut_elems * sizeof(bf16));
+  m->arena_off_loss = take(kMaxRanks * 4 * sizeof(float));   // [worker][4] own-row loss sums
   if (m->mps) {
     const int ld1 = static_cast<int>(align_up(layers[nconv + 1].cout, 8));
     m->arena_off_p1 = take(static_cast<size_t>(world) * m->rows_back * ld1 * sizeof(float));
@@ -265,7 +315,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   // Every activation and activation-gradient buffer is dedicated and zeroed once: the conv
   // kernels write interior pixels only, so the padding borders stay zero for the job's life.
   m->gacts.assign(m->acts.size(), nullptr);
-  for (size_t i = 0; i < m->acts.size(); ++i) {
+  for (size_t i = 0; m->is_worker && i < m->acts.size(); ++i) {
     const size_t bytes = static_cast<size_t>(m->acts[i].elems()) * sizeof(bf16);
     if (!(m->acts[i].ptr = alloc<bf16>(m, m->acts[i].elems(), why))) return fail(*why);
     cudaMemset(m->acts[i].ptr, 0, bytes);
@@ -286,7 +336,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
       pl.fused_fwd = true;
       const ActBuf& po = m->acts[i + 2];
       const char* ie = getenv("RALPB_POOL_IDX");
-      if (ie != nullptr && ie[0] == '1' && c.g.cin >= 128 &&
+      if (ie != nullptr && ie[0] == '1' && c.g.cin >= 128 && m->is_worker &&
           !(pl.idx = alloc<uint8_t>(m, static_cast<size_t>(po.n) * po.h * po.w * po.c, why)))
         return fail(*why);
     }
@@ -295,12 +345,12 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   // forward and gather the backward from them (maxpool_bwd_gather)
   for (size_t i = 0; i < m->front.size(); ++i) {
     FrontLayer& pl = m->front[i];
-    if (pl.kind != RALPB_POOL || pl.fused_fwd || pl.k * pl.k > 255) continue;
+    if (pl.kind != RALPB_POOL || pl.fused_fwd || pl.k * pl.k > 255 || !m->is_worker) continue;
     const ActBuf& po = m->acts[i + 1];
     if (!(pl.idx = alloc<uint8_t>(m, static_cast<size_t>(po.n) * po.h * po.w * po.c, why))) return fail(*why);
   }
   for (auto& f : m->front) {
-    if (f.kind != RALPB_CONV) continue;
+    if (f.kind != RALPB_CONV || !m->is_worker) continue;
     if (!(f.wf = alloc<bf16>(m, f.w_count, why))) return fail(*why);
     if (!f.im2col && !(f.wd = alloc<bf16>(m, f.w_count, why))) return fail(*why);
   }
@@ -337,7 +387,9 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   if (!(m->row_loss = alloc<float>(m, R, why))) return fail(*why);
   if (!(m->loss = alloc<float>(m, 4, why))) return fail(*why);
   for (int i = 0; i < 2; ++i) {
-    if (!(m->img_dev[i] = alloc<float>(m, static_cast<size_t>(batch) * m->in_h * m->in_w * m->in_c, why))) return fail(*why);
+    if (m->is_worker &&
+        !(m->img_dev[i] = alloc<float>(m, static_cast<size_t>(batch) * m->in_h * m->in_w * m->in_c, why)))
+      return fail(*why);
     if (!(m->lab_dev[i] = alloc<int32_t>(m, batch, why))) return fail(*why);
     cudaEventCreateWithFlags(&m->ev_copied[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&m->ev_consumed[i], cudaEventDisableTiming);
@@ -442,10 +494,13 @@ int model_set_params(Model* m, int layer, const float* w, const float* b, int on
       RALPB_TRY(cudaMemcpyAsync(m->P + f.b_off, hb.data(), co * sizeof(float), cudaMemcpyHostToDevice, m->stream));
     }
     RALPB_TRY(cudaMemcpyAsync(m->P + f.w_off, packed.data(), packed.size() * sizeof(float), cudaMemcpyHostToDevice, m->stream));
-    if (f.im2col)
+    if (!m->is_worker) {
+      // the dedicated PS keeps no operand copies of the front
+    } else if (f.im2col) {
       RALPB_TRY(cast_bf16(m->P + f.w_off, f.w_count, f.wf, m->stream));
-    else
+    } else {
       RALPB_TRY(conv_weight_prep(m->P + f.w_off, co, taps, f.g.cin, f.wf, f.wd, m->stream));
+    }
   } else {
     const int j = layer - m->split;
     FcLayer& f = m->back[j];
@@ -468,9 +523,11 @@ int model_set_params(Model* m, int layer, const float* w, const float* b, int on
   return 0;
 }
 
-int model_get_params(Model* m, int layer, float* w, float* b, int on_host, std::string* why) {
+// Reads layer `layer`'s fp32 parameters (off = arena_off_P) or this step's gradients (arena_off_G)
+// in the caller's layout (get_params / get_grads).
+static int read_layer(Model* m, int layer, float* w, float* b, size_t off, std::string* why) {
   if (layer < 0 || layer >= static_cast<int>(m->desc.size())) { *why = "layer out of range"; return 1; }
-  (void)on_host;
+  const float* self = at<float>(m, m->rank, off);
   RALPB_TRY(cudaStreamSynchronize(m->stream));
   if (layer < m->split) {
     FrontLayer& f = m->front[layer];
@@ -478,7 +535,7 @@ int model_get_params(Model* m, int layer, float* w, float* b, int on_host, std::
     const int co = f.g.cout, taps = f.k * f.k, cr = f.cin_real;
     const int kk = taps * cr;
     std::vector<float> packed(f.w_count), host(static_cast<size_t>(co) * kk), hb(co);
-    RALPB_TRY(cudaMemcpy(packed.data(), m->P + f.w_off, packed.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    RALPB_TRY(cudaMemcpy(packed.data(), self + f.w_off, packed.size() * sizeof(float), cudaMemcpyDeviceToHost));
     if (f.im2col) {
       for (int o = 0; o < co; ++o) {
         for (int j = 0; j < kk; ++j) host[static_cast<size_t>(o) * kk + j] = packed[static_cast<size_t>(o) * f.kpad + j];
@@ -490,7 +547,7 @@ int model_get_params(Model* m, int layer, float* w, float* b, int on_host, std::
         for (int t = 0; t < taps; ++t)
           for (int c = 0; c < cr; ++c)
             host[(static_cast<size_t>(o) * taps + t) * cr + c] = packed[(static_cast<size_t>(o) * taps + t) * cp + c];
-      RALPB_TRY(cudaMemcpy(hb.data(), m->P + f.b_off, co * sizeof(float), cudaMemcpyDeviceToHost));
+      RALPB_TRY(cudaMemcpy(hb.data(), self + f.b_off, co * sizeof(float), cudaMemcpyDeviceToHost));
     }
     RALPB_TRY(cudaMemcpy(w, host.data(), host.size() * sizeof(float), cudaMemcpyDefault));
     RALPB_TRY(cudaMemcpy(b, hb.data(), co * sizeof(float), cudaMemcpyDefault));
@@ -501,7 +558,7 @@ int model_get_params(Model* m, int layer, float* w, float* b, int on_host, std::
       // gather every rank's slice through the peer mappings (rank 0's own for W = 1)
       if (m->world > 1 && !m->peers_open) { *why = "RALP_MPS get_params needs the peers mapped"; return 1; }
       for (int q = 0; q < m->world; ++q) {
-        const float* pq = at<float>(m, q, m->arena_off_P);
+        const float* pq = at<float>(m, q, off);
         if (j == 0) {
           const size_t r0 = static_cast<size_t>(q) * m->s0;
           RALPB_TRY(cudaMemcpy(w + r0 * f.in, pq + f.w_off, static_cast<size_t>(f.lout) * f.in * sizeof(float), cudaMemcpyDefault));
@@ -512,15 +569,26 @@ int model_get_params(Model* m, int layer, float* w, float* b, int on_host, std::
         }
       }
       if (j == 1)  // FC-1's bias is updated on rank 0
-        RALPB_TRY(cudaMemcpy(b, at<float>(m, 0, m->arena_off_P) + f.b_off, f.out * sizeof(float), cudaMemcpyDefault));
+        RALPB_TRY(cudaMemcpy(b, at<float>(m, 0, off) + f.b_off, f.out * sizeof(float), cudaMemcpyDefault));
     } else {
       // RALP_MPS: later FC layers live on rank 0
-      const float* src = m->mps && (m->world == 1 || m->peers_open) ? at<float>(m, 0, m->arena_off_P) : m->P;
+      const float* src = m->mps && (m->world == 1 || m->peers_open) ? at<float>(m, 0, off) : self;
       RALPB_TRY(cudaMemcpy(w, src + f.w_off, static_cast<size_t>(f.out) * f.in * sizeof(float), cudaMemcpyDefault));
       RALPB_TRY(cudaMemcpy(b, src + f.b_off, f.out * sizeof(float), cudaMemcpyDefault));
     }
   }
   return 0;
+}
+
+int model_get_params(Model* m, int layer, float* w, float* b, int on_host, std::string* why) {
+  (void)on_host;
+  return read_layer(m, layer, w, b, m->arena_off_P, why);
+}
+
+// The gradient the last step computed for `layer` (summed over this rank's batch; the FC tail's on
+// the rank that holds it), before any cross-rank reduction.
+int model_get_grads(Model* m, int layer, float* w, float* b, std::string* why) {
+  return read_layer(m, layer, w, b, m->arena_off_G, why);
 }
 
 // ------------------------------------------------------------------ step
@@ -662,7 +730,7 @@ int mps_back_segment(Model* m, const int32_t* lab, const bf16* cut_local, float 
     PeerSignal none{};
     RALPB_TRY(push_and_signal(lab0, lab, static_cast<long long>(b) * 4 / 16, none, seq, m->counters + 1, s));
     ++m->launches;
-    m->phys_bytes += sizeof(int32_t) * b;
+    m->nvl_out += sizeof(int32_t) * b;
   }
   for (int q = 0; q < W; ++q) {
     if (q == r) continue;
@@ -672,7 +740,8 @@ int mps_back_segment(Model* m, const int32_t* lab, const bf16* cut_local, float 
     RALPB_TRY(push_and_signal(at<bf16>(m, q, m->arena_off_xfc) + static_cast<size_t>(r) * b * cut, cut_local,
                               static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + 16 + q, s));
     ++m->launches;
-    m->phys_bytes += cut_bytes;
+    m->nvl_out += cut_bytes;
+    m->logical += static_cast<long long>(b) * cut * m->elem_bytes;   // cut all-gather
   }
   {
     PeerSignal own{};
@@ -707,7 +776,8 @@ int mps_back_segment(Model* m, const int32_t* lab, const bf16* cut_local, float 
       RALPB_TRY(push_and_signal(p1_slots + static_cast<size_t>(r) * R * ld1, m->p1_local,
                                 static_cast<long long>(bytes / 16), sig, seq, m->counters + 24, s));
       ++m->launches;
-      m->phys_bytes += bytes;
+      m->nvl_out += bytes;
+      m->logical += static_cast<long long>(R) * f1.out * m->elem_bytes;   // FC-1 partial to rank 0
     }
   }
   // 4. rank 0: reduce the partials (+ b1, ReLU), the rest of the tail, the loss, and the gradient
@@ -768,7 +838,8 @@ int mps_back_segment(Model* m, const int32_t* lab, const bf16* cut_local, float 
       RALPB_TRY(push_and_signal(at<bf16>(m, q, m->arena_off_dh1), dz1, static_cast<long long>(bytes / 16), sig, seq,
                                 m->counters + 32 + q, s));
       ++m->launches;
-      m->phys_bytes += bytes;
+      m->nvl_out += bytes;
+      m->logical += static_cast<long long>(R) * f1.out * m->elem_bytes;   // FC-1 output gradient back
     }
   } else {
     RALPB_TRY(wait_flags(m->flags + kFlagDh1, 1, seq, s));
@@ -822,7 +893,8 @@ int mps_back_segment(Model* m, const int32_t* lab, const bf16* cut_local, float 
                                 m->dxp + static_cast<size_t>(q) * blk, static_cast<long long>(blk * sizeof(float) / 16),
                                 sig, seq, m->counters + 40 + q, s));
       ++m->launches;
-      m->phys_bytes += blk * sizeof(float);
+      m->nvl_out += blk * sizeof(float);
+      m->logical += static_cast<long long>(b) * cut * m->elem_bytes;   // cut-gradient reduce-scatter
     }
     PeerSignal own{};
     own.n = 1;
@@ -982,39 +1054,54 @@ int relayout_weights(Model* m, bool fc_too, std::string* why, bool dgrad_now = f
   return 0;
 }
 
-// Sharded-PS synchronisation of params[0, n) over all ranks.
+// Sharded-PS synchronisation of params[0, n) over the worker group (every rank, or the workers only
+// with a dedicated PS rank): worker w owns shard w.  Logical bytes at the reference's sites: this
+// worker's gradient push ("grad"/"push", simulator.py:647,689: every real parameter of [0, n)) and
+// the pull of the shard it owns to every worker ("pull", simulator.py:663,713); the ring strategy
+// counts its reduce-scatter + all-gather share 2*(W-1)*shard (ring_shares, simulator.py:726).
 int sync_params(Model* m, long long n, float lr, float mu, std::string* why) {
-  if (m->world == 1) {
+  const int W = m->workers;
+  const long long eb = m->elem_bytes;
+  const bool ring = m->strategy == RALPB_STRATEGY_RING || m->strategy == RALPB_STRATEGY_RING_EXTERNAL;
+  long long real_n = 0;
+  for (long long v : m->shard_real) real_n += v;
+  if (ring)
+    m->logical += 2LL * (W - 1) * m->shard_real[m->widx] * eb;
+  else
+    m->logical += real_n * eb + static_cast<long long>(W) * m->shard_real[m->widx] * eb;
+  if (W == 1) {
     RALPB_TRY(sgd_momentum(m->P, m->V, m->G, n, lr, mu, 1.f, m->stream));
     ++m->launches;
     return 0;
   }
   const uint32_t* seq = m->seq_dev;
   PeerSignal all_grad{}, all_done{};
-  all_grad.n = all_done.n = m->world;
-  for (int r = 0; r < m->world; ++r) {
-    uint32_t* fl = at<uint32_t>(m, r, m->arena_off_flags);
-    all_grad.flag[r] = fl + kFlagGrad + m->rank;
-    all_done.flag[r] = fl + kFlagDone + m->rank;
+  all_grad.n = all_done.n = W;
+  for (int w = 0; w < W; ++w) {
+    uint32_t* fl = at<uint32_t>(m, m->worker_ranks[w], m->arena_off_flags);
+    all_grad.flag[w] = fl + kFlagGrad + m->widx;
+    all_done.flag[w] = fl + kFlagDone + m->widx;
   }
   RALPB_TRY(signal_only(all_grad, seq, m->stream));
-  RALPB_TRY(wait_flags(m->flags + kFlagGrad, m->world, seq, m->stream));
+  RALPB_TRY(wait_flags(m->flags + kFlagGrad, W, seq, m->stream));
   ShardUpdate u{};
-  u.nranks = m->world;
-  u.self = m->rank;
-  const long long shard = n / m->world;  // n is a multiple of 4*world
-  u.begin = shard * m->rank;
+  u.nranks = W;
+  u.self = m->widx;
+  const long long shard = n / W;  // n is a multiple of 4 * lcm(1..8)
+  u.begin = shard * m->widx;
   u.end = u.begin + shard;
   u.lr = lr; u.mu = mu; u.gscale = 1.f;
   u.momentum = m->V;
-  for (int r = 0; r < m->world; ++r) {
-    u.grads[r] = at<float>(m, r, m->arena_off_G);
-    u.params[r] = at<float>(m, r, m->arena_off_P);
+  for (int w = 0; w < W; ++w) {
+    u.grads[w] = at<float>(m, m->worker_ranks[w], m->arena_off_G);
+    u.params[w] = at<float>(m, m->worker_ranks[w], m->arena_off_P);
   }
   RALPB_TRY(shard_update(u, all_done, seq, m->counters + 0, m->stream));
-  RALPB_TRY(wait_flags(m->flags + kFlagDone, m->world, seq, m->stream));
+  RALPB_TRY(wait_flags(m->flags + kFlagDone, W, seq, m->stream));
   m->launches += 4;
-  m->phys_bytes += 2LL * (m->world - 1) * shard * static_cast<long long>(sizeof(float));
+  const long long peer = static_cast<long long>(W - 1) * shard * static_cast<long long>(sizeof(float));
+  m->nvl_in += peer;   // gradient shards of the other workers
+  m->nvl_out += peer;  // the updated shard to the other workers
   return 0;
 }
 
@@ -1028,107 +1115,166 @@ cudaError_t mark(Model* m, int i, bool capturing) {
                    : cudaEventRecord(m->ev[i], m->stream);
 }
 
+__global__ void combine_loss_kernel(const float* slots, int n, int self, float* out) {
+  // out[0] = own share + the other workers' shares (slots[w * 4], w != self), fixed order
+  if (threadIdx.x == 0) {
+    float acc = 0.f;
+    for (int w = 0; w < n; ++w) acc += w == self ? out[0] : slots[4 * w];
+    out[0] = acc;
+  }
+}
+
+// The step's mean loss on the reporting rank when every rank computes the loss of its own rows
+// (baseline / ring): the others push their share (16 bytes) into its arena slot; it sums them in
+// worker order.  Called where the reporting rank already waits for every rank (after the sync).
+int push_loss_share(Model* m, std::string* why) {
+  if (m->workers == 1 || m->rank == m->ps_rank) return 0;
+  PeerSignal sig{};
+  sig.n = 1;
+  sig.flag[0] = at<uint32_t>(m, m->ps_rank, m->arena_off_flags) + kFlagLoss + m->widx;
+  float* slot = at<float>(m, m->ps_rank, m->arena_off_loss) + 4 * m->widx;
+  RALPB_TRY(push_and_signal(slot, m->loss, 1, sig, m->seq_dev, m->counters + 3, m->stream));
+  ++m->launches;
+  m->nvl_out += 16;
+  return 0;
+}
+
+int combine_loss(Model* m, std::string* why) {
+  if (m->workers == 1 || m->rank != m->ps_rank) return 0;
+  const int W = m->workers;
+  // flags kFlagLoss + w for every other worker w (this rank's own slot is never signalled: wait on
+  // the two contiguous ranges around it)
+  if (m->widx > 0) RALPB_TRY(wait_flags(m->flags + kFlagLoss, m->widx, m->seq_dev, m->stream));
+  if (m->widx + 1 < W) RALPB_TRY(wait_flags(m->flags + kFlagLoss + m->widx + 1, W - m->widx - 1, m->seq_dev, m->stream));
+  combine_loss_kernel<<<1, 32, 0, m->stream>>>(reinterpret_cast<const float*>(static_cast<char*>(m->arena) + m->arena_off_loss),
+                                               W, m->widx, m->loss);
+  RALPB_TRY(cudaGetLastError());
+  m->launches += 3;
+  return 0;
+}
+
 // Everything of one step after the inputs are resident in HBM: bump the device step
 // counter, front forward, cut exchange, back segment, front backward, sync, re-layout.
+// Logical bytes are counted where each transfer is issued, at the reference's count_wire sites
+// (simulator.py:677 act, :707 actgrad, :689 grad, :713 pull; :647/:663 baseline push/pull).
 int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu, bool capturing,
               std::string* why) {
   const uint32_t* seq = m->seq_dev;
   const int b = m->batch;
+  const int W = m->workers;
+  const long long eb = m->elem_bytes;
   const bool ralp = m->strategy == RALPB_STRATEGY_RALP;
   cudaStream_t s = m->stream;
   bool fc_forked = false;
   RALPB_TRY(bump_counter(m->seq_dev, s));
   ++m->launches;
+  const long long cut_logical = static_cast<long long>(b) * m->cut_elems * eb;  // one worker's cut
+  const size_t cut_bytes = static_cast<size_t>(b) * m->cut_elems * sizeof(bf16);
+  const int slot = ralp || m->mps ? m->widx : 0;   // this worker's row block in the PS input
+  const bf16* cut_local = nullptr;
 
-  // backward-data filter copies from this step's masters, on the aux stream under the forward
-  RALPB_TRY(cudaEventRecord(m->ev_wd_fork, s));
-  RALPB_TRY(cudaStreamWaitEvent(m->aux_stream, m->ev_wd_fork, 0));
-  if (prep_filters(m, false, true, m->aux_stream, why)) return 1;
-  RALPB_TRY(cudaEventRecord(m->ev_wd_join, m->aux_stream));
+  if (m->is_worker) {
+    // backward-data filter copies from this step's masters, on the aux stream under the forward
+    RALPB_TRY(cudaEventRecord(m->ev_wd_fork, s));
+    RALPB_TRY(cudaStreamWaitEvent(m->aux_stream, m->ev_wd_fork, 0));
+    if (prep_filters(m, false, true, m->aux_stream, why)) return 1;
+    RALPB_TRY(cudaEventRecord(m->ev_wd_join, m->aux_stream));
 
-  // ---------------- worker front forward
-  const FrontLayer& f0 = m->front[0];
-  const ActBuf& a0 = m->acts[0];
-  m->step_img = img;
-  if (f0.fused) {
-    // patches are built on chip by conv_first_fwd / conv_first_wgrad
-  } else if (f0.im2col) {
-    RALPB_TRY(pack_im2col(img, b, m->in_h, m->in_w, m->in_c, f0.k, f0.stride, m->desc[0].pad, a0.h, a0.w, a0.pad,
-                          f0.kpad, a0.ptr, s));
-    ++m->launches;
-  } else {
-    RALPB_TRY(pack_input(img, b, m->in_h, m->in_w, m->in_c, a0.ptr, m->in_cp, a0.pad, s));
-    ++m->launches;
-  }
-  const int slot = ralp || m->mps ? m->rank : 0;   // this worker's row block in the PS input
-  bf16* cut_dst = m->acts.back().ptr;
-  if (m->holds_back) cut_dst = m->x_fc + static_cast<size_t>(slot) * b * m->cut_elems;
-  for (size_t i = 0; i < m->front.size(); ++i) {
-    FrontLayer& f = m->front[i];
-    const ActBuf& in = m->acts[i];
-    ActBuf out = m->acts[i + 1];
-    if (i + 1 == m->front.size()) out.ptr = cut_dst;
-    if (f.fused) {
-      RALPB_TRY(conv_first_fwd(img, b, m->in_h, m->in_w, m->in_c, f.wf, out.ptr, out.pad, s, why));
-    } else if (f.im2col) {
-      // y = relu(patches . W^T) on the padded output grid (bias rides in the ones column)
-      GemmDesc d;
-      d.M = static_cast<int>(in.rows()); d.N = f.g.cout; d.K = f.kpad;
-      d.kb = std::min(64, f.kpad);
-      d.a = Operand2D{in.ptr, in.rows(), f.kpad, f.kpad};
-      d.b = Operand2D{f.wf, f.g.cout, f.kpad, f.kpad};
-      d.epi = EPI_BF16; d.relu = 1; d.out = out.ptr; d.s_m = f.g.cout;
-      d.border = 1; d.img_rows = (out.h + 2 * out.pad) * (out.w + 2 * out.pad); d.wp = out.w + 2 * out.pad;
-      d.pad = out.pad; d.h = out.h; d.w = out.w;
-      RALPB_TRY(gemm_launch(d, s, why));
-    } else if (f.kind == RALPB_CONV) {
-      // a following 2x2/2 max pool is fused into the conv epilogue (RALPB_FUSE_POOL=0: separate)
-      const bool pool_next = i + 1 < m->front.size() && m->front[i + 1].fused_fwd;
-      if (pool_next) {
-        const ActBuf& pooled = m->acts[i + 2];
-        bf16* pdst = i + 2 == m->front.size() ? cut_dst : pooled.ptr;
-        RALPB_TRY(conv_fwd_pool(f.g, in.ptr, f.wf, m->P + f.b_off, out.ptr, 1, pdst, pooled.pad, s, why,
-                                m->front[i + 1].idx));
-        ++m->launches;
-        ++i;  // the pool layer is done
-        continue;
-      }
-      RALPB_TRY(conv_fwd(f.g, in.ptr, f.wf, m->P + f.b_off, out.ptr, 1, s, why));
+    // ---------------- worker front forward
+    const FrontLayer& f0 = m->front[0];
+    const ActBuf& a0 = m->acts[0];
+    m->step_img = img;
+    if (f0.fused) {
+      // patches are built on chip by conv_first_fwd / conv_first_wgrad
+    } else if (f0.im2col) {
+      RALPB_TRY(pack_im2col(img, b, m->in_h, m->in_w, m->in_c, f0.k, f0.stride, m->desc[0].pad, a0.h, a0.w, a0.pad,
+                            f0.kpad, a0.ptr, s));
+      ++m->launches;
     } else {
-      RALPB_TRY(maxpool_fwd(in.ptr, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.ptr, out.pad, s, f.idx));
+      RALPB_TRY(pack_input(img, b, m->in_h, m->in_w, m->in_c, a0.ptr, m->in_cp, a0.pad, s));
+      ++m->launches;
     }
-    ++m->launches;
+    bf16* cut_dst = m->acts.back().ptr;
+    if (m->holds_back) cut_dst = m->x_fc + static_cast<size_t>(slot) * b * m->cut_elems;
+    for (size_t i = 0; i < m->front.size(); ++i) {
+      FrontLayer& f = m->front[i];
+      const ActBuf& in = m->acts[i];
+      ActBuf out = m->acts[i + 1];
+      if (i + 1 == m->front.size()) out.ptr = cut_dst;
+      if (f.fused) {
+        RALPB_TRY(conv_first_fwd(img, b, m->in_h, m->in_w, m->in_c, f.wf, out.ptr, out.pad, s, why));
+      } else if (f.im2col) {
+        // y = relu(patches . W^T) on the padded output grid (bias rides in the ones column)
+        GemmDesc d;
+        d.M = static_cast<int>(in.rows()); d.N = f.g.cout; d.K = f.kpad;
+        d.kb = std::min(64, f.kpad);
+        d.a = Operand2D{in.ptr, in.rows(), f.kpad, f.kpad};
+        d.b = Operand2D{f.wf, f.g.cout, f.kpad, f.kpad};
+        d.epi = EPI_BF16; d.relu = 1; d.out = out.ptr; d.s_m = f.g.cout;
+        d.border = 1; d.img_rows = (out.h + 2 * out.pad) * (out.w + 2 * out.pad); d.wp = out.w + 2 * out.pad;
+        d.pad = out.pad; d.h = out.h; d.w = out.w;
+        RALPB_TRY(gemm_launch(d, s, why));
+      } else if (f.kind == RALPB_CONV) {
+        // a following 2x2/2 max pool is fused into the conv epilogue (RALPB_FUSE_POOL=0: separate)
+        const bool pool_next = i + 1 < m->front.size() && m->front[i + 1].fused_fwd;
+        if (pool_next) {
+          const ActBuf& pooled = m->acts[i + 2];
+          bf16* pdst = i + 2 == m->front.size() ? cut_dst : pooled.ptr;
+          RALPB_TRY(conv_fwd_pool(f.g, in.ptr, f.wf, m->P + f.b_off, out.ptr, 1, pdst, pooled.pad, s, why,
+                                  m->front[i + 1].idx));
+          ++m->launches;
+          ++i;  // the pool layer is done
+          continue;
+        }
+        RALPB_TRY(conv_fwd(f.g, in.ptr, f.wf, m->P + f.b_off, out.ptr, 1, s, why));
+      } else {
+        RALPB_TRY(maxpool_fwd(in.ptr, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.ptr, out.pad, s, f.idx));
+      }
+      ++m->launches;
+    }
+    cut_local = cut_dst;
   }
-  const bf16* cut_local = cut_dst;
   RALPB_TRY(mark(m, 1, capturing));
 
   // ---------------- cut exchange + PS back segment
-  const size_t cut_bytes = static_cast<size_t>(b) * m->cut_elems * sizeof(bf16);
   const bf16* dcut = nullptr;
   if (m->mps) {
     if (mps_back_segment(m, lab, cut_local, lr, mu, &dcut, &fc_forked, why)) return 1;
   } else if (m->holds_back) {
-    RALPB_TRY(cudaMemcpyAsync(m->labels_all + static_cast<size_t>(slot) * b, lab, sizeof(int32_t) * b, cudaMemcpyDeviceToDevice, s));
-    if (ralp && m->world > 1) {
-      PeerSignal own{};
-      own.n = 1;
-      own.flag[0] = m->flags + kFlagAct + m->rank;
-      RALPB_TRY(signal_only(own, seq, s));
-      RALPB_TRY(wait_flags(m->flags + kFlagAct, m->world, seq, s));
-      m->launches += 2;
+    if (m->is_worker) {
+      RALPB_TRY(cudaMemcpyAsync(m->labels_all + static_cast<size_t>(slot) * b, lab, sizeof(int32_t) * b,
+                                cudaMemcpyDeviceToDevice, s));
+      if (ralp) m->logical += cut_logical;   // "act": this colocated worker's cut, written in place
+    }
+    if (ralp && m->workers > 1) {
+      if (m->is_worker) {
+        PeerSignal own{};
+        own.n = 1;
+        own.flag[0] = m->flags + kFlagAct + m->widx;
+        RALPB_TRY(signal_only(own, seq, s));
+        ++m->launches;
+      }
+      RALPB_TRY(wait_flags(m->flags + kFlagAct, W, seq, s));
+      ++m->launches;
     }
   } else {
-    // push labels then the cut into the PS rank's rows, raise act_ready[rank] there
+    // a remote worker: push labels then the cut into the PS rank's rows, raise act_ready there.
+    // With a dedicated PS the rows are free only once the PS has finished the previous step.
+    if (m->dedicated_ps) {
+      RALPB_TRY(wait_flags(m->flags + kFlagPsFree, 1, m->seq_dev - 1, s));
+      ++m->launches;
+    }
     int32_t* lab_ps = at<int32_t>(m, m->ps_rank, m->arena_off_lab) + static_cast<size_t>(slot) * b;
     bf16* x_ps = at<bf16>(m, m->ps_rank, m->arena_off_xfc) + static_cast<size_t>(slot) * b * m->cut_elems;
     PeerSignal none{};
     RALPB_TRY(push_and_signal(lab_ps, lab, static_cast<long long>(b) * 4 / 16, none, seq, m->counters + 1, s));
     PeerSignal sig{};
     sig.n = 1;
-    sig.flag[0] = at<uint32_t>(m, m->ps_rank, m->arena_off_flags) + kFlagAct + m->rank;
+    sig.flag[0] = at<uint32_t>(m, m->ps_rank, m->arena_off_flags) + kFlagAct + m->widx;
     RALPB_TRY(push_and_signal(x_ps, cut_local, static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + 2, s));
     m->launches += 2;
-    m->phys_bytes += cut_bytes + sizeof(int32_t) * b;
+    m->nvl_out += cut_bytes + sizeof(int32_t) * b;
+    m->logical += cut_logical;   // "act" (simulator.py:677)
   }
   if (m->mps) {
     // the sharded FC tail ran in mps_back_segment
@@ -1137,47 +1283,52 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
     const bf16* in = m->x_fc;
     if (launch_fc_forward(m, in, R, why)) return 1;
     const FcLayer& last = m->back.back();
-    const float scale = 1.f / static_cast<float>(m->world * b);
+    const float scale = 1.f / static_cast<float>(W * b);
     RALPB_TRY(softmax_xent(m->logits, R, last.out, last.ld_out, m->labels_all, scale, m->row_loss, m->dlogits, last.ld_out, s));
-    RALPB_TRY(reduce_sum(m->row_loss, R, 1.f / static_cast<float>(R), m->loss, s));
+    // this rank's rows' share of the job's mean loss (RALP: all W*b rows are here)
+    RALPB_TRY(reduce_sum(m->row_loss, R, scale, m->loss, s));
     m->launches += 2;
+    if (!ralp && push_loss_share(m, why)) return 1;
     if (launch_fc_backward_data(m, in, R, m->dx_fc, why)) return 1;
     if (ralp) {
       // return every remote worker's rows of the cut gradient first, then the FC tail's
       // weight gradients and its (PS-local, never synchronised) update run on the aux
       // stream, overlapping this rank's front backward
       // (one launch for all peers; RALPB_SCATTER_FUSED=0: one push launch per peer)
+      m->logical += static_cast<long long>(W) * cut_logical;   // "actgrad" (simulator.py:707)
       const char* sf = getenv("RALPB_SCATTER_FUSED");
       if (sf != nullptr && sf[0] == '0') {
-        for (int r = 0; r < m->world; ++r) {
+        for (int w = 0; w < W; ++w) {
+          const int r = m->worker_ranks[w];
           if (r == m->rank) continue;
           PeerSignal sig{};
           sig.n = 1;
           sig.flag[0] = at<uint32_t>(m, r, m->arena_off_flags) + kFlagActGrad;
-          RALPB_TRY(push_and_signal(at<bf16>(m, r, m->arena_off_dcut), m->dx_fc + static_cast<size_t>(r) * b * m->cut_elems,
-                                    static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + 8 + r, s));
+          RALPB_TRY(push_and_signal(at<bf16>(m, r, m->arena_off_dcut), m->dx_fc + static_cast<size_t>(w) * b * m->cut_elems,
+                                    static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + kCtrScatter + w, s));
           ++m->launches;
-          m->phys_bytes += cut_bytes;
+          m->nvl_out += cut_bytes;
         }
       } else if (m->world > 1) {
         PeerScatter sc{};
         PeerSignal sig{};
-        for (int r = 0; r < m->world; ++r) {
+        for (int w = 0; w < W; ++w) {
+          const int r = m->worker_ranks[w];
           if (r == m->rank) continue;
           sc.dst[sc.n] = at<bf16>(m, r, m->arena_off_dcut);
-          sc.src[sc.n] = m->dx_fc + static_cast<size_t>(r) * b * m->cut_elems;
+          sc.src[sc.n] = m->dx_fc + static_cast<size_t>(w) * b * m->cut_elems;
           ++sc.n;
           sig.flag[sig.n++] = at<uint32_t>(m, r, m->arena_off_flags) + kFlagActGrad;
-          m->phys_bytes += cut_bytes;
+          m->nvl_out += cut_bytes;
         }
-        RALPB_TRY(scatter_and_signal(sc, static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + 8 + m->rank, s));
+        RALPB_TRY(scatter_and_signal(sc, static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + kCtrScatter, s));
         ++m->launches;
       }
       // weight gradients on this stream (tensor/HBM work that would contend with the persistent
       // conv kernels), the HBM-bound update on the aux stream, overlapping the front backward
       // (RALPB_FC_OVERLAP=0: everything in order on one stream)
       const char* ov = getenv("RALPB_FC_OVERLAP");
-      const bool overlap = !(ov != nullptr && ov[0] == '0');
+      const bool overlap = !(ov != nullptr && ov[0] == '0') && m->is_worker;
       cudaStream_t su = overlap ? m->aux_stream : s;
       if (launch_fc_backward_weights(m, in, R, true, lr, mu, s, su, why)) return 1;
       if (overlap) {
@@ -1187,13 +1338,24 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
     } else {
       if (launch_fc_backward_weights(m, in, R, false, lr, mu, s, s, why)) return 1;
     }
-    dcut = m->dx_fc + static_cast<size_t>(slot) * b * m->cut_elems;
+    if (m->is_worker) dcut = m->dx_fc + static_cast<size_t>(slot) * b * m->cut_elems;
   } else {
     RALPB_TRY(wait_flags(m->flags + kFlagActGrad, 1, seq, s));
     ++m->launches;
     dcut = m->dcut;
   }
   RALPB_TRY(mark(m, 2, capturing));
+
+  if (!m->is_worker) {
+    // dedicated PS (RALP-N): its step ends with the FC tail's update; release the FC input rows
+    // to the workers' next cut pushes
+    PeerSignal free_rows{};
+    for (int w = 0; w < W; ++w) free_rows.flag[free_rows.n++] = at<uint32_t>(m, m->worker_ranks[w], m->arena_off_flags) + kFlagPsFree;
+    RALPB_TRY(signal_only(free_rows, seq, s));
+    ++m->launches;
+    RALPB_TRY(mark(m, 3, capturing));
+    return 0;
+  }
 
   // ---------------- worker front backward
   RALPB_TRY(cudaStreamWaitEvent(s, m->ev_wd_join, 0));
@@ -1205,12 +1367,22 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   // join the FC tail's update before this rank signals the sync: a worker can only start the
   // next step (and push its cut into x_fc, which the FC wgrads read) after that sync
   if (fc_forked) RALPB_TRY(cudaStreamWaitEvent(s, m->ev_join, 0));
-  if (m->strategy == RALPB_STRATEGY_RING_EXTERNAL) return 0;  // the caller all-reduces G, then apply
+  if (m->strategy == RALPB_STRATEGY_RING_EXTERNAL) {
+    // the caller all-reduces G, then ralpb_model_apply; count the ring share here
+    const long long sh = m->shard_real[m->widx];
+    m->logical += 2LL * (W - 1) * sh * eb;
+    return combine_loss(m, why);
+  }
   const bool placed = ralp || m->mps;
   if (sync_params(m, placed ? m->n_front : m->n_total, lr, mu, why)) return 1;
   if (relayout_weights(m, !placed, why)) return 1;
+  if (!ralp && !m->mps && combine_loss(m, why)) return 1;
   return 0;
 }
+
+// The rank whose m->loss holds the job's mean loss: the PS (RALP; baseline / ring after
+// combine_loss), rank 0 for the sharded FC tail.
+bool reports_loss(const Model* m) { return m->mps ? m->rank == 0 : m->rank == m->ps_rank; }
 
 bool graphs_enabled() {
   const char* e = getenv("RALPB_GRAPH");
@@ -1224,6 +1396,8 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
   if (m->world > 1 && !m->peers_open) { *why = "ralpb_model_ipc_open has not been called"; return 1; }
   const int b = m->batch;
   cudaStream_t s = m->stream;
+  if (m->is_worker && (images == nullptr || labels == nullptr)) { *why = "a worker rank needs images and labels"; return 1; }
+  if (!m->is_worker) on_host = 0;   // the dedicated PS receives its rows from the workers
   m->seq += 1;
   const float* img = static_cast<const float*>(images);
   const int32_t* lab = labels;
@@ -1243,7 +1417,7 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
   RALPB_TRY(cudaEventRecord(m->ev[0], s));
   if (m->profiling || !graphs_enabled()) {
     m->launches = 0;
-    m->phys_bytes = 0;
+    m->nvl_out = m->nvl_in = m->logical = 0;
     m->timer.n = 0;
     set_gemm_timer(m->profiling ? &m->timer : nullptr);
     struct Reset { ~Reset() { set_gemm_timer(nullptr); } } reset_timer;
@@ -1259,7 +1433,7 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
       for (auto& g : m->graphs)
         if (g.exec == nullptr || g.used < e->used) e = &g;
       m->launches = 0;
-      m->phys_bytes = 0;
+      m->nvl_out = m->nvl_in = m->logical = 0;
       RALPB_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
       const int rc = step_body(m, img, lab, lr, mu, true, why);
       cudaGraph_t g = nullptr;
@@ -1281,16 +1455,20 @@ int model_step(Model* m, const void* images, const int32_t* labels, int on_host,
       if (ie != cudaSuccess) { *e = Model::GraphEntry{}; *why = std::string("graph instantiate failed: ") + cudaGetErrorString(ie); return 1; }
       e->img = img; e->lab = lab; e->lr = lr; e->mu = mu;
       e->launches = m->launches;
-      e->phys = m->phys_bytes;
+      e->nvl_out = m->nvl_out;
+      e->nvl_in = m->nvl_in;
+      e->logical = m->logical;
     }
     e->used = ++m->graph_clock;
     RALPB_TRY(cudaGraphLaunch(e->exec, s));
     m->launches = e->launches;
-    m->phys_bytes = e->phys;
+    m->nvl_out = e->nvl_out;
+    m->nvl_in = e->nvl_in;
+    m->logical = e->logical;
   }
   if (on_host) RALPB_TRY(cudaEventRecord(m->ev_consumed[buf], s));
   const int slot = static_cast<int>(m->seq % Model::kLossRing);
-  if (m->mps ? m->rank == 0 : m->holds_back)
+  if (reports_loss(m))
     RALPB_TRY(cudaMemcpyAsync(m->loss_host + slot, m->loss, sizeof(float), cudaMemcpyDeviceToHost, s));
   RALPB_TRY(cudaEventRecord(m->ev_loss[slot], s));
   m->loss_seq[slot] = m->seq;
@@ -1306,7 +1484,7 @@ int model_read_loss(Model* m, int lag, float* out, std::string* why) {
   const int slot = static_cast<int>(want % Model::kLossRing);
   if (m->loss_seq[slot] != want) { *why = "step no longer in the loss ring"; return 1; }
   RALPB_TRY(cudaEventSynchronize(m->ev_loss[slot]));
-  *out = (m->mps ? m->rank == 0 : m->holds_back) ? m->loss_host[slot] : NAN;
+  *out = reports_loss(m) ? m->loss_host[slot] : NAN;
   return 0;
 }
 
@@ -1314,25 +1492,13 @@ int model_stats(Model* m, ralpb_step_stats* st, std::string* why) {
   RALPB_TRY(cudaStreamSynchronize(m->stream));
   std::memset(st, 0, sizeof(*st));
   if (!m->stats_valid) { *why = "no step has run"; return 1; }
-  const bool ralp = m->strategy == RALPB_STRATEGY_RALP;
   float loss = NAN;
-  if (m->mps ? m->rank == 0 : m->holds_back) RALPB_TRY(cudaMemcpy(&loss, m->loss, sizeof(float), cudaMemcpyDeviceToHost));
+  if (reports_loss(m)) RALPB_TRY(cudaMemcpy(&loss, m->loss, sizeof(float), cudaMemcpyDeviceToHost));
   st->loss = loss;
-  const long long eb = m->elem_bytes;
-  const bool ring = m->strategy == RALPB_STRATEGY_RING || m->strategy == RALPB_STRATEGY_RING_EXTERNAL;
-  if (m->mps) {
-    // volume_ralp_multi_ps (planner/costmodel.py): cut all-gather + cut-gradient reduce-scatter
-    // 2*W*(W-1)*O_cut, FC-1 partials to rank 0 + its gradient back 2*(W-1)*W*O_fc1, front sync 2*W*P_front
-    const long long W = m->world, o_cut = static_cast<long long>(m->batch) * m->cut_elems * eb;
-    const long long o_fc1 = static_cast<long long>(m->batch) * m->back[1].out * eb;
-    st->logical_bytes = 2 * W * (W - 1) * o_cut + 2 * (W - 1) * W * o_fc1 + W * 2 * m->real_front * eb;
-  } else if (ralp)
-    st->logical_bytes = static_cast<long long>(m->world) * 2 * (static_cast<long long>(m->batch) * m->cut_elems * eb + m->real_front * eb);
-  else if (ring)  // volume_ring: 2 * S * (W - 1) (costmodel.py:118-121)
-    st->logical_bytes = 2LL * (m->world - 1) * m->real_total * eb;
-  else
-    st->logical_bytes = static_cast<long long>(m->world) * 2 * m->real_total * eb;
-  st->physical_bytes = m->phys_bytes;
+  st->logical_bytes = m->logical;
+  st->nvlink_out_bytes = m->nvl_out;
+  st->nvlink_in_bytes = m->nvl_in;
+  st->physical_bytes = m->nvl_out + m->nvl_in;
   st->launches = m->launches;
   cudaEventElapsedTime(&st->ms_step, m->ev[0], m->ev[4]);
   cudaEventElapsedTime(&st->ms_front_fwd, m->ev[0], m->ev[1]);

@@ -51,6 +51,14 @@ struct Model {
   // configuration
   int rank = 0, world = 1, ps_rank = 0, device = 0;
   int batch = 0, split = 0, strategy = RALPB_STRATEGY_RALP, elem_bytes = 4;
+  int precision = RALPB_PRECISION_BF16;
+  int workers = 1;                 // ranks that run a conv front (world, or world - 1 for RALP-N)
+  bool dedicated_ps = false;       // RALP-N: ps_rank runs only the back segment
+  bool is_worker = true;           // this rank runs a conv front
+  int widx = 0;                    // this rank's worker index (rank order, the dedicated PS skipped)
+  std::vector<int> worker_ranks;   // worker index -> rank
+  std::vector<long long> shard_real;  // real (descriptor) parameters in each sync shard, for the
+                                      // logical byte count of the pull / ring sites
   std::vector<ralpb_layer_desc> desc;
   std::vector<FrontLayer> front;
   std::vector<FcLayer> back;
@@ -86,7 +94,8 @@ struct Model {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // front backward
   cudaEvent_t ev_wd_fork = nullptr, ev_wd_join = nullptr;  // backward-data filter copies (aux stream)
   float* row_loss = nullptr;
-  float* loss = nullptr;
+  float* loss = nullptr;           // [4]: the reported loss (mean over the job's samples), [1] this
+                                   // rank's own-row sum (baseline / ring: pushed to ps_rank's slot)
   std::vector<bf16*> gacts;        // gacts[i] = gradient w.r.t. acts[i] (dedicated, zero borders)
   // host inputs: double-buffered device staging filled on a copy stream, so the copy of step
   // t+1 overlaps the compute of step t (buffer b is reused once step t-1 has consumed it)
@@ -101,7 +110,7 @@ struct Model {
   cudaEvent_t ev_loss[kLossRing] = {};
   uint32_t loss_seq[kLossRing] = {};
   size_t arena_off_flags = 0, arena_off_P = 0, arena_off_G = 0, arena_off_xfc = 0, arena_off_lab = 0,
-         arena_off_dcut = 0;
+         arena_off_dcut = 0, arena_off_loss = 0;
 
   // peers (IPC-mapped base pointers of every rank's arena; self = arena)
   std::vector<char*> peer_base;
@@ -127,13 +136,15 @@ struct Model {
     const void* lab = nullptr;
     float lr = 0.f, mu = 0.f;
     int launches = 0;
-    long long phys = 0;
+    long long phys = 0, nvl_out = 0, nvl_in = 0, logical = 0;
     uint64_t used = 0;
   };
   GraphEntry graphs[2];            // one per staging buffer (or caller buffers)
   uint64_t graph_clock = 0;
   int launches = 0;
-  long long phys_bytes = 0;
+  long long phys_bytes = 0;        // NVLink bytes this rank moved (out + in)
+  long long nvl_out = 0, nvl_in = 0;  // ... stored to / loaded from peers
+  long long logical = 0;           // descriptor-unit bytes of this rank's count_wire sites
   cudaEvent_t ev[6] = {};
   bool profiling = false;
   GemmTimer timer;
@@ -141,7 +152,8 @@ struct Model {
 };
 
 int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int batch, int strategy,
-                 int rank, int world, int ps_rank, int elem_bytes, Model** out, std::string* why);
+                 int rank, int world, int ps_rank, int elem_bytes, int precision, int workers, Model** out,
+                 std::string* why);
 void model_destroy(Model* m);
 int model_step(Model* m, const void* images, const int32_t* labels, int on_host, float lr, float mu,
                std::string* why);
@@ -149,6 +161,7 @@ int model_stats(Model* m, ralpb_step_stats* st, std::string* why);
 int model_read_loss(Model* m, int lag, float* out, std::string* why);
 int model_set_params(Model* m, int layer, const float* w, const float* b, int on_host, std::string* why);
 int model_get_params(Model* m, int layer, float* w, float* b, int on_host, std::string* why);
+int model_get_grads(Model* m, int layer, float* w, float* b, std::string* why);
 int model_ipc_handle(Model* m, void* out, std::string* why);
 int model_ipc_open(Model* m, const void* handles, std::string* why);
 int model_set_profiling(Model* m, int on, std::string* why);

@@ -71,7 +71,10 @@ cudaError_t push_and_signal(void* dst, const void* src, long long n16, const Pee
 }
 
 // One launch for several destinations: blockIdx.y picks the (dst, src) pair, so the copies to
-// all peers are in flight together instead of one launch (and one drain) per peer.
+// all peers are in flight together instead of one launch (and one drain) per peer.  Each
+// destination row has its own last-CTA counter (counter[blockIdx.y]) and releases its own flag
+// (sig.flag[blockIdx.y] when sig.n == gridDim.y) as soon as ITS bytes are visible, so a worker
+// never waits for the copies to the other peers.
 __global__ void scatter_kernel(PeerScatter sc, long long n16, PeerSignal sig, const uint32_t* value,
                                uint32_t* counter) {
   uint4* __restrict__ dst = reinterpret_cast<uint4*>(sc.dst[blockIdx.y]);
@@ -92,7 +95,21 @@ __global__ void scatter_kernel(PeerScatter sc, long long n16, PeerSignal sig, co
 #pragma unroll
   for (int k = 0; k < 3; ++k)
     if (i + k * stride < n16) dst[i + k * stride] = t[k];
-  finish_and_signal(sig, value, counter);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t* row_counter = counter + blockIdx.y;
+    if (atomicAdd(row_counter, 1u) == gridDim.x - 1) {
+      __threadfence_system();
+      if (sig.n == static_cast<int>(gridDim.y)) {
+        if (sig.flag[blockIdx.y] != nullptr) st_release_sys(sig.flag[blockIdx.y], *value);
+      } else {
+        for (int f = 0; f < sig.n; ++f)
+          if (sig.flag[f] != nullptr) st_release_sys(sig.flag[f], *value);
+      }
+      *row_counter = 0;  // re-arm (only this CTA touches it now)
+    }
+  }
 }
 
 cudaError_t scatter_and_signal(const PeerScatter& sc, long long n16, const PeerSignal& sig, const uint32_t* value,
@@ -111,7 +128,11 @@ __global__ void signal_kernel(PeerSignal sig, const uint32_t* value) {
   if (threadIdx.x < sig.n && sig.flag[threadIdx.x] != nullptr) st_release_sys(sig.flag[threadIdx.x], *value);
 }
 
-__global__ void bump_kernel(uint32_t* counter) { *counter += 1; }
+__global__ void bump_kernel(uint32_t* counter) {
+  const uint32_t v = *counter + 1;
+  *counter = v;
+  counter[-1] = v - 1;  // the previous step's value (flags "done with step t-1")
+}
 
 cudaError_t bump_counter(uint32_t* counter, cudaStream_t s) {
   bump_kernel<<<1, 1, 0, s>>>(counter);
@@ -164,8 +185,10 @@ cudaError_t shard_update(const ShardUpdate& u, const PeerSignal& done, const uin
                          uint32_t* counter, cudaStream_t s) {
   long long n4 = (u.end - u.begin) / 4;
   int grid = static_cast<int>(std::max<long long>(1, std::min<long long>((n4 + 255) / 256, num_sms() * 4)));
-  // NVLink bytes of this rank: peer shard reads of the gradient + peer parameter writes
-  const double peer_bytes = 2.0 * (u.nranks - 1) * static_cast<double>(u.end - u.begin) * sizeof(float);
+  // NVLink bytes of this rank PER DIRECTION: (W-1) peer shard reads of the gradient come in, the
+  // same number of bytes of updated parameters go out (both directions run concurrently, so the
+  // per-direction figure is what compares with the per-direction link peak)
+  const double peer_bytes = (u.nranks - 1) * static_cast<double>(u.end - u.begin) * sizeof(float);
   launch_timed([&] { shard_update_kernel<<<grid, 256, 0, s>>>(u, done, value, counter); }, s, KIND_SHARD_UPDATE,
                peer_bytes);
   return cudaGetLastError();

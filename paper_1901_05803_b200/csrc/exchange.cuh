@@ -31,8 +31,9 @@ struct PeerScatter {
   int n;
 };
 
-// dst[j] = src[j] (n16 chunks of 16 bytes each, j < sc.n) in one launch, then set every flag in
-// `sig` to `value` once all CTAs' stores are globally visible.
+// dst[j] = src[j] (n16 chunks of 16 bytes each, j < sc.n) in one launch.  With sig.n == sc.n,
+// sig.flag[j] is set to `value` as soon as destination j's bytes are globally visible (per-row
+// last-CTA counters counter[0..sc.n)); otherwise every flag once all rows are.
 cudaError_t scatter_and_signal(const PeerScatter& sc, long long n16, const PeerSignal& sig, const uint32_t* value,
                                uint32_t* counter, cudaStream_t s);
 
@@ -45,7 +46,8 @@ cudaError_t push_and_signal(void* dst, const void* src, long long n16, const Pee
 // Set flags only (after a fence of this kernel's predecessors on the stream).
 cudaError_t signal_only(const PeerSignal& sig, const uint32_t* value, cudaStream_t s);
 
-// *counter += 1 (the per-step sequence number, first node of the step).
+// *counter += 1 (the per-step sequence number, first node of the step); counter[-1] = the new
+// value - 1 (wait target for "the peer finished the previous step").
 cudaError_t bump_counter(uint32_t* counter, cudaStream_t s);
 
 // Flag values are read from device memory (`value` points at the rank's step counter) so a

@@ -17,8 +17,9 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _lib
-from .planner.costmodel import JobSpec, StrategyKind, volume_ralp_multi_ps, volumes_for
-from .planner.layers import LayerKind, ModelGraph
+from .planner.costmodel import (JobSpec, volume_baseline, volume_ralp, volume_ralp_multi_ps,
+                                 volume_ring)
+from .planner.layers import ModelGraph
 from .report import JobReport, StepBreakdown
 
 
@@ -26,11 +27,18 @@ class ExecutorError(ValueError):
     """The job cannot be executed by this backend (unsupported layer mix etc.)."""
 
 
+def _kv(x) -> str:
+    """Enum member -> its value string.  Layer and strategy kinds are compared by value so jobs
+    built with the unmodified reference package (`ralp.ModelGraph`, `ralp.JobSpec`,
+    pkg/src/ralp/layers.py:22-34, costmodel.py:34-37) lower exactly like the mirror's."""
+    return getattr(x, "value", x)
+
+
 def infer_input_shape(model: ModelGraph) -> tuple[int, int, int]:
     """Per-sample input (h, w, c) of the first layer (a convolution): the smallest input that
     yields its recorded output shape (infer_conv, layers.py:87-103)."""
     first = model.layers[0]
-    if first.kind is not LayerKind.CONVOLUTION or first.output_shape is None:
+    if _kv(first.kind) != "conv" or first.output_shape is None:
         raise ExecutorError("the first layer must be a derived convolution")
     hp = first.hyperparams
     k, s, p, cout = hp["k"], hp.get("stride", 1), hp.get("pad", 0), hp["cout"]
@@ -48,29 +56,42 @@ def lower(model: ModelGraph, input_shape: Optional[tuple[int, int, int]] = None)
     for i, L in enumerate(model.layers):
         hp = L.hyperparams
         last = i == n - 1
-        if L.kind is LayerKind.CONVOLUTION:
+        kind = _kv(L.kind)
+        if kind == "conv":
             d = dict(kind="conv", k=hp["k"], stride=hp.get("stride", 1), pad=hp.get("pad", 0), h=h, w=w, cin=c,
                      cout=hp["cout"], relu=1)
             h, w, c = L.output_shape.h, L.output_shape.w, L.output_shape.c
-        elif L.kind is LayerKind.POOLING:
+        elif kind == "pool":
             d = dict(kind="pool", k=hp["window"], stride=hp.get("stride", hp["window"]), pad=hp.get("pad", 0), h=h,
                      w=w, cin=c, cout=c, relu=0)
             if d["pad"]:
                 raise ExecutorError(f"layer {L.name}: padded pooling is not implemented")
             h, w, c = L.output_shape.h, L.output_shape.w, L.output_shape.c
-        elif L.kind is LayerKind.FULLY_CONNECTED:
+        elif kind == "fc":
             width = flat if flat is not None else (h * w * c if h else c)
             d = dict(kind="fc", k=0, stride=0, pad=0, h=0, w=0, cin=width, cout=hp["out"], relu=0 if last else 1)
             flat = hp["out"]
             h = w = 0
             c = flat
-        elif L.kind is LayerKind.FLATTEN:
+        elif kind == "flatten":
             continue
         else:
-            raise ExecutorError(f"layer {L.name}: kind {L.kind.value} is not executable by this backend")
+            raise ExecutorError(f"layer {L.name}: kind {kind} is not executable by this backend")
         d["name"] = L.name
         out.append(d)
     return out
+
+
+def expected_volume(job, fc_sharding: str = "single") -> int:
+    """The oracle's logical synchronised bytes per step for `job` (costmodel.py:107-162), dispatched
+    on the strategy's value so a reference `ralp.JobSpec` works too."""
+    kind, m, w = _kv(job.strategy.kind), job.model, job.worker_count
+    if kind == "ralp":
+        f = volume_ralp_multi_ps if fc_sharding == "multi" else volume_ralp
+        return f(m, job.strategy.split_index, w).total_bytes_per_step
+    if kind == "ring":
+        return volume_ring(m, w).total_bytes_per_step
+    return volume_baseline(m, w).total_bytes_per_step
 
 
 def allgather_bytes(blob: bytes) -> list[bytes]:
@@ -114,6 +135,8 @@ class StepResult:
     ms_sync: float
     ms_gemm: float = 0.0
     gemm_launches: int = 0
+    nvlink_out_bytes: int = 0
+    nvlink_in_bytes: int = 0
 
 
 class RankExecutor:
@@ -122,41 +145,60 @@ class RankExecutor:
 
     def __init__(self, job: JobSpec, *, rank: int = 0, world: Optional[int] = None, ps_rank: int = 0,
                  input_shape: Optional[tuple[int, int, int]] = None, ring_backend: str = "native",
-                 fc_sharding: str = "single"):
+                 fc_sharding: str = "single", precision: str = "bf16", placement: str = "colocated"):
         """ring_backend (StrategyKind.RING_ALLREDUCE only): "native" = the hand-written
         reduce-scatter + SGD + all-gather over NVLink peer memory inside the step; "nccl" = the
         step stops after the backward, torch.distributed (NCCL) all-reduces the gradient vector
         on the model stream, then the update runs (the comparison baseline).
         fc_sharding (StrategyKind.RALP only): "single" = the reference's single PS on rank 0;
         "multi" = the FC tail's first two layers sharded over every GPU (RALPB_STRATEGY_RALP_MPS,
-        SURVEY.md 8f.1; logical bytes volume_ralp_multi_ps)."""
-        world = job.worker_count if world is None else world
-        if world != job.worker_count:
-            raise ExecutorError("one rank per worker: world size must equal worker_count")
-        kind = job.strategy.kind
+        SURVEY.md 8f.1; logical bytes volume_ralp_multi_ps).
+        precision: "bf16" (throughput) or "fp32" (the parity mode: fp32-accurate (hi, lo) bf16
+        pairs through the same tcgen05 GEMM engine, include/ralpb.h RALPB_PRECISION_FP32).
+        placement (StrategyKind.RALP only): "colocated" = W ranks, the PS role on ps_rank which is
+        also a worker; "dedicated-ps" = the paper's RALP-N (costmodel.py:244-245): world = W + 1,
+        ps_rank runs only the FC tail, every other rank is a worker."""
+        kind = _kv(job.strategy.kind)
+        if placement not in ("colocated", "dedicated-ps"):
+            raise ExecutorError(f"unknown placement {placement!r}")
+        if placement == "dedicated-ps" and (kind != "ralp" or fc_sharding != "single"):
+            raise ExecutorError("a dedicated PS rank is a layer-placed (RALP, single PS) placement")
+        workers = job.worker_count
+        world = workers + (1 if placement == "dedicated-ps" else 0) if world is None else world
+        if world != workers + (1 if placement == "dedicated-ps" else 0):
+            raise ExecutorError("one rank per worker (plus the dedicated PS rank): world size must be "
+                                f"{workers + (1 if placement == 'dedicated-ps' else 0)}")
         if ring_backend not in ("native", "nccl"):
             raise ExecutorError(f"unknown ring backend {ring_backend!r}")
         if fc_sharding not in ("single", "multi"):
             raise ExecutorError(f"unknown fc_sharding {fc_sharding!r}")
-        self.fc_sharding = fc_sharding if kind is StrategyKind.RALP else "single"
-        self.ring_backend = ring_backend if kind is StrategyKind.RING_ALLREDUCE else None
+        if precision not in _lib.PRECISIONS:
+            raise ExecutorError(f"unknown precision {precision!r}")
+        self.fc_sharding = fc_sharding if kind == "ralp" else "single"
+        self.ring_backend = ring_backend if kind == "ring" else None
+        self.precision, self.placement = precision, placement
         self.job = job
         self.model = job.model
         self.rank, self.world, self.ps_rank = rank, world, ps_rank
+        self.workers = workers
+        self.is_worker = not (placement == "dedicated-ps" and rank == ps_rank)
+        # worker index (rank order, the dedicated PS skipped): its sample block of every step
+        self.worker_index = rank - (1 if placement == "dedicated-ps" and rank > ps_rank else 0)
         self.layers = lower(job.model, input_shape)
         self.in_shape = (self.layers[0]["h"], self.layers[0]["w"], self.layers[0]["cin"])
         self.classes = self.layers[-1]["cout"]
-        split = job.strategy.split_index if kind is StrategyKind.RALP else 0
-        if kind is StrategyKind.RALP:
+        split = job.strategy.split_index if kind == "ralp" else 0
+        if kind == "ralp":
             strategy = _lib.RALPB_STRATEGY_RALP if self.fc_sharding == "single" else _lib.RALPB_STRATEGY_RALP_MPS
-        elif kind is StrategyKind.RING_ALLREDUCE:
+        elif kind == "ring":
             strategy = _lib.RALPB_STRATEGY_RING if ring_backend == "native" else _lib.RALPB_STRATEGY_RING_EXTERNAL
         else:
             strategy = _lib.RALPB_STRATEGY_BASELINE
         self._descs = _desc_array(self.layers)
         h = C.c_void_p()
         _lib.call("ralpb_model_create", C.cast(self._descs, C.c_void_p), len(self.layers), split,
-                  job.model.batch_size, strategy, rank, world, ps_rank, job.model.bytes_per_element, C.byref(h))
+                  job.model.batch_size, strategy, rank, world, ps_rank, job.model.bytes_per_element,
+                  _lib.PRECISIONS[precision], workers, C.byref(h))
         self._h = h
         if world > 1:
             self._open_peers()
@@ -193,6 +235,38 @@ class RankExecutor:
             out.append((w, b))
         return out
 
+    def get_grads(self) -> list:
+        """This rank's parameter gradients of the last step (per layer (w, b) or None), in the
+        get_params layout; the FC tail's only on the rank that holds it."""
+        out = []
+        for i, L in enumerate(self.layers):
+            if L["kind"] == "conv":
+                w = np.empty((L["cout"], L["k"], L["k"], L["cin"]), dtype=np.float32)
+            elif L["kind"] == "fc":
+                w = np.empty((L["cout"], L["cin"]), dtype=np.float32)
+            else:
+                out.append(None)
+                continue
+            b = np.empty(L["cout"], dtype=np.float32)
+            _lib.call("ralpb_model_get_grads", self._h, i, _ptr(w), _ptr(b))
+            out.append((w, b))
+        return out
+
+    def debug_buffer(self, which: int, i: int = 0) -> np.ndarray:
+        """A copy of one of the last step's device buffers (include/ralpb.h RALPB_DBG_*), flat:
+        fp32 for LOGITS / MPS_PARTIAL, bf16 values widened to fp32 otherwise (bf16 precision)."""
+        import torch
+        n = _lib.lib().ralpb_model_debug_buffer(self._h, i, which, None)
+        if n < 0:
+            raise ExecutorError(f"debug buffer {which}/{i} is not available")
+        f32 = which in (_lib.DBG_LOGITS, _lib.DBG_MPS_PARTIAL)
+        pair = self.precision == "fp32"
+        elems = n * (2 if pair else 1)
+        t = torch.empty(elems, dtype=torch.float32 if f32 else torch.bfloat16)
+        if _lib.lib().ralpb_model_debug_buffer(self._h, i, which, C.c_void_p(t.data_ptr())) != n:
+            raise ExecutorError(f"debug buffer {which}/{i}: copy failed")
+        return t.float().numpy()
+
     # ---------------------------------------------------------------- step
     @property
     def stream(self) -> int:
@@ -200,9 +274,11 @@ class RankExecutor:
 
     def step(self, images, labels, *, lr: float = 0.01, momentum: float = 0.9) -> None:
         """images/labels: numpy host arrays (pinned-ness is the caller's business) or torch
-        tensors (host or cuda)."""
+        tensors (host or cuda); None on a dedicated PS rank (it has no batch of its own)."""
         on_host = 1
-        if hasattr(images, "data_ptr"):
+        if images is None:
+            ip, lp, on_host = None, None, 0
+        elif hasattr(images, "data_ptr"):
             ip, lp = images.data_ptr(), labels.data_ptr()
             on_host = 0 if images.is_cuda else 1
         else:
@@ -239,7 +315,8 @@ class RankExecutor:
         st = _lib.StepStats()
         _lib.call("ralpb_model_stats", self._h, C.byref(st))
         return StepResult(st.loss, st.logical_bytes, st.physical_bytes, st.launches, st.ms_step, st.ms_front_fwd,
-                          st.ms_back, st.ms_front_bwd, st.ms_sync, st.ms_gemm, st.gemm_launches)
+                          st.ms_back, st.ms_front_bwd, st.ms_sync, st.ms_gemm, st.gemm_launches,
+                          st.nvlink_out_bytes, st.nvlink_in_bytes)
 
     def read_loss(self, lag: int = 0) -> float:
         """Loss of the step issued `lag` steps ago; waits for that step only."""
@@ -268,48 +345,86 @@ class RankExecutor:
             pass
 
 
+def _allgather_rows(row: list[float], world: int) -> list[list[float]]:
+    """Every rank's `row` (equal length), rank-ordered, over the initialised process group."""
+    if world == 1:
+        return [row]
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    mine = torch.tensor(row, dtype=torch.float64, device=dev)
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    return [p.cpu().tolist() for p in parts]
+
+
 def run_job(job: JobSpec, steps: int = 10, *, warmup: int = 0, seed: int = 0, lr: float = 0.01,
             momentum: float = 0.9, params=None, input_shape=None, name: Optional[str] = None,
-            ring_backend: str = "native", fc_sharding: str = "single") -> JobReport:
-    """Execute `job` for `steps` measured steps on this process's rank (RANK/WORLD_SIZE from the
-    environment, torch.distributed already initialised when W > 1).  Returns the job report on
-    every rank (rank 0's carries the loss)."""
+            ring_backend: str = "native", fc_sharding: str = "single", precision: str = "bf16",
+            placement: str = "colocated") -> JobReport:
+    """Execute `job` for `steps` measured steps on this process's rank (RANK from the environment,
+    torch.distributed already initialised when more than one rank takes part).  `job` may be the
+    mirror's JobSpec or the unmodified reference's `ralp.JobSpec`.  Every step checks that the
+    logical bytes the ranks counted at their count_wire sites sum to the oracle's volume.  Returns
+    the job report on every rank, with every worker's own measured times (rank 0's carries the
+    losses)."""
     from . import synthetic
 
     rank = int(os.environ.get("RANK", "0"))
-    ex = RankExecutor(job, rank=rank, input_shape=input_shape, ring_backend=ring_backend, fc_sharding=fc_sharding)
+    ex = RankExecutor(job, rank=rank, input_shape=input_shape, ring_backend=ring_backend, fc_sharding=fc_sharding,
+                      precision=precision, placement=placement)
     try:
         if params is None:
             params = synthetic.init_params(ex.layers, seed)
         ex.set_params(params)
         b = job.model.batch_size
         records, losses = [], []
-        expected = volumes_for(job).total_bytes_per_step
-        if ex.fc_sharding == "multi":
-            expected = volume_ralp_multi_ps(job.model, job.strategy.split_index, job.worker_count).total_bytes_per_step
+        expected = expected_volume(job, ex.fc_sharding)
         for t in range(warmup + steps):
-            imgs, labs = synthetic.batch(seed, t, rank * b, b, ex.in_shape, ex.classes)
-            ex.step(imgs, labs, lr=lr, momentum=momentum)
+            if ex.is_worker:
+                imgs, labs = synthetic.batch(seed, t, ex.worker_index * b, b, ex.in_shape, ex.classes)
+                ex.step(imgs, labs, lr=lr, momentum=momentum)
+            else:
+                ex.step(None, None, lr=lr, momentum=momentum)
             st = ex.stats()
-            if st.logical_bytes != expected:
-                raise ExecutorError(f"logical bytes {st.logical_bytes} != oracle volume {expected}")
+            rows = _allgather_rows([st.logical_bytes, st.ms_step, st.ms_front_fwd + st.ms_front_bwd, st.ms_back,
+                                    1.0 if ex.is_worker else 0.0, 1.0 if rank == ex.ps_rank else 0.0], ex.world)
+            total = int(round(sum(r[0] for r in rows)))
+            if total != expected:
+                raise ExecutorError(f"logical bytes {total} (summed over ranks) != oracle volume {expected}")
             if t >= warmup:
                 losses.append(st.loss)
-                records.append(_breakdown(name or job.model.name, len(records) + 1, st, job.worker_count))
-        return JobReport(job=name or job.model.name, strategy=job.strategy.kind.value,
+                records.append(_breakdown(name or job.model.name, len(records) + 1, rows, _kv(job.strategy.kind)))
+        return JobReport(job=name or job.model.name, strategy=_kv(job.strategy.kind),
                          worker_count=job.worker_count, batch_size=b, steps=tuple(records),
                          bytes_on_wire_per_step=expected, losses=tuple(losses))
     finally:
         ex.close()
 
 
-def _breakdown(name: str, step: int, st: StepResult, w: int) -> StepBreakdown:
-    # per-rank device times (seconds) in the reference's four categories (simulator.py:163-210);
-    # every worker is reported with this rank's timing (ranks are symmetric up to the PS role)
+def _breakdown(name: str, step: int, rows: list[list[float]], kind: str) -> StepBreakdown:
+    """Every worker's measured step (seconds) in the reference's four categories
+    (simulator.py:163-210).  worker_computation = its front forward + backward; ps_computation =
+    the back segment where the FC tail runs on that worker's GPU (the colocated PS; the dedicated
+    PS's tail is charged to every worker in equal shares, like the reference's per-worker
+    back_batch_s, simulator.py:695); communication = the rest of its step (cut / act-grad exchange,
+    waiting, sharded-PS sync).  memcopy is 0: on this backend no cut, act-grad or parameter is
+    staged through host memory (the reference models cudaMemcpy d2h/h2d, simulator.py:676,685)."""
     s = 1e-3
-    comp = (st.ms_front_fwd + st.ms_front_bwd) * s
-    return StepBreakdown(job=name, step=step, worker_computation=(comp,) * w, ps_computation=(st.ms_back * s,) * w,
-                         memcopy=(0.0,) * w, communication=(st.ms_sync * s,) * w)
+    worker_rows = [r for r in rows if r[4] > 0.5]
+    ps_rows = [r for r in rows if r[5] > 0.5 and r[4] < 0.5]
+    ps_share = (ps_rows[0][3] * s / len(worker_rows)) if ps_rows else 0.0
+    comp, ps, comm = [], [], []
+    for r in worker_rows:
+        c = (r[2] + (r[3] if kind != "ralp" else 0.0)) * s   # baseline / ring: the FC tail is worker compute
+        p = (r[3] * s if (r[5] > 0.5 and kind == "ralp") else 0.0) + ps_share
+        comp.append(c)
+        ps.append(p)
+        comm.append(max(0.0, r[1] * s - c - (r[3] * s if (r[5] > 0.5 and kind == "ralp") else 0.0)))
+    w = len(worker_rows)
+    return StepBreakdown(job=name, step=step, worker_computation=tuple(comp), ps_computation=tuple(ps),
+                         memcopy=(0.0,) * w, communication=tuple(comm))
 
 
-__all__ = ["ExecutorError", "RankExecutor", "StepResult", "infer_input_shape", "lower", "run_job", "allgather_bytes"]
+__all__ = ["ExecutorError", "RankExecutor", "StepResult", "expected_volume", "infer_input_shape", "lower", "run_job",
+           "allgather_bytes"]
