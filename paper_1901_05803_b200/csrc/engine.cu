@@ -28,6 +28,7 @@
 #include "elementwise.cuh"
 #include "engine.cuh"
 #include "gemm_host.cuh"
+#include "pair.cuh"
 
 namespace ralpb {
 
@@ -83,6 +84,9 @@ char* peer(Model* m, int r) { return m->peer_base[r]; }
 template <class T>
 T* at(Model* m, int r, size_t off) { return reinterpret_cast<T*>(peer(m, r) + off); }
 
+bool pair_mode(const Model* m);
+int pair_relayout(Model* m, bool front, bool fc, cudaStream_t s, std::string* why);
+
 }  // namespace
 
 int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int batch, int strategy,
@@ -100,8 +104,8 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     *why = "workers must equal world, or world - 1 (RALP-N: a dedicated PS rank, RALP strategy only)";
     return 1;
   }
-  if (precision == RALPB_PRECISION_FP32 && getenv("RALPB_FP32_WIP") == nullptr) {
-    *why = "precision FP32 is not available in this build";
+  if (precision == RALPB_PRECISION_FP32 && strategy == RALPB_STRATEGY_RALP_MPS) {
+    *why = "the sharded FC tail (RALP_MPS) runs in bf16 precision only";
     return 1;
   }
   auto m = new Model();
@@ -174,7 +178,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
       f.im2col = true;
       {
         const char* fe = getenv("RALPB_FIRST");
-        f.fused = conv_first_ok(d.h, d.w, d.cin, d.cout, d.k, d.stride, d.pad) &&
+        f.fused = precision == RALPB_PRECISION_BF16 && conv_first_ok(d.h, d.w, d.cin, d.cout, d.k, d.stride, d.pad) &&
                   !(fe != nullptr && std::strcmp(fe, "im2col") == 0);
       }
       f.kpad = in.c;
@@ -185,8 +189,8 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
       f.w_count = static_cast<long long>(d.cout) * f.kpad;
       f.w_off = off;
       f.b_off = -1;  // folded into column k*k*cin of the filter
-      for (int o = 0; o < d.cout; ++o)
-        real_runs.emplace_back(f.w_off + static_cast<long long>(o) * f.kpad, d.k * d.k * d.cin + 1);
+      for (int oc = 0; oc < d.cout; ++oc)
+        real_runs.emplace_back(f.w_off + static_cast<long long>(oc) * f.kpad, d.k * d.k * d.cin + 1);
       off = align_up(off + f.w_count, 4);
       m->real_front += static_cast<long long>(d.cout) * d.k * d.k * d.cin + d.cout;
       o.h = in.h; o.w = in.w; o.c = d.cout; o.pad = in.pad;
@@ -282,9 +286,10 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   m->arena_off_flags = take(kNumFlags * sizeof(uint32_t));
   m->arena_off_P = take(m->n_total * sizeof(float));
   m->arena_off_G = take(m->n_total * sizeof(float));
-  m->arena_off_xfc = take(static_cast<size_t>(m->rows_back) * m->cut_elems * sizeof(bf16));
+  const int pm = precision == RALPB_PRECISION_FP32 ? 2 : 1;  // (hi, lo) pairs: twice the bf16 elements
+  m->arena_off_xfc = take(static_cast<size_t>(m->rows_back) * m->cut_elems * sizeof(bf16) * pm);
   m->arena_off_lab = take(static_cast<size_t>(m->rows_back) * sizeof(int32_t));
-  m->arena_off_dcut = take(static_cast<size_t>(batch) * m->cut_elems * sizeof(bf16));
+  m->arena_off_dcut = take(static_cast<size_t>(batch) * m->cut_elems * sizeof(bf16) * pm);
   m->arena_off_loss = take(kMaxRanks * 4 * sizeof(float));   // [worker][4] own-row loss sums
   if (m->mps) {
     const int ld1 = static_cast<int>(align_up(layers[nconv + 1].cout, 8));
@@ -316,11 +321,11 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   // kernels write interior pixels only, so the padding borders stay zero for the job's life.
   m->gacts.assign(m->acts.size(), nullptr);
   for (size_t i = 0; m->is_worker && i < m->acts.size(); ++i) {
-    const size_t bytes = static_cast<size_t>(m->acts[i].elems()) * sizeof(bf16);
-    if (!(m->acts[i].ptr = alloc<bf16>(m, m->acts[i].elems(), why))) return fail(*why);
+    const size_t bytes = static_cast<size_t>(m->acts[i].elems()) * sizeof(bf16) * pm;
+    if (!(m->acts[i].ptr = alloc<bf16>(m, m->acts[i].elems() * pm, why))) return fail(*why);
     cudaMemset(m->acts[i].ptr, 0, bytes);
     if (i > 0 && i + 1 < m->acts.size()) {
-      if (!(m->gacts[i] = alloc<bf16>(m, m->acts[i].elems(), why))) return fail(*why);
+      if (!(m->gacts[i] = alloc<bf16>(m, m->acts[i].elems() * pm, why))) return fail(*why);
       cudaMemset(m->gacts[i], 0, bytes);
     }
   }
@@ -332,7 +337,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     FrontLayer& c = m->front[i];
     FrontLayer& pl = m->front[i + 1];
     if (c.kind == RALPB_CONV && !c.im2col && pl.kind == RALPB_POOL && pl.k == 2 && pl.stride == 2 &&
-        conv_fwd_pool_ok(c.g) && fuse_pool_enabled()) {
+        conv_fwd_pool_ok(c.g) && fuse_pool_enabled() && precision == RALPB_PRECISION_BF16) {
       pl.fused_fwd = true;
       const ActBuf& po = m->acts[i + 2];
       const char* ie = getenv("RALPB_POOL_IDX");
@@ -351,8 +356,9 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   }
   for (auto& f : m->front) {
     if (f.kind != RALPB_CONV || !m->is_worker) continue;
-    if (!(f.wf = alloc<bf16>(m, f.w_count, why))) return fail(*why);
-    if (!f.im2col && !(f.wd = alloc<bf16>(m, f.w_count, why))) return fail(*why);
+    // pair precision: [2co][taps][2ci] operand copies (pair.cuh)
+    if (!(f.wf = alloc<bf16>(m, f.w_count * pm * pm, why))) return fail(*why);
+    if (!f.im2col && !(f.wd = alloc<bf16>(m, f.w_count * pm * pm, why))) return fail(*why);
   }
   const int R = m->rows_back;
   if (m->mps) {
@@ -364,9 +370,18 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   }
   for (size_t j = 0; j < m->back.size(); ++j) {
     auto& f = m->back[j];
-    if (!(f.wbf = alloc<bf16>(m, static_cast<size_t>(f.lout) * f.lin, why))) return fail(*why);
+    if (pm == 2) {  // pair operands [2*ld_out][2*in] for the forward and the backward-data GEMMs
+      const size_t n4 = static_cast<size_t>(4) * f.ld_out * f.lin;
+      if (!(f.wbf = alloc<bf16>(m, n4, why)) || !(f.wbd = alloc<bf16>(m, n4, why))) return fail(*why);
+      cudaMemset(f.wbf, 0, n4 * sizeof(bf16));
+      cudaMemset(f.wbd, 0, n4 * sizeof(bf16));
+      m->pair_s_floats = std::max(m->pair_s_floats, n4);
+      m->pair_acc_floats = std::max(m->pair_acc_floats, static_cast<size_t>(2) * R * std::max(f.ld_out, f.lin));
+    } else if (!(f.wbf = alloc<bf16>(m, static_cast<size_t>(f.lout) * f.lin, why))) {
+      return fail(*why);
+    }
     if (j + 1 < m->back.size()) {
-      bf16* h = alloc<bf16>(m, static_cast<size_t>(R) * f.ld_out, why);
+      bf16* h = alloc<bf16>(m, static_cast<size_t>(R) * f.ld_out * pm, why);
       if (!h) return fail(*why);
       m->hid.push_back(h);
     }
@@ -375,14 +390,27 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   for (auto& f : m->back) widest = std::max(widest, f.ld_out);
   const FcLayer& last = m->back.back();
   if (!(m->logits = alloc<float>(m, static_cast<size_t>(R) * last.ld_out, why))) return fail(*why);
-  if (!(m->dlogits = alloc<bf16>(m, static_cast<size_t>(R) * last.ld_out, why))) return fail(*why);
-  cudaMemset(m->dlogits, 0, static_cast<size_t>(R) * last.ld_out * sizeof(bf16));
+  if (!(m->dlogits = alloc<bf16>(m, static_cast<size_t>(R) * last.ld_out * pm, why))) return fail(*why);
+  cudaMemset(m->dlogits, 0, static_cast<size_t>(R) * last.ld_out * sizeof(bf16) * pm);
   for (size_t j = 0; j + 1 < m->back.size(); ++j) {
-    bf16* d = alloc<bf16>(m, static_cast<size_t>(R) * m->back[j].ld_out, why);
+    bf16* d = alloc<bf16>(m, static_cast<size_t>(R) * m->back[j].ld_out * pm, why);
     if (!d) return fail(*why);
     m->dyb.push_back(d);
   }
-  if (!(m->dx_fc = alloc<bf16>(m, static_cast<size_t>(R) * m->cut_elems, why))) return fail(*why);
+  if (!(m->dx_fc = alloc<bf16>(m, static_cast<size_t>(R) * m->cut_elems * pm, why))) return fail(*why);
+  if (pm == 2) {
+    // scratch of the pair contractions: the fp32 [rows][2N] outputs before their finishing pass
+    // and the [2M][T][2C] weight-gradient blocks
+    for (size_t i = 0; i < m->front.size(); ++i) {
+      const FrontLayer& f = m->front[i];
+      if (f.kind != RALPB_CONV) continue;
+      const ActBuf& in = m->acts[i];
+      m->pair_acc_floats = std::max(m->pair_acc_floats, static_cast<size_t>(in.rows()) * 2 * std::max(f.g.cout, f.g.cin));
+      m->pair_s_floats = std::max(m->pair_s_floats, static_cast<size_t>(4) * static_cast<size_t>(f.w_count));
+    }
+    if (!(m->pair_acc = alloc<float>(m, m->pair_acc_floats, why))) return fail(*why);
+    if (!(m->pair_s = alloc<float>(m, m->pair_s_floats, why))) return fail(*why);
+  }
   if (!(m->fc_scratch = alloc<float>(m, static_cast<size_t>(R) * std::max(widest, m->cut_elems), why))) return fail(*why);
   if (!(m->row_loss = alloc<float>(m, R, why))) return fail(*why);
   if (!(m->loss = alloc<float>(m, 4, why))) return fail(*why);
@@ -494,8 +522,8 @@ int model_set_params(Model* m, int layer, const float* w, const float* b, int on
       RALPB_TRY(cudaMemcpyAsync(m->P + f.b_off, hb.data(), co * sizeof(float), cudaMemcpyHostToDevice, m->stream));
     }
     RALPB_TRY(cudaMemcpyAsync(m->P + f.w_off, packed.data(), packed.size() * sizeof(float), cudaMemcpyHostToDevice, m->stream));
-    if (!m->is_worker) {
-      // the dedicated PS keeps no operand copies of the front
+    if (!m->is_worker || pair_mode(m)) {
+      // the dedicated PS keeps no operand copies of the front; pairs: pair_relayout below
     } else if (f.im2col) {
       RALPB_TRY(cast_bf16(m->P + f.w_off, f.w_count, f.wf, m->stream));
     } else {
@@ -517,8 +545,9 @@ int model_set_params(Model* m, int layer, const float* w, const float* b, int on
       RALPB_TRY(cudaMemcpyAsync(m->P + f.w_off, w, static_cast<size_t>(f.out) * f.in * sizeof(float), kind, m->stream));
       RALPB_TRY(cudaMemcpyAsync(m->P + f.b_off, b, f.out * sizeof(float), kind, m->stream));
     }
-    RALPB_TRY(cast_bf16(m->P + f.w_off, static_cast<long long>(f.lout) * f.lin, f.wbf, m->stream));
+    if (!pair_mode(m)) RALPB_TRY(cast_bf16(m->P + f.w_off, static_cast<long long>(f.lout) * f.lin, f.wbf, m->stream));
   }
+  if (pair_mode(m) && pair_relayout(m, layer < m->split, layer >= m->split, m->stream, why)) return 1;
   RALPB_TRY(cudaStreamSynchronize(m->stream));
   return 0;
 }
@@ -1115,6 +1144,299 @@ cudaError_t mark(Model* m, int i, bool capturing) {
                    : cudaEventRecord(m->ev[i], m->stream);
 }
 
+// ------------------------------------------------------------------ pair precision
+// The parity precision (RALPB_PRECISION_FP32): the same schedule, every activation / gradient an
+// fp32-accurate (hi, lo) bf16 pair, every contraction the tcgen05 GEMM engine over the pairs with
+// an fp32 result finished by pair.cu (layouts in pair.cuh).
+
+bool pair_mode(const Model* m) { return m->precision == RALPB_PRECISION_FP32; }
+
+// FC layer j's input as (groups, channels): the cut (HWC pixels x channels) or a hidden row.
+void fc_in_geom(const Model* m, int j, int* groups, int* c) {
+  if (j == 0) {
+    const ActBuf& cut = m->acts.back();
+    *groups = cut.h * cut.w;
+    *c = cut.c;
+  } else {
+    *groups = 1;
+    *c = m->back[j].in;
+  }
+}
+
+// Pair operand copies of every parameter from the fp32 masters.
+int pair_relayout(Model* m, bool front, bool fc, cudaStream_t s, std::string* why) {
+  if (front && m->is_worker) {
+    for (auto& f : m->front) {
+      if (f.kind != RALPB_CONV) continue;
+      if (f.im2col)
+        RALPB_TRY(pair_prep_mat(m->P + f.w_off, f.g.cout, f.g.cout, 1, f.kpad, f.wf, nullptr, s));
+      else
+        RALPB_TRY(pair_prep_conv(m->P + f.w_off, f.g.cout, f.g.taps(), f.g.cin, f.wf, f.wd, s));
+      ++m->launches;
+    }
+  }
+  if (fc) {
+    for (size_t j = 0; j < m->back.size(); ++j) {
+      FcLayer& f = m->back[j];
+      int groups = 0, c = 0;
+      fc_in_geom(m, static_cast<int>(j), &groups, &c);
+      RALPB_TRY(pair_prep_mat(m->P + f.w_off, f.out, f.ld_out, groups, c, f.wbf, f.wbd, s));
+      ++m->launches;
+    }
+  }
+  return 0;
+}
+
+// out[M][N] (+)= A . B^T on the GEMM engine with an fp32 result (atomic: split-K, caller zeroes).
+int pair_gemm(Model* m, GemmDesc d, void* out, long long s_m, long long s_n, bool atomic, std::string* why) {
+  d.epi = atomic ? EPI_F32_ATOMIC : EPI_F32;
+  d.k_splits = atomic ? 0 : 1;
+  d.out = out;
+  d.s_m = s_m;
+  d.s_n = s_n;
+  RALPB_TRY(gemm_launch(d, m->stream, why));
+  ++m->launches;
+  return 0;
+}
+
+void set_border(GemmDesc* d, const ActBuf& a) {
+  d->border = 1;
+  d->img_rows = (a.h + 2 * a.pad) * (a.w + 2 * a.pad);
+  d->wp = a.w + 2 * a.pad;
+  d->pad = a.pad;
+  d->h = a.h;
+  d->w = a.w;
+}
+
+PairFinish finish_for(const ActBuf& a, const float* acc, int n, const float* bias, int relu, const bf16* mask,
+                      bf16* out2) {
+  PairFinish f{};
+  f.acc = acc;
+  f.rows = a.rows();
+  f.n = n;
+  f.ld = n;
+  f.bias = bias;
+  f.relu = relu;
+  f.mask = mask;
+  f.out2 = out2;
+  f.border = 1;
+  f.img_rows = (a.h + 2 * a.pad) * (a.w + 2 * a.pad);
+  f.wp = a.w + 2 * a.pad;
+  f.pad = a.pad;
+  f.h = a.h;
+  f.w = a.w;
+  return f;
+}
+
+int pair_front_forward(Model* m, const float* img, bf16* cut_dst, std::string* why) {
+  cudaStream_t s = m->stream;
+  const int b = m->batch;
+  for (size_t i = 0; i < m->front.size(); ++i) {
+    FrontLayer& f = m->front[i];
+    const ActBuf& in = m->acts[i];
+    ActBuf out = m->acts[i + 1];
+    if (i + 1 == m->front.size()) out.ptr = cut_dst;
+    if (f.im2col) {
+      const FrontLayer& f0 = m->front[0];
+      RALPB_TRY(pair_pack_im2col(img, b, m->in_h, m->in_w, m->in_c, f0.k, f0.stride, m->desc[0].pad, in.h, in.w, in.pad,
+                                 f0.kpad, in.ptr, s));
+      ++m->launches;
+      GemmDesc d;
+      d.M = static_cast<int>(in.rows()); d.N = 2 * f.g.cout; d.K = 2 * f.kpad;
+      d.kb = std::min(64, 2 * f.kpad);
+      d.a = Operand2D{in.ptr, in.rows(), 2 * f.kpad, 2 * f.kpad};
+      d.b = Operand2D{f.wf, 2 * f.g.cout, 2 * f.kpad, 2 * f.kpad};
+      set_border(&d, out);
+      if (pair_gemm(m, d, m->pair_acc, 2 * f.g.cout, 1, false, why)) return 1;
+      RALPB_TRY(pair_finish(finish_for(out, m->pair_acc, f.g.cout, nullptr, 1, nullptr, out.ptr), s));
+      ++m->launches;
+    } else if (f.kind == RALPB_CONV) {
+      const ConvGeom& g = f.g;
+      GemmDesc d;
+      d.M = static_cast<int>(g.q()); d.N = 2 * g.cout;
+      d.kb = std::min(64, 2 * g.cin);
+      d.K = static_cast<long long>(g.taps()) * 2 * g.cin;
+      d.a_mode = LD_K_CONV;
+      d.a = Operand2D{in.ptr, g.q(), 2 * g.cin, 2 * g.cin};
+      d.cblks = 2 * g.cin / d.kb;
+      d.b = Operand2D{f.wf, 2 * g.cout, d.K, d.K};
+      d.taps = g.taps();
+      for (int r = 0; r < g.k; ++r)
+        for (int c = 0; c < g.k; ++c) d.tap_off[r * g.k + c] = (r - g.pad) * g.wp() + (c - g.pad);
+      set_border(&d, out);
+      if (pair_gemm(m, d, m->pair_acc, 2 * g.cout, 1, false, why)) return 1;
+      RALPB_TRY(pair_finish(finish_for(out, m->pair_acc, g.cout, m->P + f.b_off, 1, nullptr, out.ptr), s));
+      ++m->launches;
+    } else {
+      RALPB_TRY(pair_maxpool_fwd(in.ptr, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.ptr, out.pad, f.idx, s));
+      ++m->launches;
+    }
+  }
+  return 0;
+}
+
+// FC tail forward + loss over R rows of x_fc: logits (fp32), dlogits (pair), loss share.
+int pair_fc_forward_loss(Model* m, int R, float scale, std::string* why) {
+  cudaStream_t s = m->stream;
+  const bf16* x = m->x_fc;
+  long long in2 = 2LL * m->cut_elems;
+  const int nb = static_cast<int>(m->back.size());
+  for (int j = 0; j < nb; ++j) {
+    FcLayer& f = m->back[j];
+    GemmDesc d;
+    d.M = R; d.N = 2 * f.ld_out; d.K = in2;
+    d.a = Operand2D{x, R, in2, in2};
+    d.b = Operand2D{f.wbf, 2 * f.ld_out, in2, in2};
+    RALPB_TRY(cudaMemsetAsync(m->pair_acc, 0, sizeof(float) * R * 2 * f.ld_out, s));
+    if (pair_gemm(m, d, m->pair_acc, 2 * f.ld_out, 1, true, why)) return 1;
+    PairFinish fin{};
+    fin.acc = m->pair_acc; fin.rows = R; fin.n = f.out; fin.ld = f.ld_out; fin.bias = m->P + f.b_off;
+    const bool hidden = j + 1 < nb;
+    fin.relu = hidden ? 1 : 0;
+    fin.out2 = hidden ? m->hid[j] : nullptr;
+    fin.out_f32 = hidden ? nullptr : m->logits;
+    fin.ld_f32 = f.ld_out;
+    RALPB_TRY(pair_finish(fin, s));
+    m->launches += 2;
+    x = hidden ? m->hid[j] : nullptr;
+    in2 = 2LL * f.ld_out;
+  }
+  const FcLayer& last = m->back.back();
+  RALPB_TRY(pair_softmax_xent(m->logits, R, last.out, last.ld_out, m->labels_all, scale, m->row_loss, m->dlogits, s));
+  RALPB_TRY(reduce_sum(m->row_loss, R, scale, m->loss, s));
+  m->launches += 2;
+  return 0;
+}
+
+// FC backward-data chain down to the cut gradient rows (pairs in the cut's pixel-group layout).
+int pair_fc_backward_data(Model* m, int R, bf16* dx_out, std::string* why) {
+  cudaStream_t s = m->stream;
+  const int nb = static_cast<int>(m->back.size());
+  for (int j = nb - 1; j >= 0; --j) {
+    FcLayer& f = m->back[j];
+    const bf16* dy = j == nb - 1 ? m->dlogits : m->dyb[j];
+    int groups = 0, c = 0;
+    fc_in_geom(m, j, &groups, &c);
+    const long long in2 = 2LL * groups * c;
+    GemmDesc d;
+    d.M = R; d.N = static_cast<int>(in2); d.K = 2 * f.ld_out;
+    d.a_mode = LD_K; d.a = Operand2D{dy, R, 2 * f.ld_out, 2 * f.ld_out};
+    d.b_mode = LD_MN; d.b = Operand2D{f.wbd, 2 * f.ld_out, in2, in2};
+    RALPB_TRY(cudaMemsetAsync(m->pair_acc, 0, sizeof(float) * R * in2, s));
+    if (pair_gemm(m, d, m->pair_acc, in2, 1, true, why)) return 1;
+    PairFinishGroups fin{};
+    fin.acc = m->pair_acc; fin.rows = R; fin.groups = groups; fin.c = c;
+    fin.mask = j > 0 ? m->hid[j - 1] : nullptr;
+    fin.out2 = j > 0 ? m->dyb[j - 1] : dx_out;
+    RALPB_TRY(pair_finish_groups(fin, s));
+    m->launches += 2;
+  }
+  return 0;
+}
+
+// FC weight / bias gradients into G, and (update) the PS-local SGD with the pair re-layout.
+int pair_fc_backward_weights(Model* m, int R, bool update, float lr, float mu, std::string* why) {
+  cudaStream_t s = m->stream;
+  const int nb = static_cast<int>(m->back.size());
+  for (int j = nb - 1; j >= 0; --j) {
+    FcLayer& f = m->back[j];
+    const bf16* dy = j == nb - 1 ? m->dlogits : m->dyb[j];
+    const bf16* x = j == 0 ? m->x_fc : m->hid[j - 1];
+    int groups = 0, c = 0;
+    fc_in_geom(m, j, &groups, &c);
+    const long long in2 = 2LL * groups * c;
+    RALPB_TRY(cudaMemsetAsync(m->G + f.b_off, 0, f.out * sizeof(float), s));
+    RALPB_TRY(pair_colsum(dy, R, f.out, f.ld_out, m->G + f.b_off, s));
+    GemmDesc w;
+    w.M = 2 * f.ld_out; w.N = static_cast<int>(in2); w.K = R;
+    w.a_mode = LD_MN; w.a = Operand2D{dy, R, 2 * f.ld_out, 2 * f.ld_out};
+    w.b_mode = LD_MN; w.b = Operand2D{x, R, in2, in2};
+    RALPB_TRY(cudaMemsetAsync(m->pair_s, 0, sizeof(float) * 2 * f.ld_out * in2, s));
+    if (pair_gemm(m, w, m->pair_s, in2, 1, true, why)) return 1;
+    RALPB_TRY(pair_reduce_wgrad(m->pair_s, f.ld_out, f.out, groups, c, m->G + f.w_off, static_cast<long long>(groups) * c, s));
+    m->launches += 3;
+  }
+  if (update) {
+    for (auto& f : m->back) {
+      RALPB_TRY(sgd_momentum(m->P + f.w_off, m->V + f.w_off, m->G + f.w_off, static_cast<long long>(f.out) * f.in, lr, mu,
+                             1.f, s));
+      RALPB_TRY(sgd_momentum(m->P + f.b_off, m->V + f.b_off, m->G + f.b_off, f.out, lr, mu, 1.f, s));
+      m->launches += 2;
+    }
+    if (pair_relayout(m, false, true, s, why)) return 1;
+  }
+  return 0;
+}
+
+int pair_front_backward(Model* m, const bf16* dcut, std::string* why) {
+  cudaStream_t s = m->stream;
+  const bf16* cur = dcut;
+  for (int i = static_cast<int>(m->front.size()) - 1; i >= 0; --i) {
+    FrontLayer& f = m->front[i];
+    const ActBuf& in = m->acts[i];
+    const ActBuf& out = m->acts[i + 1];
+    if (f.kind == RALPB_POOL) {
+      RALPB_TRY(pair_maxpool_bwd(f.idx, cur, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.pad, m->gacts[i], nullptr,
+                                 s));
+      ++m->launches;
+      cur = m->gacts[i];
+      continue;
+    }
+    if (f.im2col) {
+      // dW[co][j] = sum over the output grid of dY[row][co] * patches[row][j] (bias in column k*k*cin)
+      GemmDesc d;
+      d.M = 2 * f.g.cout; d.N = 2 * f.kpad; d.K = in.rows();
+      d.a_mode = LD_MN; d.a = Operand2D{cur, out.rows(), 2 * f.g.cout, 2 * f.g.cout};
+      d.b_mode = LD_MN; d.b = Operand2D{in.ptr, in.rows(), 2 * f.kpad, 2 * f.kpad};
+      RALPB_TRY(cudaMemsetAsync(m->pair_s, 0, sizeof(float) * 4 * f.g.cout * f.kpad, s));
+      if (pair_gemm(m, d, m->pair_s, 2 * f.kpad, 1, true, why)) return 1;
+      RALPB_TRY(pair_reduce_wgrad(m->pair_s, f.g.cout, f.g.cout, 1, f.kpad, m->G + f.w_off, f.kpad, s));
+      ++m->launches;
+      continue;
+    }
+    const ConvGeom& g = f.g;
+    // bias gradient: sum of the (masked) output gradient
+    RALPB_TRY(pair_colsum(cur, out.rows(), g.cout, g.cout, m->G + f.b_off, s));
+    // weight gradient: S[(a,co)][t][(b,ci)] = sum_q dy_a[q][co] x_b[q + off(t)][ci]
+    {
+      GemmDesc d;
+      d.M = g.taps() * 2 * g.cin; d.N = 2 * g.cout; d.K = g.q();
+      d.a_mode = LD_MN_CONV; d.a = Operand2D{in.ptr, g.q(), 2 * g.cin, 2 * g.cin}; d.a_cin = 2 * g.cin;
+      d.b_mode = LD_MN; d.b = Operand2D{cur, g.q(), 2 * g.cout, 2 * g.cout};
+      d.taps = g.taps();
+      for (int r = 0; r < g.k; ++r)
+        for (int c = 0; c < g.k; ++c) d.tap_off[r * g.k + c] = (r - g.pad) * g.wp() + (c - g.pad);
+      const int n2 = 2 * g.cout;
+      d.block_n = n2 >= 256 ? 256 : (n2 >= 128 ? 128 : (n2 >= 64 ? 64 : 32));
+      RALPB_TRY(cudaMemsetAsync(m->pair_s, 0, sizeof(float) * 4 * f.w_count, s));
+      if (pair_gemm(m, d, m->pair_s, 1, static_cast<long long>(g.taps()) * 2 * g.cin, true, why)) return 1;
+      RALPB_TRY(pair_reduce_wgrad(m->pair_s, g.cout, g.cout, g.taps(), g.cin, m->G + f.w_off,
+                                  static_cast<long long>(g.taps()) * g.cin, s));
+      m->launches += 2;
+    }
+    if (i > 0) {
+      // backward-data: out[q][(a,ci)] = sum dy[q + off'][(b,co)] wd_a; masked by the producer's ReLU
+      GemmDesc d;
+      d.M = static_cast<int>(g.q()); d.N = 2 * g.cin;
+      d.kb = std::min(64, 2 * g.cout);
+      d.K = static_cast<long long>(g.taps()) * 2 * g.cout;
+      d.a_mode = LD_K_CONV; d.a = Operand2D{cur, g.q(), 2 * g.cout, 2 * g.cout};
+      d.cblks = 2 * g.cout / d.kb;
+      d.b = Operand2D{f.wd, 2 * g.cin, d.K, d.K};
+      d.taps = g.taps();
+      for (int r = 0; r < g.k; ++r)
+        for (int c = 0; c < g.k; ++c) d.tap_off[r * g.k + c] = (r - g.pad) * g.wp() + (c - g.pad);
+      set_border(&d, in);
+      if (pair_gemm(m, d, m->pair_acc, 2 * g.cin, 1, false, why)) return 1;
+      const bool mask = m->front[i - 1].kind == RALPB_CONV;
+      RALPB_TRY(pair_finish(finish_for(in, m->pair_acc, g.cin, nullptr, 0, mask ? in.ptr : nullptr, m->gacts[i]), s));
+      ++m->launches;
+      cur = m->gacts[i];
+    }
+  }
+  return 0;
+}
+
 __global__ void combine_loss_kernel(const float* slots, int n, int self, float* out) {
   // out[0] = own share + the other workers' shares (slots[w * 4], w != self), fixed order
   if (threadIdx.x == 0) {
@@ -1169,11 +1491,18 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   RALPB_TRY(bump_counter(m->seq_dev, s));
   ++m->launches;
   const long long cut_logical = static_cast<long long>(b) * m->cut_elems * eb;  // one worker's cut
-  const size_t cut_bytes = static_cast<size_t>(b) * m->cut_elems * sizeof(bf16);
+  const bool pairs = pair_mode(m);
+  const size_t cut_row = static_cast<size_t>(m->cut_elems) * (pairs ? 2 : 1);  // bf16 elements per cut row
+  const size_t cut_bytes = static_cast<size_t>(b) * cut_row * sizeof(bf16);
   const int slot = ralp || m->mps ? m->widx : 0;   // this worker's row block in the PS input
   const bf16* cut_local = nullptr;
 
-  if (m->is_worker) {
+  if (m->is_worker && pairs) {
+    bf16* cut_dst = m->acts.back().ptr;
+    if (m->holds_back) cut_dst = m->x_fc + static_cast<size_t>(slot) * b * cut_row;
+    if (pair_front_forward(m, img, cut_dst, why)) return 1;
+    cut_local = cut_dst;
+  } else if (m->is_worker) {
     // backward-data filter copies from this step's masters, on the aux stream under the forward
     RALPB_TRY(cudaEventRecord(m->ev_wd_fork, s));
     RALPB_TRY(cudaStreamWaitEvent(m->aux_stream, m->ev_wd_fork, 0));
@@ -1265,7 +1594,7 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
       ++m->launches;
     }
     int32_t* lab_ps = at<int32_t>(m, m->ps_rank, m->arena_off_lab) + static_cast<size_t>(slot) * b;
-    bf16* x_ps = at<bf16>(m, m->ps_rank, m->arena_off_xfc) + static_cast<size_t>(slot) * b * m->cut_elems;
+    bf16* x_ps = at<bf16>(m, m->ps_rank, m->arena_off_xfc) + static_cast<size_t>(slot) * b * cut_row;
     PeerSignal none{};
     RALPB_TRY(push_and_signal(lab_ps, lab, static_cast<long long>(b) * 4 / 16, none, seq, m->counters + 1, s));
     PeerSignal sig{};
@@ -1281,15 +1610,19 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   } else if (m->holds_back) {
     const int R = m->rows_back;
     const bf16* in = m->x_fc;
-    if (launch_fc_forward(m, in, R, why)) return 1;
-    const FcLayer& last = m->back.back();
     const float scale = 1.f / static_cast<float>(W * b);
-    RALPB_TRY(softmax_xent(m->logits, R, last.out, last.ld_out, m->labels_all, scale, m->row_loss, m->dlogits, last.ld_out, s));
-    // this rank's rows' share of the job's mean loss (RALP: all W*b rows are here)
-    RALPB_TRY(reduce_sum(m->row_loss, R, scale, m->loss, s));
-    m->launches += 2;
+    if (pairs) {
+      if (pair_fc_forward_loss(m, R, scale, why)) return 1;
+    } else {
+      if (launch_fc_forward(m, in, R, why)) return 1;
+      const FcLayer& last = m->back.back();
+      RALPB_TRY(softmax_xent(m->logits, R, last.out, last.ld_out, m->labels_all, scale, m->row_loss, m->dlogits, last.ld_out, s));
+      // this rank's rows' share of the job's mean loss (RALP: all W*b rows are here)
+      RALPB_TRY(reduce_sum(m->row_loss, R, scale, m->loss, s));
+      m->launches += 2;
+    }
     if (!ralp && push_loss_share(m, why)) return 1;
-    if (launch_fc_backward_data(m, in, R, m->dx_fc, why)) return 1;
+    if (pairs ? pair_fc_backward_data(m, R, m->dx_fc, why) : launch_fc_backward_data(m, in, R, m->dx_fc, why)) return 1;
     if (ralp) {
       // return every remote worker's rows of the cut gradient first, then the FC tail's
       // weight gradients and its (PS-local, never synchronised) update run on the aux
@@ -1304,7 +1637,7 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
           PeerSignal sig{};
           sig.n = 1;
           sig.flag[0] = at<uint32_t>(m, r, m->arena_off_flags) + kFlagActGrad;
-          RALPB_TRY(push_and_signal(at<bf16>(m, r, m->arena_off_dcut), m->dx_fc + static_cast<size_t>(w) * b * m->cut_elems,
+          RALPB_TRY(push_and_signal(at<bf16>(m, r, m->arena_off_dcut), m->dx_fc + static_cast<size_t>(w) * b * cut_row,
                                     static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + kCtrScatter + w, s));
           ++m->launches;
           m->nvl_out += cut_bytes;
@@ -1316,7 +1649,7 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
           const int r = m->worker_ranks[w];
           if (r == m->rank) continue;
           sc.dst[sc.n] = at<bf16>(m, r, m->arena_off_dcut);
-          sc.src[sc.n] = m->dx_fc + static_cast<size_t>(w) * b * m->cut_elems;
+          sc.src[sc.n] = m->dx_fc + static_cast<size_t>(w) * b * cut_row;
           ++sc.n;
           sig.flag[sig.n++] = at<uint32_t>(m, r, m->arena_off_flags) + kFlagActGrad;
           m->nvl_out += cut_bytes;
@@ -1328,17 +1661,22 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
       // conv kernels), the HBM-bound update on the aux stream, overlapping the front backward
       // (RALPB_FC_OVERLAP=0: everything in order on one stream)
       const char* ov = getenv("RALPB_FC_OVERLAP");
-      const bool overlap = !(ov != nullptr && ov[0] == '0') && m->is_worker;
+      const bool overlap = !(ov != nullptr && ov[0] == '0') && m->is_worker && !pairs;
       cudaStream_t su = overlap ? m->aux_stream : s;
-      if (launch_fc_backward_weights(m, in, R, true, lr, mu, s, su, why)) return 1;
+      if (pairs) {
+        if (pair_fc_backward_weights(m, R, true, lr, mu, why)) return 1;
+      } else if (launch_fc_backward_weights(m, in, R, true, lr, mu, s, su, why)) {
+        return 1;
+      }
       if (overlap) {
         RALPB_TRY(cudaEventRecord(m->ev_join, m->aux_stream));
         fc_forked = true;
       }
     } else {
-      if (launch_fc_backward_weights(m, in, R, false, lr, mu, s, s, why)) return 1;
+      if (pairs ? pair_fc_backward_weights(m, R, false, lr, mu, why) : launch_fc_backward_weights(m, in, R, false, lr, mu, s, s, why))
+        return 1;
     }
-    if (m->is_worker) dcut = m->dx_fc + static_cast<size_t>(slot) * b * m->cut_elems;
+    if (m->is_worker) dcut = m->dx_fc + static_cast<size_t>(slot) * b * cut_row;
   } else {
     RALPB_TRY(wait_flags(m->flags + kFlagActGrad, 1, seq, s));
     ++m->launches;
@@ -1358,9 +1696,9 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   }
 
   // ---------------- worker front backward
-  RALPB_TRY(cudaStreamWaitEvent(s, m->ev_wd_join, 0));
+  if (!pairs) RALPB_TRY(cudaStreamWaitEvent(s, m->ev_wd_join, 0));
   RALPB_TRY(cudaMemsetAsync(m->G, 0, m->n_front * sizeof(float), s));
-  if (launch_front_backward(m, dcut, why)) return 1;
+  if (pairs ? pair_front_backward(m, dcut, why) : launch_front_backward(m, dcut, why)) return 1;
   RALPB_TRY(mark(m, 3, capturing));
 
   // ---------------- parameter synchronisation + re-layout
@@ -1375,7 +1713,7 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   }
   const bool placed = ralp || m->mps;
   if (sync_params(m, placed ? m->n_front : m->n_total, lr, mu, why)) return 1;
-  if (relayout_weights(m, !placed, why)) return 1;
+  if (pairs ? pair_relayout(m, true, !placed, s, why) : relayout_weights(m, !placed, why)) return 1;
   if (!ralp && !m->mps && combine_loss(m, why)) return 1;
   return 0;
 }

@@ -42,7 +42,8 @@ struct FcLayer {
   int in = 0, out = 0, relu = 1;
   int ld_out = 0;                  // padded row stride (elements) of this layer's output
   long long w_off = 0, b_off = 0;
-  bf16* wbf = nullptr;             // [lout][lin]
+  bf16* wbf = nullptr;             // [lout][lin] (pair precision: the forward pair operand)
+  bf16* wbd = nullptr;             // pair precision: the backward-data pair operand
   int lout = 0, lin = 0;           // this rank's weight block: [out][in], or a slice (RALP_MPS:
                                    // layer 0 rows [r*s0, (r+1)*s0), layer 1 columns of that range)
 };
@@ -115,6 +116,11 @@ struct Model {
   // peers (IPC-mapped base pointers of every rank's arena; self = arena)
   std::vector<char*> peer_base;
   bool peers_open = false;
+
+  // pair precision (RALPB_PRECISION_FP32, pair.cuh): fp32 scratch of the contractions
+  float* pair_acc = nullptr;
+  float* pair_s = nullptr;
+  size_t pair_acc_floats = 0, pair_s_floats = 0;
 
   // RALP_MPS (FC tail sharded over the ranks)
   bool mps = false;
