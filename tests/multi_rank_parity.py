@@ -208,16 +208,14 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
 def main():
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
-    # RALPB_SHARED_GPU=1: every rank on GPU 0 (the peer arenas are then CUDA-IPC mappings of the
-    # same device, the exchange kernels run unchanged), gloo for the host-side collectives --
-    # multi-rank coverage on a 1-GPU box; the small configurations only
-    shared = os.environ.get("RALPB_SHARED_GPU") == "1"
-    dev = 0 if shared else int(os.environ["LOCAL_RANK"])
+    # one rank per GPU only: ranks whose kernels wait on one another must never share a GPU
+    # (separate processes on one B200 raised Xid 109, B200_PROFILING.md)
+    dev = int(os.environ["LOCAL_RANK"])
+    if dev >= torch.cuda.device_count():
+        raise SystemExit("multi_rank_parity needs one GPU per rank")
     torch.cuda.set_device(dev)
-    if shared:
-        dist.init_process_group("gloo")
-    else:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    shared = False
     ok = True
     cifar = catalog_lookup("cifar_small").with_batch_size(32)
     vgg16 = catalog_lookup("vgg16").with_batch_size(4)

@@ -29,15 +29,6 @@ def _parity(n: int, port: int, env_extra: dict) -> None:
     assert r.returncode == 0 and "MULTI-RANK PARITY PASS" in r.stdout
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() != 1, reason="1-GPU box only")
-def test_two_ranks_sharing_one_gpu():
-    """Two (and three) processes on ONE B200: the same exchange kernels over CUDA-IPC mappings of the
-    same device, so the multi-rank paths (cut gather, fused act-grad scatter, sharded-PS sync,
-    RALP-N's dedicated PS, the loss combine, the sharded FC tail) are exercised on a 1-GPU box."""
-    _parity(2, 29614, {"RALPB_SHARED_GPU": "1"})
-    _parity(3, 29615, {"RALPB_SHARED_GPU": "1", "RALPB_PARITY_ONLY": "dedicated-ps"})
-
-
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
 def test_two_rank_parity_per_peer_pushes():
     """The per-peer push kernels (RALPB_SCATTER_FUSED=0, RALPB_PUSH_LEGACY=1) give the same result."""
