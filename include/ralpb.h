@@ -240,13 +240,16 @@ int ralpb_model_apply(ralpb_model* m, float lr, float mu);
 int ralpb_model_set_profiling(ralpb_model* m, int on);
 /* Per-launch records of the last profiled step: kind = 0 conv fwd/dgrad (single CTA), 1 conv
  * fwd/dgrad (CTA pair), 2 conv wgrad (CTA pair), 3 conv wgrad (single CTA), 4 first-conv fwd,
- * 5 first-conv wgrad, 6 GEMM, 7 peer push (cut gather / act-grad scatter), 8 sharded-PS update;
- * ms = CUDA-event duration; flops = algorithmic FLOPs (7, 8: bytes moved over NVLink).  Returns the
- * number of records (writes at most cap) or -1. */
+ * 5 first-conv wgrad, 6 GEMM, 7 peer push (cut gather / act-grad scatter), 8 sharded-PS update,
+ * 9 max-pool backward, 10 SGD-momentum; ms = CUDA-event duration on the launching stream;
+ * flops = algorithmic FLOPs (7, 8: bytes moved over NVLink per direction); bytes = algorithmic
+ * DRAM bytes (7, 8: NVLink bytes per direction).  Returns the number of records (writes at most
+ * cap) or -1. */
 typedef struct {
   int kind;
   float ms;
   double flops;
+  double bytes;        /* algorithmic DRAM bytes (push / shard update: NVLink bytes per direction) */
 } ralpb_launch_rec;
 int ralpb_model_timed_launches(ralpb_model* m, ralpb_launch_rec* out, int cap);
 

@@ -73,11 +73,11 @@ class LayerDesc(C.Structure):
 
 class LaunchRec(C.Structure):
     """ralpb_launch_rec (include/ralpb.h)."""
-    _fields_ = [("kind", C.c_int), ("ms", C.c_float), ("flops", C.c_double)]
+    _fields_ = [("kind", C.c_int), ("ms", C.c_float), ("flops", C.c_double), ("bytes", C.c_double)]
 
 
 LAUNCH_KINDS = ["conv_fwd", "conv_fwd_pair", "conv_wgrad_pair", "conv_wgrad", "first_conv_fwd", "first_conv_wgrad",
-                "gemm", "push", "shard_update"]
+                "gemm", "push", "shard_update", "maxpool_bwd", "sgd"]
 TENSOR_KINDS = LAUNCH_KINDS[:7]
 
 

@@ -80,6 +80,8 @@ cudaError_t conv_first_wgrad(const float* img, int n, int h, int w, int cin, con
 
 // Slab-tiled kernels (conv_slab.cu).  `c` = contracted channels, `cout` = produced channels.
 bool slab_fwd_ok(const ConvGeom& g, int c, int cout);
+double slab_fwd_bytes(const ConvGeom& g, int c, int cout, bool mask, bool pool, bool idx);
+double wgrad_bytes(const ConvGeom& g);
 bool slab_wgrad_ok(const ConvGeom& g);
 // Row-streamed 64 -> 64 channel 3x3 kernel (conv_row.cu), used by conv_slab_fwd when it applies
 // (RALPB_ROW64=0 disables).

@@ -352,7 +352,7 @@ cudaError_t conv_first_fwd(const float* img, int n, int h, int w, int cin, const
   const int grid = std::min(p.total, num_sms());
   cudaFuncSetAttribute(conv_first_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   launch_timed([&] { static_cast<void>(launch_pdl(conv_first_fwd_kernel, dim3(grid), dim3(32 * kFwdWarps), smem, s, 1, p)); }, s, KIND_FIRST_FWD,
-               2.0 * n * h * w * 27.0 * 64.0);
+               2.0 * n * h * w * 27.0 * 64.0, static_cast<double>(n) * h * w * (cin * 4.0 + 64 * 2.0));
   return cudaGetLastError();
 }
 
@@ -365,7 +365,7 @@ cudaError_t conv_first_wgrad(const float* img, int n, int h, int w, int cin, con
   const int grid = std::min(p.total, num_sms());
   cudaFuncSetAttribute(conv_first_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   launch_timed([&] { static_cast<void>(launch_pdl(conv_first_wgrad_kernel, dim3(grid), dim3(32 * (kProd + 2)), smem, s, 1, p)); }, s, KIND_FIRST_WGRAD,
-               2.0 * n * h * w * 27.0 * 64.0);
+               2.0 * n * h * w * 27.0 * 64.0, static_cast<double>(n) * h * w * (cin * 4.0 + 64 * 2.0));
   return cudaGetLastError();
 }
 

@@ -461,14 +461,14 @@ cudaError_t conv_row64_fwd(const ConvGeom& g, const void* x_pad, const void* w, 
     static_cast<void>(cudaFuncSetAttribute(conv_row64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     launch_timed([&] {
       static_cast<void>(launch_pdl(conv_row64_kernel<true>, dim3(grid), dim3(kRowThreads), smem, s, 2, p));
-    }, s, KIND_CONV_FWD_PAIR, flops);
+    }, s, KIND_CONV_FWD_PAIR, flops, slab_fwd_bytes(g, 64, 64, mask_pad != nullptr, pool_out != nullptr, false));
   } else {
     const int smem = 1024 + 9 * kTapBytes + 5 * kRowStage + 2 * 2 * 8192 + 1024;
     const int grid = std::min(p.total, sms);
     static_cast<void>(cudaFuncSetAttribute(conv_row64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     launch_timed([&] {
       static_cast<void>(launch_pdl(conv_row64_kernel<false>, dim3(grid), dim3(kRowThreads), smem, s, 1, p));
-    }, s, KIND_CONV_FWD, flops);
+    }, s, KIND_CONV_FWD, flops, slab_fwd_bytes(g, 64, 64, mask_pad != nullptr, pool_out != nullptr, false));
   }
   return cudaGetLastError();
 }

@@ -94,6 +94,21 @@ bool slab_wgrad_ok(const ConvGeom& g) {
          g.q() < (1LL << 31);
 }
 
+// Algorithmic DRAM bytes of one launch (each operand once): input interior, filters, output
+// interior (+ the ReLU mask it reads, the fused pool's output / argmax bytes).
+double slab_fwd_bytes(const ConvGeom& g, int c, int cout, bool mask, bool pool, bool idx) {
+  const double px = static_cast<double>(g.n) * g.h * g.w;
+  double b = px * c * 2.0 + static_cast<double>(g.taps()) * c * cout * 2.0 + px * cout * 2.0;
+  if (mask) b += px * cout * 2.0;
+  if (pool) b += px / 4.0 * cout * 2.0;
+  if (idx) b += px / 4.0 * cout;
+  return b;
+}
+double wgrad_bytes(const ConvGeom& g) {
+  const double px = static_cast<double>(g.n) * g.h * g.w;
+  return px * (g.cin + g.cout) * 2.0 + static_cast<double>(g.taps()) * g.cin * g.cout * 4.0;
+}
+
 cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, int c, int cout, const float* bias,
                           int relu, const void* mask_pad, void* y_pad, float* colsum, cudaStream_t s,
                           std::string* why, void* pool_out, int pool_pad, void* pool_idx) {
@@ -198,7 +213,8 @@ cudaError_t conv_slab_fwd(const ConvGeom& g, const void* x_pad, const void* w, i
     static_cast<void>(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     launch_timed([&] {
       static_cast<void>(launch_pdl(kern, dim3(grid), dim3(threads), smem, s, cluster ? 2 : 1, p));
-    }, s, cluster ? KIND_CONV_FWD_PAIR : KIND_CONV_FWD, 2.0 * g.n * g.h * g.w * static_cast<double>(g.taps()) * c * cout);
+    }, s, cluster ? KIND_CONV_FWD_PAIR : KIND_CONV_FWD, 2.0 * g.n * g.h * g.w * static_cast<double>(g.taps()) * c * cout,
+       slab_fwd_bytes(g, c, cout, mask_pad != nullptr, pool_out != nullptr, pool_idx != nullptr));
     launched = true;
   };
 #define RALPB_SLAB_CASE(KK, KS, MA)                                                                   \
@@ -265,7 +281,7 @@ cudaError_t conv_slab_wgrad(const ConvGeom& g, const void* x_pad, const void* dy
     auto go2 = [&](auto kern) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       launch_timed([&] { static_cast<void>(launch_pdl(kern, dim3(2 * clusters), dim3(256), smem2, s, 1, p)); }, s, KIND_WGRAD_PAIR,
-                   2.0 * g.n * g.h * g.w * static_cast<double>(g.taps()) * g.cin * g.cout);
+                   2.0 * g.n * g.h * g.w * static_cast<double>(g.taps()) * g.cin * g.cout, wgrad_bytes(g));
     };
     if (bh == 14) go2(conv_slab_wgrad_pair_kernel<14>); else go2(conv_slab_wgrad_pair_kernel<16>);
     cudaError_t e = cudaGetLastError();
@@ -275,7 +291,7 @@ cudaError_t conv_slab_wgrad(const ConvGeom& g, const void* x_pad, const void* dy
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     launch_timed([&] { static_cast<void>(launch_pdl(kern, dim3(grid), dim3(256), smem, s, 1, p)); }, s, KIND_WGRAD,
-                 2.0 * g.n * g.h * g.w * static_cast<double>(g.taps()) * g.cin * g.cout);
+                 2.0 * g.n * g.h * g.w * static_cast<double>(g.taps()) * g.cin * g.cout, wgrad_bytes(g));
   };
   if (g.k == 5) {
     go(bh == 14 ? conv_slab_wgrad_kernel<14, 5> : conv_slab_wgrad_kernel<16, 5>);

@@ -506,7 +506,11 @@ cudaError_t maxpool_bwd_gather(const uint8_t* idx, const __nv_bfloat16* dy, int 
   const long long work = static_cast<long long>(n) * h * w * (c / 8);
   const int grid = static_cast<int>(std::max<long long>(1, std::min((work + threads - 1) / threads,
                                                                    static_cast<long long>(num_sms()) * 16)));
-  maxpool_bwd_gather_kernel<<<grid, threads, 0, s>>>(idx, dy, n, h, w, c, pad_in, k, st, pad_out, oh, ow, dx, colsum);
+  // idx + dy read, dx written (interior)
+  const double bytes = static_cast<double>(n) * c * (static_cast<double>(oh) * ow * 3.0 + static_cast<double>(h) * w * 2.0);
+  launch_timed([&] {
+    maxpool_bwd_gather_kernel<<<grid, threads, 0, s>>>(idx, dy, n, h, w, c, pad_in, k, st, pad_out, oh, ow, dx, colsum);
+  }, s, KIND_POOL_BWD, 0.0, bytes);
   return cudaGetLastError();
 }
 
@@ -517,7 +521,9 @@ cudaError_t maxpool_bwd_idx(const uint8_t* idx, const __nv_bfloat16* dy, int n, 
   const long long work = static_cast<long long>(n) * oh * ow * (c / 8);
   const int grid = static_cast<int>(std::max<long long>(1, std::min((work + threads - 1) / threads,
                                                                    static_cast<long long>(num_sms()) * 16)));
-  maxpool_bwd_idx_kernel<<<grid, threads, 0, s>>>(idx, dy, n, oh, ow, c, pad_out, pad_in, dx, colsum);
+  const double bytes = static_cast<double>(n) * oh * ow * c * (1.0 + 2.0 + 4 * 2.0);   // idx, dy, 4 dx
+  launch_timed([&] { maxpool_bwd_idx_kernel<<<grid, threads, 0, s>>>(idx, dy, n, oh, ow, c, pad_out, pad_in, dx, colsum); },
+               s, KIND_POOL_BWD, 0.0, bytes);
   return cudaGetLastError();
 }
 
@@ -534,13 +540,19 @@ cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* dy, int n, 
     const long long cap = static_cast<long long>(num_sms()) * 16;
     return static_cast<int>(std::max<long long>(1, std::min((work + threads - 1) / threads, cap)));
   };
+  // x (interior) + dy read, dx (interior) written
+  const double bytes = static_cast<double>(n) * c * (static_cast<double>(h) * w * 4.0 + static_cast<double>(oh) * ow * 2.0);
   if (k == st && k == 2 && windows < (1LL << 31)) {
-    maxpool_bwd_disjoint_kernel<2><<<grid(windows), threads, 0, s>>>(x, dy, n, h, w, c, pad_in, pad_out, oh, ow, dx,
-                                                                     colsum);
+    launch_timed([&] {
+      maxpool_bwd_disjoint_kernel<2><<<grid(windows), threads, 0, s>>>(x, dy, n, h, w, c, pad_in, pad_out, oh, ow, dx,
+                                                                       colsum);
+    }, s, KIND_POOL_BWD, 0.0, bytes);
     return cudaGetLastError();
   }
   long long total = static_cast<long long>(n) * (h + 2 * pad_in) * (w + 2 * pad_in) * (c / 8);
-  maxpool_bwd_kernel<<<grid(total), threads, 0, s>>>(x, dy, n, h, w, c, pad_in, k, st, pad_out, oh, ow, dx, colsum);
+  launch_timed([&] {
+    maxpool_bwd_kernel<<<grid(total), threads, 0, s>>>(x, dy, n, h, w, c, pad_in, k, st, pad_out, oh, ow, dx, colsum);
+  }, s, KIND_POOL_BWD, 0.0, bytes);
   return cudaGetLastError();
 }
 
@@ -647,7 +659,9 @@ cudaError_t sgd_momentum(float* p, float* v, const float* g, long long n, float 
 cudaError_t sgd_momentum_bf16(float* p, float* v, const float* g, long long n, float lr, float mu,
                               float gscale, __nv_bfloat16* out, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  sgd_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(p, v, g, n, lr, mu, gscale, out);
+  // p, v, g read; p, v (+ the bf16 copy) written
+  launch_timed([&] { sgd_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(p, v, g, n, lr, mu, gscale, out); }, s, KIND_SGD,
+               0.0, static_cast<double>(n) * (20.0 + (out != nullptr ? 2.0 : 0.0)));
   return cudaGetLastError();
 }
 

@@ -465,6 +465,7 @@ void model_destroy(Model* m) {
     for (int i = 0; i < 2 * m->timer.cap; ++i) cudaEventDestroy(m->timer.ev[i]);
     delete[] m->timer.kind;
     delete[] m->timer.flops;
+    delete[] m->timer.bytes;
     delete[] m->timer.ev;
   }
   if (m->stream) cudaStreamDestroy(m->stream);
@@ -1843,12 +1844,14 @@ int model_stats(Model* m, ralpb_step_stats* st, std::string* why) {
   cudaEventElapsedTime(&st->ms_back, m->ev[1], m->ev[2]);
   cudaEventElapsedTime(&st->ms_front_bwd, m->ev[2], m->ev[3]);
   cudaEventElapsedTime(&st->ms_sync, m->ev[3], m->ev[4]);
-  st->gemm_launches = m->profiling ? m->timer.n : 0;
+  st->gemm_launches = 0;
   st->ms_gemm = 0.f;
   for (int i = 0; m->profiling && i < m->timer.n; ++i) {
+    if (m->timer.kind[i] > KIND_GEMM) continue;   // tensor-core launches only
     float ms = 0.f;
     cudaEventElapsedTime(&ms, m->timer.ev[2 * i], m->timer.ev[2 * i + 1]);
     st->ms_gemm += ms;
+    ++st->gemm_launches;
   }
   return 0;
 }
@@ -1879,16 +1882,18 @@ int model_timed_launches(Model* m, ralpb_launch_rec* out, int cap, int* n, std::
     out[i].kind = m->timer.kind[i];
     out[i].ms = ms;
     out[i].flops = m->timer.flops[i];
+    out[i].bytes = m->timer.bytes[i];
   }
   return 0;
 }
 
 int model_set_profiling(Model* m, int on, std::string* why) {
   if (on && m->timer.ev == nullptr) {
-    m->timer.cap = 256;
+    m->timer.cap = 512;
     m->timer.ev = new cudaEvent_t[2 * m->timer.cap];
     m->timer.kind = new int[m->timer.cap];
     m->timer.flops = new double[m->timer.cap];
+    m->timer.bytes = new double[m->timer.cap];
     for (int i = 0; i < 2 * m->timer.cap; ++i) RALPB_TRY(cudaEventCreate(&m->timer.ev[i]));
   }
   m->profiling = on != 0;

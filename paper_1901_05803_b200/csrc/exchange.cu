@@ -66,7 +66,7 @@ cudaError_t push_and_signal(void* dst, const void* src, long long n16, const Pee
   launch_timed([&] {
     push_kernel<<<grid, 512, 0, s>>>(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), n16, sig,
                                      value, counter);
-  }, s, KIND_PUSH, 16.0 * n16);
+  }, s, KIND_PUSH, 16.0 * n16, 16.0 * n16);
   return cudaGetLastError();
 }
 
@@ -119,7 +119,7 @@ cudaError_t scatter_and_signal(const PeerScatter& sc, long long n16, const PeerS
   const int gx = static_cast<int>(std::max<long long>(1, std::min<long long>((n16 + 511) / 512, want)));
   launch_timed([&] {
     scatter_kernel<<<dim3(gx, sc.n), 512, 0, s>>>(sc, n16, sig, value, counter);
-  }, s, KIND_PUSH, 16.0 * n16 * sc.n);
+  }, s, KIND_PUSH, 16.0 * n16 * sc.n, 16.0 * n16 * sc.n);
   return cudaGetLastError();
 }
 
@@ -190,7 +190,7 @@ cudaError_t shard_update(const ShardUpdate& u, const PeerSignal& done, const uin
   // per-direction figure is what compares with the per-direction link peak)
   const double peer_bytes = (u.nranks - 1) * static_cast<double>(u.end - u.begin) * sizeof(float);
   launch_timed([&] { shard_update_kernel<<<grid, 256, 0, s>>>(u, done, value, counter); }, s, KIND_SHARD_UPDATE,
-               peer_bytes);
+               peer_bytes, peer_bytes);
   return cudaGetLastError();
 }
 

@@ -189,9 +189,10 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
   }
   const long long total = static_cast<long long>(p.n_mt) * p.n_nt * p.n_ks;
   const int grid = static_cast<int>(std::min<long long>(total, sms));
+  const double esz_out = d.epi == EPI_BF16 ? 2.0 : 4.0;
   launch_timed([&] { static_cast<void>(launch_pdl(gemm_sm100_kernel, dim3(grid), dim3(kThreads), smem, stream, 1, p)); },
-               stream, KIND_GEMM,
-               2.0 * d.M * d.N * static_cast<double>(d.K));
+               stream, KIND_GEMM, 2.0 * d.M * d.N * static_cast<double>(d.K),
+               2.0 * (static_cast<double>(d.M) + d.N) * static_cast<double>(d.K) + esz_out * d.M * static_cast<double>(d.N));
   return cudaGetLastError();
 }
 

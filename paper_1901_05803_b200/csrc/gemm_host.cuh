@@ -59,7 +59,9 @@ enum LaunchKind {
   KIND_FIRST_WGRAD = 5,   // conv_first_wgrad_kernel
   KIND_GEMM = 6,          // gemm_sm100_kernel
   KIND_PUSH = 7,          // push_kernel (cut gather / act-grad scatter); "flops" = bytes moved
-  KIND_SHARD_UPDATE = 8,  // shard_update_kernel (sharded-PS RS + SGD + AG); "flops" = NVLink bytes
+  KIND_SHARD_UPDATE = 8,  // shard_update_kernel (sharded-PS RS + SGD + AG); "flops" = NVLink bytes per direction
+  KIND_POOL_BWD = 9,      // maxpool_bwd* (HBM-bound; "flops" = 0)
+  KIND_SGD = 10,          // sgd_momentum* (HBM-bound)
 };
 
 struct GemmTimer {
@@ -68,19 +70,21 @@ struct GemmTimer {
   int n = 0;
   int* kind = nullptr;        // [cap]
   double* flops = nullptr;    // [cap] algorithmic FLOPs of the launch
+  double* bytes = nullptr;    // [cap] algorithmic DRAM (or NVLink) bytes of the launch
 };
 void set_gemm_timer(GemmTimer* t);  // thread-local; nullptr disables
 GemmTimer* current_gemm_timer();
 
 // Launch `f` (a kernel launch on stream s) bracketed by the timer's events, if armed.
 template <class F>
-void launch_timed(F&& f, cudaStream_t s, int kind = KIND_GEMM, double flops = 0.0) {
+void launch_timed(F&& f, cudaStream_t s, int kind = KIND_GEMM, double flops = 0.0, double bytes = 0.0) {
   GemmTimer* tm = current_gemm_timer();
   const bool timed = tm != nullptr && tm->n < tm->cap;
   if (timed) {
     cudaEventRecord(tm->ev[2 * tm->n], s);
     tm->kind[tm->n] = kind;
     tm->flops[tm->n] = flops;
+    tm->bytes[tm->n] = bytes;
   }
   f();
   if (timed) cudaEventRecord(tm->ev[2 * tm->n++ + 1], s);

@@ -325,10 +325,11 @@ class RankExecutor:
         return out.value
 
     def timed_launches(self) -> list:
-        """[(kind name, ms, flops)] of every tensor-core launch of the last profiled step."""
+        """[(kind name, ms, flops, bytes)] of every timed launch of the last profiled step (tensor-core
+        kernels, exchange kernels, max-pool backward, SGD; include/ralpb.h ralpb_launch_rec)."""
         recs = (_lib.LaunchRec * 512)()
         n = _lib.call_count("ralpb_model_timed_launches", self._h, recs, 512)
-        return [(_lib.LAUNCH_KINDS[recs[i].kind], recs[i].ms, recs[i].flops) for i in range(min(n, 512))]
+        return [(_lib.LAUNCH_KINDS[recs[i].kind], recs[i].ms, recs[i].flops, recs[i].bytes) for i in range(min(n, 512))]
 
     def set_profiling(self, on: bool) -> None:
         _lib.call("ralpb_model_set_profiling", self._h, int(on))

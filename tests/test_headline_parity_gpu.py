@@ -77,7 +77,8 @@ def check_grad(name, got, ref, report, tol=1e-3):
 def headline():
     model = catalog_lookup("vgg16").with_batch_size(B)
     rep = profile(model)
-    assert rep.split_index == 18 and model.layer(18).name == "fc1"
+    # split index 18 (1-based): conv1..pool5 in front, fc1 onward on the PS
+    assert rep.split_index == 18 and model.layer(18).name == "pool5" and model.layer(19).name == "fc1"
     job = JobSpec(model, Strategy.ralp(rep.split_index), 1)
     ex = RankExecutor(job)
     params = synthetic.init_params(ex.layers, 0)

@@ -63,6 +63,7 @@ def run_fp32(model, strategy, steps, lr=0.01, seed=0):
     params = synthetic.init_params(ex.layers, seed)
     ex.set_params(params)
     orc = ostep.OracleState(ex.layers, params)
+    orc64 = ostep.OracleState(ex.layers, params)   # the fp32 oracle's own floor: fp64 contractions
     b = model.batch_size
     bad = []
     for t in range(steps):
@@ -70,21 +71,25 @@ def run_fp32(model, strategy, steps, lr=0.01, seed=0):
         ex.step(imgs, labs, lr=lr, momentum=0.9)
         st = ex.stats()
         lo, wire = ostep.train_step(orc, strategy, 1, [(imgs, labs)], lr=lr, mu=0.9, emulate_bf16=False)
+        l64, _ = ostep.train_step(orc64, strategy, 1, [(imgs, labs)], lr=lr, mu=0.9, emulate_bf16=False, accum64=True)
         assert st.logical_bytes == wire == expect
         rel = abs(st.loss - lo) / abs(lo)
-        print(f"  step {t}: loss gpu {st.loss:.7f} oracle {lo:.7f} rel {rel:.2e}")
+        print(f"  step {t}: loss gpu {st.loss:.7f} oracle {lo:.7f} rel {rel:.2e}   (oracle fp32 vs fp64: "
+              f"{abs(l64 - lo) / abs(lo):.2e})")
         if not rel <= LOSS_RTOL:
             bad.append(f"step {t}: loss rel {rel:.2e}")
     got = ex.get_params()
     ex.close()
-    for li, (g, w, p0) in enumerate(zip(got, orc.numpy_params(), params)):
+    for li, (g, w, w64, p0) in enumerate(zip(got, orc.numpy_params(), orc64.numpy_params(), params)):
         if g is None:
             continue
-        for nm, a, o, c in zip("wb", g, w, p0):
+        for nm, a, o, o64, c in zip("wb", g, w, w64, p0):
             rel = np.linalg.norm(a - o) / np.linalg.norm(o)
             upd = np.linalg.norm(o - c)
             urel = np.linalg.norm(a - o) / upd if upd > 0 else 0.0
-            print(f"  layer {li}.{nm}: ||dp||/||p|| {rel:.2e}  ||dp||/||update|| {urel:.2e}")
+            floor = np.linalg.norm(o64 - o) / upd if upd > 0 else 0.0
+            print(f"  layer {li}.{nm}: ||dp||/||p|| {rel:.2e}  ||dp||/||update|| {urel:.2e}  "
+                  f"(oracle fp32 vs fp64 ||dp||/||update|| {floor:.2e})")
             if not rel <= PARAM_RTOL and np.linalg.norm(o) > 0:
                 bad.append(f"layer {li}.{nm}: ||dp||/||p|| {rel:.2e}")
             if nm == "w" and not urel <= UPDATE_RTOL:
