@@ -122,8 +122,19 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def _cpu_baseline_step(sample_b: int, steps: int, warmup: int = 1):
-    """Oracle port (oracle/step.py) of the layer-placed step on the host cores, bounded sample."""
+    """Oracle port (oracle/step.py, plain fp32 torch on the host cores) of the layer-placed step,
+    W=1 at per-worker batch sample_b: a bounded sample of the workload."""
     import torch
     from oracle import step as ostep
     from paper_1901_05803_b200 import synthetic
@@ -143,6 +154,7 @@ def _cpu_baseline_step(sample_b: int, steps: int, warmup: int = 1):
         ostep.train_step(st, "ralp", 1, [batches[warmup + t]])
     dt = time.perf_counter() - t0
     return {"value": sample_b * steps / dt, "unit": "images/s", "cores": torch.get_num_threads(), "kind": "port",
+            "cpu_model": _cpu_model(), "logical_cpus": os.cpu_count(),
             "sample": f"{MODEL} {shape[0]}x{shape[1]} layer-placed step (oracle/step.py, fp32 torch CPU), W=1, b={sample_b}, "
                       f"{steps} timed steps after {warmup} warm-up, {dt:.1f} s"}
 
@@ -152,38 +164,51 @@ def _headline_split():
     return profile(catalog_lookup(MODEL).with_batch_size(BATCH)).split_index
 
 
+REF_MAX_STEPS = 3   # one b=128 VGG-16 step of the CPU port takes ~10 s on 16 host cores
+
+
 def run_reference(args):
+    """The reference arm: the reference's CPU path for this step (the oracle port -- the reference
+    itself only simulates the step) on the box's host cores, on OUR arm's workload: VGG-16 224x224,
+    b=128 per worker, the partitioner's split, fp32.  Each timed step is one full b=128 step; the
+    run is capped at REF_MAX_STEPS timed steps (+1 warm-up) so it ends within a few minutes."""
     world, rank, _ = _dist()
     if rank != 0:
         return
-    sample_b = 8
-    steps = args.steps  # each step is a b=8 sample of the workload (~0.6 s on 16 host cores)
-    cb = _cpu_baseline_step(sample_b, steps, args.warmup)
+    steps = max(1, min(args.steps, REF_MAX_STEPS))
+    cb = _cpu_baseline_step(BATCH, steps, 1)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"],
-            "unit": "images/s", "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * sample_b / cb["value"], "higher_is_better": True, "scaling": "weak",
+            "unit": "images/s", "n_gpus": args.gpus, "steps": steps, "warmup": 1,
+            "ms_per_step": 1e3 * BATCH / cb["value"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{MODEL} synthetic, layer-placed (RALP) step, CPU oracle port",
-                       "model": MODEL, "per_worker_batch": sample_b, "split": _headline_split()},
+            "config": {"workload": f"{MODEL} 224x224 synthetic, b={BATCH}/worker, W=1, partitioner split "
+                                   f"{_headline_split()} (pool5), layer-placed (RALP) step, CPU oracle port",
+                       "model": MODEL, "per_worker_batch": BATCH, "split": _headline_split(),
+                       "same_config": True, "steps_requested": args.steps,
+                       "note": f"timed steps capped at {REF_MAX_STEPS} (each ~10 s of host CPU); N>1: rank 0 "
+                               "runs the W=1 step (the CPU path does not shard)"},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def _build_executor(strategy: str, world: int, rank: int, ring_backend: str = "native", fc_sharding: str = "single"):
+def _build_executor(strategy: str, world: int, rank: int, ring_backend: str = "native", fc_sharding: str = "single",
+                    precision: str = "bf16", placement: str = "colocated"):
     from paper_1901_05803_b200 import synthetic
     from paper_1901_05803_b200.executor import RankExecutor
     from paper_1901_05803_b200.planner import JobSpec, Strategy, catalog_lookup, profile
 
     m = catalog_lookup(MODEL).with_batch_size(BATCH)
     rep = profile(m)
+    workers = world - 1 if placement == "dedicated-ps" else world
     if strategy == "ralp":
-        job = JobSpec(m, Strategy.ralp(rep.split_index), world)
+        job = JobSpec(m, Strategy.ralp(rep.split_index), workers)
     elif strategy == "ring":
         job = JobSpec(m, Strategy.ring(), world, ps_count=0)
     else:
         job = JobSpec(m, Strategy.baseline(), world)
-    ex = RankExecutor(job, rank=rank, world=world, ring_backend=ring_backend, fc_sharding=fc_sharding)
+    ex = RankExecutor(job, rank=rank, world=world, ring_backend=ring_backend, fc_sharding=fc_sharding,
+                      precision=precision, placement=placement)
     ex.set_params(synthetic.init_params(ex.layers, 0))
     return ex, job, rep
 
@@ -280,13 +305,14 @@ def run_ours(args):
     worker_flops, ps_flops = compute_load(m, rep.split_index, world)
     flops_rank = worker_flops + (ps_flops if rank == 0 else 0)
     peaks, peak_src = _peaks()
-    by_kind, xchg = {}, {}
-    for kind, lms, lfl in launches:
-        dst = by_kind if kind in TENSOR_KINDS else xchg
-        k = dst.setdefault(kind, {"launches": 0, "ms": 0.0, "flops": 0.0})
+    by_kind, xchg, hbm = {}, {}, {}
+    for kind, lms, lfl, lby in launches:
+        dst = by_kind if kind in TENSOR_KINDS else (xchg if kind in ("push", "shard_update") else hbm)
+        k = dst.setdefault(kind, {"launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0})
         k["launches"] += 1
         k["ms"] += lms
         k["flops"] += lfl
+        k["bytes"] += lby
     traffic_doc = {}
     tfile = ROOT / "profiles" / f"traffic_{MODEL}.json"
     if tfile.exists():
@@ -299,9 +325,10 @@ def run_ours(args):
         link = peaks.get("nvlink_gbs_per_direction", 770.0)
         nvlink = {"peak_gbs": link, "peak_source": "B200_PROFILING.md measured peer copy per direction"}
         for kind, k in xchg.items():
-            gbs = k["flops"] / (k["ms"] * 1e-3) / 1e9 if k["ms"] > 0 else None
-            nvlink[kind] = {"launches": k["launches"], "ms": k["ms"], "bytes": k["flops"], "gbs": gbs,
-                            "frac": gbs / link if gbs else None}
+            # bytes per direction (push: all outbound; shard update: the same number in and out)
+            gbs = k["bytes"] / (k["ms"] * 1e-3) / 1e9 if k["ms"] > 0 else None
+            nvlink[kind] = {"launches": k["launches"], "ms": k["ms"], "bytes_per_direction": k["bytes"],
+                            "gbs_per_direction": gbs, "frac": gbs / link if gbs else None}
         p_front = m.cumulative_param_bytes(rep.split_index) // m.bytes_per_element
         buf = torch.zeros(p_front, dtype=torch.float32, device="cuda")
         for _ in range(3):
@@ -323,6 +350,16 @@ def run_ours(args):
     for kind, k in by_kind.items():
         k["tflops"] = k["flops"] / (k["ms"] * 1e-3) / 1e12 if k["ms"] > 0 else None
         k["frac"] = k["tflops"] / peaks["bf16_tflops_sustained"] if k["tflops"] else None
+        k["gbs"] = k["bytes"] / (k["ms"] * 1e-3) / 1e9 if k["ms"] > 0 else None
+        k["hbm_frac"] = k["gbs"] / peaks["hbm_gbs"] if k["gbs"] else None
+    # kernels whose bound is HBM: the first conv (K = 27: pure data movement), the FC GEMMs at
+    # M = W*b rows (weight-streaming), the max-pool backward, SGD
+    for kind, k in hbm.items():
+        k["gbs"] = k["bytes"] / (k["ms"] * 1e-3) / 1e9 if k["ms"] > 0 else None
+        k["hbm_frac"] = k["gbs"] / peaks["hbm_gbs"] if k["gbs"] else None
+    hbm_view = {kk: {"launches": v["launches"], "ms": round(v["ms"], 4), "gbs": round(v["gbs"], 1) if v["gbs"] else None,
+                     "frac": round(v["hbm_frac"], 3) if v["hbm_frac"] else None}
+                for kk, v in list(hbm.items()) + [(kk, by_kind[kk]) for kk in ("first_conv_fwd", "gemm") if kk in by_kind]}
     dominant = max(by_kind, key=lambda kk: by_kind[kk]["ms"]) if by_kind else None
     dom = by_kind.get(dominant, {})
     dom_traffic = traffic_doc.get("per_kind", {}).get(dominant, {}).get("dram_bytes_per_launch")
@@ -361,9 +398,38 @@ def run_ours(args):
                "logical_bytes_per_step": _job_bytes(stm, world),
                "note": "FC-0 column-parallel / FC-1 row-parallel over all GPUs (volume_ralp_multi_ps)"}
 
+    # the parity precision (fp32-accurate (hi, lo) pairs through the same tcgen05 GEMM engine): a
+    # same-precision number beside the fp32 CPU arm
+    fp32 = None
+    if not args.no_fp32:
+        torch.cuda.empty_cache()
+        exf, _, _ = _build_executor("ralp", world, rank, precision="fp32")
+        ms_f = _time_steps(exf, dimgs, dlabs, max(3, args.steps // 4), 3, world)
+        stf = exf.stats()
+        exf.close()
+        fp32 = {"value": world * BATCH / (ms_f * 1e-3), "ms_per_step": ms_f, "dtype": "f32 (bf16 hi/lo pairs)",
+                "logical_bytes_per_step": _job_bytes(stf, world),
+                "note": "RALPB_PRECISION_FP32: every activation / gradient an fp32-accurate bf16 pair, every "
+                        "contraction on the tcgen05 GEMM engine over the pairs (4 products, fp32 accumulation); "
+                        "tests/test_parity_fp32_gpu.py pins it to the plain fp32 oracle"}
+    # RALP-N (costmodel.py:244-245): N-1 workers + a dedicated PS GPU (rank 0)
+    ralp_n = None
+    if world > 1:
+        torch.cuda.empty_cache()
+        exn, jobn, _ = _build_executor("ralp", world, rank, placement="dedicated-ps")
+        if exn.is_worker:
+            ms_n = _time_steps(exn, dimgs, dlabs, args.steps, args.warmup, world)
+        else:
+            ms_n = _time_steps(exn, [None], [None], args.steps, args.warmup, world)
+        stn = exn.stats()
+        exn.close()
+        ralp_n = {"value": (world - 1) * BATCH / (ms_n * 1e-3), "ms_per_step": ms_n, "workers": world - 1,
+                  "logical_bytes_per_step": _job_bytes(stn, world),
+                  "note": "ralp-n placement: rank 0 runs only the FC tail, ranks 1..N-1 are workers"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = _cpu_baseline_step(8, 10)
+        cpu = _cpu_baseline_step(BATCH, 1, 1)
 
     if rank == 0:
         line = {
@@ -384,6 +450,8 @@ def run_ours(args):
                           "logical_sync_bytes_per_step": _job_bytes(stb, world)},
             "ring_allreduce": ring,
             "ralp_fc_sharded": mps,
+            "ralp_dedicated_ps": ralp_n,
+            "precision_fp32": fp32,
             "breakdown_ms_rank0": {"front_fwd": st.ms_front_fwd, "back": st.ms_back, "front_bwd": st.ms_front_bwd,
                                    "sync": st.ms_sync, "tensor_kernels_sum": prof.ms_gemm,
                                    "tensor_launches": prof.gemm_launches},
@@ -400,6 +468,11 @@ def run_ours(args):
                                           "tflops": round(v["tflops"], 1) if v["tflops"] else None,
                                           "frac": round(v["frac"], 3) if v["frac"] else None}
                                      for kk, v in sorted(by_kind.items(), key=lambda kv: -kv[1]["ms"])},
+                         "hbm_bound": {"peak_gbs": peaks["hbm_gbs"], "peak_source": f"{peak_src} hbm_gbs",
+                                       "note": "algorithmic bytes per launch (each operand once) / CUDA-event time; "
+                                               "the first conv (K=27), the FC GEMMs at M=W*b rows, max-pool "
+                                               "backward and SGD are HBM-bound",
+                                       "by_kind": hbm_view},
                          "nvlink": nvlink,
                          "step": {"achieved": step_achieved,
                                   "frac": step_achieved / peaks["bf16_tflops_sustained"] if step_achieved else None,
@@ -426,6 +499,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the parity-precision comparator")
     ap.add_argument("--model", default=MODEL, help="catalog model (BASELINE configs: vgg16 headline, alexnet)")
     ap.add_argument("--batch", type=int, default=BATCH, help="per-worker batch")
     args = ap.parse_args()

@@ -158,7 +158,7 @@ extern "C" long long ralpb_model_debug_buffer(ralpb_model* m, int i, int which, 
       return -1;
   }
   if (src == nullptr) return -1;
-  if (mm->precision == RALPB_PRECISION_FP32 && esz == sizeof(bf16)) esz *= 2;  // (hi, lo) bf16 pairs
+  if (mm->precision == RALPB_PRECISION_FP32 && esz == sizeof(bf16)) esz *= mm->pieces;  // bf16 pieces
   if (host_out != nullptr) {
     if (cudaStreamSynchronize(mm->stream) != cudaSuccess) return -1;
     if (cudaMemcpy(host_out, src, n * esz, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;

@@ -286,7 +286,12 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   m->arena_off_flags = take(kNumFlags * sizeof(uint32_t));
   m->arena_off_P = take(m->n_total * sizeof(float));
   m->arena_off_G = take(m->n_total * sizeof(float));
-  const int pm = precision == RALPB_PRECISION_FP32 ? 2 : 1;  // (hi, lo) pairs: twice the bf16 elements
+  // parity precision: P bf16 pieces per value (pair.cuh; RALPB_PIECES=2 for the coarser split)
+  if (precision == RALPB_PRECISION_FP32) {
+    const char* pe = getenv("RALPB_PIECES");
+    m->pieces = pe != nullptr && atoi(pe) == 2 ? 2 : 3;
+  }
+  const int pm = precision == RALPB_PRECISION_FP32 ? m->pieces : 1;  // bf16 elements per value
   m->arena_off_xfc = take(static_cast<size_t>(m->rows_back) * m->cut_elems * sizeof(bf16) * pm);
   m->arena_off_lab = take(static_cast<size_t>(m->rows_back) * sizeof(int32_t));
   m->arena_off_dcut = take(static_cast<size_t>(batch) * m->cut_elems * sizeof(bf16) * pm);
@@ -370,13 +375,13 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   }
   for (size_t j = 0; j < m->back.size(); ++j) {
     auto& f = m->back[j];
-    if (pm == 2) {  // pair operands [2*ld_out][2*in] for the forward and the backward-data GEMMs
-      const size_t n4 = static_cast<size_t>(4) * f.ld_out * f.lin;
+    if (pm > 1) {  // piece operands [P*ld_out][P*in] for the forward and the backward-data GEMMs
+      const size_t n4 = static_cast<size_t>(pm) * pm * f.ld_out * f.lin;
       if (!(f.wbf = alloc<bf16>(m, n4, why)) || !(f.wbd = alloc<bf16>(m, n4, why))) return fail(*why);
       cudaMemset(f.wbf, 0, n4 * sizeof(bf16));
       cudaMemset(f.wbd, 0, n4 * sizeof(bf16));
       m->pair_s_floats = std::max(m->pair_s_floats, n4);
-      m->pair_acc_floats = std::max(m->pair_acc_floats, static_cast<size_t>(2) * R * std::max(f.ld_out, f.lin));
+      m->pair_acc_floats = std::max(m->pair_acc_floats, static_cast<size_t>(pm) * R * std::max(f.ld_out, f.lin));
     } else if (!(f.wbf = alloc<bf16>(m, static_cast<size_t>(f.lout) * f.lin, why))) {
       return fail(*why);
     }
@@ -398,15 +403,15 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     m->dyb.push_back(d);
   }
   if (!(m->dx_fc = alloc<bf16>(m, static_cast<size_t>(R) * m->cut_elems * pm, why))) return fail(*why);
-  if (pm == 2) {
-    // scratch of the pair contractions: the fp32 [rows][2N] outputs before their finishing pass
-    // and the [2M][T][2C] weight-gradient blocks
+  if (pm > 1) {
+    // scratch of the piece contractions: the fp32 [rows][P*N] outputs before their finishing pass
+    // and the [P*M][T][P*C] weight-gradient blocks
     for (size_t i = 0; i < m->front.size(); ++i) {
       const FrontLayer& f = m->front[i];
       if (f.kind != RALPB_CONV) continue;
       const ActBuf& in = m->acts[i];
-      m->pair_acc_floats = std::max(m->pair_acc_floats, static_cast<size_t>(in.rows()) * 2 * std::max(f.g.cout, f.g.cin));
-      m->pair_s_floats = std::max(m->pair_s_floats, static_cast<size_t>(4) * static_cast<size_t>(f.w_count));
+      m->pair_acc_floats = std::max(m->pair_acc_floats, static_cast<size_t>(in.rows()) * pm * std::max(f.g.cout, f.g.cin));
+      m->pair_s_floats = std::max(m->pair_s_floats, static_cast<size_t>(pm) * pm * static_cast<size_t>(f.w_count));
     }
     if (!(m->pair_acc = alloc<float>(m, m->pair_acc_floats, why))) return fail(*why);
     if (!(m->pair_s = alloc<float>(m, m->pair_s_floats, why))) return fail(*why);
@@ -425,6 +430,9 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   if (cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
   if (cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
   if (cudaStreamCreateWithFlags(&m->aux_stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
+  if (cudaStreamCreateWithFlags(&m->comm_stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
+  cudaEventCreateWithFlags(&m->ev_comm_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&m->ev_comm_join, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&m->ev_wd_fork, cudaEventDisableTiming);
@@ -451,6 +459,9 @@ void model_destroy(Model* m) {
   if (m->loss_host) cudaFreeHost(m->loss_host);
   if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
   if (m->aux_stream) cudaStreamDestroy(m->aux_stream);
+  if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
+  if (m->ev_comm_fork) cudaEventDestroy(m->ev_comm_fork);
+  if (m->ev_comm_join) cudaEventDestroy(m->ev_comm_join);
   if (m->ev_fork) cudaEventDestroy(m->ev_fork);
   if (m->ev_join) cudaEventDestroy(m->ev_join);
   if (m->ev_wd_fork) cudaEventDestroy(m->ev_wd_fork);
@@ -1152,6 +1163,9 @@ cudaError_t mark(Model* m, int i, bool capturing) {
 
 bool pair_mode(const Model* m) { return m->precision == RALPB_PRECISION_FP32; }
 
+// K-block (elements) of a K-major piece operand: the largest of 64 / 32 / 16 dividing its width.
+int kb_for(long long k) { return k % 64 == 0 ? 64 : (k % 32 == 0 ? 32 : 16); }
+
 // FC layer j's input as (groups, channels): the cut (HWC pixels x channels) or a hidden row.
 void fc_in_geom(const Model* m, int j, int* groups, int* c) {
   if (j == 0) {
@@ -1170,9 +1184,9 @@ int pair_relayout(Model* m, bool front, bool fc, cudaStream_t s, std::string* wh
     for (auto& f : m->front) {
       if (f.kind != RALPB_CONV) continue;
       if (f.im2col)
-        RALPB_TRY(pair_prep_mat(m->P + f.w_off, f.g.cout, f.g.cout, 1, f.kpad, f.wf, nullptr, s));
+        RALPB_TRY(pair_prep_mat(m->P + f.w_off, f.g.cout, f.g.cout, 1, f.kpad, f.wf, nullptr, m->pieces, s));
       else
-        RALPB_TRY(pair_prep_conv(m->P + f.w_off, f.g.cout, f.g.taps(), f.g.cin, f.wf, f.wd, s));
+        RALPB_TRY(pair_prep_conv(m->P + f.w_off, f.g.cout, f.g.taps(), f.g.cin, f.wf, f.wd, m->pieces, s));
       ++m->launches;
     }
   }
@@ -1181,7 +1195,7 @@ int pair_relayout(Model* m, bool front, bool fc, cudaStream_t s, std::string* wh
       FcLayer& f = m->back[j];
       int groups = 0, c = 0;
       fc_in_geom(m, static_cast<int>(j), &groups, &c);
-      RALPB_TRY(pair_prep_mat(m->P + f.w_off, f.out, f.ld_out, groups, c, f.wbf, f.wbd, s));
+      RALPB_TRY(pair_prep_mat(m->P + f.w_off, f.out, f.ld_out, groups, c, f.wbf, f.wbd, m->pieces, s));
       ++m->launches;
     }
   }
@@ -1210,8 +1224,9 @@ void set_border(GemmDesc* d, const ActBuf& a) {
 }
 
 PairFinish finish_for(const ActBuf& a, const float* acc, int n, const float* bias, int relu, const bf16* mask,
-                      bf16* out2) {
+                      bf16* out2, int P) {
   PairFinish f{};
+  f.pieces = P;
   f.acc = acc;
   f.rows = a.rows();
   f.n = n;
@@ -1230,6 +1245,7 @@ PairFinish finish_for(const ActBuf& a, const float* acc, int n, const float* bia
 }
 
 int pair_front_forward(Model* m, const float* img, bf16* cut_dst, std::string* why) {
+  const int P = m->pieces;
   cudaStream_t s = m->stream;
   const int b = m->batch;
   for (size_t i = 0; i < m->front.size(); ++i) {
@@ -1240,36 +1256,36 @@ int pair_front_forward(Model* m, const float* img, bf16* cut_dst, std::string* w
     if (f.im2col) {
       const FrontLayer& f0 = m->front[0];
       RALPB_TRY(pair_pack_im2col(img, b, m->in_h, m->in_w, m->in_c, f0.k, f0.stride, m->desc[0].pad, in.h, in.w, in.pad,
-                                 f0.kpad, in.ptr, s));
+                                 f0.kpad, in.ptr, P, s));
       ++m->launches;
       GemmDesc d;
-      d.M = static_cast<int>(in.rows()); d.N = 2 * f.g.cout; d.K = 2 * f.kpad;
-      d.kb = std::min(64, 2 * f.kpad);
-      d.a = Operand2D{in.ptr, in.rows(), 2 * f.kpad, 2 * f.kpad};
-      d.b = Operand2D{f.wf, 2 * f.g.cout, 2 * f.kpad, 2 * f.kpad};
+      d.M = static_cast<int>(in.rows()); d.N = P * f.g.cout; d.K = P * f.kpad;
+      d.kb = kb_for(P * f.kpad);
+      d.a = Operand2D{in.ptr, in.rows(), P * f.kpad, P * f.kpad};
+      d.b = Operand2D{f.wf, P * f.g.cout, P * f.kpad, P * f.kpad};
       set_border(&d, out);
-      if (pair_gemm(m, d, m->pair_acc, 2 * f.g.cout, 1, false, why)) return 1;
-      RALPB_TRY(pair_finish(finish_for(out, m->pair_acc, f.g.cout, nullptr, 1, nullptr, out.ptr), s));
+      if (pair_gemm(m, d, m->pair_acc, P * f.g.cout, 1, false, why)) return 1;
+      RALPB_TRY(pair_finish(finish_for(out, m->pair_acc, f.g.cout, nullptr, 1, nullptr, out.ptr, P), s));
       ++m->launches;
     } else if (f.kind == RALPB_CONV) {
       const ConvGeom& g = f.g;
       GemmDesc d;
-      d.M = static_cast<int>(g.q()); d.N = 2 * g.cout;
-      d.kb = std::min(64, 2 * g.cin);
-      d.K = static_cast<long long>(g.taps()) * 2 * g.cin;
+      d.M = static_cast<int>(g.q()); d.N = P * g.cout;
+      d.kb = kb_for(P * g.cin);
+      d.K = static_cast<long long>(g.taps()) * P * g.cin;
       d.a_mode = LD_K_CONV;
-      d.a = Operand2D{in.ptr, g.q(), 2 * g.cin, 2 * g.cin};
-      d.cblks = 2 * g.cin / d.kb;
-      d.b = Operand2D{f.wf, 2 * g.cout, d.K, d.K};
+      d.a = Operand2D{in.ptr, g.q(), P * g.cin, P * g.cin};
+      d.cblks = P * g.cin / d.kb;
+      d.b = Operand2D{f.wf, P * g.cout, d.K, d.K};
       d.taps = g.taps();
       for (int r = 0; r < g.k; ++r)
         for (int c = 0; c < g.k; ++c) d.tap_off[r * g.k + c] = (r - g.pad) * g.wp() + (c - g.pad);
       set_border(&d, out);
-      if (pair_gemm(m, d, m->pair_acc, 2 * g.cout, 1, false, why)) return 1;
-      RALPB_TRY(pair_finish(finish_for(out, m->pair_acc, g.cout, m->P + f.b_off, 1, nullptr, out.ptr), s));
+      if (pair_gemm(m, d, m->pair_acc, P * g.cout, 1, false, why)) return 1;
+      RALPB_TRY(pair_finish(finish_for(out, m->pair_acc, g.cout, m->P + f.b_off, 1, nullptr, out.ptr, P), s));
       ++m->launches;
     } else {
-      RALPB_TRY(pair_maxpool_fwd(in.ptr, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.ptr, out.pad, f.idx, s));
+      RALPB_TRY(pair_maxpool_fwd(in.ptr, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.ptr, out.pad, f.idx, P, s));
       ++m->launches;
     }
   }
@@ -1278,19 +1294,21 @@ int pair_front_forward(Model* m, const float* img, bf16* cut_dst, std::string* w
 
 // FC tail forward + loss over R rows of x_fc: logits (fp32), dlogits (pair), loss share.
 int pair_fc_forward_loss(Model* m, int R, float scale, std::string* why) {
+  const int P = m->pieces;
   cudaStream_t s = m->stream;
   const bf16* x = m->x_fc;
-  long long in2 = 2LL * m->cut_elems;
+  long long in2 = static_cast<long long>(P) * m->cut_elems;
   const int nb = static_cast<int>(m->back.size());
   for (int j = 0; j < nb; ++j) {
     FcLayer& f = m->back[j];
     GemmDesc d;
-    d.M = R; d.N = 2 * f.ld_out; d.K = in2;
+    d.M = R; d.N = P * f.ld_out; d.K = in2;
     d.a = Operand2D{x, R, in2, in2};
-    d.b = Operand2D{f.wbf, 2 * f.ld_out, in2, in2};
-    RALPB_TRY(cudaMemsetAsync(m->pair_acc, 0, sizeof(float) * R * 2 * f.ld_out, s));
-    if (pair_gemm(m, d, m->pair_acc, 2 * f.ld_out, 1, true, why)) return 1;
+    d.b = Operand2D{f.wbf, P * f.ld_out, in2, in2};
+    RALPB_TRY(cudaMemsetAsync(m->pair_acc, 0, sizeof(float) * R * P * f.ld_out, s));
+    if (pair_gemm(m, d, m->pair_acc, P * f.ld_out, 1, true, why)) return 1;
     PairFinish fin{};
+    fin.pieces = P;
     fin.acc = m->pair_acc; fin.rows = R; fin.n = f.out; fin.ld = f.ld_out; fin.bias = m->P + f.b_off;
     const bool hidden = j + 1 < nb;
     fin.relu = hidden ? 1 : 0;
@@ -1300,10 +1318,10 @@ int pair_fc_forward_loss(Model* m, int R, float scale, std::string* why) {
     RALPB_TRY(pair_finish(fin, s));
     m->launches += 2;
     x = hidden ? m->hid[j] : nullptr;
-    in2 = 2LL * f.ld_out;
+    in2 = static_cast<long long>(P) * f.ld_out;
   }
   const FcLayer& last = m->back.back();
-  RALPB_TRY(pair_softmax_xent(m->logits, R, last.out, last.ld_out, m->labels_all, scale, m->row_loss, m->dlogits, s));
+  RALPB_TRY(pair_softmax_xent(m->logits, R, last.out, last.ld_out, m->labels_all, scale, m->row_loss, m->dlogits, P, s));
   RALPB_TRY(reduce_sum(m->row_loss, R, scale, m->loss, s));
   m->launches += 2;
   return 0;
@@ -1311,6 +1329,7 @@ int pair_fc_forward_loss(Model* m, int R, float scale, std::string* why) {
 
 // FC backward-data chain down to the cut gradient rows (pairs in the cut's pixel-group layout).
 int pair_fc_backward_data(Model* m, int R, bf16* dx_out, std::string* why) {
+  const int P = m->pieces;
   cudaStream_t s = m->stream;
   const int nb = static_cast<int>(m->back.size());
   for (int j = nb - 1; j >= 0; --j) {
@@ -1318,14 +1337,15 @@ int pair_fc_backward_data(Model* m, int R, bf16* dx_out, std::string* why) {
     const bf16* dy = j == nb - 1 ? m->dlogits : m->dyb[j];
     int groups = 0, c = 0;
     fc_in_geom(m, j, &groups, &c);
-    const long long in2 = 2LL * groups * c;
+    const long long in2 = static_cast<long long>(P) * groups * c;
     GemmDesc d;
-    d.M = R; d.N = static_cast<int>(in2); d.K = 2 * f.ld_out;
-    d.a_mode = LD_K; d.a = Operand2D{dy, R, 2 * f.ld_out, 2 * f.ld_out};
-    d.b_mode = LD_MN; d.b = Operand2D{f.wbd, 2 * f.ld_out, in2, in2};
+    d.M = R; d.N = static_cast<int>(in2); d.K = P * f.ld_out;
+    d.a_mode = LD_K; d.a = Operand2D{dy, R, P * f.ld_out, P * f.ld_out};
+    d.b_mode = LD_MN; d.b = Operand2D{f.wbd, P * f.ld_out, in2, in2};
     RALPB_TRY(cudaMemsetAsync(m->pair_acc, 0, sizeof(float) * R * in2, s));
     if (pair_gemm(m, d, m->pair_acc, in2, 1, true, why)) return 1;
     PairFinishGroups fin{};
+    fin.pieces = P;
     fin.acc = m->pair_acc; fin.rows = R; fin.groups = groups; fin.c = c;
     fin.mask = j > 0 ? m->hid[j - 1] : nullptr;
     fin.out2 = j > 0 ? m->dyb[j - 1] : dx_out;
@@ -1337,6 +1357,7 @@ int pair_fc_backward_data(Model* m, int R, bf16* dx_out, std::string* why) {
 
 // FC weight / bias gradients into G, and (update) the PS-local SGD with the pair re-layout.
 int pair_fc_backward_weights(Model* m, int R, bool update, float lr, float mu, std::string* why) {
+  const int P = m->pieces;
   cudaStream_t s = m->stream;
   const int nb = static_cast<int>(m->back.size());
   for (int j = nb - 1; j >= 0; --j) {
@@ -1345,16 +1366,16 @@ int pair_fc_backward_weights(Model* m, int R, bool update, float lr, float mu, s
     const bf16* x = j == 0 ? m->x_fc : m->hid[j - 1];
     int groups = 0, c = 0;
     fc_in_geom(m, j, &groups, &c);
-    const long long in2 = 2LL * groups * c;
+    const long long in2 = static_cast<long long>(P) * groups * c;
     RALPB_TRY(cudaMemsetAsync(m->G + f.b_off, 0, f.out * sizeof(float), s));
-    RALPB_TRY(pair_colsum(dy, R, f.out, f.ld_out, m->G + f.b_off, s));
+    RALPB_TRY(pair_colsum(dy, R, f.out, f.ld_out, m->G + f.b_off, P, s));
     GemmDesc w;
-    w.M = 2 * f.ld_out; w.N = static_cast<int>(in2); w.K = R;
-    w.a_mode = LD_MN; w.a = Operand2D{dy, R, 2 * f.ld_out, 2 * f.ld_out};
+    w.M = P * f.ld_out; w.N = static_cast<int>(in2); w.K = R;
+    w.a_mode = LD_MN; w.a = Operand2D{dy, R, P * f.ld_out, P * f.ld_out};
     w.b_mode = LD_MN; w.b = Operand2D{x, R, in2, in2};
-    RALPB_TRY(cudaMemsetAsync(m->pair_s, 0, sizeof(float) * 2 * f.ld_out * in2, s));
+    RALPB_TRY(cudaMemsetAsync(m->pair_s, 0, sizeof(float) * P * f.ld_out * in2, s));
     if (pair_gemm(m, w, m->pair_s, in2, 1, true, why)) return 1;
-    RALPB_TRY(pair_reduce_wgrad(m->pair_s, f.ld_out, f.out, groups, c, m->G + f.w_off, static_cast<long long>(groups) * c, s));
+    RALPB_TRY(pair_reduce_wgrad(m->pair_s, f.ld_out, f.out, groups, c, m->G + f.w_off, static_cast<long long>(groups) * c, P, s));
     m->launches += 3;
   }
   if (update) {
@@ -1370,6 +1391,7 @@ int pair_fc_backward_weights(Model* m, int R, bool update, float lr, float mu, s
 }
 
 int pair_front_backward(Model* m, const bf16* dcut, std::string* why) {
+  const int P = m->pieces;
   cudaStream_t s = m->stream;
   const bf16* cur = dcut;
   for (int i = static_cast<int>(m->front.size()) - 1; i >= 0; --i) {
@@ -1378,7 +1400,7 @@ int pair_front_backward(Model* m, const bf16* dcut, std::string* why) {
     const ActBuf& out = m->acts[i + 1];
     if (f.kind == RALPB_POOL) {
       RALPB_TRY(pair_maxpool_bwd(f.idx, cur, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.pad, m->gacts[i], nullptr,
-                                 s));
+                                 P, s));
       ++m->launches;
       cur = m->gacts[i];
       continue;
@@ -1386,51 +1408,51 @@ int pair_front_backward(Model* m, const bf16* dcut, std::string* why) {
     if (f.im2col) {
       // dW[co][j] = sum over the output grid of dY[row][co] * patches[row][j] (bias in column k*k*cin)
       GemmDesc d;
-      d.M = 2 * f.g.cout; d.N = 2 * f.kpad; d.K = in.rows();
-      d.a_mode = LD_MN; d.a = Operand2D{cur, out.rows(), 2 * f.g.cout, 2 * f.g.cout};
-      d.b_mode = LD_MN; d.b = Operand2D{in.ptr, in.rows(), 2 * f.kpad, 2 * f.kpad};
-      RALPB_TRY(cudaMemsetAsync(m->pair_s, 0, sizeof(float) * 4 * f.g.cout * f.kpad, s));
-      if (pair_gemm(m, d, m->pair_s, 2 * f.kpad, 1, true, why)) return 1;
-      RALPB_TRY(pair_reduce_wgrad(m->pair_s, f.g.cout, f.g.cout, 1, f.kpad, m->G + f.w_off, f.kpad, s));
+      d.M = P * f.g.cout; d.N = P * f.kpad; d.K = in.rows();
+      d.a_mode = LD_MN; d.a = Operand2D{cur, out.rows(), P * f.g.cout, P * f.g.cout};
+      d.b_mode = LD_MN; d.b = Operand2D{in.ptr, in.rows(), P * f.kpad, P * f.kpad};
+      RALPB_TRY(cudaMemsetAsync(m->pair_s, 0, sizeof(float) * P * P * f.g.cout * f.kpad, s));
+      if (pair_gemm(m, d, m->pair_s, P * f.kpad, 1, true, why)) return 1;
+      RALPB_TRY(pair_reduce_wgrad(m->pair_s, f.g.cout, f.g.cout, 1, f.kpad, m->G + f.w_off, f.kpad, P, s));
       ++m->launches;
       continue;
     }
     const ConvGeom& g = f.g;
     // bias gradient: sum of the (masked) output gradient
-    RALPB_TRY(pair_colsum(cur, out.rows(), g.cout, g.cout, m->G + f.b_off, s));
+    RALPB_TRY(pair_colsum(cur, out.rows(), g.cout, g.cout, m->G + f.b_off, P, s));
     // weight gradient: S[(a,co)][t][(b,ci)] = sum_q dy_a[q][co] x_b[q + off(t)][ci]
     {
       GemmDesc d;
-      d.M = g.taps() * 2 * g.cin; d.N = 2 * g.cout; d.K = g.q();
-      d.a_mode = LD_MN_CONV; d.a = Operand2D{in.ptr, g.q(), 2 * g.cin, 2 * g.cin}; d.a_cin = 2 * g.cin;
-      d.b_mode = LD_MN; d.b = Operand2D{cur, g.q(), 2 * g.cout, 2 * g.cout};
+      d.M = g.taps() * P * g.cin; d.N = P * g.cout; d.K = g.q();
+      d.a_mode = LD_MN_CONV; d.a = Operand2D{in.ptr, g.q(), P * g.cin, P * g.cin}; d.a_cin = P * g.cin;
+      d.b_mode = LD_MN; d.b = Operand2D{cur, g.q(), P * g.cout, P * g.cout};
       d.taps = g.taps();
       for (int r = 0; r < g.k; ++r)
         for (int c = 0; c < g.k; ++c) d.tap_off[r * g.k + c] = (r - g.pad) * g.wp() + (c - g.pad);
-      const int n2 = 2 * g.cout;
+      const int n2 = P * g.cout;
       d.block_n = n2 >= 256 ? 256 : (n2 >= 128 ? 128 : (n2 >= 64 ? 64 : 32));
-      RALPB_TRY(cudaMemsetAsync(m->pair_s, 0, sizeof(float) * 4 * f.w_count, s));
-      if (pair_gemm(m, d, m->pair_s, 1, static_cast<long long>(g.taps()) * 2 * g.cin, true, why)) return 1;
+      RALPB_TRY(cudaMemsetAsync(m->pair_s, 0, sizeof(float) * P * P * f.w_count, s));
+      if (pair_gemm(m, d, m->pair_s, 1, static_cast<long long>(g.taps()) * P * g.cin, true, why)) return 1;
       RALPB_TRY(pair_reduce_wgrad(m->pair_s, g.cout, g.cout, g.taps(), g.cin, m->G + f.w_off,
-                                  static_cast<long long>(g.taps()) * g.cin, s));
+                                  static_cast<long long>(g.taps()) * g.cin, P, s));
       m->launches += 2;
     }
     if (i > 0) {
       // backward-data: out[q][(a,ci)] = sum dy[q + off'][(b,co)] wd_a; masked by the producer's ReLU
       GemmDesc d;
-      d.M = static_cast<int>(g.q()); d.N = 2 * g.cin;
-      d.kb = std::min(64, 2 * g.cout);
-      d.K = static_cast<long long>(g.taps()) * 2 * g.cout;
-      d.a_mode = LD_K_CONV; d.a = Operand2D{cur, g.q(), 2 * g.cout, 2 * g.cout};
-      d.cblks = 2 * g.cout / d.kb;
-      d.b = Operand2D{f.wd, 2 * g.cin, d.K, d.K};
+      d.M = static_cast<int>(g.q()); d.N = P * g.cin;
+      d.kb = kb_for(P * g.cout);
+      d.K = static_cast<long long>(g.taps()) * P * g.cout;
+      d.a_mode = LD_K_CONV; d.a = Operand2D{cur, g.q(), P * g.cout, P * g.cout};
+      d.cblks = P * g.cout / d.kb;
+      d.b = Operand2D{f.wd, P * g.cin, d.K, d.K};
       d.taps = g.taps();
       for (int r = 0; r < g.k; ++r)
         for (int c = 0; c < g.k; ++c) d.tap_off[r * g.k + c] = (r - g.pad) * g.wp() + (c - g.pad);
       set_border(&d, in);
-      if (pair_gemm(m, d, m->pair_acc, 2 * g.cin, 1, false, why)) return 1;
+      if (pair_gemm(m, d, m->pair_acc, P * g.cin, 1, false, why)) return 1;
       const bool mask = m->front[i - 1].kind == RALPB_CONV;
-      RALPB_TRY(pair_finish(finish_for(in, m->pair_acc, g.cin, nullptr, 0, mask ? in.ptr : nullptr, m->gacts[i]), s));
+      RALPB_TRY(pair_finish(finish_for(in, m->pair_acc, g.cin, nullptr, 0, mask ? in.ptr : nullptr, m->gacts[i], P), s));
       ++m->launches;
       cur = m->gacts[i];
     }
@@ -1493,10 +1515,11 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   ++m->launches;
   const long long cut_logical = static_cast<long long>(b) * m->cut_elems * eb;  // one worker's cut
   const bool pairs = pair_mode(m);
-  const size_t cut_row = static_cast<size_t>(m->cut_elems) * (pairs ? 2 : 1);  // bf16 elements per cut row
+  const size_t cut_row = static_cast<size_t>(m->cut_elems) * (pairs ? m->pieces : 1);  // bf16 elements per cut row
   const size_t cut_bytes = static_cast<size_t>(b) * cut_row * sizeof(bf16);
   const int slot = ralp || m->mps ? m->widx : 0;   // this worker's row block in the PS input
   const bf16* cut_local = nullptr;
+  bool scatter_forked = false;
 
   if (m->is_worker && pairs) {
     bf16* cut_dst = m->acts.back().ptr;
@@ -1644,6 +1667,15 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
           m->nvl_out += cut_bytes;
         }
       } else if (m->world > 1) {
+        // on the comm stream: the 128-bit peer copies to the workers run concurrently with this
+        // rank's FC weight gradients and front backward (RALPB_SCATTER_STREAM=0: in order)
+        const char* ss = getenv("RALPB_SCATTER_STREAM");
+        const bool own_stream = !(ss != nullptr && ss[0] == '0');
+        cudaStream_t sx = own_stream ? m->comm_stream : s;
+        if (own_stream) {
+          RALPB_TRY(cudaEventRecord(m->ev_comm_fork, s));
+          RALPB_TRY(cudaStreamWaitEvent(sx, m->ev_comm_fork, 0));
+        }
         PeerScatter sc{};
         PeerSignal sig{};
         for (int w = 0; w < W; ++w) {
@@ -1655,8 +1687,12 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
           sig.flag[sig.n++] = at<uint32_t>(m, r, m->arena_off_flags) + kFlagActGrad;
           m->nvl_out += cut_bytes;
         }
-        RALPB_TRY(scatter_and_signal(sc, static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + kCtrScatter, s));
+        RALPB_TRY(scatter_and_signal(sc, static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + kCtrScatter, sx));
         ++m->launches;
+        if (own_stream) {
+          RALPB_TRY(cudaEventRecord(m->ev_comm_join, sx));
+          scatter_forked = true;
+        }
       }
       // weight gradients on this stream (tensor/HBM work that would contend with the persistent
       // conv kernels), the HBM-bound update on the aux stream, overlapping the front backward
@@ -1685,6 +1721,8 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   }
   RALPB_TRY(mark(m, 2, capturing));
 
+  // the act-grad rows (dx_fc) are rewritten next step only after the sync; join the scatter here
+  if (scatter_forked && !m->is_worker) RALPB_TRY(cudaStreamWaitEvent(s, m->ev_comm_join, 0));
   if (!m->is_worker) {
     // dedicated PS (RALP-N): its step ends with the FC tail's update; release the FC input rows
     // to the workers' next cut pushes
@@ -1706,6 +1744,7 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   // join the FC tail's update before this rank signals the sync: a worker can only start the
   // next step (and push its cut into x_fc, which the FC wgrads read) after that sync
   if (fc_forked) RALPB_TRY(cudaStreamWaitEvent(s, m->ev_join, 0));
+  if (scatter_forked) RALPB_TRY(cudaStreamWaitEvent(s, m->ev_comm_join, 0));
   if (m->strategy == RALPB_STRATEGY_RING_EXTERNAL) {
     // the caller all-reduces G, then ralpb_model_apply; count the ring share here
     const long long sh = m->shard_real[m->widx];

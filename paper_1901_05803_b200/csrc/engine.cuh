@@ -53,6 +53,7 @@ struct Model {
   int rank = 0, world = 1, ps_rank = 0, device = 0;
   int batch = 0, split = 0, strategy = RALPB_STRATEGY_RALP, elem_bytes = 4;
   int precision = RALPB_PRECISION_BF16;
+  int pieces = 1;                  // bf16 pieces per value (parity precision: 3, pair.cuh)
   int workers = 1;                 // ranks that run a conv front (world, or world - 1 for RALP-N)
   bool dedicated_ps = false;       // RALP-N: ps_rank runs only the back segment
   bool is_worker = true;           // this rank runs a conv front
@@ -94,6 +95,8 @@ struct Model {
   cudaStream_t aux_stream = nullptr;   // PS: FC weight gradients + SGD, concurrent with the
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // front backward
   cudaEvent_t ev_wd_fork = nullptr, ev_wd_join = nullptr;  // backward-data filter copies (aux stream)
+  cudaStream_t comm_stream = nullptr;  // PS: the act-grad scatter, concurrent with the FC weight
+  cudaEvent_t ev_comm_fork = nullptr, ev_comm_join = nullptr;  // gradients and the front backward
   float* row_loss = nullptr;
   float* loss = nullptr;           // [4]: the reported loss (mean over the job's samples), [1] this
                                    // rank's own-row sum (baseline / ring: pushed to ps_rank's slot)

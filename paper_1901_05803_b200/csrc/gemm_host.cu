@@ -87,7 +87,10 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
   if (!(kb == 16 || kb == 32 || kb == 64)) { *why = "kb must be 16/32/64"; return cudaErrorInvalidValue; }
   p.kb = kb;
   // ---- swizzles
-  p.a_swz = a_k ? kb * 2 : (d.a_mode == LD_MN_CONV ? std::min(128, d.a_cin * 2) : 128);
+  // LD_MN_CONV: the widest swizzle atom that divides one tap's channel row (e.g. 96 channels -> 64 B)
+  const int conv_row = d.a_cin * 2;
+  p.a_swz = a_k ? kb * 2
+                : (d.a_mode == LD_MN_CONV ? (conv_row % 128 == 0 ? 128 : (conv_row % 64 == 0 ? 64 : 32)) : 128);
   p.b_swz = b_k ? kb * 2 : std::min(128, bn * 2);
   if (d.a_mode == LD_MN_CONV && (d.a_cin * 2) % p.a_swz != 0) { *why = "a_cin must be a multiple of the atom"; return cudaErrorInvalidValue; }
   p.a_bytes = a_k ? kBM * kb * 2 : kBM * 64 * 2;

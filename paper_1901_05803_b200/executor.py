@@ -260,8 +260,8 @@ class RankExecutor:
         if n < 0:
             raise ExecutorError(f"debug buffer {which}/{i} is not available")
         f32 = which in (_lib.DBG_LOGITS, _lib.DBG_MPS_PARTIAL)
-        pair = self.precision == "fp32"
-        elems = n * (2 if pair and not f32 else 1)
+        pieces = int(os.environ.get("RALPB_PIECES", "3")) if self.precision == "fp32" else 1
+        elems = n * (pieces if not f32 else 1)
         t = torch.empty(elems, dtype=torch.float32 if f32 else torch.bfloat16)
         if _lib.lib().ralpb_model_debug_buffer(self._h, i, which, C.c_void_p(t.data_ptr())) != n:
             raise ExecutorError(f"debug buffer {which}/{i}: copy failed")

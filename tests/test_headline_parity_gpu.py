@@ -213,16 +213,23 @@ def test_headline_front_backward_per_layer(headline):
 
 
 def test_headline_sgd_update(headline):
+    """First step, momentum 0: v = g, p1 = p0 - lr * g (one fused multiply-add on the GPU, so up to
+    1 ulp from the host's two roundings)."""
     params, grads, new = headline["params"], headline["grads"], headline["new"]
-    worst = 0.0
-    for p0, g, p1 in zip(params, grads, new):
+    worst, where = 0.0, None
+    for li, (p0, g, p1) in enumerate(zip(params, grads, new)):
         if p0 is None:
             continue
-        for a, gg, c in zip(p0, g, p1):
-            want = (torch.from_numpy(a) - torch.tensor(LR, dtype=torch.float32) * torch.from_numpy(gg)).numpy()
-            ulp = np.spacing(np.abs(want).astype(np.float32))
-            worst = max(worst, float((np.abs(c - want) / ulp).max()))
-    print("SGD step worst deviation (ulp):", worst)
+        for nm, a, gg, c in zip("wb", p0, g, p1):
+            want = (a.astype(np.float64) - np.float64(np.float32(LR)) * gg.astype(np.float64))
+            ulp = np.spacing(np.abs(want).astype(np.float32)).astype(np.float64)
+            dev = np.abs(c.astype(np.float64) - want) / ulp
+            k = int(np.argmax(dev))
+            print(f"  layer {li}.{nm}: worst {dev.flat[k]:.2f} ulp (p0 {a.flat[k]:.6e} g {gg.flat[k]:.6e} "
+                  f"p1 {c.flat[k]:.6e} want {want.flat[k]:.6e})")
+            if dev.flat[k] > worst:
+                worst, where = float(dev.flat[k]), f"{li}.{nm}"
+    print("SGD step worst deviation (ulp):", worst, where)
     assert worst <= 1.0
 
 
