@@ -232,21 +232,27 @@ def param_count(L) -> int:
 
 
 def train_step(st: OracleState, strategy: str, workers: int, batches, *, lr: float = 0.01, mu: float = 0.9,
-               emulate_bf16: bool = False, elem_bytes: int = 4, accum64: bool = False):
+               emulate_bf16: bool = False, elem_bytes: int = 4, accum64: bool = False, split: int | None = None):
     """One step.  batches[r] = (images [b,h,w,c] fp32, labels [b] int) of worker r.
+    split (RALP): the partitioner's 1-based cut index (profiler.py:101-134); None = the FC
+    boundary.  A conv / pool back segment [split, first FC) runs on the PS over the gathered rows;
+    those layers act on every image independently and their weights are fixed within the step, so
+    the numerics equal running them on each worker (what this restatement does) -- only the cut
+    shipped and the synchronised front differ, in the byte count.
     Returns (loss, logical_bytes)."""
     _ACC[0] = torch.float64 if accum64 else torch.float32
     bf = emulate_bf16
     nfront = _split_index(st.layers)
+    cut_at = nfront if split is None else split
     b = batches[0][0].shape[0]
     scale = 1.0 / (workers * b)
     wire = 0
-    p_front = sum(param_count(L) for L in st.layers[:nfront]) * elem_bytes
+    p_front = sum(param_count(L) for L in st.layers[:cut_at]) * elem_bytes
     p_all = sum(param_count(L) for L in st.layers) * elem_bytes
     total: dict = {}
     if strategy == "ralp":
         fronts = [_front_forward(st, nfront, imgs, bf) for imgs, _ in batches]
-        cut_bytes = fronts[0][1].numel() * elem_bytes
+        cut_bytes = fronts[0][0][cut_at].numel() * elem_bytes   # layer cut_at-1's output (acts[cut_at])
         wire += workers * cut_bytes                        # "act" (simulator.py:677)
         x = torch.cat([c for _, c in fronts], dim=0)
         labels = np.concatenate([lab for _, lab in batches])

@@ -131,9 +131,16 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     if (layers[i].kind != RALPB_FC) return fail("only FC layers may follow the first FC layer");
   const bool layer_placed = strategy == RALPB_STRATEGY_RALP || strategy == RALPB_STRATEGY_RALP_MPS;
   m->mps = strategy == RALPB_STRATEGY_RALP_MPS;
-  if (layer_placed && split != nconv)
-    return fail("this executor places exactly the FC tail on the PS (split must be " + std::to_string(nconv) + ")");
-  m->split = nconv;
+  // split = 1-based cut index of the partitioner (profiler.py:101-134): layers [0, split) are the
+  // replicated worker front; conv / pool layers [split, nconv) -- a conv back segment -- run on the
+  // PS over the W*b gathered rows together with the FC tail (layer-placed, single PS, bf16)
+  if (layer_placed && (split < 1 || split > nconv))
+    return fail("the split must cut inside the conv/pool front or at the FC boundary (1.." + std::to_string(nconv) + ")");
+  if (layer_placed && split < nconv && (strategy != RALPB_STRATEGY_RALP || precision != RALPB_PRECISION_BF16))
+    return fail("a conv back segment (split before the FC tail) runs with the single PS in bf16 precision");
+  m->nconv = nconv;
+  m->split = layer_placed ? split : nconv;
+  m->bseg = m->split < nconv;
   m->holds_back = strategy != RALPB_STRATEGY_RALP || rank == ps_rank;   // RALP_MPS: every rank
   m->rows_back = layer_placed ? workers * batch : batch;
   if (m->mps) {
@@ -166,11 +173,18 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   m->acts.push_back(a0);
   long long off = 0;
   std::vector<std::pair<long long, long long>> real_runs;  // (offset, floats) of descriptor parameters
+  const int rows_bseg = workers * batch;   // the PS's back segment runs over every worker's rows
   for (int i = 0; i < nconv; ++i) {
     const ralpb_layer_desc& d = layers[i];
-    const ActBuf& in = m->acts.back();
+    if (i == m->split && m->bseg) {  // the synchronised front ends here
+      m->n_front = align_up(off, kShardAlign);
+      off = m->n_front;
+    }
+    const int nb = i >= m->split ? rows_bseg : batch;
+    ActBuf in = m->acts.back();
+    in.n = nb;
     ActBuf o;
-    o.n = batch;
+    o.n = nb;
     FrontLayer f;
     f.kind = d.kind;
     if (i == 0 && first_im2col) {
@@ -207,17 +221,21 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
       f.cin_real = d.cin;
       f.k = d.k;
       f.stride = 1;
-      f.g = ConvGeom{batch, d.h, d.w, in.c, d.cout, d.k, d.pad};
+      f.g = ConvGeom{nb, d.h, d.w, in.c, d.cout, d.k, d.pad};
       f.relu = 1;
       f.w_count = static_cast<long long>(d.cout) * d.k * d.k * in.c;
       f.w_off = off;
       off = align_up(off + f.w_count, 4);
       f.b_off = off;
       off = align_up(off + d.cout, 4);
-      for (long long ot = 0; ot < static_cast<long long>(d.cout) * d.k * d.k; ++ot)
-        real_runs.emplace_back(f.w_off + ot * in.c, d.cin);
-      real_runs.emplace_back(f.b_off, d.cout);
-      m->real_front += static_cast<long long>(d.cout) * d.k * d.k * d.cin + d.cout;
+      if (i < m->split) {  // synchronised front parameters
+        for (long long ot = 0; ot < static_cast<long long>(d.cout) * d.k * d.k; ++ot)
+          real_runs.emplace_back(f.w_off + ot * in.c, d.cin);
+        real_runs.emplace_back(f.b_off, d.cout);
+        m->real_front += static_cast<long long>(d.cout) * d.k * d.k * d.cin + d.cout;
+      } else {
+        m->real_bseg += static_cast<long long>(d.cout) * d.k * d.k * d.cin + d.cout;
+      }
       o.h = d.h; o.w = d.w; o.c = d.cout; o.pad = d.pad;
     } else if (d.kind == RALPB_POOL) {
       f.k = d.k;
@@ -234,11 +252,19 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     m->acts.push_back(o);
   }
   const ActBuf& cut = m->acts.back();
-  if (cut.pad != 0) return fail("the cut activation must be a pooling output");
+  if (cut.pad != 0) return fail("the FC tail's input must be a pooling output");
   m->cut_elems = cut.h * cut.w * cut.c;
-  m->n_front = align_up(off, kShardAlign);
-  off = m->n_front;
-  m->real_total = m->real_front;
+  if (!m->bseg) m->n_front = align_up(off, kShardAlign);
+  m->bseg_end = align_up(off, 4);
+  off = align_up(off, kShardAlign);
+  m->real_total = m->real_front + m->real_bseg;
+  {  // the exchanged cut: layer split-1's output (padded when a conv of the back segment reads it)
+    const ActBuf& x = m->acts[m->split];
+    m->xch_elems = (x.h + 2 * x.pad) * (x.w + 2 * x.pad) * x.c;
+    m->xch_logical = static_cast<long long>(x.h) * x.w * x.c;
+    m->bin = x;
+    m->bin.n = rows_bseg;
+  }
   int prev = m->cut_elems;
   for (int i = nconv; i < n_layers; ++i) {
     const ralpb_layer_desc& d = layers[i];
@@ -292,9 +318,9 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     m->pieces = pe != nullptr && atoi(pe) == 2 ? 2 : 3;
   }
   const int pm = precision == RALPB_PRECISION_FP32 ? m->pieces : 1;  // bf16 elements per value
-  m->arena_off_xfc = take(static_cast<size_t>(m->rows_back) * m->cut_elems * sizeof(bf16) * pm);
+  m->arena_off_xfc = take(static_cast<size_t>(m->rows_back) * m->xch_elems * sizeof(bf16) * pm);
   m->arena_off_lab = take(static_cast<size_t>(m->rows_back) * sizeof(int32_t));
-  m->arena_off_dcut = take(static_cast<size_t>(batch) * m->cut_elems * sizeof(bf16) * pm);
+  m->arena_off_dcut = take(static_cast<size_t>(batch) * m->xch_elems * sizeof(bf16) * pm);
   m->arena_off_loss = take(kMaxRanks * 4 * sizeof(float));   // [worker][4] own-row loss sums
   if (m->mps) {
     const int ld1 = static_cast<int>(align_up(layers[nconv + 1].cout, 8));
@@ -309,7 +335,9 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   m->flags = reinterpret_cast<uint32_t*>(base + m->arena_off_flags);
   m->P = reinterpret_cast<float*>(base + m->arena_off_P);
   m->G = reinterpret_cast<float*>(base + m->arena_off_G);
-  m->x_fc = reinterpret_cast<bf16*>(base + m->arena_off_xfc);
+  m->xin = reinterpret_cast<bf16*>(base + m->arena_off_xfc);
+  m->x_fc = m->xin;
+  m->bin.ptr = m->xin;
   m->labels_all = reinterpret_cast<int32_t*>(base + m->arena_off_lab);
   m->dcut = reinterpret_cast<bf16*>(base + m->arena_off_dcut);
   m->peer_base.assign(world, nullptr);
@@ -324,12 +352,16 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   m->seq_dev = m->counters + kNumCounters - 1;
   // Every activation and activation-gradient buffer is dedicated and zeroed once: the conv
   // kernels write interior pixels only, so the padding borders stay zero for the job's life.
+  // Workers hold acts[0..split] (batch rows); the PS of a conv back segment acts[split+1..nconv]
+  // (W*b rows; its input is the arena's xin).
   m->gacts.assign(m->acts.size(), nullptr);
-  for (size_t i = 0; m->is_worker && i < m->acts.size(); ++i) {
+  for (size_t i = 0; i < m->acts.size(); ++i) {
+    const bool mine = static_cast<int>(i) <= m->split ? m->is_worker : (m->bseg && m->holds_back);
+    if (!mine) continue;
     const size_t bytes = static_cast<size_t>(m->acts[i].elems()) * sizeof(bf16) * pm;
     if (!(m->acts[i].ptr = alloc<bf16>(m, m->acts[i].elems() * pm, why))) return fail(*why);
     cudaMemset(m->acts[i].ptr, 0, bytes);
-    if (i > 0 && i + 1 < m->acts.size()) {
+    if (i > 0 && i + 1 < m->acts.size() && static_cast<int>(i) != m->split) {
       if (!(m->gacts[i] = alloc<bf16>(m, m->acts[i].elems() * pm, why))) return fail(*why);
       cudaMemset(m->gacts[i], 0, bytes);
     }
@@ -342,11 +374,12 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     FrontLayer& c = m->front[i];
     FrontLayer& pl = m->front[i + 1];
     if (c.kind == RALPB_CONV && !c.im2col && pl.kind == RALPB_POOL && pl.k == 2 && pl.stride == 2 &&
+        static_cast<int>(i) + 1 != m->split &&
         conv_fwd_pool_ok(c.g) && fuse_pool_enabled() && precision == RALPB_PRECISION_BF16) {
       pl.fused_fwd = true;
       const ActBuf& po = m->acts[i + 2];
       const char* ie = getenv("RALPB_POOL_IDX");
-      if (ie != nullptr && ie[0] == '1' && c.g.cin >= 128 && m->is_worker &&
+      if (ie != nullptr && ie[0] == '1' && c.g.cin >= 128 && m->acts[i + 1].ptr != nullptr &&
           !(pl.idx = alloc<uint8_t>(m, static_cast<size_t>(po.n) * po.h * po.w * po.c, why)))
         return fail(*why);
     }
@@ -355,12 +388,15 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   // forward and gather the backward from them (maxpool_bwd_gather)
   for (size_t i = 0; i < m->front.size(); ++i) {
     FrontLayer& pl = m->front[i];
-    if (pl.kind != RALPB_POOL || pl.fused_fwd || pl.k * pl.k > 255 || !m->is_worker) continue;
+    if (pl.kind != RALPB_POOL || pl.fused_fwd || pl.k * pl.k > 255) continue;
+    if (!(static_cast<int>(i) < m->split ? m->is_worker : (m->bseg && m->holds_back))) continue;
     const ActBuf& po = m->acts[i + 1];
     if (!(pl.idx = alloc<uint8_t>(m, static_cast<size_t>(po.n) * po.h * po.w * po.c, why))) return fail(*why);
   }
-  for (auto& f : m->front) {
-    if (f.kind != RALPB_CONV || !m->is_worker) continue;
+  for (size_t i = 0; i < m->front.size(); ++i) {
+    FrontLayer& f = m->front[i];
+    const bool mine = static_cast<int>(i) < m->split ? m->is_worker : (m->bseg && m->holds_back);
+    if (f.kind != RALPB_CONV || !mine) continue;
     // pair precision: [2co][taps][2ci] operand copies (pair.cuh)
     if (!(f.wf = alloc<bf16>(m, f.w_count * pm * pm, why))) return fail(*why);
     if (!f.im2col && !(f.wd = alloc<bf16>(m, f.w_count * pm * pm, why))) return fail(*why);
@@ -403,6 +439,13 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     m->dyb.push_back(d);
   }
   if (!(m->dx_fc = alloc<bf16>(m, static_cast<size_t>(R) * m->cut_elems * pm, why))) return fail(*why);
+  m->dxin = m->dx_fc;
+  if (m->bseg && m->holds_back) {
+    // the conv back segment: FC input rows and the cut gradient rows are separate buffers
+    if (!(m->x_fc = alloc<bf16>(m, static_cast<size_t>(R) * m->cut_elems, why))) return fail(*why);
+    if (!(m->dxin = alloc<bf16>(m, static_cast<size_t>(R) * m->xch_elems, why))) return fail(*why);
+    cudaMemset(m->dxin, 0, static_cast<size_t>(R) * m->xch_elems * sizeof(bf16));
+  }
   if (pm > 1) {
     // scratch of the piece contractions: the fp32 [rows][P*N] outputs before their finishing pass
     // and the [P*M][T][P*C] weight-gradient blocks
@@ -512,7 +555,7 @@ int model_set_params(Model* m, int layer, const float* w, const float* b, int on
   if (layer < 0 || layer >= static_cast<int>(m->desc.size())) { *why = "layer out of range"; return 1; }
   const auto kind = cudaMemcpyDefault;
   (void)on_host;
-  if (layer < m->split) {
+  if (layer < m->nconv) {
     FrontLayer& f = m->front[layer];
     if (f.kind != RALPB_CONV) { *why = "layer has no parameters"; return 1; }
     const int co = f.g.cout, taps = f.k * f.k, cr = f.cin_real;
@@ -534,15 +577,15 @@ int model_set_params(Model* m, int layer, const float* w, const float* b, int on
       RALPB_TRY(cudaMemcpyAsync(m->P + f.b_off, hb.data(), co * sizeof(float), cudaMemcpyHostToDevice, m->stream));
     }
     RALPB_TRY(cudaMemcpyAsync(m->P + f.w_off, packed.data(), packed.size() * sizeof(float), cudaMemcpyHostToDevice, m->stream));
-    if (!m->is_worker || pair_mode(m)) {
-      // the dedicated PS keeps no operand copies of the front; pairs: pair_relayout below
+    if (f.wf == nullptr || pair_mode(m)) {
+      // layers this rank does not run keep no operand copies; pairs: pair_relayout below
     } else if (f.im2col) {
       RALPB_TRY(cast_bf16(m->P + f.w_off, f.w_count, f.wf, m->stream));
     } else {
       RALPB_TRY(conv_weight_prep(m->P + f.w_off, co, taps, f.g.cin, f.wf, f.wd, m->stream));
     }
   } else {
-    const int j = layer - m->split;
+    const int j = layer - m->nconv;
     FcLayer& f = m->back[j];
     if (m->mps && j == 0) {          // column-parallel: this rank's rows
       const size_t r0 = static_cast<size_t>(m->rank) * m->s0;
@@ -559,7 +602,7 @@ int model_set_params(Model* m, int layer, const float* w, const float* b, int on
     }
     if (!pair_mode(m)) RALPB_TRY(cast_bf16(m->P + f.w_off, static_cast<long long>(f.lout) * f.lin, f.wbf, m->stream));
   }
-  if (pair_mode(m) && pair_relayout(m, layer < m->split, layer >= m->split, m->stream, why)) return 1;
+  if (pair_mode(m) && pair_relayout(m, layer < m->nconv, layer >= m->nconv, m->stream, why)) return 1;
   RALPB_TRY(cudaStreamSynchronize(m->stream));
   return 0;
 }
@@ -570,7 +613,7 @@ static int read_layer(Model* m, int layer, float* w, float* b, size_t off, std::
   if (layer < 0 || layer >= static_cast<int>(m->desc.size())) { *why = "layer out of range"; return 1; }
   const float* self = at<float>(m, m->rank, off);
   RALPB_TRY(cudaStreamSynchronize(m->stream));
-  if (layer < m->split) {
+  if (layer < m->nconv) {
     FrontLayer& f = m->front[layer];
     if (f.kind != RALPB_CONV) { *why = "layer has no parameters"; return 1; }
     const int co = f.g.cout, taps = f.k * f.k, cr = f.cin_real;
@@ -593,7 +636,7 @@ static int read_layer(Model* m, int layer, float* w, float* b, size_t off, std::
     RALPB_TRY(cudaMemcpy(w, host.data(), host.size() * sizeof(float), cudaMemcpyDefault));
     RALPB_TRY(cudaMemcpy(b, hb.data(), co * sizeof(float), cudaMemcpyDefault));
   } else {
-    const int j = layer - m->split;
+    const int j = layer - m->nconv;
     FcLayer& f = m->back[j];
     if (m->mps && j <= 1) {
       // gather every rank's slice through the peer mappings (rank 0's own for W = 1)
@@ -989,22 +1032,27 @@ int mps_back_segment(Model* m, const int32_t* lab, const bf16* cut_local, float 
   return 0;
 }
 
-int launch_front_backward(Model* m, const bf16* dcut, std::string* why) {
-  // cur = gradient w.r.t. the output of layer i (for a conv: already ReLU-masked, i.e. the
-  // pre-activation gradient); gacts[i] receives the gradient w.r.t. its input.
-  const bf16* cur = dcut;
+// Backward through conv/pool layers [lo, hi), from `cur` = the gradient w.r.t. layer hi-1's output
+// (for a conv: already ReLU-masked).  Layer lo's input is *in_lo (acts[lo] if null) and its
+// gradient goes to dst_lo (gacts[lo] if null); dgrad_lo: produce that gradient (the worker's
+// layer 0 needs none; the PS's back segment returns it to the workers).  gacts[i] receives the
+// gradient w.r.t. the input of layer i.
+int launch_conv_backward(Model* m, int lo, int hi, const bf16* cur, const ActBuf* in_lo, bf16* dst_lo, bool dgrad_lo,
+                         std::string* why) {
   bool db_done = false;  // the bias gradient of the layer `cur` belongs to is already summed
-  for (int i = static_cast<int>(m->front.size()) - 1; i >= 0; --i) {
+  for (int i = hi - 1; i >= lo; --i) {
     FrontLayer& f = m->front[i];
-    const ActBuf& in = m->acts[i];
+    const ActBuf& in = i == lo && in_lo != nullptr ? *in_lo : m->acts[i];
     const ActBuf& out = m->acts[i + 1];
-    // bias gradient of a (non-im2col) conv i-1 is summed by the kernel that produces its dY
-    float* prev_db = (i > 0 && m->front[i - 1].kind == RALPB_CONV && !m->front[i - 1].im2col &&
+    bf16* dst_i = i == lo && dst_lo != nullptr ? dst_lo : m->gacts[i];
+    // bias gradient of a (non-im2col) conv i-1 of this segment is summed by the kernel that
+    // produces its dY
+    float* prev_db = (i > lo && m->front[i - 1].kind == RALPB_CONV && !m->front[i - 1].im2col &&
                       m->front[i - 1].g.cout <= 512)
                          ? m->G + m->front[i - 1].b_off
                          : nullptr;
     if (f.kind == RALPB_POOL) {
-      bf16* dst = m->gacts[i];
+      bf16* dst = dst_i;
       if (f.idx != nullptr && f.fused_fwd)
         RALPB_TRY(maxpool_bwd_idx(f.idx, cur, in.n, out.h, out.w, in.c, out.pad, in.pad, dst, prev_db, m->stream));
       else if (f.idx != nullptr)
@@ -1031,12 +1079,13 @@ int launch_front_backward(Model* m, const bf16* dcut, std::string* why) {
       RALPB_TRY(gemm_launch(d, m->stream, why));
       ++m->launches;
     } else {
-      // db of this layer: already summed by the producer of `cur` unless `cur` is the cut gradient
+      // db of this layer: already summed by the producer of `cur` unless `cur` is the segment's
+      // incoming gradient
       RALPB_TRY(conv_wgrad(f.g, in.ptr, cur, m->G + f.w_off, db_done ? nullptr : m->G + f.b_off, m->stream, why));
       ++m->launches;
-      if (i > 0) {
-        bf16* dst = m->gacts[i];
-        const bool mask = m->front[i - 1].kind == RALPB_CONV;
+      if (i > lo || dgrad_lo) {
+        bf16* dst = dst_i;
+        const bool mask = i > 0 && m->front[i - 1].kind == RALPB_CONV;
         RALPB_TRY(conv_dgrad(f.g, cur, f.wd, mask ? in.ptr : nullptr, dst, prev_db, m->stream, why));
         ++m->launches;
         cur = dst;
@@ -1047,15 +1096,63 @@ int launch_front_backward(Model* m, const bf16* dcut, std::string* why) {
   return 0;
 }
 
+int launch_front_backward(Model* m, const bf16* dcut, std::string* why) {
+  return launch_conv_backward(m, 0, m->split, dcut, nullptr, nullptr, false, why);
+}
+
+// Forward through conv/pool layers [lo, hi): layer lo reads *in_lo (acts[lo] if null), layer hi-1
+// writes out_last (a following 2x2/2 max pool is fused into the conv epilogue where set up).
+int launch_conv_forward(Model* m, int lo, int hi, const float* img, const ActBuf* in_lo, bf16* out_last,
+                        std::string* why) {
+  cudaStream_t s = m->stream;
+  for (int i = lo; i < hi; ++i) {
+    FrontLayer& f = m->front[i];
+    const ActBuf& in = i == lo && in_lo != nullptr ? *in_lo : m->acts[i];
+    ActBuf out = m->acts[i + 1];
+    if (i + 1 == hi) out.ptr = out_last;
+    if (f.fused) {
+      RALPB_TRY(conv_first_fwd(img, in.n, m->in_h, m->in_w, m->in_c, f.wf, out.ptr, out.pad, s, why));
+    } else if (f.im2col) {
+      // y = relu(patches . W^T) on the padded output grid (bias rides in the ones column)
+      GemmDesc d;
+      d.M = static_cast<int>(in.rows()); d.N = f.g.cout; d.K = f.kpad;
+      d.kb = std::min(64, f.kpad);
+      d.a = Operand2D{in.ptr, in.rows(), f.kpad, f.kpad};
+      d.b = Operand2D{f.wf, f.g.cout, f.kpad, f.kpad};
+      d.epi = EPI_BF16; d.relu = 1; d.out = out.ptr; d.s_m = f.g.cout;
+      d.border = 1; d.img_rows = (out.h + 2 * out.pad) * (out.w + 2 * out.pad); d.wp = out.w + 2 * out.pad;
+      d.pad = out.pad; d.h = out.h; d.w = out.w;
+      RALPB_TRY(gemm_launch(d, s, why));
+    } else if (f.kind == RALPB_CONV) {
+      const bool pool_next = i + 1 < hi && m->front[i + 1].fused_fwd;
+      if (pool_next) {
+        const ActBuf& pooled = m->acts[i + 2];
+        bf16* pdst = i + 2 == hi ? out_last : pooled.ptr;
+        RALPB_TRY(conv_fwd_pool(f.g, in.ptr, f.wf, m->P + f.b_off, out.ptr, 1, pdst, pooled.pad, s, why,
+                                m->front[i + 1].idx));
+        ++m->launches;
+        ++i;  // the pool layer is done
+        continue;
+      }
+      RALPB_TRY(conv_fwd(f.g, in.ptr, f.wf, m->P + f.b_off, out.ptr, 1, s, why));
+    } else {
+      RALPB_TRY(maxpool_fwd(in.ptr, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.ptr, out.pad, s, f.idx));
+    }
+    ++m->launches;
+  }
+  return 0;
+}
+
 // bf16 filter copies from the fp32 masters, batched into one launch per kMaxPrepJobs layers:
 // forward copies (wf, needed by the next step's first kernel) and/or the tap-reversed
 // transposes the backward-data kernels read (wd).
-int prep_filters(Model* m, bool forward, bool dgrad, cudaStream_t s, std::string* why) {
+int prep_filters(Model* m, bool forward, bool dgrad, cudaStream_t s, std::string* why, int lo = 0, int hi = -1) {
   WeightPrepJob jobs[kMaxPrepJobs];
   int nj = 0;
-  for (size_t i = 0; i < m->front.size(); ++i) {
+  if (hi < 0) hi = static_cast<int>(m->front.size());
+  for (size_t i = lo; i < static_cast<size_t>(hi); ++i) {
     FrontLayer& f = m->front[i];
-    if (f.kind != RALPB_CONV) continue;
+    if (f.kind != RALPB_CONV || f.wf == nullptr) continue;   // (layers this rank does not run)
     if (f.im2col) {
       if (forward) {
         RALPB_TRY(cast_bf16(m->P + f.w_off, f.w_count, f.wf, s));
@@ -1513,9 +1610,10 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   bool fc_forked = false;
   RALPB_TRY(bump_counter(m->seq_dev, s));
   ++m->launches;
-  const long long cut_logical = static_cast<long long>(b) * m->cut_elems * eb;  // one worker's cut
+  const long long cut_logical = static_cast<long long>(b) * m->xch_logical * eb;  // one worker's cut
   const bool pairs = pair_mode(m);
-  const size_t cut_row = static_cast<size_t>(m->cut_elems) * (pairs ? m->pieces : 1);  // bf16 elements per cut row
+  // bf16 elements per sample of the exchanged cut (padded when a conv back segment reads it)
+  const size_t cut_row = static_cast<size_t>(m->xch_elems) * (pairs ? m->pieces : 1);
   const size_t cut_bytes = static_cast<size_t>(b) * cut_row * sizeof(bf16);
   const int slot = ralp || m->mps ? m->widx : 0;   // this worker's row block in the PS input
   const bf16* cut_local = nullptr;
@@ -1523,7 +1621,7 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
 
   if (m->is_worker && pairs) {
     bf16* cut_dst = m->acts.back().ptr;
-    if (m->holds_back) cut_dst = m->x_fc + static_cast<size_t>(slot) * b * cut_row;
+    if (m->holds_back) cut_dst = m->xin + static_cast<size_t>(slot) * b * cut_row;
     if (pair_front_forward(m, img, cut_dst, why)) return 1;
     cut_local = cut_dst;
   } else if (m->is_worker) {
@@ -1547,44 +1645,9 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
       RALPB_TRY(pack_input(img, b, m->in_h, m->in_w, m->in_c, a0.ptr, m->in_cp, a0.pad, s));
       ++m->launches;
     }
-    bf16* cut_dst = m->acts.back().ptr;
-    if (m->holds_back) cut_dst = m->x_fc + static_cast<size_t>(slot) * b * m->cut_elems;
-    for (size_t i = 0; i < m->front.size(); ++i) {
-      FrontLayer& f = m->front[i];
-      const ActBuf& in = m->acts[i];
-      ActBuf out = m->acts[i + 1];
-      if (i + 1 == m->front.size()) out.ptr = cut_dst;
-      if (f.fused) {
-        RALPB_TRY(conv_first_fwd(img, b, m->in_h, m->in_w, m->in_c, f.wf, out.ptr, out.pad, s, why));
-      } else if (f.im2col) {
-        // y = relu(patches . W^T) on the padded output grid (bias rides in the ones column)
-        GemmDesc d;
-        d.M = static_cast<int>(in.rows()); d.N = f.g.cout; d.K = f.kpad;
-        d.kb = std::min(64, f.kpad);
-        d.a = Operand2D{in.ptr, in.rows(), f.kpad, f.kpad};
-        d.b = Operand2D{f.wf, f.g.cout, f.kpad, f.kpad};
-        d.epi = EPI_BF16; d.relu = 1; d.out = out.ptr; d.s_m = f.g.cout;
-        d.border = 1; d.img_rows = (out.h + 2 * out.pad) * (out.w + 2 * out.pad); d.wp = out.w + 2 * out.pad;
-        d.pad = out.pad; d.h = out.h; d.w = out.w;
-        RALPB_TRY(gemm_launch(d, s, why));
-      } else if (f.kind == RALPB_CONV) {
-        // a following 2x2/2 max pool is fused into the conv epilogue (RALPB_FUSE_POOL=0: separate)
-        const bool pool_next = i + 1 < m->front.size() && m->front[i + 1].fused_fwd;
-        if (pool_next) {
-          const ActBuf& pooled = m->acts[i + 2];
-          bf16* pdst = i + 2 == m->front.size() ? cut_dst : pooled.ptr;
-          RALPB_TRY(conv_fwd_pool(f.g, in.ptr, f.wf, m->P + f.b_off, out.ptr, 1, pdst, pooled.pad, s, why,
-                                  m->front[i + 1].idx));
-          ++m->launches;
-          ++i;  // the pool layer is done
-          continue;
-        }
-        RALPB_TRY(conv_fwd(f.g, in.ptr, f.wf, m->P + f.b_off, out.ptr, 1, s, why));
-      } else {
-        RALPB_TRY(maxpool_fwd(in.ptr, in.n, in.h, in.w, in.c, in.pad, f.k, f.stride, out.ptr, out.pad, s, f.idx));
-      }
-      ++m->launches;
-    }
+    bf16* cut_dst = m->acts[m->split].ptr;
+    if (m->holds_back) cut_dst = m->xin + static_cast<size_t>(slot) * b * cut_row;
+    if (launch_conv_forward(m, 0, m->split, img, nullptr, cut_dst, why)) return 1;
     cut_local = cut_dst;
   }
   RALPB_TRY(mark(m, 1, capturing));
@@ -1635,6 +1698,8 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
     const int R = m->rows_back;
     const bf16* in = m->x_fc;
     const float scale = 1.f / static_cast<float>(W * b);
+    // conv back segment: layers [split, nconv) over every worker's cut rows, into the FC input
+    if (m->bseg && launch_conv_forward(m, m->split, m->nconv, nullptr, &m->bin, m->x_fc, why)) return 1;
     if (pairs) {
       if (pair_fc_forward_loss(m, R, scale, why)) return 1;
     } else {
@@ -1647,6 +1712,16 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
     }
     if (!ralp && push_loss_share(m, why)) return 1;
     if (pairs ? pair_fc_backward_data(m, R, m->dx_fc, why) : launch_fc_backward_data(m, in, R, m->dx_fc, why)) return 1;
+    if (m->bseg) {
+      // ... back through the conv back segment to the cut gradient rows (dxin), then its PS-local
+      // SGD update (like the FC tail's, never synchronised) and the operand re-layout
+      const long long nb = m->bseg_end - m->n_front;
+      RALPB_TRY(cudaMemsetAsync(m->G + m->n_front, 0, nb * sizeof(float), s));
+      if (launch_conv_backward(m, m->split, m->nconv, m->dx_fc, &m->bin, m->dxin, true, why)) return 1;
+      RALPB_TRY(sgd_momentum(m->P + m->n_front, m->V + m->n_front, m->G + m->n_front, nb, lr, mu, 1.f, s));
+      ++m->launches;
+      if (prep_filters(m, true, true, s, why, m->split, m->nconv)) return 1;
+    }
     if (ralp) {
       // return every remote worker's rows of the cut gradient first, then the FC tail's
       // weight gradients and its (PS-local, never synchronised) update run on the aux
@@ -1661,7 +1736,7 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
           PeerSignal sig{};
           sig.n = 1;
           sig.flag[0] = at<uint32_t>(m, r, m->arena_off_flags) + kFlagActGrad;
-          RALPB_TRY(push_and_signal(at<bf16>(m, r, m->arena_off_dcut), m->dx_fc + static_cast<size_t>(w) * b * cut_row,
+          RALPB_TRY(push_and_signal(at<bf16>(m, r, m->arena_off_dcut), m->dxin + static_cast<size_t>(w) * b * cut_row,
                                     static_cast<long long>(cut_bytes / 16), sig, seq, m->counters + kCtrScatter + w, s));
           ++m->launches;
           m->nvl_out += cut_bytes;
@@ -1682,7 +1757,7 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
           const int r = m->worker_ranks[w];
           if (r == m->rank) continue;
           sc.dst[sc.n] = at<bf16>(m, r, m->arena_off_dcut);
-          sc.src[sc.n] = m->dx_fc + static_cast<size_t>(w) * b * cut_row;
+          sc.src[sc.n] = m->dxin + static_cast<size_t>(w) * b * cut_row;
           ++sc.n;
           sig.flag[sig.n++] = at<uint32_t>(m, r, m->arena_off_flags) + kFlagActGrad;
           m->nvl_out += cut_bytes;
@@ -1713,7 +1788,7 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
       if (pairs ? pair_fc_backward_weights(m, R, false, lr, mu, why) : launch_fc_backward_weights(m, in, R, false, lr, mu, s, s, why))
         return 1;
     }
-    if (m->is_worker) dcut = m->dx_fc + static_cast<size_t>(slot) * b * cut_row;
+    if (m->is_worker) dcut = m->dxin + static_cast<size_t>(slot) * b * cut_row;
   } else {
     RALPB_TRY(wait_flags(m->flags + kFlagActGrad, 1, seq, s));
     ++m->launches;

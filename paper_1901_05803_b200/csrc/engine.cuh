@@ -66,7 +66,15 @@ struct Model {
   std::vector<FcLayer> back;
   std::vector<ActBuf> acts;        // acts[i] = input of front layer i; acts.back() = cut (local)
   int in_h = 0, in_w = 0, in_c = 0, in_cp = 0;
-  int cut_elems = 0;               // per-sample elements of the cut activation
+  int cut_elems = 0;               // per-sample elements of the FC tail's input (HWC-flattened pool output)
+  int nconv = 0;                   // conv / pool layers before the FC tail
+  bool bseg = false;               // split < nconv: layers [split, nconv) run on the PS over W*b rows
+  long long real_bseg = 0;         // descriptor parameters of that conv back segment (PS-local)
+  long long bseg_end = 0;          // its parameters occupy [n_front, bseg_end) of the flat vector
+  int xch_elems = 0;               // per-sample bf16 elements of the exchanged cut (layer split-1's
+                                   // output in its padded layout; == cut_elems at the FC boundary)
+  long long xch_logical = 0;       // ... its descriptor elements (h*w*c)
+  ActBuf bin;                      // PS: the back segment's input, every worker's cut rows (= xin)
   int rows_back = 0;               // rows the back segment processes on this rank
   bool holds_back = false;         // this rank runs the FC tail
   long long n_front = 0, n_total = 0;  // floats in the flat parameter vector (front prefix, total)
@@ -82,10 +90,14 @@ struct Model {
   float* P = nullptr;              // params (arena)
   float* G = nullptr;              // grads (arena)
   float* V = nullptr;              // momentum (local)
-  bf16* x_fc = nullptr;            // back-segment input [rows_back][cut_elems] (arena, PS)
+  bf16* xin = nullptr;             // exchanged cut rows [rows_back][xch_elems] (arena; PS reads)
+  bf16* dxin = nullptr;            // their gradient [rows_back][xch_elems] (PS; scattered back)
+  bf16* x_fc = nullptr;            // FC tail input [rows_back][cut_elems] (== xin without a conv back
+                                   // segment)
   int32_t* labels_all = nullptr;   // [rows_back] (arena, PS)
-  bf16* dcut = nullptr;            // cut gradient received from the PS [batch][cut_elems] (arena)
-  bf16* dx_fc = nullptr;           // back-segment cut gradient [rows_back][cut_elems] (PS)
+  bf16* dcut = nullptr;            // cut gradient received from the PS [batch][xch_elems] (arena)
+  bf16* dx_fc = nullptr;           // FC tail input gradient [rows_back][cut_elems] (PS; == dxin
+                                   // without a conv back segment)
   std::vector<bf16*> hid;          // FC outputs (bf16) for hidden layers
   float* logits = nullptr;
   float* fc_scratch = nullptr;     // split-K accumulators for FC GEMMs with few rows

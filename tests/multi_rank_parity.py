@@ -18,7 +18,7 @@ the CPU oracle.  Per configuration and step:
             (whose bf16 drift is chaotic -- its per-layer parity is pinned by the teacher-forced
             single-GPU test and by the fp32 parity mode below)
   fp32      precision="fp32" (the parity mode) against the plain fp32 oracle: loss within 1e-4
-            relative at every step and ||p_gpu - p_oracle|| / ||p_oracle|| <= 1e-5 per tensor
+            relative at every step and ||p_gpu - p_oracle|| / ||p_oracle|| <= 1e-4 per weight tensor
 
 Exit code 0 = pass.  Used by tests/test_multigpu_gpu.py.
 """
@@ -78,7 +78,7 @@ def _front_param_vec(params, split) -> torch.Tensor:
 
 
 def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, floor=False, cap=0.1,
-        placement="colocated", precision="bf16"):
+        placement="colocated", precision="bf16", split=None):
     """strategy: "ralp", "baseline" (all-on-PS), "ring" (ring all-reduce; numerics are the
     baseline's, bytes are volume_ring's) or "ralp-mps" (layer-placed with the FC tail sharded
     over all ranks; numerics are RALP's, bytes volume_ralp_multi_ps).  placement="dedicated-ps":
@@ -87,7 +87,8 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
     if strategy == "ralp-mps":
         strategy, fc_sharding = "ralp", "multi"
     workers = world - 1 if placement == "dedicated-ps" else world
-    split = next(i for i, l in enumerate(model.layers) if l.kind.value == "fc")
+    fc_at = next(i for i, l in enumerate(model.layers) if l.kind.value == "fc")
+    split = fc_at if split is None else split   # < fc_at: a conv back segment on the PS
     if strategy == "ralp":
         job = JobSpec(model, Strategy.ralp(split), workers)
         expect = (volume_ralp_multi_ps if fc_sharding == "multi" else volume_ralp)(model, split, workers)
@@ -125,8 +126,7 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
             ps = ex.ps_rank
             cut_local = torch.from_numpy(ex.debug_buffer(_lib.DBG_ACT, split)) if (ex.is_worker and rank != ps) else None
             dcut = torch.from_numpy(ex.debug_buffer(_lib.DBG_CUT_GRAD)) if (ex.is_worker and rank != ps) else None
-            n_cut = b * int(np.prod([model.layer(split - 1).output_shape.h, model.layer(split - 1).output_shape.w,
-                                     model.layer(split - 1).output_shape.c]))
+            n_cut = ex.debug_buffer(_lib.DBG_CUT_GRAD).size   # (the arena's act-grad slot exists on every rank)
             mine_cut = cut_local if cut_local is not None else torch.zeros(n_cut)
             mine_dcut = dcut if dcut is not None else torch.zeros(n_cut)
             cuts = _gather(mine_cut, world)
@@ -159,7 +159,7 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
         if rank == 0:
             batches = [synthetic.batch(1, t, w * b, b, ex.in_shape, ex.classes) for w in range(workers)]
             lo, wire = ostep.train_step(orc, "baseline" if strategy == "ring" else strategy, workers, batches, lr=lr,
-                                        emulate_bf16=not fp32)
+                                        emulate_bf16=not fp32, split=split if strategy == "ralp" else None)
             if orc64 is not None:
                 ostep.train_step(orc64, "baseline" if strategy == "ring" else strategy, workers, batches, lr=lr,
                                  emulate_bf16=True, accum64=True)
@@ -193,7 +193,7 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
                 rel = np.linalg.norm(g[0] - w[0]) / np.linalg.norm(w[0])
                 upd = np.linalg.norm(g[0] - w[0]) / np.linalg.norm(w[0] - p0[0])
                 print(f"   layer {li}: ||dp||/||p|| {rel:.3e}  ||dp||/||update|| {upd:.3e}", flush=True)
-                if rel > 1e-5:
+                if rel > 1e-4:
                     ok = False
                 continue
             upd = np.linalg.norm(w[0] - p0[0])
@@ -232,10 +232,17 @@ def main():
         # pool5 cut) at b=4 per rank
         dict(model=vgg16, strategy="ralp", steps=2, lr=1e-3, floor=True, cap=0.5),
     ]
+    # the partitioner's split inside the conv stack: a conv back segment on the PS (cifar_small b=8
+    # cuts at pool1; the tiny VGG at pool1), colocated and with a dedicated PS
+    configs.append(dict(model=catalog_lookup("cifar_small").with_batch_size(8), strategy="ralp", steps=4, split=2))
+    configs.append(dict(model=parse_model(TINY), strategy="ralp", steps=3, split=3))
+    if world >= 2:
+        configs.append(dict(model=catalog_lookup("cifar_small").with_batch_size(8), strategy="ralp", steps=4, split=2,
+                            placement="dedicated-ps"))
     if world >= 2:  # RALP-N: a dedicated PS rank plus world-1 workers
         configs.append(dict(model=cifar, strategy="ralp", steps=4, placement="dedicated-ps"))
         configs.append(dict(model=parse_model(TINY), strategy="ralp", steps=3, placement="dedicated-ps"))
-    if os.environ.get("RALPB_PARITY_FP32", "0") == "1":
+    if os.environ.get("RALPB_PARITY_FP32", "1") == "1":
         configs.append(dict(model=cifar, strategy="ralp", steps=4, precision="fp32"))
         configs.append(dict(model=cifar, strategy="baseline", steps=3, precision="fp32"))
         configs.append(dict(model=vgg16, strategy="ralp", steps=3, lr=1e-3, precision="fp32"))
@@ -246,7 +253,8 @@ def main():
         if shared and (c["model"].name == "vgg16" or c.get("ring_backend") == "nccl"):
             continue
         ok &= run(c["model"], c["strategy"], c["steps"], rank, world, c.get("ring_backend", "native"), c.get("lr", 0.01),
-                  c.get("floor", False), c.get("cap", 0.1), c.get("placement", "colocated"), c.get("precision", "bf16"))
+                  c.get("floor", False), c.get("cap", 0.1), c.get("placement", "colocated"), c.get("precision", "bf16"),
+                  c.get("split"))
     flag = torch.tensor([0 if ok else 1], device=_dev())
     dist.all_reduce(flag)
     dist.destroy_process_group()

@@ -12,7 +12,8 @@ pipeline's own noise floor, measured every time by re-running the oracle with
 float64 accumulation:
   floor(layer) = ||p_oracle64 - p_oracle32|| / ||p_oracle32 - p_init||
   dev(layer)   = ||p_gpu      - p_oracle32|| / ||p_oracle32 - p_init||
-  require dev <= 4 * floor + 0.02 for every parameter tensor after N steps,
+  require dev <= min(4 * floor + 0.02, cap) for every parameter tensor after N steps (cap 0.1;
+  0.5 for the 16-layer VGG-16, whose per-layer parity the teacher-forced headline test pins),
   and |loss_gpu - loss_oracle| <= 2e-3 * |loss_oracle| at every step.
 (The B200's tensor-core fp32 accumulation truncates per MMA, so its noise is
 larger than CPU fp32's; the factor 4 covers that, and a real bug shows up as
@@ -54,9 +55,13 @@ def _fc_boundary(model):
     return next(i for i, l in enumerate(model.layers) if l.kind.value == "fc")
 
 
-def _run(model, strategy, steps, seed=0, lr=0.01):
+def _run(model, strategy, steps, seed=0, lr=0.01, split=None):
+    """split (RALP): None = the FC-tail cut (the partitioner's choice at large batch); otherwise
+    the partitioner's own split, which may leave conv / pool layers in the back segment (run on
+    the PS over the gathered rows)."""
+    wire_split = split
     if strategy == "ralp":
-        split = _fc_boundary(model)  # the FC-tail cut (the partitioner's choice at large batch)
+        split = _fc_boundary(model) if split is None else split
         job = JobSpec(model, Strategy.ralp(split), 1)
         expect_bytes = volume_ralp(model, split, 1).total_bytes_per_step
     else:
@@ -73,7 +78,8 @@ def _run(model, strategy, steps, seed=0, lr=0.01):
         imgs, labs = synthetic.batch(seed, t, 0, b, ex.in_shape, ex.classes)
         ex.step(imgs, labs, lr=lr, momentum=0.9)
         st = ex.stats()
-        loss_o, wire = ostep.train_step(o32, strategy, 1, [(imgs, labs)], lr=lr, mu=0.9, emulate_bf16=True)
+        loss_o, wire = ostep.train_step(o32, strategy, 1, [(imgs, labs)], lr=lr, mu=0.9, emulate_bf16=True,
+                                        split=wire_split)
         ostep.train_step(o64, strategy, 1, [(imgs, labs)], lr=lr, mu=0.9, emulate_bf16=True, accum64=True)
         assert st.logical_bytes == wire == expect_bytes
         losses.append((st.loss, loss_o))
@@ -82,7 +88,7 @@ def _run(model, strategy, steps, seed=0, lr=0.01):
     return losses, got, o32.numpy_params(), o64.numpy_params(), params
 
 
-def _check(losses, got, want, want64, init):
+def _check(losses, got, want, want64, init, cap=0.1):
     bad = []
     for i, (lg, lo) in enumerate(losses):
         print(f"  step {i}: loss gpu {lg:.6f} oracle {lo:.6f}")
@@ -96,8 +102,9 @@ def _check(losses, got, want, want64, init):
             dev = np.linalg.norm(a - o) / upd
             floor = np.linalg.norm(o64 - o) / upd
             print(f"  layer {li}.{nm}: dev {dev:.3e} floor {floor:.3e}")
-            if dev > 4 * floor + 0.02:
-                bad.append(f"layer {li}.{nm}: dev {dev:.3e} > 4 * floor {floor:.3e} + 0.02")
+            bound = min(4 * floor + 0.02, cap)
+            if dev > bound:
+                bad.append(f"layer {li}.{nm}: dev {dev:.3e} > min(4 * floor {floor:.3e} + 0.02, {cap})")
     assert not bad, "\n".join(bad)
 
 
@@ -125,7 +132,7 @@ def test_vgg16_one_step_b4():
     model = catalog_lookup("vgg16").with_batch_size(4)
     losses, got, want, want64, init = _run(model, "baseline", steps=1)
     print("vgg16 b=4", losses)
-    _check(losses, got, want, want64, init)
+    _check(losses, got, want, want64, init, cap=0.5)
 
 
 def test_alexnet_steps_b4():
@@ -159,3 +166,21 @@ def test_pipelined_host_inputs_and_async_loss():
         ex.close()
         losses.append(got)
     np.testing.assert_allclose(losses[1], losses[0], rtol=1e-3)
+
+
+@pytest.mark.parametrize("name,batch,split,steps,lr,cap", [
+    ("cifar_small", 8, 2, 4, 0.01, 0.1),     # pool1 | conv2, pool2, fc1, fc2 on the PS
+    ("vgg_tiny", 8, 3, 3, 0.01, 0.1),        # pool1 | conv3..pool4 + FC tail on the PS
+    ("vgg16", 4, 6, 1, 1e-3, 0.5),           # pool2 | conv3_1..pool5 + FC tail (VGG-16 at b=4)
+    ("alexnet", 4, 2, 2, 1e-3, 0.1),         # pool1 | conv2 (5x5)..pool5 + FC tail
+])
+def test_partitioner_split_conv_back_segment(name, batch, split, steps, lr, cap):
+    """The partitioner's own split at small batch cuts inside the conv stack (profiler.py:101-134):
+    the back segment's conv / pool layers run on the PS over the gathered cut rows, the act-grad
+    returned is the gradient w.r.t. that intermediate feature map, and only the front before the
+    cut is synchronised (volume_ralp(m, split, W) bytes)."""
+    model = (parse_model(VGG_TINY) if name == "vgg_tiny" else catalog_lookup(name)).with_batch_size(batch)
+    assert profile(model).split_index == split
+    losses, got, want, want64, init = _run(model, "ralp", steps=steps, lr=lr, split=split)
+    print(name, batch, "split", split, losses)
+    _check(losses, got, want, want64, init, cap=cap)
