@@ -1,5 +1,11 @@
 """Print the key counters of every kernel in an ncu report (run here, no GPU needed).
 
+Tensor-pipe utilisation of the tcgen05 kernels: ncu 2025 on sm_100a reports the legacy
+`sm__pipe_tensor_cycles_active_realtime...pct` near 0 for UTC*MMA work (it normalises a per-SMSP
+realtime count by the wrong peak); `sm__mem_tensor_cycles_active` (= the hmma-subpipe realtime
+cycles / 4 SMSPs / elapsed SM cycles, checked on the conv13 backward-filter capture: 148.8k of
+187.2k cycles) is the consistent one and is what is printed.
+
 usage: python tools/ncu_summary.py report.ncu-rep > summary.txt
 """
 import csv
@@ -13,7 +19,9 @@ KEYS = [
     ("gpc__cycles_elapsed.max.per_second", "SM clock"),
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
-    ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor pipe active %"),
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe active % (tcgen05)"),
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe active % of active"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
     ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem->tensor-core pipe %"),
     ("l1tex__data_bank_reads.avg.pct_of_peak_sustained_elapsed", "smem bank reads %"),
     ("lts__t_bytes.sum", "L2 bytes"),
