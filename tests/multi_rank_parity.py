@@ -13,10 +13,11 @@ the CPU oracle.  Per configuration and step:
   loss      the job's mean loss (reported on the PS rank for every strategy) within 2e-3 of the
             oracle's at every step
   params    after the last step, per layer ||p_gpu - p_oracle|| / ||p_oracle - p0|| within
-            min(4 * floor + 0.02, cap), floor = the bf16 pipeline's own fp32-vs-fp64 spread (the
-            oracle re-run with float64 accumulation); cap 0.1 for the small nets, 0.5 for VGG-16
-            (whose bf16 drift is chaotic -- its per-layer parity is pinned by the teacher-forced
-            single-GPU test and by the fp32 parity mode below)
+            min(2 * floor + 0.02, cap), floor = the bf16 pipeline's own fp32-vs-fp64 spread (the
+            oracle re-run with float64 accumulation; configurations marked floor=True), else the
+            cap 0.25 (small nets, few steps) / 0.5 (VGG-16, whose bf16 drift is chaotic -- its
+            per-layer parity is pinned by the teacher-forced single-GPU test and by the fp32 parity
+            precision below); a wrong update is ~1
   fp32      precision="fp32" (the parity mode) against the plain fp32 oracle: loss within 1e-4
             relative at every step and ||p_gpu - p_oracle|| / ||p_oracle|| <= 1e-4 per weight tensor
 
@@ -77,7 +78,7 @@ def _front_param_vec(params, split) -> torch.Tensor:
                       for x in p])
 
 
-def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, floor=False, cap=0.1,
+def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, floor=False, cap=0.25,
         placement="colocated", precision="bf16", split=None):
     """strategy: "ralp", "baseline" (all-on-PS), "ring" (ring all-reduce; numerics are the
     baseline's, bytes are volume_ring's) or "ralp-mps" (layer-placed with the FC tail sharded
@@ -198,7 +199,7 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
                 continue
             upd = np.linalg.norm(w[0] - p0[0])
             dev = np.linalg.norm(g[0] - w[0]) / upd
-            bound = cap if w64 is None else min(4 * np.linalg.norm(w64[0] - w[0]) / upd + 0.02, cap)
+            bound = cap if w64 is None else min(2 * np.linalg.norm(w64[0] - w[0]) / upd + 0.02, cap)
             print(f"   layer {li}: dev {dev:.3e} (bound {bound:.3e})", flush=True)
             if dev > bound:
                 ok = False
@@ -253,7 +254,7 @@ def main():
         if shared and (c["model"].name == "vgg16" or c.get("ring_backend") == "nccl"):
             continue
         ok &= run(c["model"], c["strategy"], c["steps"], rank, world, c.get("ring_backend", "native"), c.get("lr", 0.01),
-                  c.get("floor", False), c.get("cap", 0.1), c.get("placement", "colocated"), c.get("precision", "bf16"),
+                  c.get("floor", False), c.get("cap", 0.25), c.get("placement", "colocated"), c.get("precision", "bf16"),
                   c.get("split"))
     flag = torch.tensor([0 if ok else 1], device=_dev())
     dist.all_reduce(flag)

@@ -12,8 +12,11 @@ pipeline's own noise floor, measured every time by re-running the oracle with
 float64 accumulation:
   floor(layer) = ||p_oracle64 - p_oracle32|| / ||p_oracle32 - p_init||
   dev(layer)   = ||p_gpu      - p_oracle32|| / ||p_oracle32 - p_init||
-  require dev <= min(4 * floor + 0.02, cap) for every parameter tensor after N steps (cap 0.1;
-  0.5 for the 16-layer VGG-16, whose per-layer parity the teacher-forced headline test pins),
+  require dev <= min(2 * floor + 0.02, 0.5) for every parameter tensor after N steps: a wrong
+  update (a lost gradient, a missing momentum term) is dev ~ 1; the deep nets' floor itself
+  reaches 0.1-0.35 (bf16 re-rounding flips ReLU / max-pool decisions), so the per-kernel parity
+  is pinned sharply elsewhere -- by the teacher-forced headline test (tests/test_headline_parity_gpu.py)
+  and the fp32 parity precision (tests/test_parity_fp32_gpu.py),
   and |loss_gpu - loss_oracle| <= 2e-3 * |loss_oracle| at every step.
 (The B200's tensor-core fp32 accumulation truncates per MMA, so its noise is
 larger than CPU fp32's; the factor 4 covers that, and a real bug shows up as
@@ -88,7 +91,7 @@ def _run(model, strategy, steps, seed=0, lr=0.01, split=None):
     return losses, got, o32.numpy_params(), o64.numpy_params(), params
 
 
-def _check(losses, got, want, want64, init, cap=0.1):
+def _check(losses, got, want, want64, init, cap=0.5):
     bad = []
     for i, (lg, lo) in enumerate(losses):
         print(f"  step {i}: loss gpu {lg:.6f} oracle {lo:.6f}")
@@ -102,9 +105,9 @@ def _check(losses, got, want, want64, init, cap=0.1):
             dev = np.linalg.norm(a - o) / upd
             floor = np.linalg.norm(o64 - o) / upd
             print(f"  layer {li}.{nm}: dev {dev:.3e} floor {floor:.3e}")
-            bound = min(4 * floor + 0.02, cap)
+            bound = min(2 * floor + 0.02, cap)
             if dev > bound:
-                bad.append(f"layer {li}.{nm}: dev {dev:.3e} > min(4 * floor {floor:.3e} + 0.02, {cap})")
+                bad.append(f"layer {li}.{nm}: dev {dev:.3e} > min(2 * floor {floor:.3e} + 0.02, {cap})")
     assert not bad, "\n".join(bad)
 
 
@@ -132,7 +135,7 @@ def test_vgg16_one_step_b4():
     model = catalog_lookup("vgg16").with_batch_size(4)
     losses, got, want, want64, init = _run(model, "baseline", steps=1)
     print("vgg16 b=4", losses)
-    _check(losses, got, want, want64, init, cap=0.5)
+    _check(losses, got, want, want64, init)
 
 
 def test_alexnet_steps_b4():
@@ -168,13 +171,13 @@ def test_pipelined_host_inputs_and_async_loss():
     np.testing.assert_allclose(losses[1], losses[0], rtol=1e-3)
 
 
-@pytest.mark.parametrize("name,batch,split,steps,lr,cap", [
-    ("cifar_small", 8, 2, 4, 0.01, 0.1),     # pool1 | conv2, pool2, fc1, fc2 on the PS
-    ("vgg_tiny", 8, 3, 3, 0.01, 0.1),        # pool1 | conv3..pool4 + FC tail on the PS
-    ("vgg16", 4, 6, 1, 1e-3, 0.5),           # pool2 | conv3_1..pool5 + FC tail (VGG-16 at b=4)
-    ("alexnet", 4, 2, 2, 1e-3, 0.1),         # pool1 | conv2 (5x5)..pool5 + FC tail
+@pytest.mark.parametrize("name,batch,split,steps,lr", [
+    ("cifar_small", 8, 2, 4, 0.01),     # pool1 | conv2, pool2, fc1, fc2 on the PS
+    ("vgg_tiny", 8, 3, 3, 0.01),        # pool1 | conv3..pool4 + FC tail on the PS
+    ("vgg16", 4, 6, 1, 1e-3),           # pool2 | conv3_1..pool5 + FC tail (VGG-16 at b=4)
+    ("alexnet", 4, 2, 2, 1e-3),         # pool1 | conv2 (5x5)..pool5 + FC tail
 ])
-def test_partitioner_split_conv_back_segment(name, batch, split, steps, lr, cap):
+def test_partitioner_split_conv_back_segment(name, batch, split, steps, lr):
     """The partitioner's own split at small batch cuts inside the conv stack (profiler.py:101-134):
     the back segment's conv / pool layers run on the PS over the gathered cut rows, the act-grad
     returned is the gradient w.r.t. that intermediate feature map, and only the front before the
@@ -183,4 +186,4 @@ def test_partitioner_split_conv_back_segment(name, batch, split, steps, lr, cap)
     assert profile(model).split_index == split
     losses, got, want, want64, init = _run(model, "ralp", steps=steps, lr=lr, split=split)
     print(name, batch, "split", split, losses)
-    _check(losses, got, want, want64, init, cap=cap)
+    _check(losses, got, want, want64, init)
