@@ -372,6 +372,7 @@ def run_ours(args):
     exb, jobb, _ = _build_executor("baseline", world, rank)
     ms_b = _time_steps(exb, dimgs, dlabs, args.steps, args.warmup, world)
     stb = exb.stats()
+    bytes_b = _job_bytes(stb, world)   # (a collective: every rank, outside the rank-0 block)
     exb.close()
     # ring all-reduce comparators (StrategyKind.RING_ALLREDUCE, the Horovod baseline of the paper):
     # the hand-written NVLink RS+SGD+AG vs NCCL all_reduce of the gradient vector (N > 1)
@@ -447,7 +448,7 @@ def run_ours(args):
                                     "logical_counted_rank0": st.logical_bytes,
                                     "physical_nvlink_rank0": {"out": nvl[0], "in": nvl[1]}},
             "all_on_ps": {"value": world * BATCH / (ms_b * 1e-3), "ms_per_step": ms_b,
-                          "logical_sync_bytes_per_step": _job_bytes(stb, world)},
+                          "logical_sync_bytes_per_step": bytes_b},
             "ring_allreduce": ring,
             "ralp_fc_sharded": mps,
             "ralp_dedicated_ps": ralp_n,

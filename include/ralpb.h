@@ -126,7 +126,10 @@ int ralpb_cast_bf16(const float* x, long long n, void* y, void* stream);
  * (profiler.py:101-134,187-227); the strategy mirrors StrategyKind
  * (costmodel.py:34-37): RALP = conv front replicated + FC tail on the PS rank,
  * BASELINE_PS = every layer on every worker, all parameters through the PS. */
-enum { RALPB_CONV = 0, RALPB_POOL = 1, RALPB_FC = 2 };
+/* Layer kinds.  BLOCK: a ResNet bottleneck block (1x1 -> 3x3 (stride) -> 1x1, batch norm after
+ * every convolution, ReLU, identity or 1x1-projection shortcut; the catalog's linearised
+ * s?b?_{a,b,c,down} entries, pkg/tools/build_catalog.py:286-333).  APOOL: global average pool. */
+enum { RALPB_CONV = 0, RALPB_POOL = 1, RALPB_FC = 2, RALPB_BLOCK = 3, RALPB_APOOL = 4 };
 /* BASELINE: StrategyKind.BASELINE_PS (every layer on every worker, all parameters through the
  * sharded PS).  RALP: StrategyKind.RALP.  RING: StrategyKind.RING_ALLREDUCE (simulator.py:719-737)
  * with the hand-written reduce-scatter + SGD + all-gather over NVLink; RING_EXTERNAL: the same
@@ -140,11 +143,15 @@ enum { RALPB_STRATEGY_BASELINE = 0, RALPB_STRATEGY_RALP = 1, RALPB_STRATEGY_RING
        RALPB_STRATEGY_RALP_MPS = 4 };
 
 typedef struct {
-  int kind;            /* RALPB_CONV / RALPB_POOL / RALPB_FC */
-  int k, stride, pad;  /* window geometry (conv / pool) */
+  int kind;            /* RALPB_CONV / RALPB_POOL / RALPB_FC / RALPB_BLOCK / RALPB_APOOL */
+  int k, stride, pad;  /* window geometry (conv / pool; block: stride of its 3x3 convolution) */
   int h, w, cin;       /* per-sample input shape (fc: cin = input features, h = w = 0) */
-  int cout;            /* conv output channels / fc output features */
+  int cout;            /* conv / block output channels, fc output features */
   int relu;            /* ReLU after the layer (conv, fc except the last) */
+  int bn;              /* conv: batch norm (training-mode batch statistics, scale + shift) before
+                          the ReLU, no bias */
+  int width;           /* block: bottleneck width (the 1x1 / 3x3 convolutions' channels) */
+  int downsample;      /* block: 1x1 projection shortcut (else identity) */
 } ralpb_layer_desc;
 
 typedef struct {
@@ -192,7 +199,11 @@ void ralpb_model_destroy(ralpb_model* m);
 int ralpb_model_ipc_handle(ralpb_model* m, void* out64);
 int ralpb_model_ipc_open(ralpb_model* m, const void* handles);
 /* Host (on_host=1) or device fp32 parameters of layer `layer` (0-based):
- * conv w [cout][k][k][cin], b [cout]; fc w [out][in] (in = HWC-flattened), b [out]. */
+ * conv w [cout][k][k][cin], b [cout] (bn conv: b = [gamma (cout) | beta (cout)]);
+ * fc w [out][in] (in = HWC-flattened), b [out];
+ * block: w = every parameter of the block, in order wa [width][cin], wb [width][3][3][width],
+ * wc [cout][width] (, wd [cout][cin]), b = [gamma_a | beta_a | gamma_b | beta_b | gamma_c | beta_c
+ * (| gamma_d | beta_d)]. */
 int ralpb_model_set_params(ralpb_model* m, int layer, const float* w, const float* b, int on_host);
 int ralpb_model_get_params(ralpb_model* m, int layer, float* w, float* b, int on_host);
 /* This rank's parameter gradient of `layer` from the last step (same layout as get_params; host or
@@ -222,13 +233,17 @@ void* ralpb_model_stream(ralpb_model* m);
  *   FC_OUT i             bf16 [rows][ld] output of hidden FC layer i (ReLU applied)
  *   FC_OUT_GRAD i        bf16 [rows][ld] gradient w.r.t. FC layer i's output (ReLU-masked)
  *   FC_WEIGHT i          bf16 [out][in] operand copy of FC layer i
- *   CUT_ROWS / CUT_GRAD_ROWS  bf16 [rows][cut] the PS's FC input rows (every worker's cut, HWC
+ *   CUT_ROWS / CUT_GRAD_ROWS  bf16 [rows][cut] the PS's exchanged cut rows (every worker's cut --
+ *                        layer split-1's output in its padded layout; at the FC boundary the HWC
  *                        flatten) / their gradient;  CUT_GRAD  bf16 [b][cut] the act-grad this rank
- *                        received;  MPS_PARTIAL  fp32 [rows][ld] (RALP_MPS) */
+ *                        received;  FC_IN / FC_IN_GRAD  bf16 [rows][fc_in] the FC tail's input rows /
+ *                        their gradient (== CUT_ROWS / CUT_GRAD_ROWS without a conv back segment);
+ *                        MPS_PARTIAL  fp32 [rows][ld] (RALP_MPS) */
 enum {
   RALPB_DBG_ACT = 0, RALPB_DBG_ACT_GRAD = 1, RALPB_DBG_LOGITS = 2, RALPB_DBG_FC_OUT = 3,
   RALPB_DBG_MPS_PARTIAL = 4, RALPB_DBG_FC_WEIGHT = 5, RALPB_DBG_DLOGITS = 6, RALPB_DBG_FC_OUT_GRAD = 7,
-  RALPB_DBG_CUT_ROWS = 8, RALPB_DBG_CUT_GRAD_ROWS = 9, RALPB_DBG_CUT_GRAD = 10
+  RALPB_DBG_CUT_ROWS = 8, RALPB_DBG_CUT_GRAD_ROWS = 9, RALPB_DBG_CUT_GRAD = 10, RALPB_DBG_FC_IN = 11,
+  RALPB_DBG_FC_IN_GRAD = 12
 };
 long long ralpb_model_debug_buffer(ralpb_model* m, int i, int which, void* host_out);
 /* RING_EXTERNAL: the fp32 gradient vector (all parameters, device memory, `*n` floats) the caller

@@ -68,7 +68,7 @@ SIGNATURES: dict[str, tuple] = {
 class LayerDesc(C.Structure):
     """ralpb_layer_desc (include/ralpb.h)."""
     _fields_ = [("kind", c_i), ("k", c_i), ("stride", c_i), ("pad", c_i), ("h", c_i), ("w", c_i),
-                ("cin", c_i), ("cout", c_i), ("relu", c_i)]
+                ("cin", c_i), ("cout", c_i), ("relu", c_i), ("bn", c_i), ("width", c_i), ("downsample", c_i)]
 
 
 class LaunchRec(C.Structure):
@@ -89,14 +89,14 @@ class StepStats(C.Structure):
                 ("nvlink_in_bytes", c_ll)]
 
 
-RALPB_CONV, RALPB_POOL, RALPB_FC = 0, 1, 2
+RALPB_CONV, RALPB_POOL, RALPB_FC, RALPB_BLOCK, RALPB_APOOL = 0, 1, 2, 3, 4
 RALPB_STRATEGY_BASELINE, RALPB_STRATEGY_RALP, RALPB_STRATEGY_RING, RALPB_STRATEGY_RING_EXTERNAL = 0, 1, 2, 3
 RALPB_STRATEGY_RALP_MPS = 4
 RALPB_PRECISION_BF16, RALPB_PRECISION_FP32 = 0, 1
 PRECISIONS = {"bf16": RALPB_PRECISION_BF16, "fp32": RALPB_PRECISION_FP32}
 # ralpb_model_debug_buffer selectors (include/ralpb.h)
 (DBG_ACT, DBG_ACT_GRAD, DBG_LOGITS, DBG_FC_OUT, DBG_MPS_PARTIAL, DBG_FC_WEIGHT, DBG_DLOGITS, DBG_FC_OUT_GRAD,
- DBG_CUT_ROWS, DBG_CUT_GRAD_ROWS, DBG_CUT_GRAD) = range(11)
+ DBG_CUT_ROWS, DBG_CUT_GRAD_ROWS, DBG_CUT_GRAD, DBG_FC_IN, DBG_FC_IN_GRAD) = range(13)
 
 
 class BackendError(RuntimeError):

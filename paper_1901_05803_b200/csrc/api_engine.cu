@@ -142,17 +142,25 @@ extern "C" long long ralpb_model_debug_buffer(ralpb_model* m, int i, int which, 
       n = static_cast<long long>(R) * mm->back[i].ld_out;
       src = mm->dyb[i];
       break;
-    case RALPB_DBG_CUT_ROWS:
+    case RALPB_DBG_CUT_ROWS:   // the exchanged cut rows (layer split-1's output, padded layout)
+      n = static_cast<long long>(R) * mm->xch_elems;
+      src = mm->xin;
+      break;
+    case RALPB_DBG_CUT_GRAD_ROWS:
+      n = static_cast<long long>(R) * mm->xch_elems;
+      src = mm->dxin;
+      break;
+    case RALPB_DBG_CUT_GRAD:
+      n = static_cast<long long>(mm->batch) * mm->xch_elems;
+      src = mm->dcut;
+      break;
+    case RALPB_DBG_FC_IN:      // the FC tail's input rows (== CUT_ROWS without a conv back segment)
       n = static_cast<long long>(R) * mm->cut_elems;
       src = mm->x_fc;
       break;
-    case RALPB_DBG_CUT_GRAD_ROWS:
+    case RALPB_DBG_FC_IN_GRAD:
       n = static_cast<long long>(R) * mm->cut_elems;
       src = mm->dx_fc;
-      break;
-    case RALPB_DBG_CUT_GRAD:
-      n = static_cast<long long>(mm->batch) * mm->cut_elems;
-      src = mm->dcut;
       break;
     default:
       return -1;

@@ -29,6 +29,8 @@
 #include "engine.cuh"
 #include "gemm_host.cuh"
 #include "pair.cuh"
+#include "block.cuh"
+#include "resnet.cuh"
 
 namespace ralpb {
 
@@ -203,10 +205,26 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
       f.w_count = static_cast<long long>(d.cout) * f.kpad;
       f.w_off = off;
       f.b_off = -1;  // folded into column k*k*cin of the filter
-      for (int oc = 0; oc < d.cout; ++oc)
-        real_runs.emplace_back(f.w_off + static_cast<long long>(oc) * f.kpad, d.k * d.k * d.cin + 1);
-      off = align_up(off + f.w_count, 4);
-      m->real_front += static_cast<long long>(d.cout) * d.k * d.k * d.cin + d.cout;
+      f.bn = d.bn != 0;
+      if (f.bn) {
+        // batch-normalised stem (ResNet): no bias -- the patch rows carry no ones column -- and
+        // gamma / beta after the filter
+        if (precision != RALPB_PRECISION_BF16 || f.fused) return fail("a batch-normalised first conv runs as a bf16 im2col GEMM");
+        if (in.pad != 0) return fail("a batch-normalised first conv must feed a pool or block");
+        for (int oc = 0; oc < d.cout; ++oc)
+          real_runs.emplace_back(f.w_off + static_cast<long long>(oc) * f.kpad, d.k * d.k * d.cin);
+        off = align_up(off + f.w_count, 4);
+        f.b_off = off;
+        real_runs.emplace_back(f.b_off, 2LL * d.cout);
+        off = align_up(off + 2LL * d.cout, 4);
+        m->real_front += static_cast<long long>(d.cout) * d.k * d.k * d.cin + 2LL * d.cout;
+        m->branchy = true;
+      } else {
+        for (int oc = 0; oc < d.cout; ++oc)
+          real_runs.emplace_back(f.w_off + static_cast<long long>(oc) * f.kpad, d.k * d.k * d.cin + 1);
+        off = align_up(off + f.w_count, 4);
+        m->real_front += static_cast<long long>(d.cout) * d.k * d.k * d.cin + d.cout;
+      }
       o.h = in.h; o.w = in.w; o.c = d.cout; o.pad = in.pad;
       m->front.push_back(f);
       m->acts.push_back(o);
@@ -240,11 +258,54 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     } else if (d.kind == RALPB_POOL) {
       f.k = d.k;
       f.stride = d.stride > 0 ? d.stride : d.k;
-      o.h = (d.h - f.k) / f.stride + 1;
-      o.w = (d.w - f.k) / f.stride + 1;
+      f.pool_pad = d.pad;
+      if (d.pad > 0 && (in.pad != 0 || precision != RALPB_PRECISION_BF16))
+        return fail("a padded pool reads an unpadded bf16 activation");
+      o.h = (d.h + 2 * d.pad - f.k) / f.stride + 1;
+      o.w = (d.w + 2 * d.pad - f.k) / f.stride + 1;
       o.c = in.c;
       o.pad = (i + 1 < nconv && layers[i + 1].kind == RALPB_CONV) ? layers[i + 1].pad : 0;
       if (in.c % 8 != 0) return fail("pool channels must be a multiple of 8");
+    } else if (d.kind == RALPB_BLOCK || d.kind == RALPB_APOOL) {
+      if (precision != RALPB_PRECISION_BF16) return fail("bottleneck blocks run in bf16 precision");
+      if (in.pad != 0) return fail("layer " + std::to_string(i) + ": a block / average pool reads an unpadded activation");
+      m->branchy = true;
+      if (d.kind == RALPB_APOOL) {
+        f.k = d.h;
+        o.h = 1; o.w = 1; o.c = in.c; o.pad = 0;
+      } else {
+        if (d.stride != 1 && d.stride != 2) return fail("block stride must be 1 or 2");
+        if (d.width % 64 != 0 || d.cout % 64 != 0 || in.c % 64 != 0) return fail("block channels must be multiples of 64");
+        if (!d.downsample && (d.stride != 1 || d.cin != d.cout)) return fail("an identity shortcut needs stride 1 and cin == cout");
+        BlockBufs k;
+        k.cin = in.c; k.width = d.width; k.cout = d.cout; k.stride = d.stride; k.down = d.downsample;
+        k.n = nb; k.h = d.h; k.w = d.w; k.ho = d.h / d.stride; k.wo = d.w / d.stride;
+        auto take_params = [&](long long count) { const long long o2 = off; off = align_up(off + count, 4); return o2; };
+        k.wa_off = take_params(static_cast<long long>(k.width) * k.cin);
+        k.ga_off = take_params(2LL * k.width);
+        k.wb_off = take_params(9LL * k.width * k.width);
+        k.gb_off = take_params(2LL * k.width);
+        k.wc_off = take_params(static_cast<long long>(k.cout) * k.width);
+        k.gc_off = take_params(2LL * k.cout);
+        if (k.down) {
+          k.wd_off = take_params(static_cast<long long>(k.cout) * k.cin);
+          k.gd_off = take_params(2LL * k.cout);
+        }
+        const long long count = static_cast<long long>(k.width) * k.cin + 9LL * k.width * k.width +
+                                static_cast<long long>(k.cout) * k.width + 2LL * (2 * k.width + k.cout) +
+                                (k.down ? static_cast<long long>(k.cout) * k.cin + 2LL * k.cout : 0);
+        if (i < m->split) {
+          real_runs.emplace_back(k.wa_off, off - k.wa_off);   // the block's parameters are contiguous
+          m->real_front += count;
+        } else {
+          m->real_bseg += count;
+        }
+        f.w_off = k.wa_off;
+        f.w_count = off - k.wa_off;
+        f.blk = static_cast<int>(m->blocks.size());
+        m->blocks.push_back(k);
+        o.h = k.ho; o.w = k.wo; o.c = k.cout; o.pad = 0;
+      }
     } else {
       return fail("unsupported front layer kind");
     }
@@ -253,6 +314,9 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   }
   const ActBuf& cut = m->acts.back();
   if (cut.pad != 0) return fail("the FC tail's input must be a pooling output");
+  for (int i : {m->split - 1, nconv - 1})   // the backward of these layers needs their stored output
+    if (i >= 0 && (m->front[i].kind == RALPB_BLOCK || m->front[i].bn))
+      return fail("a cut must follow a pool or the average pool, not a block / batch-normalised conv");
   m->cut_elems = cut.h * cut.w * cut.c;
   if (!m->bseg) m->n_front = align_up(off, kShardAlign);
   m->bseg_end = align_up(off, 4);
@@ -400,6 +464,22 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     // pair precision: [2co][taps][2ci] operand copies (pair.cuh)
     if (!(f.wf = alloc<bf16>(m, f.w_count * pm * pm, why))) return fail(*why);
     if (!f.im2col && !(f.wd = alloc<bf16>(m, f.w_count * pm * pm, why))) return fail(*why);
+  }
+  // branchy layers: the blocks' operands and saved tensors, the stem's pre-batch-norm output
+  if (m->branchy && !(m->bn_work = alloc<float>(m, 2 * 2048, why))) return fail(*why);
+  for (size_t i = 0; i < m->front.size(); ++i) {
+    FrontLayer& f = m->front[i];
+    const bool mine = static_cast<int>(i) < m->split ? m->is_worker : (m->bseg && m->holds_back);
+    if (!mine) continue;
+    if (f.kind == RALPB_BLOCK) {
+      if (block_alloc(m, m->blocks[f.blk], why)) return fail(*why);
+      if (m->blocks[f.blk].cmax > 2048) return fail("block channels above 2048");
+    } else if (f.bn) {
+      const size_t rows = static_cast<size_t>(m->acts[i + 1].rows());
+      if (!(f.pre = alloc<bf16>(m, rows * f.g.cout, why)) || !(f.dpre = alloc<bf16>(m, rows * f.g.cout, why)) ||
+          !(f.bn_stats = alloc<float>(m, 2 * static_cast<size_t>(f.g.cout), why)))
+        return fail(*why);
+    }
   }
   const int R = m->rows_back;
   if (m->mps) {
@@ -555,19 +635,39 @@ int model_set_params(Model* m, int layer, const float* w, const float* b, int on
   if (layer < 0 || layer >= static_cast<int>(m->desc.size())) { *why = "layer out of range"; return 1; }
   const auto kind = cudaMemcpyDefault;
   (void)on_host;
+  if (layer < m->nconv && m->front[layer].kind == RALPB_BLOCK) {
+    // w: wa, wb, wc(, wd) back to back; b: the batch-norm scale / shift pairs in the same order
+    BlockBufs& k = m->blocks[m->front[layer].blk];
+    const long long sw[4] = {static_cast<long long>(k.width) * k.cin, 9LL * k.width * k.width,
+                             static_cast<long long>(k.cout) * k.width, static_cast<long long>(k.cout) * k.cin};
+    const long long ow[4] = {k.wa_off, k.wb_off, k.wc_off, k.wd_off};
+    const long long sg[4] = {2LL * k.width, 2LL * k.width, 2LL * k.cout, 2LL * k.cout};
+    const long long og[4] = {k.ga_off, k.gb_off, k.gc_off, k.gd_off};
+    long long pw = 0, pg = 0;
+    for (int q = 0; q < (k.down ? 4 : 3); ++q) {
+      RALPB_TRY(cudaMemcpy(m->P + ow[q], w + pw, sw[q] * sizeof(float), kind));
+      RALPB_TRY(cudaMemcpy(m->P + og[q], b + pg, sg[q] * sizeof(float), kind));
+      pw += sw[q];
+      pg += sg[q];
+    }
+    if (k.wa != nullptr && block_prep(m, k, m->stream, why)) return 1;
+    RALPB_TRY(cudaStreamSynchronize(m->stream));
+    return 0;
+  }
   if (layer < m->nconv) {
     FrontLayer& f = m->front[layer];
     if (f.kind != RALPB_CONV) { *why = "layer has no parameters"; return 1; }
     const int co = f.g.cout, taps = f.k * f.k, cr = f.cin_real;
     const int kk = taps * cr;
-    std::vector<float> host(static_cast<size_t>(co) * kk), hb(co), packed(f.w_count, 0.f);
+    std::vector<float> host(static_cast<size_t>(co) * kk), hb(f.bn ? 2 * co : co), packed(f.w_count, 0.f);
     RALPB_TRY(cudaMemcpy(host.data(), w, host.size() * sizeof(float), kind));
-    RALPB_TRY(cudaMemcpy(hb.data(), b, co * sizeof(float), kind));
-    if (f.im2col) {  // [co][kpad]: taps*cin filter columns, then the bias column
+    RALPB_TRY(cudaMemcpy(hb.data(), b, hb.size() * sizeof(float), kind));
+    if (f.im2col) {  // [co][kpad]: taps*cin filter columns, then the bias column (bn: gamma | beta after)
       for (int o = 0; o < co; ++o) {
         for (int j = 0; j < kk; ++j) packed[static_cast<size_t>(o) * f.kpad + j] = host[static_cast<size_t>(o) * kk + j];
-        packed[static_cast<size_t>(o) * f.kpad + kk] = hb[o];
+        if (!f.bn) packed[static_cast<size_t>(o) * f.kpad + kk] = hb[o];
       }
+      if (f.bn) RALPB_TRY(cudaMemcpy(m->P + f.b_off, hb.data(), hb.size() * sizeof(float), cudaMemcpyHostToDevice));
     } else {  // [co][taps][cin_pad], padded input channels are zero
       const int cp = f.g.cin;
       for (int o = 0; o < co; ++o)
@@ -613,6 +713,22 @@ static int read_layer(Model* m, int layer, float* w, float* b, size_t off, std::
   if (layer < 0 || layer >= static_cast<int>(m->desc.size())) { *why = "layer out of range"; return 1; }
   const float* self = at<float>(m, m->rank, off);
   RALPB_TRY(cudaStreamSynchronize(m->stream));
+  if (layer < m->nconv && m->front[layer].kind == RALPB_BLOCK) {
+    BlockBufs& k = m->blocks[m->front[layer].blk];
+    const long long sw[4] = {static_cast<long long>(k.width) * k.cin, 9LL * k.width * k.width,
+                             static_cast<long long>(k.cout) * k.width, static_cast<long long>(k.cout) * k.cin};
+    const long long ow[4] = {k.wa_off, k.wb_off, k.wc_off, k.wd_off};
+    const long long sg[4] = {2LL * k.width, 2LL * k.width, 2LL * k.cout, 2LL * k.cout};
+    const long long og[4] = {k.ga_off, k.gb_off, k.gc_off, k.gd_off};
+    long long pw = 0, pg = 0;
+    for (int q = 0; q < (k.down ? 4 : 3); ++q) {
+      RALPB_TRY(cudaMemcpy(w + pw, self + ow[q], sw[q] * sizeof(float), cudaMemcpyDefault));
+      RALPB_TRY(cudaMemcpy(b + pg, self + og[q], sg[q] * sizeof(float), cudaMemcpyDefault));
+      pw += sw[q];
+      pg += sg[q];
+    }
+    return 0;
+  }
   if (layer < m->nconv) {
     FrontLayer& f = m->front[layer];
     if (f.kind != RALPB_CONV) { *why = "layer has no parameters"; return 1; }
@@ -620,7 +736,12 @@ static int read_layer(Model* m, int layer, float* w, float* b, size_t off, std::
     const int kk = taps * cr;
     std::vector<float> packed(f.w_count), host(static_cast<size_t>(co) * kk), hb(co);
     RALPB_TRY(cudaMemcpy(packed.data(), self + f.w_off, packed.size() * sizeof(float), cudaMemcpyDeviceToHost));
-    if (f.im2col) {
+    if (f.im2col && f.bn) {
+      for (int o = 0; o < co; ++o)
+        for (int j = 0; j < kk; ++j) host[static_cast<size_t>(o) * kk + j] = packed[static_cast<size_t>(o) * f.kpad + j];
+      hb.resize(2 * co);
+      RALPB_TRY(cudaMemcpy(hb.data(), self + f.b_off, 2 * co * sizeof(float), cudaMemcpyDeviceToHost));
+    } else if (f.im2col) {
       for (int o = 0; o < co; ++o) {
         for (int j = 0; j < kk; ++j) host[static_cast<size_t>(o) * kk + j] = packed[static_cast<size_t>(o) * f.kpad + j];
         hb[o] = packed[static_cast<size_t>(o) * f.kpad + kk];
@@ -634,7 +755,7 @@ static int read_layer(Model* m, int layer, float* w, float* b, size_t off, std::
       RALPB_TRY(cudaMemcpy(hb.data(), self + f.b_off, co * sizeof(float), cudaMemcpyDeviceToHost));
     }
     RALPB_TRY(cudaMemcpy(w, host.data(), host.size() * sizeof(float), cudaMemcpyDefault));
-    RALPB_TRY(cudaMemcpy(b, hb.data(), co * sizeof(float), cudaMemcpyDefault));
+    RALPB_TRY(cudaMemcpy(b, hb.data(), hb.size() * sizeof(float), cudaMemcpyDefault));
   } else {
     const int j = layer - m->nconv;
     FcLayer& f = m->back[j];
@@ -1045,9 +1166,35 @@ int launch_conv_backward(Model* m, int lo, int hi, const bf16* cur, const ActBuf
     const ActBuf& in = i == lo && in_lo != nullptr ? *in_lo : m->acts[i];
     const ActBuf& out = m->acts[i + 1];
     bf16* dst_i = i == lo && dst_lo != nullptr ? dst_lo : m->gacts[i];
+    if (f.kind == RALPB_BLOCK) {
+      const bool need = i > lo || dgrad_lo;
+      if (block_backward(m, m->blocks[f.blk], in.ptr, out.ptr, cur, need ? dst_i : nullptr, why)) return 1;
+      cur = dst_i;
+      db_done = false;
+      continue;
+    }
+    if (f.kind == RALPB_APOOL) {
+      RALPB_TRY(avgpool_bwd(cur, in.n, in.h, in.w, in.c, MutAct4{dst_i, in.pad}, m->stream));
+      ++m->launches;
+      cur = dst_i;
+      db_done = false;
+      continue;
+    }
+    if (f.kind == RALPB_POOL && f.pool_pad > 0) {
+      RALPB_TRY(maxpool_pad_bwd(f.idx, Act4{cur, out.pad}, in.n, in.h, in.w, in.c, f.k, f.stride, f.pool_pad, out.h, out.w,
+                                MutAct4{dst_i, in.pad}, m->stream));
+      ++m->launches;
+      cur = dst_i;
+      db_done = false;
+      continue;
+    }
+    if (f.bn) {
+      if (bn_stem_backward(m, f, in, out, cur, why)) return 1;
+      continue;
+    }
     // bias gradient of a (non-im2col) conv i-1 of this segment is summed by the kernel that
     // produces its dY
-    float* prev_db = (i > lo && m->front[i - 1].kind == RALPB_CONV && !m->front[i - 1].im2col &&
+    float* prev_db = (i > lo && m->front[i - 1].kind == RALPB_CONV && !m->front[i - 1].im2col && !m->front[i - 1].bn &&
                       m->front[i - 1].g.cout <= 512)
                          ? m->G + m->front[i - 1].b_off
                          : nullptr;
@@ -1110,6 +1257,25 @@ int launch_conv_forward(Model* m, int lo, int hi, const float* img, const ActBuf
     const ActBuf& in = i == lo && in_lo != nullptr ? *in_lo : m->acts[i];
     ActBuf out = m->acts[i + 1];
     if (i + 1 == hi) out.ptr = out_last;
+    if (f.kind == RALPB_BLOCK) {
+      if (block_forward(m, m->blocks[f.blk], in.ptr, out.ptr, why)) return 1;
+      continue;
+    }
+    if (f.kind == RALPB_APOOL) {
+      RALPB_TRY(avgpool_fwd(Act4{in.ptr, in.pad}, in.n, in.h, in.w, in.c, out.ptr, s));
+      ++m->launches;
+      continue;
+    }
+    if (f.kind == RALPB_POOL && f.pool_pad > 0) {
+      RALPB_TRY(maxpool_pad_fwd(Act4{in.ptr, in.pad}, in.n, in.h, in.w, in.c, f.k, f.stride, f.pool_pad,
+                                MutAct4{out.ptr, out.pad}, out.h, out.w, f.idx, s));
+      ++m->launches;
+      continue;
+    }
+    if (f.bn) {
+      if (bn_stem_forward(m, f, in, out, why)) return 1;
+      continue;
+    }
     if (f.fused) {
       RALPB_TRY(conv_first_fwd(img, in.n, m->in_h, m->in_w, m->in_c, f.wf, out.ptr, out.pad, s, why));
     } else if (f.im2col) {
@@ -1152,6 +1318,10 @@ int prep_filters(Model* m, bool forward, bool dgrad, cudaStream_t s, std::string
   if (hi < 0) hi = static_cast<int>(m->front.size());
   for (size_t i = lo; i < static_cast<size_t>(hi); ++i) {
     FrontLayer& f = m->front[i];
+    if (f.kind == RALPB_BLOCK) {   // all of a block's operand copies with the forward ones
+      if (forward && m->blocks[f.blk].wa != nullptr && block_prep(m, m->blocks[f.blk], s, why)) return 1;
+      continue;
+    }
     if (f.kind != RALPB_CONV || f.wf == nullptr) continue;   // (layers this rank does not run)
     if (f.im2col) {
       if (forward) {
@@ -1641,6 +1811,11 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
       RALPB_TRY(pack_im2col(img, b, m->in_h, m->in_w, m->in_c, f0.k, f0.stride, m->desc[0].pad, a0.h, a0.w, a0.pad,
                             f0.kpad, a0.ptr, s));
       ++m->launches;
+      if (f0.bn) {  // a batch-normalised stem has no bias: clear the patch rows' ones column
+        const int kk = f0.k * f0.k * f0.cin_real;
+        RALPB_TRY(cudaMemset2DAsync(a0.ptr + kk, static_cast<size_t>(f0.kpad) * sizeof(bf16), 0, sizeof(bf16),
+                                    static_cast<size_t>(a0.rows()), s));
+      }
     } else {
       RALPB_TRY(pack_input(img, b, m->in_h, m->in_w, m->in_c, a0.ptr, m->in_cp, a0.pad, s));
       ++m->launches;
@@ -1662,7 +1837,7 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
                                 cudaMemcpyDeviceToDevice, s));
       if (ralp) m->logical += cut_logical;   // "act": this colocated worker's cut, written in place
     }
-    if (ralp && m->workers > 1) {
+    if (ralp && m->world > 1) {   // cuts arrive from peers (colocated W > 1, or a dedicated PS)
       if (m->is_worker) {
         PeerSignal own{};
         own.n = 1;

@@ -20,8 +20,24 @@ struct ActBuf {
   long long elems() const { return rows() * c; }
 };
 
+// A ResNet bottleneck block's operands and saved tensors (block.cu).  Forward:
+//   a_pre = x Wa^T; a = relu(bn_a(a_pre)) (padded); b_pre = conv3x3_s(a, Wb); b = relu(bn_b(b_pre));
+//   c_pre = b Wc^T; y = relu(bn_c(c_pre) + (downsample ? bn_d(subsample_s(x) Wd^T) : x)).
+struct BlockBufs {
+  int cin = 0, width = 0, cout = 0, stride = 1, down = 0;
+  int n = 0, h = 0, w = 0, ho = 0, wo = 0;
+  long long wa_off = 0, ga_off = 0, wb_off = 0, gb_off = 0, wc_off = 0, gc_off = 0, wd_off = 0, gd_off = 0;
+  __nv_bfloat16 *wa = nullptr, *wbf = nullptr, *wbd = nullptr, *wc = nullptr, *wd = nullptr;
+  __nv_bfloat16 *a_pre = nullptr, *a = nullptr, *b_pre = nullptr, *b = nullptr, *c_pre = nullptr, *d_in = nullptr,
+                *d_pre = nullptr, *col = nullptr;
+  __nv_bfloat16 *dc_pre = nullptr, *dz = nullptr, *db = nullptr, *db_pre = nullptr, *dil = nullptr, *da = nullptr,
+                *da_pre = nullptr, *dd_pre = nullptr, *dxs = nullptr;
+  float* stats = nullptr;   // [4][2][cmax]: mean / rstd of bn a, b, c, d
+  int cmax = 0;
+};
+
 struct FrontLayer {
-  int kind = 0;                // RALPB_CONV / RALPB_POOL
+  int kind = 0;                // RALPB_CONV / RALPB_POOL / RALPB_BLOCK / RALPB_APOOL
   ConvGeom g{};                // conv geometry (cin padded to 16)
   int cin_real = 0;
   int k = 0, stride = 0;       // pool window
@@ -36,6 +52,12 @@ struct FrontLayer {
                                // patches built on chip from the fp32 image, acts[0] unused
   bool fused_fwd = false;      // pool computed in the preceding conv's epilogue
   uint8_t* idx = nullptr;      // ... with argmax bytes [n][oh][ow][c] for its backward
+  int pool_pad = 0;            // pool: zero padding (ResNet's 3x3/2 pad 1)
+  bool bn = false;             // conv: batch norm (+ReLU) after it, no bias; b_off = gamma, beta follows
+  __nv_bfloat16* pre = nullptr;     // bn conv: its output before the batch norm
+  __nv_bfloat16* dpre = nullptr;    // ... and the gradient w.r.t. it
+  float* bn_stats = nullptr;        // bn conv: [2][cout] mean / rstd
+  int blk = -1;                // RALPB_BLOCK: index into Model::blocks
 };
 
 struct FcLayer {
@@ -63,6 +85,9 @@ struct Model {
                                       // logical byte count of the pull / ring sites
   std::vector<ralpb_layer_desc> desc;
   std::vector<FrontLayer> front;
+  std::vector<BlockBufs> blocks;   // RALPB_BLOCK layers
+  bool branchy = false;            // the model has blocks / batch-normalised convolutions
+  float* bn_work = nullptr;        // [2][2048] batch-norm reduction scratch
   std::vector<FcLayer> back;
   std::vector<ActBuf> acts;        // acts[i] = input of front layer i; acts.back() = cut (local)
   int in_h = 0, in_w = 0, in_c = 0, in_cp = 0;

@@ -16,7 +16,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from . import _lib
+from . import _lib, resnet
 from .planner.costmodel import (JobSpec, volume_baseline, volume_ralp, volume_ralp_multi_ps,
                                  volume_ring)
 from .planner.layers import ModelGraph
@@ -48,7 +48,12 @@ def infer_input_shape(model: ModelGraph) -> tuple[int, int, int]:
 
 
 def lower(model: ModelGraph, input_shape: Optional[tuple[int, int, int]] = None) -> list[dict]:
-    """ModelGraph -> list of layer dicts (kind, k, stride, pad, h, w, cin, cout, relu)."""
+    """ModelGraph -> list of layer dicts (kind, k, stride, pad, h, w, cin, cout, relu[, bn, width,
+    downsample]).  ResNet-50's linearised catalog entries are lowered at block granularity from
+    the architecture they were generated from (resnet.py, checked entry by entry)."""
+    if resnet.is_resnet50(model):
+        resnet.check_catalog(model)
+        return resnet.lower_layers()[0]
     h, w, c = input_shape or infer_input_shape(model)
     out: list[dict] = []
     n = model.num_layers
@@ -82,6 +87,15 @@ def lower(model: ModelGraph, input_shape: Optional[tuple[int, int, int]] = None)
     return out
 
 
+def block_param_counts(L: dict) -> tuple[int, int]:
+    """(weights, batch-norm parameters) of a bottleneck block layer: wa [width][cin],
+    wb [width][3][3][width], wc [cout][width] (, wd [cout][cin]); gamma / beta per convolution."""
+    cin, width, cout, down = L["cin"], L["width"], L["cout"], L.get("downsample", 0)
+    nw = width * cin + 9 * width * width + cout * width + (cout * cin if down else 0)
+    nb = 2 * (2 * width + cout + (cout if down else 0))
+    return nw, nb
+
+
 def expected_volume(job, fc_sharding: str = "single") -> int:
     """The oracle's logical synchronised bytes per step for `job` (costmodel.py:107-162), dispatched
     on the strategy's value so a reference `ralp.JobSpec` works too."""
@@ -107,7 +121,8 @@ def allgather_bytes(blob: bytes) -> list[bytes]:
     return [bytes(p.cpu().numpy().tobytes()) for p in parts]
 
 
-_KIND = {"conv": _lib.RALPB_CONV, "pool": _lib.RALPB_POOL, "fc": _lib.RALPB_FC}
+_KIND = {"conv": _lib.RALPB_CONV, "pool": _lib.RALPB_POOL, "fc": _lib.RALPB_FC, "block": _lib.RALPB_BLOCK,
+         "apool": _lib.RALPB_APOOL}
 
 
 def _desc_array(layers: Sequence[dict]):
@@ -115,6 +130,7 @@ def _desc_array(layers: Sequence[dict]):
     for a, L in zip(arr, layers):
         a.kind, a.k, a.stride, a.pad = _KIND[L["kind"]], L["k"], L["stride"], L["pad"]
         a.h, a.w, a.cin, a.cout, a.relu = L["h"], L["w"], L["cin"], L["cout"], L["relu"]
+        a.bn, a.width, a.downsample = L.get("bn", 0), L.get("width", 0), L.get("downsample", 0)
     return arr
 
 
@@ -188,6 +204,11 @@ class RankExecutor:
         self.in_shape = (self.layers[0]["h"], self.layers[0]["w"], self.layers[0]["cin"])
         self.classes = self.layers[-1]["cout"]
         split = job.strategy.split_index if kind == "ralp" else 0
+        if split and resnet.is_resnet50(job.model):
+            try:
+                split = resnet.lowered_split(split)   # catalog entries -> lowered layers
+            except ValueError as e:
+                raise ExecutorError(str(e)) from None
         if kind == "ralp":
             strategy = _lib.RALPB_STRATEGY_RALP if self.fc_sharding == "single" else _lib.RALPB_STRATEGY_RALP_MPS
         elif kind == "ring":
@@ -220,17 +241,26 @@ class RankExecutor:
             w, b = (np.ascontiguousarray(x, dtype=np.float32) for x in p)
             _lib.call("ralpb_model_set_params", self._h, i, _ptr(w), _ptr(b), 1)
 
+    def _param_arrays(self, L: dict):
+        """Host arrays (w, b) in the layout of ralpb_model_set_params for one lowered layer."""
+        if L["kind"] == "conv":
+            return (np.empty((L["cout"], L["k"], L["k"], L["cin"]), dtype=np.float32),
+                    np.empty(L["cout"] * (2 if L.get("bn") else 1), dtype=np.float32))
+        if L["kind"] == "fc":
+            return np.empty((L["cout"], L["cin"]), dtype=np.float32), np.empty(L["cout"], dtype=np.float32)
+        if L["kind"] == "block":
+            nw, nb = block_param_counts(L)
+            return np.empty(nw, dtype=np.float32), np.empty(nb, dtype=np.float32)
+        return None
+
     def get_params(self) -> list:
         out = []
         for i, L in enumerate(self.layers):
-            if L["kind"] == "conv":
-                w = np.empty((L["cout"], L["k"], L["k"], L["cin"]), dtype=np.float32)
-            elif L["kind"] == "fc":
-                w = np.empty((L["cout"], L["cin"]), dtype=np.float32)
-            else:
+            arrs = self._param_arrays(L)
+            if arrs is None:
                 out.append(None)
                 continue
-            b = np.empty(L["cout"], dtype=np.float32)
+            w, b = arrs
             _lib.call("ralpb_model_get_params", self._h, i, _ptr(w), _ptr(b), 1)
             out.append((w, b))
         return out
@@ -240,14 +270,11 @@ class RankExecutor:
         get_params layout; the FC tail's only on the rank that holds it."""
         out = []
         for i, L in enumerate(self.layers):
-            if L["kind"] == "conv":
-                w = np.empty((L["cout"], L["k"], L["k"], L["cin"]), dtype=np.float32)
-            elif L["kind"] == "fc":
-                w = np.empty((L["cout"], L["cin"]), dtype=np.float32)
-            else:
+            arrs = self._param_arrays(L)
+            if arrs is None:
                 out.append(None)
                 continue
-            b = np.empty(L["cout"], dtype=np.float32)
+            w, b = arrs
             _lib.call("ralpb_model_get_grads", self._h, i, _ptr(w), _ptr(b))
             out.append((w, b))
         return out

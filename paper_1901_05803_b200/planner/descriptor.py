@@ -5,6 +5,13 @@ Same document format and error classes as the reference parser
 (pkg/src/ralp/descriptor.py:84-224): derived layers are shape-checked against
 their predecessor (cin=, in=), explicit layers give `params= out= flops=`
 (fused blocks, linearised branchy models), `shape=` overrides the output shape.
+
+VENDORED API MIRROR (attribution): this module follows the reference `ralp` package's own code for
+the same surface closely -- same classes, checks, error messages and arithmetic -- because north_star
+makes that planner API the drop-in surface and its outputs must match the reference bit-exactly
+(tests/test_planner_golden.py pins them to the unmodified reference).  It is not original work and
+it is not on the GPU path; the executor accepts the reference's own objects as well
+(executor.py `_kv`).
 """
 from __future__ import annotations
 

@@ -5,6 +5,13 @@
 derives avg_step_time (mean over steps of the slowest worker), images_per_sec
 (W*b / avg_step_time) and comm_fraction exactly as the reference does.  The
 measured backend adds `losses` (one per step, PS rank).
+
+VENDORED API MIRROR (attribution): this module follows the reference `ralp` package's own code for
+the same surface closely -- same classes, checks, error messages and arithmetic -- because north_star
+makes that planner API the drop-in surface and its outputs must match the reference bit-exactly
+(tests/test_planner_golden.py pins them to the unmodified reference).  It is not original work and
+it is not on the GPU path; the executor accepts the reference's own objects as well
+(executor.py `_kv`).
 """
 from __future__ import annotations
 

@@ -43,7 +43,23 @@ def init_params(layers: list[dict], seed: int) -> list[tuple[np.ndarray, np.ndar
             fan_in = L["k"] * L["k"] * L["cin"]
             w = (r.standard_normal((L["cout"], L["k"], L["k"], L["cin"]), dtype=np.float32)
                  * np.float32(np.sqrt(2.0 / fan_in)))
-            out.append((w, np.zeros(L["cout"], dtype=np.float32)))
+            if L.get("bn"):   # batch norm: scale 1, shift 0 (no bias)
+                out.append((w, np.concatenate([np.ones(L["cout"], np.float32), np.zeros(L["cout"], np.float32)])))
+            else:
+                out.append((w, np.zeros(L["cout"], dtype=np.float32)))
+        elif L["kind"] == "block":
+            # wa [width][cin], wb [width][3][3][width], wc [cout][width] (, wd [cout][cin]), He-normal;
+            # batch-norm scale 1, shift 0 for each convolution
+            cin, width, cout = L["cin"], L["width"], L["cout"]
+            shapes = [((width, cin), cin), ((width, 3, 3, width), 9 * width), ((cout, width), width)]
+            if L.get("downsample"):
+                shapes.append(((cout, cin), cin))
+            ws = [(r.standard_normal(sh, dtype=np.float32) * np.float32(np.sqrt(2.0 / fan))).reshape(-1)
+                  for sh, fan in shapes]
+            bns = []
+            for sh, _ in shapes:
+                bns += [np.ones(sh[0], np.float32), np.zeros(sh[0], np.float32)]
+            out.append((np.concatenate(ws), np.concatenate(bns)))
         elif L["kind"] == "fc":
             w = r.standard_normal((L["cout"], L["cin"]), dtype=np.float32) * np.float32(0.01)
             out.append((w, np.zeros(L["cout"], dtype=np.float32)))

@@ -147,15 +147,20 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
             g = ex.get_grads() if ex.is_worker else [None if p is None else (np.zeros_like(p[0]), np.zeros_like(p[1]))
                                                         for p in params]
             gv = _front_param_vec(g, nsync)
-            gsum = sum(_gather(gv, world))
+            g_all = _gather(gv, world)      # (collective: every rank)
+            gsum = sum(g_all)
+            gabs = sum(x.abs() for x in g_all)
             p1 = _front_param_vec(ex.get_params(), nsync) if ex.is_worker else None
             if p1 is not None:
                 p0 = _front_param_vec(params, nsync)
-                want = p0 - torch.tensor(lr, dtype=torch.float32) * gsum
-                # summation order of the W gradients differs (shard_update vs this sum): a few ulp
-                dev = float(((p1 - want).abs() / (want.abs() * 2.0 ** -23 + 1e-30)).max())
-                if dev > 64 * workers:
-                    print(f"[{tag} rank {rank}] sync: p1 != p0 - lr * sum g ({dev:.1f} ulp)", flush=True)
+                lr32 = torch.tensor(lr, dtype=torch.float32)
+                want = p0 - lr32 * gsum
+                # the W gradients are summed in another order by shard_update: allow a few roundings
+                # of the terms' magnitudes (|p0| + lr * sum_r |g_r|), not of the (possibly cancelled) sum
+                scale = (p0.abs() + lr32 * gabs) * 2.0 ** -23 + 1e-30
+                dev = float(((p1 - want).abs() / scale).max())
+                if dev > 4 * workers:
+                    print(f"[{tag} rank {rank}] sync: p1 != p0 - lr * sum g ({dev:.1f} roundings)", flush=True)
                     ok = False
         if rank == 0:
             batches = [synthetic.batch(1, t, w * b, b, ex.in_shape, ex.classes) for w in range(workers)]
@@ -174,7 +179,7 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
     got = ex.get_params() if ex.is_worker else None
     # every worker holds the same front (all-on-PS / ring: all) parameters
     if ex.is_worker or placement == "dedicated-ps":
-        vec = _front_param_vec(got, nsync) if got is not None else torch.zeros(1)
+        vec = _front_param_vec(got, nsync) if got is not None else torch.zeros_like(_front_param_vec(params, nsync))
         allv = _gather(vec, world)
         wr = [r for r in range(world) if not (placement == "dedicated-ps" and r == ex.ps_rank)]
         for r in wr[1:]:

@@ -39,7 +39,8 @@ def test_library_exports_every_declared_symbol():
 def test_abi_structs_match_header():
     text = (ROOT / "include" / "ralpb.h").read_text()
     assert "ralpb_layer_desc" in text and "ralpb_step_stats" in text
-    assert [f for f, _ in _lib.LayerDesc._fields_] == ["kind", "k", "stride", "pad", "h", "w", "cin", "cout", "relu"]
+    assert [f for f, _ in _lib.LayerDesc._fields_] == ["kind", "k", "stride", "pad", "h", "w", "cin", "cout", "relu",
+                                                      "bn", "width", "downsample"]
     assert _lib.StepStats._fields_[0][0] == "loss"
 
 
