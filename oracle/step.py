@@ -225,10 +225,137 @@ def softmax_xent(logits, labels, scale):
 
 def param_count(L) -> int:
     if L["kind"] == "conv":
-        return L["k"] * L["k"] * L["cin"] * L["cout"] + L["cout"]
+        return L["k"] * L["k"] * L["cin"] * L["cout"] + L["cout"] * (2 if L.get("bn") else 1)
+    if L["kind"] == "block":
+        cin, width, cout, down = L["cin"], L["width"], L["cout"], L.get("downsample", 0)
+        return (width * cin + 9 * width * width + cout * width + (cout * cin if down else 0)
+                + 2 * (2 * width + cout + (cout if down else 0)))
     if L["kind"] == "fc":
         return L["cin"] * L["cout"] + L["cout"]
     return 0
+
+
+# ---------------------------------------------------------------- branchy models (autograd restatement)
+class _Round(torch.autograd.Function):
+    """bf16 storage point: rounds the value on the way forward and its gradient on the way back
+    (the GPU stores both the activation and the gradient w.r.t. it in bf16)."""
+
+    @staticmethod
+    def forward(ctx, x):
+        return x.to(torch.bfloat16).to(x.dtype)
+
+    @staticmethod
+    def backward(ctx, g):
+        return g.to(torch.bfloat16).to(g.dtype)
+
+
+def _block_params(L, w, b):
+    """Split a block's flat (w, b) into its tensors (executor.block_param_counts order)."""
+    cin, width, cout, down = L["cin"], L["width"], L["cout"], L.get("downsample", 0)
+    shapes = [(width, cin, 1, 1), (width, width, 3, 3), (cout, width, 1, 1)] + ([(cout, cin, 1, 1)] if down else [])
+    ws, o = [], 0
+    for sh in shapes:
+        n = int(np.prod(sh))
+        if len(sh) == 4 and sh[2] == 3:   # stored [co][kh][kw][ci]
+            ws.append(w[o:o + n].reshape(sh[0], 3, 3, sh[1]).permute(0, 3, 1, 2))
+        else:
+            ws.append(w[o:o + n].reshape(sh))
+        o += n
+    bns, o = [], 0
+    for sh in shapes:
+        bns.append((b[o:o + sh[0]], b[o + sh[0]:o + 2 * sh[0]]))
+        o += 2 * sh[0]
+    return ws, bns
+
+
+def _bn(x, gamma, beta):
+    """Training-mode batch norm over the (worker's) batch, biased variance, eps 1e-5."""
+    return F.batch_norm(x, None, None, gamma, beta, training=True, momentum=0.0, eps=1e-5)
+
+
+def _branchy_forward(layers, params, x, R, dtype):
+    """Forward of a model with blocks / batch-normalised convs / padded and average pools, bf16
+    storage emulated by R at the GPU's storage points (block.cu, resnet.cu).  Returns logits."""
+    for L, p in zip(layers, params):
+        k = L["kind"]
+        if k == "conv":
+            w, b = p
+            wt = R(w.permute(0, 3, 1, 2).contiguous().to(dtype))
+            if L.get("bn"):
+                c = L["cout"]
+                pre = R(F.conv2d(x, wt, None, stride=L["stride"], padding=L["pad"]))
+                x = R(torch.relu(_bn(pre, b[:c].to(dtype), b[c:].to(dtype))))
+            else:
+                x = R(torch.relu(F.conv2d(x, wt, b.to(dtype), stride=L["stride"], padding=L["pad"])))
+        elif k == "pool":
+            x = R(F.max_pool2d(x, L["k"], L["stride"], L["pad"]))
+        elif k == "block":
+            ws, bns = _block_params(L, p[0].to(dtype), p[1].to(dtype))
+            s = L["stride"]
+            a = R(torch.relu(_bn(R(F.conv2d(x, R(ws[0]))), *bns[0])))
+            bb = R(torch.relu(_bn(R(F.conv2d(a, R(ws[1]), stride=s, padding=1)), *bns[1])))
+            c = _bn(R(F.conv2d(bb, R(ws[2]))), *bns[2])
+            short = _bn(R(F.conv2d(x[:, :, ::s, ::s], R(ws[3]))), *bns[3]) if L.get("downsample") else x
+            x = R(torch.relu(c + short))
+        elif k == "apool":
+            x = R(x.mean(dim=(2, 3), keepdim=True))
+        elif k == "fc":
+            if x.dim() == 4:
+                x = x.permute(0, 2, 3, 1).reshape(x.shape[0], -1)   # HWC flatten
+            w, b = p
+            last = L is layers[-1]
+            z = x @ R(w.to(dtype)).t() + b.to(dtype)
+            x = z if last else R(torch.relu(z))
+    return x
+
+
+def _train_step_branchy(st: OracleState, strategy: str, workers: int, batches, *, lr, mu, emulate_bf16, elem_bytes,
+                        accum64, split):
+    dtype = torch.float64 if accum64 else torch.float32
+    R = _Round.apply if emulate_bf16 else (lambda t: t)
+    leaves = []
+    params = []
+    for p in st.params:
+        if p is None:
+            params.append(None)
+            continue
+        w = p[0].detach().to(dtype).clone().requires_grad_(True)
+        b = p[1].detach().to(dtype).clone().requires_grad_(True)
+        leaves.append((w, b))
+        params.append((w, b))
+    b_sz = batches[0][0].shape[0]
+    total = 0.0
+    for imgs, labs in batches:   # every worker runs its front (and its batch norm) on its own batch
+        x = R(torch.from_numpy(np.ascontiguousarray(imgs)).permute(0, 3, 1, 2).contiguous().to(dtype))
+        logits = _branchy_forward(st.layers, params, x, R, dtype)
+        lab = torch.from_numpy(np.asarray(labs, dtype=np.int64))
+        loss = F.cross_entropy(logits, lab, reduction="sum") / (workers * b_sz)
+        loss.backward()
+        total += float(loss.detach())
+    grads = {}
+    for i, p in enumerate(params):
+        if p is not None:
+            grads[i] = (p[0].grad.to(torch.float32).reshape(st.params[i][0].shape), p[1].grad.to(torch.float32))
+    for idx, g in grads.items():
+        _sgd(st, idx, g, lr, mu)
+    nfront = _split_index(st.layers)
+    cut_at = nfront if split is None else split
+    wire = 0
+    if strategy == "ralp":
+        with torch.no_grad():
+            x = torch.from_numpy(np.ascontiguousarray(batches[0][0])).permute(0, 3, 1, 2).contiguous()
+            for L, p in zip(st.layers[:cut_at], st.params[:cut_at]):
+                x = _branchy_forward([L], [p], x, lambda t: t, torch.float32)
+        cut_elems = x[0].numel()
+        p_front = sum(param_count(L) for L in st.layers[:cut_at]) * elem_bytes
+        wire = workers * (2 * b_sz * cut_elems * elem_bytes + 2 * p_front)
+    else:
+        wire = 2 * workers * sum(param_count(L) for L in st.layers) * elem_bytes
+    return total, wire
+
+
+def _branchy(layers) -> bool:
+    return any(L["kind"] in ("block", "apool") or L.get("bn") or (L["kind"] == "pool" and L.get("pad")) for L in layers)
 
 
 def train_step(st: OracleState, strategy: str, workers: int, batches, *, lr: float = 0.01, mu: float = 0.9,
@@ -240,6 +367,9 @@ def train_step(st: OracleState, strategy: str, workers: int, batches, *, lr: flo
     the numerics equal running them on each worker (what this restatement does) -- only the cut
     shipped and the synchronised front differ, in the byte count.
     Returns (loss, logical_bytes)."""
+    if _branchy(st.layers):
+        return _train_step_branchy(st, strategy, workers, batches, lr=lr, mu=mu, emulate_bf16=emulate_bf16,
+                                   elem_bytes=elem_bytes, accum64=accum64, split=split)
     _ACC[0] = torch.float64 if accum64 else torch.float32
     bf = emulate_bf16
     nfront = _split_index(st.layers)
