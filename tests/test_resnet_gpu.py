@@ -10,8 +10,16 @@ points (oracle/step.py `_train_step_branchy`).
     gathered rows (a conv back segment with batch norm);
   * all-on-PS baseline.
 Bytes: the ranks' count_wire-site counts == volume_ralp / volume_baseline of the catalog model.
-Numerics: loss within 2e-3 of the oracle at every step; parameters after the steps within
-min(2 * floor + 0.02, 0.5) of the update, floor = the oracle's own fp32-vs-fp64 spread.
+
+Numerics.  At b=8 with batch norm and bf16 storage the step is chaotic: the oracle's own
+fp32-vs-fp64 spread after two steps is ~1.2x the update itself, so a free-running comparison cannot
+discriminate.  The free-running tests therefore check the bytes, the first step's loss (forward
+only, 2e-3) and parameters within 2 * floor + 0.02 of the update; the sharp check is per block:
+test_resnet50_teacher_forced_blocks recomputes every layer (stem, pool, each bottleneck block,
+average pool, FC) from the GPU's OWN stored input -- and its backward from the GPU's own upstream
+gradient -- with the oracle's autograd restatement, and requires outputs, input gradients and
+parameter gradients within 2e-2 relative (||.||; a wrong stride, shortcut, batch-norm statistic or
+transposition is O(1)).
 """
 import numpy as np
 import pytest
@@ -50,7 +58,7 @@ def _run(batch, strategy, steps, lr, split=None):
         print(f"  step {t}: loss gpu {st.loss:.6f} oracle {lo:.6f} bytes {st.logical_bytes} launches {st.launches} "
               f"ms {st.ms_step:.2f}")
         assert st.logical_bytes == wire == expect
-        if abs(st.loss - lo) > 2e-3 * abs(lo):
+        if t == 0 and abs(st.loss - lo) > 2e-3 * abs(lo):
             bad.append(f"step {t}: loss {st.loss} vs oracle {lo}")
     got = ex.get_params()
     ex.close()
@@ -63,7 +71,7 @@ def _run(batch, strategy, steps, lr, split=None):
                 continue
             dev = np.linalg.norm(a.reshape(-1) - o.reshape(-1)) / upd
             floor = np.linalg.norm(o64_.reshape(-1) - o.reshape(-1)) / upd
-            bound = min(2 * floor + 0.02, 0.5)
+            bound = 2 * floor + 0.02
             print(f"  layer {li} {ex.layers[li]['name']}.{nm}: dev {dev:.3e} floor {floor:.3e}")
             if dev > bound:
                 bad.append(f"layer {li}.{nm}: dev {dev:.3e} > {bound:.3e}")
@@ -85,3 +93,60 @@ def test_resnet50_blocks_on_the_ps():
 
 def test_resnet50_all_on_ps():
     _run(8, "baseline", steps=2, lr=1e-3)
+
+
+def test_resnet50_teacher_forced_blocks():
+    import torch
+    from paper_1901_05803_b200 import _lib
+    b = 8
+    model = catalog_lookup("resnet-50").with_batch_size(b)
+    ex = RankExecutor(JobSpec(model, Strategy.ralp(55), 1))
+    params = synthetic.init_params(ex.layers, 0)
+    ex.set_params(params)
+    imgs, labs = synthetic.batch(0, 0, 0, b, ex.in_shape, ex.classes)
+    ex.step(imgs, labs, lr=1e-3, momentum=0.9)
+    grads = ex.get_grads()
+    L = ex.layers
+    R = ostep._Round.apply
+    report, bad = [], []
+
+    def nchw(flat, c):
+        hw = flat.size // (b * c)
+        side = int(round(hw ** 0.5))
+        return torch.from_numpy(flat.reshape(b, side, side, c)).permute(0, 3, 1, 2).contiguous()
+
+    def rel(name, got, ref, tol=2e-2):
+        r = float((got.double() - ref.double()).norm() / ref.double().norm())
+        report.append(f"{name:28s} rel {r:.2e}")
+        if not r <= tol:
+            bad.append(f"{name}: rel {r:.2e}")
+
+    def layer_io(i):
+        x = torch.from_numpy(imgs).permute(0, 3, 1, 2).contiguous() if i == 0 else nchw(ex.debug_buffer(_lib.DBG_ACT, i), L[i]["cin"])
+        if i + 1 < 19:
+            y = nchw(ex.debug_buffer(_lib.DBG_ACT, i + 1), L[i + 1]["cin"])
+            dy = nchw(ex.debug_buffer(_lib.DBG_ACT_GRAD, i + 1), L[i + 1]["cin"])
+        else:   # the cut: the FC input rows and their gradient
+            y = torch.from_numpy(ex.debug_buffer(_lib.DBG_FC_IN).reshape(b, -1, 1, 1))
+            dy = torch.from_numpy(ex.debug_buffer(_lib.DBG_FC_IN_GRAD).reshape(b, -1, 1, 1))
+        return x, y, dy
+
+    for i in range(19):   # stem, pool1, 16 blocks, apool
+        d = L[i]
+        x, y_gpu, dy_gpu = layer_io(i)
+        xin = (R(x) if i == 0 else x).requires_grad_(True)
+        p = params[i]
+        pt = None if p is None else [torch.from_numpy(a).clone().requires_grad_(True) for a in p]
+        y = ostep._branchy_forward([d], [pt], xin, R, torch.float32)
+        rel(f"fwd {i} {d['name']}", y_gpu, y.detach(), tol=0.0 if d["kind"] == "pool" else 2e-2)
+        # backward from the GPU's own upstream gradient
+        y.backward(dy_gpu)
+        if i > 0:
+            rel(f"dgrad {i} {d['name']}", nchw(ex.debug_buffer(_lib.DBG_ACT_GRAD, i), d["cin"]), xin.grad)
+        if pt is not None:
+            gw, gb = grads[i]
+            rel(f"wgrad {i} {d['name']}", torch.from_numpy(gw.reshape(-1)), pt[0].grad.reshape(-1))
+            rel(f"bn grad {i} {d['name']}", torch.from_numpy(gb.reshape(-1)), pt[1].grad.reshape(-1))
+    ex.close()
+    print("\n".join(report))
+    assert not bad, "\n".join(bad)
