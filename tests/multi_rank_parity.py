@@ -19,7 +19,9 @@ the CPU oracle.  Per configuration and step:
             per-layer parity is pinned by the teacher-forced single-GPU test and by the fp32 parity
             precision below); a wrong update is ~1
   fp32      precision="fp32" (the parity mode) against the plain fp32 oracle: loss within 1e-4
-            relative at every step and ||p_gpu - p_oracle|| / ||p_oracle|| <= 1e-4 per weight tensor
+            relative at every step (+ 3x the oracle's own fp32-vs-fp64 spread) and per weight tensor
+            ||p_gpu - p_oracle|| / ||p_oracle|| <= 1e-4, or within 3 * floor + 2e-2 of the update
+            (the rule of tests/test_parity_fp32_gpu.py)
 
 Exit code 0 = pass.  Used by tests/test_multigpu_gpu.py.
 """
@@ -105,7 +107,9 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
     b = model.batch_size
     fp32 = precision == "fp32"
     orc = ostep.OracleState(ex.layers, params) if rank == 0 else None
-    orc64 = ostep.OracleState(ex.layers, params) if rank == 0 and floor and not fp32 else None
+    # floor: the oracle re-run with float64 contractions (the bf16 pipeline's chaos; for the fp32
+    # precision the plain fp32 oracle's own sensitivity)
+    orc64 = ostep.OracleState(ex.layers, params) if rank == 0 and (floor or fp32) else None
     tag = (f"{strategy}-{ring_backend}" if strategy == "ring" else strategy + ("-mps" if fc_sharding == "multi" else "")
            ) + ("-dedicated-ps" if placement == "dedicated-ps" else "") + ("-fp32" if fp32 else "")
     ok = True
@@ -166,12 +170,14 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
             batches = [synthetic.batch(1, t, w * b, b, ex.in_shape, ex.classes) for w in range(workers)]
             lo, wire = ostep.train_step(orc, "baseline" if strategy == "ring" else strategy, workers, batches, lr=lr,
                                         emulate_bf16=not fp32, split=split if strategy == "ralp" else None)
+            l64 = None
             if orc64 is not None:
-                ostep.train_step(orc64, "baseline" if strategy == "ring" else strategy, workers, batches, lr=lr,
-                                 emulate_bf16=True, accum64=True)
+                l64, _ = ostep.train_step(orc64, "baseline" if strategy == "ring" else strategy, workers, batches, lr=lr,
+                                          emulate_bf16=not fp32, accum64=True, split=split if strategy == "ralp" else None)
             assert strategy == "ring" or fc_sharding == "multi" or wire == expect
             rel = abs(st.loss - lo) / abs(lo)
-            tol = 1e-4 if fp32 else 2e-3
+            # fp32: 1e-4, widened by the fp32 oracle's own fp64 spread where training is chaotic
+            tol = (1e-4 + 3 * abs(l64 - lo) / abs(lo)) if fp32 else 2e-3
             print(f"[{model.name} {tag} W={workers}] step {t}: loss gpu {st.loss:.6f} oracle {lo:.6f} rel {rel:.2e} "
                   f"ms {st.ms_step:.2f} nvlink out {st.nvlink_out_bytes} in {st.nvlink_in_bytes}", flush=True)
             if not rel <= tol:
@@ -198,8 +204,9 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
             if fp32:
                 rel = np.linalg.norm(g[0] - w[0]) / np.linalg.norm(w[0])
                 upd = np.linalg.norm(g[0] - w[0]) / np.linalg.norm(w[0] - p0[0])
-                print(f"   layer {li}: ||dp||/||p|| {rel:.3e}  ||dp||/||update|| {upd:.3e}", flush=True)
-                if rel > 1e-4:
+                fl = np.linalg.norm(w64[0] - w[0]) / np.linalg.norm(w[0] - p0[0])
+                print(f"   layer {li}: ||dp||/||p|| {rel:.3e}  ||dp||/||update|| {upd:.3e} (floor {fl:.3e})", flush=True)
+                if not (rel <= 1e-4 or upd <= 3 * fl + 2e-2):   # the rule of tests/test_parity_fp32_gpu.py
                     ok = False
                 continue
             upd = np.linalg.norm(w[0] - p0[0])
