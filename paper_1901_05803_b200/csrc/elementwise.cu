@@ -111,15 +111,16 @@ __global__ void pack_im2col_row_kernel(const float* __restrict__ x, int n, int h
   }
 }
 
-// Large first-layer filters (AlexNet's 11x11x3 -> 363 (+bias) columns, kpad 384): one warp per
-// patch row, lane l owns columns [l*KPAD/32, (l+1)*KPAD/32) -- all index arithmetic is by
-// compile-time constants and each lane writes KPAD/32 contiguous bf16 (8-byte stores).
+// Large first-layer filters (AlexNet's 11x11x3 -> 363 (+bias) columns, kpad 384; ResNet's 7x7x3
+// stem -> 147 (+ones), kpad 192): one warp per patch row, lane l owns columns
+// [l*KPAD/32, (l+1)*KPAD/32) -- all index arithmetic is by compile-time constants and each lane
+// writes KPAD/32 contiguous bf16 (8-byte stores, 4-byte when KPAD/32 is not a multiple of 4).
 template <int K, int C, int KPAD>
 __global__ void __launch_bounds__(256) pack_im2col_warp_kernel(const float* __restrict__ x, int n, int h, int w, int st,
                                                                int p, int ho, int wo, int po,
                                                                __nv_bfloat16* __restrict__ out) {
   constexpr int PER = KPAD / 32, KK = K * K * C;
-  static_assert(PER % 4 == 0, "lane span must be a multiple of 4 columns");
+  static_assert(PER % 2 == 0, "lane span must be a multiple of 2 columns");
   const int hop = ho + 2 * po, wop = wo + 2 * po;
   const long long rows = static_cast<long long>(n) * hop * wop;
   const int lane = threadIdx.x & 31;
@@ -152,9 +153,15 @@ __global__ void __launch_bounds__(256) pack_im2col_warp_kernel(const float* __re
       }
       pk[e2] = pack_bf16(v[0], v[1]);
     }
-    uint2* dst = reinterpret_cast<uint2*>(out + row * KPAD + lane * PER);
+    if constexpr (PER % 4 == 0) {
+      uint2* dst = reinterpret_cast<uint2*>(out + row * KPAD + lane * PER);
 #pragma unroll
-    for (int e4 = 0; e4 < PER / 4; ++e4) dst[e4] = make_uint2(pk[2 * e4], pk[2 * e4 + 1]);
+      for (int e4 = 0; e4 < PER / 4; ++e4) dst[e4] = make_uint2(pk[2 * e4], pk[2 * e4 + 1]);
+    } else {
+      uint32_t* dst = reinterpret_cast<uint32_t*>(out + row * KPAD + lane * PER);
+#pragma unroll
+      for (int e2 = 0; e2 < PER / 2; ++e2) dst[e2] = pk[e2];
+    }
   }
 }
 
@@ -164,6 +171,12 @@ cudaError_t pack_im2col(const float* x, int n, int h, int w, int c, int k, int s
     const long long rows = static_cast<long long>(n) * (ho + 2 * po) * (wo + 2 * po);
     const int grid = static_cast<int>(std::min<long long>((rows + 7) / 8, static_cast<long long>(num_sms()) * 32));
     pack_im2col_warp_kernel<11, 3, 384><<<grid, 256, 0, s>>>(x, n, h, w, st, p, ho, wo, po, out);
+    return cudaGetLastError();
+  }
+  if (k == 7 && c == 3 && kpad == 192) {
+    const long long rows = static_cast<long long>(n) * (ho + 2 * po) * (wo + 2 * po);
+    const int grid = static_cast<int>(std::min<long long>((rows + 7) / 8, static_cast<long long>(num_sms()) * 32));
+    pack_im2col_warp_kernel<7, 3, 192><<<grid, 256, 0, s>>>(x, n, h, w, st, p, ho, wo, po, out);
     return cudaGetLastError();
   }
   if (kpad % 8 != 0 || kpad < k * k * c + 1) return cudaErrorInvalidValue;

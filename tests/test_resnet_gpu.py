@@ -14,7 +14,7 @@ Bytes: the ranks' count_wire-site counts == volume_ralp / volume_baseline of the
 Numerics.  At b=8 with batch norm and bf16 storage the step is chaotic: the oracle's own
 fp32-vs-fp64 spread after two steps is ~1.2x the update itself, so a free-running comparison cannot
 discriminate.  The free-running tests therefore check the bytes, the first step's loss (forward
-only, 2e-3) and parameters within 2 * floor + 0.02 of the update; the sharp check is per block:
+only, 5e-3) and parameters within 2 * floor + 0.02 of the update; the sharp check is per block:
 test_resnet50_teacher_forced_blocks recomputes every layer (stem, pool, each bottleneck block,
 average pool) from the GPU's OWN stored input -- and its backward from the GPU's own upstream
 gradient -- with the oracle's autograd restatement, and requires outputs within 5e-3 and input /
@@ -36,6 +36,10 @@ pytestmark = pytest.mark.gpu
 # backwards, whose mean subtractions cancel most of dz and magnify the rounding differences)
 FWD_TOL = 5e-3
 BWD_TOL = 5e-2
+# first-step loss (forward only, relative): the GPU's own step-0 loss varies run to run by up
+# to ~2.5e-3 at b=8 (batch-norm statistics are float-atomic sums in nondeterministic order and the
+# differences ride through 50 bf16 storage points); observed |gpu - oracle| / oracle <= 2.5e-3
+LOSS_TOL = 5e-3
 
 
 def _run(batch, strategy, steps, lr, split=None):
@@ -64,7 +68,7 @@ def _run(batch, strategy, steps, lr, split=None):
         print(f"  step {t}: loss gpu {st.loss:.6f} oracle {lo:.6f} bytes {st.logical_bytes} launches {st.launches} "
               f"ms {st.ms_step:.2f}")
         assert st.logical_bytes == wire == expect
-        if t == 0 and abs(st.loss - lo) > 2e-3 * abs(lo):
+        if t == 0 and abs(st.loss - lo) > LOSS_TOL * abs(lo):
             bad.append(f"step {t}: loss {st.loss} vs oracle {lo}")
     got = ex.get_params()
     ex.close()
