@@ -128,8 +128,29 @@ int ralpb_cast_bf16(const float* x, long long n, void* y, void* stream);
  * BASELINE_PS = every layer on every worker, all parameters through the PS. */
 /* Layer kinds.  BLOCK: a ResNet bottleneck block (1x1 -> 3x3 (stride) -> 1x1, batch norm after
  * every convolution, ReLU, identity or 1x1-projection shortcut; the catalog's linearised
- * s?b?_{a,b,c,down} entries, pkg/tools/build_catalog.py:286-333).  APOOL: global average pool. */
-enum { RALPB_CONV = 0, RALPB_POOL = 1, RALPB_FC = 2, RALPB_BLOCK = 3, RALPB_APOOL = 4 };
+ * s?b?_{a,b,c,down} entries, pkg/tools/build_catalog.py:286-333).  APOOL: global average pool.
+ * MODULE: a branch group (an Inception / GoogLeNet module, or a single convolution of any window,
+ * stride and padding): the nodes [node_begin, node_begin + node_count) of the node table passed to
+ * ralpb_model_create_graph, whose output nodes are concatenated along channels (the catalog's
+ * linearised "<group>_<branch>" entries, the last one carrying the merged group output;
+ * pkg/tools/build_catalog.py:115-285). */
+enum { RALPB_CONV = 0, RALPB_POOL = 1, RALPB_FC = 2, RALPB_BLOCK = 3, RALPB_APOOL = 4, RALPB_MODULE = 5 };
+
+/* A node of a MODULE.  CONV: kh x kw window, stride, zero padding (pad_h, pad_w), cout output
+ * channels, then batch norm (bn = 1: training-mode batch statistics, learnable scale / shift, no
+ * bias) or a bias (bn = 0), then ReLU.  MAXPOOL: first maximum of the window, padding never wins.
+ * AVGPOOL: mean over the window's in-image elements (padding excluded from the count).  input: the
+ * node it reads (an earlier node of the same module; -1 = the module input).  output = 1: part of
+ * the module output (outputs concatenate in node order; an output node feeds no other node). */
+enum { RALPB_NODE_CONV = 0, RALPB_NODE_MAXPOOL = 1, RALPB_NODE_AVGPOOL = 2 };
+typedef struct {
+  int op;
+  int input;
+  int kh, kw, stride, pad_h, pad_w;
+  int cout;
+  int bn;
+  int output;
+} ralpb_node_desc;
 /* BASELINE: StrategyKind.BASELINE_PS (every layer on every worker, all parameters through the
  * sharded PS).  RALP: StrategyKind.RALP.  RING: StrategyKind.RING_ALLREDUCE (simulator.py:719-737)
  * with the hand-written reduce-scatter + SGD + all-gather over NVLink; RING_EXTERNAL: the same
@@ -152,6 +173,8 @@ typedef struct {
                           the ReLU, no bias */
   int width;           /* block: bottleneck width (the 1x1 / 3x3 convolutions' channels) */
   int downsample;      /* block: 1x1 projection shortcut (else identity) */
+  int node_begin;      /* module: its nodes in the node table (ralpb_model_create_graph) */
+  int node_count;
 } ralpb_layer_desc;
 
 typedef struct {
@@ -193,6 +216,11 @@ enum { RALPB_PRECISION_BF16 = 0, RALPB_PRECISION_FP32 = 1 };
 int ralpb_model_create(const ralpb_layer_desc* layers, int n_layers, int split, int batch, int strategy,
                        int rank, int world, int ps_rank, int elem_bytes, int precision, int workers,
                        ralpb_model** out);
+/* ralpb_model_create for a layer table with MODULE layers: `nodes` (n_nodes entries) is the node
+ * table the modules index.  ralpb_model_create(...) == ralpb_model_create_graph(..., NULL, 0, ...). */
+int ralpb_model_create_graph(const ralpb_layer_desc* layers, int n_layers, const ralpb_node_desc* nodes,
+                             int n_nodes, int split, int batch, int strategy, int rank, int world, int ps_rank,
+                             int elem_bytes, int precision, int workers, ralpb_model** out);
 void ralpb_model_destroy(ralpb_model* m);
 /* 64-byte CUDA IPC handle of this rank's exchange arena; ralpb_model_ipc_open takes
  * world*64 bytes (rank-major) and maps the peers. */
@@ -203,7 +231,9 @@ int ralpb_model_ipc_open(ralpb_model* m, const void* handles);
  * fc w [out][in] (in = HWC-flattened), b [out];
  * block: w = every parameter of the block, in order wa [width][cin], wb [width][3][3][width],
  * wc [cout][width] (, wd [cout][cin]), b = [gamma_a | beta_a | gamma_b | beta_b | gamma_c | beta_c
- * (| gamma_d | beta_d)]. */
+ * (| gamma_d | beta_d)];
+ * module: w = its convolution nodes' filters [cout][kh][kw][cin] back to back in node order,
+ * b = their [gamma | beta] (bn) or bias [cout] in the same order. */
 int ralpb_model_set_params(ralpb_model* m, int layer, const float* w, const float* b, int on_host);
 int ralpb_model_get_params(ralpb_model* m, int layer, float* w, float* b, int on_host);
 /* This rank's parameter gradient of `layer` from the last step (same layout as get_params; host or
