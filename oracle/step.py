@@ -230,9 +230,55 @@ def param_count(L) -> int:
         cin, width, cout, down = L["cin"], L["width"], L["cout"], L.get("downsample", 0)
         return (width * cin + 9 * width * width + cout * width + (cout * cin if down else 0)
                 + 2 * (2 * width + cout + (cout if down else 0)))
+    if L["kind"] == "module":
+        return sum(w.numel() + b.numel() for w, b in _module_shapes(L))
     if L["kind"] == "fc":
         return L["cin"] * L["cout"] + L["cout"]
     return 0
+
+
+def _module_shapes(L):
+    """Per conv node of a module layer: (empty filter tensor [cout][kh][kw][cin], empty bn/bias)."""
+    chans, out = [], []
+    for nd in L["nodes"]:
+        ci = L["cin"] if nd["input"] < 0 else chans[nd["input"]]
+        chans.append(nd["cout"] if nd["op"] == "conv" else ci)
+        if nd["op"] == "conv":
+            out.append((torch.empty(nd["cout"], nd["kh"], nd["kw"], ci),
+                        torch.empty(nd["cout"] * (2 if nd["bn"] else 1))))
+    return out
+
+
+def _module_forward(L, p, x, R, dtype):
+    """A branch group (graph.cu): nodes in order over the module input x (NCHW), conv nodes with
+    batch norm + ReLU or bias + ReLU, max pools (padding never wins), average pools (padding not
+    counted); output nodes concatenated along channels.  p = (filters, bn / bias) flat, conv nodes
+    in order, filters [cout][kh][kw][cin]."""
+    w, b = p
+    conv_ids = [j for j, nd in enumerate(L["nodes"]) if nd["op"] == "conv"]
+    pw, ow, ob = {}, 0, 0
+    for (wt, bt), j in zip(_module_shapes(L), conv_ids):
+        pw[j] = (w[ow:ow + wt.numel()].reshape(wt.shape).permute(0, 3, 1, 2).to(dtype), b[ob:ob + bt.numel()].to(dtype))
+        ow += wt.numel()
+        ob += bt.numel()
+    vals = []
+    for j, nd in enumerate(L["nodes"]):
+        src = x if nd["input"] < 0 else vals[nd["input"]]
+        win, st, pad = (nd["kh"], nd["kw"]), nd["stride"], (nd["ph"], nd["pw"])
+        if nd["op"] == "conv":
+            wt, bt = R(pw[j][0]), pw[j][1]
+            if nd["bn"]:
+                c = nd["cout"]
+                z = R(F.conv2d(src, wt, None, stride=st, padding=pad))
+                y = R(torch.relu(_bn(z, bt[:c], bt[c:])))
+            else:
+                y = R(torch.relu(F.conv2d(src, wt, bt, stride=st, padding=pad)))
+        elif nd["op"] == "maxpool":
+            y = R(F.max_pool2d(src, win, st, pad))
+        else:
+            y = R(F.avg_pool2d(src, win, st, pad, count_include_pad=False))
+        vals.append(y)
+    return torch.cat([v for v, nd in zip(vals, L["nodes"]) if nd["output"]], dim=1)
 
 
 # ---------------------------------------------------------------- branchy models (autograd restatement)
@@ -285,8 +331,9 @@ def _branchy_forward(layers, params, x, R, dtype):
                 c = L["cout"]
                 pre = R(F.conv2d(x, wt, None, stride=L["stride"], padding=L["pad"]))
                 x = R(torch.relu(_bn(pre, b[:c].to(dtype), b[c:].to(dtype))))
-            else:
-                x = R(torch.relu(F.conv2d(x, wt, b.to(dtype), stride=L["stride"], padding=L["pad"])))
+            else:   # the first (im2col) conv carries its bias in a bf16 filter column
+                bias = R(b.to(dtype)) if L is layers[0] else b.to(dtype)
+                x = R(torch.relu(F.conv2d(x, wt, bias, stride=L["stride"], padding=L["pad"])))
         elif k == "pool":
             x = R(F.max_pool2d(x, L["k"], L["stride"], L["pad"]))
         elif k == "block":
@@ -297,6 +344,8 @@ def _branchy_forward(layers, params, x, R, dtype):
             c = _bn(R(F.conv2d(bb, R(ws[2]))), *bns[2])
             short = _bn(R(F.conv2d(x[:, :, ::s, ::s], R(ws[3]))), *bns[3]) if L.get("downsample") else x
             x = R(torch.relu(c + short))
+        elif k == "module":
+            x = _module_forward(L, p, x, R, dtype)
         elif k == "apool":
             x = R(x.mean(dim=(2, 3), keepdim=True))
         elif k == "fc":
@@ -355,7 +404,8 @@ def _train_step_branchy(st: OracleState, strategy: str, workers: int, batches, *
 
 
 def _branchy(layers) -> bool:
-    return any(L["kind"] in ("block", "apool") or L.get("bn") or (L["kind"] == "pool" and L.get("pad")) for L in layers)
+    return any(L["kind"] in ("block", "apool", "module") or L.get("bn") or (L["kind"] == "pool" and L.get("pad"))
+               for L in layers)
 
 
 def train_step(st: OracleState, strategy: str, workers: int, batches, *, lr: float = 0.01, mu: float = 0.9,

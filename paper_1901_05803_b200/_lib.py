@@ -47,6 +47,8 @@ SIGNATURES: dict[str, tuple] = {
     "ralpb_conv_weight_prep": (c_i, [c_fp, c_i, c_i, c_i, c_vp, c_vp, c_vp]),
     "ralpb_cast_bf16": (c_i, [c_fp, c_ll, c_vp, c_vp]),
     "ralpb_model_create": (c_i, [c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, C.POINTER(c_vp)]),
+    "ralpb_model_create_graph": (c_i, [c_vp, c_i, c_vp, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i, c_i,
+                                       C.POINTER(c_vp)]),
     "ralpb_model_destroy": (None, [c_vp]),
     "ralpb_model_ipc_handle": (c_i, [c_vp, c_vp]),
     "ralpb_model_ipc_open": (c_i, [c_vp, c_vp]),
@@ -68,7 +70,14 @@ SIGNATURES: dict[str, tuple] = {
 class LayerDesc(C.Structure):
     """ralpb_layer_desc (include/ralpb.h)."""
     _fields_ = [("kind", c_i), ("k", c_i), ("stride", c_i), ("pad", c_i), ("h", c_i), ("w", c_i),
-                ("cin", c_i), ("cout", c_i), ("relu", c_i), ("bn", c_i), ("width", c_i), ("downsample", c_i)]
+                ("cin", c_i), ("cout", c_i), ("relu", c_i), ("bn", c_i), ("width", c_i), ("downsample", c_i),
+                ("node_begin", c_i), ("node_count", c_i)]
+
+
+class NodeDesc(C.Structure):
+    """ralpb_node_desc (include/ralpb.h): one node of a MODULE layer."""
+    _fields_ = [("op", c_i), ("input", c_i), ("kh", c_i), ("kw", c_i), ("stride", c_i), ("pad_h", c_i),
+                ("pad_w", c_i), ("cout", c_i), ("bn", c_i), ("output", c_i)]
 
 
 class LaunchRec(C.Structure):
@@ -89,7 +98,8 @@ class StepStats(C.Structure):
                 ("nvlink_in_bytes", c_ll)]
 
 
-RALPB_CONV, RALPB_POOL, RALPB_FC, RALPB_BLOCK, RALPB_APOOL = 0, 1, 2, 3, 4
+RALPB_CONV, RALPB_POOL, RALPB_FC, RALPB_BLOCK, RALPB_APOOL, RALPB_MODULE = 0, 1, 2, 3, 4, 5
+RALPB_NODE_CONV, RALPB_NODE_MAXPOOL, RALPB_NODE_AVGPOOL = 0, 1, 2
 RALPB_STRATEGY_BASELINE, RALPB_STRATEGY_RALP, RALPB_STRATEGY_RING, RALPB_STRATEGY_RING_EXTERNAL = 0, 1, 2, 3
 RALPB_STRATEGY_RALP_MPS = 4
 RALPB_PRECISION_BF16, RALPB_PRECISION_FP32 = 0, 1

@@ -11,16 +11,23 @@ struct ralpb_model {
 
 extern "C" {
 
-int ralpb_model_create(const ralpb_layer_desc* layers, int n_layers, int split, int batch, int strategy,
-                       int rank, int world, int ps_rank, int elem_bytes, int precision, int workers,
-                       ralpb_model** out) {
+int ralpb_model_create_graph(const ralpb_layer_desc* layers, int n_layers, const ralpb_node_desc* nodes,
+                             int n_nodes, int split, int batch, int strategy, int rank, int world, int ps_rank,
+                             int elem_bytes, int precision, int workers, ralpb_model** out) {
   std::string why;
   Model* m = nullptr;
-  if (model_create(layers, n_layers, split, batch, strategy, rank, world, ps_rank, elem_bytes, precision, workers, &m,
-                   &why))
+  if (model_create(layers, n_layers, nodes, n_nodes, split, batch, strategy, rank, world, ps_rank, elem_bytes, precision,
+                   workers, &m, &why))
     return set_error("ralpb_model_create: " + why);
   *out = new ralpb_model{m};
   return 0;
+}
+
+int ralpb_model_create(const ralpb_layer_desc* layers, int n_layers, int split, int batch, int strategy,
+                       int rank, int world, int ps_rank, int elem_bytes, int precision, int workers,
+                       ralpb_model** out) {
+  return ralpb_model_create_graph(layers, n_layers, nullptr, 0, split, batch, strategy, rank, world, ps_rank, elem_bytes,
+                                  precision, workers, out);
 }
 
 void ralpb_model_destroy(ralpb_model* m) {

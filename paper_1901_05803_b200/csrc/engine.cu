@@ -30,6 +30,7 @@
 #include "gemm_host.cuh"
 #include "pair.cuh"
 #include "block.cuh"
+#include "graph.cuh"
 #include "resnet.cuh"
 
 namespace ralpb {
@@ -91,9 +92,9 @@ int pair_relayout(Model* m, bool front, bool fc, cudaStream_t s, std::string* wh
 
 }  // namespace
 
-int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int batch, int strategy,
-                 int rank, int world, int ps_rank, int elem_bytes, int precision, int workers, Model** out,
-                 std::string* why) {
+int model_create(const ralpb_layer_desc* layers, int n_layers, const ralpb_node_desc* nodes, int n_nodes, int split,
+                 int batch, int strategy, int rank, int world, int ps_rank, int elem_bytes, int precision, int workers,
+                 Model** out, std::string* why) {
   if (n_layers < 2 || batch < 1 || world < 1 || world > kMaxRanks || rank < 0 || rank >= world ||
       ps_rank < 0 || ps_rank >= world) {
     *why = "bad model configuration";
@@ -266,6 +267,31 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
       o.c = in.c;
       o.pad = (i + 1 < nconv && layers[i + 1].kind == RALPB_CONV) ? layers[i + 1].pad : 0;
       if (in.c % 8 != 0) return fail("pool channels must be a multiple of 8");
+    } else if (d.kind == RALPB_MODULE) {
+      if (precision != RALPB_PRECISION_BF16) return fail("modules run in bf16 precision");
+      if (in.pad != 0) return fail("layer " + std::to_string(i) + ": a module reads an unpadded activation");
+      if (d.node_begin < 0 || d.node_count < 1 || d.node_begin + d.node_count > n_nodes)
+        return fail("layer " + std::to_string(i) + ": node range outside the node table");
+      m->branchy = true;
+      ModuleBufs k;
+      std::vector<std::pair<long long, long long>> runs;
+      long long count = 0;
+      const long long first = off;
+      std::string w2;
+      if (module_build(k, nodes + d.node_begin, d.node_count, nb, d.h, d.w, in.c, &off, &runs, &count, &w2))
+        return fail("layer " + std::to_string(i) + ": " + w2);
+      if (d.cout != k.cout) return fail("layer " + std::to_string(i) + ": module output channels differ from its nodes'");
+      if (i < m->split) {
+        for (auto& r : runs) real_runs.push_back(r);
+        m->real_front += count;
+      } else {
+        m->real_bseg += count;
+      }
+      f.w_off = first;
+      f.w_count = off - first;
+      f.mod = static_cast<int>(m->modules.size());
+      o.h = k.ho; o.w = k.wo; o.c = k.cout; o.pad = 0;
+      m->modules.push_back(std::move(k));
     } else if (d.kind == RALPB_BLOCK || d.kind == RALPB_APOOL) {
       if (precision != RALPB_PRECISION_BF16) return fail("bottleneck blocks run in bf16 precision");
       if (in.pad != 0) return fail("layer " + std::to_string(i) + ": a block / average pool reads an unpadded activation");
@@ -315,8 +341,8 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
   const ActBuf& cut = m->acts.back();
   if (cut.pad != 0) return fail("the FC tail's input must be a pooling output");
   for (int i : {m->split - 1, nconv - 1})   // the backward of these layers needs their stored output
-    if (i >= 0 && (m->front[i].kind == RALPB_BLOCK || m->front[i].bn))
-      return fail("a cut must follow a pool or the average pool, not a block / batch-normalised conv");
+    if (i >= 0 && (m->front[i].kind == RALPB_BLOCK || m->front[i].kind == RALPB_MODULE || m->front[i].bn))
+      return fail("a cut must follow a pool or the average pool, not a block / module / batch-normalised conv");
   m->cut_elems = cut.h * cut.w * cut.c;
   if (!m->bseg) m->n_front = align_up(off, kShardAlign);
   m->bseg_end = align_up(off, 4);
@@ -474,6 +500,10 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int ba
     if (f.kind == RALPB_BLOCK) {
       if (block_alloc(m, m->blocks[f.blk], why)) return fail(*why);
       if (m->blocks[f.blk].cmax > 2048) return fail("block channels above 2048");
+    } else if (f.kind == RALPB_MODULE) {
+      if (module_alloc(m, m->modules[f.mod], why)) return fail(*why);
+      for (const ModNode& q : m->modules[f.mod].nodes)
+        if (q.d.op == RALPB_NODE_CONV && q.d.cout > 2048) return fail("module conv channels above 2048");
     } else if (f.bn) {
       const size_t rows = static_cast<size_t>(m->acts[i + 1].rows());
       if (!(f.pre = alloc<bf16>(m, rows * f.g.cout, why)) || !(f.dpre = alloc<bf16>(m, rows * f.g.cout, why)) ||
@@ -654,6 +684,22 @@ int model_set_params(Model* m, int layer, const float* w, const float* b, int on
     RALPB_TRY(cudaStreamSynchronize(m->stream));
     return 0;
   }
+  if (layer < m->nconv && m->front[layer].kind == RALPB_MODULE) {
+    // w: the conv nodes' filters back to back; b: their gamma|beta or bias in the same order
+    ModuleBufs& k = m->modules[m->front[layer].mod];
+    std::vector<std::pair<long long, long long>> wr, br;
+    module_param_runs(k, &wr, &br);
+    long long pw = 0, pb = 0;
+    for (size_t q = 0; q < wr.size(); ++q) {
+      RALPB_TRY(cudaMemcpy(m->P + wr[q].first, w + pw, wr[q].second * sizeof(float), kind));
+      RALPB_TRY(cudaMemcpy(m->P + br[q].first, b + pb, br[q].second * sizeof(float), kind));
+      pw += wr[q].second;
+      pb += br[q].second;
+    }
+    if (module_prep(m, k, m->stream, why)) return 1;
+    RALPB_TRY(cudaStreamSynchronize(m->stream));
+    return 0;
+  }
   if (layer < m->nconv) {
     FrontLayer& f = m->front[layer];
     if (f.kind != RALPB_CONV) { *why = "layer has no parameters"; return 1; }
@@ -726,6 +772,18 @@ static int read_layer(Model* m, int layer, float* w, float* b, size_t off, std::
       RALPB_TRY(cudaMemcpy(b + pg, self + og[q], sg[q] * sizeof(float), cudaMemcpyDefault));
       pw += sw[q];
       pg += sg[q];
+    }
+    return 0;
+  }
+  if (layer < m->nconv && m->front[layer].kind == RALPB_MODULE) {
+    std::vector<std::pair<long long, long long>> wr, br;
+    module_param_runs(m->modules[m->front[layer].mod], &wr, &br);
+    long long pw = 0, pb = 0;
+    for (size_t q = 0; q < wr.size(); ++q) {
+      RALPB_TRY(cudaMemcpy(w + pw, self + wr[q].first, wr[q].second * sizeof(float), cudaMemcpyDefault));
+      RALPB_TRY(cudaMemcpy(b + pb, self + br[q].first, br[q].second * sizeof(float), cudaMemcpyDefault));
+      pw += wr[q].second;
+      pb += br[q].second;
     }
     return 0;
   }
@@ -1173,6 +1231,13 @@ int launch_conv_backward(Model* m, int lo, int hi, const bf16* cur, const ActBuf
       db_done = false;
       continue;
     }
+    if (f.kind == RALPB_MODULE) {
+      const bool need = i > lo || dgrad_lo;
+      if (module_backward(m, m->modules[f.mod], in.ptr, out.ptr, cur, need ? dst_i : nullptr, why)) return 1;
+      cur = dst_i;
+      db_done = false;
+      continue;
+    }
     if (f.kind == RALPB_APOOL) {
       RALPB_TRY(avgpool_bwd(cur, in.n, in.h, in.w, in.c, MutAct4{dst_i, in.pad}, m->stream));
       ++m->launches;
@@ -1261,6 +1326,10 @@ int launch_conv_forward(Model* m, int lo, int hi, const float* img, const ActBuf
       if (block_forward(m, m->blocks[f.blk], in.ptr, out.ptr, why)) return 1;
       continue;
     }
+    if (f.kind == RALPB_MODULE) {
+      if (module_forward(m, m->modules[f.mod], in.ptr, out.ptr, why)) return 1;
+      continue;
+    }
     if (f.kind == RALPB_APOOL) {
       RALPB_TRY(avgpool_fwd(Act4{in.ptr, in.pad}, in.n, in.h, in.w, in.c, out.ptr, s));
       ++m->launches;
@@ -1320,6 +1389,10 @@ int prep_filters(Model* m, bool forward, bool dgrad, cudaStream_t s, std::string
     FrontLayer& f = m->front[i];
     if (f.kind == RALPB_BLOCK) {   // all of a block's operand copies with the forward ones
       if (forward && m->blocks[f.blk].wa != nullptr && block_prep(m, m->blocks[f.blk], s, why)) return 1;
+      continue;
+    }
+    if (f.kind == RALPB_MODULE) {
+      if (forward && module_prep(m, m->modules[f.mod], s, why)) return 1;
       continue;
     }
     if (f.kind != RALPB_CONV || f.wf == nullptr) continue;   // (layers this rank does not run)

@@ -36,6 +36,32 @@ struct BlockBufs {
   int cmax = 0;
 };
 
+// A branch group (RALPB_MODULE, graph.cu): nodes in topological order, output nodes
+// concatenated along channels into the module output [n][ho][wo][cout] (unpadded NHWC).
+struct ModNode {
+  ralpb_node_desc d{};
+  int cin = 0, h = 0, w = 0, ho = 0, wo = 0;   // per-sample input / output geometry
+  int out_off = 0;             // output node: channel offset in the module output
+  int consumers = 0;           // nodes reading this node's output
+  bool direct = false;         // conv 1x1 / stride 1 / no padding: a GEMM over the input rows
+  long long w_off = -1, b_off = -1;   // conv: filters [cout][kh*kw*cin], then gamma|beta or bias
+  __nv_bfloat16* wbf = nullptr;       // conv: bf16 copy of the filters
+  __nv_bfloat16* z = nullptr;         // bn conv: output before the batch norm
+  __nv_bfloat16* y = nullptr;         // non-output node: its output
+  __nv_bfloat16* dy = nullptr;        // non-output node: gradient w.r.t. its output
+  uint8_t* idx = nullptr;             // max pool: window position of the first max (255: not > 0)
+  float* stats = nullptr;             // bn conv: [2][cout] mean / rstd
+  long long K() const { return static_cast<long long>(d.kh) * d.kw * cin; }
+};
+struct ModuleBufs {
+  int n = 0, h = 0, w = 0, cin = 0, ho = 0, wo = 0, cout = 0;
+  std::vector<ModNode> nodes;
+  __nv_bfloat16* col = nullptr;   // im2col patches / their gradient (largest conv node)
+  __nv_bfloat16* dz = nullptr;    // gradient w.r.t. a conv node's pre-activation (largest node)
+  __nv_bfloat16* tmp = nullptr;   // a contribution to a gradient that is accumulated
+  long long col_elems = 0, dz_elems = 0, tmp_elems = 0;
+};
+
 struct FrontLayer {
   int kind = 0;                // RALPB_CONV / RALPB_POOL / RALPB_BLOCK / RALPB_APOOL
   ConvGeom g{};                // conv geometry (cin padded to 16)
@@ -58,6 +84,7 @@ struct FrontLayer {
   __nv_bfloat16* dpre = nullptr;    // ... and the gradient w.r.t. it
   float* bn_stats = nullptr;        // bn conv: [2][cout] mean / rstd
   int blk = -1;                // RALPB_BLOCK: index into Model::blocks
+  int mod = -1;                // RALPB_MODULE: index into Model::modules
 };
 
 struct FcLayer {
@@ -86,6 +113,7 @@ struct Model {
   std::vector<ralpb_layer_desc> desc;
   std::vector<FrontLayer> front;
   std::vector<BlockBufs> blocks;   // RALPB_BLOCK layers
+  std::vector<ModuleBufs> modules; // RALPB_MODULE layers
   bool branchy = false;            // the model has blocks / batch-normalised convolutions
   float* bn_work = nullptr;        // [2][2048] batch-norm reduction scratch
   std::vector<FcLayer> back;
@@ -197,7 +225,8 @@ struct Model {
   bool stats_valid = false;
 };
 
-int model_create(const ralpb_layer_desc* layers, int n_layers, int split, int batch, int strategy,
+int model_create(const ralpb_layer_desc* layers, int n_layers, const ralpb_node_desc* nodes, int n_nodes, int split,
+                 int batch, int strategy,
                  int rank, int world, int ps_rank, int elem_bytes, int precision, int workers, Model** out,
                  std::string* why);
 void model_destroy(Model* m);

@@ -1,0 +1,597 @@
+// Branch groups executed (Inception-v3 / GoogLeNet modules; also any single
+// convolution the slab kernels do not cover -- strided, unpadded or asymmetric windows).
+//
+// A module is a small DAG over its input x (graph.cuh ModNode): convolutions (kh x kw, stride,
+// zero padding; batch norm + ReLU or bias + ReLU), max pools and average pools.  Output nodes are
+// concatenated along channels: each writes its own channel slice of the module output directly
+// (pixel stride = the module's channels), so the concatenation costs no copy, and its backward
+// reads the slices of dy in place.  Semantics (the geometry behind the reference catalog's
+// linearised inception-v3 / googlenet entries, pkg/tools/build_catalog.py:115-285):
+//   conv     z = conv(x, W) (bf16);  y = relu(bn(z)) (training-mode batch statistics) or
+//            y = relu(conv(x, W) + b)
+//   maxpool  first maximum of the window, padding never wins
+//   avgpool  mean over the in-image elements of the window (padding not counted)
+// Contractions run on the tcgen05 GEMM engine: a 1x1 / stride-1 / unpadded convolution is one GEMM
+// over the NHWC rows; every other window goes through an im2col patch matrix (forward, backward-
+// filter) and a patch-gradient GEMM + col2im gather (backward-data, deterministic: no atomics).
+// Gradients of a tensor read by several nodes are accumulated in bf16 (the first contribution
+// stores, later ones add).
+#include <algorithm>
+#include "elementwise.cuh"
+#include "gemm_host.cuh"
+#include "graph.cuh"
+#include "resnet.cuh"
+
+namespace ralpb {
+
+namespace {
+
+constexpr float kBnEps = 1e-5f;
+
+#define RALPB_TRY(expr)                                   \
+  do {                                                    \
+    cudaError_t _e = (expr);                              \
+    if (_e != cudaSuccess) {                              \
+      if (why->empty()) *why = std::string(#expr);        \
+      *why += std::string(": ") + cudaGetErrorString(_e); \
+      return 1;                                           \
+    }                                                     \
+  } while (0)
+
+int grid_for(long long work, int threads) {
+  const long long blocks = (work + threads - 1) / threads;
+  const long long cap = static_cast<long long>(num_sms()) * 8;
+  return static_cast<int>(std::max<long long>(1, std::min(blocks, cap)));
+}
+
+__device__ __forceinline__ void load8(const bf16* p, float* v) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const bf16* b = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(b[j]);
+}
+__device__ __forceinline__ void store8(bf16* p, const float* v) {
+  uint4 u;
+  bf16* b = reinterpret_cast<bf16*>(&u);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) b[j] = __float2bfloat16_rn(v[j]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+// Decomposition of a flat (pixel, 8-channel group) index; pixel = (img*h + y)*w + x.
+struct Pix {
+  int g, p, img, y, x;
+  __device__ __forceinline__ Pix(long long i, int groups, int h, int w) {
+    p = static_cast<int>(i / groups);
+    g = static_cast<int>(i - static_cast<long long>(p) * groups);
+    img = p / (h * w);
+    const int r = p - img * h * w;
+    y = r / w;
+    x = r - y * w;
+  }
+};
+
+// ------------------------------------------------------------------ layouts
+// out [n*ho*wo][kh*kw*c]: column (r*kw + s)*c + ch = x[img][oy*st + r - ph][ox*st + s - pw][ch]
+// (0 outside the image); x has pixel stride ldx.
+__global__ void im2col_gen_kernel(const bf16* __restrict__ x, int ldx, int n, int h, int w, int c, int kh, int kw,
+                                  int st, int ph, int pw, int ho, int wo, bf16* __restrict__ out) {
+  const int groups = c >> 3, taps = kh * kw;
+  const long long total = static_cast<long long>(n) * ho * wo * taps * groups;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long t = i / groups;   // row * taps + tap
+    const int g = static_cast<int>(i - t * groups);
+    const long long row = t / taps;
+    const int tap = static_cast<int>(t - row * taps);
+    const int img = static_cast<int>(row / (ho * wo));
+    const int rr = static_cast<int>(row - static_cast<long long>(img) * ho * wo);
+    const int oy = rr / wo, ox = rr - oy * wo;
+    const int r = tap / kw, s = tap - r * kw;
+    const int iy = oy * st + r - ph, ix = ox * st + s - pw;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (iy >= 0 && iy < h && ix >= 0 && ix < w)
+      v = *reinterpret_cast<const uint4*>(x + (static_cast<long long>(img * h + iy) * w + ix) * ldx + g * 8);
+    *reinterpret_cast<uint4*>(out + t * c + g * 8) = v;
+  }
+}
+
+// dx[img][y][x][ch] (+)= sum over the taps (r, s) whose output position (oy, ox) reads (y, x) of
+// dcol[(img*ho + oy)*wo + ox][(r*kw + s)*c + ch]  -- the adjoint of im2col_gen, gathered
+__global__ void col2im_gen_kernel(const bf16* __restrict__ dcol, int n, int h, int w, int c, int kh, int kw, int st,
+                                  int ph, int pw, int ho, int wo, bf16* __restrict__ dx, int ldx, int acc) {
+  const int groups = c >> 3;
+  const long long total = static_cast<long long>(n) * h * w * groups;
+  const long long rowlen = static_cast<long long>(kh) * kw * c;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const Pix q(i, groups, h, w);
+    float a[8];
+    bf16* dst = dx + static_cast<long long>(q.p) * ldx + q.g * 8;
+    if (acc) {
+      load8(dst, a);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = 0.f;
+    }
+    for (int r = 0; r < kh; ++r) {
+      const int ty = q.y + ph - r;
+      if (ty < 0 || ty % st != 0 || ty / st >= ho) continue;
+      const int oy = ty / st;
+      for (int s = 0; s < kw; ++s) {
+        const int tx = q.x + pw - s;
+        if (tx < 0 || tx % st != 0 || tx / st >= wo) continue;
+        const int ox = tx / st;
+        float v[8];
+        load8(dcol + (static_cast<long long>(q.img * ho + oy) * wo + ox) * rowlen + (r * kw + s) * c + q.g * 8, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] += v[j];
+      }
+    }
+    store8(dst, a);
+  }
+}
+
+// ------------------------------------------------------------------ pools
+// thread = (output pixel, 8 channels); idx [n*ho*wo][c] (pixel stride c) = ky*kw + kx of the first
+// max, 255 where the max is not > 0 (its producer's ReLU passes no gradient there)
+__global__ void maxpool_gen_fwd_kernel(const bf16* __restrict__ x, int ldx, int n, int h, int w, int c, int kh, int kw,
+                                       int st, int ph, int pw, int ho, int wo, bf16* __restrict__ y, int ldy,
+                                       uint8_t* __restrict__ idx) {
+  const int groups = c >> 3;
+  const long long total = static_cast<long long>(n) * ho * wo * groups;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const Pix q(i, groups, ho, wo);
+    float best[8];
+    int arg[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { best[j] = 0.f; arg[j] = -1; }
+    for (int r = 0; r < kh; ++r) {
+      const int iy = q.y * st + r - ph;
+      if (iy < 0 || iy >= h) continue;
+      for (int s = 0; s < kw; ++s) {
+        const int ix = q.x * st + s - pw;
+        if (ix < 0 || ix >= w) continue;
+        float v[8];
+        load8(x + (static_cast<long long>(q.img * h + iy) * w + ix) * ldx + q.g * 8, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (arg[j] < 0 || v[j] > best[j]) { best[j] = v[j]; arg[j] = r * kw + s; }
+      }
+    }
+    store8(y + static_cast<long long>(q.p) * ldy + q.g * 8, best);
+    uint2 ix8;
+    uint8_t* b8 = reinterpret_cast<uint8_t*>(&ix8);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b8[j] = best[j] > 0.f ? static_cast<uint8_t>(arg[j]) : static_cast<uint8_t>(255);
+    *reinterpret_cast<uint2*>(idx + static_cast<long long>(q.p) * c + q.g * 8) = ix8;
+  }
+}
+
+// gather form: thread = (input pixel, 8 channels) sums dy over the windows whose argmax it is
+__global__ void maxpool_gen_bwd_kernel(const uint8_t* __restrict__ idx, const bf16* __restrict__ dy, int ldy, int n,
+                                       int h, int w, int c, int kh, int kw, int st, int ph, int pw, int ho, int wo,
+                                       bf16* __restrict__ dx, int ldx, int acc) {
+  const int groups = c >> 3;
+  const long long total = static_cast<long long>(n) * h * w * groups;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const Pix q(i, groups, h, w);
+    float a[8];
+    bf16* dst = dx + static_cast<long long>(q.p) * ldx + q.g * 8;
+    if (acc) {
+      load8(dst, a);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = 0.f;
+    }
+    for (int r = 0; r < kh; ++r) {
+      const int ty = q.y + ph - r;
+      if (ty < 0 || ty % st != 0 || ty / st >= ho) continue;
+      const int oy = ty / st;
+      for (int s = 0; s < kw; ++s) {
+        const int tx = q.x + pw - s;
+        if (tx < 0 || tx % st != 0 || tx / st >= wo) continue;
+        const int ox = tx / st;
+        const long long op = static_cast<long long>(q.img * ho + oy) * wo + ox;
+        const uint2 ix8 = *reinterpret_cast<const uint2*>(idx + op * c + q.g * 8);
+        const uint8_t* b8 = reinterpret_cast<const uint8_t*>(&ix8);
+        const int pos = r * kw + s;
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) any |= b8[j] == pos;
+        if (!any) continue;
+        float v[8];
+        load8(dy + op * ldy + q.g * 8, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) if (b8[j] == pos) a[j] += v[j];
+      }
+    }
+    store8(dst, a);
+  }
+}
+
+__device__ __forceinline__ int win_count(int o, int st, int p, int k, int extent) {
+  const int lo = max(o * st - p, 0), hi = min(o * st - p + k, extent);
+  return hi - lo;
+}
+
+__global__ void avgpool_gen_fwd_kernel(const bf16* __restrict__ x, int ldx, int n, int h, int w, int c, int kh, int kw,
+                                       int st, int ph, int pw, int ho, int wo, bf16* __restrict__ y, int ldy) {
+  const int groups = c >> 3;
+  const long long total = static_cast<long long>(n) * ho * wo * groups;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const Pix q(i, groups, ho, wo);
+    float a[8] = {0.f};
+    for (int r = 0; r < kh; ++r) {
+      const int iy = q.y * st + r - ph;
+      if (iy < 0 || iy >= h) continue;
+      for (int s = 0; s < kw; ++s) {
+        const int ix = q.x * st + s - pw;
+        if (ix < 0 || ix >= w) continue;
+        float v[8];
+        load8(x + (static_cast<long long>(q.img * h + iy) * w + ix) * ldx + q.g * 8, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] += v[j];
+      }
+    }
+    const float inv = 1.f / static_cast<float>(win_count(q.y, st, ph, kh, h) * win_count(q.x, st, pw, kw, w));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] *= inv;
+    store8(y + static_cast<long long>(q.p) * ldy + q.g * 8, a);
+  }
+}
+
+__global__ void avgpool_gen_bwd_kernel(const bf16* __restrict__ dy, int ldy, int n, int h, int w, int c, int kh, int kw,
+                                       int st, int ph, int pw, int ho, int wo, bf16* __restrict__ dx, int ldx, int acc) {
+  const int groups = c >> 3;
+  const long long total = static_cast<long long>(n) * h * w * groups;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const Pix q(i, groups, h, w);
+    float a[8];
+    bf16* dst = dx + static_cast<long long>(q.p) * ldx + q.g * 8;
+    if (acc) {
+      load8(dst, a);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = 0.f;
+    }
+    for (int r = 0; r < kh; ++r) {
+      const int ty = q.y + ph - r;
+      if (ty < 0 || ty % st != 0 || ty / st >= ho) continue;
+      const int oy = ty / st;
+      for (int s = 0; s < kw; ++s) {
+        const int tx = q.x + pw - s;
+        if (tx < 0 || tx % st != 0 || tx / st >= wo) continue;
+        const int ox = tx / st;
+        const float inv = 1.f / static_cast<float>(win_count(oy, st, ph, kh, h) * win_count(ox, st, pw, kw, w));
+        float v[8];
+        load8(dy + (static_cast<long long>(q.img * ho + oy) * wo + ox) * ldy + q.g * 8, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] += v[j] * inv;
+      }
+    }
+    store8(dst, a);
+  }
+}
+
+// dz[p][c] = dy[p*ldy + c] * (y[p*ldy2 + c] > 0)  (the ReLU of a bias convolution)
+__global__ void relu_grad_kernel(const bf16* __restrict__ dy, int ldy, const bf16* __restrict__ y, int ldyv, long long pixels,
+                                 int c, bf16* __restrict__ dz) {
+  const int groups = c >> 3;
+  const long long total = pixels * groups;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long p = i / groups;
+    const int g = static_cast<int>(i - p * groups);
+    float d[8], v[8];
+    load8(dy + p * ldy + g * 8, d);
+    load8(y + p * ldyv + g * 8, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) if (!(v[j] > 0.f)) d[j] = 0.f;
+    store8(dz + p * c + g * 8, d);
+  }
+}
+
+// ------------------------------------------------------------------ GEMM helpers
+// out[rows][n] (pixel stride ldo) = a[rows][k] . w[n][k]^T, optional bias + ReLU epilogue
+int gemm_fwd(Model* m, const bf16* a, long long rows, long long k, const bf16* w, int n, bf16* out, long long ldo,
+             const float* bias, int relu, std::string* why) {
+  GemmDesc d;
+  d.M = static_cast<int>(rows); d.N = n; d.K = k;
+  d.a = Operand2D{a, rows, k, k};
+  d.b = Operand2D{w, n, k, k};
+  d.epi = EPI_BF16; d.out = out; d.s_m = ldo;
+  d.bias = bias; d.relu = relu;
+  RALPB_TRY(gemm_launch(d, m->stream, why));
+  ++m->launches;
+  return 0;
+}
+// out[rows][k] = dz[rows][n] . w[n][k]
+int gemm_dgrad(Model* m, const bf16* dz, long long rows, int n, const bf16* w, long long k, bf16* out, std::string* why) {
+  GemmDesc d;
+  d.M = static_cast<int>(rows); d.N = static_cast<int>(k); d.K = n;
+  d.a_mode = LD_K; d.a = Operand2D{dz, rows, n, n};
+  d.b_mode = LD_MN; d.b = Operand2D{w, n, k, k};
+  d.epi = EPI_BF16; d.out = out; d.s_m = k;
+  RALPB_TRY(gemm_launch(d, m->stream, why));
+  ++m->launches;
+  return 0;
+}
+// g[n][k] += dz[rows][n]^T . x[rows][k]
+int gemm_wgrad(Model* m, const bf16* dz, long long rows, int n, const bf16* x, long long k, float* g, std::string* why) {
+  GemmDesc d;
+  d.M = n; d.N = static_cast<int>(k); d.K = rows;
+  d.a_mode = LD_MN; d.a = Operand2D{dz, rows, n, n};
+  d.b_mode = LD_MN; d.b = Operand2D{x, rows, k, k};
+  d.k_splits = 0;
+  d.epi = EPI_F32_ATOMIC; d.out = g; d.s_m = k; d.s_n = 1;
+  RALPB_TRY(gemm_launch(d, m->stream, why));
+  ++m->launches;
+  return 0;
+}
+
+template <class T>
+T* galloc(Model* m, size_t count, std::string* why) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, std::max<size_t>(count * sizeof(T), 16)) != cudaSuccess) {
+    *why = "cudaMalloc failed (" + std::to_string(count * sizeof(T)) + " bytes)";
+    return nullptr;
+  }
+  m->owned.push_back(p);
+  return static_cast<T*>(p);
+}
+
+long long al4(long long x) { return (x + 3) & ~3LL; }
+
+}  // namespace
+
+int module_build(ModuleBufs& k, const ralpb_node_desc* nodes, int n_nodes, int n, int h, int w, int cin,
+                 long long* off, std::vector<std::pair<long long, long long>>* runs, long long* count,
+                 std::string* why) {
+  if (nodes == nullptr || n_nodes <= 0) { *why = "module without nodes"; return 1; }
+  k.n = n; k.h = h; k.w = w; k.cin = cin;
+  k.nodes.assign(n_nodes, ModNode{});
+  *count = 0;
+  int ho = -1, wo = -1, cout = 0;
+  for (int j = 0; j < n_nodes; ++j) {
+    ModNode& q = k.nodes[j];
+    q.d = nodes[j];
+    const ralpb_node_desc& d = q.d;
+    const std::string tag = "module node " + std::to_string(j) + ": ";
+    if (d.input < -1 || d.input >= j) { *why = tag + "input must be an earlier node or -1"; return 1; }
+    if (d.input >= 0 && k.nodes[d.input].d.output) { *why = tag + "reads an output node"; return 1; }
+    if (d.kh < 1 || d.kw < 1 || d.stride < 1 || d.pad_h < 0 || d.pad_w < 0 || d.pad_h >= d.kh || d.pad_w >= d.kw) {
+      *why = tag + "bad window";
+      return 1;
+    }
+    if (d.input >= 0) {
+      const ModNode& src = k.nodes[d.input];
+      q.cin = src.d.op == RALPB_NODE_CONV ? src.d.cout : src.cin;
+      q.h = src.ho; q.w = src.wo;
+      k.nodes[d.input].consumers++;
+    } else {
+      q.cin = cin; q.h = h; q.w = w;
+    }
+    q.ho = (q.h + 2 * d.pad_h - d.kh) / d.stride + 1;
+    q.wo = (q.w + 2 * d.pad_w - d.kw) / d.stride + 1;
+    if (q.ho < 1 || q.wo < 1) { *why = tag + "window larger than its input"; return 1; }
+    if (q.cin % 8 != 0) { *why = tag + "input channels must be a multiple of 8"; return 1; }
+    const int c_out = d.op == RALPB_NODE_CONV ? d.cout : q.cin;
+    if (d.op == RALPB_NODE_CONV) {
+      if (d.cout % 8 != 0 || d.cout < 8) { *why = tag + "conv output channels must be a multiple of 8"; return 1; }
+      q.direct = d.kh == 1 && d.kw == 1 && d.stride == 1 && d.pad_h == 0 && d.pad_w == 0;
+      q.w_off = *off;
+      *off = al4(*off + static_cast<long long>(d.cout) * q.K());
+      q.b_off = *off;
+      const long long nb = d.bn ? 2LL * d.cout : d.cout;
+      *off = al4(*off + nb);
+      runs->emplace_back(q.w_off, static_cast<long long>(d.cout) * q.K());
+      runs->emplace_back(q.b_off, nb);
+      *count += static_cast<long long>(d.cout) * q.K() + nb;
+    } else if (d.op != RALPB_NODE_MAXPOOL && d.op != RALPB_NODE_AVGPOOL) {
+      *why = tag + "unknown op";
+      return 1;
+    }
+    if (d.output) {
+      if (ho < 0) { ho = q.ho; wo = q.wo; }
+      if (q.ho != ho || q.wo != wo) { *why = tag + "output nodes differ in spatial size"; return 1; }
+      q.out_off = cout;
+      cout += c_out;
+    }
+  }
+  for (int j = 0; j < n_nodes; ++j) {
+    const ModNode& q = k.nodes[j];
+    if (!q.d.output && q.consumers == 0) { *why = "module node " + std::to_string(j) + ": output unused"; return 1; }
+  }
+  if (cout == 0) { *why = "module without output nodes"; return 1; }
+  k.ho = ho; k.wo = wo; k.cout = cout;
+  return 0;
+}
+
+int module_alloc(Model* m, ModuleBufs& k, std::string* why) {
+  long long col = 16, dz = 16, tmp = 16;
+  for (ModNode& q : k.nodes) {
+    const long long rin = static_cast<long long>(k.n) * q.h * q.w;
+    const long long rout = static_cast<long long>(k.n) * q.ho * q.wo;
+    const int c_out = q.d.op == RALPB_NODE_CONV ? q.d.cout : q.cin;
+    if (q.d.op == RALPB_NODE_CONV) {
+      if (!(q.wbf = galloc<bf16>(m, static_cast<size_t>(q.d.cout) * q.K(), why))) return 1;
+      if (q.d.bn) {
+        if (!(q.z = galloc<bf16>(m, static_cast<size_t>(rout) * q.d.cout, why))) return 1;
+        if (!(q.stats = galloc<float>(m, 2 * static_cast<size_t>(q.d.cout), why))) return 1;
+      }
+      if (!q.direct) col = std::max(col, rout * q.K());
+      dz = std::max(dz, rout * q.d.cout);
+      tmp = std::max(tmp, rin * q.cin);   // a 1x1 backward-data contribution that is accumulated
+    } else if (q.d.op == RALPB_NODE_MAXPOOL) {
+      if (!(q.idx = galloc<uint8_t>(m, static_cast<size_t>(rout) * q.cin, why))) return 1;
+    }
+    if (!q.d.output) {
+      if (!(q.y = galloc<bf16>(m, static_cast<size_t>(rout) * c_out, why))) return 1;
+      if (!(q.dy = galloc<bf16>(m, static_cast<size_t>(rout) * c_out, why))) return 1;
+    }
+  }
+  if (!(k.col = galloc<bf16>(m, static_cast<size_t>(col), why)) || !(k.dz = galloc<bf16>(m, static_cast<size_t>(dz), why)) ||
+      !(k.tmp = galloc<bf16>(m, static_cast<size_t>(tmp), why)))
+    return 1;
+  k.col_elems = col; k.dz_elems = dz; k.tmp_elems = tmp;
+  return 0;
+}
+
+int module_prep(Model* m, ModuleBufs& k, cudaStream_t s, std::string* why) {
+  for (ModNode& q : k.nodes) {
+    if (q.d.op != RALPB_NODE_CONV || q.wbf == nullptr) continue;
+    RALPB_TRY(cast_bf16(m->P + q.w_off, static_cast<long long>(q.d.cout) * q.K(), q.wbf, s));
+    ++m->launches;
+  }
+  return 0;
+}
+
+void module_param_runs(const ModuleBufs& k, std::vector<std::pair<long long, long long>>* w_runs,
+                       std::vector<std::pair<long long, long long>>* b_runs) {
+  for (const ModNode& q : k.nodes) {
+    if (q.d.op != RALPB_NODE_CONV) continue;
+    w_runs->emplace_back(q.w_off, static_cast<long long>(q.d.cout) * q.K());
+    b_runs->emplace_back(q.b_off, q.d.bn ? 2LL * q.d.cout : q.d.cout);
+  }
+}
+
+int module_forward(Model* m, ModuleBufs& k, const bf16* x, bf16* y, std::string* why) {
+  cudaStream_t s = m->stream;
+  for (ModNode& q : k.nodes) {
+    const ralpb_node_desc& d = q.d;
+    const bf16* src = d.input < 0 ? x : k.nodes[d.input].y;
+    const int lds = q.cin;   // inputs are contiguous (the module input or a non-output node)
+    const long long rout = static_cast<long long>(k.n) * q.ho * q.wo;
+    bf16* dst = d.output ? y + q.out_off : q.y;
+    const int ldd = d.output ? k.cout : (d.op == RALPB_NODE_CONV ? d.cout : q.cin);
+    if (d.op == RALPB_NODE_CONV) {
+      const bf16* a = src;
+      if (!q.direct) {
+        const long long total = rout * d.kh * d.kw * (q.cin / 8);
+        im2col_gen_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride,
+                                                               d.pad_h, d.pad_w, q.ho, q.wo, k.col);
+        RALPB_TRY(cudaGetLastError());
+        ++m->launches;
+        a = k.col;
+      }
+      if (d.bn) {
+        if (gemm_fwd(m, a, rout, q.K(), q.wbf, d.cout, q.z, d.cout, nullptr, 0, why)) return 1;
+        RALPB_TRY(bn_stats(Act4{q.z, 0}, k.n, q.ho, q.wo, d.cout, kBnEps, m->bn_work, q.stats, q.stats + d.cout, s));
+        BnApply ap{};
+        ap.x = Act4{q.z, 0}; ap.mean = q.stats; ap.rstd = q.stats + d.cout;
+        ap.gamma = m->P + q.b_off; ap.beta = m->P + q.b_off + d.cout; ap.relu = 1;
+        ap.y = MutAct4{dst, 0, ldd};
+        ap.n = k.n; ap.h = q.ho; ap.w = q.wo; ap.c = d.cout;
+        RALPB_TRY(bn_apply(ap, s));
+        m->launches += 3;
+      } else {
+        if (gemm_fwd(m, a, rout, q.K(), q.wbf, d.cout, dst, ldd, m->P + q.b_off, 1, why)) return 1;
+      }
+    } else if (d.op == RALPB_NODE_MAXPOOL) {
+      const long long total = rout * (q.cin / 8);
+      maxpool_gen_fwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride,
+                                                                  d.pad_h, d.pad_w, q.ho, q.wo, dst, ldd, q.idx);
+      RALPB_TRY(cudaGetLastError());
+      ++m->launches;
+    } else {
+      const long long total = rout * (q.cin / 8);
+      avgpool_gen_fwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride,
+                                                                  d.pad_h, d.pad_w, q.ho, q.wo, dst, ldd);
+      RALPB_TRY(cudaGetLastError());
+      ++m->launches;
+    }
+  }
+  return 0;
+}
+
+int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const bf16* dy, bf16* dx, std::string* why) {
+  cudaStream_t s = m->stream;
+  float *P = m->P, *G = m->G;
+  // which gradient buffers have received their first contribution (reverse node order)
+  std::vector<char> started(k.nodes.size() + 1, 0);   // [0] = the module input, [j + 1] = node j
+  for (int j = static_cast<int>(k.nodes.size()) - 1; j >= 0; --j) {
+    ModNode& q = k.nodes[j];
+    const ralpb_node_desc& d = q.d;
+    const bf16* src = d.input < 0 ? x : k.nodes[d.input].y;
+    const int lds = q.cin;
+    const long long rin = static_cast<long long>(k.n) * q.h * q.w;
+    const long long rout = static_cast<long long>(k.n) * q.ho * q.wo;
+    const bf16* g_out = d.output ? dy + q.out_off : q.dy;    // gradient w.r.t. this node's output
+    const bf16* v_out = d.output ? y + q.out_off : q.y;      // ... and the output itself
+    const int ldo = d.output ? k.cout : (d.op == RALPB_NODE_CONV ? d.cout : q.cin);
+    bf16* g_in = d.input < 0 ? dx : k.nodes[d.input].dy;     // gradient w.r.t. its input (may be null)
+    char& st = started[d.input + 1];
+    const int acc = st ? 1 : 0;
+    if (d.op == RALPB_NODE_CONV) {
+      // dz: the gradient w.r.t. the pre-activation (bn: w.r.t. the pre-batch-norm output)
+      if (d.bn) {
+        BnBackward bb{};
+        bb.dy = Act4{g_out, 0, ldo}; bb.y = Act4{v_out, 0, ldo}; bb.relu_mask = 1; bb.x = Act4{q.z, 0};
+        bb.mean = q.stats; bb.rstd = q.stats + d.cout; bb.gamma = P + q.b_off;
+        bb.dgamma = G + q.b_off; bb.dbeta = G + q.b_off + d.cout;
+        bb.dx = MutAct4{k.dz, 0};
+        bb.n = k.n; bb.h = q.ho; bb.w = q.wo; bb.c = d.cout;
+        RALPB_TRY(bn_backward(bb, m->bn_work, s));
+        m->launches += 3;
+      } else {
+        const long long total = rout * (d.cout / 8);
+        relu_grad_kernel<<<grid_for(total, 256), 256, 0, s>>>(g_out, ldo, v_out, ldo, rout, d.cout, k.dz);
+        RALPB_TRY(cudaGetLastError());
+        RALPB_TRY(colsum_bf16(k.dz, rout, d.cout, d.cout, G + q.b_off, s));
+        m->launches += 2;
+      }
+      // backward-filter
+      if (q.direct) {
+        if (gemm_wgrad(m, k.dz, rout, d.cout, src, q.cin, G + q.w_off, why)) return 1;
+      } else {
+        const long long total = rout * d.kh * d.kw * (q.cin / 8);
+        im2col_gen_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride,
+                                                               d.pad_h, d.pad_w, q.ho, q.wo, k.col);
+        RALPB_TRY(cudaGetLastError());
+        ++m->launches;
+        if (gemm_wgrad(m, k.dz, rout, d.cout, k.col, q.K(), G + q.w_off, why)) return 1;
+      }
+      // backward-data
+      if (g_in != nullptr) {
+        if (q.direct) {
+          bf16* out = acc ? k.tmp : g_in;
+          if (gemm_dgrad(m, k.dz, rout, d.cout, q.wbf, q.cin, out, why)) return 1;
+          if (acc) {
+            RALPB_TRY(add_act(Act4{g_in, 0}, Act4{k.tmp, 0}, MutAct4{g_in, 0}, k.n, q.h, q.w, q.cin, s));
+            ++m->launches;
+          }
+        } else {
+          if (gemm_dgrad(m, k.dz, rout, d.cout, q.wbf, q.K(), k.col, why)) return 1;
+          const long long total = rin * (q.cin / 8);
+          col2im_gen_kernel<<<grid_for(total, 256), 256, 0, s>>>(k.col, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride,
+                                                                 d.pad_h, d.pad_w, q.ho, q.wo, g_in, lds, acc);
+          RALPB_TRY(cudaGetLastError());
+          ++m->launches;
+        }
+        st = 1;
+      }
+    } else if (g_in != nullptr) {
+      const long long total = rin * (q.cin / 8);
+      if (d.op == RALPB_NODE_MAXPOOL)
+        maxpool_gen_bwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(q.idx, g_out, ldo, k.n, q.h, q.w, q.cin, d.kh, d.kw,
+                                                                    d.stride, d.pad_h, d.pad_w, q.ho, q.wo, g_in, lds,
+                                                                    acc);
+      else
+        avgpool_gen_bwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(g_out, ldo, k.n, q.h, q.w, q.cin, d.kh, d.kw,
+                                                                    d.stride, d.pad_h, d.pad_w, q.ho, q.wo, g_in, lds,
+                                                                    acc);
+      RALPB_TRY(cudaGetLastError());
+      ++m->launches;
+      st = 1;
+    }
+  }
+  if (dx != nullptr && !started[0]) RALPB_TRY(cudaMemsetAsync(dx, 0, static_cast<size_t>(k.n) * k.h * k.w * k.cin * 2, s));
+  return 0;
+}
+
+}  // namespace ralpb

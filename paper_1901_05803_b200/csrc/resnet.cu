@@ -29,6 +29,10 @@ __device__ __forceinline__ long long toff(int p, int hw, int h, int w, int pad, 
   return (static_cast<long long>(img * (h + 2 * pad) + y + pad) * (w + 2 * pad) + x + pad) * c;
 }
 
+// pixel stride (elements) of a tensor: its own channel count unless it is a channel slice
+template <class T>
+__device__ __forceinline__ int ld_of(const T& t, int c) { return t.ld ? t.ld : c; }
+
 __device__ __forceinline__ void load8(const bf16* p, float* v) {
   const uint4 u = *reinterpret_cast<const uint4*>(p);
   const bf16* b = reinterpret_cast<const bf16*>(&u);
@@ -79,7 +83,7 @@ __global__ void __launch_bounds__(256) bn_stats_kernel(Act4 x, int pixels, int h
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int p = p0 + u * st;
-        v[u] = p < pixels ? ld16(x.p + toff(p, hw, h, w, x.pad, c) + L.g * 8) : make_uint4(0, 0, 0, 0);
+        v[u] = p < pixels ? ld16(x.p + toff(p, hw, h, w, x.pad, ld_of(x, c)) + L.g * 8) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u)
@@ -135,8 +139,8 @@ __global__ void __launch_bounds__(256, 3) bn_apply_kernel(BnApply a, int pixels)
     for (int u = 0; u < 2; ++u) {
       const int p = p0 + u * st;
       if (p < pixels) {
-        v[u] = ld16(a.x.p + toff(p, hw, a.h, a.w, a.x.pad, a.c) + L.g * 8);
-        if (a.res_kind != 0) r[u] = ld16(a.r.p + toff(p, hw, a.h, a.w, a.r.pad, a.c) + L.g * 8);
+        v[u] = ld16(a.x.p + toff(p, hw, a.h, a.w, a.x.pad, ld_of(a.x, a.c)) + L.g * 8);
+        if (a.res_kind != 0) r[u] = ld16(a.r.p + toff(p, hw, a.h, a.w, a.r.pad, ld_of(a.r, a.c)) + L.g * 8);
       }
     }
 #pragma unroll
@@ -150,7 +154,7 @@ __global__ void __launch_bounds__(256, 3) bn_apply_kernel(BnApply a, int pixels)
         if (a.res_kind != 0) o[j] += fmaf(elem(r[u], j), rsc[j], rsf[j]);
         if (a.relu) o[j] = fmaxf(o[j], 0.f);
       }
-      store8(a.y.p + toff(p, hw, a.h, a.w, a.y.pad, a.c) + L.g * 8, o);
+      store8(a.y.p + toff(p, hw, a.h, a.w, a.y.pad, ld_of(a.y, a.c)) + L.g * 8, o);
     }
   }
 }
@@ -176,9 +180,9 @@ __global__ void __launch_bounds__(256, 3) bn_bwd_reduce_kernel(BnBackward b, int
       for (int u = 0; u < U; ++u) {
         const int p = p0 + u * st;
         const bool in = p < pixels;
-        dy[u] = in ? ld16(b.dy.p + toff(p, hw, b.h, b.w, b.dy.pad, c) + L.g * 8) : z;
-        xv[u] = in ? ld16(b.x.p + toff(p, hw, b.h, b.w, b.x.pad, c) + L.g * 8) : z;
-        y[u] = in && b.relu_mask ? ld16(b.y.p + toff(p, hw, b.h, b.w, b.y.pad, c) + L.g * 8) : one;
+        dy[u] = in ? ld16(b.dy.p + toff(p, hw, b.h, b.w, b.dy.pad, ld_of(b.dy, c)) + L.g * 8) : z;
+        xv[u] = in ? ld16(b.x.p + toff(p, hw, b.h, b.w, b.x.pad, ld_of(b.x, c)) + L.g * 8) : z;
+        y[u] = in && b.relu_mask ? ld16(b.y.p + toff(p, hw, b.h, b.w, b.y.pad, ld_of(b.y, c)) + L.g * 8) : one;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -228,17 +232,17 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(BnBackward b, int pix
   const int hw = b.h * b.w, st = L.stride();
   for (int p = L.first(); p < pixels; p += st) {
     float dy[8], xv[8], y[8], dx[8];
-    load8(b.dy.p + toff(p, hw, b.h, b.w, b.dy.pad, c) + L.g * 8, dy);
-    load8(b.x.p + toff(p, hw, b.h, b.w, b.x.pad, c) + L.g * 8, xv);
+    load8(b.dy.p + toff(p, hw, b.h, b.w, b.dy.pad, ld_of(b.dy, c)) + L.g * 8, dy);
+    load8(b.x.p + toff(p, hw, b.h, b.w, b.x.pad, ld_of(b.x, c)) + L.g * 8, xv);
     if (b.relu_mask) {
-      load8(b.y.p + toff(p, hw, b.h, b.w, b.y.pad, c) + L.g * 8, y);
+      load8(b.y.p + toff(p, hw, b.h, b.w, b.y.pad, ld_of(b.y, c)) + L.g * 8, y);
 #pragma unroll
       for (int j = 0; j < 8; ++j) if (!(y[j] > 0.f)) dy[j] = 0.f;
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) dx[j] = fmaf(A[j], dy[j], fmaf(xv[j] - mu[j], B[j], C[j]));
-    store8(b.dx.p + toff(p, hw, b.h, b.w, b.dx.pad, c) + L.g * 8, dx);
-    if (b.dz_out.p != nullptr) store8(b.dz_out.p + toff(p, hw, b.h, b.w, b.dz_out.pad, c) + L.g * 8, dy);
+    store8(b.dx.p + toff(p, hw, b.h, b.w, b.dx.pad, ld_of(b.dx, c)) + L.g * 8, dx);
+    if (b.dz_out.p != nullptr) store8(b.dz_out.p + toff(p, hw, b.h, b.w, b.dz_out.pad, ld_of(b.dz_out, c)) + L.g * 8, dy);
   }
 }
 
@@ -325,11 +329,11 @@ __global__ void __launch_bounds__(256) add_act_kernel(Act4 a, Act4 b, MutAct4 y,
   const int hw = h * w;
   for (int p = L.first(); p < pixels; p += L.stride()) {
     float u[8], v[8];
-    load8(a.p + toff(p, hw, h, w, a.pad, c) + L.g * 8, u);
-    load8(b.p + toff(p, hw, h, w, b.pad, c) + L.g * 8, v);
+    load8(a.p + toff(p, hw, h, w, a.pad, ld_of(a, c)) + L.g * 8, u);
+    load8(b.p + toff(p, hw, h, w, b.pad, ld_of(b, c)) + L.g * 8, v);
 #pragma unroll
     for (int j = 0; j < 8; ++j) u[j] += v[j];
-    store8(y.p + toff(p, hw, h, w, y.pad, c) + L.g * 8, u);
+    store8(y.p + toff(p, hw, h, w, y.pad, ld_of(y, c)) + L.g * 8, u);
   }
 }
 

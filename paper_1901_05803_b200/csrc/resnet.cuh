@@ -10,13 +10,18 @@
 
 namespace ralpb {
 
+// ld: pixel stride in elements (0 = the tensor's channel count); a channel slice of a wider
+// tensor (a branch of a concatenation) has ld = the wide tensor's channels.  Honoured by the
+// batch-norm kernels and add_act.
 struct Act4 {
   const __nv_bfloat16* p = nullptr;
   int pad = 0;
+  int ld = 0;
 };
 struct MutAct4 {
   __nv_bfloat16* p = nullptr;
   int pad = 0;
+  int ld = 0;
 };
 
 // Batch statistics over the n*h*w interior pixels: mean[c], rstd[c] = 1/sqrt(var + eps) (biased

@@ -16,7 +16,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from . import _lib, resnet
+from . import _lib, branchy, resnet
 from .planner.costmodel import (JobSpec, volume_baseline, volume_ralp, volume_ralp_multi_ps,
                                  volume_ring)
 from .planner.layers import ModelGraph
@@ -50,10 +50,15 @@ def infer_input_shape(model: ModelGraph) -> tuple[int, int, int]:
 def lower(model: ModelGraph, input_shape: Optional[tuple[int, int, int]] = None) -> list[dict]:
     """ModelGraph -> list of layer dicts (kind, k, stride, pad, h, w, cin, cout, relu[, bn, width,
     downsample]).  ResNet-50's linearised catalog entries are lowered at block granularity from
-    the architecture they were generated from (resnet.py, checked entry by entry)."""
+    the architecture they were generated from (resnet.py, checked entry by entry); Inception-v3 /
+    GoogLeNet at branch-group granularity (branchy.py, likewise checked); a later convolution that is
+    not a stride-1 "same" window becomes a one-node module."""
     if resnet.is_resnet50(model):
         resnet.check_catalog(model)
         return resnet.lower_layers()[0]
+    if branchy.is_branchy_graph(model):   # Inception-v3 / GoogLeNet branch groups
+        branchy.check_catalog(model)
+        return branchy.lower_layers(model.name, None if input_shape is None else input_shape[0])[0]
     h, w, c = input_shape or infer_input_shape(model)
     out: list[dict] = []
     n = model.num_layers
@@ -63,8 +68,13 @@ def lower(model: ModelGraph, input_shape: Optional[tuple[int, int, int]] = None)
         last = i == n - 1
         kind = _kv(L.kind)
         if kind == "conv":
-            d = dict(kind="conv", k=hp["k"], stride=hp.get("stride", 1), pad=hp.get("pad", 0), h=h, w=w, cin=c,
-                     cout=hp["cout"], relu=1)
+            k, st, pd = hp["k"], hp.get("stride", 1), hp.get("pad", 0)
+            if out and (st != 1 or k != 2 * pd + 1):
+                # not a stride-1 'same' window (e.g. OverFeat's unpadded 5x5): a one-node module
+                node = branchy.conv(L.name, -1, k, k, hp["cout"], stride=st, pad=(pd, pd), bn=False, output=True)
+                d = dict(kind="module", k=0, stride=0, pad=0, h=h, w=w, cin=c, cout=hp["cout"], relu=1, nodes=[node])
+            else:
+                d = dict(kind="conv", k=k, stride=st, pad=pd, h=h, w=w, cin=c, cout=hp["cout"], relu=1)
             h, w, c = L.output_shape.h, L.output_shape.w, L.output_shape.c
         elif kind == "pool":
             d = dict(kind="pool", k=hp["window"], stride=hp.get("stride", hp["window"]), pad=hp.get("pad", 0), h=h,
@@ -122,16 +132,29 @@ def allgather_bytes(blob: bytes) -> list[bytes]:
 
 
 _KIND = {"conv": _lib.RALPB_CONV, "pool": _lib.RALPB_POOL, "fc": _lib.RALPB_FC, "block": _lib.RALPB_BLOCK,
-         "apool": _lib.RALPB_APOOL}
+         "apool": _lib.RALPB_APOOL, "module": _lib.RALPB_MODULE}
+_NODE_OP = {"conv": _lib.RALPB_NODE_CONV, "maxpool": _lib.RALPB_NODE_MAXPOOL, "avgpool": _lib.RALPB_NODE_AVGPOOL}
 
 
 def _desc_array(layers: Sequence[dict]):
+    """(ralpb_layer_desc array, ralpb_node_desc array or None) of a lowered layer table."""
     arr = (_lib.LayerDesc * len(layers))()
+    nodes = []
     for a, L in zip(arr, layers):
         a.kind, a.k, a.stride, a.pad = _KIND[L["kind"]], L["k"], L["stride"], L["pad"]
         a.h, a.w, a.cin, a.cout, a.relu = L["h"], L["w"], L["cin"], L["cout"], L["relu"]
         a.bn, a.width, a.downsample = L.get("bn", 0), L.get("width", 0), L.get("downsample", 0)
-    return arr
+        if L["kind"] == "module":
+            a.node_begin, a.node_count = len(nodes), len(L["nodes"])
+            nodes.extend(L["nodes"])
+    if not nodes:
+        return arr, None
+    narr = (_lib.NodeDesc * len(nodes))()
+    for a, nd in zip(narr, nodes):
+        a.op, a.input = _NODE_OP[nd["op"]], nd["input"]
+        a.kh, a.kw, a.stride, a.pad_h, a.pad_w = nd["kh"], nd["kw"], nd["stride"], nd["ph"], nd["pw"]
+        a.cout, a.bn, a.output = nd["cout"], nd["bn"], nd["output"]
+    return arr, narr
 
 
 def _ptr(a: np.ndarray) -> int:
@@ -204,9 +227,10 @@ class RankExecutor:
         self.in_shape = (self.layers[0]["h"], self.layers[0]["w"], self.layers[0]["cin"])
         self.classes = self.layers[-1]["cout"]
         split = job.strategy.split_index if kind == "ralp" else 0
-        if split and resnet.is_resnet50(job.model):
-            try:
-                split = resnet.lowered_split(split)   # catalog entries -> lowered layers
+        if split and (resnet.is_resnet50(job.model) or branchy.is_branchy_graph(job.model)):
+            try:   # catalog entries -> lowered layers
+                split = (resnet.lowered_split(split) if resnet.is_resnet50(job.model)
+                         else branchy.lowered_split(job.model.name, split))
             except ValueError as e:
                 raise ExecutorError(str(e)) from None
         if kind == "ralp":
@@ -215,9 +239,12 @@ class RankExecutor:
             strategy = _lib.RALPB_STRATEGY_RING if ring_backend == "native" else _lib.RALPB_STRATEGY_RING_EXTERNAL
         else:
             strategy = _lib.RALPB_STRATEGY_BASELINE
-        self._descs = _desc_array(self.layers)
+        self.lowered_split = split   # 1-based cut over the lowered layer table (0: none)
+        self._descs, self._nodes = _desc_array(self.layers)
         h = C.c_void_p()
-        _lib.call("ralpb_model_create", C.cast(self._descs, C.c_void_p), len(self.layers), split,
+        _lib.call("ralpb_model_create_graph", C.cast(self._descs, C.c_void_p), len(self.layers),
+                  None if self._nodes is None else C.cast(self._nodes, C.c_void_p),
+                  0 if self._nodes is None else len(self._nodes), split,
                   job.model.batch_size, strategy, rank, world, ps_rank, job.model.bytes_per_element,
                   _lib.PRECISIONS[precision], workers, C.byref(h))
         self._h = h
@@ -250,6 +277,9 @@ class RankExecutor:
             return np.empty((L["cout"], L["cin"]), dtype=np.float32), np.empty(L["cout"], dtype=np.float32)
         if L["kind"] == "block":
             nw, nb = block_param_counts(L)
+            return np.empty(nw, dtype=np.float32), np.empty(nb, dtype=np.float32)
+        if L["kind"] == "module":
+            nw, nb = branchy.module_param_counts(L)
             return np.empty(nw, dtype=np.float32), np.empty(nb, dtype=np.float32)
         return None
 

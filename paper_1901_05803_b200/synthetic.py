@@ -60,6 +60,21 @@ def init_params(layers: list[dict], seed: int) -> list[tuple[np.ndarray, np.ndar
             for sh, _ in shapes:
                 bns += [np.ones(sh[0], np.float32), np.zeros(sh[0], np.float32)]
             out.append((np.concatenate(ws), np.concatenate(bns)))
+        elif L["kind"] == "module":
+            # conv nodes in order: filters [cout][kh][kw][cin] He-normal (fan_in kh*kw*cin), then
+            # batch-norm scale 1 / shift 0, or a zero bias
+            from .branchy import conv_cin, node_shapes
+            shp, _ = node_shapes(L["nodes"], L["h"], L["w"], L["cin"])
+            ws, bs = [], []
+            for j, nd in enumerate(L["nodes"]):
+                if nd["op"] != "conv":
+                    continue
+                ci, co = conv_cin(L["nodes"], j, L["cin"], shp), nd["cout"]
+                fan = nd["kh"] * nd["kw"] * ci
+                ws.append((r.standard_normal((co, nd["kh"], nd["kw"], ci), dtype=np.float32)
+                           * np.float32(np.sqrt(2.0 / fan))).reshape(-1))
+                bs += [np.ones(co, np.float32), np.zeros(co, np.float32)] if nd["bn"] else [np.zeros(co, np.float32)]
+            out.append((np.concatenate(ws), np.concatenate(bs)))
         elif L["kind"] == "fc":
             w = r.standard_normal((L["cout"], L["cin"]), dtype=np.float32) * np.float32(0.01)
             out.append((w, np.zeros(L["cout"], dtype=np.float32)))

@@ -3,6 +3,7 @@ include/ralpb.h declares (no compute calls without a GPU), the lowering of the
 planner graph to the ABI layer table, the oracle step's schedule invariants, and
 the multi-rank handle exchange over gloo (world_size 2)."""
 import os
+import ctypes as C
 import re
 from pathlib import Path
 
@@ -36,12 +37,25 @@ def test_library_exports_every_declared_symbol():
     assert lib.ralpb_version() == 1
 
 
+def _header_struct_fields(name):
+    """Field names of `typedef struct { ... } name;` in include/ralpb.h, in order."""
+    text = re.sub(r"/\*.*?\*/", "", (ROOT / "include" / "ralpb.h").read_text(), flags=re.S)
+    body = re.search(r"typedef struct \{([^}]*)\}\s*" + name + r"\s*;", text).group(1)
+    fields = []
+    for decl in body.split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        names = decl.split(None, 1)[1] if not decl.startswith(("long long", "unsigned")) else decl.split(None, 2)[2]
+        fields += [n.strip().lstrip("*") for n in names.split(",")]
+    return fields
+
+
 def test_abi_structs_match_header():
-    text = (ROOT / "include" / "ralpb.h").read_text()
-    assert "ralpb_layer_desc" in text and "ralpb_step_stats" in text
-    assert [f for f, _ in _lib.LayerDesc._fields_] == ["kind", "k", "stride", "pad", "h", "w", "cin", "cout", "relu",
-                                                      "bn", "width", "downsample"]
-    assert _lib.StepStats._fields_[0][0] == "loss"
+    for ctype, cname in ((_lib.LayerDesc, "ralpb_layer_desc"), (_lib.NodeDesc, "ralpb_node_desc"),
+                         (_lib.StepStats, "ralpb_step_stats"), (_lib.LaunchRec, "ralpb_launch_rec")):
+        assert [f for f, _ in ctype._fields_] == _header_struct_fields(cname), cname
+    assert _lib.LayerDesc._fields_[-2:] == [("node_begin", C.c_int), ("node_count", C.c_int)]
 
 
 def test_lowering_vgg16():
