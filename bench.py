@@ -428,28 +428,35 @@ def run_ours(args):
                   "logical_bytes_per_step": _job_bytes(stn, world),
                   "note": "ralp-n placement: rank 0 runs only the FC tail, ranks 1..N-1 are workers"}
 
-    # ResNet-50 (BASELINE.json config 5: conv-grad sync dominated; the catalog's linearised entries
-    # executed at block granularity -- batch norm, bottlenecks, projection shortcuts): layer-placed,
-    # partitioner split 55 (apool | fc) at b=128, W = N
-    resnet50 = None
-    if not args.no_resnet and MODEL != "resnet-50":
+    # The catalog's branchy models executed, layer-placed at the partitioner's
+    # split for b=128, W = N: ResNet-50 (BASELINE.json config 5, conv-grad sync dominated; blocks with
+    # batch norm and projection shortcuts), Inception-v3 (299x299, branch groups with batch norm) and
+    # GoogLeNet (224x224, branch groups with biases)
+    def catalog_comparator(name):
         torch.cuda.empty_cache()
-        exr5, jobr5, rep5 = _build_executor("ralp", world, rank, model="resnet-50")
-        g5 = torch.Generator(device="cuda").manual_seed(4321 + rank)
-        r5i = [torch.randn(BATCH, *exr5.in_shape, generator=g5, device="cuda") for _ in range(2)]
-        r5l = [torch.randint(0, exr5.classes, (BATCH,), generator=g5, device="cuda", dtype=torch.int32) for _ in range(2)]
-        ms_r5 = _time_steps(exr5, r5i, r5l, args.steps, args.warmup, world)
-        st5 = exr5.stats()
-        exr5.close()
-        del r5i, r5l
-        wf5, pf5 = compute_load(jobr5.model, rep5.split_index, world)
-        resnet50 = {"value": world * BATCH / (ms_r5 * 1e-3), "ms_per_step": ms_r5, "split": rep5.split_index,
-                    "logical_bytes_per_step": _job_bytes(st5, world),
-                    "oracle_volume_ralp": volume_ralp(jobr5.model, rep5.split_index, world).total_bytes_per_step,
-                    "tensor_frac_of_step": (wf5 + (pf5 if rank == 0 else 0)) / (ms_r5 * 1e-3) / 1e12
-                                           / peaks["bf16_tflops_sustained"],
-                    "note": "resnet-50 224x224 synthetic, b=128/worker, layer-placed split 55 (apool | fc); "
-                            "tensor_frac_of_step = compute_load() FLOPs / wall step time / sustained bf16 peak"}
+        exc, jobc, repc = _build_executor("ralp", world, rank, model=name)
+        gc = torch.Generator(device="cuda").manual_seed(4321 + rank)
+        ci = [torch.randn(BATCH, *exc.in_shape, generator=gc, device="cuda") for _ in range(2)]
+        cl = [torch.randint(0, exc.classes, (BATCH,), generator=gc, device="cuda", dtype=torch.int32) for _ in range(2)]
+        ms_c = _time_steps(exc, ci, cl, args.steps, args.warmup, world)
+        stc = exc.stats()
+        exc.close()
+        del ci, cl
+        wfc, pfc = compute_load(jobc.model, repc.split_index, world)
+        h, w, _ = exc.in_shape
+        return {"value": world * BATCH / (ms_c * 1e-3), "ms_per_step": ms_c, "split": repc.split_index,
+                "lowered_split": exc.lowered_split,
+                "logical_bytes_per_step": _job_bytes(stc, world),
+                "oracle_volume_ralp": volume_ralp(jobc.model, repc.split_index, world).total_bytes_per_step,
+                "tensor_frac_of_step": (wfc + (pfc if rank == 0 else 0)) / (ms_c * 1e-3) / 1e12
+                                       / peaks["bf16_tflops_sustained"],
+                "note": f"{name} {h}x{w} synthetic, b={BATCH}/worker, layer-placed at the partitioner's split "
+                        f"{repc.split_index}; tensor_frac_of_step = compute_load() FLOPs / wall step time / "
+                        "sustained bf16 peak"}
+
+    resnet50 = catalog_comparator("resnet-50") if not args.no_resnet and MODEL != "resnet-50" else None
+    inception_v3 = catalog_comparator("inception-v3") if not args.no_branchy else None
+    googlenet = catalog_comparator("googlenet") if not args.no_branchy else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -477,6 +484,8 @@ def run_ours(args):
             "ralp_dedicated_ps": ralp_n,
             "precision_fp32": fp32,
             "resnet50": resnet50,
+            "inception_v3": inception_v3,
+            "googlenet": googlenet,
             "breakdown_ms_rank0": {"front_fwd": st.ms_front_fwd, "back": st.ms_back, "front_bwd": st.ms_front_bwd,
                                    "sync": st.ms_sync, "tensor_kernels_sum": prof.ms_gemm,
                                    "tensor_launches": prof.gemm_launches},
@@ -526,6 +535,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the parity-precision comparator")
     ap.add_argument("--no-resnet", action="store_true", help="skip the ResNet-50 comparator")
+    ap.add_argument("--no-branchy", action="store_true", help="skip the Inception-v3 / GoogLeNet comparators")
     ap.add_argument("--model", default=MODEL, help="catalog model (BASELINE configs: vgg16 headline, alexnet)")
     ap.add_argument("--batch", type=int, default=BATCH, help="per-worker batch")
     args = ap.parse_args()

@@ -61,9 +61,9 @@ __device__ __forceinline__ void store8(bf16* p, const float* v) {
 // Decomposition of a flat (pixel, 8-channel group) index; pixel = (img*h + y)*w + x.
 struct Pix {
   int g, p, img, y, x;
-  __device__ __forceinline__ Pix(long long i, int groups, int h, int w) {
-    p = static_cast<int>(i / groups);
-    g = static_cast<int>(i - static_cast<long long>(p) * groups);
+  __device__ __forceinline__ Pix(int i, int groups, int h, int w) {
+    p = i / groups;
+    g = i - p * groups;
     img = p / (h * w);
     const int r = p - img * h * w;
     y = r / w;
@@ -76,23 +76,23 @@ struct Pix {
 // (0 outside the image); x has pixel stride ldx.
 __global__ void im2col_gen_kernel(const bf16* __restrict__ x, int ldx, int n, int h, int w, int c, int kh, int kw,
                                   int st, int ph, int pw, int ho, int wo, bf16* __restrict__ out) {
-  const int groups = c >> 3, taps = kh * kw;
-  const long long total = static_cast<long long>(n) * ho * wo * taps * groups;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long t = i / groups;   // row * taps + tap
-    const int g = static_cast<int>(i - t * groups);
-    const long long row = t / taps;
-    const int tap = static_cast<int>(t - row * taps);
-    const int img = static_cast<int>(row / (ho * wo));
-    const int rr = static_cast<int>(row - static_cast<long long>(img) * ho * wo);
+  // 32-bit index arithmetic (module_build checks rows * taps * groups < 2^31)
+  const int groups = c >> 3, taps = kh * kw, hw = ho * wo;
+  const int total = n * hw * taps * groups;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int t = i / groups;   // row * taps + tap
+    const int g = i - t * groups;
+    const int row = t / taps;
+    const int tap = t - row * taps;
+    const int img = row / hw;
+    const int rr = row - img * hw;
     const int oy = rr / wo, ox = rr - oy * wo;
     const int r = tap / kw, s = tap - r * kw;
     const int iy = oy * st + r - ph, ix = ox * st + s - pw;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (iy >= 0 && iy < h && ix >= 0 && ix < w)
       v = *reinterpret_cast<const uint4*>(x + (static_cast<long long>(img * h + iy) * w + ix) * ldx + g * 8);
-    *reinterpret_cast<uint4*>(out + t * c + g * 8) = v;
+    *reinterpret_cast<uint4*>(out + static_cast<long long>(t) * c + g * 8) = v;
   }
 }
 
@@ -101,10 +101,9 @@ __global__ void im2col_gen_kernel(const bf16* __restrict__ x, int ldx, int n, in
 __global__ void col2im_gen_kernel(const bf16* __restrict__ dcol, int n, int h, int w, int c, int kh, int kw, int st,
                                   int ph, int pw, int ho, int wo, bf16* __restrict__ dx, int ldx, int acc) {
   const int groups = c >> 3;
-  const long long total = static_cast<long long>(n) * h * w * groups;
+  const int total = n * h * w * groups;
   const long long rowlen = static_cast<long long>(kh) * kw * c;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const Pix q(i, groups, h, w);
     float a[8];
     bf16* dst = dx + static_cast<long long>(q.p) * ldx + q.g * 8;
@@ -139,9 +138,8 @@ __global__ void maxpool_gen_fwd_kernel(const bf16* __restrict__ x, int ldx, int 
                                        int st, int ph, int pw, int ho, int wo, bf16* __restrict__ y, int ldy,
                                        uint8_t* __restrict__ idx) {
   const int groups = c >> 3;
-  const long long total = static_cast<long long>(n) * ho * wo * groups;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  const int total = n * ho * wo * groups;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const Pix q(i, groups, ho, wo);
     float best[8];
     int arg[8];
@@ -174,9 +172,8 @@ __global__ void maxpool_gen_bwd_kernel(const uint8_t* __restrict__ idx, const bf
                                        int h, int w, int c, int kh, int kw, int st, int ph, int pw, int ho, int wo,
                                        bf16* __restrict__ dx, int ldx, int acc) {
   const int groups = c >> 3;
-  const long long total = static_cast<long long>(n) * h * w * groups;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  const int total = n * h * w * groups;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const Pix q(i, groups, h, w);
     float a[8];
     bf16* dst = dx + static_cast<long long>(q.p) * ldx + q.g * 8;
@@ -220,9 +217,8 @@ __device__ __forceinline__ int win_count(int o, int st, int p, int k, int extent
 __global__ void avgpool_gen_fwd_kernel(const bf16* __restrict__ x, int ldx, int n, int h, int w, int c, int kh, int kw,
                                        int st, int ph, int pw, int ho, int wo, bf16* __restrict__ y, int ldy) {
   const int groups = c >> 3;
-  const long long total = static_cast<long long>(n) * ho * wo * groups;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  const int total = n * ho * wo * groups;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const Pix q(i, groups, ho, wo);
     float a[8] = {0.f};
     for (int r = 0; r < kh; ++r) {
@@ -247,9 +243,8 @@ __global__ void avgpool_gen_fwd_kernel(const bf16* __restrict__ x, int ldx, int 
 __global__ void avgpool_gen_bwd_kernel(const bf16* __restrict__ dy, int ldy, int n, int h, int w, int c, int kh, int kw,
                                        int st, int ph, int pw, int ho, int wo, bf16* __restrict__ dx, int ldx, int acc) {
   const int groups = c >> 3;
-  const long long total = static_cast<long long>(n) * h * w * groups;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  const int total = n * h * w * groups;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const Pix q(i, groups, h, w);
     float a[8];
     bf16* dst = dx + static_cast<long long>(q.p) * ldx + q.g * 8;
@@ -380,6 +375,11 @@ int module_build(ModuleBufs& k, const ralpb_node_desc* nodes, int n_nodes, int n
     q.wo = (q.w + 2 * d.pad_w - d.kw) / d.stride + 1;
     if (q.ho < 1 || q.wo < 1) { *why = tag + "window larger than its input"; return 1; }
     if (q.cin % 8 != 0) { *why = tag + "input channels must be a multiple of 8"; return 1; }
+    if (static_cast<long long>(n) * q.ho * q.wo * d.kh * d.kw * (q.cin / 8) >= (1LL << 31) ||
+        static_cast<long long>(n) * q.h * q.w * q.cin >= (1LL << 31)) {
+      *why = tag + "tensor too large for 32-bit indexing";
+      return 1;
+    }
     const int c_out = d.op == RALPB_NODE_CONV ? d.cout : q.cin;
     if (d.op == RALPB_NODE_CONV) {
       if (d.cout % 8 != 0 || d.cout < 8) { *why = tag + "conv output channels must be a multiple of 8"; return 1; }
