@@ -73,15 +73,15 @@ struct Pix {
 
 // ------------------------------------------------------------------ layouts
 // out [n*ho*wo][kh*kw*c]: column (r*kw + s)*c + ch = x[img][oy*st + r - ph][ox*st + s - pw][ch]
-// (0 outside the image); x has pixel stride ldx.
+// (0 outside the image); x has pixel stride ldx.  Thread = (patch row, tap): the index math runs
+// once per tap and the thread copies the tap's c channels (contiguous in x and in out) 16 bytes at
+// a time; consecutive threads write consecutive taps of a row.  32-bit indices (module_build checks
+// rows * taps < 2^31).
 __global__ void im2col_gen_kernel(const bf16* __restrict__ x, int ldx, int n, int h, int w, int c, int kh, int kw,
                                   int st, int ph, int pw, int ho, int wo, bf16* __restrict__ out) {
-  // 32-bit index arithmetic (module_build checks rows * taps * groups < 2^31)
   const int groups = c >> 3, taps = kh * kw, hw = ho * wo;
-  const int total = n * hw * taps * groups;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int t = i / groups;   // row * taps + tap
-    const int g = i - t * groups;
+  const int total = n * hw * taps;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
     const int row = t / taps;
     const int tap = t - row * taps;
     const int img = row / hw;
@@ -89,45 +89,74 @@ __global__ void im2col_gen_kernel(const bf16* __restrict__ x, int ldx, int n, in
     const int oy = rr / wo, ox = rr - oy * wo;
     const int r = tap / kw, s = tap - r * kw;
     const int iy = oy * st + r - ph, ix = ox * st + s - pw;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (iy >= 0 && iy < h && ix >= 0 && ix < w)
-      v = *reinterpret_cast<const uint4*>(x + (static_cast<long long>(img * h + iy) * w + ix) * ldx + g * 8);
-    *reinterpret_cast<uint4*>(out + static_cast<long long>(t) * c + g * 8) = v;
+    uint4* dst = reinterpret_cast<uint4*>(out + static_cast<long long>(t) * c);
+    if (iy >= 0 && iy < h && ix >= 0 && ix < w) {
+      const uint4* src = reinterpret_cast<const uint4*>(x + (static_cast<long long>(img * h + iy) * w + ix) * ldx);
+      for (int g = 0; g < groups; ++g) dst[g] = __ldg(src + g);
+    } else {
+      for (int g = 0; g < groups; ++g) dst[g] = make_uint4(0, 0, 0, 0);
+    }
   }
 }
 
 // dx[img][y][x][ch] (+)= sum over the taps (r, s) whose output position (oy, ox) reads (y, x) of
-// dcol[(img*ho + oy)*wo + ox][(r*kw + s)*c + ch]  -- the adjoint of im2col_gen, gathered
+// dcol[(img*ho + oy)*wo + ox][(r*kw + s)*c + ch]  -- the adjoint of im2col_gen, gathered.
+// Thread = (input pixel, up to kChunk 8-channel groups): one index decomposition per thread, the
+// taps' window test per tap, then kChunk contiguous 16-byte loads per contributing tap.
+constexpr int kChunk = 4;
+template <bool S1>
 __global__ void col2im_gen_kernel(const bf16* __restrict__ dcol, int n, int h, int w, int c, int kh, int kw, int st,
                                   int ph, int pw, int ho, int wo, bf16* __restrict__ dx, int ldx, int acc) {
   const int groups = c >> 3;
-  const int total = n * h * w * groups;
+  const int chunks = (groups + kChunk - 1) / kChunk;
+  const int total = n * h * w * chunks;
   const long long rowlen = static_cast<long long>(kh) * kw * c;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const Pix q(i, groups, h, w);
-    float a[8];
-    bf16* dst = dx + static_cast<long long>(q.p) * ldx + q.g * 8;
-    if (acc) {
-      load8(dst, a);
-    } else {
+    const Pix q(i, chunks, h, w);
+    const int g0 = q.g * kChunk;
+    const int ng = min(kChunk, groups - g0);
+    float a[kChunk][8];
+    bf16* dst = dx + static_cast<long long>(q.p) * ldx + g0 * 8;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) a[j] = 0.f;
-    }
-    for (int r = 0; r < kh; ++r) {
-      const int ty = q.y + ph - r;
-      if (ty < 0 || ty % st != 0 || ty / st >= ho) continue;
-      const int oy = ty / st;
-      for (int s = 0; s < kw; ++s) {
-        const int tx = q.x + pw - s;
-        if (tx < 0 || tx % st != 0 || tx / st >= wo) continue;
-        const int ox = tx / st;
-        float v[8];
-        load8(dcol + (static_cast<long long>(q.img * ho + oy) * wo + ox) * rowlen + (r * kw + s) * c + q.g * 8, v);
+    for (int u = 0; u < kChunk; ++u) {
+      if (acc && u < ng) {
+        load8(dst + u * 8, a[u]);
+      } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) a[j] += v[j];
+        for (int j = 0; j < 8; ++j) a[u][j] = 0.f;
       }
     }
-    store8(dst, a);
+    for (int r = 0; r < kh; ++r) {
+      int ty = q.y + ph - r;
+      if (ty < 0) break;   // ty decreases with r
+      if (!S1) {
+        if (ty % st != 0) continue;
+        ty /= st;
+      }
+      if (ty >= ho) continue;
+      for (int s = 0; s < kw; ++s) {
+        int tx = q.x + pw - s;
+        if (tx < 0) break;
+        if (!S1) {
+          if (tx % st != 0) continue;
+          tx /= st;
+        }
+        if (tx >= wo) continue;
+        const bf16* src = dcol + (static_cast<long long>(q.img * ho + ty) * wo + tx) * rowlen + (r * kw + s) * c + g0 * 8;
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) {
+          if (u < ng) {
+            float v[8];
+            load8(src + u * 8, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a[u][j] += v[j];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u)
+      if (u < ng) store8(dst + u * 8, a[u]);
   }
 }
 
@@ -168,6 +197,7 @@ __global__ void maxpool_gen_fwd_kernel(const bf16* __restrict__ x, int ldx, int 
 }
 
 // gather form: thread = (input pixel, 8 channels) sums dy over the windows whose argmax it is
+template <bool S1>
 __global__ void maxpool_gen_bwd_kernel(const uint8_t* __restrict__ idx, const bf16* __restrict__ dy, int ldy, int n,
                                        int h, int w, int c, int kh, int kw, int st, int ph, int pw, int ho, int wo,
                                        bf16* __restrict__ dx, int ldx, int acc) {
@@ -184,13 +214,21 @@ __global__ void maxpool_gen_bwd_kernel(const uint8_t* __restrict__ idx, const bf
       for (int j = 0; j < 8; ++j) a[j] = 0.f;
     }
     for (int r = 0; r < kh; ++r) {
-      const int ty = q.y + ph - r;
-      if (ty < 0 || ty % st != 0 || ty / st >= ho) continue;
-      const int oy = ty / st;
+      int oy = q.y + ph - r;
+      if (oy < 0) break;   // decreases with r
+      if (!S1) {
+        if (oy % st != 0) continue;
+        oy /= st;
+      }
+      if (oy >= ho) continue;
       for (int s = 0; s < kw; ++s) {
-        const int tx = q.x + pw - s;
-        if (tx < 0 || tx % st != 0 || tx / st >= wo) continue;
-        const int ox = tx / st;
+        int ox = q.x + pw - s;
+        if (ox < 0) break;
+        if (!S1) {
+          if (ox % st != 0) continue;
+          ox /= st;
+        }
+        if (ox >= wo) continue;
         const long long op = static_cast<long long>(q.img * ho + oy) * wo + ox;
         const uint2 ix8 = *reinterpret_cast<const uint2*>(idx + op * c + q.g * 8);
         const uint8_t* b8 = reinterpret_cast<const uint8_t*>(&ix8);
@@ -240,6 +278,7 @@ __global__ void avgpool_gen_fwd_kernel(const bf16* __restrict__ x, int ldx, int 
   }
 }
 
+template <bool S1>
 __global__ void avgpool_gen_bwd_kernel(const bf16* __restrict__ dy, int ldy, int n, int h, int w, int c, int kh, int kw,
                                        int st, int ph, int pw, int ho, int wo, bf16* __restrict__ dx, int ldx, int acc) {
   const int groups = c >> 3;
@@ -255,13 +294,21 @@ __global__ void avgpool_gen_bwd_kernel(const bf16* __restrict__ dy, int ldy, int
       for (int j = 0; j < 8; ++j) a[j] = 0.f;
     }
     for (int r = 0; r < kh; ++r) {
-      const int ty = q.y + ph - r;
-      if (ty < 0 || ty % st != 0 || ty / st >= ho) continue;
-      const int oy = ty / st;
+      int oy = q.y + ph - r;
+      if (oy < 0) break;   // decreases with r
+      if (!S1) {
+        if (oy % st != 0) continue;
+        oy /= st;
+      }
+      if (oy >= ho) continue;
       for (int s = 0; s < kw; ++s) {
-        const int tx = q.x + pw - s;
-        if (tx < 0 || tx % st != 0 || tx / st >= wo) continue;
-        const int ox = tx / st;
+        int ox = q.x + pw - s;
+        if (ox < 0) break;
+        if (!S1) {
+          if (ox % st != 0) continue;
+          ox /= st;
+        }
+        if (ox >= wo) continue;
         const float inv = 1.f / static_cast<float>(win_count(oy, st, ph, kh, h) * win_count(ox, st, pw, kw, w));
         float v[8];
         load8(dy + (static_cast<long long>(q.img * ho + oy) * wo + ox) * ldy + q.g * 8, v);
@@ -472,7 +519,7 @@ int module_forward(Model* m, ModuleBufs& k, const bf16* x, bf16* y, std::string*
     if (d.op == RALPB_NODE_CONV) {
       const bf16* a = src;
       if (!q.direct) {
-        const long long total = rout * d.kh * d.kw * (q.cin / 8);
+        const long long total = rout * d.kh * d.kw;
         im2col_gen_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride,
                                                                d.pad_h, d.pad_w, q.ho, q.wo, k.col);
         RALPB_TRY(cudaGetLastError());
@@ -549,7 +596,7 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
       if (q.direct) {
         if (gemm_wgrad(m, k.dz, rout, d.cout, src, q.cin, G + q.w_off, why)) return 1;
       } else {
-        const long long total = rout * d.kh * d.kw * (q.cin / 8);
+        const long long total = rout * d.kh * d.kw;
         im2col_gen_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride,
                                                                d.pad_h, d.pad_w, q.ho, q.wo, k.col);
         RALPB_TRY(cudaGetLastError());
@@ -567,9 +614,14 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
           }
         } else {
           if (gemm_dgrad(m, k.dz, rout, d.cout, q.wbf, q.K(), k.col, why)) return 1;
-          const long long total = rin * (q.cin / 8);
-          col2im_gen_kernel<<<grid_for(total, 256), 256, 0, s>>>(k.col, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride,
-                                                                 d.pad_h, d.pad_w, q.ho, q.wo, g_in, lds, acc);
+          const long long total = rin * ((q.cin / 8 + kChunk - 1) / kChunk);
+          if (d.stride == 1)
+            col2im_gen_kernel<true><<<grid_for(total, 256), 256, 0, s>>>(k.col, k.n, q.h, q.w, q.cin, d.kh, d.kw, 1,
+                                                                         d.pad_h, d.pad_w, q.ho, q.wo, g_in, lds, acc);
+          else
+            col2im_gen_kernel<false><<<grid_for(total, 256), 256, 0, s>>>(k.col, k.n, q.h, q.w, q.cin, d.kh, d.kw,
+                                                                          d.stride, d.pad_h, d.pad_w, q.ho, q.wo, g_in,
+                                                                          lds, acc);
           RALPB_TRY(cudaGetLastError());
           ++m->launches;
         }
@@ -577,14 +629,17 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
       }
     } else if (g_in != nullptr) {
       const long long total = rin * (q.cin / 8);
-      if (d.op == RALPB_NODE_MAXPOOL)
-        maxpool_gen_bwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(q.idx, g_out, ldo, k.n, q.h, q.w, q.cin, d.kh, d.kw,
-                                                                    d.stride, d.pad_h, d.pad_w, q.ho, q.wo, g_in, lds,
-                                                                    acc);
-      else
-        avgpool_gen_bwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(g_out, ldo, k.n, q.h, q.w, q.cin, d.kh, d.kw,
-                                                                    d.stride, d.pad_h, d.pad_w, q.ho, q.wo, g_in, lds,
-                                                                    acc);
+      const int gr = grid_for(total, 256);
+      const bool s1 = d.stride == 1;
+      if (d.op == RALPB_NODE_MAXPOOL) {
+        auto kern = s1 ? maxpool_gen_bwd_kernel<true> : maxpool_gen_bwd_kernel<false>;
+        kern<<<gr, 256, 0, s>>>(q.idx, g_out, ldo, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride, d.pad_h, d.pad_w, q.ho,
+                                q.wo, g_in, lds, acc);
+      } else {
+        auto kern = s1 ? avgpool_gen_bwd_kernel<true> : avgpool_gen_bwd_kernel<false>;
+        kern<<<gr, 256, 0, s>>>(g_out, ldo, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride, d.pad_h, d.pad_w, q.ho, q.wo,
+                                g_in, lds, acc);
+      }
       RALPB_TRY(cudaGetLastError());
       ++m->launches;
       st = 1;
