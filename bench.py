@@ -193,7 +193,8 @@ def run_reference(args):
 
 
 def _build_executor(strategy: str, world: int, rank: int, ring_backend: str = "native", fc_sharding: str = "single",
-                    precision: str = "bf16", placement: str = "colocated", model: str | None = None):
+                    precision: str = "bf16", placement: str = "colocated", model: str | None = None,
+                    shard_layout: str = "bytes"):
     from paper_1901_05803_b200 import synthetic
     from paper_1901_05803_b200.executor import RankExecutor
     from paper_1901_05803_b200.planner import JobSpec, Strategy, catalog_lookup, profile
@@ -208,7 +209,7 @@ def _build_executor(strategy: str, world: int, rank: int, ring_backend: str = "n
     else:
         job = JobSpec(m, Strategy.baseline(), world)
     ex = RankExecutor(job, rank=rank, world=world, ring_backend=ring_backend, fc_sharding=fc_sharding,
-                      precision=precision, placement=placement)
+                      precision=precision, placement=placement, shard_layout=shard_layout)
     ex.set_params(synthetic.init_params(ex.layers, 0))
     return ex, job, rep
 
@@ -374,6 +375,18 @@ def run_ours(args):
     stb = exb.stats()
     bytes_b = _job_bytes(stb, world)   # (a collective: every rank, outside the rank-0 block)
     exb.close()
+    # ... with the reference's own PS layout: whole weighted layers round-robin over the W shards
+    # (simulator.py:551-563), so fc1's 411 MB sits on one shard -- the paper's baseline hot spot
+    layer_shards = None
+    if world > 1:
+        torch.cuda.empty_cache()
+        exl, _, _ = _build_executor("baseline", world, rank, shard_layout="layers")
+        ms_l = _time_steps(exl, dimgs, dlabs, args.steps, args.warmup, world)
+        stl = exl.stats()
+        exl.close()
+        layer_shards = {"value": world * BATCH / (ms_l * 1e-3), "ms_per_step": ms_l,
+                        "logical_sync_bytes_per_step": _job_bytes(stl, world),
+                        "note": "all-on-PS with whole-layer round-robin PS shards (the reference's layout)"}
     # ring all-reduce comparators (StrategyKind.RING_ALLREDUCE, the Horovod baseline of the paper):
     # the hand-written NVLink RS+SGD+AG vs NCCL all_reduce of the gradient vector (N > 1)
     ring = None
@@ -479,6 +492,7 @@ def run_ours(args):
                                     "physical_nvlink_rank0": {"out": nvl[0], "in": nvl[1]}},
             "all_on_ps": {"value": world * BATCH / (ms_b * 1e-3), "ms_per_step": ms_b,
                           "logical_sync_bytes_per_step": bytes_b},
+            "all_on_ps_layer_shards": layer_shards,
             "ring_allreduce": ring,
             "ralp_fc_sharded": mps,
             "ralp_dedicated_ps": ralp_n,

@@ -160,8 +160,12 @@ typedef struct {
  * multi-PS future work; the reference forbids ps_count != 1 for RALP, costmodel.py:75-76): the
  * first FC layer column-parallel, the second row-parallel (partial sums reduced on rank 0), later
  * FC layers on rank 0; cuts all-gathered, the cut gradient reduce-scattered back. */
+/* BASELINE_LAYER_SHARDS: BASELINE with the reference's own PS shard layout -- whole weighted
+ * layers assigned round-robin to the W shards (simulator.py:551-563: "PS frameworks place whole
+ * variables"), so under parameter skew one shard carries most of the model (VGG-16: fc1) -- instead
+ * of equal contiguous byte shards.  Same logical bytes (volume_baseline), a different hot spot. */
 enum { RALPB_STRATEGY_BASELINE = 0, RALPB_STRATEGY_RALP = 1, RALPB_STRATEGY_RING = 2, RALPB_STRATEGY_RING_EXTERNAL = 3,
-       RALPB_STRATEGY_RALP_MPS = 4 };
+       RALPB_STRATEGY_RALP_MPS = 4, RALPB_STRATEGY_BASELINE_LAYER_SHARDS = 5 };
 
 typedef struct {
   int kind;            /* RALPB_CONV / RALPB_POOL / RALPB_FC / RALPB_BLOCK / RALPB_APOOL */

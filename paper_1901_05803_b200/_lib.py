@@ -102,6 +102,7 @@ RALPB_CONV, RALPB_POOL, RALPB_FC, RALPB_BLOCK, RALPB_APOOL, RALPB_MODULE = 0, 1,
 RALPB_NODE_CONV, RALPB_NODE_MAXPOOL, RALPB_NODE_AVGPOOL = 0, 1, 2
 RALPB_STRATEGY_BASELINE, RALPB_STRATEGY_RALP, RALPB_STRATEGY_RING, RALPB_STRATEGY_RING_EXTERNAL = 0, 1, 2, 3
 RALPB_STRATEGY_RALP_MPS = 4
+RALPB_STRATEGY_BASELINE_LAYER_SHARDS = 5
 RALPB_PRECISION_BF16, RALPB_PRECISION_FP32 = 0, 1
 PRECISIONS = {"bf16": RALPB_PRECISION_BF16, "fp32": RALPB_PRECISION_FP32}
 # ralpb_model_debug_buffer selectors (include/ralpb.h)

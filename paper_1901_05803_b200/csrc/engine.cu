@@ -101,7 +101,9 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, const ralpb_node_
     return 1;
   }
   if (batch % 4 != 0) { *why = "batch must be a multiple of 4"; return 1; }
-  if (strategy < RALPB_STRATEGY_BASELINE || strategy > RALPB_STRATEGY_RALP_MPS) { *why = "unknown strategy"; return 1; }
+  if (strategy < RALPB_STRATEGY_BASELINE || strategy > RALPB_STRATEGY_BASELINE_LAYER_SHARDS) { *why = "unknown strategy"; return 1; }
+  const bool layer_shards = strategy == RALPB_STRATEGY_BASELINE_LAYER_SHARDS;
+  if (layer_shards) strategy = RALPB_STRATEGY_BASELINE;   // the baseline with whole-layer PS shards
   if (precision != RALPB_PRECISION_BF16 && precision != RALPB_PRECISION_FP32) { *why = "unknown precision"; return 1; }
   if (workers != world && !(workers == world - 1 && workers >= 1 && strategy == RALPB_STRATEGY_RALP)) {
     *why = "workers must equal world, or world - 1 (RALP-N: a dedicated PS rank, RALP strategy only)";
@@ -112,6 +114,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, const ralpb_node_
     return 1;
   }
   auto m = new Model();
+  m->layer_shards = layer_shards;
   m->rank = rank; m->world = world; m->ps_rank = ps_rank; m->batch = batch;
   m->strategy = strategy; m->elem_bytes = elem_bytes;
   m->precision = precision;
@@ -388,12 +391,33 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, const ralpb_node_
     const long long n = placed ? m->n_front : m->n_total;
     const int groups = strategy == RALPB_STRATEGY_RALP ? workers : world;
     const long long shard = n / groups;
+    m->shard_ranges.assign(groups, {});
+    if (m->layer_shards) {
+      // the reference's PS layout: weighted layer k (in model order) -> shard k mod W, a layer's
+      // parameters being the contiguous span up to the next weighted layer's first tensor
+      std::vector<long long> starts;
+      for (const FrontLayer& f : m->front)
+        if (f.kind == RALPB_CONV || f.kind == RALPB_BLOCK || f.kind == RALPB_MODULE)
+          starts.push_back(f.b_off >= 0 ? std::min(f.w_off, f.b_off) : f.w_off);
+      for (const FcLayer& f : m->back) starts.push_back(std::min(f.w_off, f.b_off));
+      for (size_t k = 0; k < starts.size(); ++k) {
+        const long long hi = k + 1 < starts.size() ? starts[k + 1] : n;
+        auto& rg = m->shard_ranges[k % groups];
+        if (!rg.empty() && rg.back().second == starts[k]) rg.back().second = hi;   // merge adjacent (W = 1)
+        else rg.emplace_back(starts[k], hi);
+      }
+      for (const auto& rg : m->shard_ranges)
+        if (static_cast<int>(rg.size()) > kMaxShardRanges) return fail("too many layers per PS shard");
+    } else {
+      for (int g = 0; g < groups; ++g) m->shard_ranges[g].emplace_back(shard * g, shard * (g + 1));
+    }
     m->shard_real.assign(groups, 0);
     for (const auto& run : real_runs)
-      for (int g = 0; g < groups; ++g) {
-        const long long lo = std::max(run.first, shard * g), hi = std::min(run.first + run.second, shard * (g + 1));
-        if (hi > lo) m->shard_real[g] += hi - lo;
-      }
+      for (int g = 0; g < groups; ++g)
+        for (const auto& r : m->shard_ranges[g]) {
+          const long long lo = std::max(run.first, r.first), hi = std::min(run.first + run.second, r.second);
+          if (hi > lo) m->shard_real[g] += hi - lo;
+        }
   }
 
   // ---- exchange arena (identical layout on every rank)
@@ -1471,6 +1495,18 @@ int sync_params(Model* m, long long n, float lr, float mu, std::string* why) {
   const long long shard = n / W;  // n is a multiple of 4 * lcm(1..8)
   u.begin = shard * m->widx;
   u.end = u.begin + shard;
+  long long mine = shard;
+  if (m->layer_shards) {   // whole-layer shards (the reference's PS layout)
+    const auto& rg = m->shard_ranges[m->widx];
+    u.nr = static_cast<int>(rg.size());
+    mine = 0;
+    for (int k = 0; k < u.nr; ++k) {
+      u.rb[k] = rg[k].first;
+      u.re[k] = rg[k].second;
+      mine += rg[k].second - rg[k].first;
+    }
+    if (u.nr == 0) { u.nr = 1; u.rb[0] = u.re[0] = 0; }   // a shard without layers (W > weighted layers)
+  }
   u.lr = lr; u.mu = mu; u.gscale = 1.f;
   u.momentum = m->V;
   for (int w = 0; w < W; ++w) {
@@ -1480,7 +1516,7 @@ int sync_params(Model* m, long long n, float lr, float mu, std::string* why) {
   RALPB_TRY(shard_update(u, all_done, seq, m->counters + 0, m->stream));
   RALPB_TRY(wait_flags(m->flags + kFlagDone, W, seq, m->stream));
   m->launches += 4;
-  const long long peer = static_cast<long long>(W - 1) * shard * static_cast<long long>(sizeof(float));
+  const long long peer = static_cast<long long>(W - 1) * mine * static_cast<long long>(sizeof(float));
   m->nvl_in += peer;   // gradient shards of the other workers
   m->nvl_out += peer;  // the updated shard to the other workers
   return 0;

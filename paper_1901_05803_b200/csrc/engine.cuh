@@ -108,6 +108,8 @@ struct Model {
   bool is_worker = true;           // this rank runs a conv front
   int widx = 0;                    // this rank's worker index (rank order, the dedicated PS skipped)
   std::vector<int> worker_ranks;   // worker index -> rank
+  bool layer_shards = false;          // BASELINE_LAYER_SHARDS: whole layers round-robin over the shards
+  std::vector<std::vector<std::pair<long long, long long>>> shard_ranges;   // per shard: [lo, hi) floats
   std::vector<long long> shard_real;  // real (descriptor) parameters in each sync shard, for the
                                       // logical byte count of the pull / ring sites
   std::vector<ralpb_layer_desc> desc;

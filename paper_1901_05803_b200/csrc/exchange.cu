@@ -160,8 +160,7 @@ cudaError_t wait_flags(const uint32_t* flags, int n, const uint32_t* value, cuda
   return cudaGetLastError();
 }
 
-__global__ void shard_update_kernel(ShardUpdate u, PeerSignal done, const uint32_t* value, uint32_t* counter) {
-  const long long b4 = u.begin / 4, e4 = u.end / 4;
+__device__ __forceinline__ void shard_range(const ShardUpdate& u, long long b4, long long e4) {
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long i = b4 + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < e4; i += stride) {
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -178,17 +177,30 @@ __global__ void shard_update_kernel(ShardUpdate u, PeerSignal done, const uint32
     reinterpret_cast<float4*>(u.momentum)[i] = v;
     for (int r = 0; r < u.nranks; ++r) reinterpret_cast<float4*>(u.params[r])[i] = p;
   }
+}
+
+__global__ void shard_update_kernel(ShardUpdate u, PeerSignal done, const uint32_t* value, uint32_t* counter) {
+  if (u.nr > 0) {
+    for (int k = 0; k < u.nr; ++k) shard_range(u, u.rb[k] / 4, u.re[k] / 4);
+  } else {
+    shard_range(u, u.begin / 4, u.end / 4);
+  }
   finish_and_signal(done, value, counter);
 }
 
 cudaError_t shard_update(const ShardUpdate& u, const PeerSignal& done, const uint32_t* value,
                          uint32_t* counter, cudaStream_t s) {
-  long long n4 = (u.end - u.begin) / 4;
+  long long n = u.end - u.begin;
+  if (u.nr > 0) {
+    n = 0;
+    for (int k = 0; k < u.nr; ++k) n += u.re[k] - u.rb[k];
+  }
+  const long long n4 = n / 4;
   int grid = static_cast<int>(std::max<long long>(1, std::min<long long>((n4 + 255) / 256, num_sms() * 4)));
   // NVLink bytes of this rank PER DIRECTION: (W-1) peer shard reads of the gradient come in, the
   // same number of bytes of updated parameters go out (both directions run concurrently, so the
   // per-direction figure is what compares with the per-direction link peak)
-  const double peer_bytes = (u.nranks - 1) * static_cast<double>(u.end - u.begin) * sizeof(float);
+  const double peer_bytes = (u.nranks - 1) * static_cast<double>(n) * sizeof(float);
   launch_timed([&] { shard_update_kernel<<<grid, 256, 0, s>>>(u, done, value, counter); }, s, KIND_SHARD_UPDATE,
                peer_bytes, peer_bytes);
   return cudaGetLastError();

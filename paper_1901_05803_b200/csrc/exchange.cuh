@@ -61,12 +61,15 @@ cudaError_t wait_flags(const uint32_t* flags, int n, const uint32_t* value, cuda
 //   params[r][i] = p for every rank r
 // then signals `done` flags.  grads/params are arrays of per-rank device pointers
 // (peer pointers via IPC, local pointer for this rank).
+constexpr int kMaxShardRanges = 32;
 struct ShardUpdate {
   const float* grads[kMaxRanks];
   float* params[kMaxRanks];
   int nranks;
   int self;
   long long begin, end;  // float indices, multiples of 4
+  int nr;                // > 0: the shard is these ranges instead (whole-layer shards), multiples of 4
+  long long rb[kMaxShardRanges], re[kMaxShardRanges];
   float lr, mu, gscale;
   float* momentum;       // local, full-size vector (only the shard is touched)
 };

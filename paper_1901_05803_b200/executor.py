@@ -184,7 +184,8 @@ class RankExecutor:
 
     def __init__(self, job: JobSpec, *, rank: int = 0, world: Optional[int] = None, ps_rank: int = 0,
                  input_shape: Optional[tuple[int, int, int]] = None, ring_backend: str = "native",
-                 fc_sharding: str = "single", precision: str = "bf16", placement: str = "colocated"):
+                 fc_sharding: str = "single", precision: str = "bf16", placement: str = "colocated",
+                 shard_layout: str = "bytes"):
         """ring_backend (StrategyKind.RING_ALLREDUCE only): "native" = the hand-written
         reduce-scatter + SGD + all-gather over NVLink peer memory inside the step; "nccl" = the
         step stops after the backward, torch.distributed (NCCL) all-reduces the gradient vector
@@ -196,7 +197,11 @@ class RankExecutor:
         pairs through the same tcgen05 GEMM engine, include/ralpb.h RALPB_PRECISION_FP32).
         placement (StrategyKind.RALP only): "colocated" = W ranks, the PS role on ps_rank which is
         also a worker; "dedicated-ps" = the paper's RALP-N (costmodel.py:244-245): world = W + 1,
-        ps_rank runs only the FC tail, every other rank is a worker."""
+        ps_rank runs only the FC tail, every other rank is a worker.
+        shard_layout (StrategyKind.BASELINE_PS only): "bytes" = W equal contiguous shards of the
+        parameter vector (the B200-idiomatic layout); "layers" = the reference's own PS layout,
+        whole weighted layers round-robin over the W shards (simulator.py:551-563) -- under
+        parameter skew one shard carries most of the model, the paper's baseline hot spot."""
         kind = _kv(job.strategy.kind)
         if placement not in ("colocated", "dedicated-ps"):
             raise ExecutorError(f"unknown placement {placement!r}")
@@ -213,6 +218,9 @@ class RankExecutor:
             raise ExecutorError(f"unknown fc_sharding {fc_sharding!r}")
         if precision not in _lib.PRECISIONS:
             raise ExecutorError(f"unknown precision {precision!r}")
+        if shard_layout not in ("bytes", "layers") or (shard_layout == "layers" and kind != "baseline"):
+            raise ExecutorError(f"shard_layout {shard_layout!r}: 'bytes', or 'layers' for the all-on-PS baseline")
+        self.shard_layout = shard_layout
         self.fc_sharding = fc_sharding if kind == "ralp" else "single"
         self.ring_backend = ring_backend if kind == "ring" else None
         self.precision, self.placement = precision, placement
@@ -237,6 +245,8 @@ class RankExecutor:
             strategy = _lib.RALPB_STRATEGY_RALP if self.fc_sharding == "single" else _lib.RALPB_STRATEGY_RALP_MPS
         elif kind == "ring":
             strategy = _lib.RALPB_STRATEGY_RING if ring_backend == "native" else _lib.RALPB_STRATEGY_RING_EXTERNAL
+        elif shard_layout == "layers":
+            strategy = _lib.RALPB_STRATEGY_BASELINE_LAYER_SHARDS
         else:
             strategy = _lib.RALPB_STRATEGY_BASELINE
         self.lowered_split = split   # 1-based cut over the lowered layer table (0: none)
@@ -419,7 +429,7 @@ def _allgather_rows(row: list[float], world: int) -> list[list[float]]:
 def run_job(job: JobSpec, steps: int = 10, *, warmup: int = 0, seed: int = 0, lr: float = 0.01,
             momentum: float = 0.9, params=None, input_shape=None, name: Optional[str] = None,
             ring_backend: str = "native", fc_sharding: str = "single", precision: str = "bf16",
-            placement: str = "colocated") -> JobReport:
+            placement: str = "colocated", shard_layout: str = "bytes") -> JobReport:
     """Execute `job` for `steps` measured steps on this process's rank (RANK from the environment,
     torch.distributed already initialised when more than one rank takes part).  `job` may be the
     mirror's JobSpec or the unmodified reference's `ralp.JobSpec`.  Every step checks that the
@@ -430,7 +440,7 @@ def run_job(job: JobSpec, steps: int = 10, *, warmup: int = 0, seed: int = 0, lr
 
     rank = int(os.environ.get("RANK", "0"))
     ex = RankExecutor(job, rank=rank, input_shape=input_shape, ring_backend=ring_backend, fc_sharding=fc_sharding,
-                      precision=precision, placement=placement)
+                      precision=precision, placement=placement, shard_layout=shard_layout)
     try:
         if params is None:
             params = synthetic.init_params(ex.layers, seed)

@@ -86,9 +86,11 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
     baseline's, bytes are volume_ring's) or "ralp-mps" (layer-placed with the FC tail sharded
     over all ranks; numerics are RALP's, bytes volume_ralp_multi_ps).  placement="dedicated-ps":
     RALP-N, rank 0 runs only the FC tail and ranks 1..world-1 are the workers."""
-    fc_sharding = "single"
+    fc_sharding, shard_layout = "single", "bytes"
     if strategy == "ralp-mps":
         strategy, fc_sharding = "ralp", "multi"
+    if strategy == "baseline-layers":   # the reference's whole-layer round-robin PS shards
+        strategy, shard_layout = "baseline", "layers"
     workers = world - 1 if placement == "dedicated-ps" else world
     fc_at = next(i for i, l in enumerate(model.layers) if l.kind.value == "fc")
     split = fc_at if split is None else split   # < fc_at: a conv back segment on the PS
@@ -101,7 +103,7 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
         job, expect = JobSpec(model, Strategy.baseline(), workers), volume_baseline(model, workers)
     expect = expect.total_bytes_per_step
     ex = RankExecutor(job, rank=rank, world=world, ring_backend=ring_backend, fc_sharding=fc_sharding,
-                      placement=placement, precision=precision)
+                      placement=placement, precision=precision, shard_layout=shard_layout)
     params = synthetic.init_params(ex.layers, 1)
     ex.set_params(params)
     b = model.batch_size
@@ -111,10 +113,11 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
     # precision the plain fp32 oracle's own sensitivity)
     orc64 = ostep.OracleState(ex.layers, params) if rank == 0 and (floor or fp32) else None
     tag = (f"{strategy}-{ring_backend}" if strategy == "ring" else strategy + ("-mps" if fc_sharding == "multi" else "")
-           ) + ("-dedicated-ps" if placement == "dedicated-ps" else "") + ("-fp32" if fp32 else "")
+           ) + ("-dedicated-ps" if placement == "dedicated-ps" else "") + ("-fp32" if fp32 else "") + (
+        "-layer-shards" if shard_layout == "layers" else "")
     ok = True
     sync_all = strategy != "ralp"   # all-on-PS / ring synchronise every parameter
-    nsync = len(params) if sync_all else split
+    nsync = len(params) if sync_all else ex.lowered_split   # lowered layers (branch groups: != catalog split)
     for t in range(steps):
         if ex.is_worker:
             imgs, labs = synthetic.batch(1, t, ex.worker_index * b, b, ex.in_shape, ex.classes)
@@ -129,7 +132,7 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
         # ---- exchange: bit-exact cut rows / act-grad rows (layer-placed, single PS)
         if strategy == "ralp" and fc_sharding == "single" and not fp32:
             ps = ex.ps_rank
-            cut_local = torch.from_numpy(ex.debug_buffer(_lib.DBG_ACT, split)) if (ex.is_worker and rank != ps) else None
+            cut_local = torch.from_numpy(ex.debug_buffer(_lib.DBG_ACT, ex.lowered_split)) if (ex.is_worker and rank != ps) else None
             dcut = torch.from_numpy(ex.debug_buffer(_lib.DBG_CUT_GRAD)) if (ex.is_worker and rank != ps) else None
             n_cut = ex.debug_buffer(_lib.DBG_CUT_GRAD).size   # (the arena's act-grad slot exists on every rank)
             mine_cut = cut_local if cut_local is not None else torch.zeros(n_cut)
@@ -169,11 +172,11 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
         if rank == 0:
             batches = [synthetic.batch(1, t, w * b, b, ex.in_shape, ex.classes) for w in range(workers)]
             lo, wire = ostep.train_step(orc, "baseline" if strategy == "ring" else strategy, workers, batches, lr=lr,
-                                        emulate_bf16=not fp32, split=split if strategy == "ralp" else None)
+                                        emulate_bf16=not fp32, split=ex.lowered_split if strategy == "ralp" else None)
             l64 = None
             if orc64 is not None:
                 l64, _ = ostep.train_step(orc64, "baseline" if strategy == "ring" else strategy, workers, batches, lr=lr,
-                                          emulate_bf16=not fp32, accum64=True, split=split if strategy == "ralp" else None)
+                                          emulate_bf16=not fp32, accum64=True, split=ex.lowered_split if strategy == "ralp" else None)
             assert strategy == "ring" or fc_sharding == "multi" or wire == expect
             rel = abs(st.loss - lo) / abs(lo)
             # fp32: 1e-4, widened by the fp32 oracle's own fp64 spread where training is chaotic
@@ -194,7 +197,7 @@ def run(model, strategy, steps, rank, world, ring_backend="native", lr=0.01, flo
                 ok = False
     if rank == 0 and got is None:
         got = ex.get_params()   # the dedicated PS holds the FC tail; its front copy is not synced
-        got = [g if i >= split else None for i, g in enumerate(got)]
+        got = [g if i >= ex.lowered_split else None for i, g in enumerate(got)]
     ex.close()
     if rank == 0:
         w64s = orc64.numpy_params() if orc64 is not None else [None] * len(got)
@@ -240,6 +243,11 @@ def main():
         dict(model=cifar, strategy="ring", steps=3),
         dict(model=cifar, strategy="ring", steps=3, ring_backend="nccl"),
         dict(model=cifar, strategy="ralp-mps", steps=4),
+        dict(model=cifar, strategy="baseline-layers", steps=3),
+        dict(model=parse_model(TINY), strategy="baseline-layers", steps=3),
+        # branch groups (RALPB_MODULE) synchronised across ranks: GoogLeNet, FC-tail split
+        dict(model=catalog_lookup("googlenet").with_batch_size(4), strategy="ralp", steps=2, lr=1e-3, floor=True,
+             cap=0.5, split=62),
         dict(model=parse_model(TINY), strategy="ralp-mps", steps=3),
         # full VGG-16 geometry (224x224: first-conv, row-streamed 64-channel, slab pair kernels,
         # pool5 cut) at b=4 per rank
