@@ -11,12 +11,21 @@
 // 3x3 runs as an im2col GEMM forward / backward-filter, and its backward-data as the stride-1
 // kernel over the gradient dilated with zeros.  Storage is bf16 everywhere; every reduction fp32.
 #include <algorithm>
+#include <cstdlib>
 #include "block.cuh"
 #include "elementwise.cuh"
 #include "gemm_host.cuh"
 #include "resnet.cuh"
 
 namespace ralpb {
+
+bool bn_stats_fused() {
+  static const bool on = [] {
+    const char* e = getenv("RALPB_BN_STATS");
+    return e != nullptr && std::string(e) == "fused";
+  }();
+  return on;
+}
 
 namespace {
 
@@ -32,9 +41,11 @@ constexpr float kBnEps = 1e-5f;
     }                                                     \
   } while (0)
 
-// out[rows][n] = a[rows][k] . w[n][k]^T  (bf16 out).  With `stats` (the batch norm that follows):
-// the epilogue also sums each column and its square into m->bn_work (zeroed here) and mean / rstd
-// are finished into stats[0..n) / stats[n..2n) -- no separate statistics pass over `out`.
+// out[rows][n] = a[rows][k] . w[n][k]^T  (bf16 out).  With mean / rstd (the batch norm that
+// follows): its statistics over the rows -- by default one bn_stats pass over `out`; with
+// RALPB_BN_STATS=fused the GEMM epilogue sums each column and its square instead (measured slower:
+// the transpose-reduce costs the memory-bound 1x1 GEMMs more than the pass it saves, +1.9 ms vs
+// -1.35 ms per ResNet-50 step, profiles/r02/launches_resnet50_bnfused_summary.txt).
 int mm_fwd(Model* m, const bf16* a, long long rows, int k, const bf16* w, int n, bf16* out, std::string* why,
            float* mean = nullptr, float* rstd = nullptr) {
   GemmDesc d;
@@ -42,14 +53,18 @@ int mm_fwd(Model* m, const bf16* a, long long rows, int k, const bf16* w, int n,
   d.a = Operand2D{a, rows, k, k};
   d.b = Operand2D{w, n, k, k};
   d.epi = EPI_BF16; d.out = out; d.s_m = n;
-  if (mean != nullptr) {
+  const bool fused = mean != nullptr && bn_stats_fused();
+  if (fused) {
     RALPB_TRY(cudaMemsetAsync(m->bn_work, 0, sizeof(float) * 2 * n, m->stream));
     d.colstats = m->bn_work;
   }
   RALPB_TRY(gemm_launch(d, m->stream, why));
   ++m->launches;
-  if (mean != nullptr) {
+  if (fused) {
     RALPB_TRY(bn_finish(m->bn_work, n, rows, kBnEps, mean, rstd, m->stream));
+    ++m->launches;
+  } else if (mean != nullptr) {
+    RALPB_TRY(bn_stats(Act4{out, 0}, 1, 1, static_cast<int>(rows), n, kBnEps, m->bn_work, mean, rstd, m->stream));
     ++m->launches;
   }
   return 0;

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include "elementwise.cuh"
 #include "gemm_host.cuh"
+#include "block.cuh"
 #include "graph.cuh"
 #include "resnet.cuh"
 
@@ -73,28 +74,41 @@ struct Pix {
 
 // ------------------------------------------------------------------ layouts
 // out [n*ho*wo][kh*kw*c]: column (r*kw + s)*c + ch = x[img][oy*st + r - ph][ox*st + s - pw][ch]
-// (0 outside the image); x has pixel stride ldx.  Thread = (patch row, tap): the index math runs
-// once per tap and the thread copies the tap's c channels (contiguous in x and in out) 16 bytes at
-// a time; consecutive threads write consecutive taps of a row.  32-bit indices (module_build checks
-// rows * taps < 2^31).
-__global__ void im2col_gen_kernel(const bf16* __restrict__ x, int ldx, int n, int h, int w, int c, int kh, int kw,
-                                  int st, int ph, int pw, int ho, int wo, bf16* __restrict__ out) {
+// (0 outside the image); x has pixel stride ldx.  One warp per patch row: the lanes walk the
+// row's 16-byte chunks in order (tap-major), so every store instruction writes 512 contiguous
+// bytes; the row's (img, oy, ox) is decomposed once, a chunk's tap comes from incremental
+// (tap, group) counters and its (r - ph, s - pw) offsets from a per-block shared table.
+constexpr int kMaxTapsGen = 64;
+__global__ void __launch_bounds__(256) im2col_gen_kernel(const bf16* __restrict__ x, int ldx, int n, int h, int w, int c,
+                                                         int kh, int kw, int st, int ph, int pw, int ho, int wo,
+                                                         bf16* __restrict__ out) {
+  __shared__ int2 toff[kMaxTapsGen];
   const int groups = c >> 3, taps = kh * kw, hw = ho * wo;
-  const int total = n * hw * taps;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    const int row = t / taps;
-    const int tap = t - row * taps;
+  for (int t = threadIdx.x; t < taps; t += blockDim.x) toff[t] = make_int2(t / kw - ph, t % kw - pw);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int rows = n * hw;
+  const int chunks = taps * groups;
+  const int q32 = 32 / groups, r32 = 32 % groups;   // advance of (tap, group) per 32 chunks
+  const int t0 = lane / groups, g0 = lane % groups;
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += (gridDim.x * blockDim.x) >> 5) {
     const int img = row / hw;
     const int rr = row - img * hw;
     const int oy = rr / wo, ox = rr - oy * wo;
-    const int r = tap / kw, s = tap - r * kw;
-    const int iy = oy * st + r - ph, ix = ox * st + s - pw;
-    uint4* dst = reinterpret_cast<uint4*>(out + static_cast<long long>(t) * c);
-    if (iy >= 0 && iy < h && ix >= 0 && ix < w) {
-      const uint4* src = reinterpret_cast<const uint4*>(x + (static_cast<long long>(img * h + iy) * w + ix) * ldx);
-      for (int g = 0; g < groups; ++g) dst[g] = __ldg(src + g);
-    } else {
-      for (int g = 0; g < groups; ++g) dst[g] = make_uint4(0, 0, 0, 0);
+    const int y0 = oy * st, x0 = ox * st;
+    const bf16* xi = x + static_cast<long long>(img) * h * w * ldx;
+    uint4* orow = reinterpret_cast<uint4*>(out + static_cast<long long>(row) * chunks * 8);
+    int tap = t0, g = g0;
+    for (int j = lane; j < chunks; j += 32) {
+      const int2 o = toff[tap];
+      const int iy = y0 + o.x, ix = x0 + o.y;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (iy >= 0 && iy < h && ix >= 0 && ix < w)
+        v = __ldg(reinterpret_cast<const uint4*>(xi + (static_cast<long long>(iy) * w + ix) * ldx) + g);
+      orow[j] = v;
+      tap += q32;
+      g += r32;
+      if (g >= groups) { g -= groups; ++tap; }
     }
   }
 }
@@ -423,6 +437,7 @@ int module_build(ModuleBufs& k, const ralpb_node_desc* nodes, int n_nodes, int n
     q.wo = (q.w + 2 * d.pad_w - d.kw) / d.stride + 1;
     if (q.ho < 1 || q.wo < 1) { *why = tag + "window larger than its input"; return 1; }
     if (q.cin % 8 != 0) { *why = tag + "input channels must be a multiple of 8"; return 1; }
+    if (d.kh * d.kw > 64) { *why = tag + "windows above 64 taps are not implemented"; return 1; }
     if (static_cast<long long>(n) * q.ho * q.wo * d.kh * d.kw * (q.cin / 8) >= (1LL << 31) ||
         static_cast<long long>(n) * q.h * q.w * q.cin >= (1LL << 31)) {
       *why = tag + "tensor too large for 32-bit indexing";
@@ -520,7 +535,7 @@ int module_forward(Model* m, ModuleBufs& k, const bf16* x, bf16* y, std::string*
     if (d.op == RALPB_NODE_CONV) {
       const bf16* a = src;
       if (!q.direct) {
-        const long long total = rout * d.kh * d.kw;
+        const long long total = rout * 32;   // a warp per patch row
         im2col_gen_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride,
                                                                d.pad_h, d.pad_w, q.ho, q.wo, k.col);
         RALPB_TRY(cudaGetLastError());
@@ -528,10 +543,14 @@ int module_forward(Model* m, ModuleBufs& k, const bf16* x, bf16* y, std::string*
         a = k.col;
       }
       if (d.bn) {
-        // batch-norm statistics fused into the GEMM epilogue (sums of the stored bf16 output)
-        RALPB_TRY(cudaMemsetAsync(m->bn_work, 0, sizeof(float) * 2 * d.cout, s));
-        if (gemm_fwd(m, a, rout, q.K(), q.wbf, d.cout, q.z, d.cout, nullptr, 0, why, m->bn_work)) return 1;
-        RALPB_TRY(bn_finish(m->bn_work, d.cout, rout, kBnEps, q.stats, q.stats + d.cout, s));
+        if (bn_stats_fused()) {   // statistics from the GEMM epilogue (RALPB_BN_STATS=fused; block.cu)
+          RALPB_TRY(cudaMemsetAsync(m->bn_work, 0, sizeof(float) * 2 * d.cout, s));
+          if (gemm_fwd(m, a, rout, q.K(), q.wbf, d.cout, q.z, d.cout, nullptr, 0, why, m->bn_work)) return 1;
+          RALPB_TRY(bn_finish(m->bn_work, d.cout, rout, kBnEps, q.stats, q.stats + d.cout, s));
+        } else {
+          if (gemm_fwd(m, a, rout, q.K(), q.wbf, d.cout, q.z, d.cout, nullptr, 0, why)) return 1;
+          RALPB_TRY(bn_stats(Act4{q.z, 0}, k.n, q.ho, q.wo, d.cout, kBnEps, m->bn_work, q.stats, q.stats + d.cout, s));
+        }
         BnApply ap{};
         ap.x = Act4{q.z, 0}; ap.mean = q.stats; ap.rstd = q.stats + d.cout;
         ap.gamma = m->P + q.b_off; ap.beta = m->P + q.b_off + d.cout; ap.relu = 1;
@@ -599,7 +618,7 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
       if (q.direct) {
         if (gemm_wgrad(m, k.dz, rout, d.cout, src, q.cin, G + q.w_off, why)) return 1;
       } else {
-        const long long total = rout * d.kh * d.kw;
+        const long long total = rout * 32;   // a warp per patch row
         im2col_gen_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride,
                                                                d.pad_h, d.pad_w, q.ho, q.wo, k.col);
         RALPB_TRY(cudaGetLastError());
