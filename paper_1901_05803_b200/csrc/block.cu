@@ -11,21 +11,12 @@
 // 3x3 runs as an im2col GEMM forward / backward-filter, and its backward-data as the stride-1
 // kernel over the gradient dilated with zeros.  Storage is bf16 everywhere; every reduction fp32.
 #include <algorithm>
-#include <cstdlib>
 #include "block.cuh"
 #include "elementwise.cuh"
 #include "gemm_host.cuh"
 #include "resnet.cuh"
 
 namespace ralpb {
-
-bool bn_stats_fused() {
-  static const bool on = [] {
-    const char* e = getenv("RALPB_BN_STATS");
-    return e != nullptr && std::string(e) == "fused";
-  }();
-  return on;
-}
 
 namespace {
 
@@ -41,32 +32,15 @@ constexpr float kBnEps = 1e-5f;
     }                                                     \
   } while (0)
 
-// out[rows][n] = a[rows][k] . w[n][k]^T  (bf16 out).  With mean / rstd (the batch norm that
-// follows): its statistics over the rows -- by default one bn_stats pass over `out`; with
-// RALPB_BN_STATS=fused the GEMM epilogue sums each column and its square instead (measured slower:
-// the transpose-reduce costs the memory-bound 1x1 GEMMs more than the pass it saves, +1.9 ms vs
-// -1.35 ms per ResNet-50 step, profiles/r02/launches_resnet50_bnfused_summary.txt).
-int mm_fwd(Model* m, const bf16* a, long long rows, int k, const bf16* w, int n, bf16* out, std::string* why,
-           float* mean = nullptr, float* rstd = nullptr) {
+// out[rows][n] = a[rows][k] . w[n][k]^T  (bf16 out)
+int mm_fwd(Model* m, const bf16* a, long long rows, int k, const bf16* w, int n, bf16* out, std::string* why) {
   GemmDesc d;
   d.M = static_cast<int>(rows); d.N = n; d.K = k;
   d.a = Operand2D{a, rows, k, k};
   d.b = Operand2D{w, n, k, k};
   d.epi = EPI_BF16; d.out = out; d.s_m = n;
-  const bool fused = mean != nullptr && bn_stats_fused();
-  if (fused) {
-    RALPB_TRY(cudaMemsetAsync(m->bn_work, 0, sizeof(float) * 2 * n, m->stream));
-    d.colstats = m->bn_work;
-  }
   RALPB_TRY(gemm_launch(d, m->stream, why));
   ++m->launches;
-  if (fused) {
-    RALPB_TRY(bn_finish(m->bn_work, n, rows, kBnEps, mean, rstd, m->stream));
-    ++m->launches;
-  } else if (mean != nullptr) {
-    RALPB_TRY(bn_stats(Act4{out, 0}, 1, 1, static_cast<int>(rows), n, kBnEps, m->bn_work, mean, rstd, m->stream));
-    ++m->launches;
-  }
   return 0;
 }
 // out[rows][k] = dy[rows][n] . w[n][k]
@@ -167,7 +141,8 @@ int block_forward(Model* m, BlockBufs& k, const bf16* x, bf16* y, std::string* w
   const bool s1 = k.stride == 1;
   float* P = m->P;
   // conv a (1x1) + bn_a + ReLU -> a (padded for the 3x3)
-  if (mm_fwd(m, x, rin, k.cin, k.wa, k.width, k.a_pre, why, mean_of(k, 0), rstd_of(k, 0))) return 1;
+  if (mm_fwd(m, x, rin, k.cin, k.wa, k.width, k.a_pre, why)) return 1;
+  RALPB_TRY(bn_stats(Act4{k.a_pre, 0}, k.n, k.h, k.w, k.width, kBnEps, m->bn_work, mean_of(k, 0), rstd_of(k, 0), s));
   {
     BnApply ap{};
     ap.x = Act4{k.a_pre, 0}; ap.mean = mean_of(k, 0); ap.rstd = rstd_of(k, 0);
@@ -176,14 +151,14 @@ int block_forward(Model* m, BlockBufs& k, const bf16* x, bf16* y, std::string* w
     RALPB_TRY(bn_apply(ap, s));
   }
   // conv b (3x3, stride s) + bn_b + ReLU -> b
-  const Act4 bpre{k.b_pre, s1 ? 1 : 0};
   if (s1) {
     RALPB_TRY(conv_fwd(geom_b(k), k.a, k.wbf, nullptr, k.b_pre, 0, s, why));
-    RALPB_TRY(bn_stats(bpre, k.n, k.ho, k.wo, k.width, kBnEps, m->bn_work, mean_of(k, 1), rstd_of(k, 1), s));
   } else {
     RALPB_TRY(im2col_bf16(Act4{k.a, 1}, k.n, k.h, k.w, k.width, 3, k.stride, 1, k.ho, k.wo, k.col, s));
-    if (mm_fwd(m, k.col, rout, 9 * k.width, k.wbf, k.width, k.b_pre, why, mean_of(k, 1), rstd_of(k, 1))) return 1;
+    if (mm_fwd(m, k.col, rout, 9 * k.width, k.wbf, k.width, k.b_pre, why)) return 1;
   }
+  const Act4 bpre{k.b_pre, s1 ? 1 : 0};
+  RALPB_TRY(bn_stats(bpre, k.n, k.ho, k.wo, k.width, kBnEps, m->bn_work, mean_of(k, 1), rstd_of(k, 1), s));
   {
     BnApply ap{};
     ap.x = bpre; ap.mean = mean_of(k, 1); ap.rstd = rstd_of(k, 1);
@@ -192,14 +167,16 @@ int block_forward(Model* m, BlockBufs& k, const bf16* x, bf16* y, std::string* w
     RALPB_TRY(bn_apply(ap, s));
   }
   // conv c (1x1), the shortcut, bn_c + add + ReLU -> y
-  if (mm_fwd(m, k.b, rout, k.width, k.wc, k.cout, k.c_pre, why, mean_of(k, 2), rstd_of(k, 2))) return 1;
+  if (mm_fwd(m, k.b, rout, k.width, k.wc, k.cout, k.c_pre, why)) return 1;
+  RALPB_TRY(bn_stats(Act4{k.c_pre, 0}, k.n, k.ho, k.wo, k.cout, kBnEps, m->bn_work, mean_of(k, 2), rstd_of(k, 2), s));
   if (k.down) {
     const bf16* xin = x;
     if (!s1) {
       RALPB_TRY(subsample(Act4{x, 0}, k.n, k.h, k.w, k.cin, k.stride, k.d_in, s));
       xin = k.d_in;
     }
-    if (mm_fwd(m, xin, rout, k.cin, k.wd, k.cout, k.d_pre, why, mean_of(k, 3), rstd_of(k, 3))) return 1;
+    if (mm_fwd(m, xin, rout, k.cin, k.wd, k.cout, k.d_pre, why)) return 1;
+    RALPB_TRY(bn_stats(Act4{k.d_pre, 0}, k.n, k.ho, k.wo, k.cout, kBnEps, m->bn_work, mean_of(k, 3), rstd_of(k, 3), s));
   }
   {
     BnApply ap{};
@@ -300,8 +277,9 @@ int block_backward(Model* m, BlockBufs& k, const bf16* x, const bf16* y, const b
 int bn_stem_forward(Model* m, FrontLayer& f, const ActBuf& in, const ActBuf& out, std::string* why) {
   cudaStream_t s = m->stream;
   const long long rows = in.rows();
+  if (mm_fwd(m, in.ptr, rows, f.kpad, f.wf, f.g.cout, f.pre, why)) return 1;
   const int c = f.g.cout;
-  if (mm_fwd(m, in.ptr, rows, f.kpad, f.wf, c, f.pre, why, f.bn_stats, f.bn_stats + c)) return 1;
+  RALPB_TRY(bn_stats(Act4{f.pre, 0}, out.n, out.h, out.w, c, kBnEps, m->bn_work, f.bn_stats, f.bn_stats + c, s));
   BnApply ap{};
   ap.x = Act4{f.pre, 0}; ap.mean = f.bn_stats; ap.rstd = f.bn_stats + c;
   ap.gamma = m->P + f.b_off; ap.beta = m->P + f.b_off + c; ap.relu = 1; ap.y = MutAct4{out.ptr, out.pad};

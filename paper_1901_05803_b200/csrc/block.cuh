@@ -7,8 +7,6 @@
 namespace ralpb {
 
 int block_alloc(Model* m, BlockBufs& k, std::string* why);
-// RALPB_BN_STATS=fused: batch-norm statistics from the producing GEMM's epilogue (off by default)
-bool bn_stats_fused();
 int block_prep(Model* m, BlockBufs& k, cudaStream_t s, std::string* why);
 // x [n][h][w][cin] -> y [n][ho][wo][cout] (unpadded NHWC)
 int block_forward(Model* m, BlockBufs& k, const __nv_bfloat16* x, __nv_bfloat16* y, std::string* why);

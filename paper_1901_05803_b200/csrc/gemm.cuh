@@ -62,12 +62,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
   uint64_t* tfull = empty + stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* s_stats = reinterpret_cast<float*>(tmem_slot + 4);   // colstats: [2][N] per-CTA partial sums
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  if (p.colstats != nullptr)
-    for (int i = threadIdx.x; i < 2 * p.N; i += blockDim.x) s_stats[i] = 0.f;
   const int bn = p.block_n;
   const uint32_t tmem_cols = bn * 2 <= 32 ? 32 : (bn * 2 <= 64 ? 64 : (bn * 2 <= 128 ? 128 : (bn * 2 <= 256 ? 256 : 512)));
 
@@ -184,37 +181,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
         tmem_wait_ld();
         const int n0 = nt * bn + c;
         if (n0 >= p.N) continue;           // warp-uniform
+        if (!row_ok && !p.tma_epi) continue;
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (p.colstats != nullptr) {
-          // batch-norm statistics of the stored (bf16) output, fused: per column the sum and the
-          // sum of squares over this warp's 32 rows (transpose-reduce: lane l ends with column
-          // n0 + l, 31 shuffles per quantity), then one shared-memory atomic per column
-          float a1[32], a2[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float b = row_ok ? __bfloat162float(__float2bfloat16_rn(v[j])) : 0.f;
-            a1[j] = b;
-            a2[j] = b * b;
-          }
-#pragma unroll
-          for (int off = 16; off >= 1; off >>= 1) {
-            const bool up = lane & off;
-#pragma unroll
-            for (int j = 0; j < off; ++j) {
-              const float s1 = up ? a1[j] : a1[j + off], k1 = up ? a1[j + off] : a1[j];
-              const float s2 = up ? a2[j] : a2[j + off], k2 = up ? a2[j + off] : a2[j];
-              a1[j] = k1 + __shfl_xor_sync(0xffffffffu, s1, off);
-              a2[j] = k2 + __shfl_xor_sync(0xffffffffu, s2, off);
-            }
-          }
-          if (n0 + lane < p.N) {
-            atomicAdd(&s_stats[n0 + lane], a1[0]);
-            atomicAdd(&s_stats[p.N + n0 + lane], a2[0]);
-          }
-        }
-        if (!row_ok && !p.tma_epi) continue;
         const bool full_chunk = n0 + 32 <= p.N;
         if (p.bias != nullptr) {
 #pragma unroll
@@ -348,8 +318,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
     tc_fence_after();
     tmem_dealloc(tmem_base, tmem_cols);
   }
-  if (p.colstats != nullptr)
-    for (int i = threadIdx.x; i < 2 * p.N; i += blockDim.x) atomicAdd(p.colstats + i, s_stats[i]);
 }
 
 }  // namespace ralpb

@@ -156,15 +156,10 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
   // ---- stages
   const int stage_bytes = kAStage + p.b_stage_bytes;
   const int staging = p.tma_epi ? 2 * 16384 : 0;
-  if (d.colstats != nullptr && (d.epi != EPI_BF16 || d.N > 4096)) {
-    *why = "colstats: EPI_BF16 with N <= 4096 only";
-    return cudaErrorInvalidValue;
-  }
-  const int stats_bytes = d.colstats != nullptr ? 2 * d.N * 4 : 0;
-  const int budget = 227 * 1024 - 1024 - 256 - staging - stats_bytes;
+  const int budget = 227 * 1024 - 1024 - 256 - staging;
   p.stages = std::min(8, budget / stage_bytes);
   if (const char* e = getenv("RALPB_STAGES")) p.stages = std::max(1, std::min(p.stages, atoi(e)));
-  const int smem = 1024 + p.stages * stage_bytes + staging + 256 + stats_bytes;
+  const int smem = 1024 + p.stages * stage_bytes + staging + 256;
   p.idesc = umma_idesc_bf16(kBM, bn, !a_k, !b_k);
   p.a_mode = d.a_mode;
   p.b_mode = d.b_mode;
@@ -186,7 +181,6 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
   p.mask = reinterpret_cast<const __nv_bfloat16*>(d.mask);
   p.mask_s = d.mask_s;
   p.border = d.border;
-  p.colstats = d.colstats;
   p.img_rows = d.img_rows;
   p.wp = d.wp;
   p.pad = d.pad;

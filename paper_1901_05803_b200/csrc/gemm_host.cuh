@@ -38,7 +38,6 @@ struct GemmDesc {
   float sgd_lr = 0.f, sgd_mu = 0.f;
   const void* mask = nullptr;
   long long mask_s = 0;
-  float* colstats = nullptr;  // EPI_BF16 only: += [sum | sum of squares] per column of the stored output
   int border = 0;
   int img_rows = 1, wp = 1, pad = 0, h = 0, w = 0;
 };

@@ -66,8 +66,6 @@ struct alignas(64) GemmParams {
   float sgd_lr, sgd_mu;
   const __nv_bfloat16* mask;  // relu-backward mask source (mask[m*mask_s + n] > 0), or nullptr
   long long mask_s;
-  float* colstats;          // optional (EPI_BF16): += per column [sum | sum of squares] of the stored
-                            // bf16 output over the M rows ([2][N] fp32; fused batch-norm statistics)
   int border;               // zero rows that are padding positions of the padded layout
   int img_rows, wp, pad, h, w;
 };

@@ -19,7 +19,6 @@
 #include <algorithm>
 #include "elementwise.cuh"
 #include "gemm_host.cuh"
-#include "block.cuh"
 #include "graph.cuh"
 #include "resnet.cuh"
 
@@ -355,14 +354,13 @@ __global__ void relu_grad_kernel(const bf16* __restrict__ dy, int ldy, const bf1
 // ------------------------------------------------------------------ GEMM helpers
 // out[rows][n] (pixel stride ldo) = a[rows][k] . w[n][k]^T, optional bias + ReLU epilogue
 int gemm_fwd(Model* m, const bf16* a, long long rows, long long k, const bf16* w, int n, bf16* out, long long ldo,
-             const float* bias, int relu, std::string* why, float* colstats = nullptr) {
+             const float* bias, int relu, std::string* why) {
   GemmDesc d;
   d.M = static_cast<int>(rows); d.N = n; d.K = k;
   d.a = Operand2D{a, rows, k, k};
   d.b = Operand2D{w, n, k, k};
   d.epi = EPI_BF16; d.out = out; d.s_m = ldo;
   d.bias = bias; d.relu = relu;
-  d.colstats = colstats;
   RALPB_TRY(gemm_launch(d, m->stream, why));
   ++m->launches;
   return 0;
@@ -543,14 +541,8 @@ int module_forward(Model* m, ModuleBufs& k, const bf16* x, bf16* y, std::string*
         a = k.col;
       }
       if (d.bn) {
-        if (bn_stats_fused()) {   // statistics from the GEMM epilogue (RALPB_BN_STATS=fused; block.cu)
-          RALPB_TRY(cudaMemsetAsync(m->bn_work, 0, sizeof(float) * 2 * d.cout, s));
-          if (gemm_fwd(m, a, rout, q.K(), q.wbf, d.cout, q.z, d.cout, nullptr, 0, why, m->bn_work)) return 1;
-          RALPB_TRY(bn_finish(m->bn_work, d.cout, rout, kBnEps, q.stats, q.stats + d.cout, s));
-        } else {
-          if (gemm_fwd(m, a, rout, q.K(), q.wbf, d.cout, q.z, d.cout, nullptr, 0, why)) return 1;
-          RALPB_TRY(bn_stats(Act4{q.z, 0}, k.n, q.ho, q.wo, d.cout, kBnEps, m->bn_work, q.stats, q.stats + d.cout, s));
-        }
+        if (gemm_fwd(m, a, rout, q.K(), q.wbf, d.cout, q.z, d.cout, nullptr, 0, why)) return 1;
+        RALPB_TRY(bn_stats(Act4{q.z, 0}, k.n, q.ho, q.wo, d.cout, kBnEps, m->bn_work, q.stats, q.stats + d.cout, s));
         BnApply ap{};
         ap.x = Act4{q.z, 0}; ap.mean = q.stats; ap.rstd = q.stats + d.cout;
         ap.gamma = m->P + q.b_off; ap.beta = m->P + q.b_off + d.cout; ap.relu = 1;

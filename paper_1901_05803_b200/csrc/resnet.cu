@@ -474,11 +474,6 @@ cudaError_t bn_stats(Act4 x, int n, int h, int w, int c, float eps, float* work,
   return cudaGetLastError();
 }
 
-cudaError_t bn_finish(const float* sums, int c, long long count, float eps, float* mean, float* rstd, cudaStream_t s) {
-  bn_finish_kernel<<<(c + 255) / 256, 256, 0, s>>>(sums, c, 1.f / static_cast<float>(count), eps, mean, rstd);
-  return cudaGetLastError();
-}
-
 cudaError_t bn_apply(const BnApply& a, cudaStream_t s) {
   const long long pixels = static_cast<long long>(a.n) * a.h * a.w;
   if (a.c % 8 != 0 || a.c / 8 > 256 || !fits(pixels * a.c)) return cudaErrorInvalidValue;

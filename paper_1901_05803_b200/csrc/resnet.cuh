@@ -30,10 +30,6 @@ struct MutAct4 {
 cudaError_t bn_stats(Act4 x, int n, int h, int w, int c, float eps, float* work, float* mean, float* rstd,
                      cudaStream_t s);
 
-// mean / rstd from [sum | sum of squares] (c each) over `count` values -- the statistics a GEMM
-// epilogue accumulated (GemmDesc::colstats), finishing what bn_stats does in one pass
-cudaError_t bn_finish(const float* sums, int c, long long count, float eps, float* mean, float* rstd, cudaStream_t s);
-
 // y = act((x - mean) * rstd * gamma + beta + residual), act = ReLU if relu; residual: none
 // (res_kind 0), a raw tensor r (1), or the batch norm of r with its own statistics (2).
 struct BnApply {
