@@ -150,3 +150,44 @@ def test_handle_exchange_gloo_world2():
         p.join(60)
     for r in range(2):
         assert res[r] == [bytes([0]) * 64, bytes([1]) * 64]
+
+
+def _report_worker(rank, world, port, q, placement):
+    """One rank of run_job's report assembly (executor._allgather_rows + _breakdown) over gloo."""
+    from paper_1901_05803_b200.executor import _allgather_rows, _breakdown
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # row: [step, ms_step, ms_front (fwd + bwd), ms_back, is_worker, holds_back]
+    dedicated = placement == "dedicated-ps"
+    is_worker = not (dedicated and rank == 0)
+    row = [1.0, 10.0 + rank, 6.0 + rank if is_worker else 0.0, 2.0 if rank == 0 else 0.0, float(is_worker),
+           float(rank == 0)]
+    rows = _allgather_rows(row, world)
+    bd = _breakdown("job", 1, rows, "ralp")
+    q.put((rank, rows, bd.worker_computation, bd.ps_computation, bd.communication, bd.memcopy))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("placement", ["colocated", "dedicated-ps"])
+def test_report_rows_gloo_world2(placement):
+    """run_job's per-worker report at world 2: every rank gathers every rank's measured row in rank
+    order and charges times per worker (the colocated PS's back segment to worker 0; a dedicated PS's
+    to the workers in equal shares)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + os.getpid() % 1000 + (7 if placement == "dedicated-ps" else 0)
+    procs = [ctx.Process(target=_report_worker, args=(r, 2, port, q, placement)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r[0], r[1:]) for r in (q.get(timeout=120) for _ in range(2)))
+    for p in procs:
+        p.join(60)
+    assert res[0] == res[1]   # every rank holds the same report
+    rows, comp, ps, comm, mem = res[0]
+    assert [r[1] for r in rows] == [10.0, 11.0]
+    if placement == "colocated":
+        assert comp == pytest.approx((6e-3, 7e-3)) and ps == pytest.approx((2e-3, 0.0))
+        assert comm == pytest.approx((10e-3 - 6e-3 - 2e-3, 11e-3 - 7e-3))
+        assert mem == (0.0, 0.0)
+    else:   # one worker (rank 1); the dedicated PS's 2 ms charged to it
+        assert comp == pytest.approx((7e-3,)) and ps == pytest.approx((2e-3,)) and mem == (0.0,)
