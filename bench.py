@@ -367,18 +367,37 @@ def run_ours(args):
     step_ms = sum(k["ms"] for k in by_kind.values())
     step_achieved = flops_rank / (step_ms * 1e-3) / 1e12 if step_ms > 0 else None
 
-    # all-on-PS comparator (StrategyKind.BASELINE_PS): same workload, every layer on every worker
     ex.close()
-    torch.cuda.empty_cache()
-    exb, jobb, _ = _build_executor("baseline", world, rank)
-    ms_b = _time_steps(exb, dimgs, dlabs, args.steps, args.warmup, world)
-    stb = exb.stats()
-    bytes_b = _job_bytes(stb, world)   # (a collective: every rank, outside the rank-0 block)
-    exb.close()
+    cmp = not args.quick   # --quick: the headline line only (A/B runs)
+    # the same layer-placed step with ONE parameter sync after the whole backward (no sync bucket
+    # under the remaining backward, RALPB_SYNC_BUCKET=0): what the bucketed sync saves
+    unbucketed = None
+    if world > 1:
+        torch.cuda.empty_cache()
+        os.environ["RALPB_SYNC_BUCKET"] = "0"
+        try:
+            exu, _, _ = _build_executor("ralp", world, rank)
+        finally:
+            os.environ.pop("RALPB_SYNC_BUCKET", None)
+        ms_u = _time_steps(exu, dimgs, dlabs, args.steps, args.warmup, world)
+        stu = exu.stats()
+        exu.close()
+        unbucketed = {"value": world * BATCH / (ms_u * 1e-3), "ms_per_step": ms_u,
+                      "ms_sync_rank0": stu.ms_sync,
+                      "note": "RALPB_SYNC_BUCKET=0: the whole front synchronised after the backward"}
+    # all-on-PS comparator (StrategyKind.BASELINE_PS): same workload, every layer on every worker
+    ms_b = bytes_b = None
+    if cmp:
+        torch.cuda.empty_cache()
+        exb, jobb, _ = _build_executor("baseline", world, rank)
+        ms_b = _time_steps(exb, dimgs, dlabs, args.steps, args.warmup, world)
+        stb = exb.stats()
+        bytes_b = _job_bytes(stb, world)   # (a collective: every rank, outside the rank-0 block)
+        exb.close()
     # ... with the reference's own PS layout: whole weighted layers round-robin over the W shards
     # (simulator.py:551-563), so fc1's 411 MB sits on one shard -- the paper's baseline hot spot
     layer_shards = None
-    if world > 1:
+    if world > 1 and cmp:
         torch.cuda.empty_cache()
         exl, _, _ = _build_executor("baseline", world, rank, shard_layout="layers")
         ms_l = _time_steps(exl, dimgs, dlabs, args.steps, args.warmup, world)
@@ -390,7 +409,7 @@ def run_ours(args):
     # ring all-reduce comparators (StrategyKind.RING_ALLREDUCE, the Horovod baseline of the paper):
     # the hand-written NVLink RS+SGD+AG vs NCCL all_reduce of the gradient vector (N > 1)
     ring = None
-    if world > 1:
+    if world > 1 and cmp:
         ring = {}
         for backend in ("native", "nccl"):
             torch.cuda.empty_cache()
@@ -402,7 +421,7 @@ def run_ours(args):
                              "logical_sync_bytes_per_step": _job_bytes(str_, world)}
     # layer-placed with the FC tail sharded over every GPU (the paper's multi-PS)
     mps = None
-    if world > 1:
+    if world > 1 and cmp:
         torch.cuda.empty_cache()
         exm, _, _ = _build_executor("ralp", world, rank, fc_sharding="multi")
         ms_m = _time_steps(exm, dimgs, dlabs, args.steps, args.warmup, world)
@@ -415,7 +434,7 @@ def run_ours(args):
     # the parity precision (fp32-accurate (hi, lo) pairs through the same tcgen05 GEMM engine): a
     # same-precision number beside the fp32 CPU arm
     fp32 = None
-    if not args.no_fp32:
+    if not args.no_fp32 and cmp:
         torch.cuda.empty_cache()
         exf, _, _ = _build_executor("ralp", world, rank, precision="fp32")
         ms_f = _time_steps(exf, dimgs, dlabs, max(3, args.steps // 4), 3, world)
@@ -428,7 +447,7 @@ def run_ours(args):
                         "tests/test_parity_fp32_gpu.py pins it to the plain fp32 oracle"}
     # RALP-N (costmodel.py:244-245): N-1 workers + a dedicated PS GPU (rank 0)
     ralp_n = None
-    if world > 1:
+    if world > 1 and cmp:
         torch.cuda.empty_cache()
         exn, jobn, _ = _build_executor("ralp", world, rank, placement="dedicated-ps")
         if exn.is_worker:
@@ -467,12 +486,12 @@ def run_ours(args):
                         f"{repc.split_index}; tensor_frac_of_step = compute_load() FLOPs / wall step time / "
                         "sustained bf16 peak"}
 
-    resnet50 = catalog_comparator("resnet-50") if not args.no_resnet and MODEL != "resnet-50" else None
-    inception_v3 = catalog_comparator("inception-v3") if not args.no_branchy else None
-    googlenet = catalog_comparator("googlenet") if not args.no_branchy else None
+    resnet50 = catalog_comparator("resnet-50") if cmp and not args.no_resnet and MODEL != "resnet-50" else None
+    inception_v3 = catalog_comparator("inception-v3") if cmp and not args.no_branchy else None
+    googlenet = catalog_comparator("googlenet") if cmp and not args.no_branchy else None
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and cmp:
         cpu = _cpu_baseline_step(BATCH, 1, 1)
 
     if rank == 0:
@@ -490,8 +509,9 @@ def run_ours(args):
                                     "oracle_volume_ralp": volume_ralp(m, rep.split_index, world).total_bytes_per_step,
                                     "logical_counted_rank0": st.logical_bytes,
                                     "physical_nvlink_rank0": {"out": nvl[0], "in": nvl[1]}},
-            "all_on_ps": {"value": world * BATCH / (ms_b * 1e-3), "ms_per_step": ms_b,
-                          "logical_sync_bytes_per_step": bytes_b},
+            "all_on_ps": None if ms_b is None else {"value": world * BATCH / (ms_b * 1e-3), "ms_per_step": ms_b,
+                                                    "logical_sync_bytes_per_step": bytes_b},
+            "ralp_unbucketed_sync": unbucketed,
             "all_on_ps_layer_shards": layer_shards,
             "ring_allreduce": ring,
             "ralp_fc_sharded": mps,
@@ -550,6 +570,7 @@ def main():
     ap.add_argument("--no-fp32", action="store_true", help="skip the parity-precision comparator")
     ap.add_argument("--no-resnet", action="store_true", help="skip the ResNet-50 comparator")
     ap.add_argument("--no-branchy", action="store_true", help="skip the Inception-v3 / GoogLeNet comparators")
+    ap.add_argument("--quick", action="store_true", help="headline line only (no comparators / CPU baseline)")
     ap.add_argument("--model", default=MODEL, help="catalog model (BASELINE configs: vgg16 headline, alexnet)")
     ap.add_argument("--batch", type=int, default=BATCH, help="per-worker batch")
     args = ap.parse_args()

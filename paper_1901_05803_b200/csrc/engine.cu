@@ -51,7 +51,9 @@ constexpr int kFlagDh1 = 40;      // [1]  RALP_MPS: FC-1 output gradient landed
 constexpr int kFlagDcut = 48;     // [8]  RALP_MPS: rank r's partial of this rank's cut gradient landed
 constexpr int kFlagLoss = 56;     // [7]  ps_rank: worker w's own-row loss sum landed (baseline / ring)
 constexpr int kFlagPsFree = 64;   // [1]  worker: the dedicated PS finished the previous step
-constexpr int kNumFlags = 80;
+constexpr int kFlagGradB = 80;    // [8]  rank r finished the backward of the sync bucket's layers
+constexpr int kFlagDoneB = 88;    // [8]  rank r finished its shard of the sync bucket
+constexpr int kNumFlags = 96;
 constexpr int kCtrScatter = 48;   // [8]  per-destination counters of the fused act-grad scatter
 // The parameter vector is padded to a multiple of 4 * lcm(1..8) floats, so every sync group size
 // (world, or world - 1 workers with a dedicated PS) splits it into float4-aligned equal shards.
@@ -351,6 +353,47 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, const ralpb_node_
   m->bseg_end = align_up(off, 4);
   off = align_up(off, kShardAlign);
   m->real_total = m->real_front + m->real_bseg;
+  // sync bucket (layer-placed, W > 1, bf16): the smallest cut k whose earlier layers still hold
+  // >= 30 % of the front's forward FLOPs (their backward hides the bucket's update) while layers
+  // [k, split) hold >= half of the synchronised parameters.  RALPB_SYNC_BUCKET=0: one sync after
+  // the whole backward.
+  {
+    const char* be = getenv("RALPB_SYNC_BUCKET");
+    const bool want = !(be != nullptr && be[0] == '0') && layer_placed && workers > 1 &&
+                      precision == RALPB_PRECISION_BF16 && !m->layer_shards;
+    if (want) {
+      std::vector<double> fl(m->split, 0.0);
+      double total = 0.0;
+      for (int i = 0; i < m->split; ++i) {
+        const ralpb_layer_desc& d = layers[i];
+        const FrontLayer& f = m->front[i];
+        const ActBuf& o = m->acts[i + 1];
+        if (d.kind == RALPB_CONV) {
+          fl[i] = 2.0 * d.k * d.k * d.cin * d.cout * o.h * o.w;
+        } else if (d.kind == RALPB_BLOCK) {
+          const BlockBufs& k = m->blocks[f.blk];
+          fl[i] = 2.0 * (static_cast<double>(k.h) * k.w * k.cin * k.width + 9.0 * k.ho * k.wo * k.width * k.width +
+                         static_cast<double>(k.ho) * k.wo * k.width * k.cout +
+                         (k.down ? static_cast<double>(k.ho) * k.wo * k.cin * k.cout : 0.0));
+        } else if (d.kind == RALPB_MODULE) {
+          for (const ModNode& q : m->modules[f.mod].nodes)
+            if (q.d.op == RALPB_NODE_CONV) fl[i] += 2.0 * q.K() * q.d.cout * q.ho * q.wo;
+        }
+        total += fl[i];
+      }
+      double before = 0.0;
+      for (int i = 0; i < m->split; ++i) {
+        const FrontLayer& f = m->front[i];
+        const bool has_params = f.kind == RALPB_CONV || f.kind == RALPB_BLOCK || f.kind == RALPB_MODULE;
+        if (i > 0 && has_params && before >= 0.3 * total && 2 * (m->n_front - f.w_off) >= m->n_front) {
+          m->bucket_k = i;
+          m->bucket_lo = f.w_off;
+          break;
+        }
+        before += fl[i];
+      }
+    }
+  }
   {  // the exchanged cut: layer split-1's output (padded when a conv of the back segment reads it)
     const ActBuf& x = m->acts[m->split];
     m->xch_elems = (x.h + 2 * x.pad) * (x.w + 2 * x.pad) * x.c;
@@ -608,6 +651,9 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, const ralpb_node_
   if (cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
   if (cudaStreamCreateWithFlags(&m->aux_stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
   if (cudaStreamCreateWithFlags(&m->comm_stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
+  if (cudaStreamCreateWithFlags(&m->sync_stream, cudaStreamNonBlocking) != cudaSuccess) return fail("stream");
+  cudaEventCreateWithFlags(&m->ev_b1, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&m->ev_b1_done, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&m->ev_comm_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&m->ev_comm_join, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming);
@@ -637,6 +683,9 @@ void model_destroy(Model* m) {
   if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
   if (m->aux_stream) cudaStreamDestroy(m->aux_stream);
   if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
+  if (m->sync_stream) cudaStreamDestroy(m->sync_stream);
+  if (m->ev_b1) cudaEventDestroy(m->ev_b1);
+  if (m->ev_b1_done) cudaEventDestroy(m->ev_b1_done);
   if (m->ev_comm_fork) cudaEventDestroy(m->ev_comm_fork);
   if (m->ev_comm_join) cudaEventDestroy(m->ev_comm_join);
   if (m->ev_fork) cudaEventDestroy(m->ev_fork);
@@ -1240,10 +1289,16 @@ int mps_back_segment(Model* m, const int32_t* lab, const bf16* cut_local, float 
 // gradient goes to dst_lo (gacts[lo] if null); dgrad_lo: produce that gradient (the worker's
 // layer 0 needs none; the PS's back segment returns it to the workers).  gacts[i] receives the
 // gradient w.r.t. the input of layer i.
+int sync_bucket_fork(Model* m, float lr, float mu, std::string* why);
+
 int launch_conv_backward(Model* m, int lo, int hi, const bf16* cur, const ActBuf* in_lo, bf16* dst_lo, bool dgrad_lo,
                          std::string* why) {
   bool db_done = false;  // the bias gradient of the layer `cur` belongs to is already summed
   for (int i = hi - 1; i >= lo; --i) {
+    // the worker front's backward: layers [bucket_k, split) are done -> their sync forks off
+    if (lo == 0 && hi == m->split && i == m->bucket_k - 1 && m->bucket_k > 0 && m->is_worker &&
+        sync_bucket_fork(m, m->step_lr, m->step_mu, why))
+      return 1;
     FrontLayer& f = m->front[i];
     const ActBuf& in = i == lo && in_lo != nullptr ? *in_lo : m->acts[i];
     const ActBuf& out = m->acts[i + 1];
@@ -1464,6 +1519,23 @@ int relayout_weights(Model* m, bool fc_too, std::string* why, bool dgrad_now = f
 // worker's gradient push ("grad"/"push", simulator.py:647,689: every real parameter of [0, n)) and
 // the pull of the shard it owns to every worker ("pull", simulator.py:663,713); the ring strategy
 // counts its reduce-scatter + all-gather share 2*(W-1)*shard (ring_shares, simulator.py:726).
+int sync_range(Model* m, long long lo, long long hi, int fg, int fd, uint32_t* counter, cudaStream_t s, float lr,
+               float mu, std::string* why);
+
+// The sync bucket (layers [bucket_k, split) -- the late, parameter-heavy layers whose backward is
+// done first): forked onto sync_stream right after layer bucket_k's backward-filter, its sharded
+// update over [bucket_lo, n_front) runs while this rank's backward of the early layers continues;
+// the update kernels are small (no shared memory) and co-reside with the persistent conv kernels.
+int sync_bucket_fork(Model* m, float lr, float mu, std::string* why) {
+  RALPB_TRY(cudaEventRecord(m->ev_b1, m->stream));
+  RALPB_TRY(cudaStreamWaitEvent(m->sync_stream, m->ev_b1, 0));
+  if (sync_range(m, m->bucket_lo, m->n_front, kFlagGradB, kFlagDoneB, m->counters + 4, m->sync_stream, lr, mu, why))
+    return 1;
+  RALPB_TRY(cudaEventRecord(m->ev_b1_done, m->sync_stream));
+  m->bucket_forked = true;
+  return 0;
+}
+
 int sync_params(Model* m, long long n, float lr, float mu, std::string* why) {
   const int W = m->workers;
   const long long eb = m->elem_bytes;
@@ -1479,23 +1551,46 @@ int sync_params(Model* m, long long n, float lr, float mu, std::string* why) {
     ++m->launches;
     return 0;
   }
+  // a sync bucket (the late layers, updated under the remaining backward by sync_bucket_fork):
+  // here only [0, bucket_lo), then wait for the bucket's shards of every worker
+  const bool bucket = m->bucket_forked;
+  if (bucket) n = m->bucket_lo;
+  if (sync_range(m, 0, n, kFlagGrad, kFlagDone, m->counters + 0, m->stream, lr, mu, why)) return 1;
+  if (bucket) {
+    RALPB_TRY(cudaStreamWaitEvent(m->stream, m->ev_b1_done, 0));
+    RALPB_TRY(wait_flags(m->flags + kFlagDoneB, W, m->seq_dev, m->stream));
+    ++m->launches;
+    m->bucket_forked = false;
+  }
+  return 0;
+}
+
+// One sharded-PS update of params[lo, hi) on stream s: signal this rank's gradient ready (flag
+// base fg) on every worker, wait for all, update this rank's shard (whole-layer ranges with
+// layer_shards), store it into every worker, signal done (flag base fd).
+int sync_range(Model* m, long long lo, long long hi, int fg, int fd, uint32_t* counter, cudaStream_t s, float lr,
+               float mu, std::string* why) {
+  const int W = m->workers;
+  const long long n = hi - lo;
   const uint32_t* seq = m->seq_dev;
   PeerSignal all_grad{}, all_done{};
   all_grad.n = all_done.n = W;
   for (int w = 0; w < W; ++w) {
     uint32_t* fl = at<uint32_t>(m, m->worker_ranks[w], m->arena_off_flags);
-    all_grad.flag[w] = fl + kFlagGrad + m->widx;
-    all_done.flag[w] = fl + kFlagDone + m->widx;
+    all_grad.flag[w] = fl + fg + m->widx;
+    all_done.flag[w] = fl + fd + m->widx;
   }
-  RALPB_TRY(signal_only(all_grad, seq, m->stream));
-  RALPB_TRY(wait_flags(m->flags + kFlagGrad, W, seq, m->stream));
+  RALPB_TRY(signal_only(all_grad, seq, s));
+  RALPB_TRY(wait_flags(m->flags + fg, W, seq, s));
   ShardUpdate u{};
   u.nranks = W;
   u.self = m->widx;
-  const long long shard = n / W;  // n is a multiple of 4 * lcm(1..8)
-  u.begin = shard * m->widx;
-  u.end = u.begin + shard;
-  long long mine = shard;
+  // equal shards, multiples of 4 floats (the last one takes the remainder)
+  const long long shard = ((n + 4LL * W - 1) / (4LL * W)) * 4;
+  u.begin = std::min(hi, lo + shard * m->widx);
+  u.end = std::min(hi, u.begin + shard);
+  if (m->widx == W - 1) u.end = hi;
+  long long mine = u.end - u.begin;
   if (m->layer_shards) {   // whole-layer shards (the reference's PS layout)
     const auto& rg = m->shard_ranges[m->widx];
     u.nr = static_cast<int>(rg.size());
@@ -1513,9 +1608,9 @@ int sync_params(Model* m, long long n, float lr, float mu, std::string* why) {
     u.grads[w] = at<float>(m, m->worker_ranks[w], m->arena_off_G);
     u.params[w] = at<float>(m, m->worker_ranks[w], m->arena_off_P);
   }
-  RALPB_TRY(shard_update(u, all_done, seq, m->counters + 0, m->stream));
-  RALPB_TRY(wait_flags(m->flags + kFlagDone, W, seq, m->stream));
-  m->launches += 4;
+  RALPB_TRY(shard_update(u, all_done, seq, counter, s));
+  if (fd == kFlagDone) RALPB_TRY(wait_flags(m->flags + fd, W, seq, s));   // (the bucket's wait: in sync_params)
+  m->launches += fd == kFlagDone ? 4 : 3;
   const long long peer = static_cast<long long>(W - 1) * mine * static_cast<long long>(sizeof(float));
   m->nvl_in += peer;   // gradient shards of the other workers
   m->nvl_out += peer;  // the updated shard to the other workers
@@ -1887,6 +1982,9 @@ int step_body(Model* m, const float* img, const int32_t* lab, float lr, float mu
   const bool ralp = m->strategy == RALPB_STRATEGY_RALP;
   cudaStream_t s = m->stream;
   bool fc_forked = false;
+  m->step_lr = lr;
+  m->step_mu = mu;
+  m->bucket_forked = false;
   RALPB_TRY(bump_counter(m->seq_dev, s));
   ++m->launches;
   const long long cut_logical = static_cast<long long>(b) * m->xch_logical * eb;  // one worker's cut

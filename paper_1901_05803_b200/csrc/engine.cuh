@@ -109,6 +109,12 @@ struct Model {
   int widx = 0;                    // this rank's worker index (rank order, the dedicated PS skipped)
   std::vector<int> worker_ranks;   // worker index -> rank
   bool layer_shards = false;          // BASELINE_LAYER_SHARDS: whole layers round-robin over the shards
+  int bucket_k = -1;                  // sync bucket: layers [bucket_k, split) are synchronised on
+  long long bucket_lo = 0;            // sync_stream under the remaining backward; their parameters
+  bool bucket_forked = false;         // are [bucket_lo, n_front); forked in the current step body
+  cudaStream_t sync_stream = nullptr;
+  cudaEvent_t ev_b1 = nullptr, ev_b1_done = nullptr;
+  float step_lr = 0.f, step_mu = 0.f; // hyper-parameters of the step being issued
   std::vector<std::vector<std::pair<long long, long long>>> shard_ranges;   // per shard: [lo, hi) floats
   std::vector<long long> shard_real;  // real (descriptor) parameters in each sync shard, for the
                                       // logical byte count of the pull / ring sites
