@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
   const int stages = p.stages;
   uint8_t* sA = smem;
   uint8_t* sB = smem + stages * kAStage;
-  uint8_t* sC = sB + stages * p.b_stage_bytes;   // tma_epi: 2 x 16 KB output staging
+  uint8_t* sC = sB + stages * p.b_stage_bytes;   // tma_epi: 16 KB output staging per epilogue warpgroup
   uint64_t* full = reinterpret_cast<uint64_t*>(sC + (p.tma_epi ? 2 * 16384 : 0));
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 32 * kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -161,8 +161,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 4) {
+    // Two epilogue warpgroups drain each accumulator: group g takes the 32-column chunks
+    // c = 32 * (2j + g), with its own staging (bf16: two 8 KB boxes; fp32: one 16 KB box), named
+    // barrier and TMA-issuing thread -- the narrow-K GEMMs (1x1 convolutions, K = 64..512) are
+    // epilogue-bound, one warpgroup storing 128 x 256 bf16 per tile took ~3.8 us.
+    const int g = (warp - 4) >> 2;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
+    const int lead = 128 + 128 * g;
+    const bool two_bufs = p.epi == EPI_BF16;
+    uint8_t* sCg = sC + g * 16384;
     int acc = 0, ks_out = 0;
     uint32_t acc_phase = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
@@ -175,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
       const bool row_ok = m < p.M;
       const bool zero_row = row_ok && p.border && is_border_row(p, m);
       const uint32_t t_base = tmem_base + acc * bn + (static_cast<uint32_t>(q * 32) << 16);
-      for (int c = 0; c < bn; c += 32) {
+      for (int c = 32 * g; c < bn; c += 64) {
         uint32_t r[32];
         tmem_ld32(t_base + c, r);
         tmem_wait_ld();
@@ -218,9 +226,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
           // stage this row's 32 values (fp32: 128-byte SW128 row; bf16: 64-byte SW64 row) and
           // write the 128 x 32 block with one TMA store / reduce-add (rows >= M and columns >= N
           // are clipped by the tensor map)
-          uint8_t* buf = sC + ((ks_out & 1) << 14);
-          if (threadIdx.x == 128) bulk_wait_read<1>();
-          named_bar_sync(1, 128);
+          uint8_t* buf = sCg + (two_bufs ? ((ks_out & 1) << 13) : 0);
+          if (threadIdx.x == lead) {
+            if (two_bufs) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+          }
+          named_bar_sync(1 + g, 128);
           if (p.epi == EPI_BF16) {
             uint8_t* rp = buf + row * 64;
 #pragma unroll
@@ -236,8 +247,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
                   make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
           fence_proxy_async_smem();
-          named_bar_sync(1, 128);
-          if (threadIdx.x == 128) {
+          named_bar_sync(1 + g, 128);
+          if (threadIdx.x == lead) {
             if (p.tma_epi == 2) tma_reduce_add_2d(&p.tmC, buf, n0, mt * kBM);
             else tma_store_2d(&p.tmC, buf, n0, mt * kBM);
             bulk_commit();
@@ -309,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
       mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-    if (p.tma_epi && threadIdx.x == 128) bulk_wait_all();
+    if (p.tma_epi && threadIdx.x == lead) bulk_wait_all();
   }
 
   tc_fence_before();

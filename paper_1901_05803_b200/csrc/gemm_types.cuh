@@ -5,8 +5,8 @@
 //
 //   D[m, n] = sum_k A[m, k] * B[n, k]       (bf16 operands, fp32 in TMEM)
 //
-// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer,
-// warp 2 = TMEM allocator, warps 4..7 = epilogue (one TMEM lane = one row each).
+// Roles (384 threads): warp 0 (and 3) = TMA producers, warp 1 = MMA issuer,
+// warp 2 = TMEM allocator, warps 4..11 = two epilogue warpgroups (one TMEM lane = one row).
 // Accumulators are double-buffered in TMEM so the epilogue of tile i overlaps
 // the main loop of tile i+1.
 //
@@ -31,7 +31,8 @@ enum EpiMode : int { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_ATOMIC = 2, EPI_SGD = 3 
 constexpr int kBM = 128;
 constexpr int kMaxTaps = 32;
 constexpr int kAStage = 128 * 128;  // 16 KB: 128 rows x 128 B (or 2 MN atoms x 64 rows)
-constexpr int kThreads = 256;
+constexpr int kEpiWarps = 8;                     // two epilogue warpgroups (warps 4..11)
+constexpr int kThreads = 128 + 32 * kEpiWarps;   // + producer, MMA, TMEM-allocator warps
 
 struct alignas(64) GemmParams {
   CUtensorMap tmA;
