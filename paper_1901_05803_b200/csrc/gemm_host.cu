@@ -77,19 +77,6 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
   int bn = d.block_n;
   if (bn == 0) {
     bn = d.N >= 256 ? 256 : (d.N > 64 ? 128 : (d.N > 32 ? 64 : 32));
-    // wave quantisation of the persistent grid: where the widest tile leaves few waves (<= 4), a
-    // narrower one that cuts waves x tile width by >= 15 % wins (e.g. M = 25088, N = 256: 196
-    // tiles = 1.3 waves at 256 wide, 392 = 2.6 waves at 128); not for split-K (atomic) GEMMs,
-    // whose split count is chosen below for the same purpose
-    if (d.epi != EPI_F32_ATOMIC && d.k_splits <= 1) {
-      const long long mt = (d.M + kBM - 1) / kBM, sms = num_sms();
-      auto waves = [&](int b) { return (mt * ((d.N + b - 1) / b) + sms - 1) / sms; };
-      if (waves(bn) <= 4) {
-        long long best = waves(bn) * bn;
-        for (int b = bn / 2; b >= 64; b /= 2)
-          if (waves(b) * b * 100 < best * 85) { best = waves(b) * b; bn = b; }
-      }
-    }
   }
   if (!(bn == 32 || bn == 64 || bn == 128 || bn == 256)) { *why = "bad block_n"; return cudaErrorInvalidValue; }
   if (!is_k(d.b_mode) && bn < 32) { *why = "MN-major B needs BN>=32"; return cudaErrorInvalidValue; }
