@@ -431,7 +431,7 @@ def run_ours(args):
                "logical_bytes_per_step": _job_bytes(stm, world),
                "note": "FC-0 column-parallel / FC-1 row-parallel over all GPUs (volume_ralp_multi_ps)"}
 
-    # the parity precision (fp32-accurate (hi, lo) pairs through the same tcgen05 GEMM engine): a
+    # the parity precision (fp32 values as three bf16 pieces through the same tcgen05 GEMM engine): a
     # same-precision number beside the fp32 CPU arm
     fp32 = None
     if not args.no_fp32 and cmp:
@@ -440,10 +440,10 @@ def run_ours(args):
         ms_f = _time_steps(exf, dimgs, dlabs, max(3, args.steps // 4), 3, world)
         stf = exf.stats()
         exf.close()
-        fp32 = {"value": world * BATCH / (ms_f * 1e-3), "ms_per_step": ms_f, "dtype": "f32 (bf16 hi/lo pairs)",
+        fp32 = {"value": world * BATCH / (ms_f * 1e-3), "ms_per_step": ms_f, "dtype": "f32 (three bf16 pieces)",
                 "logical_bytes_per_step": _job_bytes(stf, world),
-                "note": "RALPB_PRECISION_FP32: every activation / gradient an fp32-accurate bf16 pair, every "
-                        "contraction on the tcgen05 GEMM engine over the pairs (4 products, fp32 accumulation); "
+                "note": "RALPB_PRECISION_FP32: every activation / gradient three bf16 pieces (exact in fp32), every "
+                        "contraction on the tcgen05 GEMM engine over the pieces (9 products, fp32 accumulation); "
                         "tests/test_parity_fp32_gpu.py pins it to the plain fp32 oracle"}
     # RALP-N (costmodel.py:244-245): N-1 workers + a dedicated PS GPU (rank 0)
     ralp_n = None

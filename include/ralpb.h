@@ -206,10 +206,10 @@ typedef struct ralpb_model ralpb_model;
 
 /* Arithmetic of the step.  BF16: bf16 operands / activations, fp32 accumulation, fp32 master
  * parameters (the throughput mode).  FP32: the parity mode north_star pins to the fp32 oracle --
- * every activation, activation gradient and GEMM operand is carried as an fp32-accurate (hi, lo)
- * bf16 pair (x = hi + lo, |x - hi - lo| <= 2^-17 |x|) and every contraction runs on the same tcgen05
- * GEMM engine over the pairs (hi*hi + hi*lo + lo*hi + lo*lo, fp32 accumulation), so results match
- * plain fp32 arithmetic to ~1e-5 relative (reference unit: elem_bytes=4, layers.py:238-250). */
+ * every activation, activation gradient and GEMM operand is carried as three bf16 pieces
+ * (hi, mid, lo; their sum is the fp32 value exactly) and every contraction runs on the same tcgen05
+ * GEMM engine over the pieces (all 9 piece products, fp32 accumulation), so results match plain
+ * fp32 arithmetic to ~1e-5 relative (reference unit: elem_bytes=4, layers.py:238-250). */
 enum { RALPB_PRECISION_BF16 = 0, RALPB_PRECISION_FP32 = 1 };
 
 /* Replaces JobSpec + _JobRun.__init__ (costmodel.py:64-86, simulator.py:517-567).
@@ -260,8 +260,8 @@ int ralpb_model_read_loss(ralpb_model* m, int lag, float* out);
 void* ralpb_model_stream(ralpb_model* m);
 /* Inspection: copies one of the last step's device buffers to host_out (may be NULL to query) and
  * returns its element count, or -1.  Layouts (BF16 precision; FP32 precision: every bf16 buffer is
- * stored as (hi, lo) pairs -- per pixel / row the hi channels then the lo channels -- and the
- * byte size doubles):
+ * stored as three pieces -- per pixel / row the hi channels, then the mid, then the lo channels --
+ * and the byte size triples; the element count returned is the value count):
  *   ACT i / ACT_GRAD i   bf16 padded NHWC input of front layer i / its gradient
  *   LOGITS               fp32 [rows][ld]            DLOGITS          bf16 [rows][ld]
  *   FC_OUT i             bf16 [rows][ld] output of hidden FC layer i (ReLU applied)

@@ -193,8 +193,8 @@ class RankExecutor:
         fc_sharding (StrategyKind.RALP only): "single" = the reference's single PS on rank 0;
         "multi" = the FC tail's first two layers sharded over every GPU (RALPB_STRATEGY_RALP_MPS,
         SURVEY.md 8f.1; logical bytes volume_ralp_multi_ps).
-        precision: "bf16" (throughput) or "fp32" (the parity mode: fp32-accurate (hi, lo) bf16
-        pairs through the same tcgen05 GEMM engine, include/ralpb.h RALPB_PRECISION_FP32).
+        precision: "bf16" (throughput) or "fp32" (the parity mode: fp32 values as three bf16
+        pieces through the same tcgen05 GEMM engine, include/ralpb.h RALPB_PRECISION_FP32).
         placement (StrategyKind.RALP only): "colocated" = W ranks, the PS role on ps_rank which is
         also a worker; "dedicated-ps" = the paper's RALP-N (costmodel.py:244-245): world = W + 1,
         ps_rank runs only the FC tail, every other rank is a worker.

@@ -2,8 +2,8 @@
 
 north_star: "loss and parameters after N steps from identical seeds and synthetic inputs must
 match within a stated fp32 relative tolerance (e.g. 1e-4)".  In this mode every activation and
-gradient is an fp32-accurate (hi, lo) bf16 pair and every contraction runs on the tcgen05 GEMM
-engine over the pairs (hi*hi + hi*lo + lo*hi + lo*lo, fp32 accumulation; pair.cuh), so the whole
+gradient is three bf16 pieces (hi, mid, lo: exact in fp32) and every contraction runs on the tcgen05
+GEMM engine over the pieces (all 9 piece products, fp32 accumulation; pair.cuh), so the whole
 step is fp32-accurate.  The oracle runs in plain fp32 torch on the CPU (oracle/step.py,
 emulate_bf16=False -- no GPU rounding emulated).  Three bf16 pieces hold every fp32 value exactly
 (pair.cuh), so what remains is fp32 summation order (tensor-core accumulation vs the CPU's).
