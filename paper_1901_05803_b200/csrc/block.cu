@@ -122,6 +122,10 @@ int block_alloc(Model* m, BlockBufs& k, std::string* why) {
   BA(k.da_pre, rin * k.width, false);
 #undef BA
   if (!(k.stats = balloc<float>(m, 8 * static_cast<size_t>(k.cmax), why, true))) return 1;
+  if (!(k.ma = balloc<uint8_t>(m, static_cast<size_t>(rin) * k.width / 8, why)) ||
+      !(k.mb = balloc<uint8_t>(m, static_cast<size_t>(rout) * k.width / 8, why)) ||
+      !(k.mc = balloc<uint8_t>(m, static_cast<size_t>(rout) * k.cout / 8, why)))
+    return 1;
   return 0;
 }
 
@@ -147,6 +151,7 @@ int block_forward(Model* m, BlockBufs& k, const bf16* x, bf16* y, std::string* w
     BnApply ap{};
     ap.x = Act4{k.a_pre, 0}; ap.mean = mean_of(k, 0); ap.rstd = rstd_of(k, 0);
     ap.gamma = P + k.ga_off; ap.beta = P + k.ga_off + k.width; ap.relu = 1; ap.y = MutAct4{k.a, 1};
+    ap.mask_out = k.ma;
     ap.n = k.n; ap.h = k.h; ap.w = k.w; ap.c = k.width;
     RALPB_TRY(bn_apply(ap, s));
   }
@@ -163,6 +168,7 @@ int block_forward(Model* m, BlockBufs& k, const bf16* x, bf16* y, std::string* w
     BnApply ap{};
     ap.x = bpre; ap.mean = mean_of(k, 1); ap.rstd = rstd_of(k, 1);
     ap.gamma = P + k.gb_off; ap.beta = P + k.gb_off + k.width; ap.relu = 1; ap.y = MutAct4{k.b, 0};
+    ap.mask_out = k.mb;
     ap.n = k.n; ap.h = k.ho; ap.w = k.wo; ap.c = k.width;
     RALPB_TRY(bn_apply(ap, s));
   }
@@ -189,6 +195,7 @@ int block_forward(Model* m, BlockBufs& k, const bf16* x, bf16* y, std::string* w
       ap.res_kind = 1; ap.r = Act4{x, 0};
     }
     ap.relu = 1; ap.y = MutAct4{y, 0};
+    ap.mask_out = k.mc;
     ap.n = k.n; ap.h = k.ho; ap.w = k.wo; ap.c = k.cout;
     RALPB_TRY(bn_apply(ap, s));
   }
@@ -206,6 +213,7 @@ int block_backward(Model* m, BlockBufs& k, const bf16* x, const bf16* y, const b
   {
     BnBackward bb{};
     bb.dy = Act4{dy, 0}; bb.y = Act4{y, 0}; bb.relu_mask = 1; bb.x = Act4{k.c_pre, 0};
+    bb.mask_in = k.mc;
     bb.mean = mean_of(k, 2); bb.rstd = rstd_of(k, 2); bb.gamma = P + k.gc_off;
     bb.dgamma = G + k.gc_off; bb.dbeta = G + k.gc_off + k.cout;
     bb.dx = MutAct4{k.dc_pre, 0}; bb.dz_out = MutAct4{k.dz, 0};
@@ -220,6 +228,7 @@ int block_backward(Model* m, BlockBufs& k, const bf16* x, const bf16* y, const b
   {
     BnBackward bb{};
     bb.dy = Act4{k.db, 0}; bb.y = Act4{k.b, 0}; bb.relu_mask = 1; bb.x = Act4{k.b_pre, s1 ? 1 : 0};
+    bb.mask_in = k.mb;
     bb.mean = mean_of(k, 1); bb.rstd = rstd_of(k, 1); bb.gamma = P + k.gb_off;
     bb.dgamma = G + k.gb_off; bb.dbeta = G + k.gb_off + k.width;
     bb.dx = dbpre;
@@ -239,6 +248,7 @@ int block_backward(Model* m, BlockBufs& k, const bf16* x, const bf16* y, const b
   {
     BnBackward bb{};
     bb.dy = Act4{k.da, 1}; bb.y = Act4{k.a, 1}; bb.relu_mask = 1; bb.x = Act4{k.a_pre, 0};
+    bb.mask_in = k.ma;
     bb.mean = mean_of(k, 0); bb.rstd = rstd_of(k, 0); bb.gamma = P + k.ga_off;
     bb.dgamma = G + k.ga_off; bb.dbeta = G + k.ga_off + k.width;
     bb.dx = MutAct4{k.da_pre, 0};
@@ -283,6 +293,7 @@ int bn_stem_forward(Model* m, FrontLayer& f, const ActBuf& in, const ActBuf& out
   BnApply ap{};
   ap.x = Act4{f.pre, 0}; ap.mean = f.bn_stats; ap.rstd = f.bn_stats + c;
   ap.gamma = m->P + f.b_off; ap.beta = m->P + f.b_off + c; ap.relu = 1; ap.y = MutAct4{out.ptr, out.pad};
+  ap.mask_out = f.bn_mask;
   ap.n = out.n; ap.h = out.h; ap.w = out.w; ap.c = c;
   RALPB_TRY(bn_apply(ap, s));
   m->launches += 3;
@@ -294,6 +305,7 @@ int bn_stem_backward(Model* m, FrontLayer& f, const ActBuf& in, const ActBuf& ou
   const int c = f.g.cout;
   BnBackward bb{};
   bb.dy = Act4{dy, out.pad}; bb.y = Act4{out.ptr, out.pad}; bb.relu_mask = 1; bb.x = Act4{f.pre, 0};
+  bb.mask_in = f.bn_mask;
   bb.mean = f.bn_stats; bb.rstd = f.bn_stats + c; bb.gamma = m->P + f.b_off;
   bb.dgamma = m->G + f.b_off; bb.dbeta = m->G + f.b_off + c;
   bb.dx = MutAct4{f.dpre, 0};

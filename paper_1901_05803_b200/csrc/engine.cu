@@ -574,7 +574,8 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, const ralpb_node_
     } else if (f.bn) {
       const size_t rows = static_cast<size_t>(m->acts[i + 1].rows());
       if (!(f.pre = alloc<bf16>(m, rows * f.g.cout, why)) || !(f.dpre = alloc<bf16>(m, rows * f.g.cout, why)) ||
-          !(f.bn_stats = alloc<float>(m, 2 * static_cast<size_t>(f.g.cout), why)))
+          !(f.bn_stats = alloc<float>(m, 2 * static_cast<size_t>(f.g.cout), why)) ||
+          !(f.bn_mask = alloc<uint8_t>(m, rows * f.g.cout / 8, why)))
         return fail(*why);
     }
   }

@@ -33,6 +33,7 @@ struct BlockBufs {
   __nv_bfloat16 *dc_pre = nullptr, *dz = nullptr, *db = nullptr, *db_pre = nullptr, *dil = nullptr, *da = nullptr,
                 *da_pre = nullptr, *dd_pre = nullptr, *dxs = nullptr;
   float* stats = nullptr;   // [4][2][cmax]: mean / rstd of bn a, b, c, d
+  uint8_t *ma = nullptr, *mb = nullptr, *mc = nullptr;   // ReLU masks (bits) of a, b and the output
   int cmax = 0;
 };
 
@@ -51,6 +52,7 @@ struct ModNode {
   __nv_bfloat16* dy = nullptr;        // non-output node: gradient w.r.t. its output
   uint8_t* idx = nullptr;             // max pool: window position of the first max (255: not > 0)
   float* stats = nullptr;             // bn conv: [2][cout] mean / rstd
+  uint8_t* mask = nullptr;            // bn conv: ReLU mask bits of its output [rows][cout/8]
   long long K() const { return static_cast<long long>(d.kh) * d.kw * cin; }
 };
 struct ModuleBufs {
@@ -83,6 +85,7 @@ struct FrontLayer {
   __nv_bfloat16* pre = nullptr;     // bn conv: its output before the batch norm
   __nv_bfloat16* dpre = nullptr;    // ... and the gradient w.r.t. it
   float* bn_stats = nullptr;        // bn conv: [2][cout] mean / rstd
+  uint8_t* bn_mask = nullptr;       // bn conv: ReLU mask bits of its output [rows][cout/8]
   int blk = -1;                // RALPB_BLOCK: index into Model::blocks
   int mod = -1;                // RALPB_MODULE: index into Model::modules
 };

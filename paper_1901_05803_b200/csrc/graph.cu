@@ -484,6 +484,7 @@ int module_alloc(Model* m, ModuleBufs& k, std::string* why) {
       if (q.d.bn) {
         if (!(q.z = galloc<bf16>(m, static_cast<size_t>(rout) * q.d.cout, why))) return 1;
         if (!(q.stats = galloc<float>(m, 2 * static_cast<size_t>(q.d.cout), why))) return 1;
+        if (!(q.mask = galloc<uint8_t>(m, static_cast<size_t>(rout) * q.d.cout / 8, why))) return 1;
       }
       if (!q.direct) col = std::max(col, rout * q.K());
       dz = std::max(dz, rout * q.d.cout);
@@ -547,6 +548,7 @@ int module_forward(Model* m, ModuleBufs& k, const bf16* x, bf16* y, std::string*
         ap.x = Act4{q.z, 0}; ap.mean = q.stats; ap.rstd = q.stats + d.cout;
         ap.gamma = m->P + q.b_off; ap.beta = m->P + q.b_off + d.cout; ap.relu = 1;
         ap.y = MutAct4{dst, 0, ldd};
+        ap.mask_out = q.mask;
         ap.n = k.n; ap.h = q.ho; ap.w = q.wo; ap.c = d.cout;
         RALPB_TRY(bn_apply(ap, s));
         m->launches += 3;
@@ -593,6 +595,7 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
       if (d.bn) {
         BnBackward bb{};
         bb.dy = Act4{g_out, 0, ldo}; bb.y = Act4{v_out, 0, ldo}; bb.relu_mask = 1; bb.x = Act4{q.z, 0};
+        bb.mask_in = q.mask;
         bb.mean = q.stats; bb.rstd = q.stats + d.cout; bb.gamma = P + q.b_off;
         bb.dgamma = G + q.b_off; bb.dbeta = G + q.b_off + d.cout;
         bb.dx = MutAct4{k.dz, 0};

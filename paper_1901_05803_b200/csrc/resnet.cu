@@ -155,12 +155,19 @@ __global__ void __launch_bounds__(256, 3) bn_apply_kernel(BnApply a, int pixels)
         if (a.relu) o[j] = fmaxf(o[j], 0.f);
       }
       store8(a.y.p + toff(p, hw, a.h, a.w, a.y.pad, ld_of(a.y, a.c)) + L.g * 8, o);
+      if (a.mask_out != nullptr) {   // bits of the STORED (bf16) values
+        uint32_t bits = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bits |= (__bfloat162float(__float2bfloat16_rn(o[j])) > 0.f ? 1u : 0u) << j;
+        a.mask_out[static_cast<long long>(p) * (a.c >> 3) + L.g] = static_cast<uint8_t>(bits);
+      }
     }
   }
 }
 
 // ------------------------------------------------------------------ backward
 // sums: [0, c) sum dz;  [c, 2c) sum dz * (x - mean)   (times rstd in bn_bwd_params / apply)
+template <bool BITS>   // BITS: the ReLU mask from mask_in bits (else from y)
 __global__ void __launch_bounds__(256, 3) bn_bwd_reduce_kernel(BnBackward b, int pixels, float* __restrict__ sums) {
   extern __shared__ float sh[];  // [2][c]
   const int c = b.c;
@@ -172,23 +179,30 @@ __global__ void __launch_bounds__(256, 3) bn_bwd_reduce_kernel(BnBackward b, int
 #pragma unroll
     for (int j = 0; j < 8; ++j) mu[j] = b.mean[L.g * 8 + j];
     const int hw = b.h * b.w, st = L.stride();
-    constexpr int U = 2;
+    constexpr int U = BITS ? 4 : 2;
     for (int p0 = L.first(); p0 < pixels; p0 += U * st) {
       const uint4 z = make_uint4(0, 0, 0, 0), one = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);
-      uint4 dy[U], xv[U], y[U];
+      uint4 dy[U], xv[U], y[BITS ? 1 : U];
+      uint32_t mb[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int p = p0 + u * st;
         const bool in = p < pixels;
         dy[u] = in ? ld16(b.dy.p + toff(p, hw, b.h, b.w, b.dy.pad, ld_of(b.dy, c)) + L.g * 8) : z;
         xv[u] = in ? ld16(b.x.p + toff(p, hw, b.h, b.w, b.x.pad, ld_of(b.x, c)) + L.g * 8) : z;
-        y[u] = in && b.relu_mask ? ld16(b.y.p + toff(p, hw, b.h, b.w, b.y.pad, ld_of(b.y, c)) + L.g * 8) : one;
+        if constexpr (BITS) {
+          mb[u] = in && b.relu_mask ? b.mask_in[static_cast<long long>(p) * (c >> 3) + L.g] : 0xFFu;
+        } else {
+          y[u] = in && b.relu_mask ? ld16(b.y.p + toff(p, hw, b.h, b.w, b.y.pad, ld_of(b.y, c)) + L.g * 8) : one;
+          mb[u] = 0xFFu;
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const float d = elem(y[u], j) > 0.f ? elem(dy[u], j) : 0.f;   // dy is 0 past the end
+          const bool live = BITS ? ((mb[u] >> j) & 1u) != 0 : elem(y[BITS ? 0 : u], j) > 0.f;
+          const float d = live ? elem(dy[u], j) : 0.f;   // dy is 0 past the end
           sd[j] += d;
           sx[j] += d * (elem(xv[u], j) - mu[j]);
         }
@@ -234,7 +248,11 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(BnBackward b, int pix
     float dy[8], xv[8], y[8], dx[8];
     load8(b.dy.p + toff(p, hw, b.h, b.w, b.dy.pad, ld_of(b.dy, c)) + L.g * 8, dy);
     load8(b.x.p + toff(p, hw, b.h, b.w, b.x.pad, ld_of(b.x, c)) + L.g * 8, xv);
-    if (b.relu_mask) {
+    if (b.relu_mask && b.mask_in != nullptr) {
+      const uint32_t bits = b.mask_in[static_cast<long long>(p) * (c >> 3) + L.g];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) if (!((bits >> j) & 1u)) dy[j] = 0.f;
+    } else if (b.relu_mask) {
       load8(b.y.p + toff(p, hw, b.h, b.w, b.y.pad, ld_of(b.y, c)) + L.g * 8, y);
 #pragma unroll
       for (int j = 0; j < 8; ++j) if (!(y[j] > 0.f)) dy[j] = 0.f;
@@ -488,7 +506,12 @@ cudaError_t bn_backward(const BnBackward& b, float* work, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(work, 0, sizeof(float) * 2 * b.c, s);
   if (e != cudaSuccess) return e;
   const int lanes = 256 / (b.c / 8);
-  bn_bwd_reduce_kernel<<<stats_grid(bn_bwd_reduce_kernel, sizeof(float) * 2 * b.c, pixels, lanes), 256, sizeof(float) * 2 * b.c, s>>>(b, static_cast<int>(pixels), work);
+  if (b.mask_in != nullptr)
+    bn_bwd_reduce_kernel<true><<<stats_grid(bn_bwd_reduce_kernel<true>, sizeof(float) * 2 * b.c, pixels, lanes), 256,
+                                 sizeof(float) * 2 * b.c, s>>>(b, static_cast<int>(pixels), work);
+  else
+    bn_bwd_reduce_kernel<false><<<stats_grid(bn_bwd_reduce_kernel<false>, sizeof(float) * 2 * b.c, pixels, lanes), 256,
+                                  sizeof(float) * 2 * b.c, s>>>(b, static_cast<int>(pixels), work);
   bn_bwd_params_kernel<<<(b.c + 255) / 256, 256, 0, s>>>(work, b.rstd, b.c, b.dgamma, b.dbeta);
   bn_bwd_apply_kernel<<<pixel_grid(pixels, lanes), 256, 0, s>>>(b, static_cast<int>(pixels), work,
                                                                 1.f / static_cast<float>(pixels));

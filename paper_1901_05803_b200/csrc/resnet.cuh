@@ -41,6 +41,8 @@ struct BnApply {
   int relu;
   MutAct4 y;
   int n, h, w, c;
+  uint8_t* mask_out = nullptr;   // optional (relu): [n*h*w][c/8] bytes, bit j of byte (p, g) = the
+                                 // stored y[p][8g + j] > 0 -- the ReLU mask its backward reads
 };
 cudaError_t bn_apply(const BnApply& a, cudaStream_t s);
 
@@ -58,6 +60,8 @@ struct BnBackward {
   MutAct4 dx;
   MutAct4 dz_out;    // optional
   int n, h, w, c;
+  const uint8_t* mask_in = nullptr;   // relu_mask from BnApply::mask_out bits instead of reading y
+                                      // (1/16 of its bytes, read twice per backward)
 };
 cudaError_t bn_backward(const BnBackward& b, float* work, cudaStream_t s);
 
