@@ -121,7 +121,7 @@ int block_alloc(Model* m, BlockBufs& k, std::string* why) {
   BA(k.da, rpad * k.width, true);
   BA(k.da_pre, rin * k.width, false);
 #undef BA
-  if (!(k.stats = balloc<float>(m, 8 * static_cast<size_t>(k.cmax), why, true))) return 1;
+  if (!(k.stats = balloc<float>(m, 8 * static_cast<size_t>(k.cmax) * k.groups, why, true))) return 1;
   if (!(k.ma = balloc<uint8_t>(m, static_cast<size_t>(rin) * k.width / 8, why)) ||
       !(k.mb = balloc<uint8_t>(m, static_cast<size_t>(rout) * k.width / 8, why)) ||
       !(k.mc = balloc<uint8_t>(m, static_cast<size_t>(rout) * k.cout / 8, why)))
@@ -146,12 +146,14 @@ int block_forward(Model* m, BlockBufs& k, const bf16* x, bf16* y, std::string* w
   float* P = m->P;
   // conv a (1x1) + bn_a + ReLU -> a (padded for the 3x3)
   if (mm_fwd(m, x, rin, k.cin, k.wa, k.width, k.a_pre, why)) return 1;
-  RALPB_TRY(bn_stats(Act4{k.a_pre, 0}, k.n, k.h, k.w, k.width, kBnEps, m->bn_work, mean_of(k, 0), rstd_of(k, 0), s));
+  RALPB_TRY(bn_stats(Act4{k.a_pre, 0}, k.n, k.h, k.w, k.width, kBnEps, m->bn_work, mean_of(k, 0), rstd_of(k, 0), s,
+                     k.groups, 8LL * k.cmax));
   {
     BnApply ap{};
     ap.x = Act4{k.a_pre, 0}; ap.mean = mean_of(k, 0); ap.rstd = rstd_of(k, 0);
     ap.gamma = P + k.ga_off; ap.beta = P + k.ga_off + k.width; ap.relu = 1; ap.y = MutAct4{k.a, 1};
     ap.mask_out = k.ma;
+    ap.groups = k.groups; ap.stat_stride = 8LL * k.cmax;
     ap.n = k.n; ap.h = k.h; ap.w = k.w; ap.c = k.width;
     RALPB_TRY(bn_apply(ap, s));
   }
@@ -163,18 +165,21 @@ int block_forward(Model* m, BlockBufs& k, const bf16* x, bf16* y, std::string* w
     if (mm_fwd(m, k.col, rout, 9 * k.width, k.wbf, k.width, k.b_pre, why)) return 1;
   }
   const Act4 bpre{k.b_pre, s1 ? 1 : 0};
-  RALPB_TRY(bn_stats(bpre, k.n, k.ho, k.wo, k.width, kBnEps, m->bn_work, mean_of(k, 1), rstd_of(k, 1), s));
+  RALPB_TRY(bn_stats(bpre, k.n, k.ho, k.wo, k.width, kBnEps, m->bn_work, mean_of(k, 1), rstd_of(k, 1), s,
+                     k.groups, 8LL * k.cmax));
   {
     BnApply ap{};
     ap.x = bpre; ap.mean = mean_of(k, 1); ap.rstd = rstd_of(k, 1);
     ap.gamma = P + k.gb_off; ap.beta = P + k.gb_off + k.width; ap.relu = 1; ap.y = MutAct4{k.b, 0};
     ap.mask_out = k.mb;
+    ap.groups = k.groups; ap.stat_stride = 8LL * k.cmax;
     ap.n = k.n; ap.h = k.ho; ap.w = k.wo; ap.c = k.width;
     RALPB_TRY(bn_apply(ap, s));
   }
   // conv c (1x1), the shortcut, bn_c + add + ReLU -> y
   if (mm_fwd(m, k.b, rout, k.width, k.wc, k.cout, k.c_pre, why)) return 1;
-  RALPB_TRY(bn_stats(Act4{k.c_pre, 0}, k.n, k.ho, k.wo, k.cout, kBnEps, m->bn_work, mean_of(k, 2), rstd_of(k, 2), s));
+  RALPB_TRY(bn_stats(Act4{k.c_pre, 0}, k.n, k.ho, k.wo, k.cout, kBnEps, m->bn_work, mean_of(k, 2), rstd_of(k, 2), s,
+                     k.groups, 8LL * k.cmax));
   if (k.down) {
     const bf16* xin = x;
     if (!s1) {
@@ -182,7 +187,8 @@ int block_forward(Model* m, BlockBufs& k, const bf16* x, bf16* y, std::string* w
       xin = k.d_in;
     }
     if (mm_fwd(m, xin, rout, k.cin, k.wd, k.cout, k.d_pre, why)) return 1;
-    RALPB_TRY(bn_stats(Act4{k.d_pre, 0}, k.n, k.ho, k.wo, k.cout, kBnEps, m->bn_work, mean_of(k, 3), rstd_of(k, 3), s));
+    RALPB_TRY(bn_stats(Act4{k.d_pre, 0}, k.n, k.ho, k.wo, k.cout, kBnEps, m->bn_work, mean_of(k, 3), rstd_of(k, 3), s,
+                       k.groups, 8LL * k.cmax));
   }
   {
     BnApply ap{};
@@ -196,6 +202,7 @@ int block_forward(Model* m, BlockBufs& k, const bf16* x, bf16* y, std::string* w
     }
     ap.relu = 1; ap.y = MutAct4{y, 0};
     ap.mask_out = k.mc;
+    ap.groups = k.groups; ap.stat_stride = 8LL * k.cmax;
     ap.n = k.n; ap.h = k.ho; ap.w = k.wo; ap.c = k.cout;
     RALPB_TRY(bn_apply(ap, s));
   }
@@ -217,6 +224,7 @@ int block_backward(Model* m, BlockBufs& k, const bf16* x, const bf16* y, const b
     bb.mean = mean_of(k, 2); bb.rstd = rstd_of(k, 2); bb.gamma = P + k.gc_off;
     bb.dgamma = G + k.gc_off; bb.dbeta = G + k.gc_off + k.cout;
     bb.dx = MutAct4{k.dc_pre, 0}; bb.dz_out = MutAct4{k.dz, 0};
+    bb.groups = k.groups; bb.stat_stride = 8LL * k.cmax;
     bb.n = k.n; bb.h = k.ho; bb.w = k.wo; bb.c = k.cout;
     RALPB_TRY(bn_backward(bb, m->bn_work, s));
   }
@@ -232,6 +240,7 @@ int block_backward(Model* m, BlockBufs& k, const bf16* x, const bf16* y, const b
     bb.mean = mean_of(k, 1); bb.rstd = rstd_of(k, 1); bb.gamma = P + k.gb_off;
     bb.dgamma = G + k.gb_off; bb.dbeta = G + k.gb_off + k.width;
     bb.dx = dbpre;
+    bb.groups = k.groups; bb.stat_stride = 8LL * k.cmax;
     bb.n = k.n; bb.h = k.ho; bb.w = k.wo; bb.c = k.width;
     RALPB_TRY(bn_backward(bb, m->bn_work, s));
   }
@@ -252,6 +261,7 @@ int block_backward(Model* m, BlockBufs& k, const bf16* x, const bf16* y, const b
     bb.mean = mean_of(k, 0); bb.rstd = rstd_of(k, 0); bb.gamma = P + k.ga_off;
     bb.dgamma = G + k.ga_off; bb.dbeta = G + k.ga_off + k.width;
     bb.dx = MutAct4{k.da_pre, 0};
+    bb.groups = k.groups; bb.stat_stride = 8LL * k.cmax;
     bb.n = k.n; bb.h = k.h; bb.w = k.w; bb.c = k.width;
     RALPB_TRY(bn_backward(bb, m->bn_work, s));
   }
@@ -265,6 +275,7 @@ int block_backward(Model* m, BlockBufs& k, const bf16* x, const bf16* y, const b
     bb.mean = mean_of(k, 3); bb.rstd = rstd_of(k, 3); bb.gamma = P + k.gd_off;
     bb.dgamma = G + k.gd_off; bb.dbeta = G + k.gd_off + k.cout;
     bb.dx = MutAct4{k.dd_pre, 0};
+    bb.groups = k.groups; bb.stat_stride = 8LL * k.cmax;
     bb.n = k.n; bb.h = k.ho; bb.w = k.wo; bb.c = k.cout;
     RALPB_TRY(bn_backward(bb, m->bn_work, s));
     if (mm_wgrad(m, k.dd_pre, rout, k.cout, s1 ? x : k.d_in, k.cin, G + k.wd_off, why)) return 1;

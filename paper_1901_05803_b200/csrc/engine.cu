@@ -285,6 +285,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, const ralpb_node_
       std::string w2;
       if (module_build(k, nodes + d.node_begin, d.node_count, nb, d.h, d.w, in.c, &off, &runs, &count, &w2))
         return fail("layer " + std::to_string(i) + ": " + w2);
+      k.groups = i >= m->split ? workers : 1;   // the PS's back segment: per-worker statistics
       if (d.cout != k.cout) return fail("layer " + std::to_string(i) + ": module output channels differ from its nodes'");
       if (i < m->split) {
         for (auto& r : runs) real_runs.push_back(r);
@@ -311,6 +312,7 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, const ralpb_node_
         BlockBufs k;
         k.cin = in.c; k.width = d.width; k.cout = d.cout; k.stride = d.stride; k.down = d.downsample;
         k.n = nb; k.h = d.h; k.w = d.w; k.ho = d.h / d.stride; k.wo = d.w / d.stride;
+        k.groups = i >= m->split ? workers : 1;   // the PS's back segment: per-worker statistics
         auto take_params = [&](long long count) { const long long o2 = off; off = align_up(off + count, 4); return o2; };
         k.wa_off = take_params(static_cast<long long>(k.width) * k.cin);
         k.ga_off = take_params(2LL * k.width);

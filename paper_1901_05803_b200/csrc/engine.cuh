@@ -26,6 +26,8 @@ struct ActBuf {
 struct BlockBufs {
   int cin = 0, width = 0, cout = 0, stride = 1, down = 0;
   int n = 0, h = 0, w = 0, ho = 0, wo = 0;
+  int groups = 1;                 // batch-norm statistics per image group (the PS's back segment:
+                                  // one group per worker's b rows)
   long long wa_off = 0, ga_off = 0, wb_off = 0, gb_off = 0, wc_off = 0, gc_off = 0, wd_off = 0, gd_off = 0;
   __nv_bfloat16 *wa = nullptr, *wbf = nullptr, *wbd = nullptr, *wc = nullptr, *wd = nullptr;
   __nv_bfloat16 *a_pre = nullptr, *a = nullptr, *b_pre = nullptr, *b = nullptr, *c_pre = nullptr, *d_in = nullptr,
@@ -57,6 +59,7 @@ struct ModNode {
 };
 struct ModuleBufs {
   int n = 0, h = 0, w = 0, cin = 0, ho = 0, wo = 0, cout = 0;
+  int groups = 1;                 // batch-norm statistics per image group (see BlockBufs)
   std::vector<ModNode> nodes;
   __nv_bfloat16* col = nullptr;   // im2col patches / their gradient (largest conv node)
   __nv_bfloat16* dz = nullptr;    // gradient w.r.t. a conv node's pre-activation (largest node)

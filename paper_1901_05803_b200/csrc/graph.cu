@@ -483,7 +483,7 @@ int module_alloc(Model* m, ModuleBufs& k, std::string* why) {
       if (!(q.wbf = galloc<bf16>(m, static_cast<size_t>(q.d.cout) * q.K(), why))) return 1;
       if (q.d.bn) {
         if (!(q.z = galloc<bf16>(m, static_cast<size_t>(rout) * q.d.cout, why))) return 1;
-        if (!(q.stats = galloc<float>(m, 2 * static_cast<size_t>(q.d.cout), why))) return 1;
+        if (!(q.stats = galloc<float>(m, 2 * static_cast<size_t>(q.d.cout) * k.groups, why))) return 1;
         if (!(q.mask = galloc<uint8_t>(m, static_cast<size_t>(rout) * q.d.cout / 8, why))) return 1;
       }
       if (!q.direct) col = std::max(col, rout * q.K());
@@ -543,13 +543,15 @@ int module_forward(Model* m, ModuleBufs& k, const bf16* x, bf16* y, std::string*
       }
       if (d.bn) {
         if (gemm_fwd(m, a, rout, q.K(), q.wbf, d.cout, q.z, d.cout, nullptr, 0, why)) return 1;
-        RALPB_TRY(bn_stats(Act4{q.z, 0}, k.n, q.ho, q.wo, d.cout, kBnEps, m->bn_work, q.stats, q.stats + d.cout, s));
+        RALPB_TRY(bn_stats(Act4{q.z, 0}, k.n, q.ho, q.wo, d.cout, kBnEps, m->bn_work, q.stats, q.stats + d.cout, s,
+                           k.groups, 2LL * d.cout));
         BnApply ap{};
         ap.x = Act4{q.z, 0}; ap.mean = q.stats; ap.rstd = q.stats + d.cout;
         ap.gamma = m->P + q.b_off; ap.beta = m->P + q.b_off + d.cout; ap.relu = 1;
         ap.y = MutAct4{dst, 0, ldd};
         ap.mask_out = q.mask;
         ap.n = k.n; ap.h = q.ho; ap.w = q.wo; ap.c = d.cout;
+        ap.groups = k.groups; ap.stat_stride = 2LL * d.cout;
         RALPB_TRY(bn_apply(ap, s));
         m->launches += 3;
       } else {
@@ -600,6 +602,7 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
         bb.dgamma = G + q.b_off; bb.dbeta = G + q.b_off + d.cout;
         bb.dx = MutAct4{k.dz, 0};
         bb.n = k.n; bb.h = q.ho; bb.w = q.wo; bb.c = d.cout;
+        bb.groups = k.groups; bb.stat_stride = 2LL * d.cout;
         RALPB_TRY(bn_backward(bb, m->bn_work, s));
         m->launches += 3;
       } else {

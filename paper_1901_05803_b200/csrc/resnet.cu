@@ -479,8 +479,25 @@ bool fits(long long elems) { return elems < (1LL << 31); }
 
 }  // namespace
 
+// image group g of a batch tensor (groups of n / groups consecutive images)
+template <class T>
+T group_slice(T a, long long img0, int h, int w, int c) {
+  if (a.p != nullptr) a.p += img0 * (h + 2 * a.pad) * (w + 2 * a.pad) * static_cast<long long>(a.ld ? a.ld : c);
+  return a;
+}
+
 cudaError_t bn_stats(Act4 x, int n, int h, int w, int c, float eps, float* work, float* mean, float* rstd,
-                     cudaStream_t s) {
+                     cudaStream_t s, int groups, long long stat_stride) {
+  if (groups > 1) {
+    if (n % groups != 0) return cudaErrorInvalidValue;
+    const int gn = n / groups;
+    for (int g = 0; g < groups; ++g) {
+      const cudaError_t e = bn_stats(group_slice(x, static_cast<long long>(g) * gn, h, w, c), gn, h, w, c, eps, work,
+                                     mean + g * stat_stride, rstd + g * stat_stride, s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   const long long pixels = static_cast<long long>(n) * h * w;
   if (c % 8 != 0 || c / 8 > 256 || !fits(pixels * c)) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(work, 0, sizeof(float) * 2 * c, s);
@@ -493,6 +510,25 @@ cudaError_t bn_stats(Act4 x, int n, int h, int w, int c, float eps, float* work,
 }
 
 cudaError_t bn_apply(const BnApply& a, cudaStream_t s) {
+  if (a.groups > 1) {
+    if (a.n % a.groups != 0) return cudaErrorInvalidValue;
+    const int gn = a.n / a.groups;
+    for (int g = 0; g < a.groups; ++g) {
+      BnApply q = a;
+      const long long i0 = static_cast<long long>(g) * gn, o = g * a.stat_stride;
+      q.groups = 1;
+      q.n = gn;
+      q.x = group_slice(a.x, i0, a.h, a.w, a.c);
+      q.r = group_slice(a.r, i0, a.h, a.w, a.c);
+      q.y = group_slice(a.y, i0, a.h, a.w, a.c);
+      q.mean = a.mean + o; q.rstd = a.rstd + o;
+      if (a.res_kind == 2) { q.r_mean = a.r_mean + o; q.r_rstd = a.r_rstd + o; }
+      if (a.mask_out != nullptr) q.mask_out = a.mask_out + i0 * a.h * a.w * (a.c / 8);
+      const cudaError_t e = bn_apply(q, s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   const long long pixels = static_cast<long long>(a.n) * a.h * a.w;
   if (a.c % 8 != 0 || a.c / 8 > 256 || !fits(pixels * a.c)) return cudaErrorInvalidValue;
   const int lanes = 256 / (a.c / 8);
@@ -501,6 +537,26 @@ cudaError_t bn_apply(const BnApply& a, cudaStream_t s) {
 }
 
 cudaError_t bn_backward(const BnBackward& b, float* work, cudaStream_t s) {
+  if (b.groups > 1) {
+    if (b.n % b.groups != 0) return cudaErrorInvalidValue;
+    const int gn = b.n / b.groups;
+    for (int g = 0; g < b.groups; ++g) {
+      BnBackward q = b;
+      const long long i0 = static_cast<long long>(g) * gn, o = g * b.stat_stride;
+      q.groups = 1;
+      q.n = gn;
+      q.dy = group_slice(b.dy, i0, b.h, b.w, b.c);
+      q.y = group_slice(b.y, i0, b.h, b.w, b.c);
+      q.x = group_slice(b.x, i0, b.h, b.w, b.c);
+      q.dx = group_slice(b.dx, i0, b.h, b.w, b.c);
+      q.dz_out = group_slice(b.dz_out, i0, b.h, b.w, b.c);
+      q.mean = b.mean + o; q.rstd = b.rstd + o;
+      if (b.mask_in != nullptr) q.mask_in = b.mask_in + i0 * b.h * b.w * (b.c / 8);
+      const cudaError_t e = bn_backward(q, work, s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   const long long pixels = static_cast<long long>(b.n) * b.h * b.w;
   if (b.c % 8 != 0 || b.c / 8 > 256 || !fits(pixels * b.c)) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(work, 0, sizeof(float) * 2 * b.c, s);

@@ -27,8 +27,11 @@ struct MutAct4 {
 // Batch statistics over the n*h*w interior pixels: mean[c], rstd[c] = 1/sqrt(var + eps) (biased
 // variance, training mode; torch.nn.functional.batch_norm(training=True)).  `work` is fp32 [2c]
 // scratch (zeroed here).
+// groups > 1: the n images form `groups` equal consecutive groups, each normalised with its own
+// statistics (mean / rstd of group g at + g * stat_stride): per-worker batch statistics for layers
+// the PS runs over every worker's gathered rows.
 cudaError_t bn_stats(Act4 x, int n, int h, int w, int c, float eps, float* work, float* mean, float* rstd,
-                     cudaStream_t s);
+                     cudaStream_t s, int groups = 1, long long stat_stride = 0);
 
 // y = act((x - mean) * rstd * gamma + beta + residual), act = ReLU if relu; residual: none
 // (res_kind 0), a raw tensor r (1), or the batch norm of r with its own statistics (2).
@@ -43,6 +46,8 @@ struct BnApply {
   int n, h, w, c;
   uint8_t* mask_out = nullptr;   // optional (relu): [n*h*w][c/8] bytes, bit j of byte (p, g) = the
                                  // stored y[p][8g + j] > 0 -- the ReLU mask its backward reads
+  int groups = 1;                // per-group statistics (see bn_stats)
+  long long stat_stride = 0;
 };
 cudaError_t bn_apply(const BnApply& a, cudaStream_t s);
 
@@ -62,6 +67,8 @@ struct BnBackward {
   int n, h, w, c;
   const uint8_t* mask_in = nullptr;   // relu_mask from BnApply::mask_out bits instead of reading y
                                       // (1/16 of its bytes, read twice per backward)
+  int groups = 1;                     // per-group statistics (see bn_stats); dgamma / dbeta summed
+  long long stat_stride = 0;
 };
 cudaError_t bn_backward(const BnBackward& b, float* work, cudaStream_t s);
 

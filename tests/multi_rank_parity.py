@@ -255,6 +255,13 @@ def main():
         # exact sync / exchange ones above, the first step's loss (5e-3) and the floor rule (no cap)
         dict(model=catalog_lookup("resnet-50").with_batch_size(4), strategy="ralp", steps=2, lr=1e-3, floor=True,
              cap=100.0, split=55, loss_tol=5e-3, loss_steps=1),
+        # ... and with the sixteen blocks / eleven branch groups on the PS (splits 2 / 7, the
+        # partitioner's cuts at b <= 64): the PS normalises each worker's rows with that worker's
+        # own batch statistics, as the oracle's per-worker steps do
+        dict(model=catalog_lookup("resnet-50").with_batch_size(4), strategy="ralp", steps=2, lr=1e-3, floor=True,
+             cap=100.0, split=2, loss_tol=5e-3, loss_steps=1),
+        dict(model=catalog_lookup("inception-v3").with_batch_size(4), strategy="ralp", steps=2, lr=1e-3, floor=True,
+             cap=100.0, split=7, loss_tol=5e-3, loss_steps=1),
         dict(model=parse_model(TINY), strategy="ralp-mps", steps=3),
         # full VGG-16 geometry (224x224: first-conv, row-streamed 64-channel, slab pair kernels,
         # pool5 cut) at b=4 per rank
