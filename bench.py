@@ -159,6 +159,23 @@ def _cpu_baseline_step(sample_b: int, steps: int, warmup: int = 1):
                       f"{steps} timed steps after {warmup} warm-up, {dt:.1f} s"}
 
 
+def _overlap(timeline):
+    """Per side stream (aux: FC update; comm: act-grad scatter; sync: the sync bucket), the time its
+    timed kernels ran and how much of it overlapped the main stream's timed kernels (profiling
+    pass, rank 0's clock)."""
+    main = sorted((t0, t0 + d) for _, st, t0, d in timeline if st == "main")
+    out = {}
+    for _, st, t0, d in timeline:
+        if st == "main" or st == "?":
+            continue
+        ov = sum(max(0.0, min(t0 + d, b) - max(t0, a)) for a, b in main)
+        o = out.setdefault(st, {"launches": 0, "ms": 0.0, "overlapped_ms": 0.0})
+        o["launches"] += 1
+        o["ms"] += d
+        o["overlapped_ms"] += min(ov, d)
+    return {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()} for k, v in out.items()}
+
+
 def _headline_split():
     from paper_1901_05803_b200.planner import catalog_lookup, profile
     return profile(catalog_lookup(MODEL).with_batch_size(BATCH)).split_index
@@ -302,7 +319,13 @@ def run_ours(args):
     ex.step(dimgs[0], dlabs[0])
     prof = ex.stats()
     launches = ex.timed_launches()
+    timeline = ex.timeline()
     ex.set_profiling(False)
+    overlap = _overlap(timeline)
+    if rank == 0 and os.environ.get("RALPB_TIMELINE_OUT"):
+        Path(os.environ["RALPB_TIMELINE_OUT"]).write_text(json.dumps(
+            {"world": world, "rank": rank, "launches": [dict(kind=k, stream=st, t0_ms=t0, ms=d) for k, st, t0, d in timeline]},
+            indent=0))
     worker_flops, ps_flops = compute_load(m, rep.split_index, world)
     flops_rank = worker_flops + (ps_flops if rank == 0 else 0)
     peaks, peak_src = _peaks()
@@ -520,6 +543,7 @@ def run_ours(args):
             "resnet50": resnet50,
             "inception_v3": inception_v3,
             "googlenet": googlenet,
+            "overlap_rank0": overlap,
             "breakdown_ms_rank0": {"front_fwd": st.ms_front_fwd, "back": st.ms_back, "front_bwd": st.ms_front_bwd,
                                    "sync": st.ms_sync, "tensor_kernels_sum": prof.ms_gemm,
                                    "tensor_launches": prof.gemm_launches},

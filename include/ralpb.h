@@ -299,6 +299,8 @@ typedef struct {
   float ms;
   double flops;
   double bytes;        /* algorithmic DRAM bytes (push / shard update: NVLink bytes per direction) */
+  float t0;            /* start, ms after the step's first event (a per-rank timeline) */
+  int stream;          /* 0 main, 1 aux (FC update / filter copies), 2 comm (act-grad scatter), 3 sync (bucket) */
 } ralpb_launch_rec;
 int ralpb_model_timed_launches(ralpb_model* m, ralpb_launch_rec* out, int cap);
 

@@ -82,7 +82,8 @@ class NodeDesc(C.Structure):
 
 class LaunchRec(C.Structure):
     """ralpb_launch_rec (include/ralpb.h)."""
-    _fields_ = [("kind", C.c_int), ("ms", C.c_float), ("flops", C.c_double), ("bytes", C.c_double)]
+    _fields_ = [("kind", C.c_int), ("ms", C.c_float), ("flops", C.c_double), ("bytes", C.c_double),
+                ("t0", C.c_float), ("stream", C.c_int)]
 
 
 LAUNCH_KINDS = ["conv_fwd", "conv_fwd_pair", "conv_wgrad_pair", "conv_wgrad", "first_conv_fwd", "first_conv_wgrad",

@@ -706,6 +706,7 @@ void model_destroy(Model* m) {
     delete[] m->timer.kind;
     delete[] m->timer.flops;
     delete[] m->timer.bytes;
+    delete[] m->timer.stream;
     delete[] m->timer.ev;
   }
   if (m->stream) cudaStreamDestroy(m->stream);
@@ -2382,6 +2383,11 @@ int model_timed_launches(Model* m, ralpb_launch_rec* out, int cap, int* n, std::
     out[i].ms = ms;
     out[i].flops = m->timer.flops[i];
     out[i].bytes = m->timer.bytes[i];
+    float t0 = 0.f;
+    cudaEventElapsedTime(&t0, m->ev[0], m->timer.ev[2 * i]);
+    out[i].t0 = t0;
+    const cudaStream_t st = m->timer.stream[i];
+    out[i].stream = st == m->stream ? 0 : st == m->aux_stream ? 1 : st == m->comm_stream ? 2 : st == m->sync_stream ? 3 : -1;
   }
   return 0;
 }
@@ -2393,6 +2399,7 @@ int model_set_profiling(Model* m, int on, std::string* why) {
     m->timer.kind = new int[m->timer.cap];
     m->timer.flops = new double[m->timer.cap];
     m->timer.bytes = new double[m->timer.cap];
+    m->timer.stream = new cudaStream_t[m->timer.cap];
     for (int i = 0; i < 2 * m->timer.cap; ++i) RALPB_TRY(cudaEventCreate(&m->timer.ev[i]));
   }
   m->profiling = on != 0;

@@ -71,6 +71,7 @@ struct GemmTimer {
   int* kind = nullptr;        // [cap]
   double* flops = nullptr;    // [cap] algorithmic FLOPs of the launch
   double* bytes = nullptr;    // [cap] algorithmic DRAM (or NVLink) bytes of the launch
+  cudaStream_t* stream = nullptr;   // [cap] the launching stream
 };
 void set_gemm_timer(GemmTimer* t);  // thread-local; nullptr disables
 GemmTimer* current_gemm_timer();
@@ -85,6 +86,7 @@ void launch_timed(F&& f, cudaStream_t s, int kind = KIND_GEMM, double flops = 0.
     tm->kind[tm->n] = kind;
     tm->flops[tm->n] = flops;
     tm->bytes[tm->n] = bytes;
+    if (tm->stream != nullptr) tm->stream[tm->n] = s;
   }
   f();
   if (timed) cudaEventRecord(tm->ev[2 * tm->n++ + 1], s);

@@ -398,6 +398,17 @@ class RankExecutor:
         n = _lib.call_count("ralpb_model_timed_launches", self._h, recs, 512)
         return [(_lib.LAUNCH_KINDS[recs[i].kind], recs[i].ms, recs[i].flops, recs[i].bytes) for i in range(min(n, 512))]
 
+    STREAMS = ("main", "aux", "comm", "sync")
+
+    def timeline(self) -> list:
+        """[(kind name, stream name, start ms, duration ms)] of the last profiled step on this rank
+        (start relative to the step's first event): the overlap of the act-grad scatter (comm),
+        the FC update (aux) and the sync bucket (sync) with the main stream's kernels."""
+        recs = (_lib.LaunchRec * 512)()
+        n = _lib.call_count("ralpb_model_timed_launches", self._h, recs, 512)
+        return [(_lib.LAUNCH_KINDS[recs[i].kind], self.STREAMS[recs[i].stream] if 0 <= recs[i].stream < 4 else "?",
+                 recs[i].t0, recs[i].ms) for i in range(min(n, 512))]
+
     def set_profiling(self, on: bool) -> None:
         _lib.call("ralpb_model_set_profiling", self._h, int(on))
 
