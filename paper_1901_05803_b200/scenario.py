@@ -457,3 +457,35 @@ __all__ = ["B200_NODE", "CapacityError", "ClusterSpec", "DEFAULT_CLUSTER", "Meas
 
 if __name__ == "__main__":
     raise SystemExit(_rank_main(sys.argv[1], sys.argv[2]))
+
+
+def _as_scenario(scn) -> Scenario:
+    """This module's Scenario, or the reference's (`ralp.Scenario`: jobs as (name, JobSpec, Placement)
+    tuples over a catalog model) converted by value."""
+    if isinstance(scn, Scenario):
+        return scn
+    c = scn.cluster
+    cluster = ClusterSpec(**{f: getattr(c, f) for f in ClusterSpec.__dataclass_fields__ if hasattr(c, f)})
+    jobs = []
+    for name, spec, pl in scn.jobs:
+        jobs.append(ScenarioJob(name=name, spec=spec, placement=Placement(tuple(map(tuple, pl.workers)),
+                                                                         tuple(map(tuple, pl.ps))),
+                                model_ref=spec.model.name))
+    return Scenario(cluster=cluster, jobs=tuple(jobs), steps=scn.steps)
+
+
+def simulate_run(scenario, **kw) -> MeasuredReport:
+    """The drop-in for the reference's `simulate_run(Scenario) -> SimReport` (simulator.py:743-770),
+    MEASURED instead of simulated: every job of the scenario (this module's, or the reference's own
+    `ralp.Scenario` over catalog models) runs for real on this node's B200s (run_scenario) and the
+    report has the SimReport schema (`to_dict` / `to_json` / `timeline_csv`)."""
+    return run_scenario(_as_scenario(scenario), **kw)
+
+
+def simulate_step(scenario, **kw) -> list:
+    """`simulate_step` (simulator.py:773-776), measured: one step per job, its StepBreakdown."""
+    rep = run_scenario(_as_scenario(scenario), steps=1, **kw)
+    return [j.steps[0] for j in rep.jobs]
+
+
+SimReport = MeasuredReport

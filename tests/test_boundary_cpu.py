@@ -31,7 +31,8 @@ def ralp():
     return mod
 
 
-@pytest.mark.parametrize("name", ["vgg11", "vgg16", "alexnet", "cifar_small"])
+@pytest.mark.parametrize("name", ["vgg11", "vgg16", "alexnet", "cifar_small", "overfeat", "lenet", "resnet-50",
+                                  "inception-v3", "googlenet"])
 def test_reference_model_graph_lowers_like_the_mirror(ralp, name):
     try:
         ref_model = ralp.catalog_lookup(name)
@@ -113,3 +114,29 @@ def test_report_rows_gather_gloo(world):
         rows = res[r]
         assert [row[0] for row in rows] == [float(i) for i in range(world)]     # rank order
         assert sum(row[0] for row in rows) == sum(range(world))                 # the byte total
+
+
+def test_package_surface_covers_the_reference(ralp):
+    """Every name the reference package exports (pkg/src/ralp/__init__.py:46-91) is importable
+    from this package, except the network simulator's consolidation study (out of scope)."""
+    import paper_1901_05803_b200 as pkg
+    out_of_scope = {"simulate_consolidation", "ConsolidationReport"}
+    missing = [n for n in ralp.__all__ if n not in out_of_scope and not hasattr(pkg, n)]
+    assert not missing, missing
+
+
+def test_reference_scenario_converts_by_value(ralp):
+    """A scenario built with the reference's own types (ralp.Scenario of (name, JobSpec, Placement))
+    is what simulate_run / simulate_step execute: converted by value, placements and checks kept."""
+    from paper_1901_05803_b200.scenario import Scenario, _as_scenario
+    model = ralp.catalog_lookup("vgg11").with_batch_size(32)
+    split = ralp.profile(model).split_index
+    spec = ralp.JobSpec(model, ralp.Strategy.ralp(split), 2)
+    pl = ralp.spread_placement(ralp.DEFAULT_CLUSTER, [(2, 1)])[0]
+    ref = ralp.Scenario(ralp.DEFAULT_CLUSTER, (("j0", spec, pl),), steps=3)
+    mine = _as_scenario(ref)
+    assert isinstance(mine, Scenario) and mine.steps == 3
+    (job,) = mine.jobs
+    assert job.name == "j0" and job.model_ref == "vgg11" and job.spec is spec
+    assert job.placement.workers == tuple(map(tuple, pl.workers)) and job.placement.ps == tuple(map(tuple, pl.ps))
+    assert mine.cluster.machines == ralp.DEFAULT_CLUSTER.machines
