@@ -146,3 +146,18 @@ def test_run_scenario_on_gpu(capsys, tmp_path):
     assert len(d["losses"]) == 3 and all(0.0 < l < 20.0 for l in d["losses"])
     assert d["images_per_sec"] > 0 and d["predicted_step_time"] > 0 and d["gpus"] == [0]
     assert len(tl.read_text().splitlines()) == 1 + 3
+
+
+@pytest.mark.gpu
+def test_simulate_step_measured_on_gpu():
+    """The package's drop-in `simulate_step(Scenario)` (simulator.py:773-776) executes one step of
+    every job for real and returns its StepBreakdown (every worker's own measured times)."""
+    import paper_1901_05803_b200 as pkg
+    m = catalog_lookup("cifar_small").with_batch_size(64)
+    spec = JobSpec(m, Strategy.ralp(4), 1)
+    cluster = pkg.ClusterSpec(machines=1, gpus_per_machine=2, gpu_flops_per_sec=1e15, memcopy_bytes_per_sec=50e9,
+                              link_bytes_per_sec=450e9, intra_machine_bytes_per_sec=450e9)
+    pl = pkg.spread_placement(cluster, [(1, 1)])[0]
+    scn = pkg.Scenario(cluster, (S.ScenarioJob("j", spec, pl, "cifar_small"),), steps=1)
+    (sb,) = pkg.simulate_step(scn, warmup=1)
+    assert len(sb.worker_computation) == 1 and sb.worker_computation[0] > 0 and sb.memcopy == (0.0,)
