@@ -509,6 +509,7 @@ def run_ours(args):
                         f"{repc.split_index}; tensor_frac_of_step = compute_load() FLOPs / wall step time / "
                         "sustained bf16 peak"}
 
+    alexnet = catalog_comparator("alexnet") if cmp and MODEL != "alexnet" else None   # BASELINE config 2
     resnet50 = catalog_comparator("resnet-50") if cmp and not args.no_resnet and MODEL != "resnet-50" else None
     inception_v3 = catalog_comparator("inception-v3") if cmp and not args.no_branchy else None
     googlenet = catalog_comparator("googlenet") if cmp and not args.no_branchy else None
@@ -540,6 +541,7 @@ def run_ours(args):
             "ralp_fc_sharded": mps,
             "ralp_dedicated_ps": ralp_n,
             "precision_fp32": fp32,
+            "alexnet": alexnet,
             "resnet50": resnet50,
             "inception_v3": inception_v3,
             "googlenet": googlenet,

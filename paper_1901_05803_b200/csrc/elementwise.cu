@@ -111,74 +111,110 @@ __global__ void pack_im2col_row_kernel(const float* __restrict__ x, int n, int h
   }
 }
 
-// Large first-layer filters (AlexNet's 11x11x3 -> 363 (+bias) columns, kpad 384; ResNet's 7x7x3
-// stem -> 147 (+ones), kpad 192): one warp per patch row, lane l owns columns
-// [l*KPAD/32, (l+1)*KPAD/32) -- all index arithmetic is by compile-time constants and each lane
-// writes KPAD/32 contiguous bf16 (8-byte stores, 4-byte when KPAD/32 is not a multiple of 4).
+// Large first-layer filters (AlexNet's 11x11x3 -> 363 (+bias) columns, kpad 384; ResNet's /
+// GoogLeNet's 7x7x3 stem -> 147 (+ones), kpad 192).  One CTA per row of the padded output grid
+// (img, py): the K image rows its patches read are staged in shared memory as fp32 with coalesced
+// loads (zero outside the image; each image row is staged by ~K/st output rows instead of being
+// gathered column by column by every patch), then each warp builds whole patch rows from shared
+// memory: lane l owns columns [l*KPAD/32, (l+1)*KPAD/32), index arithmetic by compile-time
+// constants, 8-byte stores (4-byte when KPAD/32 is not a multiple of 4).
 template <int K, int C, int KPAD>
-__global__ void __launch_bounds__(256) pack_im2col_warp_kernel(const float* __restrict__ x, int n, int h, int w, int st,
+__global__ void __launch_bounds__(256) pack_im2col_smem_kernel(const float* __restrict__ x, int n, int h, int w, int st,
                                                                int p, int ho, int wo, int po,
                                                                __nv_bfloat16* __restrict__ out) {
   constexpr int PER = KPAD / 32, KK = K * K * C;
   static_assert(PER % 2 == 0, "lane span must be a multiple of 2 columns");
+  extern __shared__ float sx[];   // [K][w * C]
   const int hop = ho + 2 * po, wop = wo + 2 * po;
-  const long long rows = static_cast<long long>(n) * hop * wop;
-  const int lane = threadIdx.x & 31;
-  const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
-  for (long long row = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
-       row += warps) {
-    const long long img = row / (static_cast<long long>(hop) * wop);
-    const int rem = static_cast<int>(row - img * hop * wop);
-    const int oy = rem / wop - po, ox = rem % wop - po;
-    const bool interior = oy >= 0 && oy < ho && ox >= 0 && ox < wo;
-    const float* base = x + img * h * w * C;
-    uint32_t pk[PER / 2];
-#pragma unroll
-    for (int e2 = 0; e2 < PER / 2; ++e2) {
-      float v[2];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int j = lane * PER + 2 * e2 + q;
-        float val = 0.f;
-        if (interior) {
-          if (j < KK) {
-            const int ch = j % C, tap = j / C;
-            const int iy = oy * st + tap / K - p, ix = ox * st + tap % K - p;
-            if (iy >= 0 && iy < h && ix >= 0 && ix < w) val = __ldg(base + (static_cast<long long>(iy) * w + ix) * C + ch);
-          } else if (j == KK) {
-            val = 1.f;
-          }
-        }
-        v[q] = val;
+  const int rowlen = w * C;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int gr = blockIdx.x; gr < n * hop; gr += gridDim.x) {
+    const int img = gr / hop, py = gr - img * hop;
+    const int oy = py - po;
+    const bool row_in = oy >= 0 && oy < ho;
+    __syncthreads();   // the previous row's patches are built
+    if (row_in) {
+      const float* xi = x + static_cast<long long>(img) * h * rowlen;
+      for (int i = threadIdx.x; i < K * rowlen; i += blockDim.x) {
+        const int r = i / rowlen;
+        const int iy = oy * st - p + r;
+        sx[i] = (iy >= 0 && iy < h) ? __ldg(xi + static_cast<long long>(iy) * rowlen + (i - r * rowlen)) : 0.f;
       }
-      pk[e2] = pack_bf16(v[0], v[1]);
     }
-    if constexpr (PER % 4 == 0) {
-      uint2* dst = reinterpret_cast<uint2*>(out + row * KPAD + lane * PER);
+    __syncthreads();
+    for (int px = warp; px < wop; px += nwarps) {
+      const int ox = px - po;
+      const bool interior = row_in && ox >= 0 && ox < wo;
+      const int x0 = ox * st - p;
+      float v[PER];
+      if constexpr (PER % C == 0) {
+        // the lane's columns are PER / C whole taps: their (row, column) offsets are per-lane
+        // constants (tap_r / tap_s), so a value is one bounds test and one shared-memory load
 #pragma unroll
-      for (int e4 = 0; e4 < PER / 4; ++e4) dst[e4] = make_uint2(pk[2 * e4], pk[2 * e4 + 1]);
-    } else {
-      uint32_t* dst = reinterpret_cast<uint32_t*>(out + row * KPAD + lane * PER);
+        for (int t = 0; t < PER / C; ++t) {
+          const int tap = lane * (PER / C) + t;
+          const int r = tap / K, sc = tap - r * K;
+          const int ix = x0 + sc;
+          const bool ok = interior && tap < K * K && ix >= 0 && ix < w;
 #pragma unroll
-      for (int e2 = 0; e2 < PER / 2; ++e2) dst[e2] = pk[e2];
+          for (int ch = 0; ch < C; ++ch)
+            v[t * C + ch] = ok ? sx[r * rowlen + ix * C + ch] : 0.f;
+          if (tap == K * K) v[t * C] = interior ? 1.f : 0.f;   // the ones (bias) column
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+          const int j = lane * PER + e;
+          float val = 0.f;
+          if (interior) {
+            if (j < KK) {
+              const int ch = j % C, tap = j / C;
+              const int r = tap / K, ix = x0 + tap % K;
+              if (ix >= 0 && ix < w) val = sx[r * rowlen + ix * C + ch];
+            } else if (j == KK) {
+              val = 1.f;
+            }
+          }
+          v[e] = val;
+        }
+      }
+      uint32_t pk[PER / 2];
+#pragma unroll
+      for (int e2 = 0; e2 < PER / 2; ++e2) pk[e2] = pack_bf16(v[2 * e2], v[2 * e2 + 1]);
+      __nv_bfloat16* orow = out + (static_cast<long long>(gr) * wop + px) * KPAD + lane * PER;
+      if constexpr (PER % 4 == 0) {
+        uint2* dst = reinterpret_cast<uint2*>(orow);
+#pragma unroll
+        for (int e4 = 0; e4 < PER / 4; ++e4) dst[e4] = make_uint2(pk[2 * e4], pk[2 * e4 + 1]);
+      } else {
+        uint32_t* dst = reinterpret_cast<uint32_t*>(orow);
+#pragma unroll
+        for (int e2 = 0; e2 < PER / 2; ++e2) dst[e2] = pk[e2];
+      }
     }
   }
 }
 
+template <int K, int C, int KPAD>
+cudaError_t launch_im2col_smem(const float* x, int n, int h, int w, int st, int p, int ho, int wo, int po,
+                               __nv_bfloat16* out, cudaStream_t s) {
+  const size_t smem = sizeof(float) * K * static_cast<size_t>(w) * C;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pack_im2col_smem_kernel<K, C, KPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const long long rows = static_cast<long long>(n) * (ho + 2 * po);
+  const int grid = static_cast<int>(std::min<long long>(rows, static_cast<long long>(num_sms()) * 16));
+  pack_im2col_smem_kernel<K, C, KPAD><<<grid, 256, smem, s>>>(x, n, h, w, st, p, ho, wo, po, out);
+  return cudaGetLastError();
+}
+
 cudaError_t pack_im2col(const float* x, int n, int h, int w, int c, int k, int st, int p, int ho, int wo,
                         int po, int kpad, __nv_bfloat16* out, cudaStream_t s) {
-  if (k == 11 && c == 3 && kpad == 384) {
-    const long long rows = static_cast<long long>(n) * (ho + 2 * po) * (wo + 2 * po);
-    const int grid = static_cast<int>(std::min<long long>((rows + 7) / 8, static_cast<long long>(num_sms()) * 32));
-    pack_im2col_warp_kernel<11, 3, 384><<<grid, 256, 0, s>>>(x, n, h, w, st, p, ho, wo, po, out);
-    return cudaGetLastError();
-  }
-  if (k == 7 && c == 3 && kpad == 192) {
-    const long long rows = static_cast<long long>(n) * (ho + 2 * po) * (wo + 2 * po);
-    const int grid = static_cast<int>(std::min<long long>((rows + 7) / 8, static_cast<long long>(num_sms()) * 32));
-    pack_im2col_warp_kernel<7, 3, 192><<<grid, 256, 0, s>>>(x, n, h, w, st, p, ho, wo, po, out);
-    return cudaGetLastError();
-  }
+  if (k == 11 && c == 3 && kpad == 384) return launch_im2col_smem<11, 3, 384>(x, n, h, w, st, p, ho, wo, po, out, s);
+  if (k == 7 && c == 3 && kpad == 192) return launch_im2col_smem<7, 3, 192>(x, n, h, w, st, p, ho, wo, po, out, s);
   if (kpad % 8 != 0 || kpad < k * k * c + 1) return cudaErrorInvalidValue;
   const long long rows = static_cast<long long>(n) * (ho + 2 * po) * (wo + 2 * po);
   if (k == 3 && c == 3 && kpad == 32 && rows < (1LL << 31)) {
@@ -198,14 +234,14 @@ __global__ void maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, int n, i
   const int ohp = oh + 2 * po, owp = ow + 2 * po;
   const int hp = h + 2 * pi, wp = w + 2 * pi;
   const int cv = c / 8;
-  const long long total = static_cast<long long>(n) * ohp * owp * cv;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    int cg = static_cast<int>(i % cv);
-    long long pos = i / cv;
-    long long img = pos / (ohp * owp);
-    int r = static_cast<int>(pos - img * ohp * owp);
-    int py = r / owp, px = r - (r / owp) * owp;
+  // 32-bit index arithmetic (the launcher checks n * ohp * owp * cv < 2^31)
+  const int total = n * ohp * owp * cv;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int pos = i / cv;
+    const int cg = i - pos * cv;
+    const long long img = pos / (ohp * owp);
+    const int r = pos - static_cast<int>(img) * ohp * owp;
+    const int py = r / owp, px = r - py * owp;
     int oy = py - po, ox = px - po;
     uint4 res = make_uint4(0, 0, 0, 0);
     if (oy >= 0 && oy < oh && ox >= 0 && ox < ow) {
@@ -236,7 +272,7 @@ __global__ void maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, int n, i
         *reinterpret_cast<uint2*>(idx + ((img * oh + oy) * ow + ox) * c + cg * 8) = iw;
       }
     }
-    *reinterpret_cast<uint4*>(y + pos * c + cg * 8) = res;
+    *reinterpret_cast<uint4*>(y + static_cast<long long>(pos) * c + cg * 8) = res;
   }
 }
 
@@ -246,6 +282,7 @@ cudaError_t maxpool_fwd(const __nv_bfloat16* x, int n, int h, int w, int c, int 
   if (c % 8 != 0) return cudaErrorInvalidValue;
   int oh = (h - k) / st + 1, ow = (w - k) / st + 1;
   long long total = static_cast<long long>(n) * (oh + 2 * pad_out) * (ow + 2 * pad_out) * (c / 8);
+  if (total >= (1LL << 31)) return cudaErrorInvalidValue;
   maxpool_fwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, n, h, w, c, pad_in, k, st, y, pad_out, oh, ow, idx);
   return cudaGetLastError();
 }
@@ -463,22 +500,28 @@ __global__ void maxpool_bwd_idx_kernel(const uint8_t* __restrict__ idx, const __
 // position x 8 channels gathers dy from the (at most ceil(k/st)^2) windows whose recorded
 // argmax is this position -- 8 + 16 bytes per covering window instead of re-reading the
 // k*k inputs of every window.
+// KC / STC > 0: the window and stride as compile-time constants (AlexNet's overlapping 3/2 pools:
+// the covering-window bounds and position arithmetic fold into a few instructions; the kernel is
+// instruction-bound on these L2-resident tensors).
+template <int KC, int STC>
 __global__ void maxpool_bwd_gather_kernel(const uint8_t* __restrict__ idx, const __nv_bfloat16* __restrict__ dy,
-                                          int n, int h, int w, int c, int pi, int k, int st, int po, int oh, int ow,
-                                          __nv_bfloat16* __restrict__ dx, float* __restrict__ colsum) {
+                                          int n, int h, int w, int c, int pi, int k_rt, int st_rt, int po, int oh,
+                                          int ow, __nv_bfloat16* __restrict__ dx, float* __restrict__ colsum) {
+  const int k = KC > 0 ? KC : k_rt;
+  const int st = STC > 0 ? STC : st_rt;
   __shared__ float s_col[kPoolColsumMax];
   float csum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   const int cv = c >> 3;
-  const long long total = static_cast<long long>(n) * h * w * cv;
+  // 32-bit index arithmetic (the launcher checks n * h * w * cv < 2^31)
+  const int total = n * h * w * cv;
   const int hp = h + 2 * pi, wp = w + 2 * pi;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int cg = static_cast<int>(i % cv);
-    const long long pix = i / cv;
-    const int ix = static_cast<int>(pix % w);
-    const long long t = pix / w;
-    const int iy = static_cast<int>(t % h);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int pix = i / cv;
+    const int cg = i - pix * cv;
+    const int t = pix / w;
+    const int ix = pix - t * w;
     const long long img = t / h;
+    const int iy = t - static_cast<int>(img) * h;
     float g[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const int oy0 = iy - k + 1 > 0 ? (iy - k + st) / st : 0;
     const int ox0 = ix - k + 1 > 0 ? (ix - k + st) / st : 0;
@@ -517,12 +560,19 @@ cudaError_t maxpool_bwd_gather(const uint8_t* idx, const __nv_bfloat16* dy, int 
   const int oh = (h - k) / st + 1, ow = (w - k) / st + 1;
   const int threads = pool_threads(c);
   const long long work = static_cast<long long>(n) * h * w * (c / 8);
+  if (work >= (1LL << 31)) return cudaErrorInvalidValue;
+  // 4 resident blocks per SM: each block flushes c column-sum atomics at its end
   const int grid = static_cast<int>(std::max<long long>(1, std::min((work + threads - 1) / threads,
-                                                                   static_cast<long long>(num_sms()) * 16)));
+                                                                   static_cast<long long>(num_sms()) * 4)));
   // idx + dy read, dx written (interior)
   const double bytes = static_cast<double>(n) * c * (static_cast<double>(oh) * ow * 3.0 + static_cast<double>(h) * w * 2.0);
   launch_timed([&] {
-    maxpool_bwd_gather_kernel<<<grid, threads, 0, s>>>(idx, dy, n, h, w, c, pad_in, k, st, pad_out, oh, ow, dx, colsum);
+    if (k == 3 && st == 2)
+      maxpool_bwd_gather_kernel<3, 2><<<grid, threads, 0, s>>>(idx, dy, n, h, w, c, pad_in, k, st, pad_out, oh, ow, dx,
+                                                               colsum);
+    else
+      maxpool_bwd_gather_kernel<0, 0><<<grid, threads, 0, s>>>(idx, dy, n, h, w, c, pad_in, k, st, pad_out, oh, ow, dx,
+                                                               colsum);
   }, s, KIND_POOL_BWD, 0.0, bytes);
   return cudaGetLastError();
 }
