@@ -83,7 +83,6 @@ T* alloc(Model* m, size_t count, std::string* why) {
   return static_cast<T*>(p);
 }
 
-bool is_ps(const Model* m) { return m->rank == m->ps_rank; }
 
 char* peer(Model* m, int r) { return m->peer_base[r]; }
 template <class T>
