@@ -11,12 +11,21 @@
 // 3x3 runs as an im2col GEMM forward / backward-filter, and its backward-data as the stride-1
 // kernel over the gradient dilated with zeros.  Storage is bf16 everywhere; every reduction fp32.
 #include <algorithm>
+#include <cstdlib>
 #include "block.cuh"
 #include "elementwise.cuh"
 #include "gemm_host.cuh"
 #include "resnet.cuh"
 
 namespace ralpb {
+
+bool res_epilogue() {
+  static const bool on = [] {
+    const char* e = getenv("RALPB_RES_EPI");
+    return e != nullptr && e[0] == '1';
+  }();
+  return on;
+}
 
 namespace {
 
@@ -43,13 +52,15 @@ int mm_fwd(Model* m, const bf16* a, long long rows, int k, const bf16* w, int n,
   ++m->launches;
   return 0;
 }
-// out[rows][k] = dy[rows][n] . w[n][k]
-int mm_dgrad(Model* m, const bf16* dy, long long rows, int n, const bf16* w, int k, bf16* out, std::string* why) {
+// out[rows][k] = dy[rows][n] . w[n][k] (+ residual[rows][k]: a gradient summed in the epilogue; may be out)
+int mm_dgrad(Model* m, const bf16* dy, long long rows, int n, const bf16* w, int k, bf16* out, std::string* why,
+             const bf16* residual = nullptr) {
   GemmDesc d;
   d.M = static_cast<int>(rows); d.N = k; d.K = n;
   d.a_mode = LD_K; d.a = Operand2D{dy, rows, n, n};
   d.b_mode = LD_MN; d.b = Operand2D{w, n, k, k};
   d.epi = EPI_BF16; d.out = out; d.s_m = k;
+  d.residual = residual; d.res_s = k;
   RALPB_TRY(gemm_launch(d, m->stream, why));
   ++m->launches;
   return 0;
@@ -267,7 +278,11 @@ int block_backward(Model* m, BlockBufs& k, const bf16* x, const bf16* y, const b
   }
   // conv a
   if (mm_wgrad(m, k.da_pre, rin, k.width, x, k.cin, G + k.wa_off, why)) return 1;
-  if (dx != nullptr && mm_dgrad(m, k.da_pre, rin, k.width, k.wa, k.cin, dx, why)) return 1;
+  // dx = Wa^T da_pre (+ the identity shortcut's gradient dz, summed in the GEMM epilogue)
+  const bool fuse = res_epilogue();
+  if (dx != nullptr &&
+      mm_dgrad(m, k.da_pre, rin, k.width, k.wa, k.cin, dx, why, k.down || !fuse ? nullptr : k.dz))
+    return 1;
   // the shortcut
   if (k.down) {
     BnBackward bb{};
@@ -280,16 +295,20 @@ int block_backward(Model* m, BlockBufs& k, const bf16* x, const bf16* y, const b
     RALPB_TRY(bn_backward(bb, m->bn_work, s));
     if (mm_wgrad(m, k.dd_pre, rout, k.cout, s1 ? x : k.d_in, k.cin, G + k.wd_off, why)) return 1;
     if (dx != nullptr) {
-      if (mm_dgrad(m, k.dd_pre, rout, k.cout, k.wd, k.cin, k.dxs, why)) return 1;
-      if (s1)
+      if (s1 && fuse) {   // the projection's gradient accumulated into dx in the GEMM epilogue
+        if (mm_dgrad(m, k.dd_pre, rout, k.cout, k.wd, k.cin, dx, why, dx)) return 1;
+      } else if (s1) {
+        if (mm_dgrad(m, k.dd_pre, rout, k.cout, k.wd, k.cin, k.dxs, why)) return 1;
         RALPB_TRY(add_act(Act4{dx, 0}, Act4{k.dxs, 0}, MutAct4{dx, 0}, k.n, k.h, k.w, k.cin, s));
-      else
+      } else {
+        if (mm_dgrad(m, k.dd_pre, rout, k.cout, k.wd, k.cin, k.dxs, why)) return 1;
         RALPB_TRY(add_strided(k.dxs, k.n, k.ho, k.wo, k.cin, k.stride, MutAct4{dx, 0}, s));
+      }
     }
-  } else if (dx != nullptr) {
+  } else if (dx != nullptr && !fuse) {
     RALPB_TRY(add_act(Act4{dx, 0}, Act4{k.dz, 0}, MutAct4{dx, 0}, k.n, k.h, k.w, k.cin, s));
   }
-  m->launches += 24;
+  m->launches += fuse && !(k.down && !s1) ? 23 : 24;
   return 0;
 }
 

@@ -7,6 +7,10 @@
 namespace ralpb {
 
 int block_alloc(Model* m, BlockBufs& k, std::string* why);
+// RALPB_RES_EPI=1: a gradient summed into another in the dgrad GEMM's epilogue (GemmDesc::residual)
+// instead of a separate add pass -- measured slower (the narrow-K 1x1 dgrad GEMMs are epilogue-
+// bound: ResNet-50 15.80 vs 15.66 ms, Inception-v3 34.6 vs 34.2 ms, GoogLeNet 9.93 vs 9.67 ms)
+bool res_epilogue();
 int block_prep(Model* m, BlockBufs& k, cudaStream_t s, std::string* why);
 // x [n][h][w][cin] -> y [n][ho][wo][cout] (unpadded NHWC)
 int block_forward(Model* m, BlockBufs& k, const __nv_bfloat16* x, __nv_bfloat16* y, std::string* why);

@@ -63,8 +63,7 @@ struct ModuleBufs {
   std::vector<ModNode> nodes;
   __nv_bfloat16* col = nullptr;   // im2col patches / their gradient (largest conv node)
   __nv_bfloat16* dz = nullptr;    // gradient w.r.t. a conv node's pre-activation (largest node)
-  __nv_bfloat16* tmp = nullptr;   // a contribution to a gradient that is accumulated
-  long long col_elems = 0, dz_elems = 0, tmp_elems = 0;
+  long long col_elems = 0, dz_elems = 0;
 };
 
 struct FrontLayer {

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
         }
-        if (p.mask != nullptr) {
+        if (p.mask != nullptr && row_ok) {   // (rows >= M: never stored, and past the mask's end)
           const __nv_bfloat16* mp = p.mask + static_cast<long long>(m) * p.mask_s + n0;
           if (full_chunk) {
 #pragma unroll
@@ -216,6 +216,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
           } else {
             _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n0 + j < p.N)
               if (!(__bfloat162float(mp[j]) > 0.f)) v[j] = 0.f;
+          }
+        }
+        if (p.residual != nullptr && row_ok) {   // out += residual (a gradient summed into this one)
+          const __nv_bfloat16* rp = p.residual + static_cast<long long>(m) * p.res_s + n0;
+          if (full_chunk) {
+#pragma unroll
+            for (int j4 = 0; j4 < 4; ++j4) {
+              uint4 u = *reinterpret_cast<const uint4*>(rp + j4 * 8);
+              const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[j4 * 8 + e] += __bfloat162float(hb[e]);
+            }
+          } else {
+            _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n0 + j < p.N) v[j] += __bfloat162float(rp[j]);
           }
         }
         if (zero_row) {

@@ -180,6 +180,9 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
   p.sgd_mu = d.sgd_mu;
   p.mask = reinterpret_cast<const __nv_bfloat16*>(d.mask);
   p.mask_s = d.mask_s;
+  p.residual = reinterpret_cast<const __nv_bfloat16*>(d.residual);
+  p.res_s = d.res_s;
+  if (d.residual != nullptr && d.epi != EPI_BF16) { *why = "residual: EPI_BF16 only"; return cudaErrorInvalidValue; }
   p.border = d.border;
   p.img_rows = d.img_rows;
   p.wp = d.wp;

@@ -38,6 +38,8 @@ struct GemmDesc {
   float sgd_lr = 0.f, sgd_mu = 0.f;
   const void* mask = nullptr;
   long long mask_s = 0;
+  const void* residual = nullptr;   // EPI_BF16: += residual[m*res_s + n] before the store (may alias out)
+  long long res_s = 0;
   int border = 0;
   int img_rows = 1, wp = 1, pad = 0, h = 0, w = 0;
 };

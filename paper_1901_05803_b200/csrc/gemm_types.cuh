@@ -67,6 +67,8 @@ struct alignas(64) GemmParams {
   float sgd_lr, sgd_mu;
   const __nv_bfloat16* mask;  // relu-backward mask source (mask[m*mask_s + n] > 0), or nullptr
   long long mask_s;
+  const __nv_bfloat16* residual;  // EPI_BF16: out = acc + residual[m*res_s + n] (may alias out), or nullptr
+  long long res_s;
   int border;               // zero rows that are padding positions of the padded layout
   int img_rows, wp, pad, h, w;
 };

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include "elementwise.cuh"
 #include "gemm_host.cuh"
+#include "block.cuh"
 #include "graph.cuh"
 #include "resnet.cuh"
 
@@ -365,13 +366,15 @@ int gemm_fwd(Model* m, const bf16* a, long long rows, long long k, const bf16* w
   ++m->launches;
   return 0;
 }
-// out[rows][k] = dz[rows][n] . w[n][k]
-int gemm_dgrad(Model* m, const bf16* dz, long long rows, int n, const bf16* w, long long k, bf16* out, std::string* why) {
+// out[rows][k] = dz[rows][n] . w[n][k] (+ residual, e.g. out itself: accumulate in the epilogue)
+int gemm_dgrad(Model* m, const bf16* dz, long long rows, int n, const bf16* w, long long k, bf16* out, std::string* why,
+               const bf16* residual = nullptr) {
   GemmDesc d;
   d.M = static_cast<int>(rows); d.N = static_cast<int>(k); d.K = n;
   d.a_mode = LD_K; d.a = Operand2D{dz, rows, n, n};
   d.b_mode = LD_MN; d.b = Operand2D{w, n, k, k};
   d.epi = EPI_BF16; d.out = out; d.s_m = k;
+  d.residual = residual; d.res_s = k;
   RALPB_TRY(gemm_launch(d, m->stream, why));
   ++m->launches;
   return 0;
@@ -474,9 +477,8 @@ int module_build(ModuleBufs& k, const ralpb_node_desc* nodes, int n_nodes, int n
 }
 
 int module_alloc(Model* m, ModuleBufs& k, std::string* why) {
-  long long col = 16, dz = 16, tmp = 16;
+  long long col = 16, dz = 16;
   for (ModNode& q : k.nodes) {
-    const long long rin = static_cast<long long>(k.n) * q.h * q.w;
     const long long rout = static_cast<long long>(k.n) * q.ho * q.wo;
     const int c_out = q.d.op == RALPB_NODE_CONV ? q.d.cout : q.cin;
     if (q.d.op == RALPB_NODE_CONV) {
@@ -487,8 +489,8 @@ int module_alloc(Model* m, ModuleBufs& k, std::string* why) {
         if (!(q.mask = galloc<uint8_t>(m, static_cast<size_t>(rout) * q.d.cout / 8, why))) return 1;
       }
       if (!q.direct) col = std::max(col, rout * q.K());
+      else if (!res_epilogue()) col = std::max(col, static_cast<long long>(k.n) * q.h * q.w * q.cin);   // add-pass path
       dz = std::max(dz, rout * q.d.cout);
-      tmp = std::max(tmp, rin * q.cin);   // a 1x1 backward-data contribution that is accumulated
     } else if (q.d.op == RALPB_NODE_MAXPOOL) {
       if (!(q.idx = galloc<uint8_t>(m, static_cast<size_t>(rout) * q.cin, why))) return 1;
     }
@@ -497,10 +499,9 @@ int module_alloc(Model* m, ModuleBufs& k, std::string* why) {
       if (!(q.dy = galloc<bf16>(m, static_cast<size_t>(rout) * c_out, why))) return 1;
     }
   }
-  if (!(k.col = galloc<bf16>(m, static_cast<size_t>(col), why)) || !(k.dz = galloc<bf16>(m, static_cast<size_t>(dz), why)) ||
-      !(k.tmp = galloc<bf16>(m, static_cast<size_t>(tmp), why)))
+  if (!(k.col = galloc<bf16>(m, static_cast<size_t>(col), why)) || !(k.dz = galloc<bf16>(m, static_cast<size_t>(dz), why)))
     return 1;
-  k.col_elems = col; k.dz_elems = dz; k.tmp_elems = tmp;
+  k.col_elems = col; k.dz_elems = dz;
   return 0;
 }
 
@@ -625,13 +626,12 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
       }
       // backward-data
       if (g_in != nullptr) {
-        if (q.direct) {
-          bf16* out = acc ? k.tmp : g_in;
-          if (gemm_dgrad(m, k.dz, rout, d.cout, q.wbf, q.cin, out, why)) return 1;
-          if (acc) {
-            RALPB_TRY(add_act(Act4{g_in, 0}, Act4{k.tmp, 0}, MutAct4{g_in, 0}, k.n, q.h, q.w, q.cin, s));
-            ++m->launches;
-          }
+        if (q.direct && (!acc || res_epilogue())) {   // a later contribution: summed in the GEMM epilogue
+          if (gemm_dgrad(m, k.dz, rout, d.cout, q.wbf, q.cin, g_in, why, acc ? g_in : nullptr)) return 1;
+        } else if (q.direct) {   // RALPB_RES_EPI=0: via the patch workspace and an add pass
+          if (gemm_dgrad(m, k.dz, rout, d.cout, q.wbf, q.cin, k.col, why)) return 1;
+          RALPB_TRY(add_act(Act4{g_in, 0}, Act4{k.col, 0}, MutAct4{g_in, 0}, k.n, q.h, q.w, q.cin, s));
+          ++m->launches;
         } else {
           if (gemm_dgrad(m, k.dz, rout, d.cout, q.wbf, q.K(), k.col, why)) return 1;
           const long long total = rin * ((q.cin / 8 + kChunk - 1) / kChunk);
