@@ -14,6 +14,9 @@ static bool check_geom(const ConvGeom& g, std::string* why) {
   return true;
 }
 
+// K-block of the implicit-GEMM A operand: the widest of 64 / 32 / 16 channels dividing c
+static int kb_for(int c) { return c % 64 == 0 ? 64 : (c % 32 == 0 ? 32 : 16); }
+
 static void fill_taps(const ConvGeom& g, GemmDesc* d) {
   d->taps = g.taps();
   for (int r = 0; r < g.k; ++r)
@@ -35,7 +38,7 @@ cudaError_t conv_fwd_flat(const ConvGeom& g, const void* x_pad, const void* w, c
   GemmDesc d;
   d.M = static_cast<int>(g.q());
   d.N = g.cout;
-  d.kb = std::min(64, g.cin);
+  d.kb = kb_for(g.cin);
   d.K = static_cast<long long>(g.taps()) * g.cin;
   d.a_mode = LD_K_CONV;
   d.a = Operand2D{x_pad, g.q(), g.cin, g.cin};
@@ -59,7 +62,7 @@ cudaError_t conv_dgrad_flat(const ConvGeom& g, const void* dy_pad, const void* w
   GemmDesc d;
   d.M = static_cast<int>(g.q());
   d.N = g.cin;
-  d.kb = std::min(64, g.cout);
+  d.kb = kb_for(g.cout);
   d.K = static_cast<long long>(g.taps()) * g.cout;
   d.a_mode = LD_K_CONV;
   d.a = Operand2D{dy_pad, g.q(), g.cout, g.cout};

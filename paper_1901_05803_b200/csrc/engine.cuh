@@ -47,9 +47,16 @@ struct ModNode {
   int out_off = 0;             // output node: channel offset in the module output
   int consumers = 0;           // nodes reading this node's output
   bool direct = false;         // conv 1x1 / stride 1 / no padding: a GEMM over the input rows
+  bool same = false;           // conv 3x3 / 5x5, stride 1, "same" padding p, channels % 16: the
+  int p = 0;                   // implicit-GEMM conv kernels (conv.cuh) over padded copies
+  __nv_bfloat16* xp = nullptr;        // same: the input, padded by p (zero borders)
+  __nv_bfloat16* dzp = nullptr;       // same: gradient w.r.t. the pre-activation, padded
+  __nv_bfloat16* dxp = nullptr;       // same: gradient w.r.t. the input, padded
+  __nv_bfloat16* wdb = nullptr;       // same: backward-data filters [cin][taps reversed][cout]
   long long w_off = -1, b_off = -1;   // conv: filters [cout][kh*kw*cin], then gamma|beta or bias
   __nv_bfloat16* wbf = nullptr;       // conv: bf16 copy of the filters
-  __nv_bfloat16* z = nullptr;         // bn conv: output before the batch norm
+  __nv_bfloat16* z = nullptr;         // bn conv: output before the batch norm (same: padded; bias
+                                      // conv: the same path's padded output)
   __nv_bfloat16* y = nullptr;         // non-output node: its output
   __nv_bfloat16* dy = nullptr;        // non-output node: gradient w.r.t. its output
   uint8_t* idx = nullptr;             // max pool: window position of the first max (255: not > 0)

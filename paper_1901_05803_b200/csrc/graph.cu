@@ -17,6 +17,8 @@
 // Gradients of a tensor read by several nodes are accumulated in bf16 (the first contribution
 // stores, later ones add).
 #include <algorithm>
+#include <cstdlib>
+#include "conv.cuh"
 #include "elementwise.cuh"
 #include "gemm_host.cuh"
 #include "block.cuh"
@@ -334,6 +336,39 @@ __global__ void avgpool_gen_bwd_kernel(const bf16* __restrict__ dy, int ldy, int
   }
 }
 
+// xp (interior of [n][h+2p][w+2p][c], borders untouched = zero) = x ([n][h][w], pixel stride ldx)
+__global__ void pad_copy_kernel(const bf16* __restrict__ x, int ldx, int n, int h, int w, int c, int pad,
+                                bf16* __restrict__ xp) {
+  const int groups = c >> 3;
+  const int total = n * h * w * groups;
+  const int hp = h + 2 * pad, wp = w + 2 * pad;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const Pix q(i, groups, h, w);
+    *reinterpret_cast<uint4*>(xp + (static_cast<long long>(q.img * hp + q.y + pad) * wp + q.x + pad) * c + q.g * 8) =
+        *reinterpret_cast<const uint4*>(x + static_cast<long long>(q.p) * ldx + q.g * 8);
+  }
+}
+
+// dst ([n][h][w], pixel stride ldd) (+)= the interior of src ([n][h+2p][w+2p][c])
+__global__ void unpad_kernel(const bf16* __restrict__ src, int n, int h, int w, int c, int pad, bf16* __restrict__ dst,
+                             int ldd, int acc) {
+  const int groups = c >> 3;
+  const int total = n * h * w * groups;
+  const int hp = h + 2 * pad, wp = w + 2 * pad;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const Pix q(i, groups, h, w);
+    float a[8], v[8];
+    load8(src + (static_cast<long long>(q.img * hp + q.y + pad) * wp + q.x + pad) * c + q.g * 8, v);
+    bf16* d = dst + static_cast<long long>(q.p) * ldd + q.g * 8;
+    if (acc) {
+      load8(d, a);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] += a[j];
+    }
+    store8(d, v);
+  }
+}
+
 // dz[p][c] = dy[p*ldy + c] * (y[p*ldy2 + c] > 0)  (the ReLU of a bias convolution)
 __global__ void relu_grad_kernel(const bf16* __restrict__ dy, int ldy, const bf16* __restrict__ y, int ldyv, long long pixels,
                                  int c, bf16* __restrict__ dz) {
@@ -405,6 +440,22 @@ T* galloc(Model* m, size_t count, std::string* why) {
 
 long long al4(long long x) { return (x + 3) & ~3LL; }
 
+// RALPB_MODULE_IMPLICIT=0: every non-1x1 window through im2col (the A/B baseline)
+bool implicit_same() {
+  static const bool on = [] {
+    const char* e = getenv("RALPB_MODULE_IMPLICIT");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
+template <class T>
+T* galloc_zero(Model* m, size_t count, std::string* why) {
+  T* p = galloc<T>(m, count, why);
+  if (p != nullptr) cudaMemset(p, 0, std::max<size_t>(count * sizeof(T), 16));
+  return p;
+}
+
 }  // namespace
 
 int module_build(ModuleBufs& k, const ralpb_node_desc* nodes, int n_nodes, int n, int h, int w, int cin,
@@ -448,6 +499,12 @@ int module_build(ModuleBufs& k, const ralpb_node_desc* nodes, int n_nodes, int n
     if (d.op == RALPB_NODE_CONV) {
       if (d.cout % 8 != 0 || d.cout < 8) { *why = tag + "conv output channels must be a multiple of 8"; return 1; }
       q.direct = d.kh == 1 && d.kw == 1 && d.stride == 1 && d.pad_h == 0 && d.pad_w == 0;
+      // ... where the padded grid adds <= 35 % (the implicit kernels compute over it; measured: small
+      // 7x7 / 14x14 windows are faster through im2col)
+      q.same = implicit_same() && d.kh == d.kw && (d.kh == 3 || d.kh == 5) && d.stride == 1 && d.pad_h == d.pad_w &&
+               d.kh == 2 * d.pad_h + 1 && q.cin % 16 == 0 && d.cout % 16 == 0 &&
+               100LL * (q.h + 2 * d.pad_h) * (q.w + 2 * d.pad_w) <= 135LL * q.h * q.w;
+      q.p = q.same ? d.pad_h : 0;
       q.w_off = *off;
       *off = al4(*off + static_cast<long long>(d.cout) * q.K());
       q.b_off = *off;
@@ -481,7 +538,19 @@ int module_alloc(Model* m, ModuleBufs& k, std::string* why) {
   for (ModNode& q : k.nodes) {
     const long long rout = static_cast<long long>(k.n) * q.ho * q.wo;
     const int c_out = q.d.op == RALPB_NODE_CONV ? q.d.cout : q.cin;
-    if (q.d.op == RALPB_NODE_CONV) {
+    if (q.d.op == RALPB_NODE_CONV && q.same) {
+      // the padded input copy, (pre-activation) output, and the gradients, all with zero borders
+      const size_t pix = static_cast<size_t>(k.n) * (q.h + 2 * q.p) * (q.w + 2 * q.p);
+      if (!(q.wbf = galloc<bf16>(m, static_cast<size_t>(q.d.cout) * q.K(), why)) ||
+          !(q.wdb = galloc<bf16>(m, static_cast<size_t>(q.d.cout) * q.K(), why)) ||
+          !(q.xp = galloc_zero<bf16>(m, pix * q.cin, why)) || !(q.z = galloc_zero<bf16>(m, pix * q.d.cout, why)) ||
+          !(q.dzp = galloc_zero<bf16>(m, pix * q.d.cout, why)) || !(q.dxp = galloc_zero<bf16>(m, pix * q.cin, why)))
+        return 1;
+      if (q.d.bn && (!(q.stats = galloc<float>(m, 2 * static_cast<size_t>(q.d.cout) * k.groups, why)) ||
+                     !(q.mask = galloc<uint8_t>(m, static_cast<size_t>(rout) * q.d.cout / 8, why))))
+        return 1;
+      dz = std::max(dz, rout * q.d.cout);
+    } else if (q.d.op == RALPB_NODE_CONV) {
       if (!(q.wbf = galloc<bf16>(m, static_cast<size_t>(q.d.cout) * q.K(), why))) return 1;
       if (q.d.bn) {
         if (!(q.z = galloc<bf16>(m, static_cast<size_t>(rout) * q.d.cout, why))) return 1;
@@ -508,7 +577,10 @@ int module_alloc(Model* m, ModuleBufs& k, std::string* why) {
 int module_prep(Model* m, ModuleBufs& k, cudaStream_t s, std::string* why) {
   for (ModNode& q : k.nodes) {
     if (q.d.op != RALPB_NODE_CONV || q.wbf == nullptr) continue;
-    RALPB_TRY(cast_bf16(m->P + q.w_off, static_cast<long long>(q.d.cout) * q.K(), q.wbf, s));
+    if (q.same)   // [cout][taps][cin] forward copy and the tap-reversed transpose for backward-data
+      RALPB_TRY(conv_weight_prep(m->P + q.w_off, q.d.cout, q.d.kh * q.d.kw, q.cin, q.wbf, q.wdb, s));
+    else
+      RALPB_TRY(cast_bf16(m->P + q.w_off, static_cast<long long>(q.d.cout) * q.K(), q.wbf, s));
     ++m->launches;
   }
   return 0;
@@ -532,7 +604,34 @@ int module_forward(Model* m, ModuleBufs& k, const bf16* x, bf16* y, std::string*
     const long long rout = static_cast<long long>(k.n) * q.ho * q.wo;
     bf16* dst = d.output ? y + q.out_off : q.y;
     const int ldd = d.output ? k.cout : (d.op == RALPB_NODE_CONV ? d.cout : q.cin);
-    if (d.op == RALPB_NODE_CONV) {
+    if (d.op == RALPB_NODE_CONV && q.same) {
+      // implicit GEMM over a padded copy of the input (slab / flat kernels of conv.cuh): no patch
+      // matrix; the (pre-activation) output lands in the interior of z
+      const ConvGeom g{k.n, q.h, q.w, q.cin, d.cout, d.kh, q.p};
+      const long long tin = static_cast<long long>(k.n) * q.h * q.w * (q.cin / 8);
+      pad_copy_kernel<<<grid_for(tin, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, q.p, q.xp);
+      RALPB_TRY(cudaGetLastError());
+      RALPB_TRY(conv_fwd(g, q.xp, q.wbf, d.bn ? nullptr : m->P + q.b_off, q.z, d.bn ? 0 : 1, s, why));
+      m->launches += 2;
+      if (d.bn) {
+        RALPB_TRY(bn_stats(Act4{q.z, q.p}, k.n, q.ho, q.wo, d.cout, kBnEps, m->bn_work, q.stats, q.stats + d.cout, s,
+                           k.groups, 2LL * d.cout));
+        BnApply ap{};
+        ap.x = Act4{q.z, q.p}; ap.mean = q.stats; ap.rstd = q.stats + d.cout;
+        ap.gamma = m->P + q.b_off; ap.beta = m->P + q.b_off + d.cout; ap.relu = 1;
+        ap.y = MutAct4{dst, 0, ldd};
+        ap.mask_out = q.mask;
+        ap.n = k.n; ap.h = q.ho; ap.w = q.wo; ap.c = d.cout;
+        ap.groups = k.groups; ap.stat_stride = 2LL * d.cout;
+        RALPB_TRY(bn_apply(ap, s));
+        m->launches += 3;
+      } else {
+        const long long tout = rout * (d.cout / 8);
+        unpad_kernel<<<grid_for(tout, 256), 256, 0, s>>>(q.z, k.n, q.ho, q.wo, d.cout, q.p, dst, ldd, 0);
+        RALPB_TRY(cudaGetLastError());
+        ++m->launches;
+      }
+    } else if (d.op == RALPB_NODE_CONV) {
       const bf16* a = src;
       if (!q.direct) {
         const long long total = rout * 32;   // a warp per patch row
@@ -593,7 +692,39 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
     bf16* g_in = d.input < 0 ? dx : k.nodes[d.input].dy;     // gradient w.r.t. its input (may be null)
     char& st = started[d.input + 1];
     const int acc = st ? 1 : 0;
-    if (d.op == RALPB_NODE_CONV) {
+    if (d.op == RALPB_NODE_CONV && q.same) {
+      const ConvGeom g{k.n, q.h, q.w, q.cin, d.cout, d.kh, q.p};
+      if (d.bn) {   // dz (padded) from the batch-norm backward
+        BnBackward bb{};
+        bb.dy = Act4{g_out, 0, ldo}; bb.y = Act4{v_out, 0, ldo}; bb.relu_mask = 1; bb.x = Act4{q.z, q.p};
+        bb.mask_in = q.mask;
+        bb.mean = q.stats; bb.rstd = q.stats + d.cout; bb.gamma = P + q.b_off;
+        bb.dgamma = G + q.b_off; bb.dbeta = G + q.b_off + d.cout;
+        bb.dx = MutAct4{q.dzp, q.p};
+        bb.n = k.n; bb.h = q.ho; bb.w = q.wo; bb.c = d.cout;
+        bb.groups = k.groups; bb.stat_stride = 2LL * d.cout;
+        RALPB_TRY(bn_backward(bb, m->bn_work, s));
+        m->launches += 3;
+      } else {      // dz = dy * relu'(y), then its padded copy; the bias gradient = its column sums
+        const long long total = rout * (d.cout / 8);
+        relu_grad_kernel<<<grid_for(total, 256), 256, 0, s>>>(g_out, ldo, v_out, ldo, rout, d.cout, k.dz);
+        RALPB_TRY(cudaGetLastError());
+        pad_copy_kernel<<<grid_for(total, 256), 256, 0, s>>>(k.dz, d.cout, k.n, q.ho, q.wo, d.cout, q.p, q.dzp);
+        RALPB_TRY(cudaGetLastError());
+        RALPB_TRY(colsum_bf16(k.dz, rout, d.cout, d.cout, G + q.b_off, s));
+        m->launches += 3;
+      }
+      RALPB_TRY(conv_wgrad(g, q.xp, q.dzp, G + q.w_off, nullptr, s, why));
+      ++m->launches;
+      if (g_in != nullptr) {
+        RALPB_TRY(conv_dgrad(g, q.dzp, q.wdb, nullptr, q.dxp, nullptr, s, why));
+        const long long tin = rin * (q.cin / 8);
+        unpad_kernel<<<grid_for(tin, 256), 256, 0, s>>>(q.dxp, k.n, q.h, q.w, q.cin, q.p, g_in, lds, acc);
+        RALPB_TRY(cudaGetLastError());
+        m->launches += 2;
+        st = 1;
+      }
+    } else if (d.op == RALPB_NODE_CONV) {
       // dz: the gradient w.r.t. the pre-activation (bn: w.r.t. the pre-batch-norm output)
       if (d.bn) {
         BnBackward bb{};
