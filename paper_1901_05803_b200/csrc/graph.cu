@@ -448,6 +448,15 @@ bool implicit_same() {
   }();
   return on;
 }
+// channel alignment the implicit path requires (RALPB_MODULE_IMPLICIT_ALIGN, default 32): narrower
+// K-blocks (16 channels) starve the implicit GEMM's pipeline
+int implicit_align() {
+  static const int a = [] {
+    const char* e = getenv("RALPB_MODULE_IMPLICIT_ALIGN");
+    return e != nullptr ? std::max(16, atoi(e)) : 32;
+  }();
+  return a;
+}
 
 template <class T>
 T* galloc_zero(Model* m, size_t count, std::string* why) {
@@ -502,7 +511,7 @@ int module_build(ModuleBufs& k, const ralpb_node_desc* nodes, int n_nodes, int n
       // ... where the padded grid adds <= 35 % (the implicit kernels compute over it; measured: small
       // 7x7 / 14x14 windows are faster through im2col)
       q.same = implicit_same() && d.kh == d.kw && (d.kh == 3 || d.kh == 5) && d.stride == 1 && d.pad_h == d.pad_w &&
-               d.kh == 2 * d.pad_h + 1 && q.cin % 16 == 0 && d.cout % 16 == 0 &&
+               d.kh == 2 * d.pad_h + 1 && q.cin % implicit_align() == 0 && d.cout % implicit_align() == 0 &&
                100LL * (q.h + 2 * d.pad_h) * (q.w + 2 * d.pad_w) <= 135LL * q.h * q.w;
       q.p = q.same ? d.pad_h : 0;
       q.w_off = *off;
