@@ -49,6 +49,7 @@ struct ModNode {
   bool direct = false;         // conv 1x1 / stride 1 / no padding: a GEMM over the input rows
   bool same = false;           // conv 3x3 / 5x5, stride 1, "same" padding p, channels % 16: the
   int p = 0;                   // implicit-GEMM conv kernels (conv.cuh) over padded copies
+  int crop = 0;                // same, 'valid' node (pad 0): its outputs are the same conv's cropped by p
   __nv_bfloat16* xp = nullptr;        // same: the input, padded by p (zero borders)
   __nv_bfloat16* dzp = nullptr;       // same: gradient w.r.t. the pre-activation, padded
   __nv_bfloat16* dxp = nullptr;       // same: gradient w.r.t. the input, padded

@@ -12,8 +12,10 @@
 //   maxpool  first maximum of the window, padding never wins
 //   avgpool  mean over the in-image elements of the window (padding not counted)
 // Contractions run on the tcgen05 GEMM engine: a 1x1 / stride-1 / unpadded convolution is one GEMM
-// over the NHWC rows; every other window goes through an im2col patch matrix (forward, backward-
-// filter) and a patch-gradient GEMM + col2im gather (backward-data, deterministic: no atomics).
+// over the NHWC rows; a square 3x3 / 5x5 stride-1 'same' (or 'valid': cropped 'same') window with
+// 32-aligned channels runs on the implicit-GEMM conv kernels (conv.cuh) over a padded copy of its
+// input; every other window goes through an im2col patch matrix (forward, backward-filter) and a
+// patch-gradient GEMM + col2im gather (backward-data, deterministic: no atomics).
 // Gradients of a tensor read by several nodes are accumulated in bf16 (the first contribution
 // stores, later ones add).
 #include <algorithm>
@@ -510,10 +512,14 @@ int module_build(ModuleBufs& k, const ralpb_node_desc* nodes, int n_nodes, int n
       q.direct = d.kh == 1 && d.kw == 1 && d.stride == 1 && d.pad_h == 0 && d.pad_w == 0;
       // ... where the padded grid adds <= 35 % (the implicit kernels compute over it; measured: small
       // 7x7 / 14x14 windows are faster through im2col)
+      // 'same' (pad (k-1)/2) or 'valid' (pad 0: the same convolution's outputs cropped by (k-1)/2)
+      const int kp = (d.kh - 1) / 2;
+      const bool valid = d.pad_h == 0 && d.pad_w == 0;
       q.same = implicit_same() && d.kh == d.kw && (d.kh == 3 || d.kh == 5) && d.stride == 1 && d.pad_h == d.pad_w &&
-               d.kh == 2 * d.pad_h + 1 && q.cin % implicit_align() == 0 && d.cout % implicit_align() == 0 &&
-               100LL * (q.h + 2 * d.pad_h) * (q.w + 2 * d.pad_w) <= 135LL * q.h * q.w;
-      q.p = q.same ? d.pad_h : 0;
+               (d.pad_h == kp || valid) && q.cin % implicit_align() == 0 && d.cout % implicit_align() == 0 &&
+               100LL * (q.h + 2 * kp) * (q.w + 2 * kp) <= 135LL * q.ho * q.wo;
+      q.p = q.same ? kp : 0;
+      q.crop = q.same && valid ? kp : 0;
       q.w_off = *off;
       *off = al4(*off + static_cast<long long>(d.cout) * q.K());
       q.b_off = *off;
@@ -623,10 +629,11 @@ int module_forward(Model* m, ModuleBufs& k, const bf16* x, bf16* y, std::string*
       RALPB_TRY(conv_fwd(g, q.xp, q.wbf, d.bn ? nullptr : m->P + q.b_off, q.z, d.bn ? 0 : 1, s, why));
       m->launches += 2;
       if (d.bn) {
-        RALPB_TRY(bn_stats(Act4{q.z, q.p}, k.n, q.ho, q.wo, d.cout, kBnEps, m->bn_work, q.stats, q.stats + d.cout, s,
+        RALPB_TRY(bn_stats(Act4{q.z, q.p + q.crop}, k.n, q.ho, q.wo, d.cout, kBnEps, m->bn_work, q.stats,
+                           q.stats + d.cout, s,
                            k.groups, 2LL * d.cout));
         BnApply ap{};
-        ap.x = Act4{q.z, q.p}; ap.mean = q.stats; ap.rstd = q.stats + d.cout;
+        ap.x = Act4{q.z, q.p + q.crop}; ap.mean = q.stats; ap.rstd = q.stats + d.cout;
         ap.gamma = m->P + q.b_off; ap.beta = m->P + q.b_off + d.cout; ap.relu = 1;
         ap.y = MutAct4{dst, 0, ldd};
         ap.mask_out = q.mask;
@@ -636,7 +643,7 @@ int module_forward(Model* m, ModuleBufs& k, const bf16* x, bf16* y, std::string*
         m->launches += 3;
       } else {
         const long long tout = rout * (d.cout / 8);
-        unpad_kernel<<<grid_for(tout, 256), 256, 0, s>>>(q.z, k.n, q.ho, q.wo, d.cout, q.p, dst, ldd, 0);
+        unpad_kernel<<<grid_for(tout, 256), 256, 0, s>>>(q.z, k.n, q.ho, q.wo, d.cout, q.p + q.crop, dst, ldd, 0);
         RALPB_TRY(cudaGetLastError());
         ++m->launches;
       }
@@ -705,11 +712,11 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
       const ConvGeom g{k.n, q.h, q.w, q.cin, d.cout, d.kh, q.p};
       if (d.bn) {   // dz (padded) from the batch-norm backward
         BnBackward bb{};
-        bb.dy = Act4{g_out, 0, ldo}; bb.y = Act4{v_out, 0, ldo}; bb.relu_mask = 1; bb.x = Act4{q.z, q.p};
+        bb.dy = Act4{g_out, 0, ldo}; bb.y = Act4{v_out, 0, ldo}; bb.relu_mask = 1; bb.x = Act4{q.z, q.p + q.crop};
         bb.mask_in = q.mask;
         bb.mean = q.stats; bb.rstd = q.stats + d.cout; bb.gamma = P + q.b_off;
         bb.dgamma = G + q.b_off; bb.dbeta = G + q.b_off + d.cout;
-        bb.dx = MutAct4{q.dzp, q.p};
+        bb.dx = MutAct4{q.dzp, q.p + q.crop};   // (a cropped ring of the same conv's outputs stays 0)
         bb.n = k.n; bb.h = q.ho; bb.w = q.wo; bb.c = d.cout;
         bb.groups = k.groups; bb.stat_stride = 2LL * d.cout;
         RALPB_TRY(bn_backward(bb, m->bn_work, s));
@@ -718,7 +725,7 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
         const long long total = rout * (d.cout / 8);
         relu_grad_kernel<<<grid_for(total, 256), 256, 0, s>>>(g_out, ldo, v_out, ldo, rout, d.cout, k.dz);
         RALPB_TRY(cudaGetLastError());
-        pad_copy_kernel<<<grid_for(total, 256), 256, 0, s>>>(k.dz, d.cout, k.n, q.ho, q.wo, d.cout, q.p, q.dzp);
+        pad_copy_kernel<<<grid_for(total, 256), 256, 0, s>>>(k.dz, d.cout, k.n, q.ho, q.wo, d.cout, q.p + q.crop, q.dzp);
         RALPB_TRY(cudaGetLastError());
         RALPB_TRY(colsum_bf16(k.dz, rout, d.cout, d.cout, G + q.b_off, s));
         m->launches += 3;
