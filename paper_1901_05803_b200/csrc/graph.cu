@@ -270,6 +270,63 @@ __device__ __forceinline__ int win_count(int o, int st, int p, int k, int extent
   return hi - lo;
 }
 
+// The 3x3 / stride-1 / pad-1 average pool of the Inception groups (the output grid is the input
+// grid): a window's in-image count is (3 - [y at an edge]) x (3 - [x at an edge]), its inverse from a
+// table -- no per-tap window arithmetic.  y (+)= / dx (+)= as the general kernels.
+__constant__ float kInvCount[10] = {0.f, 1.f, 1.f / 2, 1.f / 3, 1.f / 4, 1.f / 5, 1.f / 6, 1.f / 7, 1.f / 8, 1.f / 9};
+__device__ __forceinline__ int span3(int v, int n) { return 3 - (v == 0) - (v == n - 1); }
+
+__global__ void avgpool3_fwd_kernel(const bf16* __restrict__ x, int ldx, int n, int h, int w, int c,
+                                    bf16* __restrict__ y, int ldy) {
+  const int groups = c >> 3;
+  const int total = n * h * w * groups;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const Pix q(i, groups, h, w);
+    float a[8] = {0.f};
+    const int y0 = max(q.y - 1, 0), y1 = min(q.y + 1, h - 1), x0 = max(q.x - 1, 0), x1 = min(q.x + 1, w - 1);
+    for (int iy = y0; iy <= y1; ++iy)
+      for (int ix = x0; ix <= x1; ++ix) {
+        float v[8];
+        load8(x + (static_cast<long long>(q.img * h + iy) * w + ix) * ldx + q.g * 8, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] += v[j];
+      }
+    const float inv = kInvCount[span3(q.y, h) * span3(q.x, w)];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] *= inv;
+    store8(y + static_cast<long long>(q.p) * ldy + q.g * 8, a);
+  }
+}
+
+__global__ void avgpool3_bwd_kernel(const bf16* __restrict__ dy, int ldy, int n, int h, int w, int c,
+                                    bf16* __restrict__ dx, int ldx, int acc) {
+  const int groups = c >> 3;
+  const int total = n * h * w * groups;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const Pix q(i, groups, h, w);
+    float a[8];
+    bf16* dst = dx + static_cast<long long>(q.p) * ldx + q.g * 8;
+    if (acc) {
+      load8(dst, a);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = 0.f;
+    }
+    const int y0 = max(q.y - 1, 0), y1 = min(q.y + 1, h - 1), x0 = max(q.x - 1, 0), x1 = min(q.x + 1, w - 1);
+    for (int oy = y0; oy <= y1; ++oy) {
+      const int sy = span3(oy, h);
+      for (int ox = x0; ox <= x1; ++ox) {
+        const float inv = kInvCount[sy * span3(ox, w)];
+        float v[8];
+        load8(dy + (static_cast<long long>(q.img * h + oy) * w + ox) * ldy + q.g * 8, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] += v[j] * inv;
+      }
+    }
+    store8(dst, a);
+  }
+}
+
 __global__ void avgpool_gen_fwd_kernel(const bf16* __restrict__ x, int ldx, int n, int h, int w, int c, int kh, int kw,
                                        int st, int ph, int pw, int ho, int wo, bf16* __restrict__ y, int ldy) {
   const int groups = c >> 3;
@@ -681,8 +738,11 @@ int module_forward(Model* m, ModuleBufs& k, const bf16* x, bf16* y, std::string*
       ++m->launches;
     } else {
       const long long total = rout * (q.cin / 8);
-      avgpool_gen_fwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride,
-                                                                  d.pad_h, d.pad_w, q.ho, q.wo, dst, ldd);
+      if (d.kh == 3 && d.kw == 3 && d.stride == 1 && d.pad_h == 1 && d.pad_w == 1 && q.h > 1 && q.w > 1)
+        avgpool3_fwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, dst, ldd);
+      else
+        avgpool_gen_fwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, d.kh, d.kw,
+                                                                    d.stride, d.pad_h, d.pad_w, q.ho, q.wo, dst, ldd);
       RALPB_TRY(cudaGetLastError());
       ++m->launches;
     }
@@ -803,6 +863,13 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
         kern<<<gr, 256, 0, s>>>(q.idx, g_out, ldo, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride, d.pad_h, d.pad_w, q.ho,
                                 q.wo, g_in, lds, acc);
       } else {
+        if (d.kh == 3 && d.kw == 3 && s1 && d.pad_h == 1 && d.pad_w == 1 && q.h > 1 && q.w > 1) {
+          avgpool3_bwd_kernel<<<gr, 256, 0, s>>>(g_out, ldo, k.n, q.h, q.w, q.cin, g_in, lds, acc);
+          RALPB_TRY(cudaGetLastError());
+          ++m->launches;
+          st = 1;
+          continue;
+        }
         auto kern = s1 ? avgpool_gen_bwd_kernel<true> : avgpool_gen_bwd_kernel<false>;
         kern<<<gr, 256, 0, s>>>(g_out, ldo, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride, d.pad_h, d.pad_w, q.ho, q.wo,
                                 g_in, lds, acc);
