@@ -63,12 +63,27 @@ struct ModNode {
   uint8_t* idx = nullptr;             // max pool: window position of the first max (255: not > 0)
   float* stats = nullptr;             // bn conv: [2][cout] mean / rstd
   uint8_t* mask = nullptr;            // bn conv: ReLU mask bits of its output [rows][cout/8]
+  int grp = -1, grp_col = 0;          // sibling group (ModGroup) and this node's first column in it
   long long K() const { return static_cast<long long>(d.kh) * d.kw * cin; }
+};
+// Sibling 1x1 convolutions (batch-normalised, same input): one GEMM over the concatenated
+// filters [ncat][cin] (their parameters are laid out back to back), one statistics pass over the
+// concatenated pre-activations, one backward-filter and one backward-data GEMM over the
+// concatenated gradient (the sum over the siblings' input gradients falls out of the contraction).
+struct ModGroup {
+  std::vector<int> members;           // node indices, ascending
+  int ncat = 0;                       // sum of the members' output channels
+  long long w_off = -1;               // the members' filters, contiguous [ncat][cin]
+  __nv_bfloat16* wbf = nullptr;       // bf16 copy
+  __nv_bfloat16* z = nullptr;         // pre-batch-norm outputs [rows][ncat]
+  __nv_bfloat16* dz = nullptr;        // gradient w.r.t. them [rows][ncat]
+  float* stats = nullptr;             // [groups][2][ncat] mean / rstd
 };
 struct ModuleBufs {
   int n = 0, h = 0, w = 0, cin = 0, ho = 0, wo = 0, cout = 0;
   int groups = 1;                 // batch-norm statistics per image group (see BlockBufs)
   std::vector<ModNode> nodes;
+  std::vector<ModGroup> sib;      // sibling 1x1 groups (RALPB_MODULE_FUSE=0: none)
   __nv_bfloat16* col = nullptr;   // im2col patches / their gradient (largest conv node)
   __nv_bfloat16* dz = nullptr;    // gradient w.r.t. a conv node's pre-activation (largest node)
   long long col_elems = 0, dz_elems = 0;

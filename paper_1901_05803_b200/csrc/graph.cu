@@ -283,9 +283,13 @@ __global__ void avgpool3_fwd_kernel(const bf16* __restrict__ x, int ldx, int n, 
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const Pix q(i, groups, h, w);
     float a[8] = {0.f};
-    const int y0 = max(q.y - 1, 0), y1 = min(q.y + 1, h - 1), x0 = max(q.x - 1, 0), x1 = min(q.x + 1, w - 1);
-    for (int iy = y0; iy <= y1; ++iy)
-      for (int ix = x0; ix <= x1; ++ix) {
+    // fully unrolled, predicated window: all nine loads are in flight together
+#pragma unroll
+    for (int ry = -1; ry <= 1; ++ry)
+#pragma unroll
+      for (int rx = -1; rx <= 1; ++rx) {
+        const int iy = q.y + ry, ix = q.x + rx;
+        if (iy < 0 || iy >= h || ix < 0 || ix >= w) continue;
         float v[8];
         load8(x + (static_cast<long long>(q.img * h + iy) * w + ix) * ldx + q.g * 8, v);
 #pragma unroll
@@ -312,17 +316,18 @@ __global__ void avgpool3_bwd_kernel(const bf16* __restrict__ dy, int ldy, int n,
 #pragma unroll
       for (int j = 0; j < 8; ++j) a[j] = 0.f;
     }
-    const int y0 = max(q.y - 1, 0), y1 = min(q.y + 1, h - 1), x0 = max(q.x - 1, 0), x1 = min(q.x + 1, w - 1);
-    for (int oy = y0; oy <= y1; ++oy) {
-      const int sy = span3(oy, h);
-      for (int ox = x0; ox <= x1; ++ox) {
-        const float inv = kInvCount[sy * span3(ox, w)];
+#pragma unroll
+    for (int ry = -1; ry <= 1; ++ry)
+#pragma unroll
+      for (int rx = -1; rx <= 1; ++rx) {
+        const int oy = q.y + ry, ox = q.x + rx;
+        if (oy < 0 || oy >= h || ox < 0 || ox >= w) continue;
+        const float inv = kInvCount[span3(oy, h) * span3(ox, w)];
         float v[8];
         load8(dy + (static_cast<long long>(q.img * h + oy) * w + ox) * ldy + q.g * 8, v);
 #pragma unroll
         for (int j = 0; j < 8; ++j) a[j] += v[j] * inv;
       }
-    }
     store8(dst, a);
   }
 }
@@ -430,7 +435,7 @@ __global__ void unpad_kernel(const bf16* __restrict__ src, int n, int h, int w, 
 
 // dz[p][c] = dy[p*ldy + c] * (y[p*ldy2 + c] > 0)  (the ReLU of a bias convolution)
 __global__ void relu_grad_kernel(const bf16* __restrict__ dy, int ldy, const bf16* __restrict__ y, int ldyv, long long pixels,
-                                 int c, bf16* __restrict__ dz) {
+                                 int c, bf16* __restrict__ dz, int ldz) {
   const int groups = c >> 3;
   const long long total = pixels * groups;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -442,7 +447,7 @@ __global__ void relu_grad_kernel(const bf16* __restrict__ dy, int ldy, const bf1
     load8(y + p * ldyv + g * 8, v);
 #pragma unroll
     for (int j = 0; j < 8; ++j) if (!(v[j] > 0.f)) d[j] = 0.f;
-    store8(dz + p * c + g * 8, d);
+    store8(dz + p * ldz + g * 8, d);
   }
 }
 
@@ -517,6 +522,15 @@ int implicit_align() {
   return a;
 }
 
+// RALPB_MODULE_FUSE=0: sibling 1x1 convolutions run as separate GEMMs (the A/B baseline)
+bool module_fuse() {
+  static const bool on = [] {
+    const char* e = getenv("RALPB_MODULE_FUSE");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
 template <class T>
 T* galloc_zero(Model* m, size_t count, std::string* why) {
   T* p = galloc<T>(m, count, why);
@@ -577,14 +591,6 @@ int module_build(ModuleBufs& k, const ralpb_node_desc* nodes, int n_nodes, int n
                100LL * (q.h + 2 * kp) * (q.w + 2 * kp) <= 135LL * q.ho * q.wo;
       q.p = q.same ? kp : 0;
       q.crop = q.same && valid ? kp : 0;
-      q.w_off = *off;
-      *off = al4(*off + static_cast<long long>(d.cout) * q.K());
-      q.b_off = *off;
-      const long long nb = d.bn ? 2LL * d.cout : d.cout;
-      *off = al4(*off + nb);
-      runs->emplace_back(q.w_off, static_cast<long long>(d.cout) * q.K());
-      runs->emplace_back(q.b_off, nb);
-      *count += static_cast<long long>(d.cout) * q.K() + nb;
     } else if (d.op != RALPB_NODE_MAXPOOL && d.op != RALPB_NODE_AVGPOOL) {
       *why = tag + "unknown op";
       return 1;
@@ -602,6 +608,50 @@ int module_build(ModuleBufs& k, const ralpb_node_desc* nodes, int n_nodes, int n
   }
   if (cout == 0) { *why = "module without output nodes"; return 1; }
   k.ho = ho; k.wo = wo; k.cout = cout;
+  // sibling 1x1 groups: batch-normalised direct convs reading the same tensor
+  k.sib.clear();
+  if (module_fuse()) {
+    for (int j = 0; j < n_nodes; ++j) {
+      ModNode& q = k.nodes[j];
+      if (q.d.op != RALPB_NODE_CONV || !q.direct || q.grp >= 0) continue;
+      ModGroup g;
+      for (int i = j; i < n_nodes; ++i) {
+        ModNode& r = k.nodes[i];
+        if (r.d.op == RALPB_NODE_CONV && r.direct && r.d.bn == q.d.bn && r.grp < 0 && r.d.input == q.d.input &&
+            g.ncat + r.d.cout <= 2048)
+          g.members.push_back(i), g.ncat += r.d.cout;
+      }
+      if (g.members.size() < 2) continue;
+      for (int i : g.members) {
+        k.nodes[i].grp = static_cast<int>(k.sib.size());
+        k.nodes[i].grp_col = 0;
+      }
+      int col = 0;
+      for (int i : g.members) k.nodes[i].grp_col = col, col += k.nodes[i].d.cout;
+      k.sib.push_back(std::move(g));
+    }
+  }
+  // parameter offsets, node order; a group's filters back to back at its first member
+  for (int j = 0; j < n_nodes; ++j) {
+    ModNode& q = k.nodes[j];
+    const ralpb_node_desc& d = q.d;
+    if (d.op != RALPB_NODE_CONV) continue;
+    if (q.grp >= 0 && k.sib[q.grp].members[0] == j) {
+      ModGroup& g = k.sib[q.grp];
+      g.w_off = *off;
+      for (int i : g.members) k.nodes[i].w_off = *off + static_cast<long long>(k.nodes[i].grp_col) * q.cin;
+      *off = al4(*off + static_cast<long long>(g.ncat) * q.cin);
+    } else if (q.grp < 0) {
+      q.w_off = *off;
+      *off = al4(*off + static_cast<long long>(d.cout) * q.K());
+    }
+    q.b_off = *off;
+    const long long nb = d.bn ? 2LL * d.cout : d.cout;
+    *off = al4(*off + nb);
+    runs->emplace_back(q.w_off, static_cast<long long>(d.cout) * q.K());
+    runs->emplace_back(q.b_off, nb);
+    *count += static_cast<long long>(d.cout) * q.K() + nb;
+  }
   return 0;
 }
 
@@ -622,6 +672,18 @@ int module_alloc(Model* m, ModuleBufs& k, std::string* why) {
                      !(q.mask = galloc<uint8_t>(m, static_cast<size_t>(rout) * q.d.cout / 8, why))))
         return 1;
       dz = std::max(dz, rout * q.d.cout);
+    } else if (q.d.op == RALPB_NODE_CONV && q.grp >= 0) {
+      ModGroup& g = k.sib[q.grp];
+      if (g.members[0] == &q - k.nodes.data()) {
+        const size_t rz = static_cast<size_t>(rout) * g.ncat;
+        if (!(g.wbf = galloc<bf16>(m, static_cast<size_t>(g.ncat) * q.cin, why)) || !(g.dz = galloc<bf16>(m, rz, why)))
+          return 1;
+        if (q.d.bn && (!(g.z = galloc<bf16>(m, rz, why)) ||
+                       !(g.stats = galloc<float>(m, 2 * static_cast<size_t>(g.ncat) * k.groups, why))))
+          return 1;
+        if (!res_epilogue()) col = std::max(col, static_cast<long long>(k.n) * q.h * q.w * q.cin);   // add-pass path
+      }
+      if (q.d.bn && !(q.mask = galloc<uint8_t>(m, static_cast<size_t>(rout) * q.d.cout / 8, why))) return 1;
     } else if (q.d.op == RALPB_NODE_CONV) {
       if (!(q.wbf = galloc<bf16>(m, static_cast<size_t>(q.d.cout) * q.K(), why))) return 1;
       if (q.d.bn) {
@@ -647,6 +709,10 @@ int module_alloc(Model* m, ModuleBufs& k, std::string* why) {
 }
 
 int module_prep(Model* m, ModuleBufs& k, cudaStream_t s, std::string* why) {
+  for (const ModGroup& g : k.sib) {
+    RALPB_TRY(cast_bf16(m->P + g.w_off, static_cast<long long>(g.ncat) * k.nodes[g.members[0]].cin, g.wbf, s));
+    ++m->launches;
+  }
   for (ModNode& q : k.nodes) {
     if (q.d.op != RALPB_NODE_CONV || q.wbf == nullptr) continue;
     if (q.same)   // [cout][taps][cin] forward copy and the tap-reversed transpose for backward-data
@@ -676,7 +742,33 @@ int module_forward(Model* m, ModuleBufs& k, const bf16* x, bf16* y, std::string*
     const long long rout = static_cast<long long>(k.n) * q.ho * q.wo;
     bf16* dst = d.output ? y + q.out_off : q.y;
     const int ldd = d.output ? k.cout : (d.op == RALPB_NODE_CONV ? d.cout : q.cin);
-    if (d.op == RALPB_NODE_CONV && q.same) {
+    if (d.op == RALPB_NODE_CONV && q.grp >= 0) {
+      const ModGroup& g = k.sib[q.grp];
+      if (!d.bn) {   // bias + ReLU epilogue into this node's destination, filters from the group copy
+        if (gemm_fwd(m, src, rout, q.cin, g.wbf + static_cast<long long>(q.grp_col) * q.cin, d.cout, dst, ldd,
+                     m->P + q.b_off, 1, why))
+          return 1;
+        continue;
+      }
+      if (g.members[0] != &q - k.nodes.data()) continue;   // ran with the group's first member
+      if (gemm_fwd(m, src, rout, q.cin, g.wbf, g.ncat, g.z, g.ncat, nullptr, 0, why)) return 1;
+      RALPB_TRY(bn_stats(Act4{g.z, 0, g.ncat}, k.n, q.ho, q.wo, g.ncat, kBnEps, m->bn_work, g.stats, g.stats + g.ncat, s,
+                         k.groups, 2LL * g.ncat));
+      m->launches += 2;
+      for (int i : g.members) {
+        const ModNode& r = k.nodes[i];
+        BnApply ap{};
+        ap.x = Act4{g.z + r.grp_col, 0, g.ncat};
+        ap.mean = g.stats + r.grp_col; ap.rstd = g.stats + g.ncat + r.grp_col;
+        ap.gamma = m->P + r.b_off; ap.beta = m->P + r.b_off + r.d.cout; ap.relu = 1;
+        ap.y = r.d.output ? MutAct4{y + r.out_off, 0, k.cout} : MutAct4{r.y, 0, r.d.cout};
+        ap.mask_out = r.mask;
+        ap.n = k.n; ap.h = r.ho; ap.w = r.wo; ap.c = r.d.cout;
+        ap.groups = k.groups; ap.stat_stride = 2LL * g.ncat;
+        RALPB_TRY(bn_apply(ap, s));
+        ++m->launches;
+      }
+    } else if (d.op == RALPB_NODE_CONV && q.same) {
       // implicit GEMM over a padded copy of the input (slab / flat kernels of conv.cuh): no patch
       // matrix; the (pre-activation) output lands in the interior of z
       const ConvGeom g{k.n, q.h, q.w, q.cin, d.cout, d.kh, q.p};
@@ -768,7 +860,40 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
     bf16* g_in = d.input < 0 ? dx : k.nodes[d.input].dy;     // gradient w.r.t. its input (may be null)
     char& st = started[d.input + 1];
     const int acc = st ? 1 : 0;
-    if (d.op == RALPB_NODE_CONV && q.same) {
+    if (d.op == RALPB_NODE_CONV && q.grp >= 0) {
+      const ModGroup& g = k.sib[q.grp];
+      if (!d.bn) {   // dz = dy * relu'(y) into the group's gradient columns; bias gradient = column sums
+        const long long total = rout * (d.cout / 8);
+        relu_grad_kernel<<<grid_for(total, 256), 256, 0, s>>>(g_out, ldo, v_out, ldo, rout, d.cout, g.dz + q.grp_col,
+                                                              g.ncat);
+        RALPB_TRY(cudaGetLastError());
+        RALPB_TRY(colsum_bf16(g.dz + q.grp_col, rout, d.cout, g.ncat, G + q.b_off, s));
+        m->launches += 2;
+      } else {
+        BnBackward bb{};
+        bb.dy = Act4{g_out, 0, ldo}; bb.y = Act4{v_out, 0, ldo}; bb.relu_mask = 1; bb.x = Act4{g.z + q.grp_col, 0, g.ncat};
+        bb.mask_in = q.mask;
+        bb.mean = g.stats + q.grp_col; bb.rstd = g.stats + g.ncat + q.grp_col; bb.gamma = P + q.b_off;
+        bb.dgamma = G + q.b_off; bb.dbeta = G + q.b_off + d.cout;
+        bb.dx = MutAct4{g.dz + q.grp_col, 0, g.ncat};
+        bb.n = k.n; bb.h = q.ho; bb.w = q.wo; bb.c = d.cout;
+        bb.groups = k.groups; bb.stat_stride = 2LL * g.ncat;
+        RALPB_TRY(bn_backward(bb, m->bn_work, s));
+        m->launches += 3;
+      }
+      if (g.members[0] != j) continue;   // the group's contractions run once every member's dz is in
+      if (gemm_wgrad(m, g.dz, rout, g.ncat, src, q.cin, G + g.w_off, why)) return 1;
+      if (g_in != nullptr) {
+        if (!acc || res_epilogue()) {
+          if (gemm_dgrad(m, g.dz, rout, g.ncat, g.wbf, q.cin, g_in, why, acc ? g_in : nullptr)) return 1;
+        } else {
+          if (gemm_dgrad(m, g.dz, rout, g.ncat, g.wbf, q.cin, k.col, why)) return 1;
+          RALPB_TRY(add_act(Act4{g_in, 0}, Act4{k.col, 0}, MutAct4{g_in, 0}, k.n, q.h, q.w, q.cin, s));
+          ++m->launches;
+        }
+        st = 1;
+      }
+    } else if (d.op == RALPB_NODE_CONV && q.same) {
       const ConvGeom g{k.n, q.h, q.w, q.cin, d.cout, d.kh, q.p};
       if (d.bn) {   // dz (padded) from the batch-norm backward
         BnBackward bb{};
@@ -783,7 +908,7 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
         m->launches += 3;
       } else {      // dz = dy * relu'(y), then its padded copy; the bias gradient = its column sums
         const long long total = rout * (d.cout / 8);
-        relu_grad_kernel<<<grid_for(total, 256), 256, 0, s>>>(g_out, ldo, v_out, ldo, rout, d.cout, k.dz);
+        relu_grad_kernel<<<grid_for(total, 256), 256, 0, s>>>(g_out, ldo, v_out, ldo, rout, d.cout, k.dz, d.cout);
         RALPB_TRY(cudaGetLastError());
         pad_copy_kernel<<<grid_for(total, 256), 256, 0, s>>>(k.dz, d.cout, k.n, q.ho, q.wo, d.cout, q.p + q.crop, q.dzp);
         RALPB_TRY(cudaGetLastError());
@@ -815,7 +940,7 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
         m->launches += 3;
       } else {
         const long long total = rout * (d.cout / 8);
-        relu_grad_kernel<<<grid_for(total, 256), 256, 0, s>>>(g_out, ldo, v_out, ldo, rout, d.cout, k.dz);
+        relu_grad_kernel<<<grid_for(total, 256), 256, 0, s>>>(g_out, ldo, v_out, ldo, rout, d.cout, k.dz, d.cout);
         RALPB_TRY(cudaGetLastError());
         RALPB_TRY(colsum_bf16(k.dz, rout, d.cout, d.cout, G + q.b_off, s));
         m->launches += 2;

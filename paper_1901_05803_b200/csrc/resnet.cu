@@ -395,6 +395,9 @@ __global__ void maxpool_pad_fwd_kernel(Act4 x, int n, int h, int w, int c, int k
 }
 
 // gather form: thread = (input pixel, 8 channels) sums dy over the windows whose argmax it is
+// KC > 0: compile-time ceil(k / st) (windows covering one input per axis) -- the window
+// loads are unrolled and issued together; KC == 0: runtime loops.
+template <int KC>
 __global__ void maxpool_pad_bwd_kernel(const uint8_t* __restrict__ idx, Act4 dy, int n, int h, int w, int c, int k,
                                        int st, int p, int oh, int ow, MutAct4 dx) {
   const int groups = c >> 3;
@@ -409,21 +412,48 @@ __global__ void maxpool_pad_bwd_kernel(const uint8_t* __restrict__ idx, Act4 dy,
     const int oy_lo = yy >= k ? (yy - k) / st + 1 : 0, oy_hi = min(oh - 1, yy / st);
     const int ox_lo = xx >= k ? (xx - k) / st + 1 : 0, ox_hi = min(ow - 1, xx / st);
     float acc[8] = {0.f};
-    for (int oy = oy_lo; oy <= oy_hi; ++oy)
-      for (int ox = ox_lo; ox <= ox_hi; ++ox) {
-        const int pos = (yy - oy * st) * k + (xx - ox * st);
-        const uint2 ix8 = *reinterpret_cast<const uint2*>(idx + static_cast<long long>((img * oh + oy) * ow + ox) * c + g * 8);
-        const uint8_t* b8 = reinterpret_cast<const uint8_t*>(&ix8);
-        bool any = false;
+    const long long dy_row = static_cast<long long>(ow + 2 * dy.pad);
+    const __nv_bfloat16* dy_img = dy.p + (static_cast<long long>(img * (oh + 2 * dy.pad) + dy.pad) * dy_row + dy.pad) * c + g * 8;
+    const uint8_t* idx_img = idx + static_cast<long long>(img * oh) * ow * c + g * 8;
+    if constexpr (KC > 0) {
+      uint2 ix8[KC][KC];
+      float v[KC][KC][8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) any |= b8[j] == pos;
-        if (!any) continue;
-        float v[8];
-        load8(dy.p + (static_cast<long long>(img * (oh + 2 * dy.pad) + oy + dy.pad) * (ow + 2 * dy.pad) + ox + dy.pad) * c +
-                  g * 8, v);
+      for (int a = 0; a < KC; ++a)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) if (b8[j] == pos) acc[j] += v[j];
-      }
+        for (int b = 0; b < KC; ++b) {
+          const int oy = oy_hi - a, ox = ox_hi - b;
+          ix8[a][b] = make_uint2(0xffffffffu, 0xffffffffu);
+          if (oy >= oy_lo && ox >= ox_lo) {
+            ix8[a][b] = *reinterpret_cast<const uint2*>(idx_img + static_cast<long long>(oy * ow + ox) * c);
+            load8(dy_img + (oy * dy_row + ox) * c, v[a][b]);
+          }
+        }
+#pragma unroll
+      for (int a = 0; a < KC; ++a)
+#pragma unroll
+        for (int b = 0; b < KC; ++b) {
+          const int pos = (yy - (oy_hi - a) * st) * k + (xx - (ox_hi - b) * st);
+          const uint8_t* b8 = reinterpret_cast<const uint8_t*>(&ix8[a][b]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) if (b8[j] == pos) acc[j] += v[a][b][j];
+        }
+    } else {
+      for (int oy = oy_lo; oy <= oy_hi; ++oy)
+        for (int ox = ox_lo; ox <= ox_hi; ++ox) {
+          const int pos = (yy - oy * st) * k + (xx - ox * st);
+          const uint2 ix8 = *reinterpret_cast<const uint2*>(idx_img + static_cast<long long>(oy * ow + ox) * c);
+          const uint8_t* b8 = reinterpret_cast<const uint8_t*>(&ix8);
+          bool any = false;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) any |= b8[j] == pos;
+          if (!any) continue;
+          float v[8];
+          load8(dy_img + (oy * dy_row + ox) * c, v);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) if (b8[j] == pos) acc[j] += v[j];
+        }
+    }
     store8(dx.p + (static_cast<long long>(img * (h + 2 * dx.pad) + y0 + dx.pad) * (w + 2 * dx.pad) + x0 + dx.pad) * c + g * 8,
            acc);
   }
@@ -624,7 +654,10 @@ cudaError_t maxpool_pad_bwd(const uint8_t* idx, Act4 dy, int n, int h, int w, in
                             int ow, MutAct4 dx, cudaStream_t s) {
   const long long total = static_cast<long long>(n) * h * w * (c / 8);
   if (c % 8 != 0 || !fits(total * 8)) return cudaErrorInvalidValue;
-  maxpool_pad_bwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(idx, dy, n, h, w, c, k, st, p, oh, ow, dx);
+  if (k == 3 && st == 2)
+    maxpool_pad_bwd_kernel<2><<<grid_for(total, 256), 256, 0, s>>>(idx, dy, n, h, w, c, k, st, p, oh, ow, dx);
+  else
+    maxpool_pad_bwd_kernel<0><<<grid_for(total, 256), 256, 0, s>>>(idx, dy, n, h, w, c, k, st, p, oh, ow, dx);
   return cudaGetLastError();
 }
 
