@@ -525,21 +525,55 @@ __global__ void maxpool_bwd_gather_kernel(const uint8_t* __restrict__ idx, const
     float g[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const int oy0 = iy - k + 1 > 0 ? (iy - k + st) / st : 0;
     const int ox0 = ix - k + 1 > 0 ? (ix - k + st) / st : 0;
-    for (int oy = oy0; oy <= iy / st && oy < oh; ++oy) {
-      for (int ox = ox0; ox <= ix / st && ox < ow; ++ox) {
-        const int mine = (iy - oy * st) * k + (ix - ox * st);
-        const long long o = (img * oh + oy) * ow + ox;
-        const uint2 iw = *reinterpret_cast<const uint2*>(idx + o * c + cg * 8);
-        const uint8_t* ib = reinterpret_cast<const uint8_t*>(&iw);
-        bool any = false;
+    if constexpr (KC > 0 && STC > 0) {
+      // compile-time window count per axis: every covering window's idx and dy are loaded at once
+      // (the runtime loop serialised a dependent idx -> dy load chain per window)
+      constexpr int NW = (KC + STC - 1) / STC;
+      const int oy_hi = min(iy / st, oh - 1), ox_hi = min(ix / st, ow - 1);
+      uint2 iw[NW][NW];
+      uint4 dv[NW][NW];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) any |= ib[e] == mine;
-        if (!any) continue;
-        const uint4 dv = *reinterpret_cast<const uint4*>(dy + ((img * (oh + 2 * po) + oy + po) * (ow + 2 * po) + ox + po) * c + cg * 8);
-        const __nv_bfloat16* db = reinterpret_cast<const __nv_bfloat16*>(&dv);
+      for (int a = 0; a < NW; ++a)
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (ib[e] == mine) g[e] += __bfloat162float(db[e]);
+        for (int b = 0; b < NW; ++b) {
+          const int oy = oy_hi - a, ox = ox_hi - b;
+          iw[a][b] = make_uint2(0xffffffffu, 0xffffffffu);
+          dv[a][b] = make_uint4(0, 0, 0, 0);
+          if (oy >= oy0 && ox >= ox0) {
+            const long long o = (img * oh + oy) * ow + ox;
+            iw[a][b] = *reinterpret_cast<const uint2*>(idx + o * c + cg * 8);
+            dv[a][b] = *reinterpret_cast<const uint4*>(dy + ((img * (oh + 2 * po) + oy + po) * (ow + 2 * po) + ox + po) * c +
+                                                       cg * 8);
+          }
+        }
+#pragma unroll
+      for (int a = 0; a < NW; ++a)
+#pragma unroll
+        for (int b = 0; b < NW; ++b) {
+          const int mine = (iy - (oy_hi - a) * st) * k + (ix - (ox_hi - b) * st);
+          const uint8_t* ib = reinterpret_cast<const uint8_t*>(&iw[a][b]);
+          const __nv_bfloat16* db = reinterpret_cast<const __nv_bfloat16*>(&dv[a][b]);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (ib[e] == mine) g[e] += __bfloat162float(db[e]);
+        }
+    } else {
+      for (int oy = oy0; oy <= iy / st && oy < oh; ++oy) {
+        for (int ox = ox0; ox <= ix / st && ox < ow; ++ox) {
+          const int mine = (iy - oy * st) * k + (ix - ox * st);
+          const long long o = (img * oh + oy) * ow + ox;
+          const uint2 iw = *reinterpret_cast<const uint2*>(idx + o * c + cg * 8);
+          const uint8_t* ib = reinterpret_cast<const uint8_t*>(&iw);
+          bool any = false;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) any |= ib[e] == mine;
+          if (!any) continue;
+          const uint4 dv = *reinterpret_cast<const uint4*>(dy + ((img * (oh + 2 * po) + oy + po) * (ow + 2 * po) + ox + po) * c + cg * 8);
+          const __nv_bfloat16* db = reinterpret_cast<const __nv_bfloat16*>(&dv);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (ib[e] == mine) g[e] += __bfloat162float(db[e]);
+        }
       }
     }
     uint4 res;
@@ -561,9 +595,12 @@ cudaError_t maxpool_bwd_gather(const uint8_t* idx, const __nv_bfloat16* dy, int 
   const int threads = pool_threads(c);
   const long long work = static_cast<long long>(n) * h * w * (c / 8);
   if (work >= (1LL << 31)) return cudaErrorInvalidValue;
-  // 4 resident blocks per SM: each block flushes c column-sum atomics at its end
+  // with a column sum, 4 resident blocks per SM (each block flushes c atomics at its end); without,
+  // a full SM of threads (RALPB_POOL_GATHER_BLOCKS overrides the per-SM block count)
+  static const int bps = [] { const char* e = getenv("RALPB_POOL_GATHER_BLOCKS"); return e ? atoi(e) : 8; }();
   const int grid = static_cast<int>(std::max<long long>(1, std::min((work + threads - 1) / threads,
-                                                                   static_cast<long long>(num_sms()) * 4)));
+                                                                   static_cast<long long>(num_sms()) *
+                                                                       (colsum != nullptr ? 4 : bps))));
   // idx + dy read, dx written (interior)
   const double bytes = static_cast<double>(n) * c * (static_cast<double>(oh) * ow * 3.0 + static_cast<double>(h) * w * 2.0);
   launch_timed([&] {
