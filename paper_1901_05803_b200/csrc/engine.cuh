@@ -50,6 +50,9 @@ struct ModNode {
   bool same = false;           // conv 3x3 / 5x5, stride 1, "same" padding p, channels % 16: the
   int p = 0;                   // implicit-GEMM conv kernels (conv.cuh) over padded copies
   int crop = 0;                // same, 'valid' node (pad 0): its outputs are the same conv's cropped by p
+  int cpad = 0;                // same: input channels as the implicit kernels see them (cin, or cin
+                               // zero-extended to the channel alignment)
+  float* gw = nullptr;         // same, cpad > cin: the padded filters (fp32, prep) / their gradient
   __nv_bfloat16* xp = nullptr;        // same: the input, padded by p (zero borders)
   __nv_bfloat16* dzp = nullptr;       // same: gradient w.r.t. the pre-activation, padded
   __nv_bfloat16* dxp = nullptr;       // same: gradient w.r.t. the input, padded

@@ -402,27 +402,27 @@ __global__ void avgpool_gen_bwd_kernel(const bf16* __restrict__ dy, int ldy, int
 
 // xp (interior of [n][h+2p][w+2p][c], borders untouched = zero) = x ([n][h][w], pixel stride ldx)
 __global__ void pad_copy_kernel(const bf16* __restrict__ x, int ldx, int n, int h, int w, int c, int pad,
-                                bf16* __restrict__ xp) {
+                                bf16* __restrict__ xp, int ldp) {
   const int groups = c >> 3;
   const int total = n * h * w * groups;
   const int hp = h + 2 * pad, wp = w + 2 * pad;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const Pix q(i, groups, h, w);
-    *reinterpret_cast<uint4*>(xp + (static_cast<long long>(q.img * hp + q.y + pad) * wp + q.x + pad) * c + q.g * 8) =
+    *reinterpret_cast<uint4*>(xp + (static_cast<long long>(q.img * hp + q.y + pad) * wp + q.x + pad) * ldp + q.g * 8) =
         *reinterpret_cast<const uint4*>(x + static_cast<long long>(q.p) * ldx + q.g * 8);
   }
 }
 
 // dst ([n][h][w], pixel stride ldd) (+)= the interior of src ([n][h+2p][w+2p][c])
-__global__ void unpad_kernel(const bf16* __restrict__ src, int n, int h, int w, int c, int pad, bf16* __restrict__ dst,
-                             int ldd, int acc) {
+__global__ void unpad_kernel(const bf16* __restrict__ src, int lds, int n, int h, int w, int c, int pad,
+                             bf16* __restrict__ dst, int ldd, int acc) {
   const int groups = c >> 3;
   const int total = n * h * w * groups;
   const int hp = h + 2 * pad, wp = w + 2 * pad;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const Pix q(i, groups, h, w);
     float a[8], v[8];
-    load8(src + (static_cast<long long>(q.img * hp + q.y + pad) * wp + q.x + pad) * c + q.g * 8, v);
+    load8(src + (static_cast<long long>(q.img * hp + q.y + pad) * wp + q.x + pad) * lds + q.g * 8, v);
     bf16* d = dst + static_cast<long long>(q.p) * ldd + q.g * 8;
     if (acc) {
       load8(d, a);
@@ -430,6 +430,27 @@ __global__ void unpad_kernel(const bf16* __restrict__ src, int n, int h, int w, 
       for (int j = 0; j < 8; ++j) v[j] += a[j];
     }
     store8(d, v);
+  }
+}
+
+// wp[r][cp] = w[r][c] for c < cin, 0 beyond (r = co * taps + t): filters over zero-extended channels
+__global__ void filter_pad_kernel(const float* __restrict__ w, long long rows, int cin, int cpad, float* __restrict__ wp) {
+  const long long total = rows * cpad;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / cpad;
+    const int c = static_cast<int>(i - r * cpad);
+    wp[i] = c < cin ? w[r * cin + c] : 0.f;
+  }
+}
+// g[r][c] += gp[r][c] for c < cin: the padded filter gradient back onto the descriptor's filters
+__global__ void filter_unpad_add_kernel(const float* __restrict__ gp, long long rows, int cin, int cpad, float* __restrict__ g) {
+  const long long total = rows * cin;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / cin;
+    const int c = static_cast<int>(i - r * cin);
+    g[i] += gp[r * cpad + c];
   }
 }
 
@@ -531,6 +552,18 @@ bool module_fuse() {
   return on;
 }
 
+// input channels the implicit path takes: aligned, or (RALPB_MODULE_CPAD_MIN = c > 0) at least c
+// 16-aligned channels, zero-extended to the alignment.  Off by default: measured on Inception-v3,
+// its 80-channel 3x3 (73x73) lands on the flat implicit kernels, slower than im2col (28.6 vs 28.2 ms);
+// 48 (adds the 35x35 groups' 48-channel 5x5s) 27.8 vs 27.9-28.2 ms -- within box noise.
+bool implicit_cin(int c) {
+  static const int lo = [] {
+    const char* e = getenv("RALPB_MODULE_CPAD_MIN");
+    return e != nullptr ? atoi(e) : 0;
+  }();
+  return c % implicit_align() == 0 || (lo > 0 && c % 16 == 0 && c >= lo);
+}
+
 template <class T>
 T* galloc_zero(Model* m, size_t count, std::string* why) {
   T* p = galloc<T>(m, count, why);
@@ -587,9 +620,10 @@ int module_build(ModuleBufs& k, const ralpb_node_desc* nodes, int n_nodes, int n
       const int kp = (d.kh - 1) / 2;
       const bool valid = d.pad_h == 0 && d.pad_w == 0;
       q.same = implicit_same() && d.kh == d.kw && (d.kh == 3 || d.kh == 5) && d.stride == 1 && d.pad_h == d.pad_w &&
-               (d.pad_h == kp || valid) && q.cin % implicit_align() == 0 && d.cout % implicit_align() == 0 &&
+               (d.pad_h == kp || valid) && implicit_cin(q.cin) && d.cout % implicit_align() == 0 &&
                100LL * (q.h + 2 * kp) * (q.w + 2 * kp) <= 135LL * q.ho * q.wo;
       q.p = q.same ? kp : 0;
+      q.cpad = q.same ? (q.cin + implicit_align() - 1) / implicit_align() * implicit_align() : q.cin;
       q.crop = q.same && valid ? kp : 0;
     } else if (d.op != RALPB_NODE_MAXPOOL && d.op != RALPB_NODE_AVGPOOL) {
       *why = tag + "unknown op";
@@ -663,11 +697,12 @@ int module_alloc(Model* m, ModuleBufs& k, std::string* why) {
     if (q.d.op == RALPB_NODE_CONV && q.same) {
       // the padded input copy, (pre-activation) output, and the gradients, all with zero borders
       const size_t pix = static_cast<size_t>(k.n) * (q.h + 2 * q.p) * (q.w + 2 * q.p);
-      if (!(q.wbf = galloc<bf16>(m, static_cast<size_t>(q.d.cout) * q.K(), why)) ||
-          !(q.wdb = galloc<bf16>(m, static_cast<size_t>(q.d.cout) * q.K(), why)) ||
-          !(q.xp = galloc_zero<bf16>(m, pix * q.cin, why)) || !(q.z = galloc_zero<bf16>(m, pix * q.d.cout, why)) ||
-          !(q.dzp = galloc_zero<bf16>(m, pix * q.d.cout, why)) || !(q.dxp = galloc_zero<bf16>(m, pix * q.cin, why)))
+      const size_t wpad = static_cast<size_t>(q.d.cout) * q.d.kh * q.d.kw * q.cpad;
+      if (!(q.wbf = galloc<bf16>(m, wpad, why)) || !(q.wdb = galloc<bf16>(m, wpad, why)) ||
+          !(q.xp = galloc_zero<bf16>(m, pix * q.cpad, why)) || !(q.z = galloc_zero<bf16>(m, pix * q.d.cout, why)) ||
+          !(q.dzp = galloc_zero<bf16>(m, pix * q.d.cout, why)) || !(q.dxp = galloc_zero<bf16>(m, pix * q.cpad, why)))
         return 1;
+      if (q.cpad != q.cin && !(q.gw = galloc<float>(m, wpad, why))) return 1;
       if (q.d.bn && (!(q.stats = galloc<float>(m, 2 * static_cast<size_t>(q.d.cout) * k.groups, why)) ||
                      !(q.mask = galloc<uint8_t>(m, static_cast<size_t>(rout) * q.d.cout / 8, why))))
         return 1;
@@ -715,7 +750,13 @@ int module_prep(Model* m, ModuleBufs& k, cudaStream_t s, std::string* why) {
   }
   for (ModNode& q : k.nodes) {
     if (q.d.op != RALPB_NODE_CONV || q.wbf == nullptr) continue;
-    if (q.same)   // [cout][taps][cin] forward copy and the tap-reversed transpose for backward-data
+    if (q.same && q.cpad != q.cin) {   // via the zero-extended fp32 filters
+      const long long rows = static_cast<long long>(q.d.cout) * q.d.kh * q.d.kw;
+      filter_pad_kernel<<<grid_for(rows * q.cpad, 256), 256, 0, s>>>(m->P + q.w_off, rows, q.cin, q.cpad, q.gw);
+      RALPB_TRY(cudaGetLastError());
+      RALPB_TRY(conv_weight_prep(q.gw, q.d.cout, q.d.kh * q.d.kw, q.cpad, q.wbf, q.wdb, s));
+      ++m->launches;
+    } else if (q.same)   // [cout][taps][cin] forward copy and the tap-reversed transpose for backward-data
       RALPB_TRY(conv_weight_prep(m->P + q.w_off, q.d.cout, q.d.kh * q.d.kw, q.cin, q.wbf, q.wdb, s));
     else
       RALPB_TRY(cast_bf16(m->P + q.w_off, static_cast<long long>(q.d.cout) * q.K(), q.wbf, s));
@@ -771,9 +812,9 @@ int module_forward(Model* m, ModuleBufs& k, const bf16* x, bf16* y, std::string*
     } else if (d.op == RALPB_NODE_CONV && q.same) {
       // implicit GEMM over a padded copy of the input (slab / flat kernels of conv.cuh): no patch
       // matrix; the (pre-activation) output lands in the interior of z
-      const ConvGeom g{k.n, q.h, q.w, q.cin, d.cout, d.kh, q.p};
+      const ConvGeom g{k.n, q.h, q.w, q.cpad, d.cout, d.kh, q.p};
       const long long tin = static_cast<long long>(k.n) * q.h * q.w * (q.cin / 8);
-      pad_copy_kernel<<<grid_for(tin, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, q.p, q.xp);
+      pad_copy_kernel<<<grid_for(tin, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, q.p, q.xp, q.cpad);
       RALPB_TRY(cudaGetLastError());
       RALPB_TRY(conv_fwd(g, q.xp, q.wbf, d.bn ? nullptr : m->P + q.b_off, q.z, d.bn ? 0 : 1, s, why));
       m->launches += 2;
@@ -792,7 +833,7 @@ int module_forward(Model* m, ModuleBufs& k, const bf16* x, bf16* y, std::string*
         m->launches += 3;
       } else {
         const long long tout = rout * (d.cout / 8);
-        unpad_kernel<<<grid_for(tout, 256), 256, 0, s>>>(q.z, k.n, q.ho, q.wo, d.cout, q.p + q.crop, dst, ldd, 0);
+        unpad_kernel<<<grid_for(tout, 256), 256, 0, s>>>(q.z, d.cout, k.n, q.ho, q.wo, d.cout, q.p + q.crop, dst, ldd, 0);
         RALPB_TRY(cudaGetLastError());
         ++m->launches;
       }
@@ -894,7 +935,7 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
         st = 1;
       }
     } else if (d.op == RALPB_NODE_CONV && q.same) {
-      const ConvGeom g{k.n, q.h, q.w, q.cin, d.cout, d.kh, q.p};
+      const ConvGeom g{k.n, q.h, q.w, q.cpad, d.cout, d.kh, q.p};
       if (d.bn) {   // dz (padded) from the batch-norm backward
         BnBackward bb{};
         bb.dy = Act4{g_out, 0, ldo}; bb.y = Act4{v_out, 0, ldo}; bb.relu_mask = 1; bb.x = Act4{q.z, q.p + q.crop};
@@ -910,17 +951,27 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
         const long long total = rout * (d.cout / 8);
         relu_grad_kernel<<<grid_for(total, 256), 256, 0, s>>>(g_out, ldo, v_out, ldo, rout, d.cout, k.dz, d.cout);
         RALPB_TRY(cudaGetLastError());
-        pad_copy_kernel<<<grid_for(total, 256), 256, 0, s>>>(k.dz, d.cout, k.n, q.ho, q.wo, d.cout, q.p + q.crop, q.dzp);
+        pad_copy_kernel<<<grid_for(total, 256), 256, 0, s>>>(k.dz, d.cout, k.n, q.ho, q.wo, d.cout, q.p + q.crop, q.dzp,
+                                                             d.cout);
         RALPB_TRY(cudaGetLastError());
         RALPB_TRY(colsum_bf16(k.dz, rout, d.cout, d.cout, G + q.b_off, s));
         m->launches += 3;
       }
-      RALPB_TRY(conv_wgrad(g, q.xp, q.dzp, G + q.w_off, nullptr, s, why));
-      ++m->launches;
+      if (q.cpad != q.cin) {   // into the padded scratch, then onto the descriptor's filters
+        const long long rows = static_cast<long long>(d.cout) * d.kh * d.kw;
+        RALPB_TRY(cudaMemsetAsync(q.gw, 0, static_cast<size_t>(rows) * q.cpad * sizeof(float), s));
+        RALPB_TRY(conv_wgrad(g, q.xp, q.dzp, q.gw, nullptr, s, why));
+        filter_unpad_add_kernel<<<grid_for(rows * q.cin, 256), 256, 0, s>>>(q.gw, rows, q.cin, q.cpad, G + q.w_off);
+        RALPB_TRY(cudaGetLastError());
+        m->launches += 2;
+      } else {
+        RALPB_TRY(conv_wgrad(g, q.xp, q.dzp, G + q.w_off, nullptr, s, why));
+        ++m->launches;
+      }
       if (g_in != nullptr) {
         RALPB_TRY(conv_dgrad(g, q.dzp, q.wdb, nullptr, q.dxp, nullptr, s, why));
         const long long tin = rin * (q.cin / 8);
-        unpad_kernel<<<grid_for(tin, 256), 256, 0, s>>>(q.dxp, k.n, q.h, q.w, q.cin, q.p, g_in, lds, acc);
+        unpad_kernel<<<grid_for(tin, 256), 256, 0, s>>>(q.dxp, q.cpad, k.n, q.h, q.w, q.cin, q.p, g_in, lds, acc);
         RALPB_TRY(cudaGetLastError());
         m->launches += 2;
         st = 1;
