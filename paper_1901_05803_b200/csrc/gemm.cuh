@@ -90,10 +90,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
 
   const int total = p.n_mt * p.n_nt * p.n_ks;
 
-  if (warp == 0 || warp == 3) {
-    // Two producer warps take alternate k-blocks: a TMA issue keeps its thread busy for
-    // hundreds of cycles (tools/exp_tma.cu), so issuing from two threads doubles the rate.
-    const int pid = warp == 0 ? 0 : 1;
+  if (warp == 0 || warp == 3 || (warp == 2 && p.producers == 3)) {
+    // Producer warps take k-blocks round-robin: a TMA issue keeps its thread busy for
+    // hundreds of cycles (tools/exp_tma.cu), so issuing from two threads doubles the rate.  The
+    // MN-major modes issue one box per swizzle atom (up to 4 + 4 per k-block): there the
+    // TMEM-allocator warp joins as a third producer (backward-filter GEMMs 20-33 % faster at narrow
+    // channels; issuing the atoms lane-parallel from one warp measured slower).
+    const int np = p.producers;
+    const int pid = warp == 0 ? 0 : (warp == 3 ? 1 : 2);
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
@@ -106,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_sm100_kernel(const __grid_co
         int kb0 = ks * p.kblocks_per_split;
         int kb1 = min(kb0 + p.kblocks_per_split, p.kblocks_total);
         for (int kk = kb0; kk < kb1; ++kk, ++seq) {
-          if ((seq & 1) != pid) {
+          if (seq % np != pid) {
             if (++stage == stages) { stage = 0; phase ^= 1; }
             continue;
           }

@@ -157,9 +157,22 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream, std::string* why
   const int stage_bytes = kAStage + p.b_stage_bytes;
   const int staging = p.tma_epi ? 2 * 16384 : 0;
   const int budget = 227 * 1024 - 1024 - 256 - staging;
-  p.stages = std::min(8, budget / stage_bytes);
+  static const int max_stages = [] { const char* e = getenv("RALPB_GEMM_MAX_STAGES"); return e ? atoi(e) : 8; }();
+  p.stages = std::min(max_stages, budget / stage_bytes);
   if (const char* e = getenv("RALPB_STAGES")) p.stages = std::max(1, std::min(p.stages, atoi(e)));
   const int smem = 1024 + p.stages * stage_bytes + staging + 256;
+  // RALPB_GEMM_PRODUCERS=2 keeps two producer warps for the MN-major modes too (A/B)
+  static const int mn_producers = [] {
+    const char* e = getenv("RALPB_GEMM_PRODUCERS");
+    return e != nullptr ? std::max(2, std::min(3, atoi(e))) : 3;
+  }();
+  // RALPB_GEMM_PRODUCERS_K=3: the K-major modes too (Inception / GoogLeNet / ResNet-50 steps
+  // -0.3-0.6 %, the VGG-16 step within noise, -0.3 %: left at 2)
+  static const int k_producers = [] {
+    const char* e = getenv("RALPB_GEMM_PRODUCERS_K");
+    return e != nullptr ? std::max(2, std::min(3, atoi(e))) : 2;
+  }();
+  p.producers = (d.a_mode == LD_MN || d.a_mode == LD_MN_CONV) ? mn_producers : k_producers;
   p.idesc = umma_idesc_bf16(kBM, bn, !a_k, !b_k);
   p.a_mode = d.a_mode;
   p.b_mode = d.b_mode;

@@ -46,6 +46,7 @@ struct alignas(64) GemmParams {
   int block_n;              // BN (32..256)
   int kb;                   // K elements per k-block (K-major); MN-major blocks are 64 rows
   int stages;
+  int producers;            // TMA-issuing warps (2, or 3 for MN-major operands)
   int b_stage_bytes;
   uint32_t idesc;
   int a_mode, b_mode;

@@ -35,7 +35,12 @@ def main():
     ap.add_argument("--layer", type=int, default=-1)
     ap.add_argument("--op", default="all")
     ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--shape", default="", help="h,cin,cout: one extra shape instead of VGG-16's")
     a = ap.parse_args()
+    global LAYERS, REPEATS
+    if a.shape:
+        LAYERS = [tuple(int(v) for v in a.shape.split(","))]
+        REPEATS = [1]
     N = a.n
     tot = {"fwd": 0.0, "dgrad": 0.0, "wgrad": 0.0}
     for li, (h, cin, cout) in enumerate(LAYERS):
@@ -53,7 +58,7 @@ def main():
         res = {}
         if a.op in ("all", "fwd"):
             res["fwd"] = timeit(lambda: ops.conv_fwd(x, w, b, n=N, h=h, w_=h, cin=cin, cout=cout, k=3, pad=1, out=y), a.iters)
-        if a.op in ("all", "dgrad") and li > 0:
+        if a.op in ("all", "dgrad") and (li > 0 or a.shape):
             res["dgrad"] = timeit(lambda: ops.conv_dgrad(dy, wd, x, n=N, h=h, w_=h, cin=cin, cout=cout, k=3, pad=1, out=dx), a.iters)
         if a.op in ("all", "wgrad"):
             res["wgrad"] = timeit(lambda: ops.conv_wgrad(x, dy, n=N, h=h, w_=h, cin=cin, cout=cout, k=3, pad=1, out=dw), a.iters)
