@@ -560,7 +560,10 @@ int model_create(const ralpb_layer_desc* layers, int n_layers, const ralpb_node_
     if (!f.im2col && !(f.wd = alloc<bf16>(m, f.w_count * pm * pm, why))) return fail(*why);
   }
   // branchy layers: the blocks' operands and saved tensors, the stem's pre-batch-norm output
-  if (m->branchy && !(m->bn_work = alloc<float>(m, 2 * 2048, why))) return fail(*why);
+  if (m->branchy) {   // zeroed once: every reduction leaves its accumulators and ticket zero
+    if (!(m->bn_work = alloc<float>(m, kBnWorkFloats, why))) return fail(*why);
+    if (cudaMemset(m->bn_work, 0, kBnWorkFloats * sizeof(float)) != cudaSuccess) return fail("bn scratch memset");
+  }
   for (size_t i = 0; i < m->front.size(); ++i) {
     FrontLayer& f = m->front[i];
     const bool mine = static_cast<int>(i) < m->split ? m->is_worker : (m->bseg && m->holds_back);

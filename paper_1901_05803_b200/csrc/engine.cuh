@@ -154,7 +154,7 @@ struct Model {
   std::vector<BlockBufs> blocks;   // RALPB_BLOCK layers
   std::vector<ModuleBufs> modules; // RALPB_MODULE layers
   bool branchy = false;            // the model has blocks / batch-normalised convolutions
-  float* bn_work = nullptr;        // [2][2048] batch-norm reduction scratch
+  float* bn_work = nullptr;        // kBnWorkFloats batch-norm reduction scratch (resnet.cuh)
   std::vector<FcLayer> back;
   std::vector<ActBuf> acts;        // acts[i] = input of front layer i; acts.back() = cut (local)
   int in_h = 0, in_w = 0, in_c = 0, in_cp = 0;

@@ -70,7 +70,22 @@ struct Lane {
 // ------------------------------------------------------------------ batch norm statistics
 constexpr int kU = 4;   // pixels in flight per thread in the reductions
 
-__global__ void __launch_bounds__(256) bn_stats_kernel(Act4 x, int pixels, int h, int w, int c, float* __restrict__ sums) {
+// The reduction's last block (a ticket after every block's flush) turns the sums into the result
+// and zeroes the accumulators for the next reduction: no memset, no separate finishing launch.
+__device__ __forceinline__ unsigned* bn_ticket(float* work) { return reinterpret_cast<unsigned*>(work + 4 * 2048); }
+__device__ __forceinline__ bool bn_last_block(float* work) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(bn_ticket(work), 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+__global__ void __launch_bounds__(256) bn_stats_kernel(Act4 x, int pixels, int h, int w, int c, float* __restrict__ sums,
+                                                       float inv_m, float eps, float* __restrict__ mean,
+                                                       float* __restrict__ rstd) {
   extern __shared__ float sh[];  // [2][c]
   const Lane L(c);
   for (int i = threadIdx.x; i < 2 * c; i += blockDim.x) sh[i] = 0.f;
@@ -102,16 +117,16 @@ __global__ void __launch_bounds__(256) bn_stats_kernel(Act4 x, int pixels, int h
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 2 * c; i += blockDim.x) atomicAdd(sums + i, sh[i]);
-}
-
-__global__ void bn_finish_kernel(const float* __restrict__ sums, int c, float inv_m, float eps, float* __restrict__ mean,
-                                 float* __restrict__ rstd) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= c) return;
-  const float m = sums[i] * inv_m;
-  const float var = fmaxf(sums[c + i] * inv_m - m * m, 0.f);
-  mean[i] = m;
-  rstd[i] = rsqrtf(var + eps);
+  if (!bn_last_block(sums)) return;
+  for (int i = threadIdx.x; i < c; i += blockDim.x) {
+    const float m = __ldcg(sums + i) * inv_m;
+    const float var = fmaxf(__ldcg(sums + c + i) * inv_m - m * m, 0.f);
+    mean[i] = m;
+    rstd[i] = rsqrtf(var + eps);
+    sums[i] = 0.f;
+    sums[c + i] = 0.f;
+  }
+  if (threadIdx.x == 0) *bn_ticket(sums) = 0u;
 }
 
 // ------------------------------------------------------------------ apply
@@ -167,6 +182,8 @@ __global__ void __launch_bounds__(256, 3) bn_apply_kernel(BnApply a, int pixels)
 
 // ------------------------------------------------------------------ backward
 // sums: [0, c) sum dz;  [c, 2c) sum dz * (x - mean)   (times rstd in bn_bwd_params / apply)
+// The last block scales sum dz (x - mean) by rstd (-> sum dz * xhat), adds dbeta / dgamma, and
+// leaves the finished pair at sums + 2 * 2048 for the apply pass.
 template <bool BITS>   // BITS: the ReLU mask from mask_in bits (else from y)
 __global__ void __launch_bounds__(256, 3) bn_bwd_reduce_kernel(BnBackward b, int pixels, float* __restrict__ sums) {
   extern __shared__ float sh[];  // [2][c]
@@ -215,15 +232,19 @@ __global__ void __launch_bounds__(256, 3) bn_bwd_reduce_kernel(BnBackward b, int
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 2 * c; i += blockDim.x) atomicAdd(sums + i, sh[i]);
-}
-
-__global__ void bn_bwd_params_kernel(float* __restrict__ sums, const float* __restrict__ rstd, int c,
-                                     float* __restrict__ dgamma, float* __restrict__ dbeta) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= c) return;
-  sums[c + i] *= rstd[i];   // -> sum dz * xhat
-  dbeta[i] += sums[i];
-  dgamma[i] += sums[c + i];
+  if (!bn_last_block(sums)) return;
+  float* fin = sums + 2 * 2048;
+  for (int i = threadIdx.x; i < c; i += blockDim.x) {
+    const float sd = __ldcg(sums + i);
+    const float sx = __ldcg(sums + c + i) * b.rstd[i];   // -> sum dz * xhat
+    fin[i] = sd;
+    fin[c + i] = sx;
+    b.dbeta[i] += sd;
+    b.dgamma[i] += sx;
+    sums[i] = 0.f;
+    sums[c + i] = 0.f;
+  }
+  if (threadIdx.x == 0) *bn_ticket(sums) = 0u;
 }
 
 // dx = A * dz + (x - mean) * B + C,  A = gamma * rstd, B = -A * rstd * sum(dz xhat) / M,
@@ -499,7 +520,8 @@ int stats_grid(K kernel, size_t smem, long long pixels, int lanes) {
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem) != cudaSuccess || per_sm < 1) per_sm = 1;
   const long long want = static_cast<long long>(num_sms()) * per_sm;
-  return static_cast<int>(std::max<long long>(1, std::min(want, (pixels + lanes - 1) / lanes)));
+  // >= 16 pixels per lane: every block flushes 2c global atomics, which dominate small tensors
+  return static_cast<int>(std::max<long long>(1, std::min(want, (pixels + 16LL * lanes - 1) / (16LL * lanes))));
 }
 int pixel_grid(long long pixels, int lanes) {
   const long long want = static_cast<long long>(num_sms()) * 8;
@@ -530,12 +552,9 @@ cudaError_t bn_stats(Act4 x, int n, int h, int w, int c, float eps, float* work,
   }
   const long long pixels = static_cast<long long>(n) * h * w;
   if (c % 8 != 0 || c / 8 > 256 || !fits(pixels * c)) return cudaErrorInvalidValue;
-  cudaError_t e = cudaMemsetAsync(work, 0, sizeof(float) * 2 * c, s);
-  if (e != cudaSuccess) return e;
   const int lanes = 256 / (c / 8);
-  bn_stats_kernel<<<stats_grid(bn_stats_kernel, sizeof(float) * 2 * c, pixels, lanes), 256, sizeof(float) * 2 * c, s>>>(x, static_cast<int>(pixels), h, w, c,
-                                                                                 work);
-  bn_finish_kernel<<<(c + 255) / 256, 256, 0, s>>>(work, c, 1.f / static_cast<float>(pixels), eps, mean, rstd);
+  bn_stats_kernel<<<stats_grid(bn_stats_kernel, sizeof(float) * 2 * c, pixels, lanes), 256, sizeof(float) * 2 * c, s>>>(
+      x, static_cast<int>(pixels), h, w, c, work, 1.f / static_cast<float>(pixels), eps, mean, rstd);
   return cudaGetLastError();
 }
 
@@ -589,8 +608,6 @@ cudaError_t bn_backward(const BnBackward& b, float* work, cudaStream_t s) {
   }
   const long long pixels = static_cast<long long>(b.n) * b.h * b.w;
   if (b.c % 8 != 0 || b.c / 8 > 256 || !fits(pixels * b.c)) return cudaErrorInvalidValue;
-  cudaError_t e = cudaMemsetAsync(work, 0, sizeof(float) * 2 * b.c, s);
-  if (e != cudaSuccess) return e;
   const int lanes = 256 / (b.c / 8);
   if (b.mask_in != nullptr)
     bn_bwd_reduce_kernel<true><<<stats_grid(bn_bwd_reduce_kernel<true>, sizeof(float) * 2 * b.c, pixels, lanes), 256,
@@ -598,8 +615,7 @@ cudaError_t bn_backward(const BnBackward& b, float* work, cudaStream_t s) {
   else
     bn_bwd_reduce_kernel<false><<<stats_grid(bn_bwd_reduce_kernel<false>, sizeof(float) * 2 * b.c, pixels, lanes), 256,
                                   sizeof(float) * 2 * b.c, s>>>(b, static_cast<int>(pixels), work);
-  bn_bwd_params_kernel<<<(b.c + 255) / 256, 256, 0, s>>>(work, b.rstd, b.c, b.dgamma, b.dbeta);
-  bn_bwd_apply_kernel<<<pixel_grid(pixels, lanes), 256, 0, s>>>(b, static_cast<int>(pixels), work,
+  bn_bwd_apply_kernel<<<pixel_grid(pixels, lanes), 256, 0, s>>>(b, static_cast<int>(pixels), work + 2 * 2048,
                                                                 1.f / static_cast<float>(pixels));
   return cudaGetLastError();
 }

@@ -25,11 +25,13 @@ struct MutAct4 {
 };
 
 // Batch statistics over the n*h*w interior pixels: mean[c], rstd[c] = 1/sqrt(var + eps) (biased
-// variance, training mode; torch.nn.functional.batch_norm(training=True)).  `work` is fp32 [2c]
-// scratch (zeroed here).
+// variance, training mode; torch.nn.functional.batch_norm(training=True)).  `work` is the
+// kBnWorkFloats scratch (zeroed once at allocation): [2][2048] accumulators the reduction's last
+// block finishes and zeroes again, [2][2048] finished sums (backward), a block ticket.
 // groups > 1: the n images form `groups` equal consecutive groups, each normalised with its own
 // statistics (mean / rstd of group g at + g * stat_stride): per-worker batch statistics for layers
 // the PS runs over every worker's gathered rows.
+constexpr int kBnWorkFloats = 4 * 2048 + 64;
 cudaError_t bn_stats(Act4 x, int n, int h, int w, int c, float eps, float* work, float* mean, float* rstd,
                      cudaStream_t s, int groups = 1, long long stat_stride = 0);
 
