@@ -745,6 +745,7 @@ int module_alloc(Model* m, ModuleBufs& k, std::string* why) {
 
 int module_prep(Model* m, ModuleBufs& k, cudaStream_t s, std::string* why) {
   for (const ModGroup& g : k.sib) {
+    if (g.wbf == nullptr) continue;   // a layer this rank does not run (not allocated)
     RALPB_TRY(cast_bf16(m->P + g.w_off, static_cast<long long>(g.ncat) * k.nodes[g.members[0]].cin, g.wbf, s));
     ++m->launches;
   }
