@@ -433,6 +433,56 @@ __global__ void unpad_kernel(const bf16* __restrict__ src, int lds, int n, int h
   }
 }
 
+// dz = dy * relu'(y) over [n][h][w][c] (dy / y at pixel strides ldy / ldyv), stored bf16 at pixel
+// stride ldz -- into the interior of a buffer padded by `pad` when pad > 0 (the implicit convs'
+// layout) -- and, with db, the bias gradient db[c] += sum of the stored dz (block partial sums in
+// shared memory, one global atomic per channel per block): the relu-grad, pad-copy and column-sum
+// passes of a bias convolution in one.  blockDim must be a multiple of c / 8.
+__global__ void relu_grad_colsum_kernel(const bf16* __restrict__ dy, int ldy, const bf16* __restrict__ y, int ldyv,
+                                        int n, int h, int w, int c, bf16* __restrict__ dz, int ldz, int pad,
+                                        float* __restrict__ db) {
+  __shared__ float s_col[2048];
+  const int groups = c >> 3;
+  const int total = n * h * w * groups;
+  float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const Pix q(i, groups, h, w);
+    float d[8], v[8];
+    load8(dy + static_cast<long long>(q.p) * ldy + q.g * 8, d);
+    load8(y + static_cast<long long>(q.p) * ldyv + q.g * 8, v);
+    uint4 u;
+    bf16* b = reinterpret_cast<bf16*>(&u);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      b[j] = __float2bfloat16_rn(v[j] > 0.f ? d[j] : 0.f);
+      cs[j] += __bfloat162float(b[j]);
+    }
+    const long long o = pad > 0 ? (static_cast<long long>(q.img * (h + 2 * pad) + q.y + pad) * (w + 2 * pad) + q.x + pad)
+                                : static_cast<long long>(q.p);
+    *reinterpret_cast<uint4*>(dz + o * ldz + q.g * 8) = u;
+  }
+  if (db == nullptr) return;
+  for (int i = threadIdx.x; i < c; i += blockDim.x) s_col[i] = 0.f;
+  __syncthreads();
+  const int g = threadIdx.x % groups;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) atomicAdd(&s_col[g * 8 + j], cs[j]);
+  __syncthreads();
+  for (int i = threadIdx.x; i < c; i += blockDim.x) atomicAdd(db + i, s_col[i]);
+}
+
+cudaError_t relu_grad_colsum(const bf16* dy, int ldy, const bf16* y, int ldyv, int n, int h, int w, int c, bf16* dz,
+                             int ldz, int pad, float* db, cudaStream_t s) {
+  const int groups = c / 8;
+  if (c % 8 != 0 || groups > 256 || static_cast<long long>(n) * h * w * groups >= (1LL << 31)) return cudaErrorInvalidValue;
+  const int threads = (256 / groups) * groups;
+  const long long total = static_cast<long long>(n) * h * w * groups;
+  const int grid = static_cast<int>(std::max<long long>(1, std::min((total + threads - 1) / threads,
+                                                                   static_cast<long long>(num_sms()) * 4)));
+  relu_grad_colsum_kernel<<<grid, threads, 0, s>>>(dy, ldy, y, ldyv, n, h, w, c, dz, ldz, pad, db);
+  return cudaGetLastError();
+}
+
 // wp[r][cp] = w[r][c] for c < cin, 0 beyond (r = co * taps + t): filters over zero-extended channels
 __global__ void filter_pad_kernel(const float* __restrict__ w, long long rows, int cin, int cpad, float* __restrict__ wp) {
   const long long total = rows * cpad;
@@ -451,24 +501,6 @@ __global__ void filter_unpad_add_kernel(const float* __restrict__ gp, long long 
     const long long r = i / cin;
     const int c = static_cast<int>(i - r * cin);
     g[i] += gp[r * cpad + c];
-  }
-}
-
-// dz[p][c] = dy[p*ldy + c] * (y[p*ldy2 + c] > 0)  (the ReLU of a bias convolution)
-__global__ void relu_grad_kernel(const bf16* __restrict__ dy, int ldy, const bf16* __restrict__ y, int ldyv, long long pixels,
-                                 int c, bf16* __restrict__ dz, int ldz) {
-  const int groups = c >> 3;
-  const long long total = pixels * groups;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long p = i / groups;
-    const int g = static_cast<int>(i - p * groups);
-    float d[8], v[8];
-    load8(dy + p * ldy + g * 8, d);
-    load8(y + p * ldyv + g * 8, v);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) if (!(v[j] > 0.f)) d[j] = 0.f;
-    store8(dz + p * ldz + g * 8, d);
   }
 }
 
@@ -905,12 +937,9 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
     if (d.op == RALPB_NODE_CONV && q.grp >= 0) {
       const ModGroup& g = k.sib[q.grp];
       if (!d.bn) {   // dz = dy * relu'(y) into the group's gradient columns; bias gradient = column sums
-        const long long total = rout * (d.cout / 8);
-        relu_grad_kernel<<<grid_for(total, 256), 256, 0, s>>>(g_out, ldo, v_out, ldo, rout, d.cout, g.dz + q.grp_col,
-                                                              g.ncat);
-        RALPB_TRY(cudaGetLastError());
-        RALPB_TRY(colsum_bf16(g.dz + q.grp_col, rout, d.cout, g.ncat, G + q.b_off, s));
-        m->launches += 2;
+        RALPB_TRY(relu_grad_colsum(g_out, ldo, v_out, ldo, k.n, q.ho, q.wo, d.cout, g.dz + q.grp_col, g.ncat, 0,
+                                   G + q.b_off, s));
+        ++m->launches;
       } else {
         BnBackward bb{};
         bb.dy = Act4{g_out, 0, ldo}; bb.y = Act4{v_out, 0, ldo}; bb.relu_mask = 1; bb.x = Act4{g.z + q.grp_col, 0, g.ncat};
@@ -948,15 +977,10 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
         bb.groups = k.groups; bb.stat_stride = 2LL * d.cout;
         RALPB_TRY(bn_backward(bb, m->bn_work, s));
         m->launches += 3;
-      } else {      // dz = dy * relu'(y), then its padded copy; the bias gradient = its column sums
-        const long long total = rout * (d.cout / 8);
-        relu_grad_kernel<<<grid_for(total, 256), 256, 0, s>>>(g_out, ldo, v_out, ldo, rout, d.cout, k.dz, d.cout);
-        RALPB_TRY(cudaGetLastError());
-        pad_copy_kernel<<<grid_for(total, 256), 256, 0, s>>>(k.dz, d.cout, k.n, q.ho, q.wo, d.cout, q.p + q.crop, q.dzp,
-                                                             d.cout);
-        RALPB_TRY(cudaGetLastError());
-        RALPB_TRY(colsum_bf16(k.dz, rout, d.cout, d.cout, G + q.b_off, s));
-        m->launches += 3;
+      } else {      // dz = dy * relu'(y) straight into the padded buffer; bias gradient = its column sums
+        RALPB_TRY(relu_grad_colsum(g_out, ldo, v_out, ldo, k.n, q.ho, q.wo, d.cout, q.dzp, d.cout, q.p + q.crop,
+                                   G + q.b_off, s));
+        ++m->launches;
       }
       if (q.cpad != q.cin) {   // into the padded scratch, then onto the descriptor's filters
         const long long rows = static_cast<long long>(d.cout) * d.kh * d.kw;
@@ -991,11 +1015,8 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
         RALPB_TRY(bn_backward(bb, m->bn_work, s));
         m->launches += 3;
       } else {
-        const long long total = rout * (d.cout / 8);
-        relu_grad_kernel<<<grid_for(total, 256), 256, 0, s>>>(g_out, ldo, v_out, ldo, rout, d.cout, k.dz, d.cout);
-        RALPB_TRY(cudaGetLastError());
-        RALPB_TRY(colsum_bf16(k.dz, rout, d.cout, d.cout, G + q.b_off, s));
-        m->launches += 2;
+        RALPB_TRY(relu_grad_colsum(g_out, ldo, v_out, ldo, k.n, q.ho, q.wo, d.cout, k.dz, d.cout, 0, G + q.b_off, s));
+        ++m->launches;
       }
       // backward-filter
       if (q.direct) {
