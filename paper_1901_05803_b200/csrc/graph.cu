@@ -181,9 +181,11 @@ __global__ void col2im_gen_kernel(const bf16* __restrict__ dcol, int n, int h, i
 // ------------------------------------------------------------------ pools
 // thread = (output pixel, 8 channels); idx [n*ho*wo][c] (pixel stride c) = ky*kw + kx of the first
 // max, 255 where the max is not > 0 (its producer's ReLU passes no gradient there)
-__global__ void maxpool_gen_fwd_kernel(const bf16* __restrict__ x, int ldx, int n, int h, int w, int c, int kh, int kw,
+template <int KC>   // KC > 0: a compile-time KC x KC window (unrolled: every load in flight at once)
+__global__ void maxpool_gen_fwd_kernel(const bf16* __restrict__ x, int ldx, int n, int h, int w, int c, int kh_rt, int kw_rt,
                                        int st, int ph, int pw, int ho, int wo, bf16* __restrict__ y, int ldy,
                                        uint8_t* __restrict__ idx) {
+  const int kh = KC > 0 ? KC : kh_rt, kw = KC > 0 ? KC : kw_rt;
   const int groups = c >> 3;
   const int total = n * ho * wo * groups;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -192,9 +194,11 @@ __global__ void maxpool_gen_fwd_kernel(const bf16* __restrict__ x, int ldx, int 
     int arg[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) { best[j] = 0.f; arg[j] = -1; }
+#pragma unroll
     for (int r = 0; r < kh; ++r) {
       const int iy = q.y * st + r - ph;
       if (iy < 0 || iy >= h) continue;
+#pragma unroll
       for (int s = 0; s < kw; ++s) {
         const int ix = q.x * st + s - pw;
         if (ix < 0 || ix >= w) continue;
@@ -215,10 +219,11 @@ __global__ void maxpool_gen_fwd_kernel(const bf16* __restrict__ x, int ldx, int 
 }
 
 // gather form: thread = (input pixel, 8 channels) sums dy over the windows whose argmax it is
-template <bool S1>
+template <bool S1, int KC = 0>   // KC > 0: compile-time KC x KC window (unrolled)
 __global__ void maxpool_gen_bwd_kernel(const uint8_t* __restrict__ idx, const bf16* __restrict__ dy, int ldy, int n,
-                                       int h, int w, int c, int kh, int kw, int st, int ph, int pw, int ho, int wo,
+                                       int h, int w, int c, int kh_rt, int kw_rt, int st, int ph, int pw, int ho, int wo,
                                        bf16* __restrict__ dx, int ldx, int acc) {
+  const int kh = KC > 0 ? KC : kh_rt, kw = KC > 0 ? KC : kw_rt;
   const int groups = c >> 3;
   const int total = n * h * w * groups;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -231,6 +236,7 @@ __global__ void maxpool_gen_bwd_kernel(const uint8_t* __restrict__ idx, const bf
 #pragma unroll
       for (int j = 0; j < 8; ++j) a[j] = 0.f;
     }
+#pragma unroll
     for (int r = 0; r < kh; ++r) {
       int oy = q.y + ph - r;
       if (oy < 0) break;   // decreases with r
@@ -239,6 +245,7 @@ __global__ void maxpool_gen_bwd_kernel(const uint8_t* __restrict__ idx, const bf
         oy /= st;
       }
       if (oy >= ho) continue;
+#pragma unroll
       for (int s = 0; s < kw; ++s) {
         int ox = q.x + pw - s;
         if (ox < 0) break;
@@ -898,8 +905,9 @@ int module_forward(Model* m, ModuleBufs& k, const bf16* x, bf16* y, std::string*
       }
     } else if (d.op == RALPB_NODE_MAXPOOL) {
       const long long total = rout * (q.cin / 8);
-      maxpool_gen_fwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride,
-                                                                  d.pad_h, d.pad_w, q.ho, q.wo, dst, ldd, q.idx);
+      auto kern = d.kh == 3 && d.kw == 3 ? maxpool_gen_fwd_kernel<3> : maxpool_gen_fwd_kernel<0>;
+      kern<<<grid_for(total, 256), 256, 0, s>>>(src, lds, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride, d.pad_h, d.pad_w,
+                                                q.ho, q.wo, dst, ldd, q.idx);
       RALPB_TRY(cudaGetLastError());
       ++m->launches;
     } else {
@@ -1057,7 +1065,9 @@ int module_backward(Model* m, ModuleBufs& k, const bf16* x, const bf16* y, const
       const int gr = grid_for(total, 256);
       const bool s1 = d.stride == 1;
       if (d.op == RALPB_NODE_MAXPOOL) {
-        auto kern = s1 ? maxpool_gen_bwd_kernel<true> : maxpool_gen_bwd_kernel<false>;
+        const bool k3 = d.kh == 3 && d.kw == 3;
+        auto kern = s1 ? (k3 ? maxpool_gen_bwd_kernel<true, 3> : maxpool_gen_bwd_kernel<true>)
+                       : (k3 ? maxpool_gen_bwd_kernel<false, 3> : maxpool_gen_bwd_kernel<false>);
         kern<<<gr, 256, 0, s>>>(q.idx, g_out, ldo, k.n, q.h, q.w, q.cin, d.kh, d.kw, d.stride, d.pad_h, d.pad_w, q.ho,
                                 q.wo, g_in, lds, acc);
       } else {

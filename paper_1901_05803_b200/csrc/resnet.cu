@@ -378,8 +378,10 @@ __global__ void __launch_bounds__(256) add_act_kernel(Act4 a, Act4 b, MutAct4 y,
 
 // ------------------------------------------------------------------ pools
 // thread = (output pixel, 8 channels): k*k 16-byte loads, first max wins, padding never wins
-__global__ void maxpool_pad_fwd_kernel(Act4 x, int n, int h, int w, int c, int k, int st, int p, MutAct4 y, int oh,
+template <int KC>   // KC > 0: compile-time KC x KC window (unrolled: the loads in flight together)
+__global__ void maxpool_pad_fwd_kernel(Act4 x, int n, int h, int w, int c, int k_rt, int st, int p, MutAct4 y, int oh,
                                        int ow, uint8_t* __restrict__ idx) {
+  const int k = KC > 0 ? KC : k_rt;
   const int groups = c >> 3;
   const int total = n * oh * ow * groups;
   const int hp = h + 2 * x.pad, wp = w + 2 * x.pad;
@@ -392,9 +394,11 @@ __global__ void maxpool_pad_fwd_kernel(Act4 x, int n, int h, int w, int c, int k
     int arg[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) { best[j] = 0.f; arg[j] = -1; }
+#pragma unroll
     for (int ky = 0; ky < k; ++ky) {
       const int iy = oy * st + ky - p;
       if (iy < 0 || iy >= h) continue;
+#pragma unroll
       for (int kx = 0; kx < k; ++kx) {
         const int ix = ox * st + kx - p;
         if (ix < 0 || ix >= w) continue;
@@ -662,7 +666,10 @@ cudaError_t maxpool_pad_fwd(Act4 x, int n, int h, int w, int c, int k, int st, i
                             uint8_t* idx, cudaStream_t s) {
   const long long total = static_cast<long long>(n) * oh * ow * (c / 8);
   if (c % 8 != 0 || !fits(total * 8)) return cudaErrorInvalidValue;
-  maxpool_pad_fwd_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, n, h, w, c, k, st, p, y, oh, ow, idx);
+  if (k == 3)
+    maxpool_pad_fwd_kernel<3><<<grid_for(total, 256), 256, 0, s>>>(x, n, h, w, c, k, st, p, y, oh, ow, idx);
+  else
+    maxpool_pad_fwd_kernel<0><<<grid_for(total, 256), 256, 0, s>>>(x, n, h, w, c, k, st, p, y, oh, ow, idx);
   return cudaGetLastError();
 }
 
