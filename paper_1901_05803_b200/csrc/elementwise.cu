@@ -942,6 +942,55 @@ cudaError_t cast_bf16(const float* x, long long n, __nv_bfloat16* y, cudaStream_
   return cudaGetLastError();
 }
 
+struct CastBatch {
+  CastJob j[kMaxCastJobs];
+  long long start[kMaxCastJobs + 1];   // first 4-element chunk of each job
+  int n;
+};
+// thread = one 4-element chunk of one job (jobs located by binary search over the chunk starts)
+__global__ void cast_batch_kernel(const __grid_constant__ CastBatch b) {
+  const long long total = b.start[b.n];
+  for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < total;
+       v += static_cast<long long>(gridDim.x) * blockDim.x) {
+    int lo = 0, hi = b.n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (b.start[mid] <= v) lo = mid; else hi = mid - 1;
+    }
+    const CastJob& j = b.j[lo];
+    const long long o = (v - b.start[lo]) * 4;
+    if (o + 4 <= j.n) {
+      const float4 f = *reinterpret_cast<const float4*>(j.x + o);
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(f.x, f.y), p1 = __floats2bfloat162_rn(f.z, f.w);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&p0);
+      u.y = *reinterpret_cast<uint32_t*>(&p1);
+      *reinterpret_cast<uint2*>(j.y + o) = u;
+    } else {
+      for (long long e = o; e < j.n; ++e) j.y[e] = __float2bfloat16_rn(j.x[e]);
+    }
+  }
+}
+
+cudaError_t cast_bf16_batch(const CastJob* jobs, int n, cudaStream_t s) {
+  for (int base = 0; base < n; base += kMaxCastJobs) {
+    CastBatch b{};
+    b.n = std::min(kMaxCastJobs, n - base);
+    b.start[0] = 0;
+    for (int i = 0; i < b.n; ++i) {
+      b.j[i] = jobs[base + i];
+      if ((reinterpret_cast<uintptr_t>(b.j[i].x) & 15) || (reinterpret_cast<uintptr_t>(b.j[i].y) & 7))
+        return cudaErrorMisalignedAddress;
+      b.start[i + 1] = b.start[i] + (b.j[i].n + 3) / 4;
+    }
+    if (b.start[b.n] == 0) continue;
+    cast_batch_kernel<<<grid_for(b.start[b.n], 256), 256, 0, s>>>(b);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace ralpb
 
 namespace ralpb {

@@ -96,5 +96,14 @@ cudaError_t gemm_finalize(const float* acc, int rows, int cols, long long ld_acc
                           long long ld_out, cudaStream_t s);
 // fp32 -> bf16 cast.
 cudaError_t cast_bf16(const float* x, long long n, __nv_bfloat16* y, cudaStream_t s);
+// Several fp32 -> bf16 casts in one launch (x and y 16-byte / 8-byte aligned: parameter offsets are
+// multiples of 4 floats), up to kMaxCastJobs per launch.
+struct CastJob {
+  const float* x;
+  __nv_bfloat16* y;
+  long long n;
+};
+constexpr int kMaxCastJobs = 64;
+cudaError_t cast_bf16_batch(const CastJob* jobs, int n, cudaStream_t s);
 
 }  // namespace ralpb

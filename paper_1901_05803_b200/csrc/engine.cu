@@ -1469,6 +1469,7 @@ int launch_conv_forward(Model* m, int lo, int hi, const float* img, const ActBuf
 int prep_filters(Model* m, bool forward, bool dgrad, cudaStream_t s, std::string* why, int lo = 0, int hi = -1) {
   WeightPrepJob jobs[kMaxPrepJobs];
   int nj = 0;
+  std::vector<CastJob> casts;   // plain filter casts (branch-group nodes, im2col layers): one launch
   if (hi < 0) hi = static_cast<int>(m->front.size());
   for (size_t i = lo; i < static_cast<size_t>(hi); ++i) {
     FrontLayer& f = m->front[i];
@@ -1477,15 +1478,12 @@ int prep_filters(Model* m, bool forward, bool dgrad, cudaStream_t s, std::string
       continue;
     }
     if (f.kind == RALPB_MODULE) {
-      if (forward && module_prep(m, m->modules[f.mod], s, why)) return 1;
+      if (forward && module_prep(m, m->modules[f.mod], s, why, &casts)) return 1;
       continue;
     }
     if (f.kind != RALPB_CONV || f.wf == nullptr) continue;   // (layers this rank does not run)
     if (f.im2col) {
-      if (forward) {
-        RALPB_TRY(cast_bf16(m->P + f.w_off, f.w_count, f.wf, s));
-        ++m->launches;
-      }
+      if (forward) casts.push_back(CastJob{m->P + f.w_off, f.wf, f.w_count});
       continue;
     }
     if (!forward && i == 0) continue;   // no backward-data for the first layer
@@ -1502,6 +1500,10 @@ int prep_filters(Model* m, bool forward, bool dgrad, cudaStream_t s, std::string
   if (nj > 0) {
     RALPB_TRY(conv_weight_prep_batch(jobs, nj, s));
     ++m->launches;
+  }
+  if (!casts.empty()) {
+    RALPB_TRY(cast_bf16_batch(casts.data(), static_cast<int>(casts.size()), s));
+    m->launches += (static_cast<int>(casts.size()) + kMaxCastJobs - 1) / kMaxCastJobs;
   }
   return 0;
 }

@@ -782,11 +782,19 @@ int module_alloc(Model* m, ModuleBufs& k, std::string* why) {
   return 0;
 }
 
-int module_prep(Model* m, ModuleBufs& k, cudaStream_t s, std::string* why) {
+int module_prep(Model* m, ModuleBufs& k, cudaStream_t s, std::string* why, std::vector<CastJob>* casts) {
+  auto cast = [&](const float* x, long long n, bf16* y) -> int {
+    if (casts != nullptr) {
+      casts->push_back(CastJob{x, y, n});
+      return 0;
+    }
+    RALPB_TRY(cast_bf16(x, n, y, s));
+    ++m->launches;
+    return 0;
+  };
   for (const ModGroup& g : k.sib) {
     if (g.wbf == nullptr) continue;   // a layer this rank does not run (not allocated)
-    RALPB_TRY(cast_bf16(m->P + g.w_off, static_cast<long long>(g.ncat) * k.nodes[g.members[0]].cin, g.wbf, s));
-    ++m->launches;
+    if (cast(m->P + g.w_off, static_cast<long long>(g.ncat) * k.nodes[g.members[0]].cin, g.wbf)) return 1;
   }
   for (ModNode& q : k.nodes) {
     if (q.d.op != RALPB_NODE_CONV || q.wbf == nullptr) continue;
@@ -796,11 +804,12 @@ int module_prep(Model* m, ModuleBufs& k, cudaStream_t s, std::string* why) {
       RALPB_TRY(cudaGetLastError());
       RALPB_TRY(conv_weight_prep(q.gw, q.d.cout, q.d.kh * q.d.kw, q.cpad, q.wbf, q.wdb, s));
       ++m->launches;
-    } else if (q.same)   // [cout][taps][cin] forward copy and the tap-reversed transpose for backward-data
+    } else if (q.same) {   // [cout][taps][cin] forward copy and the tap-reversed transpose for backward-data
       RALPB_TRY(conv_weight_prep(m->P + q.w_off, q.d.cout, q.d.kh * q.d.kw, q.cin, q.wbf, q.wdb, s));
-    else
-      RALPB_TRY(cast_bf16(m->P + q.w_off, static_cast<long long>(q.d.cout) * q.K(), q.wbf, s));
-    ++m->launches;
+      ++m->launches;
+    } else if (cast(m->P + q.w_off, static_cast<long long>(q.d.cout) * q.K(), q.wbf)) {
+      return 1;
+    }
   }
   return 0;
 }

@@ -15,7 +15,8 @@ int module_build(ModuleBufs& k, const ralpb_node_desc* nodes, int n_nodes, int n
                  long long* off, std::vector<std::pair<long long, long long>>* runs, long long* count,
                  std::string* why);
 int module_alloc(Model* m, ModuleBufs& k, std::string* why);
-int module_prep(Model* m, ModuleBufs& k, cudaStream_t s, std::string* why);
+// casts: when given, the filter casts are appended (one batched launch by the caller)
+int module_prep(Model* m, ModuleBufs& k, cudaStream_t s, std::string* why, std::vector<CastJob>* casts = nullptr);
 // x [n][h][w][cin] -> y [n][ho][wo][cout] (unpadded NHWC)
 int module_forward(Model* m, ModuleBufs& k, const __nv_bfloat16* x, __nv_bfloat16* y, std::string* why);
 // dy w.r.t. y -> dx w.r.t. x (may be null); parameter gradients into G
