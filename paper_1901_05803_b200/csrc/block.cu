@@ -140,7 +140,17 @@ int block_alloc(Model* m, BlockBufs& k, std::string* why) {
   return 0;
 }
 
-int block_prep(Model* m, BlockBufs& k, cudaStream_t s, std::string* why) {
+int block_prep(Model* m, BlockBufs& k, cudaStream_t s, std::string* why, std::vector<CastJob>* casts,
+               std::vector<WeightPrepJob>* preps) {
+  if (casts != nullptr && preps != nullptr) {
+    casts->push_back(CastJob{m->P + k.wa_off, k.wa, static_cast<long long>(k.width) * k.cin});
+    casts->push_back(CastJob{m->P + k.wc_off, k.wc, static_cast<long long>(k.cout) * k.width});
+    if (k.down) casts->push_back(CastJob{m->P + k.wd_off, k.wd, static_cast<long long>(k.cout) * k.cin});
+    WeightPrepJob j{};
+    j.w = m->P + k.wb_off; j.wf = k.wbf; j.wd = k.wbd; j.co = k.width; j.taps = 9; j.ci = k.width;
+    preps->push_back(j);
+    return 0;
+  }
   RALPB_TRY(cast_bf16(m->P + k.wa_off, static_cast<long long>(k.width) * k.cin, k.wa, s));
   RALPB_TRY(conv_weight_prep(m->P + k.wb_off, k.width, 9, k.width, k.wbf, k.wbd, s));
   RALPB_TRY(cast_bf16(m->P + k.wc_off, static_cast<long long>(k.cout) * k.width, k.wc, s));

@@ -2,6 +2,8 @@
 // RALPB_BLOCK layers and bn convolutions of a branchy model.
 #pragma once
 #include <string>
+#include <vector>
+#include "elementwise.cuh"
 #include "engine.cuh"
 
 namespace ralpb {
@@ -11,7 +13,9 @@ int block_alloc(Model* m, BlockBufs& k, std::string* why);
 // instead of a separate add pass -- measured slower (the narrow-K 1x1 dgrad GEMMs are epilogue-
 // bound: ResNet-50 15.80 vs 15.66 ms, Inception-v3 34.6 vs 34.2 ms, GoogLeNet 9.93 vs 9.67 ms)
 bool res_epilogue();
-int block_prep(Model* m, BlockBufs& k, cudaStream_t s, std::string* why);
+// casts / preps: when given, the operand copies are appended for the caller's batched launches
+int block_prep(Model* m, BlockBufs& k, cudaStream_t s, std::string* why, std::vector<CastJob>* casts = nullptr,
+               std::vector<WeightPrepJob>* preps = nullptr);
 // x [n][h][w][cin] -> y [n][ho][wo][cout] (unpadded NHWC)
 int block_forward(Model* m, BlockBufs& k, const __nv_bfloat16* x, __nv_bfloat16* y, std::string* why);
 // dy w.r.t. y -> dx w.r.t. x (dx may be null: no input gradient); parameter gradients into G

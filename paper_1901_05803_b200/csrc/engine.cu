@@ -1474,7 +1474,18 @@ int prep_filters(Model* m, bool forward, bool dgrad, cudaStream_t s, std::string
   for (size_t i = lo; i < static_cast<size_t>(hi); ++i) {
     FrontLayer& f = m->front[i];
     if (f.kind == RALPB_BLOCK) {   // all of a block's operand copies with the forward ones
-      if (forward && m->blocks[f.blk].wa != nullptr && block_prep(m, m->blocks[f.blk], s, why)) return 1;
+      if (forward && m->blocks[f.blk].wa != nullptr) {
+        std::vector<WeightPrepJob> bj;
+        if (block_prep(m, m->blocks[f.blk], s, why, &casts, &bj)) return 1;
+        for (const WeightPrepJob& j : bj) {
+          if (nj == kMaxPrepJobs) {
+            RALPB_TRY(conv_weight_prep_batch(jobs, nj, s));
+            ++m->launches;
+            nj = 0;
+          }
+          jobs[nj++] = j;
+        }
+      }
       continue;
     }
     if (f.kind == RALPB_MODULE) {

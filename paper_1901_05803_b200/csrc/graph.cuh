@@ -4,6 +4,8 @@
 #include <string>
 #include <utility>
 #include <vector>
+#include <vector>
+#include "elementwise.cuh"
 #include "engine.cuh"
 
 namespace ralpb {
